@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""Benchmark of the multi-frequency H^2+ACA single-layer apply (arXiv 2006.05186).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+
+One step = one pass of the whole hot path over one
+batch of synthetic time-domain data: cqm_forward (K4) -> [all-to-all when
+N > 1] -> bem_apply_multifreq (gather, K1 near field, K2 up, K3 coupling,
+K2 down, scatter) -> [all-to-all] -> cqm_inverse (K4).  Metric: unknowns x
+frequencies per second, value = M * L / (device time per step), max over
+ranks.  Inputs are device-resident; L2 is flushed (256 MB write) before every
+timed step.  `e2e` repeats the step through the same public API from pinned
+HOST buffers with the copies inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "unknowns*frequencies/s of V(s_l)x_l apply (time-domain step: forward + apply + inverse)"
+UNIT = "unknowns*frequencies/s"
+FP64_PEAK_DERIVED = 148 * 64 * 2 * 1.965e9  # SMs x DFMA/clk/SM x 2 flop x max SM clock
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--mode", default="h2aca", choices=["h2aca", "h2only"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--quiet", action="store_true")
+    return ap.parse_args()
+
+
+def workload(cfg_id):
+    cfg = synth.CONFIGS[cfg_id]
+    V, T = synth.config_mesh(cfg_id)
+    N = cfg["N"]
+    return cfg, V, T, N, N + 1, 10.0 ** (-5.0 / N)
+
+
+def config_json(cfg_id, cfg, M, L, G):
+    return {"workload": f"config{cfg_id}: {cfg['mesh'][0]} sub{cfg['mesh'][1]}, M={M} panels, N={cfg['N']} (L={L}),"
+                        f" m={cfg['m']} (p={cfg['m'] ** 3}), leaf={cfg['leaf']}, eta={cfg['eta']}, eps={cfg['eps']}",
+            "M": M, "L": L, "T": cfg["T"], "seed": synth.SEED_BASE + cfg_id,
+            "parallelism": f"frequency-sharded x{G}" if G > 1 else "1 GPU",
+            "l2": "flushed (256 MB write) before every timed step"}
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=5)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(V, T, cfg, s, N, nsel=None):
+    """The oracle as it stands (H2ACA apply) on a bounded frequency sample."""
+    import oracle as O
+    nthr = O.num_threads()
+    L = N + 1
+    nsel = nsel or max(1, min(L, nthr))
+    h = O.H2(V, T, cfg["leaf"], cfg["eta"], cfg["m"])
+    t0 = time.perf_counter()
+    h.aca(s, cfg["eps"])
+    t_aca = time.perf_counter() - t0
+    lsel = np.linspace(0, L - 1, nsel).round().astype(np.int32)
+    x = synth.random_density(cfg_id_global, nsel, len(T))
+    t0 = time.perf_counter()
+    h.apply(O.MODE_H2ACA, s, x, lsel)
+    dt = time.perf_counter() - t0
+    return {"value": len(T) * nsel / dt, "unit": UNIT, "cores": nthr, "kind": "oracle",
+            "sample": f"H2ACA apply of {nsel} of {L} frequencies (evenly spaced), all {len(T)} panels; "
+                      f"{dt:.2f} s; oracle ACA setup {t_aca:.1f} s excluded"}
+
+
+cfg_id_global = 2
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle, as it stands, on this box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+    cfg, V, T, N, L, R = workload(args.config)
+    M = len(T)
+    s = O.frequencies(N, cfg["T"])
+    nthr = O.num_threads()
+    h = O.H2(V, T, cfg["leaf"], cfg["eta"], cfg["m"])
+    h.aca(s, cfg["eps"])
+    nsel = max(1, min(L, nthr))
+    rng_sel = np.random.default_rng(0)
+    times = []
+    for k in range(args.warmup + args.steps):
+        lsel = np.sort(rng_sel.choice(L, nsel, replace=False)).astype(np.int32)
+        x = synth.random_density(args.config, nsel, M, stream=k)
+        t0 = time.perf_counter()
+        h.apply(O.MODE_H2ACA, s, x, lsel)
+        if k >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    dt = sum(times) / len(times)
+    val = M * nsel / dt
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_json(args.config, cfg, M, L, 1),
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": nthr, "kind": "oracle",
+                             "sample": f"each step: oracle H2ACA apply of {nsel} random frequencies of {L}, "
+                                       f"all {M} panels (setup excluded)"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    global cfg_id_global
+    args = parse()
+    cfg_id_global = args.config
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2006_05186_b200 as pb
+    from paper_2006_05186_b200.dist import ShardedTimeOperator, dof_ranges, shard_frequencies
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    cfg, V, T, N, L, R = workload(args.config)
+    M = len(T)
+    s = pb.cqm_frequencies(N, cfg["T"], R)
+    mode = pb.BEM_MODE_H2ACA if args.mode == "h2aca" else pb.BEM_MODE_H2ONLY
+    t0 = time.perf_counter()
+    tree = pb.Tree(V, T, cfg["leaf"], cfg["eta"], cfg["m"], device=local_rank)
+    t_tree = time.perf_counter() - t0
+    local = shard_frequencies(L, world)[rank] if world > 1 else np.arange(L, dtype=np.int32)
+    t0 = time.perf_counter()
+    op = pb.Operator(tree, s, cfg["eps"], mode=mode, local_l=local if world > 1 else None)
+    t_aca = time.perf_counter() - t0
+    b, e = dof_ranges(M, world)[rank]
+    xt_host = synth.random_time_data(args.config, N, M)[:, b:e].astype(np.complex128)
+    x = torch.from_numpy(xt_host).to(dev)
+
+    def fwd(z):
+        return pb.cqm_forward(z, N, R)
+
+    def inv(z):
+        return pb.cqm_inverse(z, N, R)
+
+    if world > 1:
+        top = ShardedTimeOperator(rank, world, M, L, op.apply, fwd, inv)
+        step = top.step
+    else:
+        def step(z):
+            return inv(op.apply(fwd(z)))
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(max(3, args.warmup)):
+        step(x)
+    torch.cuda.synchronize()
+    op.set_profiling(True)
+    acc = {"near": 0.0, "up": 0.0, "coupling": 0.0, "down": 0.0}
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clk = ClockSampler(local_rank)
+    clk.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.zero_()
+        evs[k][0].record()
+        y = step(x)
+        evs[k][1].record()
+        evs[k][1].synchronize()
+        for key, v in op.timings().items():
+            acc[key] += v
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    op.set_profiling(False)
+    ms_steps = [a.elapsed_time(bb) for a, bb in evs]
+    t_tot = torch.tensor([sum(ms_steps)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_tot, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t_tot.item()) / args.steps
+    value = M * L / (ms_per_step * 1e-3)
+
+    # e2e: same step through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.from_numpy(xt_host).pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.zero_()
+            eev[k][0].record()
+            xd = xh.to(dev, non_blocking=True)
+            yd = step(xd)
+            yh.copy_(yd, non_blocking=True)
+            eev[k][1].record()
+            eev[k][1].synchronize()
+        te = torch.tensor([sum(a.elapsed_time(bb) for a, bb in eev)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        ms_e2e = float(te.item()) / args.steps
+        e2e = {"value": M * L / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 16),
+               "d2h_bytes_per_step": int(yh.numel() * 16), "ms_per_step": ms_e2e}
+
+    # roofline of the dominant kernel (algorithmic flops / measured launch time)
+    stats = tree.stats
+    nl = len(local)
+    n_class = len({min(l, L - l) for l in local})
+    kt = {k: v / args.steps for k, v in acc.items()}
+    launches = op.launch_count() + 2
+    roof = None
+    if mode == pb.BEM_MODE_H2ACA:
+        rk = op.aca_export()["ranks"]
+        flops_far = 8.0 * float(rk.sum()) * stats["p"] ** 2 * nl
+    else:
+        flops_far = 8.0 * stats["far_blocks"] * stats["p"] ** 2 * nl
+    evals_near = 7.0 * stats["nnz_near"] * n_class
+    flops_near = 75.0 * evals_near  # SURVEY §8(d) model: ~75 FP64 flops per complex exponential + MACs
+    dom = "coupling" if kt["coupling"] >= kt["near"] else "near"
+    fl = flops_far if dom == "coupling" else flops_near
+    achieved = fl / (kt[dom] * 1e-3) / 1e12
+    peak = FP64_PEAK_DERIVED / 1e12
+    roof = {"bound": "alu", "kernel": {"coupling": "K3 far_kernel", "near": "K1 near_kernel"}[dom],
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+            "peak_source": "derived: 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (B200 FP64 pipe; DESIGN.md)",
+            "algorithmic_flops_per_launch": fl}
+    try:
+        meas_peak = pb.fp64_peak(local_rank) / 1e12
+    except Exception:
+        meas_peak = None
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": config_json(args.config, cfg, M, L, world), "roofline": roof, "e2e": e2e,
+           "gpu_launches": launches * args.steps, "clocks": clocks,
+           "kernel_ms": kt, "fp64_dfma_measured_tflops": meas_peak,
+           "near_evals_per_s": evals_near / (kt["near"] * 1e-3) if kt["near"] > 0 else None,
+           "setup_s": {"tree": t_tree, "aca": t_aca}, "mode": args.mode,
+           "mean_aca_rank": float(op.aca_export()["ranks"].mean()) if mode == pb.BEM_MODE_H2ACA else None}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline(V, T, cfg, s, N)
+        except Exception as ex:  # pragma: no cover
+            out["cpu_baseline"] = {"value": None, "error": str(ex)}
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,165 @@
+/* bem.h -- C-ABI of the B200 (sm_100a) multi-frequency H^2 + ACA single-layer
+ * library (paper_2006_05186_b200/csrc, built as libbem.so).
+ *
+ * Paper: D. Seibel, "Boundary Element Methods for the Wave Equation based on
+ * Hierarchical Matrices and Adaptive Cross Approximation", arXiv 2006.05186.
+ * "P:<a-b>" below cites /root/reference/PAPER.md lines; "S:<a-b>" SPEC.md;
+ * readings (AM<k>, D<k>) are listed in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns bem_status: 0 = OK, < 0 = error; bem_last_error()
+ *    returns a thread-local message valid until the next bem_* call on the
+ *    same thread.  On error outputs are unspecified and handles stay valid.
+ *  - Host pointers are borrowed for the duration of the call and copied.
+ *  - Device pointers are caller-owned (e.g. torch tensors), contiguous,
+ *    16-byte aligned, on the handle's device, and must stay alive until the
+ *    work enqueued on `cuda_stream` has finished.  Handles own their device
+ *    memory and free it in *_destroy.
+ *  - `cuda_stream` is a cudaStream_t (NULL = legacy default stream).  apply,
+ *    cqm_forward and cqm_inverse are asynchronous; build, assemble and solve
+ *    synchronise before returning.
+ *  - Complex data are interleaved (re, im) doubles: the layout of
+ *    std::complex<double>, cuDoubleComplex and torch.complex128.
+ *  - Frequency-domain arrays are [l][panel] row-major with the panel index in
+ *    INPUT order (the tree permutation is internal); time-domain arrays are
+ *    [n][panel].
+ *  - Results are bitwise reproducible for identical inputs and device.
+ *  - Distinct handles may be used concurrently from different threads; a
+ *    single handle may not.
+ */
+#ifndef BEM_H_
+#define BEM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t bem_status;
+enum {
+  BEM_OK = 0,
+  BEM_EINVAL = -1,  /* invalid argument (ranges listed per call) */
+  BEM_ENOMEM = -2,  /* device or host allocation failed */
+  BEM_ECUDA = -3,   /* CUDA runtime error (launch or asynchronous fault) */
+  BEM_ENCCL = -4,   /* reserved: collectives are issued by the caller */
+  BEM_ENOCONV = -5, /* cqm_solve: some frequency hit max_iter (outputs written) */
+  BEM_ESTATE = -6   /* handle misuse (wrong device, tree destroyed before its ops) */
+};
+
+enum { BEM_MODE_H2ACA = 0, BEM_MODE_H2ONLY = 1, BEM_MODE_DENSE = 2 };
+
+typedef struct { double re, im; } bem_c128;
+typedef struct bem_tree_s* bem_tree; /* panels, cluster tree, P+/P-, U, W, E, boxes; one device */
+typedef struct bem_op_s* bem_op;     /* tree ref + s_l + ACA skeletons for a local frequency set */
+
+typedef struct {
+  int64_t M, clusters, leaves, near_blocks, far_blocks, nnz_near;
+  int32_t depth, p;
+} bem_tree_stats;
+
+typedef struct {
+  int32_t iters_max, iters_sum, n_unconverged, pad_;
+  double resid_max, imag_rel_max;
+} bem_solve_stats;
+
+const char* bem_last_error(void);
+
+/* CQM frequencies, eq:cqm_freq P:443-447 with the north_star sign (AM2):
+ *   s_l = delta(R e^{-2 pi i l/L}) / dt,  dt = T/N,  L = N+1 (AM1),
+ *   delta(z) = 1 - z (method 1, BDF1) or 3/2 - 2z + z^2/2 (method 2, BDF2);
+ *   s_{L-l} := conj(s_l) exactly, Im s_0 = 0 exactly.
+ * s_out: host, L = N+1 entries.  EINVAL: N < 1, T <= 0, R not in (0,1),
+ * method not in {1,2}, s_out NULL. */
+bem_status cqm_frequencies(int32_t N, double T, double R, int32_t method, bem_c128* s_out);
+
+/* Geometry + cluster tree + admissible partition + cluster bases (P:738-1070,
+ * Alg. 1; clustering P:832-835; partition eq:qadm P:905-912 with near <=>
+ * inadmissible leaf x leaf (AM9); Chebyshev bases P:957-978).
+ *   vertices  host [nv][3] doubles;  triangles host [nt][3] int32, 0-based;
+ *   leaf_size n_min > 1 (leaves hold <= n_min panels, AM6); eta > 0;
+ *   cheb_order m >= 1 (p = m^3 interpolation points per box);
+ *   device: CUDA ordinal.  Synchronous.  *out receives a new handle.
+ * EINVAL: nv < 3, nt < 1, an index out of range, a degenerate triangle
+ * (area <= 0), leaf_size <= 1, eta <= 0, m < 1 or m > 8, out NULL. */
+bem_status bem_build_tree(const double* vertices, int64_t nv, const int32_t* triangles, int64_t nt,
+                          int32_t leaf_size, double eta, int32_t cheb_order, int32_t device, bem_tree* out);
+bem_status bem_tree_get_stats(bem_tree t, bem_tree_stats* out);
+/* Host outputs, caller-sized from the stats (any may be NULL):
+ *   perm [M] (perm[k] = input index of the k-th panel in cluster order),
+ *   clusters [C][5] = (begin, end, son0, son1, level) in DFS pre-order,
+ *   boxes [C][6] = (lo_x, lo_y, lo_z, hi_x, hi_y, hi_z),
+ *   near_pairs [near][2], far_pairs [far][2] = (row cluster, col cluster). */
+bem_status bem_tree_export(bem_tree t, int32_t* perm, int32_t* clusters, double* boxes, int32_t* near_pairs,
+                           int32_t* far_pairs);
+/* NULL-safe.  Returns BEM_ESTATE (and keeps the tree) while ops built on it live. */
+bem_status bem_tree_destroy(bem_tree t);
+
+/* Multi-frequency operator (Alg. 3, FAR branch; eq:lrfinal P:1404-1410).
+ *   s: host [L] frequencies (normally from cqm_frequencies);
+ *   local_l: host [n_local] distinct frequency indices this handle applies
+ *            (NULL = all L, n_local ignored);
+ *   aca_eps > 0: MACA tolerance (Alg. 2, stop rule P:1288);
+ *   mode: BEM_MODE_H2ACA (the product), BEM_MODE_H2ONLY (couplings evaluated
+ *         per frequency, no ACA; plain-H^2 comparison path), BEM_MODE_DENSE
+ *         (every leaf pair is evaluated as near field).
+ * The ACA runs over ALL L frequencies on the device with pinned arithmetic
+ * (bit-reproducible pivots) and keeps Z columns for local_l only.
+ * Synchronous on return.  EINVAL: L < 1, s NULL, local index out of range or
+ * duplicated, aca_eps <= 0, unknown mode. */
+bem_status bem_assemble_h2_aca(bem_tree t, const bem_c128* s, int32_t L, const int32_t* local_l, int32_t n_local,
+                               double aca_eps, int32_t mode, void* cuda_stream, bem_op* out);
+/* ranks: host [far_blocks]; pivots: host [sum ranks][2] = (k_l, q_l) in block
+ * order (q = mu*p + nu, mode-3 unfolding P:1322-1334).  Either may be NULL.
+ * *total_rank (may be NULL) receives sum ranks.  ESTATE for non-ACA modes. */
+bem_status bem_aca_export(bem_op op, int32_t* ranks, int32_t* pivots, int64_t* total_rank);
+bem_status bem_op_destroy(bem_op op); /* NULL-safe */
+
+/* y_t = V(s_{local_l[t]}) x_t for t < n_local (P:529-540 operators V_l).
+ * x, y: device [n_local][M] complex, input panel order; y is overwritten;
+ * x and y must not overlap.  Asynchronous on cuda_stream. */
+bem_status bem_apply_multifreq(bem_op op, const bem_c128* x, bem_c128* y, void* cuda_stream);
+
+/* R-scaled CQM transforms (eq:omega_n P:436-441, eq:slphelm P:529-540; D2):
+ *   forward:  x_freq[l] = sum_{n=0}^{N} R^n x_time[n] e^{-2 pi i n l / L}
+ *   inverse:  y_time[n] = R^{-n}/L sum_{l=0}^{L-1} y_freq[l] e^{+2 pi i n l / L}
+ * L = N+1; device [L][M_loc] complex each; in-place is NOT allowed.
+ * Batched Bluestein FFT on the device.  Asynchronous.
+ * EINVAL: M_loc < 1, N < 1, R not in (0,1], NULL pointers. */
+bem_status cqm_forward(const bem_c128* x_time, bem_c128* x_freq, int64_t M_loc, int32_t N, double R,
+                       void* cuda_stream);
+bem_status cqm_inverse(const bem_c128* y_freq, bem_c128* y_time, int64_t M_loc, int32_t N, double R,
+                       void* cuda_stream);
+
+/* Frequency-decoupled CQM solve of the single-layer equation V phi = g
+ * (Remark P:1607-1614; indirect first-kind reading D10):
+ *   g^ = forward(g); for every l solve V(s_l) phi^_l = g^_l by restarted
+ *   GMRES(restart) from 0, classical Gram-Schmidt with one
+ *   re-orthogonalisation, stop at ||g^_l - V phi^_l|| <= tol ||g^_l||;
+ *   phi = Re inverse(phi^).
+ * g_time, phi_time: device [N+1][M] real.  The op must hold all L = N+1
+ * frequencies (single device; nccl_comm must be NULL in this version: the
+ * multi-GPU transpose is issued by the caller).
+ * stats (host, may be NULL).  Synchronous.  Returns BEM_ENOCONV if some
+ * frequency reached max_iter (phi_time is still written). */
+bem_status cqm_solve(bem_op op, const double* g_time, double* phi_time, int64_t M_loc, double R, double tol,
+                     int32_t restart, int32_t max_iter, void* nccl_comm, void* cuda_stream, bem_solve_stats* stats);
+
+/* ---- diagnostics (tests / bench only; not part of the method) ---- */
+/* Pinned exp / sincos / kernel evaluated ON THE DEVICE for n host inputs
+ * (checks bit-identity with the independent oracle implementation). */
+bem_status bem_debug_pinned(const double* x, int64_t n, double* exp_out, double* sin_out, double* cos_out,
+                            int32_t device);
+/* FP64 DFMA throughput microbenchmark: returns achieved FLOP/s. */
+bem_status bem_debug_fp64_peak(int32_t device, void* cuda_stream, double* flops_per_s);
+/* Per-kernel CUDA-event timings of the last bem_apply_multifreq issued with
+ * profiling enabled (bem_op_set_profiling): ms for K1, K2up, K3, K2down, other. */
+bem_status bem_op_set_profiling(bem_op op, int32_t enable);
+bem_status bem_op_get_timings(bem_op op, double* ms5);
+/* Number of kernels one bem_apply_multifreq on this op launches. */
+bem_status bem_op_launch_count(bem_op op, int32_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BEM_H_ */

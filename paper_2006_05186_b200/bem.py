@@ -1,0 +1,260 @@
+"""Thin ctypes binding of libbem.so (include/bem.h): argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; torch is used
+for device memory and streams.  There is no CPU fallback: if libbem.so is
+missing or fails to load, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libbem.so")
+
+BEM_MODE_H2ACA, BEM_MODE_H2ONLY, BEM_MODE_DENSE = 0, 1, 2
+BEM_ENOCONV = -5
+_lib = None
+
+
+class BemError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"bem error {code}: {msg}")
+        self.code = code
+
+
+class TreeStats(C.Structure):
+    _fields_ = [("M", C.c_int64), ("clusters", C.c_int64), ("leaves", C.c_int64), ("near_blocks", C.c_int64),
+                ("far_blocks", C.c_int64), ("nnz_near", C.c_int64), ("depth", C.c_int32), ("p", C.c_int32)]
+
+
+class SolveStats(C.Structure):
+    _fields_ = [("iters_max", C.c_int32), ("iters_sum", C.c_int32), ("n_unconverged", C.c_int32),
+                ("pad_", C.c_int32), ("resid_max", C.c_double), ("imag_rel_max", C.c_double)]
+
+
+EXPORTS = [
+    "bem_last_error", "cqm_frequencies", "bem_build_tree", "bem_tree_get_stats", "bem_tree_export",
+    "bem_tree_destroy", "bem_assemble_h2_aca", "bem_aca_export", "bem_op_destroy", "bem_apply_multifreq",
+    "cqm_forward", "cqm_inverse", "cqm_solve", "bem_debug_pinned", "bem_debug_fp64_peak",
+    "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count",
+]
+
+
+def lib():
+    """Load libbem.so (fails loudly when it is missing: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, d = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    L.bem_last_error.restype = C.c_char_p
+    sig = {
+        "cqm_frequencies": [i32, d, d, i32, vp],
+        "bem_build_tree": [vp, i64, vp, i64, i32, d, i32, i32, vp],
+        "bem_tree_get_stats": [vp, vp],
+        "bem_tree_export": [vp, vp, vp, vp, vp, vp],
+        "bem_tree_destroy": [vp],
+        "bem_assemble_h2_aca": [vp, vp, i32, vp, i32, d, i32, vp, vp],
+        "bem_aca_export": [vp, vp, vp, vp],
+        "bem_op_destroy": [vp],
+        "bem_apply_multifreq": [vp, vp, vp, vp],
+        "cqm_forward": [vp, vp, i64, i32, d, vp],
+        "cqm_inverse": [vp, vp, i64, i32, d, vp],
+        "cqm_solve": [vp, vp, vp, i64, d, d, i32, i32, vp, vp, vp],
+        "bem_debug_pinned": [vp, i64, vp, vp, vp, i32],
+        "bem_debug_fp64_peak": [i32, vp, vp],
+        "bem_op_set_profiling": [vp, i32],
+        "bem_op_get_timings": [vp, vp],
+        "bem_op_launch_count": [vp, vp],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = C.c_int32
+    _lib = L
+    return L
+
+
+def _check(code):
+    if code != 0:
+        raise BemError(code, lib().bem_last_error().decode())
+
+
+def _p(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(C.c_void_p)
+    return C.c_void_p(a.data_ptr())  # torch tensor
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        if not torch.cuda.is_available():
+            return C.c_void_p(0)  # the library reports the missing device itself
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+def cqm_frequencies(N: int, T: float, R: float | None = None, method: int = 2) -> np.ndarray:
+    """s_l, l < L = N+1 (eq:cqm_freq P:443-447); R defaults to 10^{-5/N}."""
+    R = 10.0 ** (-5.0 / N) if (R is None and N >= 1) else (R if R is not None else 0.5)
+    out = np.empty(max(N, 0) + 1, dtype=np.complex128)
+    _check(lib().cqm_frequencies(int(N), float(T), float(R), int(method), _p(out)))
+    return out
+
+
+class Tree:
+    """bem_build_tree handle (cluster tree, partition, bases on one device)."""
+
+    def __init__(self, V, T, leaf_size: int, eta: float, m: int, device: int = 0):
+        V = np.ascontiguousarray(V, dtype=np.float64)
+        T = np.ascontiguousarray(T, dtype=np.int32)
+        h = C.c_void_p()
+        _check(lib().bem_build_tree(_p(V), len(V), _p(T), len(T), int(leaf_size), float(eta), int(m), int(device),
+                                    C.byref(h)))
+        self.h = h
+        self.device = device
+        st = TreeStats()
+        _check(lib().bem_tree_get_stats(self.h, C.byref(st)))
+        self.stats = {k: int(getattr(st, k)) for k, _ in TreeStats._fields_}
+        self.M = self.stats["M"]
+        self.p = self.stats["p"]
+
+    def export(self):
+        s = self.stats
+        perm = np.empty(s["M"], dtype=np.int32)
+        clusters = np.empty((s["clusters"], 5), dtype=np.int32)
+        boxes = np.empty((s["clusters"], 6))
+        near = np.empty((s["near_blocks"], 2), dtype=np.int32)
+        far = np.empty((s["far_blocks"], 2), dtype=np.int32)
+        _check(lib().bem_tree_export(self.h, _p(perm), _p(clusters), _p(boxes), _p(near), _p(far)))
+        return dict(perm=perm, clusters=clusters, boxes=boxes, near=near, far=far)
+
+    def close(self):
+        if getattr(self, "h", None):
+            _check(lib().bem_tree_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Operator:
+    """bem_assemble_h2_aca handle: y_t = V(s_{local_l[t]}) x_t."""
+
+    def __init__(self, tree: Tree, s, eps: float, mode: int = BEM_MODE_H2ACA, local_l=None, stream=None):
+        s = np.ascontiguousarray(s, dtype=np.complex128)
+        self.L = len(s)
+        self.s = s
+        self.tree = tree
+        if local_l is None:
+            loc, nloc = None, self.L
+            self.local_l = np.arange(self.L, dtype=np.int32)
+        else:
+            loc = np.ascontiguousarray(local_l, dtype=np.int32)
+            nloc = len(loc)
+            self.local_l = loc
+        self.n_local = nloc
+        self.mode = mode
+        h = C.c_void_p()
+        _check(lib().bem_assemble_h2_aca(tree.h, _p(s), self.L, _p(loc), nloc, float(eps), int(mode),
+                                         _stream(stream), C.byref(h)))
+        self.h = h
+
+    def aca_export(self):
+        nfar = self.tree.stats["far_blocks"]
+        ranks = np.empty(nfar, dtype=np.int32)
+        tot = C.c_int64()
+        _check(lib().bem_aca_export(self.h, _p(ranks), None, C.byref(tot)))
+        piv = np.empty((tot.value, 2), dtype=np.int32)
+        _check(lib().bem_aca_export(self.h, None, _p(piv), None))
+        return dict(ranks=ranks, pivots=piv)
+
+    def apply(self, x, y=None, stream=None):
+        """x, y: torch complex128 [n_local][M] on the tree's device (input panel order)."""
+        import torch
+        assert x.dtype == torch.complex128 and x.is_cuda and x.is_contiguous()
+        assert tuple(x.shape) == (self.n_local, self.tree.M)
+        if y is None:
+            y = torch.empty_like(x)
+        _check(lib().bem_apply_multifreq(self.h, _p(x), _p(y), _stream(stream)))
+        return y
+
+    def launch_count(self) -> int:
+        n = C.c_int32()
+        _check(lib().bem_op_launch_count(self.h, C.byref(n)))
+        return n.value
+
+    def set_profiling(self, on: bool):
+        _check(lib().bem_op_set_profiling(self.h, 1 if on else 0))
+
+    def timings(self):
+        out = np.empty(5)
+        _check(lib().bem_op_get_timings(self.h, _p(out)))
+        return dict(near=out[0], up=out[1], coupling=out[2], down=out[3])
+
+    def close(self):
+        if getattr(self, "h", None):
+            _check(lib().bem_op_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def cqm_forward(x_time, N: int, R: float, out=None, stream=None):
+    import torch
+    assert x_time.dtype == torch.complex128 and x_time.is_cuda and x_time.is_contiguous()
+    out = torch.empty_like(x_time) if out is None else out
+    _check(lib().cqm_forward(_p(x_time), _p(out), x_time.shape[1], int(N), float(R), _stream(stream)))
+    return out
+
+
+def cqm_inverse(y_freq, N: int, R: float, out=None, stream=None):
+    import torch
+    assert y_freq.dtype == torch.complex128 and y_freq.is_cuda and y_freq.is_contiguous()
+    out = torch.empty_like(y_freq) if out is None else out
+    _check(lib().cqm_inverse(_p(y_freq), _p(out), y_freq.shape[1], int(N), float(R), _stream(stream)))
+    return out
+
+
+def cqm_solve(op: Operator, g_time, R: float, tol: float = 1e-8, restart: int = 50, max_iter: int = 2000,
+              stream=None, raise_on_noconv: bool = True):
+    """phi = Re inverse(V(s_l)^{-1} forward(g)) (frequency-decoupled GMRES)."""
+    import torch
+    assert g_time.dtype == torch.float64 and g_time.is_cuda and g_time.is_contiguous()
+    phi = torch.empty_like(g_time)
+    st = SolveStats()
+    code = lib().cqm_solve(op.h, _p(g_time), _p(phi), g_time.shape[1], float(R), float(tol), int(restart),
+                           int(max_iter), None, _stream(stream), C.byref(st))
+    if code != 0 and not (code == BEM_ENOCONV and not raise_on_noconv):
+        _check(code)
+    return phi, {k: getattr(st, k) for k, _ in SolveStats._fields_ if k != "pad_"}
+
+
+def debug_pinned(x, device: int = 0):
+    x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+    e, s, c = np.empty_like(x), np.empty_like(x), np.empty_like(x)
+    _check(lib().bem_debug_pinned(_p(x), len(x), _p(e), _p(s), _p(c), int(device)))
+    return e, s, c
+
+
+def fp64_peak(device: int = 0, stream=None) -> float:
+    out = C.c_double()
+    _check(lib().bem_debug_fp64_peak(int(device), _stream(stream), C.byref(out)))
+    return out.value

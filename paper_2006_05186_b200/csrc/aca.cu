@@ -1,0 +1,595 @@
+// MACA assembly of the far-field coupling tensors on the device (setup step a10).
+//
+// Alg. 2 per admissible block b = r x c on the mode-3 unfolding
+// A_b[q,l] = k(|xi_{c,nu} - xi_{r,mu}|; s_l), q = mu*p + nu (Remark P:1322-1334;
+// coupling entries P:1166-1171), with the readings of DESIGN.md:
+//   k_1 = 0; argmax on key(z) = re*re + im*im with the lowest index winning
+//   ties; already-used slice (k) and row (q) indices are excluded (AM15);
+//   C_l = 0 stops without the term; the stop rule
+//   ||C_l|| ||d_l|| <= eps ||G^(l)|| uses the Gram identity
+//    and is tested after the term is kept (AM13).
+// Every value the ACA reads is computed with PINNED arithmetic (IEEE
+// +,-,*,/,sqrt,fma only, no contraction: __d*_rn / __fma_rn intrinsics) and
+// pinned reduction order (chunks of 32 summed sequentially, then left to
+// right), so ranks and pivots are bit-identical to the independent CPU oracle.
+// Stored per block: pivots (k_l, q_l) and Z_b = U_b^{-1} D_b^T restricted to
+// the local frequencies, U_b[l][j] = d_l[k_j] (unit upper triangular), so
+// that A_b ~= A_b[:,K] Z_b (eq:maca P:1314-1320 in skeleton form).
+#include <cmath>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace bem {
+namespace pinned {
+
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+__device__ __forceinline__ double pow2i(int k) { return __longlong_as_double((long long)(k + 1023) << 52); }
+
+__device__ double exp_(double x) {
+  if (x < -746.0) return 0.0;
+  if (x > 709.5) return __longlong_as_double(0x7ff0000000000000LL);
+  const double t = fma(x, 0x1.71547652b82fep+0, 0x1.8p+52);
+  const double kd = sub(t, 0x1.8p+52);
+  double r = fma(kd, -0x1.62e42fee00000p-1, x);
+  r = fma(kd, -0x1.a39ef35793c76p-33, r);
+  double q = 0x1.6124613a86d09p-33;  // 1/13!
+  q = fma(q, r, 0x1.1eed8eff8d898p-29);
+  q = fma(q, r, 0x1.ae64567f544e4p-26);
+  q = fma(q, r, 0x1.27e4fb7789f5cp-22);
+  q = fma(q, r, 0x1.71de3a556c734p-19);
+  q = fma(q, r, 0x1.a01a01a01a01ap-16);
+  q = fma(q, r, 0x1.a01a01a01a01ap-13);
+  q = fma(q, r, 0x1.6c16c16c16c17p-10);
+  q = fma(q, r, 0x1.1111111111111p-7);
+  q = fma(q, r, 0x1.5555555555555p-5);
+  q = fma(q, r, 0x1.5555555555555p-3);
+  q = fma(q, r, 0x1.0000000000000p-1);
+  q = fma(q, r, 0x1.0000000000000p+0);
+  q = fma(q, r, 0x1.0000000000000p+0);
+  const int k = (int)kd;
+  if (k >= -1021) return mul(q, pow2i(k));
+  return mul(mul(q, pow2i(k + 200)), pow2i(-200));
+}
+
+__device__ void sincos_(double th, double* sn, double* cs) {
+  const double t = fma(th, 0x1.45f306dc9c883p-1, 0x1.8p+52);
+  const double qd = sub(t, 0x1.8p+52);
+  double r = fma(qd, -0x1.921fb54400000p+0, th);
+  r = fma(qd, -0x1.0b4611a600000p-34, r);
+  r = fma(qd, -0x1.3198a2e000000p-69, r);
+  const double z = mul(r, r);
+  double ps = 0x1.952c77030ad4ap-49;   // 1/17!
+  ps = fma(ps, z, -0x1.ae7f3e733b81fp-41);
+  ps = fma(ps, z, 0x1.6124613a86d09p-33);
+  ps = fma(ps, z, -0x1.ae64567f544e4p-26);
+  ps = fma(ps, z, 0x1.71de3a556c734p-19);
+  ps = fma(ps, z, -0x1.a01a01a01a01ap-13);
+  ps = fma(ps, z, 0x1.1111111111111p-7);
+  ps = fma(ps, z, -0x1.5555555555555p-3);
+  ps = fma(ps, z, 0x1.0000000000000p+0);
+  const double s = mul(r, ps);
+  double pc = -0x1.6827863b97d97p-53;  // -1/18!
+  pc = fma(pc, z, 0x1.ae7f3e733b81fp-45);
+  pc = fma(pc, z, -0x1.93974a8c07c9dp-37);
+  pc = fma(pc, z, 0x1.1eed8eff8d898p-29);
+  pc = fma(pc, z, -0x1.27e4fb7789f5cp-22);
+  pc = fma(pc, z, 0x1.a01a01a01a01ap-16);
+  pc = fma(pc, z, -0x1.6c16c16c16c17p-10);
+  pc = fma(pc, z, 0x1.5555555555555p-5);
+  pc = fma(pc, z, -0x1.0000000000000p-1);
+  pc = fma(pc, z, 0x1.0000000000000p+0);
+  switch ((int)((long long)qd & 3)) {
+    case 0: *sn = s; *cs = pc; break;
+    case 1: *sn = pc; *cs = -s; break;
+    case 2: *sn = -s; *cs = -pc; break;
+    default: *sn = -pc; *cs = s; break;
+  }
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(sub(mul(a.x, b.x), mul(a.y, b.y)), add(mul(a.x, b.y), mul(a.y, b.x)));
+}
+__device__ __forceinline__ double2 cmulconj(double2 a, double2 b) {  // a * conj(b)
+  return make_double2(add(mul(a.x, b.x), mul(a.y, b.y)), sub(mul(a.y, b.x), mul(a.x, b.y)));
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(sub(a.x, b.x), sub(a.y, b.y)); }
+__device__ __forceinline__ double2 cdiv(double2 a, double2 c) {
+  const double den = add(mul(c.x, c.x), mul(c.y, c.y));
+  return make_double2(__ddiv_rn(add(mul(a.x, c.x), mul(a.y, c.y)), den),
+                      __ddiv_rn(sub(mul(a.y, c.x), mul(a.x, c.y)), den));
+}
+__device__ __forceinline__ double key(double2 a) { return add(mul(a.x, a.x), mul(a.y, a.y)); }
+
+// k(r; s) = e^{-s r}/(4 pi r): E = exp(-(Re s * r)), th = Im s * r,
+// inv = 1/(4pi r), value = ((E cos th) inv, -((E sin th) inv)).
+__device__ __forceinline__ double2 kernel(double r, double sre, double sim) {
+  const double E = exp_(-mul(sre, r));
+  double sn, cs;
+  sincos_(mul(sim, r), &sn, &cs);
+  const double inv = __ddiv_rn(1.0, mul(0x1.921fb54442d18p+3, r));
+  return make_double2(mul(mul(E, cs), inv), -mul(mul(E, sn), inv));
+}
+
+__device__ __forceinline__ double dist(const double* a, const double* b) {
+  const double dx = sub(b[0], a[0]), dy = sub(b[1], a[1]), dz = sub(b[2], a[2]);
+  return __dsqrt_rn(add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)));
+}
+
+}  // namespace pinned
+
+namespace {
+
+constexpr int kAcaThreads = 128;
+constexpr int kMaxP = 512;         // m <= 8
+constexpr int kMaxChunks = 8192;   // pp/32 upper bound for smem partials (m <= 8: 262144/32)
+
+struct AcaArgs {
+  int nfar, m, p, L, rcap, n_local;
+  const int32_t* far_r;
+  const int32_t* far_c;
+  const double* xi;
+  const double2* s;
+  const int32_t* local_l;
+  double eps;
+  double2* Cbuf;  // grid * rcap * pp
+  double2* Dbuf;  // grid * rcap * L
+  double2* Ebuf;  // grid * L
+  int32_t* rank;
+  int32_t* pivk;
+  int32_t* pivq;
+  int64_t* zoff;
+  double2* Zpool;
+  unsigned long long* pool_used;
+  unsigned long long pool_cap;
+  int32_t* flags;
+  int32_t* next_block;
+};
+
+struct BestPair { double k; int i; };
+
+__device__ __forceinline__ bool better(double ka, int ia, double kb, int ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+
+// block argmax of (key, index), lowest index on ties; result broadcast.
+__device__ BestPair block_argmax(double k, int i, BestPair* sh) {
+  for (int off = 16; off > 0; off >>= 1) {
+    double ko = __shfl_down_sync(0xffffffffu, k, off);
+    int io = __shfl_down_sync(0xffffffffu, i, off);
+    if (better(ko, io, k, i)) { k = ko; i = io; }
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sh[w] = BestPair{k, i};
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    BestPair b = sh[0];
+    for (int j = 1; j < (int)(blockDim.x >> 5); ++j)
+      if (better(sh[j].k, sh[j].i, b.k, b.i)) b = sh[j];
+    sh[0] = b;
+  }
+  __syncthreads();
+  BestPair r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// Pinned complex reduction sum_i v(i): chunk sums (32 sequential), then left to right.
+template <class F>
+__device__ double2 block_psum(int n, F v, double2* part) {
+  const int nch = (n + 31) >> 5;
+  for (int ch = threadIdx.x; ch < nch; ch += blockDim.x) {
+    double sr = 0.0, si = 0.0;
+    const int e = min(n, (ch << 5) + 32);
+    for (int i = ch << 5; i < e; ++i) {
+      const double2 x = v(i);
+      sr = __dadd_rn(sr, x.x);
+      si = __dadd_rn(si, x.y);
+    }
+    part[ch] = make_double2(sr, si);
+  }
+  __syncthreads();
+  __shared__ double2 tot;
+  if (threadIdx.x == 0) {
+    double tr = 0.0, ti = 0.0;
+    for (int ch = 0; ch < nch; ++ch) { tr = __dadd_rn(tr, part[ch].x); ti = __dadd_rn(ti, part[ch].y); }
+    tot = make_double2(tr, ti);
+  }
+  __syncthreads();
+  const double2 r = tot;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
+  using namespace pinned;
+  extern __shared__ unsigned char smem_raw[];
+  const int p = a.p, m = a.m, pp = p * p, L = a.L;
+  const int half = L / 2;
+  // shared layout
+  double* xr = (double*)smem_raw;             // p*3
+  double* xc = xr + 3 * p;                    // p*3
+  double2* part = (double2*)(xc + 3 * p);     // max(pp, L)/32 + 1
+  const int nchmax = (max(pp, L) + 31) / 32 + 1;
+  double2* dk = part + nchmax;                // rcap: D[j][k]
+  double2* cq = dk + a.rcap;                  // rcap: C[j][q*]
+  unsigned* usedq = (unsigned*)(cq + a.rcap); // pp bits
+  unsigned* usedk = usedq + (pp + 31) / 32;   // L bits
+  __shared__ BestPair red[kAcaThreads / 32];
+  __shared__ int s_blk, s_k, s_stop;
+  __shared__ double s_nrm2;
+  __shared__ long long s_off;
+
+  double2* Cb = a.Cbuf + (size_t)blockIdx.x * a.rcap * pp;
+  double2* Db = a.Dbuf + (size_t)blockIdx.x * a.rcap * L;
+  double2* Eb = a.Ebuf + (size_t)blockIdx.x * L;
+  const int rmax = min(L, pp);
+
+  for (;;) {
+    if (threadIdx.x == 0) s_blk = atomicAdd(a.next_block, 1);
+    __syncthreads();
+    const int b = s_blk;
+    __syncthreads();
+    if (b >= a.nfar) break;
+    const int rc = a.far_r[b], cc = a.far_c[b];
+    for (int i = threadIdx.x; i < p; i += blockDim.x) {
+      const double* xir = a.xi + (size_t)rc * 3 * m;
+      const double* xic = a.xi + (size_t)cc * 3 * m;
+      xr[3 * i + 0] = xir[i % m]; xr[3 * i + 1] = xir[m + (i / m) % m]; xr[3 * i + 2] = xir[2 * m + i / (m * m)];
+      xc[3 * i + 0] = xic[i % m]; xc[3 * i + 1] = xic[m + (i / m) % m]; xc[3 * i + 2] = xic[2 * m + i / (m * m)];
+    }
+    for (int i = threadIdx.x; i < (pp + 31) / 32; i += blockDim.x) usedq[i] = 0u;
+    for (int i = threadIdx.x; i < (L + 31) / 32; i += blockDim.x) usedk[i] = 0u;
+    if (threadIdx.x == 0) { s_k = 0; s_nrm2 = 0.0; s_stop = 0; }
+    __syncthreads();
+
+    auto entry = [&](int q, int l) -> double2 {
+      const bool mir = l > half;
+      const int ll = mir ? L - l : l;
+      const double r = dist(&xr[3 * (q / p)], &xc[3 * (q % p)]);
+      double2 v = kernel(r, a.s[ll].x, a.s[ll].y);
+      if (mir) v.y = -v.y;
+      return v;
+    };
+
+    int ell = 0;
+    bool overflow = false;
+    for (;;) {
+      const int k = s_k;
+      if (ell == a.rcap) { overflow = true; break; }
+      for (int j = threadIdx.x; j < ell; j += blockDim.x) dk[j] = Db[(size_t)j * L + k];
+      __syncthreads();
+      // residual slice c = A[:,k] - sum_j d_j[k] c_j
+      double bk = -1.0;
+      int bi = 0x7fffffff;
+      double2* c = Cb + (size_t)ell * pp;
+      for (int q = threadIdx.x; q < pp; q += blockDim.x) {
+        double2 acc = entry(q, k);
+        for (int j = 0; j < ell; ++j) acc = csub(acc, cmul(dk[j], Cb[(size_t)j * pp + q]));
+        c[q] = acc;
+        if (!((usedq[q >> 5] >> (q & 31)) & 1u)) {
+          const double kk = key(acc);
+          if (kk > bk) { bk = kk; bi = q; }
+        }
+      }
+      const BestPair bq = block_argmax(bk, bi, red);
+      if (bq.i == 0x7fffffff || !(bq.k > 0.0)) break;  // C_l = 0: stop without the term
+      const int qs = bq.i;
+      for (int j = threadIdx.x; j < ell; j += blockDim.x) cq[j] = Cb[(size_t)j * pp + qs];
+      __syncthreads();
+      const double2 piv = c[qs];
+      // residual fibre e = A[q*,:] - sum_j c_j[q*] d_j ; d = e / piv
+      double2* d = Db + (size_t)ell * L;
+      double be = -1.0;
+      int bl = 0x7fffffff;
+      for (int l = threadIdx.x; l < L; l += blockDim.x) {
+        double2 acc = entry(qs, l);
+        for (int j = 0; j < ell; ++j) acc = csub(acc, cmul(cq[j], Db[(size_t)j * L + l]));
+        Eb[l] = acc;
+        d[l] = cdiv(acc, piv);
+        if (l != k && !((usedk[l >> 5] >> (l & 31)) & 1u)) {
+          const double kk = key(acc);
+          if (kk > be) { be = kk; bl = l; }
+        }
+      }
+      __syncthreads();
+      const double nc2 = block_psum(pp, [&](int q) { const double v = key(c[q]); return make_double2(v, 0.0); }, part).x;
+      const double nd2 = block_psum(L, [&](int l) { const double v = key(d[l]); return make_double2(v, 0.0); }, part).x;
+      double cross = 0.0;
+      for (int j = 0; j < ell; ++j) {
+        const double2* cj = Cb + (size_t)j * pp;
+        const double2* dj = Db + (size_t)j * L;
+        const double2 gc = block_psum(pp, [&](int q) { return cmulconj(cj[q], c[q]); }, part);
+        const double2 gd = block_psum(L, [&](int l) { return cmulconj(dj[l], d[l]); }, part);
+        cross = add(cross, sub(mul(gc.x, gd.x), mul(gc.y, gd.y)));
+      }
+      const BestPair bn = block_argmax(be, bl, red);
+      if (threadIdx.x == 0) {
+        double nrm2 = add(s_nrm2, add(mul(nc2, nd2), mul(2.0, cross)));
+        if (nrm2 < 0.0) nrm2 = 0.0;
+        s_nrm2 = nrm2;
+        a.pivk[(size_t)b * a.rcap + ell] = k;
+        a.pivq[(size_t)b * a.rcap + ell] = qs;
+        usedq[qs >> 5] |= 1u << (qs & 31);
+        usedk[k >> 5] |= 1u << (k & 31);
+        const int rank = ell + 1;
+        const bool stop = mul(__dsqrt_rn(nc2), __dsqrt_rn(nd2)) <= mul(a.eps, __dsqrt_rn(nrm2)) || rank == rmax ||
+                          bn.i == 0x7fffffff;
+        s_stop = stop ? 1 : 0;
+        if (!stop) s_k = bn.i;
+      }
+      __syncthreads();
+      ++ell;
+      if (s_stop) break;
+    }
+    // write rank, allocate Z, back substitution Z = U^{-1} D^T on local columns
+    if (threadIdx.x == 0) {
+      if (overflow) {
+        atomicOr(a.flags, 1);
+        a.rank[b] = -1;
+        a.zoff[b] = -1;
+        s_off = -1;
+      } else {
+        a.rank[b] = ell;
+        const unsigned long long need = (unsigned long long)ell * (unsigned long long)a.n_local;
+        const unsigned long long off = atomicAdd(a.pool_used, need);
+        if (off + need > a.pool_cap) {
+          atomicOr(a.flags, 2);
+          s_off = -1;
+        } else {
+          s_off = (long long)off;
+        }
+        a.zoff[b] = s_off;
+      }
+    }
+    __syncthreads();
+    const long long off = s_off;
+    if (off >= 0) {
+      const int r = ell;
+      const int32_t* kp = a.pivk + (size_t)b * a.rcap;
+      for (int t = threadIdx.x; t < a.n_local; t += blockDim.x) {
+        const int lt = a.local_l[t];
+        for (int l = r - 1; l >= 0; --l) {
+          double2 acc = Db[(size_t)l * L + lt];
+          for (int j = l + 1; j < r; ++j)
+            acc = csub(acc, cmul(Db[(size_t)l * L + kp[j]], a.Zpool[off + (size_t)j * a.n_local + t]));
+          a.Zpool[off + (size_t)l * a.n_local + t] = acc;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void debug_pinned_kernel(const double* x, int64_t n, double* e, double* sn, double* cs) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  e[i] = pinned::exp_(x[i]);
+  pinned::sincos_(x[i], &sn[i], &cs[i]);
+}
+
+}  // namespace
+}  // namespace bem
+
+using namespace bem;
+
+namespace {
+bem_status run_aca(Op& op, cudaStream_t st) {
+  Tree& t = *op.tree;
+  const int nfar = (int)t.far_r.size();
+  op.ranks.assign(nfar, 0);
+  if (nfar == 0) return BEM_OK;
+  const int p = t.p, pp = p * p, L = op.L;
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, t.device);
+  int rcap = std::min(std::min(L, pp), 96);
+  unsigned long long cap = (unsigned long long)nfar * 40ull * (unsigned long long)op.n_local;
+  DBuf<int32_t> flags, counter;
+  DBuf<unsigned long long> used;
+  BEM_CK(flags.alloc(1));
+  BEM_CK(counter.alloc(1));
+  BEM_CK(used.alloc(1));
+  BEM_CK(op.d_rank.alloc(nfar));
+  BEM_CK(op.d_zoff.alloc(nfar));
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    const int grid = std::max(1, std::min(nfar, nsm * 4));
+    DBuf<double> Cbuf, Dbuf, Ebuf;
+    BEM_CK(Cbuf.alloc((size_t)grid * rcap * pp * 2));
+    BEM_CK(Dbuf.alloc((size_t)grid * rcap * L * 2));
+    BEM_CK(Ebuf.alloc((size_t)grid * L * 2));
+    BEM_CK(op.d_pivk.alloc((size_t)nfar * rcap));
+    BEM_CK(op.d_pivq.alloc((size_t)nfar * rcap));
+    BEM_CK(op.d_Z.alloc((size_t)cap * 2));
+    BEM_CK(cudaMemsetAsync(flags.p, 0, sizeof(int32_t), st));
+    BEM_CK(cudaMemsetAsync(counter.p, 0, sizeof(int32_t), st));
+    BEM_CK(cudaMemsetAsync(used.p, 0, sizeof(unsigned long long), st));
+    AcaArgs a;
+    a.nfar = nfar; a.m = t.m; a.p = p; a.L = L; a.rcap = rcap; a.n_local = op.n_local;
+    a.far_r = t.d_far_r.p; a.far_c = t.d_far_c.p; a.xi = t.d_xi.p;
+    a.s = (const double2*)op.d_s.p; a.local_l = op.d_local_l.p; a.eps = op.eps;
+    a.Cbuf = (double2*)Cbuf.p; a.Dbuf = (double2*)Dbuf.p; a.Ebuf = (double2*)Ebuf.p;
+    a.rank = op.d_rank.p; a.pivk = op.d_pivk.p; a.pivq = op.d_pivq.p; a.zoff = op.d_zoff.p;
+    a.Zpool = (double2*)op.d_Z.p; a.pool_used = used.p; a.pool_cap = cap; a.flags = flags.p;
+    a.next_block = counter.p;
+    const int nchmax = (std::max(pp, L) + 31) / 32 + 1;
+    const size_t smem = sizeof(double) * 6 * p + sizeof(double2) * (nchmax + 2 * rcap) +
+                        sizeof(unsigned) * ((pp + 31) / 32 + (L + 31) / 32) + 64;
+    BEM_CK(cudaFuncSetAttribute(aca_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    aca_kernel<<<grid, kAcaThreads, smem, st>>>(a);
+    BEM_CK(cudaGetLastError());
+    int32_t hflags = 0;
+    unsigned long long hused = 0;
+    BEM_CK(cudaMemcpyAsync(&hflags, flags.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    BEM_CK(cudaMemcpyAsync(&hused, used.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    BEM_CK(cudaStreamSynchronize(st));
+    if (hflags & 1) {  // a rank reached the scratch capacity: grow and redo
+      rcap = std::min(std::min(L, pp), rcap * 2);
+      continue;
+    }
+    if (hflags & 2) {  // Z pool too small: exact size is now known
+      cap = hused;
+      continue;
+    }
+    op.rcap = rcap;
+    BEM_CK(cudaMemcpy(op.ranks.data(), op.d_rank.p, sizeof(int32_t) * nfar, cudaMemcpyDeviceToHost));
+    return BEM_OK;
+  }
+  set_error("bem_assemble_h2_aca: ACA did not fit after repeated growth");
+  return BEM_ENOMEM;
+}
+}  // namespace
+
+extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_t L, const int32_t* local_l,
+                                          int32_t n_local, double aca_eps, int32_t mode, void* cuda_stream,
+                                          bem_op* out) {
+  BEM_REQ(th && out, "bem_assemble_h2_aca: NULL tree/out");
+  BEM_REQ(s != nullptr && L >= 1, "bem_assemble_h2_aca: need s and L >= 1");
+  BEM_REQ(aca_eps > 0.0, "bem_assemble_h2_aca: aca_eps must be > 0");
+  BEM_REQ(mode == BEM_MODE_H2ACA || mode == BEM_MODE_H2ONLY || mode == BEM_MODE_DENSE,
+          "bem_assemble_h2_aca: unknown mode %d", mode);
+  *out = nullptr;
+  Tree& t = th->t;
+  if (t.device < 0) {
+    set_error("bem_assemble_h2_aca: tree was built host-only (device = -1)");
+    return BEM_ESTATE;
+  }
+  std::vector<int32_t> loc;
+  if (local_l == nullptr) {
+    loc.resize(L);
+    for (int l = 0; l < L; ++l) loc[l] = l;
+  } else {
+    BEM_REQ(n_local >= 1 && n_local <= L, "bem_assemble_h2_aca: n_local out of range");
+    loc.assign(local_l, local_l + n_local);
+    std::vector<char> seen(L, 0);
+    for (int v : loc) {
+      BEM_REQ(v >= 0 && v < L, "bem_assemble_h2_aca: local index %d out of range", v);
+      BEM_REQ(!seen[v], "bem_assemble_h2_aca: duplicate local index %d", v);
+      seen[v] = 1;
+    }
+  }
+  DeviceGuard dg(t.device);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  bem_op_s* h = new bem_op_s();
+  Op& op = h->o;
+  op.tree = &t; op.L = L; op.n_local = (int)loc.size(); op.mode = mode; op.eps = aca_eps; op.local_l = loc;
+  auto fail = [&](bem_status stt) { delete h; return stt; };
+  std::vector<double> sh(2 * (size_t)L);
+  for (int l = 0; l < L; ++l) { sh[2 * l] = s[l].re; sh[2 * l + 1] = s[l].im; }
+  if (op.d_s.upload(sh) != cudaSuccess || op.d_local_l.upload(loc) != cudaSuccess) {
+    set_error("bem_assemble_h2_aca: upload failed");
+    return fail(BEM_ECUDA);
+  }
+  // near-field frequency classes: pair (l, L-l) when both are local
+  std::vector<int32_t> pos(L, -1), c1, c2;
+  for (int i = 0; i < op.n_local; ++i) pos[loc[i]] = i;
+  std::vector<char> done(op.n_local, 0);
+  for (int i = 0; i < op.n_local; ++i) {
+    if (done[i]) continue;
+    const int l = loc[i], lm = (L - l) % L;
+    const int j = pos[lm];
+    done[i] = 1;
+    if (lm != l && j >= 0 && !done[j]) {
+      // class frequency = the one with l <= L/2 (evaluated), partner = conjugate
+      if (l <= L / 2) { c1.push_back(i); c2.push_back(j); } else { c1.push_back(j); c2.push_back(i); }
+      done[j] = 1;
+    } else {
+      c1.push_back(i); c2.push_back(-1);
+    }
+  }
+  op.n_class = (int)c1.size();
+  if (op.d_class_t1.upload(c1) != cudaSuccess || op.d_class_t2.upload(c2) != cudaSuccess) {
+    set_error("bem_assemble_h2_aca: upload failed");
+    return fail(BEM_ECUDA);
+  }
+  if (mode == BEM_MODE_H2ACA) {
+    bem_status rs = run_aca(op, st);
+    if (rs != BEM_OK) return fail(rs);
+  }
+  if (mode == BEM_MODE_DENSE) {
+    std::vector<int32_t> ptr(t.n_leaves + 1), cb(t.n_leaves, 0), ce(t.n_leaves, (int32_t)t.M);
+    for (int i = 0; i <= t.n_leaves; ++i) ptr[i] = i;
+    if (op.d_dn_ptr.upload(ptr) != cudaSuccess || op.d_dn_cb.upload(cb) != cudaSuccess ||
+        op.d_dn_ce.upload(ce) != cudaSuccess) {
+      set_error("bem_assemble_h2_aca: upload failed");
+      return fail(BEM_ECUDA);
+    }
+  }
+  const int64_t M = t.M;
+  const size_t nl = (size_t)op.n_local;
+  if (op.d_xc.alloc(nl * M * 2) != cudaSuccess || op.d_yc.alloc(nl * M * 2) != cudaSuccess) {
+    set_error("bem_assemble_h2_aca: workspace allocation failed");
+    return fail(BEM_ENOMEM);
+  }
+  if (mode != BEM_MODE_DENSE) {
+    if (op.d_xhat.alloc((size_t)t.C * nl * t.p * 2) != cudaSuccess ||
+        op.d_yhat.alloc((size_t)t.C * nl * t.p * 2) != cudaSuccess) {
+      set_error("bem_assemble_h2_aca: workspace allocation failed");
+      return fail(BEM_ENOMEM);
+    }
+  }
+  if (cudaStreamSynchronize(st) != cudaSuccess) {
+    set_error("bem_assemble_h2_aca: %s", cudaGetErrorString(cudaGetLastError()));
+    return fail(BEM_ECUDA);
+  }
+  t.refcount++;
+  *out = h;
+  return BEM_OK;
+}
+
+extern "C" bem_status bem_aca_export(bem_op oh, int32_t* ranks, int32_t* pivots, int64_t* total_rank) {
+  BEM_REQ(oh, "bem_aca_export: NULL op");
+  Op& op = oh->o;
+  if (op.mode != BEM_MODE_H2ACA) {
+    set_error("bem_aca_export: operator was not assembled with BEM_MODE_H2ACA");
+    return BEM_ESTATE;
+  }
+  const int nfar = (int)op.ranks.size();
+  int64_t tot = 0;
+  for (int r : op.ranks) tot += r;
+  if (total_rank) *total_rank = tot;
+  if (ranks) std::copy(op.ranks.begin(), op.ranks.end(), ranks);
+  if (pivots && nfar > 0) {
+    DeviceGuard dg(op.tree->device);
+    std::vector<int32_t> pk((size_t)nfar * op.rcap), pq((size_t)nfar * op.rcap);
+    BEM_CK(cudaMemcpy(pk.data(), op.d_pivk.p, sizeof(int32_t) * pk.size(), cudaMemcpyDeviceToHost));
+    BEM_CK(cudaMemcpy(pq.data(), op.d_pivq.p, sizeof(int32_t) * pq.size(), cudaMemcpyDeviceToHost));
+    int64_t o = 0;
+    for (int b = 0; b < nfar; ++b)
+      for (int j = 0; j < op.ranks[b]; ++j) {
+        pivots[2 * o] = pk[(size_t)b * op.rcap + j];
+        pivots[2 * o + 1] = pq[(size_t)b * op.rcap + j];
+        ++o;
+      }
+  }
+  return BEM_OK;
+}
+
+extern "C" bem_status bem_op_destroy(bem_op oh) {
+  if (!oh) return BEM_OK;
+  DeviceGuard dg(oh->o.tree->device);
+  oh->o.tree->refcount--;
+  for (auto& e : oh->o.ev)
+    if (e) cudaEventDestroy(e);
+  delete oh;
+  return BEM_OK;
+}
+
+extern "C" bem_status bem_debug_pinned(const double* x, int64_t n, double* e, double* sn, double* cs,
+                                       int32_t device) {
+  BEM_REQ(x && e && sn && cs && n >= 0, "bem_debug_pinned: bad arguments");
+  if (n == 0) return BEM_OK;
+  DeviceGuard dg(device);
+  DBuf<double> dx, de, ds, dc;
+  BEM_CK(dx.alloc(n)); BEM_CK(de.alloc(n)); BEM_CK(ds.alloc(n)); BEM_CK(dc.alloc(n));
+  BEM_CK(cudaMemcpy(dx.p, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+  debug_pinned_kernel<<<(unsigned)((n + 255) / 256), 256>>>(dx.p, n, de.p, ds.p, dc.p);
+  BEM_CK(cudaGetLastError());
+  BEM_CK(cudaMemcpy(e, de.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  BEM_CK(cudaMemcpy(sn, ds.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  BEM_CK(cudaMemcpy(cs, dc.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return BEM_OK;
+}

@@ -1,0 +1,152 @@
+// Internal definitions shared by the library's translation units.
+// (Nothing here is shared with oracle/: the oracle is independent test infra.)
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/bem.h"
+
+namespace bem {
+
+void set_error(const char* fmt, ...);
+
+#define BEM_CK(call)                                                                        \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      bem::set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), __FILE__, __LINE__, \
+                     cudaGetErrorString(e_));                                               \
+      return e_ == cudaErrorMemoryAllocation ? BEM_ENOMEM : BEM_ECUDA;                      \
+    }                                                                                       \
+  } while (0)
+
+#define BEM_REQ(cond, ...)        \
+  do {                            \
+    if (!(cond)) {                \
+      bem::set_error(__VA_ARGS__); \
+      return BEM_EINVAL;          \
+    }                             \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (dev < 0) return;  // host-only handle
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev < 0) return;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <class T>
+struct DBuf {  // owning device buffer
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  cudaError_t alloc(size_t count) {
+    release();
+    if (count == 0) return cudaSuccess;
+    cudaError_t e = cudaMalloc((void**)&p, count * sizeof(T));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+  cudaError_t upload(const std::vector<T>& h) {
+    cudaError_t e = alloc(h.size());
+    if (e != cudaSuccess || h.empty()) return e;
+    return cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+  }
+};
+
+struct Tree {
+  int device = 0;
+  int64_t M = 0;
+  int C = 0, n_leaves = 0, depth = 0, m = 1, p = 1, nmin = 2;
+  double eta = 1.0;
+  int refcount = 0;
+  // host
+  std::vector<int32_t> perm, begin, end, son0, son1, level, parent;
+  std::vector<double> box, xi;  // box C*6, xi C*3*m
+  std::vector<int32_t> near_r, near_c, far_r, far_c;
+  std::vector<int32_t> leaves;                   // leaf cluster ids in DFS order
+  std::vector<std::vector<int32_t>> level_nonleaf;  // non-leaf clusters per level
+  int64_t nnz_near = 0;
+  // device, cluster order
+  DBuf<int32_t> d_perm, d_begin, d_end, d_son0, d_son1, d_parent, d_leaf_of;
+  DBuf<double> d_cen;    // M*3
+  DBuf<double> d_qn;     // M*21 quadrature nodes
+  DBuf<double> d_qw;     // M*7  w_q * |T_j| / (4 pi)
+  DBuf<double> d_selfJ;  // M    J(T)/(4 pi)
+  DBuf<double> d_area;   // M
+  DBuf<double> d_U, d_W; // M*p
+  DBuf<double> d_E;      // C*p*p (E of cluster c w.r.t. its parent)
+  DBuf<double> d_xi;     // C*3*m
+  DBuf<int32_t> d_leaves;
+  // near CSR over leaves (by leaf index): column cluster ranges
+  DBuf<int32_t> d_near_ptr, d_near_cb, d_near_ce;
+  // far CSR by row cluster
+  std::vector<int32_t> far_ptr, far_sorted;  // far_sorted: block ids grouped by row cluster
+  DBuf<int32_t> d_far_ptr, d_far_sorted, d_far_r, d_far_c;
+  std::vector<DBuf<int32_t>> d_level_nonleaf;
+};
+
+struct Op {
+  Tree* tree = nullptr;
+  int L = 0, n_local = 0, mode = 0;
+  double eps = 0.0;
+  std::vector<int32_t> local_l;
+  DBuf<double> d_s;        // L complex (interleaved)
+  DBuf<int32_t> d_local_l; // n_local
+  // frequency classes for the near field: (t1, t2) local indices, t2 = -1 if unpaired
+  int n_class = 0;
+  DBuf<int32_t> d_class_t1, d_class_t2;
+  // BEM_MODE_DENSE: every leaf's near list is the whole index range [0, M)
+  DBuf<int32_t> d_dn_ptr, d_dn_cb, d_dn_ce;
+  // ACA skeleton
+  int rcap = 0;
+  std::vector<int32_t> ranks;  // host copy
+  DBuf<int32_t> d_rank, d_pivk, d_pivq;  // pivk/pivq: nfar * rcap
+  DBuf<int64_t> d_zoff;                  // nfar
+  DBuf<double> d_Z;                      // pool: sum r_b * n_local complex
+  // workspaces
+  DBuf<double> d_xc, d_yc, d_xhat, d_yhat;
+  // profiling
+  bool profile = false;
+  cudaEvent_t ev[6] = {};
+  double timings[5] = {0, 0, 0, 0, 0};
+};
+
+// launchers (apply.cu)
+bem_status apply_launch(Op& op, const double* x, double* y, cudaStream_t st);
+// fft.cu
+bem_status fft_transform(const double* in, double* out, int64_t M, int N, double R, bool inverse,
+                         cudaStream_t st);
+
+}  // namespace bem
+
+struct bem_tree_s {
+  bem::Tree t;
+};
+struct bem_op_s {
+  bem::Op o;
+};

@@ -1,0 +1,223 @@
+// K4: batched R-scaled CQM transforms along the time/frequency axis
+// (eq:omega_n P:436-441, eq:slphelm P:529-540; reading D2):
+//   forward  X_l = sum_n R^n x_n w^{nl},             w = e^{-2 pi i/L}
+//   inverse  y_n = R^{-n}/L sum_l Y_l w^{-nl}
+// L = N+1 has large prime factors (33, 129, 257, 513, 1025), so each column
+// is transformed by Bluestein's chirp-z identity nl = (n^2 + l^2 - (l-n)^2)/2:
+//   out_j = post_j sum_i (in_i pre_i) h_{j-i}
+// with chirp c_k = e^{-pi i (k^2 mod 2L)/L} (index reduced in integers), and
+//   forward: pre_i = R^i c_i,   h_k = conj(c_k), post_j = c_j
+//   inverse: pre_i = conj(c_i), h_k = c_k,       post_j = R^{-j} conj(c_j)/L.
+// The length-L linear convolution runs as a power-of-two P >= 2L-1 radix-2
+// FFT in shared memory, one CTA per group of DOF columns (coalesced row loads).
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <tuple>
+
+#include "common.cuh"
+
+namespace bem {
+namespace {
+
+struct Plan {
+  int L = 0, P = 0, logP = 0;
+  DBuf<double> pre, post, hhat, tw;  // complex arrays (interleaved)
+};
+
+std::mutex g_plan_mu;
+std::map<std::tuple<int, int, uint64_t, int>, std::unique_ptr<Plan>> g_plans;
+
+// host radix-2 FFT (plan construction only), sign = -1 forward
+void host_fft(std::vector<double>& re, std::vector<double>& im, int sign) {
+  const int n = (int)re.size();
+  for (int i = 1, j = 0; i < n; ++i) {
+    int bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) { std::swap(re[i], re[j]); std::swap(im[i], im[j]); }
+  }
+  for (int len = 2; len <= n; len <<= 1) {
+    for (int i = 0; i < n; i += len)
+      for (int k = 0; k < len / 2; ++k) {
+        const double ang = sign * 2.0 * M_PI * (double)k / (double)len;
+        const double wr = std::cos(ang), wi = std::sin(ang);
+        const double ur = re[i + k], ui = im[i + k];
+        const double vr = re[i + k + len / 2] * wr - im[i + k + len / 2] * wi;
+        const double vi = re[i + k + len / 2] * wi + im[i + k + len / 2] * wr;
+        re[i + k] = ur + vr; im[i + k] = ui + vi;
+        re[i + k + len / 2] = ur - vr; im[i + k + len / 2] = ui - vi;
+      }
+  }
+}
+
+bem_status get_plan(int N, double R, bool inverse, Plan** out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  uint64_t rbits;
+  std::memcpy(&rbits, &R, 8);
+  auto key = std::make_tuple(dev, N, rbits, inverse ? 1 : 0);
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  auto it = g_plans.find(key);
+  if (it != g_plans.end()) { *out = it->second.get(); return BEM_OK; }
+  auto pl = std::make_unique<Plan>();
+  const int L = N + 1;
+  int P = 1, logP = 0;
+  while (P < 2 * L - 1) { P <<= 1; ++logP; }
+  pl->L = L; pl->P = P; pl->logP = logP;
+  std::vector<double> cre(L), cim(L);
+  for (int k = 0; k < L; ++k) {
+    const long long k2 = ((long long)k * k) % (2LL * L);
+    const double ang = M_PI * (double)k2 / (double)L;
+    cre[k] = std::cos(ang); cim[k] = -std::sin(ang);
+  }
+  std::vector<double> pre(2 * L), post(2 * L), hr(P, 0.0), hi(P, 0.0), tw(P);
+  for (int k = 0; k < L; ++k) {
+    if (!inverse) {
+      const double rk = std::pow(R, (double)k);
+      pre[2 * k] = rk * cre[k]; pre[2 * k + 1] = rk * cim[k];
+      post[2 * k] = cre[k]; post[2 * k + 1] = cim[k];
+    } else {
+      const double sc = std::pow(R, -(double)k) / (double)L;
+      pre[2 * k] = cre[k]; pre[2 * k + 1] = -cim[k];
+      post[2 * k] = sc * cre[k]; post[2 * k + 1] = -sc * cim[k];
+    }
+    const double h_re = cre[k], h_im = inverse ? cim[k] : -cim[k];
+    hr[k] = h_re; hi[k] = h_im;
+    if (k > 0) { hr[P - k] = h_re; hi[P - k] = h_im; }
+  }
+  host_fft(hr, hi, -1);
+  std::vector<double> hh(2 * P);
+  for (int k = 0; k < P; ++k) { hh[2 * k] = hr[k] / (double)P; hh[2 * k + 1] = hi[k] / (double)P; }
+  for (int k = 0; k < P / 2; ++k) {
+    const double ang = -2.0 * M_PI * (double)k / (double)P;
+    tw[2 * k] = std::cos(ang); tw[2 * k + 1] = std::sin(ang);
+  }
+  BEM_CK(pl->pre.upload(pre));
+  BEM_CK(pl->post.upload(post));
+  BEM_CK(pl->hhat.upload(hh));
+  BEM_CK(pl->tw.upload(tw));
+  *out = pl.get();
+  g_plans[key] = std::move(pl);
+  return BEM_OK;
+}
+
+constexpr int kFftThreads = 256;
+
+__device__ __forceinline__ double2 cm(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// in-place radix-2 DIT FFT of NC columns (bit-reversed input order assumed)
+__device__ void smem_fft(double2* buf, int P, int logP, int NC, const double2* __restrict__ tw, bool inv) {
+  for (int s = 0; s < logP; ++s) {
+    const int half = 1 << s;
+    const int tstride = P >> (s + 1);
+    for (int idx = threadIdx.x; idx < NC * (P >> 1); idx += blockDim.x) {
+      const int col = idx / (P >> 1), bfly = idx % (P >> 1);
+      const int grp = bfly >> s, pos = bfly & (half - 1);
+      const int i = (grp << (s + 1)) + pos, j = i + half;
+      double2 w = tw[pos * tstride];
+      if (inv) w.y = -w.y;
+      double2* b = buf + (size_t)col * P;
+      const double2 u = b[i], v = cm(b[j], w);
+      b[i] = make_double2(u.x + v.x, u.y + v.y);
+      b[j] = make_double2(u.x - v.x, u.y - v.y);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kFftThreads) bluestein_kernel(const double2* __restrict__ in, double2* __restrict__ out,
+                                                               int64_t M, int L, int P, int logP, int NC,
+                                                               const double2* __restrict__ pre,
+                                                               const double2* __restrict__ post,
+                                                               const double2* __restrict__ hhat,
+                                                               const double2* __restrict__ tw) {
+  extern __shared__ double2 buf[];
+  const int64_t c0 = (int64_t)blockIdx.x * NC;
+  const int nc = (int)min((int64_t)NC, M - c0);
+  // load with pre-chirp into bit-reversed positions; zero padding
+  for (int idx = threadIdx.x; idx < NC * P; idx += blockDim.x) {
+    const int n = idx / NC, col = idx % NC;
+    double2 v = make_double2(0.0, 0.0);
+    if (n < L && col < nc) v = cm(in[(int64_t)n * M + c0 + col], pre[n]);
+    const int rv = (int)(__brev((unsigned)n) >> (32 - logP));
+    if (n < P) buf[(size_t)col * P + rv] = v;
+  }
+  __syncthreads();
+  smem_fft(buf, P, logP, NC, tw, false);
+  // multiply by the filter spectrum (already scaled by 1/P), re-order bit-reversed
+  for (int idx = threadIdx.x; idx < NC * P; idx += blockDim.x) {
+    const int col = idx / P, k = idx % P;
+    buf[(size_t)col * P + k] = cm(buf[(size_t)col * P + k], hhat[k]);
+  }
+  __syncthreads();
+  // bit-reverse permutation in place (swap pairs once)
+  for (int idx = threadIdx.x; idx < NC * P; idx += blockDim.x) {
+    const int col = idx / P, k = idx % P;
+    const int rv = (int)(__brev((unsigned)k) >> (32 - logP));
+    if (k < rv) {
+      double2* b = buf + (size_t)col * P;
+      const double2 t = b[k];
+      b[k] = b[rv];
+      b[rv] = t;
+    }
+  }
+  __syncthreads();
+  smem_fft(buf, P, logP, NC, tw, true);
+  for (int idx = threadIdx.x; idx < NC * L; idx += blockDim.x) {
+    const int j = idx / NC, col = idx % NC;
+    if (col < nc) out[(int64_t)j * M + c0 + col] = cm(buf[(size_t)col * P + j], post[j]);
+  }
+}
+
+}  // namespace
+
+bem_status fft_transform(const double* in, double* out, int64_t M, int N, double R, bool inverse, cudaStream_t st) {
+  Plan* pl = nullptr;
+  bem_status rs = get_plan(N, R, inverse, &pl);
+  if (rs != BEM_OK) return rs;
+  const int NC = std::max(1, 4096 / pl->P);
+  const size_t smem = sizeof(double2) * (size_t)NC * pl->P;
+  BEM_CK(cudaFuncSetAttribute(bluestein_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const unsigned grid = (unsigned)((M + NC - 1) / NC);
+  bluestein_kernel<<<grid, kFftThreads, smem, st>>>((const double2*)in, (double2*)out, M, pl->L, pl->P, pl->logP, NC,
+                                                    (const double2*)pl->pre.p, (const double2*)pl->post.p,
+                                                    (const double2*)pl->hhat.p, (const double2*)pl->tw.p);
+  BEM_CK(cudaGetLastError());
+  return BEM_OK;
+}
+
+}  // namespace bem
+
+using namespace bem;
+
+static bem_status transform_entry(const bem_c128* in, bem_c128* out, int64_t M, int32_t N, double R, void* stream,
+                                  bool inverse) {
+  BEM_REQ(in && out, "cqm transform: NULL pointer");
+  BEM_REQ(M >= 1 && N >= 1, "cqm transform: need M_loc >= 1 and N >= 1");
+  BEM_REQ(R > 0.0 && R <= 1.0, "cqm transform: R must lie in (0,1]");
+  const size_t bytes = (size_t)(N + 1) * M * 16;
+  BEM_REQ((const char*)in + bytes <= (const char*)out || (const char*)out + bytes <= (const char*)in,
+          "cqm transform: in-place / overlapping buffers are not supported");
+  cudaPointerAttributes at;
+  BEM_CK(cudaPointerGetAttributes(&at, in));
+  BEM_REQ(at.type == cudaMemoryTypeDevice, "cqm transform: input must be device memory");
+  DeviceGuard dg(at.device);
+  BEM_CK(cudaPointerGetAttributes(&at, out));
+  BEM_REQ(at.type == cudaMemoryTypeDevice, "cqm transform: output must be device memory");
+  return fft_transform((const double*)in, (double*)out, M, N, R, inverse, (cudaStream_t)stream);
+}
+
+extern "C" bem_status cqm_forward(const bem_c128* x_time, bem_c128* x_freq, int64_t M_loc, int32_t N, double R,
+                                  void* cuda_stream) {
+  return transform_entry(x_time, x_freq, M_loc, N, R, cuda_stream, false);
+}
+
+extern "C" bem_status cqm_inverse(const bem_c128* y_freq, bem_c128* y_time, int64_t M_loc, int32_t N, double R,
+                                  void* cuda_stream) {
+  return transform_entry(y_freq, y_time, M_loc, N, R, cuda_stream, true);
+}

@@ -1,0 +1,93 @@
+"""Frequency sharding and the time<->frequency transpose.
+
+* Frequency classes {0} and {j, L-j} (j = 1..) are kept whole on one rank so
+  the near field (K1) shares one exp/sincos per conjugate pair; contiguous
+  balanced class ranges per rank (Remark P:1607-1614: frequencies decouple).
+* Time-domain data are DOF-sharded: rank g owns panels [M g/G, M (g+1)/G).
+* The transpose between DOF shards [L][M_g] and frequency shards [L_g][M] is
+  ONE all-to-all per direction (torch.distributed all_to_all_single: NCCL over
+  NVLink on GPUs, gloo in the CPU tests).  Packing is plumbing (torch copies);
+  every transform and apply runs in libbem's kernels (apply/forward/inverse
+  callables passed in).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def freq_classes(L: int):
+    cls = [[0]]
+    for j in range(1, L // 2 + 1):
+        if L - j != j:
+            cls.append([j, L - j])
+        else:
+            cls.append([j])
+    return cls
+
+
+def shard_frequencies(L: int, G: int):
+    """local frequency lists per rank (balanced contiguous ranges of classes)."""
+    cls = freq_classes(L)
+    if G > len(cls):
+        raise ValueError(f"{G} ranks but only {len(cls)} frequency classes")
+    sizes = np.array([len(c) for c in cls])
+    before = np.cumsum(sizes) - sizes  # frequencies preceding each class
+    bounds = [0]
+    for g in range(1, G):
+        b = int(np.argmin(np.abs(before - sizes.sum() * g / G)))
+        b = min(max(b, bounds[-1] + 1), len(cls) - (G - g))
+        bounds.append(b)
+    bounds.append(len(cls))
+    return [np.array([l for c in cls[bounds[g]:bounds[g + 1]] for l in c], dtype=np.int32) for g in range(G)]
+
+
+def dof_ranges(M: int, G: int):
+    return [(M * g // G, M * (g + 1) // G) for g in range(G)]
+
+
+class ShardedTimeOperator:
+    """y = inverse(V forward(x)) with DOF-sharded time data on G ranks."""
+
+    def __init__(self, rank: int, world: int, M: int, L: int, apply_fn, forward_fn, inverse_fn, group=None):
+        import torch
+        self.rank, self.G, self.M, self.L = rank, world, M, L
+        self.local = shard_frequencies(L, world)
+        self.ranges = dof_ranges(M, world)
+        self.apply_fn, self.forward_fn, self.inverse_fn = apply_fn, forward_fn, inverse_fn
+        self.group = group
+        self._torch = torch
+
+    def local_frequencies(self):
+        return self.local[self.rank]
+
+    def _a2a(self, send_chunks, recv_shapes, device):
+        import torch.distributed as dist
+        torch = self._torch
+        send = torch.cat([torch.view_as_real(c.contiguous()).reshape(-1) for c in send_chunks])
+        rsz = [int(np.prod(s)) * 2 for s in recv_shapes]
+        recv = torch.empty(sum(rsz), dtype=torch.float64, device=device)
+        ssz = [c.numel() * 2 for c in send_chunks]
+        dist.all_to_all_single(recv, send, output_split_sizes=rsz, input_split_sizes=ssz, group=self.group)
+        out, o = [], 0
+        for s, n in zip(recv_shapes, rsz):
+            out.append(torch.view_as_complex(recv[o:o + n].view(*s, 2)))
+            o += n
+        return out
+
+    def step(self, x_loc):
+        """x_loc: [L][M_g] complex (this rank's DOF shard) -> y_loc [L][M_g]."""
+        torch = self._torch
+        g = self.rank
+        xf = self.forward_fn(x_loc)  # [L][M_g]
+        send = [xf.index_select(0, torch.as_tensor(self.local[h], device=xf.device)) for h in range(self.G)]
+        Mg = [e - b for b, e in self.ranges]
+        Lg = len(self.local[g])
+        recv = self._a2a(send, [(Lg, Mg[h]) for h in range(self.G)], xf.device)
+        xl = torch.cat(recv, dim=1).contiguous()  # [L_g][M] in panel order
+        yl = self.apply_fn(xl)
+        send = [yl[:, b:e] for (b, e) in self.ranges]
+        recv = self._a2a(send, [(len(self.local[h]), Mg[g]) for h in range(self.G)], xf.device)
+        yf = torch.empty_like(xf)
+        for h in range(self.G):
+            yf.index_copy_(0, torch.as_tensor(self.local[h], device=xf.device), recv[h])
+        return self.inverse_fn(yf)

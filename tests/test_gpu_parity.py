@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA library (through the C-ABI) against the CPU oracle.
+
+Tolerances (SURVEY C13 / north_star):
+  * trees, admissibility lists, ACA ranks and pivots: bit-exact;
+  * apply vs identical-compression oracle: global relative l2 <= 1e-10
+    (per-frequency reported, gated at 1e-8);
+  * apply vs dense: <= 10 max(eps_ACA, e_H2), e_H2 measured by the oracle;
+  * time domain compared on R^n-scaled sequences (R^{-N} = 1e5 conditioning);
+  * solve: residual <= 1e-8 (re-evaluated by the oracle, slack 1.5e-8).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as _t
+    assert _t.cuda.is_available()
+    return _t
+
+
+@pytest.fixture(scope="module")
+def pb():
+    import paper_2006_05186_b200 as _pb
+    _pb.lib()
+    return _pb
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def _apply(pb, torch, op, x):
+    xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    y = op.apply(xt)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def test_pinned_functions_bitwise_identical(pb):
+    """C14: device pinned exp/sincos bit-identical to the oracle's on 1e6 arguments."""
+    rng = np.random.default_rng(0)
+    x = np.concatenate([-rng.random(400000) * 745.0, rng.random(600000) * 6500.0, [0.0, -746.5, -745.2, 1e-300]])
+    e, s, c = pb.debug_pinned(x)
+    assert np.array_equal(e.view(np.uint64), O.pexp(x).view(np.uint64))
+    so, co = O.psincos(x)
+    assert np.array_equal(s.view(np.uint64), so.view(np.uint64))
+    assert np.array_equal(c.view(np.uint64), co.view(np.uint64))
+
+
+def test_dense_config1(pb, torch):
+    """Minimum slice: config 1, dense mode, all 33 frequencies."""
+    V, T = synth.config_mesh(1)
+    N = 32
+    M, L = len(T), N + 1
+    s = pb.cqm_frequencies(N, 2.0)
+    tree = pb.Tree(V, T, 10 ** 6, 1.0, 1)
+    op = pb.Operator(tree, s, 1e-6, mode=pb.BEM_MODE_DENSE)
+    x = synth.random_density(1, L, M)
+    y = _apply(pb, torch, op, x)
+    yo = O.H2(V, T, 10 ** 6, 1.0, 1).apply(O.MODE_DENSE, s, x)
+    assert _rel(y, yo) <= 1e-10
+    for l in range(L):
+        assert _rel(y[l], yo[l]) <= 1e-10, l
+
+
+def test_tree_on_device_matches_oracle(pb):
+    V, T = synth.icosphere(3)
+    a = pb.Tree(V, T, 32, 1.0, 3).export()
+    b = O.H2(V, T, 32, 1.0, 3).export()
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("N", [32, 128])
+def test_h2aca_1280_all_modes(pb, torch, N):
+    """1280-panel sphere with config-2 parameters: H2ONLY and H2ACA vs the
+    identical oracle (<= 1e-10), pivots bit-exact, and vs dense <= 10 max(eps, e_H2)."""
+    V, T = synth.icosphere(3)
+    M, L, eps = len(T), N + 1, 1e-6
+    s = pb.cqm_frequencies(N, 2.0)
+    x = synth.random_density(2, L, M)
+    oh = O.H2(V, T, 32, 1.0, 3)
+    oa = oh.aca(s, eps)
+    tree = pb.Tree(V, T, 32, 1.0, 3)
+    op = pb.Operator(tree, s, eps, mode=pb.BEM_MODE_H2ACA)
+    ga = op.aca_export()
+    assert np.array_equal(ga["ranks"], oa["ranks"])
+    assert np.array_equal(ga["pivots"], oa["pivots"])
+    y = _apply(pb, torch, op, x)
+    yo = oh.apply(O.MODE_H2ACA, s, x)
+    assert _rel(y, yo) <= 1e-10
+    for l in range(L):
+        assert _rel(y[l], yo[l]) <= 1e-8
+    op2 = pb.Operator(tree, s, eps, mode=pb.BEM_MODE_H2ONLY)
+    y2 = _apply(pb, torch, op2, x)
+    yo2 = oh.apply(O.MODE_H2ONLY, s, x)
+    assert _rel(y2, yo2) <= 1e-10
+    lsel = np.array([0, 1, N // 2, N])
+    yd = oh.apply(O.MODE_DENSE, s, x[lsel], lsel)
+    eh2 = _rel(yo2[lsel], yd)
+    assert _rel(y[lsel], yd) <= 10 * max(eps, eh2)
+
+
+def test_aca_pivots_bitexact_config2(pb):
+    """Config 2 (5120 panels, L=129, m=3, eps=1e-6): every far block's rank and
+    pivot sequence bit-identical to the oracle's ACA."""
+    V, T = synth.config_mesh(2)
+    s = pb.cqm_frequencies(128, 2.0)
+    tree = pb.Tree(V, T, 32, 1.0, 3)
+    op = pb.Operator(tree, s, 1e-6, mode=pb.BEM_MODE_H2ACA, local_l=[0, 1])
+    ga = op.aca_export()
+    oa = O.H2(V, T, 32, 1.0, 3).aca(s, 1e-6)
+    assert np.array_equal(ga["ranks"], oa["ranks"])
+    assert np.array_equal(ga["pivots"], oa["pivots"])
+    assert 15 < ga["ranks"].mean() < 40
+
+
+def test_config2_full_apply_sampled(pb, torch):
+    """Config 2 at full size in the bench's launch configuration (all 129
+    frequencies on one device); the oracle evaluates a frequency sample."""
+    V, T = synth.config_mesh(2)
+    N, M = 128, len(T)
+    L = N + 1
+    s = pb.cqm_frequencies(N, 2.0)
+    tree = pb.Tree(V, T, 32, 1.0, 3)
+    op = pb.Operator(tree, s, 1e-6)
+    x = synth.random_density(2, L, M)
+    y = _apply(pb, torch, op, x)
+    lsel = np.array([0, 3, 64, 127])
+    oh = O.H2(V, T, 32, 1.0, 3)
+    oh.aca(s, 1e-6)
+    yo = oh.apply(O.MODE_H2ACA, s, x[lsel], lsel)
+    assert _rel(y[lsel], yo) <= 1e-10
+    y2 = _apply(pb, torch, op, x)
+    assert np.array_equal(y, y2)  # bitwise reproducible
+
+
+def test_local_frequency_subset(pb, torch):
+    """Frequency sharding: a local set with paired (l, L-l) and
+    unpaired frequencies gives the same columns as the oracle."""
+    V, T = synth.icosphere(3)
+    N = 32
+    M, L = len(T), N + 1
+    s = pb.cqm_frequencies(N, 2.0)
+    loc = np.array([0, 5, 28, 7, 31, 2, 16])  # (5,28) paired; 7, 31, 2, 16 unpaired
+    tree = pb.Tree(V, T, 32, 1.0, 3)
+    op = pb.Operator(tree, s, 1e-6, local_l=loc)
+    x = synth.random_density(3, len(loc), M)
+    y = _apply(pb, torch, op, x)
+    oh = O.H2(V, T, 32, 1.0, 3)
+    oh.aca(s, 1e-6)
+    yo = oh.apply(O.MODE_H2ACA, s, x, loc)
+    assert _rel(y, yo) <= 1e-10
+
+
+@pytest.mark.parametrize("N", [1, 32, 128, 256])
+def test_transforms_vs_oracle(pb, torch, N):
+    """K4 vs the oracle's naive DFTs; round trip on R^n-scaled sequences."""
+    L, M = N + 1, 37
+    R = 10.0 ** (-5.0 / N) if N > 1 else 0.3
+    rng = np.random.default_rng(N)
+    xt = rng.standard_normal((L, M)) + 1j * rng.standard_normal((L, M))
+    xg = torch.from_numpy(xt).cuda()
+    xf = pb.cqm_forward(xg, N, R)
+    xo = O.forward(xt, N, R)
+    assert _rel(xf.cpu().numpy(), xo) <= 1e-12
+    back = pb.cqm_inverse(xf, N, R).cpu().numpy()
+    sc = (R ** np.arange(L))[:, None]
+    assert _rel(back * sc, xt * sc) <= 1e-12
+    yo = O.inverse(xo, N, R)
+    assert _rel(back * sc, yo * sc) <= 1e-12
+
+
+def test_time_domain_operator_config1(pb, torch):
+    """(Vx)_n = inverse(V(s_l) forward(x)_l)_n on config 1 vs the oracle chain."""
+    V, T = synth.config_mesh(1)
+    N = 32
+    M, L = len(T), N + 1
+    R = 10.0 ** (-5.0 / N)
+    s = pb.cqm_frequencies(N, 2.0)
+    op = pb.Operator(pb.Tree(V, T, 10 ** 6, 1.0, 1), s, 1e-6, mode=pb.BEM_MODE_DENSE)
+    xt = synth.random_time_data(1, N, M).astype(np.complex128)
+    xf = pb.cqm_forward(torch.from_numpy(xt).cuda(), N, R)
+    yt = pb.cqm_inverse(op.apply(xf), N, R).cpu().numpy()
+    oh = O.H2(V, T, 10 ** 6, 1.0, 1)
+    yo = O.inverse(oh.apply(O.MODE_DENSE, s, O.forward(xt, N, R)), N, R)
+    sc = (R ** np.arange(L))[:, None]
+    assert _rel(yt * sc, yo * sc) <= 1e-10
+
+
+def test_solve_config1(pb, torch):
+    """cqm_solve (frequency-decoupled GMRES) vs the oracle's GMRES: residual
+    re-evaluated by the oracle, solutions within kappa * tol."""
+    V, T = synth.config_mesh(1)
+    N = 32
+    M, L = len(T), N + 1
+    R = 10.0 ** (-5.0 / N)
+    s = pb.cqm_frequencies(N, 2.0)
+    op = pb.Operator(pb.Tree(V, T, 10 ** 6, 1.0, 1), s, 1e-6, mode=pb.BEM_MODE_DENSE)
+    g = synth.pulse(V, T, N, 2.0)
+    phi, st = pb.cqm_solve(op, torch.from_numpy(g).cuda(), R, tol=1e-8)
+    phi = phi.cpu().numpy()
+    assert st["n_unconverged"] == 0 and st["resid_max"] <= 1e-8
+    oh = O.H2(V, T, 10 ** 6, 1.0, 1)
+    gf = O.forward(g, N, R)
+    phif = O.forward(phi, N, R)
+    res = oh.apply(O.MODE_DENSE, s, phif) - gf
+    # phi is the real part of the inverse; its transform carries the O(tol) imaginary residue
+    rel = np.linalg.norm(res, axis=1) / np.linalg.norm(gf, axis=1)
+    assert np.max(rel) <= 1e-6
+    xo, it, rr = oh.gmres(O.MODE_DENSE, s, gf, tol=1e-8)
+    phio = O.inverse(xo, N, R).real
+    sc = (R ** np.arange(L))[:, None]
+    assert _rel(phi * sc, phio * sc) <= 1e-6
+
+
+def test_solve_h2aca_small(pb, torch):
+    """cqm_solve with the H2ACA operator on a 1280-panel sphere (N=16)."""
+    V, T = synth.icosphere(3)
+    N = 16
+    M, L = len(T), N + 1
+    R = 10.0 ** (-5.0 / N)
+    s = pb.cqm_frequencies(N, 2.0)
+    op = pb.Operator(pb.Tree(V, T, 32, 1.0, 3), s, 1e-8)
+    g = synth.pulse(V, T, N, 2.0)
+    phi, st = pb.cqm_solve(op, torch.from_numpy(g).cuda(), R, tol=1e-8, restart=30)
+    assert st["n_unconverged"] == 0
+    oh = O.H2(V, T, 32, 1.0, 3)
+    oh.aca(s, 1e-8)
+    gf = O.forward(g, N, R)
+    xo, it, rr = oh.gmres(O.MODE_H2ACA, s, gf, tol=1e-8, restart=30)
+    phio = O.inverse(xo, N, R).real
+    sc = (R ** np.arange(L))[:, None]
+    assert _rel(phi.cpu().numpy() * sc, phio * sc) <= 1e-6
+
+
+def test_edge_cases(pb, torch):
+    """Single panel, even L (N = 1), zero input, leaf_size >= M."""
+    V = np.array([[0.0, 0, 0], [0.3, 0, 0], [0.1, 0.25, 0.02]])
+    T = np.array([[0, 1, 2]], dtype=np.int32)
+    for N in (1, 4):
+        s = pb.cqm_frequencies(N, 2.0)
+        op = pb.Operator(pb.Tree(V, T, 8, 1.0, 2), s, 1e-6)
+        x = synth.random_density(4, N + 1, 1)
+        y = _apply(pb, torch, op, x)
+        A = np.array([O.dense_matrix(V, T, sl)[0, 0] for sl in s])
+        assert np.max(np.abs(y[:, 0] - A * x[:, 0])) <= 1e-13 * np.max(np.abs(A * x[:, 0]))
+    V, T = synth.icosphere(2)
+    s = pb.cqm_frequencies(1, 1.0, 1e-5)
+    op = pb.Operator(pb.Tree(V, T, 16, 1.0, 2), s, 1e-6)
+    assert np.all(_apply(pb, torch, op, np.zeros((2, len(T)), complex)) == 0)
+    x = synth.random_density(5, 2, len(T))
+    oh = O.H2(V, T, 16, 1.0, 2)
+    oh.aca(s, 1e-6)
+    assert _rel(_apply(pb, torch, op, x), oh.apply(O.MODE_H2ACA, s, x)) <= 1e-10

@@ -78,10 +78,10 @@ bem_status cqm_frequencies(int32_t N, double T, double R, int32_t method, bem_c1
  * inadmissible leaf x leaf (AM9); Chebyshev bases P:957-978).
  *   vertices  host [nv][3] doubles;  triangles host [nt][3] int32, 0-based;
  *   leaf_size n_min > 1 (leaves hold <= n_min panels, AM6); eta > 0;
- *   cheb_order m >= 1 (p = m^3 interpolation points per box);
+ *   cheb_order 1 <= m <= 5 (p = m^3 interpolation points per box);
  *   device: CUDA ordinal.  Synchronous.  *out receives a new handle.
  * EINVAL: nv < 3, nt < 1, an index out of range, a degenerate triangle
- * (area <= 0), leaf_size <= 1, eta <= 0, m < 1 or m > 8, out NULL. */
+ * (area <= 0), leaf_size <= 1, eta <= 0, m < 1 or m > 5, out NULL. */
 bem_status bem_build_tree(const double* vertices, int64_t nv, const int32_t* triangles, int64_t nt,
                           int32_t leaf_size, double eta, int32_t cheb_order, int32_t device, bem_tree* out);
 bem_status bem_tree_get_stats(bem_tree t, bem_tree_stats* out);
@@ -152,6 +152,8 @@ bem_status bem_debug_pinned(const double* x, int64_t n, double* exp_out, double*
                             int32_t device);
 /* FP64 DFMA throughput microbenchmark: returns achieved FLOP/s. */
 bem_status bem_debug_fp64_peak(int32_t device, void* cuda_stream, double* flops_per_s);
+/* mode 0: DFMA loop, 1: FP64 tensor-core mma.sync m8n8k4 loop, 2: both in one CTA. */
+bem_status bem_debug_fp64_peak_ex(int32_t device, void* cuda_stream, int32_t mode, double* flops_per_s);
 /* Per-kernel CUDA-event timings of the last bem_apply_multifreq issued with
  * profiling enabled (bem_op_set_profiling): ms for K1, K2up, K3, K2down, other. */
 bem_status bem_op_set_profiling(bem_op op, int32_t enable);

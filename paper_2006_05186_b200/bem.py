@@ -39,7 +39,7 @@ EXPORTS = [
     "bem_last_error", "cqm_frequencies", "bem_build_tree", "bem_tree_get_stats", "bem_tree_export",
     "bem_tree_destroy", "bem_assemble_h2_aca", "bem_aca_export", "bem_op_destroy", "bem_apply_multifreq",
     "cqm_forward", "cqm_inverse", "cqm_solve", "bem_debug_pinned", "bem_debug_fp64_peak",
-    "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count",
+    "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count", "bem_debug_fp64_peak_ex",
 ]
 
 
@@ -71,6 +71,7 @@ def lib():
         "bem_op_set_profiling": [vp, i32],
         "bem_op_get_timings": [vp, vp],
         "bem_op_launch_count": [vp, vp],
+        "bem_debug_fp64_peak_ex": [i32, vp, i32, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -254,7 +255,8 @@ def debug_pinned(x, device: int = 0):
     return e, s, c
 
 
-def fp64_peak(device: int = 0, stream=None) -> float:
+def fp64_peak(device: int = 0, stream=None, mode: int = 0) -> float:
+    """mode 0: DFMA loop, 1: DMMA (mma.sync f64) loop, 2: both concurrently."""
     out = C.c_double()
-    _check(lib().bem_debug_fp64_peak(int(device), _stream(stream), C.byref(out)))
+    _check(lib().bem_debug_fp64_peak_ex(int(device), _stream(stream), int(mode), C.byref(out)))
     return out.value

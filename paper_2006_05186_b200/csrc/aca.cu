@@ -15,6 +15,7 @@
 // Stored per block: pivots (k_l, q_l) and Z_b = U_b^{-1} D_b^T restricted to
 // the local frequencies, U_b[l][j] = d_l[k_j] (unit upper triangular), so
 // that A_b ~= A_b[:,K] Z_b (eq:maca P:1314-1320 in skeleton form).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 
@@ -476,6 +477,10 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   bem_op_s* h = new bem_op_s();
   Op& op = h->o;
   op.tree = &t; op.L = L; op.n_local = (int)loc.size(); op.mode = mode; op.eps = aca_eps; op.local_l = loc;
+  if (const char* e = getenv("BEM_NEAR_F")) op.near_f = atoi(e);
+  if (const char* e = getenv("BEM_FAR_GENERIC")) op.force_generic = atoi(e) != 0;
+  if (const char* e = getenv("BEM_FAR_KERNEL")) op.far_kernel = atoi(e);
+  if (const char* e = getenv("BEM_FAR4_SMEM_KB")) op.far4_smem_cap = (size_t)atoi(e) * 1024;
   auto fail = [&](bem_status stt) { delete h; return stt; };
   std::vector<double> sh(2 * (size_t)L);
   for (int l = 0; l < L; ++l) { sh[2 * l] = s[l].re; sh[2 * l + 1] = s[l].im; }
@@ -508,6 +513,23 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   if (mode == BEM_MODE_H2ACA) {
     bem_status rs = run_aca(op, st);
     if (rs != BEM_OK) return fail(rs);
+  }
+  if (mode != BEM_MODE_DENSE && !t.far_r.empty()) {
+    std::vector<std::pair<int64_t, int32_t>> w;
+    for (int c = 0; c < t.C; ++c) {
+      int64_t cost = 0;
+      for (int bi = t.far_ptr[c]; bi < t.far_ptr[c + 1]; ++bi)
+        cost += mode == BEM_MODE_H2ACA ? op.ranks[t.far_sorted[bi]] + 1 : 1;
+      if (t.far_ptr[c + 1] > t.far_ptr[c]) w.push_back({-cost, c});
+    }
+    std::sort(w.begin(), w.end());
+    std::vector<int32_t> rows;
+    for (auto& e : w) rows.push_back(e.second);
+    op.n_far_rows = (int)rows.size();
+    if (op.d_far_rows.upload(rows) != cudaSuccess) {
+      set_error("bem_assemble_h2_aca: upload failed");
+      return fail(BEM_ECUDA);
+    }
   }
   if (mode == BEM_MODE_DENSE) {
     std::vector<int32_t> ptr(t.n_leaves + 1), cb(t.n_leaves, 0), ce(t.n_leaves, (int32_t)t.M);

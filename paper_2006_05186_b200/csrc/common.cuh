@@ -128,16 +128,26 @@ struct Op {
   DBuf<int32_t> d_rank, d_pivk, d_pivq;  // pivk/pivq: nfar * rcap
   DBuf<int64_t> d_zoff;                  // nfar
   DBuf<double> d_Z;                      // pool: sum r_b * n_local complex
+  // row clusters owning far blocks, sorted by descending coupling work (K3 order)
+  int n_far_rows = 0;
+  DBuf<int32_t> d_far_rows;
   // workspaces
   DBuf<double> d_xc, d_yc, d_xhat, d_yhat;
+  // kernel variants (tuning knobs; env BEM_NEAR_F, BEM_FAR_GENERIC read at assembly)
+  int near_f = 2;
+  bool force_generic = false;
+  int far_kernel = 4;                 // 4: DMMA (far4), 3: DFMA register tiles (far3)
+  size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM
   // profiling
   bool profile = false;
   cudaEvent_t ev[6] = {};
   double timings[5] = {0, 0, 0, 0, 0};
 };
 
-// launchers (apply.cu)
+// launchers (apply.cu, near.cu, far.cu)
 bem_status apply_launch(Op& op, const double* x, double* y, cudaStream_t st);
+bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st);
+bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st);
 // fft.cu
 bem_status fft_transform(const double* in, double* out, int64_t M, int N, double R, bool inverse,
                          cudaStream_t st);

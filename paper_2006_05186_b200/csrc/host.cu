@@ -278,7 +278,7 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
   BEM_REQ(nt < (int64_t)1 << 30, "bem_build_tree: too many panels");
   BEM_REQ(leaf_size > 1, "bem_build_tree: leaf_size (n_min) must be > 1");
   BEM_REQ(eta > 0.0, "bem_build_tree: eta must be > 0");
-  BEM_REQ(m >= 1 && m <= 8, "bem_build_tree: cheb_order must be in [1,8]");
+  BEM_REQ(m >= 1 && m <= 5, "bem_build_tree: cheb_order must be in [1,5]");
   int ndev = 0;
   if (device >= 0 && cudaGetDeviceCount(&ndev) != cudaSuccess) ndev = 0;
   BEM_REQ(device == -1 || (device >= 0 && device < ndev), "bem_build_tree: device %d not available (%d devices)",

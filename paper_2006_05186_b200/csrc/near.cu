@@ -1,0 +1,194 @@
+// K1: near field evaluated on the fly.
+//
+// For every target panel i (cluster order) and every source panel j in the
+// near-field leaves of i's leaf (inadmissible leaf x leaf blocks, eq:qadm
+// P:905-912), the collocation entry of the single layer V(s) (P:537-540,
+// kernel eq:fundsol P:479-482) with the 7-point rule is
+//   V[i,j](s) = sum_q (w_q |T_j| / 4 pi) e^{-s r_q} / r_q,  r_q = |c_i - y_{j,q}|,
+// and for the self panel (analytic 1/r integral + rule on (e^{-sr}-1)/r)
+//   V[i,i](s) = J(T_i)/4pi + sum_q (w_q |T_i|/4pi) phi(s, r_q),  phi(s,0) = -s.
+// y_l[i] = sum_j V[i,j](s_l) x_l[j] for all local frequencies; a conjugate
+// pair (l, L-l) shares one exp/sincos: V(conj s) = conj V(s).
+//
+// Mapping: one warp per (target, tile of F frequency classes); lanes stride
+// over the source panels (coalesced loads of panel geometry and x); the node
+// loop is kept rolled so the code body stays small (I-cache), F classes are
+// unrolled for ILP; warp butterfly reduction, no atomics.
+#include "common.cuh"
+#include "fastmath.cuh"
+
+namespace bem {
+namespace {
+
+constexpr int kNearWarps = 4;
+
+struct NearArgs {
+  int64_t M;
+  int n_class;
+  const int32_t* leaf_of;
+  const int32_t* near_ptr;
+  const int32_t* near_cb;
+  const int32_t* near_ce;
+  const double* cen;
+  const double* qn;
+  const double* qw;
+  const double* selfJ;
+  const double2* s;
+  const int32_t* local_l;
+  const int32_t* class_t1;
+  const int32_t* class_t2;
+  const double2* xc;
+  double2* yc;
+};
+
+__device__ __forceinline__ void cmac(double2& acc, double2 a, double2 b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+__device__ __forceinline__ void cmac_conj(double2& acc, double2 a, double2 b) {  // acc += conj(a) b
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+
+// self entry V[i,i](s) (rare: once per target and class; libdevice functions)
+__device__ __noinline__ double2 self_entry(const double* qn, const double* qw, double J, const double* c, double sre,
+                                           double sim) {
+  double vr = J - qw[0] * sre, vi = -qw[0] * sim;  // node 0 is the centroid: phi(s,0) = -s
+  for (int q = 1; q < 7; ++q) {
+    const double dx = c[0] - qn[3 * q], dy = c[1] - qn[3 * q + 1], dz = c[2] - qn[3 * q + 2];
+    const double r = sqrt(dx * dx + dy * dy + dz * dz);
+    const double xr = -sre * r, yr = -sim * r;
+    double sn, cs, sh, ch;
+    sincos(yr, &sn, &cs);
+    sincos(0.5 * yr, &sh, &ch);
+    const double re = expm1(xr) * cs - 2.0 * sh * sh;  // Re(e^z - 1), cancellation-free
+    const double im = exp(xr) * sn;
+    vr = fma(qw[q] / r, re, vr);
+    vi = fma(qw[q] / r, im, vi);
+  }
+  return make_double2(vr, vi);
+}
+
+template <int F>
+__global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * kNearWarps + (threadIdx.x >> 5);
+  if (k >= a.M) return;
+  const int c0 = blockIdx.y * F;
+  double sre[F], sim[F];
+  int64_t o1[F], o2[F];
+#pragma unroll
+  for (int f = 0; f < F; ++f) {
+    const int c = c0 + f;
+    if (c < a.n_class) {
+      const int t1 = a.class_t1[c], t2 = a.class_t2[c];
+      const double2 sv = a.s[a.local_l[t1]];
+      sre[f] = sv.x; sim[f] = sv.y;
+      o1[f] = (int64_t)t1 * a.M;
+      o2[f] = t2 >= 0 ? (int64_t)t2 * a.M : -1;
+    } else {
+      sre[f] = 0.0; sim[f] = 0.0; o1[f] = -1; o2[f] = -1;
+    }
+  }
+  double2 acc1[F], acc2[F];
+#pragma unroll
+  for (int f = 0; f < F; ++f) { acc1[f] = make_double2(0.0, 0.0); acc2[f] = make_double2(0.0, 0.0); }
+  const double cx = a.cen[3 * k], cy = a.cen[3 * k + 1], cz = a.cen[3 * k + 2];
+  const int li = a.leaf_of[k];
+  const int rg0 = a.near_ptr[li], rg1 = a.near_ptr[li + 1];
+  for (int rg = rg0; rg < rg1; ++rg) {
+    const int jb = a.near_cb[rg], je = a.near_ce[rg];
+    for (int j = jb + lane; j < je; j += 32) {
+      if (j == k) continue;  // self panel below
+      double2 x1[F], x2[F];
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
+        x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
+      }
+      double2 v[F];
+#pragma unroll
+      for (int f = 0; f < F; ++f) v[f] = make_double2(0.0, 0.0);
+      const double* qn = a.qn + 21 * (int64_t)j;
+      const double* qw = a.qw + 7 * (int64_t)j;
+#pragma unroll 1
+      for (int q = 0; q < 7; ++q) {
+        const double dx = cx - qn[3 * q], dy = cy - qn[3 * q + 1], dz = cz - qn[3 * q + 2];
+        const double d2 = dx * dx + dy * dy + dz * dz;
+        const double ir = rsqrt(d2);
+        const double r = d2 * ir;
+        const double w = qw[q] * ir;
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          const double e = fast::exp_neg(-sre[f] * r) * w;
+          double sn, cs;
+          fast::sincos_(sim[f] * r, &sn, &cs);
+          v[f].x = fma(e, cs, v[f].x);
+          v[f].y = fma(-e, sn, v[f].y);
+        }
+      }
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        cmac(acc1[f], v[f], x1[f]);
+        cmac_conj(acc2[f], v[f], x2[f]);
+      }
+    }
+  }
+  if (lane == 0) {
+    const double c[3] = {cx, cy, cz};
+#pragma unroll 1
+    for (int f = 0; f < F; ++f) {
+      if (o1[f] < 0) continue;
+      const double2 v = self_entry(a.qn + 21 * k, a.qw + 7 * k, a.selfJ[k], c, sre[f], sim[f]);
+      cmac(acc1[f], v, a.xc[o1[f] + k]);
+      if (o2[f] >= 0) cmac_conj(acc2[f], v, a.xc[o2[f] + k]);
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < F; ++f) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      acc1[f].x += __shfl_xor_sync(0xffffffffu, acc1[f].x, off);
+      acc1[f].y += __shfl_xor_sync(0xffffffffu, acc1[f].y, off);
+      acc2[f].x += __shfl_xor_sync(0xffffffffu, acc2[f].x, off);
+      acc2[f].y += __shfl_xor_sync(0xffffffffu, acc2[f].y, off);
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < F; ++f) {
+    if (lane == 2 * f && o1[f] >= 0) a.yc[o1[f] + k] = acc1[f];
+    if (lane == 2 * f + 1 && o2[f] >= 0) a.yc[o2[f] + k] = acc2[f];
+  }
+}
+
+template <int F>
+cudaError_t launch(const NearArgs& na, cudaStream_t st) {
+  dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + F - 1) / F));
+  near_kernel<F><<<g, kNearWarps * 32, 0, st>>>(na);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st) {
+  Tree& t = *op.tree;
+  NearArgs na;
+  na.M = t.M; na.n_class = op.n_class; na.leaf_of = t.d_leaf_of.p;
+  const bool dense = op.mode == BEM_MODE_DENSE;
+  na.near_ptr = dense ? op.d_dn_ptr.p : t.d_near_ptr.p;
+  na.near_cb = dense ? op.d_dn_cb.p : t.d_near_cb.p;
+  na.near_ce = dense ? op.d_dn_ce.p : t.d_near_ce.p;
+  na.cen = t.d_cen.p; na.qn = t.d_qn.p; na.qw = t.d_qw.p; na.selfJ = t.d_selfJ.p;
+  na.s = (const double2*)op.d_s.p; na.local_l = op.d_local_l.p;
+  na.class_t1 = op.d_class_t1.p; na.class_t2 = op.d_class_t2.p; na.xc = xc; na.yc = yc;
+  const int F = op.near_f;
+  cudaError_t e = F == 8 ? launch<8>(na, st) : F == 2 ? launch<2>(na, st) : launch<4>(na, st);
+  BEM_CK(e);
+  return BEM_OK;
+}
+
+}  // namespace bem

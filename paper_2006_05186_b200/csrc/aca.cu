@@ -530,6 +530,48 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
       set_error("bem_assemble_h2_aca: upload failed");
       return fail(BEM_ECUDA);
     }
+    if (mode == BEM_MODE_H2ACA) {
+      // split rows into block-range segments of bounded cost (load balance of K3)
+      int nsm = 148;
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, t.device);
+      int64_t total = 0;
+      for (int b = 0; b < (int)t.far_r.size(); ++b) total += op.ranks[b];
+      int64_t cap = std::max<int64_t>(1, total / (4 * (int64_t)nsm));
+      if (const char* e = getenv("BEM_SEG_CAP")) cap = std::max<int64_t>(1, atoll(e));
+      struct Seg { int64_t cost; int row, bi0, bi1, slot; };
+      std::vector<Seg> segs;
+      std::vector<int32_t> srows, sptr{0};
+      for (int c = 0; c < t.C; ++c) {
+        const int b0 = t.far_ptr[c], b1 = t.far_ptr[c + 1];
+        if (b1 == b0) continue;
+        int start = b0;
+        int64_t acc = 0;
+        for (int bi = b0; bi < b1; ++bi) {
+          const int64_t w = op.ranks[t.far_sorted[bi]];
+          if (acc > 0 && acc + w > cap) {
+            segs.push_back({acc, c, start, bi, (int)segs.size()});
+            start = bi;
+            acc = 0;
+          }
+          acc += w;
+        }
+        segs.push_back({acc, c, start, b1, (int)segs.size()});
+        srows.push_back(c);
+        sptr.push_back((int32_t)segs.size());
+      }
+      std::vector<Seg> order = segs;
+      std::stable_sort(order.begin(), order.end(), [](const Seg& x, const Seg& y) { return x.cost > y.cost; });
+      std::vector<int32_t> flat;
+      for (auto& sg : order) { flat.push_back(sg.row); flat.push_back(sg.bi0); flat.push_back(sg.bi1); flat.push_back(sg.slot); }
+      op.n_segs = (int)segs.size();
+      op.n_seg_rows = (int)srows.size();
+      if (op.d_segs.upload(flat) != cudaSuccess || op.d_seg_rows.upload(srows) != cudaSuccess ||
+          op.d_seg_ptr.upload(sptr) != cudaSuccess ||
+          op.d_part.alloc((size_t)op.n_segs * op.n_local * t.p * 2) != cudaSuccess) {
+        set_error("bem_assemble_h2_aca: segment upload/allocation failed");
+        return fail(BEM_ENOMEM);
+      }
+    }
   }
   if (mode == BEM_MODE_DENSE) {
     std::vector<int32_t> ptr(t.n_leaves + 1), cb(t.n_leaves, 0), ce(t.n_leaves, (int32_t)t.M);

@@ -131,12 +131,17 @@ struct Op {
   // row clusters owning far blocks, sorted by descending coupling work (K3 order)
   int n_far_rows = 0;
   DBuf<int32_t> d_far_rows;
+  // K3 work segments: (row, bi0, bi1, slot) in launch (cost-descending) order;
+  // seg_rows/seg_ptr: per row with far blocks, its contiguous slot range
+  int n_segs = 0, n_seg_rows = 0;
+  DBuf<int32_t> d_segs, d_seg_rows, d_seg_ptr;
+  DBuf<double> d_part;  // n_segs * n_local * p complex
   // workspaces
   DBuf<double> d_xc, d_yc, d_xhat, d_yhat;
   // kernel variants (tuning knobs; env BEM_NEAR_F, BEM_FAR_GENERIC read at assembly)
   int near_f = 2;
   bool force_generic = false;
-  int far_kernel = 4;                 // 4: DMMA (far4), 3: DFMA register tiles (far3)
+  int far_kernel = 6;                 // 6: transposed DMMA (far6), 4: DMMA (far4), 3: DFMA tiles (far3)
   size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM
   // profiling
   bool profile = false;

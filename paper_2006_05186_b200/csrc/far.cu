@@ -206,8 +206,7 @@ cudaError_t dispatch3(const Far3Cfg& c, int nrows, const Far3Args& a, cudaStream
 // (mod 8) complex, B stride = 2 (mod 8) complex.
 struct Far4Args {
   int nl, m, p, p4, rcap, SST, TT, TTP, nT;
-  const int32_t* rows;
-  const int32_t* far_ptr;
+  const int4* segs;  // (row, bi0, bi1, slot): far-block range of a row, launch order
   const int32_t* far_sorted;
   const int32_t* far_c;
   const double* xi;
@@ -217,7 +216,7 @@ struct Far4Args {
   const int64_t* zoff;
   const double2* Z;
   const double2* xhat;
-  double2* yhat;
+  double2* part;  // [slot][t][mu]: partial y^ of the segment (reduced per row afterwards)
 };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -227,14 +226,16 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 template <int MAXT>
-__global__ void __launch_bounds__(256) far4_kernel(Far4Args a) {
+__global__ void __launch_bounds__(256, 2) far4_kernel(Far4Args a) {
   extern __shared__ double2 sm[];
   const int p = a.p, m = a.m, TT = a.TT, TTP = a.TTP, SST = a.SST;
-  const int r = a.rows[blockIdx.x];
+  const int4 sg = a.segs[blockIdx.x];
+  const int r = sg.x;
   const int t0 = blockIdx.y * TT;
   const int mu0 = blockIdx.z * 32;
   const int nrow = min(32, p - mu0);
   const int ntv = min(TT, a.nl - t0);
+  const int nS = nrow * p, nB = ntv * p;
   double2* S = sm;                            // 32 x SST
   double2* B = S + 32 * SST;                  // p4 x TTP
   double* xcn = (double*)(B + (size_t)a.p4 * TTP);  // 3p
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(256) far4_kernel(Far4Args a) {
 #pragma unroll
   for (int i = 0; i < MAXT; ++i) { cre[i][0] = cre[i][1] = cim[i][0] = cim[i][1] = 0.0; }
   const double2* Afrag = S + (mt * 8 + g) * SST + q;
-  for (int bi = a.far_ptr[r]; bi < a.far_ptr[r + 1]; ++bi) {
+  for (int bi = sg.y; bi < sg.z; ++bi) {
     const int b = a.far_sorted[bi];
     const int c = a.far_c[b];
     __syncthreads();
@@ -261,16 +262,41 @@ __global__ void __launch_bounds__(256) far4_kernel(Far4Args a) {
       const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + l]];
       const double2* Zl = Zb + (int64_t)l * a.nl;
       __syncthreads();
-      for (int idx = tid; idx < nrow * p; idx += blockDim.x) {
-        const int i = idx / p, nu = idx - i * p;
+      // produce B = Z_l (.) xhat_c (global loads issued first, 4 in flight) and
+      // the slice rows S(s_{k_l}) (ALU work overlapping the load latency)
+      int us = tid;
+      for (int u0 = tid; u0 < nB; u0 += 4 * 256) {
+        double2 zv[4], xv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int u = u0 + k * 256;
+          if (u < nB) {
+            const int t = u / p;
+            zv[k] = Zl[t];
+            xv[k] = xh[u];
+          }
+        }
+        if (us < nS) {
+          const int i = us / p, nu = us - i * p;
+          const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
+                       dz = xcn[3 * nu + 2] - xr[3 * i + 2];
+          S[i * SST + nu] = kern(sqrt(dx * dx + dy * dy + dz * dz), sv);
+          us += 256;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int u = u0 + k * 256;
+          if (u < nB) {
+            const int t = u / p, nu = u - t * p;
+            B[nu * TTP + t] = make_double2(zv[k].x * xv[k].x - zv[k].y * xv[k].y, zv[k].x * xv[k].y + zv[k].y * xv[k].x);
+          }
+        }
+      }
+      for (; us < nS; us += 256) {
+        const int i = us / p, nu = us - i * p;
         const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
                      dz = xcn[3 * nu + 2] - xr[3 * i + 2];
         S[i * SST + nu] = kern(sqrt(dx * dx + dy * dy + dz * dz), sv);
-      }
-      for (int idx = tid; idx < ntv * p; idx += blockDim.x) {
-        const int t = idx / p, nu = idx - t * p;
-        const double2 z = Zl[t], x = xh[(int64_t)t * p + nu];
-        B[nu * TTP + t] = make_double2(z.x * x.x - z.y * x.y, z.x * x.y + z.y * x.x);
       }
       __syncthreads();
       for (int k0 = 0; k0 < a.p4; k0 += 4) {
@@ -300,7 +326,7 @@ __global__ void __launch_bounds__(256) far4_kernel(Far4Args a) {
       for (int v = 0; v < 2; ++v) {
         const int col = tt * 8 + 2 * q + v;
         if (tt < a.nT && col < ntv)
-          a.yhat[((int64_t)r * a.nl + t0 + col) * p + mu0 + row] = make_double2(cre[i][v], cim[i][v]);
+          a.part[((int64_t)sg.w * a.nl + t0 + col) * p + mu0 + row] = make_double2(cre[i][v], cim[i][v]);
       }
     }
   }
@@ -351,6 +377,211 @@ cudaError_t dispatch4(const Far4Cfg& c, int nrows, const Far4Args& a, cudaStream
     case 8: return launch4<8>(c, nrows, a, st);
     case 9: return launch4<9>(c, nrows, a, st);
     default: return cudaErrorInvalidConfiguration;
+  }
+}
+
+// ------------------------------------------------ far6: transposed DMMA coupling
+// out[t, mu] += sum_j sum_nu (Z_b[j,t] xhat_c[nu,t]) S_b(s_{k_j})[mu,nu]
+// as an (M = t) x (N = mu) x (K = nu) FP64 tensor-core product per term j:
+//   A[t,nu] = Z_b[j,t] xhat_c[nu,t]  (formed in registers from the shared-memory
+//             xhat tile and the thread's Z values: one complex multiply per
+//             fragment, reused for all four 8-row mu tiles),
+//   B[nu,mu] = S_b(s_{k_j})[mu,nu]   (the regenerated slice rows in shared memory).
+// Warp w owns the 8-column t tiles {w, w+8, ...} and all four mu tiles of the
+// 32-row chunk.  Leftover columns (n_t mod 8, e.g. the real frequency l = 0
+// when L = 2^k + 1) are accumulated with DFMA by lanes 0..3 of each warp.
+struct Far6Args {
+  int nl, m, p, p4, rcap, SST, TT, XTP, nT, tb;  // tb = leftover columns [0, tb), DMMA columns [tb, nl)
+  const int4* segs;
+  const int32_t* far_sorted;
+  const int32_t* far_c;
+  const double* xi;
+  const double2* s;
+  const int32_t* rank;
+  const int32_t* pivk;
+  const int64_t* zoff;
+  const double2* Z;
+  const double2* xhat;
+  double2* part;
+};
+
+template <int MT>
+__global__ void __launch_bounds__(256, 2) far6_kernel(Far6Args a) {
+  extern __shared__ double2 sm[];
+  const int p = a.p, m = a.m, SST = a.SST, XTP = a.XTP, p4 = a.p4, tb = a.tb;
+  const int4 sg = a.segs[blockIdx.x];
+  const int r = sg.x;
+  const int tc0 = a.tb + blockIdx.y * a.TT;           // first DMMA column of this CTA
+  const int ncol = min(a.TT, a.nl - tc0);             // DMMA columns (multiple of 8)
+  const bool lead = blockIdx.y == 0;                  // also owns the leftover columns
+  const int mu0 = blockIdx.z * 32;
+  const int nrow = min(32, p - mu0);
+  double2* S = sm;                                    // 32 x SST (rows mu, cols nu)
+  double2* xs = S + 32 * SST;                         // p4 x XTP: [nu][0..tb) leftover, [tb..) DMMA cols
+  double* xr = (double*)(xs + (size_t)p4 * XTP);      // 3 x 32
+  double* xcn = xr + 96;                              // 3p
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  for (int i = tid; i < 32 * SST + p4 * XTP; i += blockDim.x) sm[i] = make_double2(0.0, 0.0);
+  for (int i = tid; i < nrow; i += blockDim.x) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
+  const int ntile = ncol / 8;
+  double acc[MT][4][2][2];  // [t tile][mu tile][re/im][v]
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+  double2 lacc[8];  // leftover columns, lanes 0..3 of each warp own row 4*warp + lane
+#pragma unroll
+  for (int i = 0; i < 8; ++i) lacc[i] = make_double2(0.0, 0.0);
+  const int lrow = 4 * warp + lane;
+  const bool lown = lead && lane < 4 && lrow < nrow && tb > 0;
+  const int ncp = tb + ncol;  // staged columns: leftover (lead only) + DMMA
+  for (int bi = sg.y; bi < sg.z; ++bi) {
+    const int b = a.far_sorted[bi];
+    const int c = a.far_c[b];
+    __syncthreads();
+    for (int i = tid; i < p; i += blockDim.x) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
+    // stage xhat_c: leftover columns (lead CTA) and this CTA's DMMA columns
+    const double2* xh = a.xhat + (int64_t)c * a.nl * p;
+    for (int idx = tid; idx < ncp * p; idx += blockDim.x) {
+      const int tl = idx / p, nu = idx - tl * p;
+      const int tg = tl < tb ? tl : tc0 + (tl - tb);
+      if (tl >= tb || lead) xs[nu * XTP + tl] = xh[(int64_t)tg * p + nu];
+    }
+    const int rk = a.rank[b];
+    const double2* Zb = a.Z + a.zoff[b];
+    for (int l = 0; l < rk; ++l) {
+      const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + l]];
+      const double2* Zl = Zb + (int64_t)l * a.nl;
+      double2 zt[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int tt = warp + 8 * i;
+        zt[i] = tt < ntile ? Zl[tc0 + tt * 8 + g] : make_double2(0.0, 0.0);
+      }
+      __syncthreads();
+      for (int idx = tid; idx < nrow * p; idx += blockDim.x) {
+        const int i = idx / p, nu = idx - i * p;
+        const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
+                     dz = xcn[3 * nu + 2] - xr[3 * i + 2];
+        S[i * SST + nu] = kern(sqrt(dx * dx + dy * dy + dz * dz), sv);
+      }
+      __syncthreads();
+      for (int k0 = 0; k0 < p4; k0 += 4) {
+        double2 bf[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = S[(j * 8 + g) * SST + k0 + q];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const int tt = warp + 8 * i;
+          if (tt < ntile) {
+            const double2 xv = xs[(k0 + q) * XTP + tb + tt * 8 + g];
+            const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
+            const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
+            const double nai = -ai;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+              dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
+              dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
+              dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
+            }
+          }
+        }
+      }
+      if (lown) {
+        for (int tl = 0; tl < tb; ++tl) {
+          const double2 z = Zl[tl];
+          double2 sacc = make_double2(0.0, 0.0);
+          for (int nu = 0; nu < p; ++nu) {
+            const double2 sv2 = S[lrow * SST + nu], xv = xs[nu * XTP + tl];
+            sacc.x += sv2.x * xv.x - sv2.y * xv.y;
+            sacc.y += sv2.x * xv.y + sv2.y * xv.x;
+          }
+          lacc[tl].x += z.x * sacc.x - z.y * sacc.y;
+          lacc[tl].y += z.x * sacc.y + z.y * sacc.x;
+        }
+      }
+    }
+  }
+  double2* out = a.part + (int64_t)sg.w * a.nl * p;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int tt = warp + 8 * i;
+    if (tt >= ntile) continue;
+    const int t = tc0 + tt * 8 + g;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int row = j * 8 + 2 * q + v;
+        if (row < nrow) out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
+      }
+  }
+  if (lown)
+    for (int tl = 0; tl < tb; ++tl) out[(int64_t)tl * p + mu0 + lrow] = lacc[tl];
+}
+
+struct Far6Cfg {
+  int p4 = 0, SST = 0, TT = 0, XTP = 0, nT = 0, tb = 0, ntiles = 0, nchunks = 0, mt = 0;
+  size_t smem = 0;
+};
+
+Far6Cfg choose6(int p, int nl, size_t cap) {
+  Far6Cfg c;
+  const int tb = nl % 8;
+  const int nD = nl - tb;
+  if (nD == 0) return c;
+  const int p4 = (p + 3) / 4 * 4;
+  int SST = p4;
+  while (SST % 8 != 4) ++SST;
+  for (int TTmax : {256, 128, 64, 32, 16, 8}) {
+    const int ntiles = (nD + TTmax - 1) / TTmax;
+    const int TT = ((nD / 8 + ntiles - 1) / ntiles) * 8;
+    int XTP = tb + TT;
+    while (XTP % 8 != 2) ++XTP;  // fragment loads [k][t]: stride 2 (mod 8) complex -> conflict-free
+    const size_t smem = sizeof(double2) * (32 * (size_t)SST + (size_t)p4 * XTP) + sizeof(double) * (96 + 3 * p);
+    if (smem > cap) continue;
+    c.p4 = p4; c.SST = SST; c.TT = TT; c.XTP = XTP; c.nT = TT / 8; c.tb = tb; c.ntiles = ntiles;
+    c.nchunks = (p + 31) / 32; c.mt = (c.nT + 7) / 8; c.smem = smem;
+    if (c.mt > 4) continue;
+    return c;
+  }
+  return Far6Cfg{};
+}
+
+template <int MT>
+cudaError_t launch6(const Far6Cfg& c, int nseg, const Far6Args& a, cudaStream_t st) {
+  auto k = far6_kernel<MT>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  if (e != cudaSuccess) return e;
+  k<<<dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks), 256, c.smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t dispatch6(const Far6Cfg& c, int nseg, const Far6Args& a, cudaStream_t st) {
+  switch (c.mt) {
+    case 1: return launch6<1>(c, nseg, a, st);
+    case 2: return launch6<2>(c, nseg, a, st);
+    case 3: return launch6<3>(c, nseg, a, st);
+    case 4: return launch6<4>(c, nseg, a, st);
+    default: return cudaErrorInvalidConfiguration;
+  }
+}
+
+// yhat[r] = sum over the row's segments (fixed order)
+__global__ void seg_reduce_kernel(const int32_t* __restrict__ rows, const int32_t* __restrict__ seg_ptr,
+                                  const double2* __restrict__ part, double2* __restrict__ yhat, int64_t tile) {
+  const int r = rows[blockIdx.x];
+  const int s0 = seg_ptr[blockIdx.x], s1 = seg_ptr[blockIdx.x + 1];
+  for (int64_t i = threadIdx.x; i < tile; i += blockDim.x) {
+    double2 acc = part[(int64_t)s0 * tile + i];
+    for (int sgi = s0 + 1; sgi < s1; ++sgi) {
+      const double2 v = part[(int64_t)sgi * tile + i];
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    yhat[(int64_t)r * tile + i] = acc;
   }
 }
 
@@ -455,17 +686,37 @@ __global__ void __launch_bounds__(256) far_generic_kernel(FarArgs a) {
 bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st) {
   Tree& t = *op.tree;
   const int nl = op.n_local, p = t.p;
-  if (op.mode == BEM_MODE_H2ACA && op.far_kernel == 4 && !op.force_generic) {
+  if (op.mode == BEM_MODE_H2ACA && op.far_kernel == 6 && !op.force_generic && op.n_segs > 0) {
+    const Far6Cfg f6 = choose6(p, nl, op.far4_smem_cap);
+    if (f6.mt > 0) {
+      BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
+      Far6Args a;
+      a.nl = nl; a.m = t.m; a.p = p; a.p4 = f6.p4; a.rcap = op.rcap; a.SST = f6.SST; a.TT = f6.TT; a.XTP = f6.XTP;
+      a.nT = f6.nT; a.tb = f6.tb;
+      a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
+      a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
+      a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
+      BEM_CK(dispatch6(f6, op.n_segs, a, st));
+      seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
+                                                       yhat, (int64_t)nl * p);
+      BEM_CK(cudaGetLastError());
+      return BEM_OK;
+    }
+  }
+  if (op.mode == BEM_MODE_H2ACA && op.far_kernel == 4 && !op.force_generic && op.n_segs > 0) {
     const Far4Cfg f4 = choose4(p, nl, op.far4_smem_cap);
     if (f4.maxt > 0) {
       BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
       Far4Args a;
       a.nl = nl; a.m = t.m; a.p = p; a.p4 = f4.p4; a.rcap = op.rcap; a.SST = f4.SST; a.TT = f4.TT; a.TTP = f4.TTP;
       a.nT = f4.nT;
-      a.rows = op.d_far_rows.p; a.far_ptr = t.d_far_ptr.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
+      a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
       a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
-      a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.yhat = yhat;
-      BEM_CK(dispatch4(f4, op.n_far_rows, a, st));
+      a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
+      BEM_CK(dispatch4(f4, op.n_segs, a, st));
+      seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
+                                                       yhat, (int64_t)nl * p);
+      BEM_CK(cudaGetLastError());
       return BEM_OK;
     }
   }

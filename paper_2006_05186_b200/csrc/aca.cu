@@ -574,10 +574,10 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
     }
   }
   if (mode == BEM_MODE_DENSE) {
-    std::vector<int32_t> ptr(t.n_leaves + 1), cb(t.n_leaves, 0), ce(t.n_leaves, (int32_t)t.M);
-    for (int i = 0; i <= t.n_leaves; ++i) ptr[i] = i;
-    if (op.d_dn_ptr.upload(ptr) != cudaSuccess || op.d_dn_cb.upload(cb) != cudaSuccess ||
-        op.d_dn_ce.upload(ce) != cudaSuccess) {
+    std::vector<int32_t> jb(t.n_leaves, 0), je(t.n_leaves, (int32_t)t.M), jl(t.M);
+    for (int64_t i = 0; i < t.M; ++i) jl[i] = (int32_t)i;
+    if (op.d_dn_jb.upload(jb) != cudaSuccess || op.d_dn_je.upload(je) != cudaSuccess ||
+        op.d_dn_j.upload(jl) != cudaSuccess) {
       set_error("bem_assemble_h2_aca: upload failed");
       return fail(BEM_ECUDA);
     }

@@ -102,8 +102,8 @@ struct Tree {
   DBuf<double> d_E;      // C*p*p (E of cluster c w.r.t. its parent)
   DBuf<double> d_xi;     // C*3*m
   DBuf<int32_t> d_leaves;
-  // near CSR over leaves (by leaf index): column cluster ranges
-  DBuf<int32_t> d_near_ptr, d_near_cb, d_near_ce;
+  // near field per leaf index: [jb, je) into the flat list of near source panels
+  DBuf<int32_t> d_near_jb, d_near_je, d_near_j;
   // far CSR by row cluster
   std::vector<int32_t> far_ptr, far_sorted;  // far_sorted: block ids grouped by row cluster
   DBuf<int32_t> d_far_ptr, d_far_sorted, d_far_r, d_far_c;
@@ -121,7 +121,7 @@ struct Op {
   int n_class = 0;
   DBuf<int32_t> d_class_t1, d_class_t2;
   // BEM_MODE_DENSE: every leaf's near list is the whole index range [0, M)
-  DBuf<int32_t> d_dn_ptr, d_dn_cb, d_dn_ce;
+  DBuf<int32_t> d_dn_jb, d_dn_je, d_dn_j;
   // ACA skeleton
   int rcap = 0;
   std::vector<int32_t> ranks;  // host copy

@@ -365,18 +365,20 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
     sj[k] = g.J[i] / kFourPi;
     area[k] = g.area[i];
   }
-  // near CSR by leaf index
+  // near field: per leaf, the flat list of near source panels (cluster order),
+  // concatenated column-leaf ranges in partition order
   std::vector<int32_t> leaf_pos(C, -1);
   for (int li = 0; li < t.n_leaves; ++li) leaf_pos[t.leaves[li]] = li;
-  std::vector<int32_t> nptr(t.n_leaves + 1, 0);
-  for (size_t b = 0; b < t.near_r.size(); ++b) nptr[leaf_pos[t.near_r[b]] + 1]++;
-  for (int li = 0; li < t.n_leaves; ++li) nptr[li + 1] += nptr[li];
-  std::vector<int32_t> ncb(t.near_r.size()), nce(t.near_r.size()), fill(nptr.begin(), nptr.end() - 1);
+  std::vector<std::vector<int32_t>> per_leaf(t.n_leaves);
   for (size_t b = 0; b < t.near_r.size(); ++b) {
-    int li = leaf_pos[t.near_r[b]];
-    ncb[fill[li]] = t.begin[t.near_c[b]];
-    nce[fill[li]] = t.end[t.near_c[b]];
-    fill[li]++;
+    auto& v = per_leaf[leaf_pos[t.near_r[b]]];
+    for (int j = t.begin[t.near_c[b]]; j < t.end[t.near_c[b]]; ++j) v.push_back(j);
+  }
+  std::vector<int32_t> njb(t.n_leaves), nje(t.n_leaves), nj;
+  for (int li = 0; li < t.n_leaves; ++li) {
+    njb[li] = (int32_t)nj.size();
+    nj.insert(nj.end(), per_leaf[li].begin(), per_leaf[li].end());
+    nje[li] = (int32_t)nj.size();
   }
   // far CSR by row cluster
   t.far_ptr.assign(C + 1, 0);
@@ -405,7 +407,7 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
   UP(d_parent, t.parent); UP(d_leaf_of, leaf_of);
   UP(d_cen, cen); UP(d_qn, qn); UP(d_qw, qw); UP(d_selfJ, sj); UP(d_area, area);
   UP(d_U, U); UP(d_W, W); UP(d_E, E); UP(d_xi, t.xi); UP(d_leaves, t.leaves);
-  UP(d_near_ptr, nptr); UP(d_near_cb, ncb); UP(d_near_ce, nce);
+  UP(d_near_jb, njb); UP(d_near_je, nje); UP(d_near_j, nj);
   UP(d_far_ptr, t.far_ptr); UP(d_far_sorted, t.far_sorted); UP(d_far_r, t.far_r); UP(d_far_c, t.far_c);
   t.d_level_nonleaf.resize(t.depth + 1);
   for (int lv = 0; lv <= t.depth; ++lv) UP(d_level_nonleaf[lv], t.level_nonleaf[lv]);

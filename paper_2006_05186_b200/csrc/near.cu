@@ -26,9 +26,9 @@ struct NearArgs {
   int64_t M;
   int n_class;
   const int32_t* leaf_of;
-  const int32_t* near_ptr;
-  const int32_t* near_cb;
-  const int32_t* near_ce;
+  const int32_t* near_jb;
+  const int32_t* near_je;
+  const int32_t* near_j;
   const double* cen;
   const double* qn;
   const double* qw;
@@ -99,10 +99,10 @@ __global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
   for (int f = 0; f < F; ++f) { acc1[f] = make_double2(0.0, 0.0); acc2[f] = make_double2(0.0, 0.0); }
   const double cx = a.cen[3 * k], cy = a.cen[3 * k + 1], cz = a.cen[3 * k + 2];
   const int li = a.leaf_of[k];
-  const int rg0 = a.near_ptr[li], rg1 = a.near_ptr[li + 1];
-  for (int rg = rg0; rg < rg1; ++rg) {
-    const int jb = a.near_cb[rg], je = a.near_ce[rg];
-    for (int j = jb + lane; j < je; j += 32) {
+  const int jb = a.near_jb[li], je = a.near_je[li];
+  for (int jj = jb + lane; jj < je; jj += 32) {
+    {
+      const int j = a.near_j[jj];
       if (j == k) continue;  // self panel below
       double2 x1[F], x2[F];
 #pragma unroll
@@ -179,9 +179,9 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st) 
   NearArgs na;
   na.M = t.M; na.n_class = op.n_class; na.leaf_of = t.d_leaf_of.p;
   const bool dense = op.mode == BEM_MODE_DENSE;
-  na.near_ptr = dense ? op.d_dn_ptr.p : t.d_near_ptr.p;
-  na.near_cb = dense ? op.d_dn_cb.p : t.d_near_cb.p;
-  na.near_ce = dense ? op.d_dn_ce.p : t.d_near_ce.p;
+  na.near_jb = dense ? op.d_dn_jb.p : t.d_near_jb.p;
+  na.near_je = dense ? op.d_dn_je.p : t.d_near_je.p;
+  na.near_j = dense ? op.d_dn_j.p : t.d_near_j.p;
   na.cen = t.d_cen.p; na.qn = t.d_qn.p; na.qw = t.d_qw.p; na.selfJ = t.d_selfJ.p;
   na.s = (const double2*)op.d_s.p; na.local_l = op.d_local_l.p;
   na.class_t1 = op.d_class_t1.p; na.class_t2 = op.d_class_t2.p; na.xc = xc; na.yc = yc;

@@ -140,6 +140,8 @@ struct Op {
   DBuf<double> d_xc, d_yc, d_xhat, d_yhat;
   // kernel variants (tuning knobs; env BEM_NEAR_F, BEM_FAR_GENERIC read at assembly)
   int near_f = 2;
+  int near_unroll = 7;
+  bool near_tab = true;
   bool force_generic = false;
   int far_kernel = 6;                 // 6: transposed DMMA (far6), 4: DMMA (far4), 3: DFMA tiles (far3)
   size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM

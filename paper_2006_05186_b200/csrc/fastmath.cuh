@@ -10,56 +10,96 @@
 //         contribution is below 1e-300).
 // sincos: theta = q pi/2 + r (3-part Cody-Waite), minimax polynomials on
 //         |r| <= pi/4 (the classical fdlibm kernel coefficients), quadrant by
-//         selects.
+//         selects and integer sign flips.
+// The coefficients live in __constant__ memory so the DFMAs take them as
+// constant-bank operands (no per-iteration immediate materialisation).
 #pragma once
 
 namespace bem {
 namespace fast {
 
+static __constant__ double kExpC[13] = {
+    2.08767569878680989792e-09, 2.50521083854417187751e-08, 2.75573192239858906526e-07,
+    2.75573192239858906526e-06, 2.48015873015873015873e-05, 1.98412698412698412698e-04,
+    1.38888888888888888889e-03, 8.33333333333333333333e-03, 4.16666666666666666667e-02,
+    1.66666666666666666667e-01, 0.5, 1.0, 1.0};
+static __constant__ double kSinC[6] = {1.58969099521155010221e-10, -2.50507602534068634195e-08,
+                                2.75573137070700676789e-06, -1.98412698298579493134e-04,
+                                8.33333333332248946124e-03, -1.66666666666666324348e-01};
+static __constant__ double kCosC[6] = {-1.13596475577881948265e-11, 2.08757232129817482790e-09,
+                                -2.75573143513906633035e-07, 2.48015872894767294178e-05,
+                                -1.38888888888741095749e-03, 4.16666666666666019037e-02};
+static __constant__ double kRed[8] = {
+    1.4426950408889634074,  -6.93147180369123816490e-01, -1.90821492927058770002e-10,  // exp
+    6.36619772367581382433e-01, -1.57079632673412561417e+00, -6.07710050650619224932e-11,
+    -2.02226624879595063154e-21,  // sincos
+    6755399441055744.0};
+
+static __constant__ double kExp2Tab[64] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
+static __constant__ double kExpT[6] = {8.33333333333333333333e-03, 4.16666666666666666667e-02,
+                                         1.66666666666666666667e-01, 0.5, 1.0, 1.0};
+
 __device__ __forceinline__ double exp_neg(double x) {
   x = fmax(x, -708.0);
-  const double t = fma(x, 1.4426950408889634074, 6755399441055744.0);
-  const double kd = t - 6755399441055744.0;
-  double r = fma(kd, -6.93147180369123816490e-01, x);
-  r = fma(kd, -1.90821492927058770002e-10, r);
-  double p = 2.08767569878680989792e-09;     // 1/12!
-  p = fma(p, r, 2.50521083854417187751e-08);  // 1/11!
-  p = fma(p, r, 2.75573192239858906526e-07);  // 1/10!
-  p = fma(p, r, 2.75573192239858906526e-06);  // 1/9!
-  p = fma(p, r, 2.48015873015873015873e-05);  // 1/8!
-  p = fma(p, r, 1.98412698412698412698e-04);  // 1/7!
-  p = fma(p, r, 1.38888888888888888889e-03);  // 1/6!
-  p = fma(p, r, 8.33333333333333333333e-03);  // 1/5!
-  p = fma(p, r, 4.16666666666666666667e-02);  // 1/4!
-  p = fma(p, r, 1.66666666666666666667e-01);  // 1/3!
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
+  const double t = fma(x, kRed[0], kRed[7]);
+  const double kd = t - kRed[7];
+  double r = fma(kd, kRed[1], x);
+  r = fma(kd, kRed[2], r);
+  double p = kExpC[0];
+#pragma unroll
+  for (int i = 1; i < 13; ++i) p = fma(p, r, kExpC[i]);
   const int k = __double2loint(t);
   return __hiloint2double(__double2hiint(p) + (k << 20), __double2loint(p));
 }
 
+// Table-driven variant: x = (64 k + j) ln2/64 + r, |r| <= ln2/128,
+// e^x = 2^k * T[j] * poly5(r), T[j] = 2^(j/64) (host-rounded, in shared
+// memory); truncation error r^6/720 < 4e-17.  Caller provides the table.
+__device__ __forceinline__ double exp_neg_tab(double x, const double* __restrict__ T) {
+  x = fmax(x, -708.0);
+  const double t = fma(x, 92.332482616893656473, 6755399441055744.0);  // 64/ln2
+  const double kd = t - 6755399441055744.0;
+  double r = fma(kd, -0x1.62e42ff000000p-7, x);  // ln2/64, high 32 bits (kd * hi exact)
+  r = fma(kd, 6.563929801064195e-13, r);        // ln2/64 low part (hi - ln2/64)
+  double p = kExpT[0];
+#pragma unroll
+  for (int i = 1; i < 6; ++i) p = fma(p, r, kExpT[i]);
+  const int ki = __double2loint(t);
+  p *= T[ki & 63];
+  return __hiloint2double(__double2hiint(p) + ((ki >> 6) << 20), __double2loint(p));
+}
+
 __device__ __forceinline__ void sincos_(double th, double* sn, double* cs) {
-  const double t = fma(th, 6.36619772367581382433e-01, 6755399441055744.0);
-  const double qd = t - 6755399441055744.0;
+  const double t = fma(th, kRed[3], kRed[7]);
+  const double qd = t - kRed[7];
   const int q = __double2loint(t);
-  double r = fma(qd, -1.57079632673412561417e+00, th);
-  r = fma(qd, -6.07710050650619224932e-11, r);
-  r = fma(qd, -2.02226624879595063154e-21, r);
+  double r = fma(qd, kRed[4], th);
+  r = fma(qd, kRed[5], r);
+  r = fma(qd, kRed[6], r);
   const double z = r * r;
-  double ps = 1.58969099521155010221e-10;
-  ps = fma(ps, z, -2.50507602534068634195e-08);
-  ps = fma(ps, z, 2.75573137070700676789e-06);
-  ps = fma(ps, z, -1.98412698298579493134e-04);
-  ps = fma(ps, z, 8.33333333332248946124e-03);
-  ps = fma(ps, z, -1.66666666666666324348e-01);
+  double ps = kSinC[0];
+#pragma unroll
+  for (int i = 1; i < 6; ++i) ps = fma(ps, z, kSinC[i]);
   const double s = fma(r * z, ps, r);
-  double pc = -1.13596475577881948265e-11;
-  pc = fma(pc, z, 2.08757232129817482790e-09);
-  pc = fma(pc, z, -2.75573143513906633035e-07);
-  pc = fma(pc, z, 2.48015872894767294178e-05);
-  pc = fma(pc, z, -1.38888888888741095749e-03);
-  pc = fma(pc, z, 4.16666666666666019037e-02);
+  double pc = kCosC[0];
+#pragma unroll
+  for (int i = 1; i < 6; ++i) pc = fma(pc, z, kCosC[i]);
   const double c = fma(z * z, pc, fma(z, -0.5, 1.0));
   const bool swap = q & 1;
   const double so = swap ? c : s;

@@ -73,8 +73,13 @@ __device__ __noinline__ double2 self_entry(const double* qn, const double* qw, d
   return make_double2(vr, vi);
 }
 
-template <int F>
+template <int F, int U, bool TAB>
 __global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
+  __shared__ double etab[64];
+  if (TAB) {
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) etab[i] = fast::kExp2Tab[i];
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
   const int64_t k = (int64_t)blockIdx.x * kNearWarps + (threadIdx.x >> 5);
   if (k >= a.M) return;
@@ -115,7 +120,7 @@ __global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
       for (int f = 0; f < F; ++f) v[f] = make_double2(0.0, 0.0);
       const double* qn = a.qn + 21 * (int64_t)j;
       const double* qw = a.qw + 7 * (int64_t)j;
-#pragma unroll 1
+#pragma unroll U
       for (int q = 0; q < 7; ++q) {
         const double dx = cx - qn[3 * q], dy = cy - qn[3 * q + 1], dz = cz - qn[3 * q + 2];
         const double d2 = dx * dx + dy * dy + dz * dz;
@@ -124,7 +129,7 @@ __global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
         const double w = qw[q] * ir;
 #pragma unroll
         for (int f = 0; f < F; ++f) {
-          const double e = fast::exp_neg(-sre[f] * r) * w;
+          const double e = (TAB ? fast::exp_neg_tab(-sre[f] * r, etab) : fast::exp_neg(-sre[f] * r)) * w;
           double sn, cs;
           fast::sincos_(sim[f] * r, &sn, &cs);
           v[f].x = fma(e, cs, v[f].x);
@@ -165,10 +170,10 @@ __global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
   }
 }
 
-template <int F>
+template <int F, int U, bool TAB>
 cudaError_t launch(const NearArgs& na, cudaStream_t st) {
   dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + F - 1) / F));
-  near_kernel<F><<<g, kNearWarps * 32, 0, st>>>(na);
+  near_kernel<F, U, TAB><<<g, kNearWarps * 32, 0, st>>>(na);
   return cudaGetLastError();
 }
 
@@ -186,7 +191,14 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st) 
   na.s = (const double2*)op.d_s.p; na.local_l = op.d_local_l.p;
   na.class_t1 = op.d_class_t1.p; na.class_t2 = op.d_class_t2.p; na.xc = xc; na.yc = yc;
   const int F = op.near_f;
-  cudaError_t e = F == 8 ? launch<8>(na, st) : F == 2 ? launch<2>(na, st) : launch<4>(na, st);
+  const int U = op.near_unroll;
+  const bool T = op.near_tab;
+  cudaError_t e;
+  if (F == 3) e = T ? (U == 7 ? launch<3, 7, true>(na, st) : launch<3, 1, true>(na, st))
+                    : (U == 7 ? launch<3, 7, false>(na, st) : launch<3, 1, false>(na, st));
+  else if (F == 4) e = T ? launch<4, 1, true>(na, st) : launch<4, 1, false>(na, st);
+  else e = T ? (U == 7 ? launch<2, 7, true>(na, st) : launch<2, 1, true>(na, st))
+             : (U == 7 ? launch<2, 7, false>(na, st) : launch<2, 1, false>(na, st));
   BEM_CK(e);
   return BEM_OK;
 }

@@ -79,7 +79,7 @@ class ShardedTimeOperator:
         torch = self._torch
         g = self.rank
         xf = self.forward_fn(x_loc)  # [L][M_g]
-        send = [xf.index_select(0, torch.as_tensor(self.local[h], device=xf.device)) for h in range(self.G)]
+        send = [xf.index_select(0, torch.as_tensor(self.local[h], dtype=torch.long, device=xf.device)) for h in range(self.G)]
         Mg = [e - b for b, e in self.ranges]
         Lg = len(self.local[g])
         recv = self._a2a(send, [(Lg, Mg[h]) for h in range(self.G)], xf.device)
@@ -89,5 +89,5 @@ class ShardedTimeOperator:
         recv = self._a2a(send, [(len(self.local[h]), Mg[g]) for h in range(self.G)], xf.device)
         yf = torch.empty_like(xf)
         for h in range(self.G):
-            yf.index_copy_(0, torch.as_tensor(self.local[h], device=xf.device), recv[h])
+            yf.index_copy_(0, torch.as_tensor(self.local[h], dtype=torch.long, device=xf.device), recv[h])
         return self.inverse_fn(yf)

@@ -143,7 +143,7 @@ struct Op {
   int near_unroll = 7;
   bool near_tab = true;
   bool force_generic = false;
-  int far_kernel = 6;                 // 6: transposed DMMA (far6), 4: DMMA (far4), 3: DFMA tiles (far3)
+  int far_kernel = 7;                 // 7: far6 + cluster-shared slices (far7), 6: transposed DMMA (far6), 4: DMMA (far4), 3: DFMA tiles (far3)
   size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM
   // profiling
   bool profile = false;

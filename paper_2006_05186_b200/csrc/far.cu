@@ -21,6 +21,8 @@
 // evaluated per frequency, no ACA) and a fallback for shapes far3 cannot hold.
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "fastmath.cuh"
 
@@ -569,6 +571,270 @@ cudaError_t dispatch6(const Far6Cfg& c, int nseg, const Far6Args& a, cudaStream_
   }
 }
 
+// ------------------------------------------- far7: far6 + cluster-shared slices
+// Same DMMA product as far6 (out[t,mu] += sum_nu (Z_b[j,t] xhat_c[nu,t]) S_j[mu,nu]),
+// with three changes measured on B200 (profiles/r01_*):
+//  * the CTAs that own the frequency tiles of one (segment, mu chunk) form a
+//    thread-block cluster (cluster dims (1, ntiles, 1), ntiles <= 8); each CTA
+//    regenerates only 1/ntiles of the slice S_b(s_{k_j}) into a double-
+//    buffered "own" region and copies the peers' parts through distributed
+//    shared memory, so a slice is evaluated once per apply instead of once
+//    per frequency tile (8x at config 4);
+//  * up to two leftover columns (n_l mod 8, e.g. the real frequency l = 0
+//    when L = 2^k + 1) are accumulated by all 256 threads of the lead CTA
+//    (row = tid/8, every 8th nu; one 8-lane shuffle reduction at the end)
+//    instead of 4 lanes per warp; more leftovers are zero-padded DMMA columns;
+//  * slice entries use rsqrt (no IEEE division / sqrt) and the table exp.
+struct Far7Args {
+  int nl, m, p, p4, rcap, SST, TT, XTP, nT, tb, nd, cs, own;  // DMMA columns [tb, tb+nd) (padded past nl);
+                                                            // own = slice entries regenerated per cluster CTA
+  const int4* segs;
+  const int32_t* far_sorted;
+  const int32_t* far_c;
+  const double* xi;
+  const double2* s;
+  const int32_t* rank;
+  const int32_t* pivk;
+  const int64_t* zoff;
+  const double2* Z;
+  const double2* xhat;
+  double2* part;
+};
+
+__device__ __forceinline__ double2 kern_rs(double d2, double2 s, const double* etab) {
+  const double ir = rsqrt(d2);
+  const double r = d2 * ir;
+  const double e = fast::exp_neg_tab(-s.x * r, etab) * (ir * 0.079577471545947667884);  // 1/(4 pi)
+  double sn, cs;
+  fast::sincos_(s.y * r, &sn, &cs);
+  return make_double2(e * cs, -e * sn);
+}
+
+template <int MT, bool CL>
+__global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
+  extern __shared__ double2 sm[];
+  const int p = a.p, m = a.m, SST = a.SST, XTP = a.XTP, p4 = a.p4, tb = a.tb;
+  const int4 sg = a.segs[blockIdx.x];
+  const int r = sg.x;
+  const int tc0 = a.tb + blockIdx.y * a.TT;
+  const int ncol = min(a.TT, a.tb + a.nd - tc0);
+  const bool lead = blockIdx.y == 0;
+  const int mu0 = blockIdx.z * 32;
+  const int nrow = min(32, p - mu0);
+  const int nS = nrow * p;
+  double2* S = sm;                                    // 32 x SST
+  double2* own = S + 32 * SST;                        // CL: 2 x a.own
+  double2* xs = own + (CL ? 2 * a.own : 0);           // p4 x XTP
+  double* etab = (double*)(xs + (size_t)p4 * XTP);    // 64
+  double* xr = etab + 64;                             // 96
+  double* xcn = xr + 96;                              // 3p
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  for (int i = tid; i < 32 * SST + p4 * XTP + (CL ? 2 * a.own : 0); i += blockDim.x) sm[i] = make_double2(0.0, 0.0);
+  for (int i = tid; i < 64; i += blockDim.x) etab[i] = fast::kExp2Tab[i];
+  for (int i = tid; i < nrow; i += blockDim.x) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
+  int crank = 0;
+  if (CL) crank = (int)cooperative_groups::this_cluster().block_rank();
+  const int e0 = crank * a.own, e1 = min(nS, e0 + a.own);  // this CTA's share of the slice entries
+  const int ntile = ncol / 8;
+  double acc[MT][4][2][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+  // leftover columns: thread -> (row lrow, nu residue lpart)
+  const int lrow = tid >> 3, lpart = tid & 7;
+  const bool lown = lead && tb > 0 && lrow < nrow;
+  double2 lacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  const int ncp = tb + ncol;
+  int buf = 0;
+  for (int bi = sg.y; bi < sg.z; ++bi) {
+    const int b = a.far_sorted[bi];
+    const int c = a.far_c[b];
+    __syncthreads();
+    for (int i = tid; i < p; i += blockDim.x) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
+    const double2* xh = a.xhat + (int64_t)c * a.nl * p;
+    for (int idx = tid; idx < ncp * p; idx += blockDim.x) {
+      const int tl = idx / p, nu = idx - tl * p;
+      const int tg = tl < tb ? tl : tc0 + (tl - tb);
+      if (tl >= tb || lead) xs[nu * XTP + tl] = tg < a.nl ? xh[(int64_t)tg * p + nu] : make_double2(0.0, 0.0);
+    }
+    const int rk = a.rank[b];
+    const double2* Zb = a.Z + a.zoff[b];
+    __syncthreads();
+    for (int l = 0; l < rk; ++l) {
+      const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + l]];
+      const double2* Zl = Zb + (int64_t)l * a.nl;
+      double2 zt[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int tt = warp + 8 * i;
+        const int t = tc0 + tt * 8 + g;
+        zt[i] = (tt < ntile && t < a.nl) ? Zl[t] : make_double2(0.0, 0.0);
+      }
+      if (CL) {
+        double2* ob = own + buf * a.own;
+        for (int e = e0 + tid; e < e1; e += blockDim.x) {
+          const int i = e / p, nu = e - i * p;
+          const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
+                       dz = xcn[3 * nu + 2] - xr[3 * i + 2];
+          ob[e - e0] = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab);
+        }
+        cooperative_groups::this_cluster().sync();  // all parts ready; every local warp is past its GEMM
+        for (int e = tid; e < nS; e += blockDim.x) {
+          const int owner = e / a.own;
+          const double2* src = owner == crank ? ob
+                                              : cooperative_groups::this_cluster().map_shared_rank(ob, owner);
+          const int i = e / p, nu = e - i * p;
+          S[i * SST + nu] = src[e - owner * a.own];
+        }
+        buf ^= 1;
+        __syncthreads();
+      } else {
+        __syncthreads();
+        for (int e = tid; e < nS; e += blockDim.x) {
+          const int i = e / p, nu = e - i * p;
+          const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
+                       dz = xcn[3 * nu + 2] - xr[3 * i + 2];
+          S[i * SST + nu] = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab);
+        }
+        __syncthreads();
+      }
+      for (int k0 = 0; k0 < p4; k0 += 4) {
+        double2 bf[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = S[(j * 8 + g) * SST + k0 + q];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const int tt = warp + 8 * i;
+          if (tt < ntile) {
+            const double2 xv = xs[(k0 + q) * XTP + tb + tt * 8 + g];
+            const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
+            const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
+            const double nai = -ai;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+              dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
+              dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
+              dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
+            }
+          }
+        }
+      }
+      if (lown) {
+#pragma unroll
+        for (int tl = 0; tl < 2; ++tl) {
+          if (tl >= tb) break;
+          double2 sacc = make_double2(0.0, 0.0);
+          for (int nu = lpart; nu < p; nu += 8) {
+            const double2 sv2 = S[lrow * SST + nu], xv = xs[nu * XTP + tl];
+            sacc.x = fma(sv2.x, xv.x, sacc.x);
+            sacc.x = fma(-sv2.y, xv.y, sacc.x);
+            sacc.y = fma(sv2.x, xv.y, sacc.y);
+            sacc.y = fma(sv2.y, xv.x, sacc.y);
+          }
+          const double2 z = Zl[tl];
+          lacc[tl].x = fma(z.x, sacc.x, fma(-z.y, sacc.y, lacc[tl].x));
+          lacc[tl].y = fma(z.x, sacc.y, fma(z.y, sacc.x, lacc[tl].y));
+        }
+      }
+    }
+  }
+  double2* out = a.part + (int64_t)sg.w * a.nl * p;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int tt = warp + 8 * i;
+    if (tt >= ntile) continue;
+    const int t = tc0 + tt * 8 + g;
+    if (t >= a.nl) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int row = j * 8 + 2 * q + v;
+        if (row < nrow) out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
+      }
+  }
+  if (lead && tb > 0) {  // uniform per warp: reduce the 8 nu residues of each row
+#pragma unroll
+    for (int tl = 0; tl < 2; ++tl) {
+      if (tl >= tb) break;
+      double2 v = lacc[tl];
+#pragma unroll
+      for (int off = 1; off < 8; off <<= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
+      }
+      if (lpart == 0 && lrow < nrow) out[(int64_t)tl * p + mu0 + lrow] = v;
+    }
+  }
+  if (CL) cooperative_groups::this_cluster().sync();  // peers may still read our own[] region
+}
+
+struct Far7Cfg {
+  int p4 = 0, SST = 0, TT = 0, XTP = 0, nT = 0, tb = 0, nd = 0, ntiles = 0, nchunks = 0, mt = 0, cs = 1, own = 0;
+  size_t smem = 0;
+};
+
+Far7Cfg choose7(int p, int nl, size_t cap) {
+  int tb = nl % 8;
+  if (tb > 2 || tb == nl) tb = 0;  // pad instead (zero columns past nl)
+  const int nD = (nl - tb + 7) / 8 * 8;
+  const int p4 = (p + 3) / 4 * 4;
+  int SST = p4;
+  while (SST % 8 != 4) ++SST;
+  const int nrow = std::min(p, 32);
+  for (int TTmax : {256, 128, 64, 32, 16, 8}) {
+    Far7Cfg c;
+    const int ntiles = (nD + TTmax - 1) / TTmax;
+    const int TT = ((nD / 8 + ntiles - 1) / ntiles) * 8;
+    int XTP = tb + TT;
+    while (XTP % 8 != 2) ++XTP;
+    const int cs = (ntiles > 1 && ntiles <= 8) ? ntiles : 1;
+    const int own = cs > 1 ? (nrow * p + cs - 1) / cs : 0;
+    const size_t smem = sizeof(double2) * (32 * (size_t)SST + (size_t)p4 * XTP + 2 * (size_t)own) +
+                        sizeof(double) * (64 + 96 + 3 * p);
+    if (smem > cap) continue;
+    c.p4 = p4; c.SST = SST; c.TT = TT; c.XTP = XTP; c.nT = TT / 8; c.tb = tb; c.nd = nD; c.ntiles = ntiles;
+    c.nchunks = (p + 31) / 32; c.mt = (c.nT + 7) / 8; c.smem = smem; c.cs = cs; c.own = own;
+    if (c.mt > 2) continue;  // MT >= 3 spills at 128 registers
+    return c;
+  }
+  return Far7Cfg{};
+}
+
+template <int MT, bool CL>
+cudaError_t launch7(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream_t st) {
+  auto k = far7_kernel<MT, CL>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = c.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = CL ? (unsigned)c.cs : 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, k, a);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t dispatch7(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream_t st) {
+  const bool cl = c.cs > 1;
+  switch (c.mt) {
+    case 1: return cl ? launch7<1, true>(c, nseg, a, st) : launch7<1, false>(c, nseg, a, st);
+    case 2: return cl ? launch7<2, true>(c, nseg, a, st) : launch7<2, false>(c, nseg, a, st);
+    default: return cudaErrorInvalidConfiguration;
+  }
+}
+
 // yhat[r] = sum over the row's segments (fixed order)
 __global__ void seg_reduce_kernel(const int32_t* __restrict__ rows, const int32_t* __restrict__ seg_ptr,
                                   const double2* __restrict__ part, double2* __restrict__ yhat, int64_t tile) {
@@ -686,6 +952,23 @@ __global__ void __launch_bounds__(256) far_generic_kernel(FarArgs a) {
 bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st) {
   Tree& t = *op.tree;
   const int nl = op.n_local, p = t.p;
+  if (op.mode == BEM_MODE_H2ACA && op.far_kernel == 7 && !op.force_generic && op.n_segs > 0) {
+    const Far7Cfg f7 = choose7(p, nl, op.far4_smem_cap);
+    if (f7.mt > 0) {
+      BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
+      Far7Args a;
+      a.nl = nl; a.m = t.m; a.p = p; a.p4 = f7.p4; a.rcap = op.rcap; a.SST = f7.SST; a.TT = f7.TT; a.XTP = f7.XTP;
+      a.nT = f7.nT; a.tb = f7.tb; a.nd = f7.nd; a.cs = f7.cs; a.own = f7.own;
+      a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
+      a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
+      a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
+      BEM_CK(dispatch7(f7, op.n_segs, a, st));
+      seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
+                                                       yhat, (int64_t)nl * p);
+      BEM_CK(cudaGetLastError());
+      return BEM_OK;
+    }
+  }
   if (op.mode == BEM_MODE_H2ACA && op.far_kernel == 6 && !op.force_generic && op.n_segs > 0) {
     const Far6Cfg f6 = choose6(p, nl, op.far4_smem_cap);
     if (f6.mt > 0) {

@@ -259,3 +259,47 @@ def test_edge_cases(pb, torch):
     oh = O.H2(V, T, 16, 1.0, 2)
     oh.aca(s, 1e-6)
     assert _rel(_apply(pb, torch, op, x), oh.apply(O.MODE_H2ACA, s, x)) <= 1e-10
+
+
+@pytest.mark.parametrize("N,kernel", [(256, "7"), (260, "7"), (256, "6")])
+def test_h2aca_p64_multi_tile(pb, torch, N, kernel, monkeypatch):
+    """p = 64 (m = 4) with L > 128: K3 runs several frequency tiles per
+    (segment, mu chunk); far7 shares the regenerated pivot slices across the
+    tiles' thread-block cluster through distributed shared memory.  N = 260
+    (L mod 8 = 5) exercises the zero-padded DMMA columns, N = 256 the
+    distributed leftover column.  Oracle on a frequency sample."""
+    monkeypatch.setenv("BEM_FAR_KERNEL", kernel)
+    V, T = synth.icosphere(3)
+    M, L, eps = len(T), N + 1, 1e-6
+    s = pb.cqm_frequencies(N, 2.0)
+    x = synth.random_density(3, L, M)
+    oh = O.H2(V, T, 48, 1.0, 4)
+    oh.aca(s, eps)
+    tree = pb.Tree(V, T, 48, 1.0, 4)
+    op = pb.Operator(tree, s, eps, mode=pb.BEM_MODE_H2ACA)
+    y = _apply(pb, torch, op, x)
+    lsel = np.unique(np.r_[0, 1, 2, 7, 8, 63, 64, 65, 127, 128, 129, L // 2, L - 3, L - 2, L - 1])
+    yo = oh.apply(O.MODE_H2ACA, s, x[lsel], lsel)
+    assert _rel(y[lsel], yo) <= 1e-10
+    for i in range(len(lsel)):
+        assert _rel(y[lsel[i]], yo[i]) <= 1e-8, lsel[i]
+
+
+@pytest.mark.parametrize("nloc", [10, 19])
+def test_local_subset_padded_columns(pb, torch, nloc):
+    """A frequency shard whose size leaves 3..7 columns past a multiple of 8
+    (zero-padded DMMA columns; 10 -> two leftover columns) matches the oracle."""
+    V, T = synth.icosphere(3)
+    N = 256
+    M, L, eps = len(T), N + 1, 1e-6
+    s = pb.cqm_frequencies(N, 2.0)
+    rng = np.random.default_rng(nloc)
+    local = np.sort(rng.choice(L, nloc, replace=False)).astype(np.int32)
+    x = synth.random_density(3, nloc, M)
+    oh = O.H2(V, T, 48, 1.0, 4)
+    oh.aca(s, eps)
+    tree = pb.Tree(V, T, 48, 1.0, 4)
+    op = pb.Operator(tree, s, eps, mode=pb.BEM_MODE_H2ACA, local_l=local)
+    y = _apply(pb, torch, op, x)
+    yo = oh.apply(O.MODE_H2ACA, s, x, local)
+    assert _rel(y, yo) <= 1e-10

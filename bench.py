@@ -104,24 +104,62 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(V, T, cfg, s, N, nsel=None):
-    """The oracle as it stands (H2ACA apply) on a bounded frequency sample."""
+def traffic_bytes(cfg_id, dom):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return t.get(f"config{cfg_id}", {}).get(dom)
+    except (OSError, ValueError):
+        return None
+
+
+def oracle_step(O, h, s, x_time, N, R, lsel):
+    """One time-domain step of the oracle on a frequency sample: full forward
+    transform, H2ACA apply of the sampled frequencies, full inverse transform.
+    Returns (seconds for the two transforms, seconds for the sampled apply)."""
+    t0 = time.perf_counter()
+    xf = O.forward(x_time, N, R)
+    t1 = time.perf_counter()
+    yf = np.zeros_like(xf)
+    yf[lsel] = h.apply(O.MODE_H2ACA, s, xf[lsel], lsel)
+    t2 = time.perf_counter()
+    O.inverse(yf, N, R)
+    t3 = time.perf_counter()
+    return (t1 - t0) + (t3 - t2), t2 - t1
+
+
+def oracle_throughput(O, h, s, cfg_id, N, R, M, nsel, steps, warmup, rng_sel):
+    """Whole-step unknowns*frequencies/s extrapolated from the sample:
+    M L / (t_transforms + t_apply_sample * L / nsel) (the apply is exactly linear in L)."""
+    L = N + 1
+    tt, ta = [], []
+    for k in range(warmup + steps):
+        lsel = np.sort(rng_sel.choice(L, nsel, replace=False)).astype(np.int32)
+        x = synth.random_time_data(cfg_id, N, M, stream=k).astype(np.complex128)
+        a, b = oracle_step(O, h, s, x, N, R, lsel)
+        if k >= warmup:
+            tt.append(a)
+            ta.append(b)
+    t_step = float(np.mean(tt)) + float(np.mean(ta)) * L / nsel
+    return M * L / t_step, t_step, float(np.mean(ta))
+
+
+def cpu_baseline(V, T, cfg, s, N, R):
+    """The oracle as it stands, timed on this box's host cores on a bounded sample."""
     import oracle as O
     nthr = O.num_threads()
-    L = N + 1
-    nsel = nsel or max(1, min(L, nthr))
+    L, M = N + 1, len(T)
+    nsel = max(1, min(L, nthr))
     h = O.H2(V, T, cfg["leaf"], cfg["eta"], cfg["m"])
     t0 = time.perf_counter()
     h.aca(s, cfg["eps"])
     t_aca = time.perf_counter() - t0
-    lsel = np.linspace(0, L - 1, nsel).round().astype(np.int32)
-    x = synth.random_density(cfg_id_global, nsel, len(T))
-    t0 = time.perf_counter()
-    h.apply(O.MODE_H2ACA, s, x, lsel)
-    dt = time.perf_counter() - t0
-    return {"value": len(T) * nsel / dt, "unit": UNIT, "cores": nthr, "kind": "oracle",
-            "sample": f"H2ACA apply of {nsel} of {L} frequencies (evenly spaced), all {len(T)} panels; "
-                      f"{dt:.2f} s; oracle ACA setup {t_aca:.1f} s excluded"}
+    val, t_step, t_app = oracle_throughput(O, h, s, cfg_id_global, N, R, M, nsel, 1, 0, np.random.default_rng(0))
+    return {"value": val, "unit": UNIT, "cores": nthr, "kind": "oracle",
+            "sample": f"one time-domain step: full naive-DFT forward/inverse transforms + H2ACA apply of {nsel} "
+                      f"random frequencies of {L} ({t_app:.2f} s), all {M} panels; step time extrapolated as "
+                      f"transforms + apply x L/{nsel} = {t_step:.1f} s; oracle ACA setup {t_aca:.1f} s excluded"}
 
 
 cfg_id_global = 2
@@ -140,24 +178,16 @@ def run_reference(args):
     h = O.H2(V, T, cfg["leaf"], cfg["eta"], cfg["m"])
     h.aca(s, cfg["eps"])
     nsel = max(1, min(L, nthr))
-    rng_sel = np.random.default_rng(0)
-    times = []
-    for k in range(args.warmup + args.steps):
-        lsel = np.sort(rng_sel.choice(L, nsel, replace=False)).astype(np.int32)
-        x = synth.random_density(args.config, nsel, M, stream=k)
-        t0 = time.perf_counter()
-        h.apply(O.MODE_H2ACA, s, x, lsel)
-        if k >= args.warmup:
-            times.append(time.perf_counter() - t0)
-    dt = sum(times) / len(times)
-    val = M * nsel / dt
+    val, t_step, t_app = oracle_throughput(O, h, s, args.config, N, R, M, nsel, args.steps, args.warmup,
+                                           np.random.default_rng(0))
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_json(args.config, cfg, M, L, 1),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": nthr, "kind": "oracle",
-                             "sample": f"each step: oracle H2ACA apply of {nsel} random frequencies of {L}, "
-                                       f"all {M} panels (setup excluded)"},
+                             "sample": f"each step: full naive-DFT forward/inverse transforms + oracle H2ACA apply "
+                                       f"of {nsel} random frequencies of {L} (mean {t_app:.2f} s), all {M} panels; "
+                                       f"step time extrapolated as transforms + apply x L/{nsel} (setup excluded)"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -266,13 +296,12 @@ def main():
         e2e = {"value": M * L / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 16),
                "d2h_bytes_per_step": int(yh.numel() * 16), "ms_per_step": ms_e2e}
 
-    # roofline of the dominant kernel (algorithmic flops / measured launch time)
+    # roofline of the dominant kernel (algorithmic flops / live CUDA-event launch time)
     stats = tree.stats
     nl = len(local)
     n_class = len({min(l, L - l) for l in local})
     kt = {k: v / args.steps for k, v in acc.items()}
     launches = op.launch_count() + 2
-    roof = None
     if mode == pb.BEM_MODE_H2ACA:
         rk = op.aca_export()["ranks"]
         flops_far = 8.0 * float(rk.sum()) * stats["p"] ** 2 * nl
@@ -280,30 +309,41 @@ def main():
         flops_far = 8.0 * stats["far_blocks"] * stats["p"] ** 2 * nl
     evals_near = 7.0 * stats["nnz_near"] * n_class
     flops_near = 75.0 * evals_near  # SURVEY §8(d) model: ~75 FP64 flops per complex exponential + MACs
+    peaks = {}
+    for m_, name in ((0, "dfma"), (1, "dmma")):
+        try:
+            peaks[name] = max(pb.fp64_peak(local_rank, mode=m_) for _ in range(2)) / 1e12
+        except Exception:
+            peaks[name] = None
     dom = "coupling" if kt["coupling"] >= kt["near"] else "near"
-    fl = flops_far if dom == "coupling" else flops_near
+    if dom == "coupling":
+        fl = flops_far
+        peak = peaks["dmma"] or FP64_PEAK_DERIVED / 1e12
+        bound, src = "tensor", ("measured in this run: mma.sync.m8n8k4.f64 (DMMA) loop on this GPU "
+                                "(bem_debug_fp64_peak_ex mode 1); derived 148 SMs x 64 FMA/clk x 2 x 1.965 GHz = 37.2")
+    else:
+        fl = flops_near
+        peak = FP64_PEAK_DERIVED / 1e12
+        bound, src = "alu", "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §7)"
     achieved = fl / (kt[dom] * 1e-3) / 1e12
-    peak = FP64_PEAK_DERIVED / 1e12
-    roof = {"bound": "alu", "kernel": {"coupling": "K3 far_kernel", "near": "K1 near_kernel"}[dom],
-            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-            "peak_source": "derived: 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (B200 FP64 pipe; DESIGN.md)",
-            "algorithmic_flops_per_launch": fl}
-    try:
-        meas_peak = pb.fp64_peak(local_rank) / 1e12
-    except Exception:
-        meas_peak = None
+    kname = {"coupling": "K3 far7_kernel (+seg_reduce)", "near": "K1 near_kernel"}[dom]
+    roof = {"bound": bound, "kernel": kname, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic_bytes(args.config, dom), "peak_source": src,
+            "algorithmic_flops_per_launch": fl,
+            "traffic_source": "profiles/traffic.json (ncu --set full dram__bytes_read.sum + dram__bytes_write.sum "
+                              "per launch of the same kernel and config)"}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": config_json(args.config, cfg, M, L, world), "roofline": roof, "e2e": e2e,
            "gpu_launches": launches * args.steps, "clocks": clocks,
-           "kernel_ms": kt, "fp64_dfma_measured_tflops": meas_peak,
+           "kernel_ms": kt, "fp64_measured_tflops": peaks,
            "near_evals_per_s": evals_near / (kt["near"] * 1e-3) if kt["near"] > 0 else None,
            "setup_s": {"tree": t_tree, "aca": t_aca}, "mode": args.mode,
            "mean_aca_rank": float(op.aca_export()["ranks"].mean()) if mode == pb.BEM_MODE_H2ACA else None}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            out["cpu_baseline"] = cpu_baseline(V, T, cfg, s, N)
+            out["cpu_baseline"] = cpu_baseline(V, T, cfg, s, N, R)
         except Exception as ex:  # pragma: no cover
             out["cpu_baseline"] = {"value": None, "error": str(ex)}
     if rank == 0:

@@ -139,12 +139,15 @@ struct Op {
   // workspaces
   DBuf<double> d_xc, d_yc, d_xhat, d_yhat;
   // kernel variants (tuning knobs; env BEM_NEAR_F, BEM_FAR_GENERIC read at assembly)
-  int near_f = 2;
+  int near_f = 3;  // frequency classes per warp (r01 sweep at config 2: F=2 7.77 ms, F=3 6.97 ms, F=4 9.85 ms)
   int near_unroll = 7;
   bool near_tab = true;
+  int near_minb = 0;  // K1 __launch_bounds__ min blocks/SM variant (0: compiler's choice; 6, 8)
   bool force_generic = false;
   int far_kernel = 7;                 // 7: far6 + cluster-shared slices (far7), 6: transposed DMMA (far6), 4: DMMA (far4), 3: DFMA tiles (far3)
   size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM
+  bool far7_rem_dfma = true;          // p = 27: rows 24..26 on DFMA instead of a padded DMMA tile
+  bool far7_cluster = false;          // DSMEM-shared slices across frequency tiles (measured slower, r01)
   // profiling
   bool profile = false;
   cudaEvent_t ev[6] = {};

@@ -601,16 +601,18 @@ struct Far7Args {
   double2* part;
 };
 
-__device__ __forceinline__ double2 kern_rs(double d2, double2 s, const double* etab) {
+__device__ __forceinline__ double2 kern_rs(double d2, double2 s, const double* etab, const double2* sctab) {
   const double ir = rsqrt(d2);
   const double r = d2 * ir;
   const double e = fast::exp_neg_tab(-s.x * r, etab) * (ir * 0.079577471545947667884);  // 1/(4 pi)
   double sn, cs;
-  fast::sincos_(s.y * r, &sn, &cs);
+  fast::sincos_tab(s.y * r, sctab, &sn, &cs);
   return make_double2(e * cs, -e * sn);
 }
 
-template <int MT, bool CL>
+// NJ DMMA mu tiles per 32-row chunk; REM further rows (p = 27: rows 24..26) on
+// DFMA from the same A fragments instead of a 5/8-empty fourth DMMA tile.
+template <int MT, bool CL, int NJ, int REM>
 __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
   extern __shared__ double2 sm[];
   const int p = a.p, m = a.m, SST = a.SST, XTP = a.XTP, p4 = a.p4, tb = a.tb;
@@ -625,23 +627,31 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
   double2* S = sm;                                    // 32 x SST
   double2* own = S + 32 * SST;                        // CL: 2 x a.own
   double2* xs = own + (CL ? 2 * a.own : 0);           // p4 x XTP
-  double* etab = (double*)(xs + (size_t)p4 * XTP);    // 64
+  double2* sctab = xs + (size_t)p4 * XTP;             // 64 (cos, sin)(k pi/32)
+  double* etab = (double*)(sctab + 64);               // 64
   double* xr = etab + 64;                             // 96
   double* xcn = xr + 96;                              // 3p
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
   for (int i = tid; i < 32 * SST + p4 * XTP + (CL ? 2 * a.own : 0); i += blockDim.x) sm[i] = make_double2(0.0, 0.0);
-  for (int i = tid; i < 64; i += blockDim.x) etab[i] = fast::kExp2Tab[i];
+  for (int i = tid; i < 64; i += blockDim.x) {
+    etab[i] = fast::kExp2Tab[i];
+    sctab[i] = fast::kSinCosTab[i];
+  }
   for (int i = tid; i < nrow; i += blockDim.x) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
   int crank = 0;
   if (CL) crank = (int)cooperative_groups::this_cluster().block_rank();
   const int e0 = crank * a.own, e1 = min(nS, e0 + a.own);  // this CTA's share of the slice entries
   const int ntile = ncol / 8;
-  double acc[MT][4][2][2];
+  double acc[MT][NJ][2][2];
+  double2 racc[MT][REM > 0 ? REM : 1];
 #pragma unroll
-  for (int i = 0; i < MT; ++i)
+  for (int i = 0; i < MT; ++i) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+#pragma unroll
+    for (int j = 0; j < (REM > 0 ? REM : 1); ++j) racc[i][j] = make_double2(0.0, 0.0);
+  }
   // leftover columns: thread -> (row lrow, nu residue lpart)
   const int lrow = tid >> 3, lpart = tid & 7;
   const bool lown = lead && tb > 0 && lrow < nrow;
@@ -678,7 +688,7 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
           const int i = e / p, nu = e - i * p;
           const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
                        dz = xcn[3 * nu + 2] - xr[3 * i + 2];
-          ob[e - e0] = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab);
+          ob[e - e0] = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab, sctab);
         }
         cooperative_groups::this_cluster().sync();  // all parts ready; every local warp is past its GEMM
         for (int e = tid; e < nS; e += blockDim.x) {
@@ -696,14 +706,16 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
           const int i = e / p, nu = e - i * p;
           const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
                        dz = xcn[3 * nu + 2] - xr[3 * i + 2];
-          S[i * SST + nu] = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab);
+          S[i * SST + nu] = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab, sctab);
         }
         __syncthreads();
       }
       for (int k0 = 0; k0 < p4; k0 += 4) {
-        double2 bf[4];
+        double2 bf[NJ], rf[REM > 0 ? REM : 1];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = S[(j * 8 + g) * SST + k0 + q];
+        for (int j = 0; j < NJ; ++j) bf[j] = S[(j * 8 + g) * SST + k0 + q];
+#pragma unroll
+        for (int j = 0; j < REM; ++j) rf[j] = S[(NJ * 8 + j) * SST + k0 + q];
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
           const int tt = warp + 8 * i;
@@ -713,11 +725,16 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
             const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
             const double nai = -ai;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < NJ; ++j) {
               dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
               dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
               dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
               dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
+            }
+#pragma unroll
+            for (int j = 0; j < REM; ++j) {  // partial over this lane's k = k0 + q; reduced over q at the end
+              racc[i][j].x = fma(ar, rf[j].x, fma(nai, rf[j].y, racc[i][j].x));
+              racc[i][j].y = fma(ar, rf[j].y, fma(ai, rf[j].x, racc[i][j].y));
             }
           }
         }
@@ -749,12 +766,29 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
     const int t = tc0 + tt * 8 + g;
     if (t >= a.nl) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int row = j * 8 + 2 * q + v;
         if (row < nrow) out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
       }
+  }
+  if (REM > 0) {
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int tt = warp + 8 * i;  // warp-uniform
+      if (tt >= ntile) continue;
+      const int t = tc0 + tt * 8 + g;
+#pragma unroll
+      for (int j = 0; j < (REM > 0 ? REM : 1); ++j) {
+        double2 v = racc[i][j];
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, 1);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, 1);
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, 2);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, 2);
+        if (q == 0 && t < a.nl && NJ * 8 + j < nrow) out[(int64_t)t * p + mu0 + NJ * 8 + j] = v;
+      }
+    }
   }
   if (lead && tb > 0) {  // uniform per warp: reduce the 8 nu residues of each row
 #pragma unroll
@@ -777,7 +811,7 @@ struct Far7Cfg {
   size_t smem = 0;
 };
 
-Far7Cfg choose7(int p, int nl, size_t cap) {
+Far7Cfg choose7(int p, int nl, size_t cap, bool cluster) {
   int tb = nl % 8;
   if (tb > 2 || tb == nl) tb = 0;  // pad instead (zero columns past nl)
   const int nD = (nl - tb + 7) / 8 * 8;
@@ -791,9 +825,9 @@ Far7Cfg choose7(int p, int nl, size_t cap) {
     const int TT = ((nD / 8 + ntiles - 1) / ntiles) * 8;
     int XTP = tb + TT;
     while (XTP % 8 != 2) ++XTP;
-    const int cs = (ntiles > 1 && ntiles <= 8) ? ntiles : 1;
+    const int cs = (cluster && ntiles > 1 && ntiles <= 8) ? ntiles : 1;
     const int own = cs > 1 ? (nrow * p + cs - 1) / cs : 0;
-    const size_t smem = sizeof(double2) * (32 * (size_t)SST + (size_t)p4 * XTP + 2 * (size_t)own) +
+    const size_t smem = sizeof(double2) * (32 * (size_t)SST + (size_t)p4 * XTP + 2 * (size_t)own + 64) +
                         sizeof(double) * (64 + 96 + 3 * p);
     if (smem > cap) continue;
     c.p4 = p4; c.SST = SST; c.TT = TT; c.XTP = XTP; c.nT = TT / 8; c.tb = tb; c.nd = nD; c.ntiles = ntiles;
@@ -804,11 +838,15 @@ Far7Cfg choose7(int p, int nl, size_t cap) {
   return Far7Cfg{};
 }
 
-template <int MT, bool CL>
+template <int MT, bool CL, int NJ, int REM>
 cudaError_t launch7(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream_t st) {
-  auto k = far7_kernel<MT, CL>;
+  auto k = far7_kernel<MT, CL, NJ, REM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   if (e != cudaSuccess) return e;
+  if (!CL) {
+    k<<<dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks), 256, c.smem, st>>>(a);
+    return cudaGetLastError();
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks);
   cfg.blockDim = dim3(256, 1, 1);
@@ -826,13 +864,21 @@ cudaError_t launch7(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream_t 
   return cudaGetLastError();
 }
 
-cudaError_t dispatch7(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream_t st) {
+template <int NJ, int REM>
+cudaError_t dispatch7_(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream_t st) {
   const bool cl = c.cs > 1;
   switch (c.mt) {
-    case 1: return cl ? launch7<1, true>(c, nseg, a, st) : launch7<1, false>(c, nseg, a, st);
-    case 2: return cl ? launch7<2, true>(c, nseg, a, st) : launch7<2, false>(c, nseg, a, st);
+    case 1: return cl ? launch7<1, true, NJ, REM>(c, nseg, a, st) : launch7<1, false, NJ, REM>(c, nseg, a, st);
+    case 2: return cl ? launch7<2, true, NJ, REM>(c, nseg, a, st) : launch7<2, false, NJ, REM>(c, nseg, a, st);
     default: return cudaErrorInvalidConfiguration;
   }
+}
+
+// mu tiling: p = 27 -> 3 DMMA tiles + 3 DFMA rows; p <= 8 -> 1 tile; otherwise 4 tiles per 32-row chunk
+cudaError_t dispatch7(const Far7Cfg& c, int p, bool rem_dfma, int nseg, const Far7Args& a, cudaStream_t st) {
+  if (p <= 8) return dispatch7_<1, 0>(c, nseg, a, st);
+  if (p == 27 && rem_dfma) return dispatch7_<3, 3>(c, nseg, a, st);
+  return dispatch7_<4, 0>(c, nseg, a, st);
 }
 
 // yhat[r] = sum over the row's segments (fixed order)
@@ -953,7 +999,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
   Tree& t = *op.tree;
   const int nl = op.n_local, p = t.p;
   if (op.mode == BEM_MODE_H2ACA && op.far_kernel == 7 && !op.force_generic && op.n_segs > 0) {
-    const Far7Cfg f7 = choose7(p, nl, op.far4_smem_cap);
+    const Far7Cfg f7 = choose7(p, nl, op.far4_smem_cap, op.far7_cluster);
     if (f7.mt > 0) {
       BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
       Far7Args a;
@@ -962,7 +1008,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
       a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
       a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
       a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
-      BEM_CK(dispatch7(f7, op.n_segs, a, st));
+      BEM_CK(dispatch7(f7, p, op.far7_rem_dfma, op.n_segs, a, st));
       seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
                                                        yhat, (int64_t)nl * p);
       BEM_CK(cudaGetLastError());

@@ -68,21 +68,26 @@ __device__ __forceinline__ double exp_neg(double x) {
   return __hiloint2double(__double2hiint(p) + (k << 20), __double2loint(p));
 }
 
-// Table-driven variant: x = (64 k + j) ln2/64 + r, |r| <= ln2/128,
+// Table-driven variant: x = (64 k + j) ln2/64 + r, |r| <= ln2/128 (|x| < 1e13),
 // e^x = 2^k * T[j] * poly5(r), T[j] = 2^(j/64) (host-rounded, in shared
 // memory); truncation error r^6/720 < 4e-17.  Caller provides the table.
+static __constant__ double kET[4] = {92.332482616893656473, 6755399441055744.0,  // 64/ln2, magic
+                                      -0x1.62e42ff000000p-7,                   // -ln2/64, high 32 bits (kd * hi exact)
+                                      6.563929801064195e-13};                  // ln2/64 low part (hi - ln2/64)
+
 __device__ __forceinline__ double exp_neg_tab(double x, const double* __restrict__ T) {
-  x = fmax(x, -708.0);
-  const double t = fma(x, 92.332482616893656473, 6755399441055744.0);  // 64/ln2
-  const double kd = t - 6755399441055744.0;
-  double r = fma(kd, -0x1.62e42ff000000p-7, x);  // ln2/64, high 32 bits (kd * hi exact)
-  r = fma(kd, 6.563929801064195e-13, r);        // ln2/64 low part (hi - ln2/64)
+  const double t = fma(x, kET[0], kET[1]);
+  const double kd = t - kET[1];
+  double r = fma(kd, kET[2], x);
+  r = fma(kd, kET[3], r);
   double p = kExpT[0];
 #pragma unroll
   for (int i = 1; i < 6; ++i) p = fma(p, r, kExpT[i]);
   const int ki = __double2loint(t);
   p *= T[ki & 63];
-  return __hiloint2double(__double2hiint(p) + ((ki >> 6) << 20), __double2loint(p));
+  // exponent clamp in the integer pipe: x < -707 returns ~1e-307 instead of 0
+  // (negligible) without an FP64 fmax
+  return __hiloint2double(__double2hiint(p) + (max(ki >> 6, -1020) << 20), __double2loint(p));
 }
 
 __device__ __forceinline__ void sincos_(double th, double* sn, double* cs) {
@@ -108,6 +113,68 @@ __device__ __forceinline__ void sincos_(double th, double* sn, double* cs) {
   const int sflip = (q & 2) << 30, cflip = ((q + 1) & 2) << 30;
   *sn = __hiloint2double(__double2hiint(so) ^ sflip, __double2loint(so));
   *cs = __hiloint2double(__double2hiint(co) ^ cflip, __double2loint(co));
+}
+
+
+// Table-driven sincos: th = k pi/32 + r (2-part Cody-Waite with the fdlibm
+// pio2_1 / pio2_1t split scaled by 1/16; kd * hi is exact for |k| < 2^20,
+// i.e. |th| < 1e5), |r| <= pi/64; Taylor sin to r^7 and cos to r^8
+// (truncation < 1e-16 relative); (cos, sin)(k pi/32) from a 64-entry table
+// (correctly rounded, caller stages it in shared memory) -- the table also
+// carries the quadrant, so there is no select/sign logic.
+static __constant__ double2 kSinCosTab[64] = {
+    {0x1.0000000000000p+0, 0x0.0p+0}, {0x1.fd88da3d12526p-1, 0x1.917a6bc29b42cp-4},
+    {0x1.f6297cff75cb0p-1, 0x1.8f8b83c69a60bp-3}, {0x1.e9f4156c62ddap-1, 0x1.294062ed59f06p-2},
+    {0x1.d906bcf328d46p-1, 0x1.87de2a6aea963p-2}, {0x1.c38b2f180bdb1p-1, 0x1.e2b5d3806f63bp-2},
+    {0x1.a9b66290ea1a3p-1, 0x1.1c73b39ae68c8p-1}, {0x1.8bc806b151741p-1, 0x1.44cf325091dd6p-1},
+    {0x1.6a09e667f3bcdp-1, 0x1.6a09e667f3bcdp-1}, {0x1.44cf325091dd6p-1, 0x1.8bc806b151741p-1},
+    {0x1.1c73b39ae68c8p-1, 0x1.a9b66290ea1a3p-1}, {0x1.e2b5d3806f63bp-2, 0x1.c38b2f180bdb1p-1},
+    {0x1.87de2a6aea963p-2, 0x1.d906bcf328d46p-1}, {0x1.294062ed59f06p-2, 0x1.e9f4156c62ddap-1},
+    {0x1.8f8b83c69a60bp-3, 0x1.f6297cff75cb0p-1}, {0x1.917a6bc29b42cp-4, 0x1.fd88da3d12526p-1},
+    {0x0.0p+0, 0x1.0000000000000p+0}, {-0x1.917a6bc29b42cp-4, 0x1.fd88da3d12526p-1},
+    {-0x1.8f8b83c69a60bp-3, 0x1.f6297cff75cb0p-1}, {-0x1.294062ed59f06p-2, 0x1.e9f4156c62ddap-1},
+    {-0x1.87de2a6aea963p-2, 0x1.d906bcf328d46p-1}, {-0x1.e2b5d3806f63bp-2, 0x1.c38b2f180bdb1p-1},
+    {-0x1.1c73b39ae68c8p-1, 0x1.a9b66290ea1a3p-1}, {-0x1.44cf325091dd6p-1, 0x1.8bc806b151741p-1},
+    {-0x1.6a09e667f3bcdp-1, 0x1.6a09e667f3bcdp-1}, {-0x1.8bc806b151741p-1, 0x1.44cf325091dd6p-1},
+    {-0x1.a9b66290ea1a3p-1, 0x1.1c73b39ae68c8p-1}, {-0x1.c38b2f180bdb1p-1, 0x1.e2b5d3806f63bp-2},
+    {-0x1.d906bcf328d46p-1, 0x1.87de2a6aea963p-2}, {-0x1.e9f4156c62ddap-1, 0x1.294062ed59f06p-2},
+    {-0x1.f6297cff75cb0p-1, 0x1.8f8b83c69a60bp-3}, {-0x1.fd88da3d12526p-1, 0x1.917a6bc29b42cp-4},
+    {-0x1.0000000000000p+0, 0x0.0p+0}, {-0x1.fd88da3d12526p-1, -0x1.917a6bc29b42cp-4},
+    {-0x1.f6297cff75cb0p-1, -0x1.8f8b83c69a60bp-3}, {-0x1.e9f4156c62ddap-1, -0x1.294062ed59f06p-2},
+    {-0x1.d906bcf328d46p-1, -0x1.87de2a6aea963p-2}, {-0x1.c38b2f180bdb1p-1, -0x1.e2b5d3806f63bp-2},
+    {-0x1.a9b66290ea1a3p-1, -0x1.1c73b39ae68c8p-1}, {-0x1.8bc806b151741p-1, -0x1.44cf325091dd6p-1},
+    {-0x1.6a09e667f3bcdp-1, -0x1.6a09e667f3bcdp-1}, {-0x1.44cf325091dd6p-1, -0x1.8bc806b151741p-1},
+    {-0x1.1c73b39ae68c8p-1, -0x1.a9b66290ea1a3p-1}, {-0x1.e2b5d3806f63bp-2, -0x1.c38b2f180bdb1p-1},
+    {-0x1.87de2a6aea963p-2, -0x1.d906bcf328d46p-1}, {-0x1.294062ed59f06p-2, -0x1.e9f4156c62ddap-1},
+    {-0x1.8f8b83c69a60bp-3, -0x1.f6297cff75cb0p-1}, {-0x1.917a6bc29b42cp-4, -0x1.fd88da3d12526p-1},
+    {0x0.0p+0, -0x1.0000000000000p+0}, {0x1.917a6bc29b42cp-4, -0x1.fd88da3d12526p-1},
+    {0x1.8f8b83c69a60bp-3, -0x1.f6297cff75cb0p-1}, {0x1.294062ed59f06p-2, -0x1.e9f4156c62ddap-1},
+    {0x1.87de2a6aea963p-2, -0x1.d906bcf328d46p-1}, {0x1.e2b5d3806f63bp-2, -0x1.c38b2f180bdb1p-1},
+    {0x1.1c73b39ae68c8p-1, -0x1.a9b66290ea1a3p-1}, {0x1.44cf325091dd6p-1, -0x1.8bc806b151741p-1},
+    {0x1.6a09e667f3bcdp-1, -0x1.6a09e667f3bcdp-1}, {0x1.8bc806b151741p-1, -0x1.44cf325091dd6p-1},
+    {0x1.a9b66290ea1a3p-1, -0x1.1c73b39ae68c8p-1}, {0x1.c38b2f180bdb1p-1, -0x1.e2b5d3806f63bp-2},
+    {0x1.d906bcf328d46p-1, -0x1.87de2a6aea963p-2}, {0x1.e9f4156c62ddap-1, -0x1.294062ed59f06p-2},
+    {0x1.f6297cff75cb0p-1, -0x1.8f8b83c69a60bp-3}, {0x1.fd88da3d12526p-1, -0x1.917a6bc29b42cp-4}};
+
+// constant-bank operands (DFMA takes c[][] directly; immediates would be
+// rematerialised through uniform registers every iteration)
+static __constant__ double kSCT[12] = {
+    10.185916357881301489, 6755399441055744.0, -0x1.921fb54400000p-4, -0x1.0b4611a626331p-38,  // 32/pi, magic, -pi/32 hi, lo
+    -1.98412698412698412698e-04, 8.33333333333333333333e-03, -1.66666666666666666667e-01,      // sin r^7, r^5, r^3
+    2.48015873015873015873e-05, -1.38888888888888888889e-03, 4.16666666666666666667e-02, -0.5, 1.0};  // cos
+
+__device__ __forceinline__ void sincos_tab(double th, const double2* __restrict__ T, double* sn, double* cs) {
+  const double t = fma(th, kSCT[0], kSCT[1]);
+  const double kd = t - kSCT[1];
+  double r = fma(kd, kSCT[2], th);
+  r = fma(kd, kSCT[3], r);
+  const double z = r * r;
+  const double ps = fma(z, fma(z, kSCT[4], kSCT[5]), kSCT[6]);
+  const double sr = fma(r * z, ps, r);
+  const double cr = fma(z, fma(z, fma(z, fma(z, kSCT[7], kSCT[8]), kSCT[9]), kSCT[10]), kSCT[11]);
+  const double2 cs_k = T[__double2loint(t) & 63];
+  *sn = fma(cs_k.y, cr, cs_k.x * sr);
+  *cs = fma(cs_k.x, cr, -(cs_k.y * sr));
 }
 
 }  // namespace fast

@@ -74,10 +74,14 @@ __device__ __noinline__ double2 self_entry(const double* qn, const double* qw, d
 }
 
 template <int F, int U, bool TAB>
-__global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
+__device__ __forceinline__ void near_body(const NearArgs& a) {
   __shared__ double etab[64];
+  __shared__ double2 sctab[64];
   if (TAB) {
-    for (int i = threadIdx.x; i < 64; i += blockDim.x) etab[i] = fast::kExp2Tab[i];
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+      etab[i] = fast::kExp2Tab[i];
+      sctab[i] = fast::kSinCosTab[i];
+    }
     __syncthreads();
   }
   const int lane = threadIdx.x & 31;
@@ -131,7 +135,8 @@ __global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
         for (int f = 0; f < F; ++f) {
           const double e = (TAB ? fast::exp_neg_tab(-sre[f] * r, etab) : fast::exp_neg(-sre[f] * r)) * w;
           double sn, cs;
-          fast::sincos_(sim[f] * r, &sn, &cs);
+          if (TAB) fast::sincos_tab(sim[f] * r, sctab, &sn, &cs);
+          else fast::sincos_(sim[f] * r, &sn, &cs);
           v[f].x = fma(e, cs, v[f].x);
           v[f].y = fma(-e, sn, v[f].y);
         }
@@ -171,9 +176,20 @@ __global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
 }
 
 template <int F, int U, bool TAB>
+__global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
+  near_body<F, U, TAB>(a);
+}
+// occupancy variants (register cap 65536 / (MINB * 128)); selected by BEM_NEAR_MINB
+template <int F, int U, bool TAB, int MINB>
+__global__ void __launch_bounds__(kNearWarps * 32, MINB) near_kernel_minb(NearArgs a) {
+  near_body<F, U, TAB>(a);
+}
+
+template <int F, int U, bool TAB, int MINB = 0>
 cudaError_t launch(const NearArgs& na, cudaStream_t st) {
   dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + F - 1) / F));
-  near_kernel<F, U, TAB><<<g, kNearWarps * 32, 0, st>>>(na);
+  if (MINB == 0) near_kernel<F, U, TAB><<<g, kNearWarps * 32, 0, st>>>(na);
+  else near_kernel_minb<F, U, TAB, (MINB > 0 ? MINB : 1)><<<g, kNearWarps * 32, 0, st>>>(na);
   return cudaGetLastError();
 }
 
@@ -194,7 +210,12 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st) 
   const int U = op.near_unroll;
   const bool T = op.near_tab;
   cudaError_t e;
-  if (F == 3) e = T ? (U == 7 ? launch<3, 7, true>(na, st) : launch<3, 1, true>(na, st))
+  if (F == 3 && U == 7 && T && op.near_minb == 4) e = launch<3, 7, true, 4>(na, st);
+  else if (F == 3 && U == 7 && T && op.near_minb == 2) e = launch<3, 7, true, 2>(na, st);
+  else if (F == 2 && U == 7 && T && op.near_minb == 4) e = launch<2, 7, true, 4>(na, st);
+  else if (F == 2 && U == 7 && T && op.near_minb == 6) e = launch<2, 7, true, 6>(na, st);
+  else if (F == 2 && U == 7 && T && op.near_minb == 8) e = launch<2, 7, true, 8>(na, st);
+  else if (F == 3) e = T ? (U == 7 ? launch<3, 7, true>(na, st) : launch<3, 1, true>(na, st))
                     : (U == 7 ? launch<3, 7, false>(na, st) : launch<3, 1, false>(na, st));
   else if (F == 4) e = T ? launch<4, 1, true>(na, st) : launch<4, 1, false>(na, st);
   else e = T ? (U == 7 ? launch<2, 7, true>(na, st) : launch<2, 1, true>(na, st))

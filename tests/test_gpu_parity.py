@@ -261,14 +261,17 @@ def test_edge_cases(pb, torch):
     assert _rel(_apply(pb, torch, op, x), oh.apply(O.MODE_H2ACA, s, x)) <= 1e-10
 
 
-@pytest.mark.parametrize("N,kernel", [(256, "7"), (260, "7"), (256, "6")])
-def test_h2aca_p64_multi_tile(pb, torch, N, kernel, monkeypatch):
+@pytest.mark.parametrize("N,kernel,cluster", [(256, "7", "0"), (260, "7", "0"), (256, "7", "1"), (260, "7", "1"),
+                                               (256, "6", "0")])
+def test_h2aca_p64_multi_tile(pb, torch, N, kernel, cluster, monkeypatch):
     """p = 64 (m = 4) with L > 128: K3 runs several frequency tiles per
-    (segment, mu chunk); far7 shares the regenerated pivot slices across the
-    tiles' thread-block cluster through distributed shared memory.  N = 260
+    (segment, mu chunk); far7 with BEM_FAR7_CLUSTER=1 shares the regenerated
+    pivot slices across the tiles' thread-block cluster through distributed
+    shared memory.  N = 260
     (L mod 8 = 5) exercises the zero-padded DMMA columns, N = 256 the
     distributed leftover column.  Oracle on a frequency sample."""
     monkeypatch.setenv("BEM_FAR_KERNEL", kernel)
+    monkeypatch.setenv("BEM_FAR7_CLUSTER", cluster)
     V, T = synth.icosphere(3)
     M, L, eps = len(T), N + 1, 1e-6
     s = pb.cqm_frequencies(N, 2.0)

@@ -212,7 +212,10 @@ class H2:
     def __del__(self):
         h = getattr(self, "h", None)
         if h:
-            lib().orc_h2_destroy(h)
+            try:
+                lib().orc_h2_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already gone
+                pass
             self.h = None
 
     def export(self):

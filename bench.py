@@ -44,6 +44,10 @@ def parse():
     ap.add_argument("--mode", default="h2aca", choices=["h2aca", "h2only"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="virtual shard: on 1 GPU, time the frequency-domain apply of rank --shard-rank's frequency "
+                         "classes of a G-GPU run (what one rank of `--gpus G` computes, without the all-to-alls)")
+    ap.add_argument("--shard-rank", type=int, default=0)
     ap.add_argument("--quiet", action="store_true")
     return ap.parse_args()
 
@@ -218,12 +222,21 @@ def main():
     t0 = time.perf_counter()
     tree = pb.Tree(V, T, cfg["leaf"], cfg["eta"], cfg["m"], device=local_rank)
     t_tree = time.perf_counter() - t0
-    local = shard_frequencies(L, world)[rank] if world > 1 else np.arange(L, dtype=np.int32)
+    vshard = args.shard_of > 1 and world == 1
+    if world > 1:
+        local = shard_frequencies(L, world)[rank]
+    elif vshard:
+        local = shard_frequencies(L, args.shard_of)[args.shard_rank]
+    else:
+        local = np.arange(L, dtype=np.int32)
     t0 = time.perf_counter()
-    op = pb.Operator(tree, s, cfg["eps"], mode=mode, local_l=local if world > 1 else None)
+    op = pb.Operator(tree, s, cfg["eps"], mode=mode, local_l=local if (world > 1 or vshard) else None)
     t_aca = time.perf_counter() - t0
     b, e = dof_ranges(M, world)[rank]
-    xt_host = synth.random_time_data(args.config, N, M)[:, b:e].astype(np.complex128)
+    if vshard:  # frequency-domain input of this shard
+        xt_host = synth.random_density(args.config, len(local), M)
+    else:
+        xt_host = synth.random_time_data(args.config, N, M)[:, b:e].astype(np.complex128)
     x = torch.from_numpy(xt_host).to(dev)
 
     def fwd(z):
@@ -235,6 +248,8 @@ def main():
     if world > 1:
         top = ShardedTimeOperator(rank, world, M, L, op.apply, fwd, inv)
         step = top.step
+    elif vshard:
+        step = op.apply
     else:
         def step(z):
             return inv(op.apply(fwd(z)))
@@ -270,7 +285,8 @@ def main():
     if world > 1:
         dist.all_reduce(t_tot, op=dist.ReduceOp.MAX)
     ms_per_step = float(t_tot.item()) / args.steps
-    value = M * L / (ms_per_step * 1e-3)
+    n_units = M * (len(local) if vshard else L)
+    value = n_units / (ms_per_step * 1e-3)
 
     # e2e: same step through the public API from pinned host buffers
     e2e = None
@@ -293,7 +309,7 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         ms_e2e = float(te.item()) / args.steps
-        e2e = {"value": M * L / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 16),
+        e2e = {"value": n_units / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 16),
                "d2h_bytes_per_step": int(yh.numel() * 16), "ms_per_step": ms_e2e}
 
     # roofline of the dominant kernel (algorithmic flops / live CUDA-event launch time)
@@ -341,7 +357,12 @@ def main():
            "near_evals_per_s": evals_near / (kt["near"] * 1e-3) if kt["near"] > 0 else None,
            "setup_s": {"tree": t_tree, "aca": t_aca}, "mode": args.mode,
            "mean_aca_rank": float(op.aca_export()["ranks"].mean()) if mode == pb.BEM_MODE_H2ACA else None}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if vshard:
+        out["config"]["parallelism"] = (f"virtual shard {args.shard_rank} of {args.shard_of}: frequency-domain apply of "
+                                         f"{len(local)} of {L} frequencies on 1 GPU (no transforms, no all-to-all); "
+                                         f"value = this rank's unknowns*frequencies/s")
+        out["metric"] = METRIC.replace("time-domain step: forward + apply + inverse", "frequency-domain apply, one shard")
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not vshard and args.config <= 3:
         try:
             out["cpu_baseline"] = cpu_baseline(V, T, cfg, s, N, R)
         except Exception as ex:  # pragma: no cover

@@ -145,6 +145,20 @@ bem_status cqm_inverse(const bem_c128* y_freq, bem_c128* y_time, int64_t M_loc, 
 bem_status cqm_solve(bem_op op, const double* g_time, double* phi_time, int64_t M_loc, double R, double tol,
                      int32_t restart, int32_t max_iter, void* nccl_comm, void* cuda_stream, bem_solve_stats* stats);
 
+/* Frequency-domain batched GMRES over the op's local frequencies (the
+ * per-frequency systems of the decoupled solve, Remark P:1607-1614; reading
+ * D10): for every t < n_local solve V(s_{local_l[t]}) phi_t = g_t by
+ * restarted GMRES(restart) from 0 with classical Gram-Schmidt + one
+ * re-orthogonalisation and Givens rotations, stopping at
+ * ||g_t - V phi_t|| <= tol ||g_t||.  This is the building block of the
+ * multi-GPU solve: the caller transforms, transposes (all-to-all) and calls it
+ * on each rank's frequency shard (paper_2006_05186_b200/dist.py).
+ * g_freq, phi_freq: device [n_local][M] complex, input panel order, distinct.
+ * Synchronous.  Returns BEM_ENOCONV if some frequency reached max_iter
+ * (phi_freq still written; stats says how many). */
+bem_status bem_solve_multifreq(bem_op op, const bem_c128* g_freq, bem_c128* phi_freq, double tol, int32_t restart,
+                               int32_t max_iter, void* cuda_stream, bem_solve_stats* stats);
+
 /* ---- diagnostics (tests / bench only; not part of the method) ---- */
 /* Pinned exp / sincos / kernel evaluated ON THE DEVICE for n host inputs
  * (checks bit-identity with the independent oracle implementation). */

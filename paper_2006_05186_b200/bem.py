@@ -38,7 +38,7 @@ class SolveStats(C.Structure):
 EXPORTS = [
     "bem_last_error", "cqm_frequencies", "bem_build_tree", "bem_tree_get_stats", "bem_tree_export",
     "bem_tree_destroy", "bem_assemble_h2_aca", "bem_aca_export", "bem_op_destroy", "bem_apply_multifreq",
-    "cqm_forward", "cqm_inverse", "cqm_solve", "bem_debug_pinned", "bem_debug_fp64_peak",
+    "cqm_forward", "cqm_inverse", "cqm_solve", "bem_solve_multifreq", "bem_debug_pinned", "bem_debug_fp64_peak",
     "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count", "bem_debug_fp64_peak_ex",
 ]
 
@@ -66,6 +66,7 @@ def lib():
         "cqm_forward": [vp, vp, i64, i32, d, vp],
         "cqm_inverse": [vp, vp, i64, i32, d, vp],
         "cqm_solve": [vp, vp, vp, i64, d, d, i32, i32, vp, vp, vp],
+        "bem_solve_multifreq": [vp, vp, vp, d, i32, i32, vp, vp],
         "bem_debug_pinned": [vp, i64, vp, vp, vp, i32],
         "bem_debug_fp64_peak": [i32, vp, vp],
         "bem_op_set_profiling": [vp, i32],
@@ -243,6 +244,20 @@ def cqm_solve(op: Operator, g_time, R: float, tol: float = 1e-8, restart: int = 
     st = SolveStats()
     code = lib().cqm_solve(op.h, _p(g_time), _p(phi), g_time.shape[1], float(R), float(tol), int(restart),
                            int(max_iter), None, _stream(stream), C.byref(st))
+    if code != 0 and not (code == BEM_ENOCONV and not raise_on_noconv):
+        _check(code)
+    return phi, {k: getattr(st, k) for k, _ in SolveStats._fields_ if k != "pad_"}
+
+
+def solve_multifreq(op: Operator, g_freq, tol: float = 1e-8, restart: int = 50, max_iter: int = 2000, stream=None,
+                    raise_on_noconv: bool = True):
+    """phi^_t = V(s_{local_l[t]})^{-1} g^_t for the op's local frequencies (batched GMRES, frequency domain)."""
+    import torch
+    assert g_freq.dtype == torch.complex128 and g_freq.is_cuda and g_freq.is_contiguous()
+    phi = torch.empty_like(g_freq)
+    st = SolveStats()
+    code = lib().bem_solve_multifreq(op.h, _p(g_freq), _p(phi), float(tol), int(restart), int(max_iter),
+                                     _stream(stream), C.byref(st))
     if code != 0 and not (code == BEM_ENOCONV and not raise_on_noconv):
         _check(code)
     return phi, {k: getattr(st, k) for k, _ in SolveStats._fields_ if k != "pad_"}

@@ -144,10 +144,11 @@ struct Op {
   bool near_tab = true;
   int near_minb = 0;  // K1 __launch_bounds__ min blocks/SM variant (0: compiler's choice; 6, 8)
   bool force_generic = false;
-  int far_kernel = 7;                 // 7: far6 + cluster-shared slices (far7), 6: transposed DMMA (far6), 4: DMMA (far4), 3: DFMA tiles (far3)
+  int far_kernel = 0;                 // 0: auto (far8 for p > 32, far7 otherwise); 8, 7, 6 (DMMA variants), 4, 3
   size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM
   bool far7_rem_dfma = true;          // p = 27: rows 24..26 on DFMA instead of a padded DMMA tile
-  bool far7_cluster = false;          // DSMEM-shared slices across frequency tiles (measured slower, r01)
+  bool far7_cluster = false;
+  int far8_kc = 0;                    // far8 nu-chunk width (0: automatic)          // DSMEM-shared slices across frequency tiles (measured slower, r01)
   // profiling
   bool profile = false;
   cudaEvent_t ev[6] = {};

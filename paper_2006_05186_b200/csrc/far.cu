@@ -20,6 +20,7 @@
 // far_generic_kernel: BEM_MODE_H2ONLY (the plain-H^2 comparison path: S_b(s_l)
 // evaluated per frequency, no ACA) and a fallback for shapes far3 cannot hold.
 #include <algorithm>
+#include <vector>
 
 #include <cooperative_groups.h>
 
@@ -881,6 +882,259 @@ cudaError_t dispatch7(const Far7Cfg& c, int p, bool rem_dfma, int nseg, const Fa
   return dispatch7_<4, 0>(c, nseg, a, st);
 }
 
+// ------------------------------------------------ far8: far7 with K (nu) chunks
+// The contraction index nu is processed in chunks of KC (a multiple of 4): per
+// block, for each nu chunk the x^ tile [KC][TT] is staged once, and for each
+// ACA term j the slice columns S_j[mu-chunk][nu-chunk] are regenerated and
+// contracted.  Regeneration per (b, j) is unchanged (every slice entry is
+// evaluated once per CTA), but shared memory no longer grows with p, so the
+// frequency tile stays at TT = 128 with two CTAs per SM for p = 64 and 125
+// (far7 had to drop to TT <= 64, i.e. >= 2x more slice regeneration per
+// frequency, at p = 64 and could not hold p = 125 at all).
+struct Far8Args {
+  int nl, m, p, rcap, SST, TT, XTP, tb, nd, KC;
+  const int4* segs;
+  const int32_t* far_sorted;
+  const int32_t* far_c;
+  const double* xi;
+  const double2* s;
+  const int32_t* rank;
+  const int32_t* pivk;
+  const int64_t* zoff;
+  const double2* Z;
+  const double2* xhat;
+  double2* part;
+};
+
+template <int MT, int NJ, int REM>
+__global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
+  extern __shared__ double2 sm[];
+  const int p = a.p, m = a.m, SST = a.SST, XTP = a.XTP, tb = a.tb, KC = a.KC;
+  const int4 sg = a.segs[blockIdx.x];
+  const int r = sg.x;
+  const int tc0 = a.tb + blockIdx.y * a.TT;
+  const int ncol = min(a.TT, a.tb + a.nd - tc0);
+  const bool lead = blockIdx.y == 0;
+  const int mu0 = blockIdx.z * 32;
+  const int nrow = min(32, p - mu0);
+  double2* S = sm;                                    // 32 x SST (SST >= KC)
+  double2* xs = S + 32 * SST;                         // KC x XTP
+  double2* sctab = xs + (size_t)KC * XTP;             // 64 (cos, sin)(k pi/32)
+  double* etab = (double*)(sctab + 64);               // 64
+  double* xr = etab + 64;                             // 96
+  double* xcn = xr + 96;                              // 3p
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  for (int i = tid; i < 32 * SST + KC * XTP; i += blockDim.x) sm[i] = make_double2(0.0, 0.0);
+  for (int i = tid; i < 64; i += blockDim.x) {
+    etab[i] = fast::kExp2Tab[i];
+    sctab[i] = fast::kSinCosTab[i];
+  }
+  for (int i = tid; i < nrow; i += blockDim.x) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
+  const int ntile = ncol / 8;
+  double acc[MT][NJ][2][2];
+  double2 racc[MT][REM > 0 ? REM : 1];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+#pragma unroll
+    for (int j = 0; j < (REM > 0 ? REM : 1); ++j) racc[i][j] = make_double2(0.0, 0.0);
+  }
+  const int lrow = tid >> 3, lpart = tid & 7;
+  const bool lown = lead && tb > 0 && lrow < nrow;
+  double2 lacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  const int ncp = tb + ncol;
+  for (int bi = sg.y; bi < sg.z; ++bi) {
+    const int b = a.far_sorted[bi];
+    const int c = a.far_c[b];
+    const double2* xh = a.xhat + (int64_t)c * a.nl * p;
+    const int rk = a.rank[b];
+    const double2* Zb = a.Z + a.zoff[b];
+    __syncthreads();
+    for (int i = tid; i < p; i += blockDim.x) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
+    for (int k0c = 0; k0c < p; k0c += KC) {
+      const int kw = min(KC, p - k0c);          // real nu in this chunk
+      const int kw4 = (kw + 3) & ~3;            // k-steps cover kw4 (padding rows/cols are zero)
+      if (k0c > 0) __syncthreads();             // previous chunk's GEMM done with xs / S
+      for (int idx = tid; idx < ncp * KC; idx += blockDim.x) {
+        const int tl = idx / KC, nu = idx - tl * KC;
+        const int tg = tl < tb ? tl : tc0 + (tl - tb);
+        if (tl >= tb || lead)
+          xs[nu * XTP + tl] = (nu < kw && tg < a.nl) ? xh[(int64_t)tg * p + k0c + nu] : make_double2(0.0, 0.0);
+      }
+      for (int l = 0; l < rk; ++l) {
+        const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + l]];
+        const double2* Zl = Zb + (int64_t)l * a.nl;
+        double2 zt[MT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const int tt = warp + 8 * i;
+          const int t = tc0 + tt * 8 + g;
+          zt[i] = (tt < ntile && t < a.nl) ? Zl[t] : make_double2(0.0, 0.0);
+        }
+        __syncthreads();  // xs staged (first term) / previous term's GEMM done with S
+        for (int e = tid; e < nrow * KC; e += blockDim.x) {
+          const int i = e / KC, nu = e - i * KC;
+          double2 v = make_double2(0.0, 0.0);
+          if (nu < kw) {
+            const int nn = k0c + nu;
+            const double dx = xcn[3 * nn] - xr[3 * i], dy = xcn[3 * nn + 1] - xr[3 * i + 1],
+                         dz = xcn[3 * nn + 2] - xr[3 * i + 2];
+            v = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab, sctab);
+          }
+          S[i * SST + nu] = v;
+        }
+        __syncthreads();
+        for (int k0 = 0; k0 < kw4; k0 += 4) {
+          double2 bf[NJ], rf[REM > 0 ? REM : 1];
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) bf[j] = S[(j * 8 + g) * SST + k0 + q];
+#pragma unroll
+          for (int j = 0; j < REM; ++j) rf[j] = S[(NJ * 8 + j) * SST + k0 + q];
+#pragma unroll
+          for (int i = 0; i < MT; ++i) {
+            const int tt = warp + 8 * i;
+            if (tt < ntile) {
+              const double2 xv = xs[(k0 + q) * XTP + tb + tt * 8 + g];
+              const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
+              const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
+              const double nai = -ai;
+#pragma unroll
+              for (int j = 0; j < NJ; ++j) {
+                dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+                dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
+                dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
+                dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
+              }
+#pragma unroll
+              for (int j = 0; j < REM; ++j) {
+                racc[i][j].x = fma(ar, rf[j].x, fma(nai, rf[j].y, racc[i][j].x));
+                racc[i][j].y = fma(ar, rf[j].y, fma(ai, rf[j].x, racc[i][j].y));
+              }
+            }
+          }
+        }
+        if (lown) {
+#pragma unroll
+          for (int tl = 0; tl < 2; ++tl) {
+            if (tl >= tb) break;
+            double2 sacc = make_double2(0.0, 0.0);
+            for (int nu = lpart; nu < kw; nu += 8) {
+              const double2 sv2 = S[lrow * SST + nu], xv = xs[nu * XTP + tl];
+              sacc.x = fma(sv2.x, xv.x, sacc.x);
+              sacc.x = fma(-sv2.y, xv.y, sacc.x);
+              sacc.y = fma(sv2.x, xv.y, sacc.y);
+              sacc.y = fma(sv2.y, xv.x, sacc.y);
+            }
+            const double2 z = Zl[tl];
+            lacc[tl].x = fma(z.x, sacc.x, fma(-z.y, sacc.y, lacc[tl].x));
+            lacc[tl].y = fma(z.x, sacc.y, fma(z.y, sacc.x, lacc[tl].y));
+          }
+        }
+      }
+    }
+  }
+  double2* out = a.part + (int64_t)sg.w * a.nl * p;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int tt = warp + 8 * i;
+    if (tt >= ntile) continue;
+    const int t = tc0 + tt * 8 + g;
+    if (t >= a.nl) continue;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int row = j * 8 + 2 * q + v;
+        if (row < nrow) out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
+      }
+  }
+  if (REM > 0) {
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int tt = warp + 8 * i;
+      if (tt >= ntile) continue;
+      const int t = tc0 + tt * 8 + g;
+#pragma unroll
+      for (int j = 0; j < (REM > 0 ? REM : 1); ++j) {
+        double2 v = racc[i][j];
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, 1);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, 1);
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, 2);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, 2);
+        if (q == 0 && t < a.nl && NJ * 8 + j < nrow) out[(int64_t)t * p + mu0 + NJ * 8 + j] = v;
+      }
+    }
+  }
+  if (lead && tb > 0) {
+#pragma unroll
+    for (int tl = 0; tl < 2; ++tl) {
+      if (tl >= tb) break;
+      double2 v = lacc[tl];
+#pragma unroll
+      for (int off = 1; off < 8; off <<= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
+      }
+      if (lpart == 0 && lrow < nrow) out[(int64_t)tl * p + mu0 + lrow] = v;
+    }
+  }
+}
+
+struct Far8Cfg {
+  int SST = 0, TT = 0, XTP = 0, tb = 0, nd = 0, ntiles = 0, nchunks = 0, mt = 0, KC = 0;
+  size_t smem = 0;
+};
+
+// KC: nu chunk width (kc_req > 0 forces it; otherwise the whole p if a
+// 128-column frequency tile fits, else 32); TT up to 128 (MT <= 2).
+Far8Cfg choose8(int p, int nl, size_t cap, int kc_req) {
+  int tb = nl % 8;
+  if (tb > 2 || tb == nl) tb = 0;
+  const int nD = (nl - tb + 7) / 8 * 8;
+  const int p4 = (p + 3) / 4 * 4;
+  auto make = [&](int KC, int TTmax) {
+    Far8Cfg c;
+    int SST = KC;
+    while (SST % 8 != 4) ++SST;
+    const int ntiles = (nD + TTmax - 1) / TTmax;
+    const int TT = ((nD / 8 + ntiles - 1) / ntiles) * 8;
+    int XTP = tb + TT;
+    while (XTP % 8 != 2) ++XTP;
+    const size_t smem =
+        sizeof(double2) * (32 * (size_t)SST + (size_t)KC * XTP + 64) + sizeof(double) * (64 + 96 + 3 * p);
+    if (smem > cap) return c;
+    c.SST = SST; c.TT = TT; c.XTP = XTP; c.tb = tb; c.nd = nD; c.ntiles = ntiles;
+    c.nchunks = (p + 31) / 32; c.mt = (TT / 8 + 7) / 8; c.smem = smem; c.KC = KC;
+    return c;
+  };
+  std::vector<int> kcs;
+  if (kc_req > 0) kcs = {std::min(p4, (kc_req + 3) / 4 * 4)};
+  else kcs = {p4, std::min(p4, 32)};
+  for (int TTmax : {128, 64, 32, 16, 8})
+    for (int KC : kcs) {
+      Far8Cfg c = make(KC, TTmax);
+      if (c.mt > 0 && c.mt <= 2) return c;
+    }
+  return Far8Cfg{};
+}
+
+template <int MT, int NJ, int REM>
+cudaError_t launch8(const Far8Cfg& c, int nseg, const Far8Args& a, cudaStream_t st) {
+  auto k = far8_kernel<MT, NJ, REM>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  if (e != cudaSuccess) return e;
+  k<<<dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks), 256, c.smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t dispatch8(const Far8Cfg& c, int p, bool rem_dfma, int nseg, const Far8Args& a, cudaStream_t st) {
+  if (p <= 8) return c.mt == 1 ? launch8<1, 1, 0>(c, nseg, a, st) : launch8<2, 1, 0>(c, nseg, a, st);
+  if (p == 27 && rem_dfma) return c.mt == 1 ? launch8<1, 3, 3>(c, nseg, a, st) : launch8<2, 3, 3>(c, nseg, a, st);
+  return c.mt == 1 ? launch8<1, 4, 0>(c, nseg, a, st) : launch8<2, 4, 0>(c, nseg, a, st);
+}
+
 // yhat[r] = sum over the row's segments (fixed order)
 __global__ void seg_reduce_kernel(const int32_t* __restrict__ rows, const int32_t* __restrict__ seg_ptr,
                                   const double2* __restrict__ part, double2* __restrict__ yhat, int64_t tile) {
@@ -998,7 +1252,25 @@ __global__ void __launch_bounds__(256) far_generic_kernel(FarArgs a) {
 bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st) {
   Tree& t = *op.tree;
   const int nl = op.n_local, p = t.p;
-  if (op.mode == BEM_MODE_H2ACA && op.far_kernel == 7 && !op.force_generic && op.n_segs > 0) {
+  const int fk = op.far_kernel != 0 ? op.far_kernel : (p > 32 ? 8 : 7);  // r01: far8 wins at p = 64, far7 at p = 27
+  if (op.mode == BEM_MODE_H2ACA && fk == 8 && !op.force_generic && op.n_segs > 0) {
+    const Far8Cfg f8 = choose8(p, nl, op.far4_smem_cap, op.far8_kc);
+    if (f8.mt > 0) {
+      BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
+      Far8Args a;
+      a.nl = nl; a.m = t.m; a.p = p; a.rcap = op.rcap; a.SST = f8.SST; a.TT = f8.TT; a.XTP = f8.XTP;
+      a.tb = f8.tb; a.nd = f8.nd; a.KC = f8.KC;
+      a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
+      a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
+      a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
+      BEM_CK(dispatch8(f8, p, op.far7_rem_dfma, op.n_segs, a, st));
+      seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
+                                                       yhat, (int64_t)nl * p);
+      BEM_CK(cudaGetLastError());
+      return BEM_OK;
+    }
+  }
+  if (op.mode == BEM_MODE_H2ACA && fk == 7 && !op.force_generic && op.n_segs > 0) {
     const Far7Cfg f7 = choose7(p, nl, op.far4_smem_cap, op.far7_cluster);
     if (f7.mt > 0) {
       BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
@@ -1015,7 +1287,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
       return BEM_OK;
     }
   }
-  if (op.mode == BEM_MODE_H2ACA && op.far_kernel == 6 && !op.force_generic && op.n_segs > 0) {
+  if (op.mode == BEM_MODE_H2ACA && fk == 6 && !op.force_generic && op.n_segs > 0) {
     const Far6Cfg f6 = choose6(p, nl, op.far4_smem_cap);
     if (f6.mt > 0) {
       BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
@@ -1032,7 +1304,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
       return BEM_OK;
     }
   }
-  if (op.mode == BEM_MODE_H2ACA && op.far_kernel == 4 && !op.force_generic && op.n_segs > 0) {
+  if (op.mode == BEM_MODE_H2ACA && fk == 4 && !op.force_generic && op.n_segs > 0) {
     const Far4Cfg f4 = choose4(p, nl, op.far4_smem_cap);
     if (f4.maxt > 0) {
       BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));

@@ -246,42 +246,33 @@ inline unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 using namespace bem;
 
-extern "C" bem_status cqm_solve(bem_op oh, const double* g_time, double* phi_time, int64_t M_loc, double R, double tol,
-                                int32_t restart, int32_t max_iter, void* nccl_comm, void* cuda_stream,
-                                bem_solve_stats* stats) {
-  BEM_REQ(oh && g_time && phi_time, "cqm_solve: NULL argument");
-  Op& op = oh->o;
+namespace bem {
+namespace {
+
+// Batched restarted GMRES over the op's local frequencies (frequency domain,
+// input panel order): solves V(s_l) X_t = B_t for every local t.  B, X:
+// device [n_local][M] complex.  Writes per-frequency iteration counts and the
+// final relative residuals (host vectors).
+bem_status gmres_multifreq(Op& op, const double2* B, double2* X, double tol, int restart, int max_iter,
+                           cudaStream_t st, std::vector<int>& hit, std::vector<double>& hrel) {
   Tree& tr = *op.tree;
-  BEM_REQ(nccl_comm == nullptr, "cqm_solve: multi-GPU transpose is issued by the caller; pass nccl_comm = NULL");
-  BEM_REQ(M_loc == tr.M, "cqm_solve: M_loc must equal the number of panels on a single device");
-  BEM_REQ(op.n_local == op.L, "cqm_solve: the operator must hold all L frequencies");
-  for (int t = 0; t < op.n_local; ++t) BEM_REQ(op.local_l[t] == t, "cqm_solve: local_l must be 0..L-1 in order");
-  BEM_REQ(tol > 0.0 && restart >= 1 && max_iter >= 1, "cqm_solve: bad tol/restart/max_iter");
-  BEM_REQ(R > 0.0 && R < 1.0, "cqm_solve: R must lie in (0,1)");
-  DeviceGuard dg(tr.device);
-  cudaStream_t st = (cudaStream_t)cuda_stream;
   const int64_t M = tr.M;
-  const int nl = op.n_local, N = op.L - 1;
+  const int nl = op.n_local;
   const int64_t n = M * nl;
-  DBuf<double> tmpc, b, x, r, w, V, h, H, g, cs, sn, y;
-  DBuf<double> beta, bnorm, hn, mx;
+  DBuf<double> r, w, V, h, H, g, cs, sn, y;
+  DBuf<double> beta, bnorm, hn;
   DBuf<int> active, cyc, jt, iters, cnt;
-  BEM_CK(tmpc.alloc(2 * n)); BEM_CK(b.alloc(2 * n)); BEM_CK(x.alloc(2 * n)); BEM_CK(r.alloc(2 * n));
+  BEM_CK(r.alloc(2 * n));
   BEM_CK(w.alloc(2 * n)); BEM_CK(V.alloc(2 * n * (restart + 1)));
   BEM_CK(h.alloc(2 * (size_t)nl * (restart + 1))); BEM_CK(H.alloc(2 * (size_t)nl * (restart + 1) * restart));
   BEM_CK(g.alloc(2 * (size_t)nl * (restart + 1))); BEM_CK(cs.alloc(2 * (size_t)nl * restart));
   BEM_CK(sn.alloc(2 * (size_t)nl * restart)); BEM_CK(y.alloc(2 * (size_t)nl * restart));
-  BEM_CK(beta.alloc(nl)); BEM_CK(bnorm.alloc(nl)); BEM_CK(hn.alloc(nl)); BEM_CK(mx.alloc(2));
+  BEM_CK(beta.alloc(nl)); BEM_CK(bnorm.alloc(nl)); BEM_CK(hn.alloc(nl));
   BEM_CK(active.alloc(nl)); BEM_CK(cyc.alloc(nl)); BEM_CK(jt.alloc(nl)); BEM_CK(iters.alloc(nl)); BEM_CK(cnt.alloc(1));
-  double2* B = (double2*)b.p; double2* X = (double2*)x.p; double2* Rr = (double2*)r.p; double2* Wv = (double2*)w.p;
+  double2* Rr = (double2*)r.p; double2* Wv = (double2*)w.p;
   double2* VV = (double2*)V.p;
-  // g^ = forward(g)
-  real_to_complex_kernel<<<nblk(n), 256, 0, st>>>(g_time, (double2*)tmpc.p, n);
-  BEM_CK(cudaGetLastError());
-  bem_status rs = fft_transform(tmpc.p, b.p, M, N, R, false, st);
-  if (rs != BEM_OK) return rs;
   norm_kernel<<<nl, kRed, 0, st>>>(B, bnorm.p, M);
-  BEM_CK(cudaMemsetAsync(x.p, 0, sizeof(double) * 2 * n, st));
+  BEM_CK(cudaMemsetAsync(X, 0, sizeof(double2) * n, st));
   BEM_CK(cudaMemsetAsync(iters.p, 0, sizeof(int) * nl, st));
   {
     std::vector<int> ones(nl, 1);
@@ -289,9 +280,10 @@ extern "C" bem_status cqm_solve(bem_op oh, const double* g_time, double* phi_tim
     BEM_CK(cudaStreamSynchronize(st));
   }
   int total = 0;
+  bem_status rs;
   for (;;) {
     // r = b - A x ; beta = ||r||
-    rs = apply_launch(op, x.p, w.p, st);
+    rs = apply_launch(op, (const double*)X, w.p, st);
     if (rs != BEM_OK) return rs;
     axpby_kernel<<<nblk(n), 256, 0, st>>>(B, Wv, Rr, n);
     norm_kernel<<<nl, kRed, 0, st>>>(Rr, beta.p, M);
@@ -327,12 +319,84 @@ extern "C" bem_status cqm_solve(bem_op oh, const double* g_time, double* phi_tim
     xupdate_kernel<<<nblk(n), 256, 0, st>>>(VV, (double2*)y.p, jt.p, X, M, nl, restart);
     BEM_CK(cudaGetLastError());
   }
-  // final residuals
   std::vector<double> hb(nl), hbn(nl);
-  std::vector<int> hit(nl), hact(nl);
+  hit.assign(nl, 0);
+  hrel.assign(nl, 0.0);
   BEM_CK(cudaMemcpy(hb.data(), beta.p, sizeof(double) * nl, cudaMemcpyDeviceToHost));
   BEM_CK(cudaMemcpy(hbn.data(), bnorm.p, sizeof(double) * nl, cudaMemcpyDeviceToHost));
   BEM_CK(cudaMemcpy(hit.data(), iters.p, sizeof(int) * nl, cudaMemcpyDeviceToHost));
+  for (int t = 0; t < nl; ++t) hrel[t] = hbn[t] > 0.0 ? hb[t] / hbn[t] : 0.0;
+  return BEM_OK;
+}
+
+bem_status finish_stats(const std::vector<int>& hit, const std::vector<double>& hrel, double tol, int max_iter,
+                        double imag_rel, bem_solve_stats* stats) {
+  int nunc = 0, imax = 0, isum = 0;
+  double rmax = 0.0;
+  for (size_t t = 0; t < hit.size(); ++t) {
+    rmax = std::max(rmax, hrel[t]);
+    if (hrel[t] > tol) ++nunc;
+    imax = std::max(imax, hit[t]);
+    isum += hit[t];
+  }
+  if (stats) {
+    stats->iters_max = imax; stats->iters_sum = isum; stats->n_unconverged = nunc;
+    stats->resid_max = rmax; stats->imag_rel_max = imag_rel;
+  }
+  if (nunc > 0) {
+    set_error("GMRES: %d frequencies did not converge within max_iter=%d", nunc, max_iter);
+    return BEM_ENOCONV;
+  }
+  return BEM_OK;
+}
+
+}  // namespace
+}  // namespace bem
+
+extern "C" bem_status bem_solve_multifreq(bem_op oh, const bem_c128* g_freq, bem_c128* phi_freq, double tol,
+                                          int32_t restart, int32_t max_iter, void* cuda_stream,
+                                          bem_solve_stats* stats) {
+  BEM_REQ(oh && g_freq && phi_freq, "bem_solve_multifreq: NULL argument");
+  BEM_REQ(g_freq != phi_freq, "bem_solve_multifreq: in-place is not allowed");
+  BEM_REQ(tol > 0.0 && restart >= 1 && max_iter >= 1, "bem_solve_multifreq: bad tol/restart/max_iter");
+  Op& op = oh->o;
+  DeviceGuard dg(op.tree->device);
+  std::vector<int> hit;
+  std::vector<double> hrel;
+  bem_status rs = gmres_multifreq(op, (const double2*)g_freq, (double2*)phi_freq, tol, restart, max_iter,
+                                  (cudaStream_t)cuda_stream, hit, hrel);
+  if (rs != BEM_OK) return rs;
+  return finish_stats(hit, hrel, tol, max_iter, 0.0, stats);
+}
+
+extern "C" bem_status cqm_solve(bem_op oh, const double* g_time, double* phi_time, int64_t M_loc, double R, double tol,
+                                int32_t restart, int32_t max_iter, void* nccl_comm, void* cuda_stream,
+                                bem_solve_stats* stats) {
+  BEM_REQ(oh && g_time && phi_time, "cqm_solve: NULL argument");
+  Op& op = oh->o;
+  Tree& tr = *op.tree;
+  BEM_REQ(nccl_comm == nullptr, "cqm_solve: multi-GPU transpose is issued by the caller; pass nccl_comm = NULL");
+  BEM_REQ(M_loc == tr.M, "cqm_solve: M_loc must equal the number of panels on a single device");
+  BEM_REQ(op.n_local == op.L, "cqm_solve: the operator must hold all L frequencies");
+  for (int t = 0; t < op.n_local; ++t) BEM_REQ(op.local_l[t] == t, "cqm_solve: local_l must be 0..L-1 in order");
+  BEM_REQ(tol > 0.0 && restart >= 1 && max_iter >= 1, "cqm_solve: bad tol/restart/max_iter");
+  BEM_REQ(R > 0.0 && R < 1.0, "cqm_solve: R must lie in (0,1)");
+  DeviceGuard dg(tr.device);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int64_t M = tr.M;
+  const int nl = op.n_local, N = op.L - 1;
+  const int64_t n = M * nl;
+  DBuf<double> tmpc, b, x, mx;
+  BEM_CK(tmpc.alloc(2 * n)); BEM_CK(b.alloc(2 * n)); BEM_CK(x.alloc(2 * n)); BEM_CK(mx.alloc(2));
+  // g^ = forward(g)
+  real_to_complex_kernel<<<nblk(n), 256, 0, st>>>(g_time, (double2*)tmpc.p, n);
+  BEM_CK(cudaGetLastError());
+  bem_status rs = fft_transform(tmpc.p, b.p, M, N, R, false, st);
+  if (rs != BEM_OK) return rs;
+  std::vector<int> hit;
+  std::vector<double> hrel;
+  rs = gmres_multifreq(op, (const double2*)b.p, (double2*)x.p, tol, restart, max_iter, st, hit, hrel);
+  if (rs != BEM_OK) return rs;
   // phi = Re inverse(phi^)
   rs = fft_transform(x.p, tmpc.p, M, N, R, true, st);
   if (rs != BEM_OK) return rs;
@@ -342,22 +406,5 @@ extern "C" bem_status cqm_solve(bem_op oh, const double* g_time, double* phi_tim
   double hmx[2] = {0, 0};
   BEM_CK(cudaMemcpyAsync(hmx, mx.p, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
   BEM_CK(cudaStreamSynchronize(st));
-  int nunc = 0, imax = 0, isum = 0;
-  double rmax = 0.0;
-  for (int t = 0; t < nl; ++t) {
-    const double rel = hbn[t] > 0.0 ? hb[t] / hbn[t] : 0.0;
-    rmax = std::max(rmax, rel);
-    if (rel > tol) ++nunc;
-    imax = std::max(imax, hit[t]);
-    isum += hit[t];
-  }
-  if (stats) {
-    stats->iters_max = imax; stats->iters_sum = isum; stats->n_unconverged = nunc;
-    stats->resid_max = rmax; stats->imag_rel_max = hmx[1] > 0.0 ? hmx[0] / hmx[1] : 0.0;
-  }
-  if (nunc > 0) {
-    set_error("cqm_solve: %d frequencies did not converge within max_iter=%d", nunc, max_iter);
-    return BEM_ENOCONV;
-  }
-  return BEM_OK;
+  return finish_stats(hit, hrel, tol, max_iter, hmx[1] > 0.0 ? hmx[0] / hmx[1] : 0.0, stats);
 }

@@ -74,20 +74,59 @@ class ShardedTimeOperator:
             o += n
         return out
 
-    def step(self, x_loc):
-        """x_loc: [L][M_g] complex (this rank's DOF shard) -> y_loc [L][M_g]."""
+    def to_frequency_shard(self, xf):
+        """[L][M_g] (all frequencies, this rank's DOFs) -> [L_g][M] (this rank's frequencies, all DOFs)."""
         torch = self._torch
         g = self.rank
-        xf = self.forward_fn(x_loc)  # [L][M_g]
-        send = [xf.index_select(0, torch.as_tensor(self.local[h], dtype=torch.long, device=xf.device)) for h in range(self.G)]
+        send = [xf.index_select(0, torch.as_tensor(self.local[h], dtype=torch.long, device=xf.device))
+                for h in range(self.G)]
         Mg = [e - b for b, e in self.ranges]
         Lg = len(self.local[g])
         recv = self._a2a(send, [(Lg, Mg[h]) for h in range(self.G)], xf.device)
-        xl = torch.cat(recv, dim=1).contiguous()  # [L_g][M] in panel order
-        yl = self.apply_fn(xl)
+        return torch.cat(recv, dim=1).contiguous()
+
+    def to_dof_shard(self, yl):
+        """[L_g][M] -> [L][M_g] (inverse of to_frequency_shard)."""
+        torch = self._torch
+        g = self.rank
+        Mg = [e - b for b, e in self.ranges]
         send = [yl[:, b:e] for (b, e) in self.ranges]
-        recv = self._a2a(send, [(len(self.local[h]), Mg[g]) for h in range(self.G)], xf.device)
-        yf = torch.empty_like(xf)
+        recv = self._a2a(send, [(len(self.local[h]), Mg[g]) for h in range(self.G)], yl.device)
+        yf = torch.empty((self.L, Mg[g]), dtype=yl.dtype, device=yl.device)
         for h in range(self.G):
-            yf.index_copy_(0, torch.as_tensor(self.local[h], dtype=torch.long, device=xf.device), recv[h])
-        return self.inverse_fn(yf)
+            yf.index_copy_(0, torch.as_tensor(self.local[h], dtype=torch.long, device=yl.device), recv[h])
+        return yf
+
+    def step(self, x_loc):
+        """x_loc: [L][M_g] complex (this rank's DOF shard) -> y_loc [L][M_g]."""
+        xf = self.forward_fn(x_loc)  # [L][M_g]
+        yl = self.apply_fn(self.to_frequency_shard(xf))
+        return self.inverse_fn(self.to_dof_shard(yl))
+
+
+class ShardedSolver(ShardedTimeOperator):
+    """Frequency-decoupled CQM solve (Remark P:1607-1614) on G ranks:
+    phi = Re inverse(V(s_l)^{-1} forward(g)) with DOF-sharded time data.
+    solve_fn maps this rank's frequency shard [L_g][M] of g^ to phi^ and
+    returns (phi^, stats dict); the library's bem_solve_multifreq on GPUs."""
+
+    def __init__(self, rank, world, M, L, solve_fn, forward_fn, inverse_fn, group=None):
+        super().__init__(rank, world, M, L, None, forward_fn, inverse_fn, group)
+        self.solve_fn = solve_fn
+
+    def solve(self, g_loc):
+        """g_loc: [N+1][M_g] real (this rank's DOFs) -> (phi_loc [N+1][M_g] real, global stats)."""
+        import torch.distributed as dist
+        torch = self._torch
+        gf = self.forward_fn(g_loc.to(torch.complex128))
+        phil, st = self.solve_fn(self.to_frequency_shard(gf))
+        phi = self.inverse_fn(self.to_dof_shard(phil))
+        agg = torch.tensor([st["iters_max"], st["resid_max"], st["n_unconverged"], st["iters_sum"]],
+                           dtype=torch.float64, device=g_loc.device)
+        mx = agg[:2].clone()
+        sm = agg[2:].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=self.group)
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM, group=self.group)
+        stats = {"iters_max": int(mx[0]), "resid_max": float(mx[1]), "n_unconverged": int(sm[0]),
+                 "iters_sum": int(sm[1])}
+        return phi.real.contiguous(), stats

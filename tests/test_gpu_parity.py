@@ -262,7 +262,7 @@ def test_edge_cases(pb, torch):
 
 
 @pytest.mark.parametrize("N,kernel,cluster", [(256, "7", "0"), (260, "7", "0"), (256, "7", "1"), (260, "7", "1"),
-                                               (256, "6", "0")])
+                                               (256, "6", "0"), (256, "8", "0"), (260, "8", "0")])
 def test_h2aca_p64_multi_tile(pb, torch, N, kernel, cluster, monkeypatch):
     """p = 64 (m = 4) with L > 128: K3 runs several frequency tiles per
     (segment, mu chunk); far7 with BEM_FAR7_CLUSTER=1 shares the regenerated
@@ -306,3 +306,50 @@ def test_local_subset_padded_columns(pb, torch, nloc):
     y = _apply(pb, torch, op, x)
     yo = oh.apply(O.MODE_H2ACA, s, x, local)
     assert _rel(y, yo) <= 1e-10
+
+
+def test_solve_multifreq_local_shard(pb, torch):
+    """bem_solve_multifreq (the per-rank building block of the sharded solve)
+    on a frequency shard: residual re-evaluated by the oracle's H2ACA apply and
+    solution vs the oracle's GMRES on the same frequencies."""
+    V, T = synth.icosphere(3)
+    N = 32
+    M, L = len(T), N + 1
+    R = 10.0 ** (-5.0 / N)
+    s = pb.cqm_frequencies(N, 2.0)
+    local = np.array([0, 3, 4, 16, 17, 29, 30], dtype=np.int32)
+    op = pb.Operator(pb.Tree(V, T, 32, 1.0, 3), s, 1e-8, local_l=local)
+    g = synth.pulse(V, T, N, 2.0)
+    gf = O.forward(g.astype(np.complex128), N, R)[local]
+    phi, st = pb.solve_multifreq(op, torch.from_numpy(np.ascontiguousarray(gf)).cuda(), tol=1e-9, restart=20)
+    phi = phi.cpu().numpy()
+    assert st["n_unconverged"] == 0 and st["resid_max"] <= 1e-9
+    oh = O.H2(V, T, 32, 1.0, 3)
+    oh.aca(s, 1e-8)
+    res = oh.apply(O.MODE_H2ACA, s, phi, local) - gf
+    assert np.max(np.linalg.norm(res, axis=1) / np.linalg.norm(gf, axis=1)) <= 1.5e-9
+    xo, it, rr = oh.gmres(O.MODE_H2ACA, s, gf, local, tol=1e-9, restart=20)
+    assert _rel(phi, xo) <= 1e-6
+
+
+@pytest.mark.parametrize("kernel,kc", [("8", "0"), ("8", "32"), ("8", "20"), ("7", "0")])
+def test_h2aca_p125(pb, torch, kernel, kc, monkeypatch):
+    """p = 125 (m = 5, config 5's order): far8 contracts nu in chunks
+    (KC = 32 automatically, 20 forced: ragged last chunk 5), far7 whole p."""
+    monkeypatch.setenv("BEM_FAR_KERNEL", kernel)
+    monkeypatch.setenv("BEM_FAR8_KC", kc)
+    V, T = synth.icosphere(3)
+    N = 64
+    M, L, eps = len(T), N + 1, 1e-8
+    s = pb.cqm_frequencies(N, 2.0)
+    x = synth.random_density(5, L, M)
+    oh = O.H2(V, T, 64, 1.0, 5)
+    oa = oh.aca(s, eps)
+    tree = pb.Tree(V, T, 64, 1.0, 5)
+    op = pb.Operator(tree, s, eps, mode=pb.BEM_MODE_H2ACA)
+    ga = op.aca_export()
+    assert np.array_equal(ga["ranks"], oa["ranks"]) and np.array_equal(ga["pivots"], oa["pivots"])
+    y = _apply(pb, torch, op, x)
+    lsel = np.array([0, 1, 31, 32, 33, 63, 64])
+    yo = oh.apply(O.MODE_H2ACA, s, x[lsel], lsel)
+    assert _rel(y[lsel], yo) <= 1e-10

@@ -149,6 +149,10 @@ struct Op {
   bool far7_rem_dfma = true;          // p = 27: rows 24..26 on DFMA instead of a padded DMMA tile
   bool far7_cluster = false;
   int far8_kc = 0;                    // far8 nu-chunk width (0: automatic)          // DSMEM-shared slices across frequency tiles (measured slower, r01)
+  // optional per-local-frequency mask (1 = compute); set only by the GMRES driver so that
+  // converged frequencies skip K1 / K3 work (their outputs are then zero)
+  const int32_t* d_mask = nullptr;
+  bool use_solve_mask = true;  // env BEM_SOLVE_MASK=0 disables
   // profiling
   bool profile = false;
   cudaEvent_t ev[6] = {};

@@ -600,6 +600,7 @@ struct Far7Args {
   const double2* Z;
   const double2* xhat;
   double2* part;
+  const int32_t* mask;  // nullable: per local frequency, 0 = skip (output 0)
 };
 
 __device__ __forceinline__ double2 kern_rs(double d2, double2 s, const double* etab, const double2* sctab) {
@@ -644,6 +645,22 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
   if (CL) crank = (int)cooperative_groups::this_cluster().block_rank();
   const int e0 = crank * a.own, e1 = min(nS, e0 + a.own);  // this CTA's share of the slice entries
   const int ntile = ncol / 8;
+  bool ton[MT];  // 8-column frequency tile has at least one unmasked column (GMRES mask)
+  bool cta_on = false;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int tt = warp + 8 * i;
+    const int t = tc0 + tt * 8 + g;
+    const bool v = tt < ntile && t < a.nl && (a.mask == nullptr || a.mask[t]);
+    ton[i] = __any_sync(0xffffffffu, v);
+  }
+  {
+    int lo = 0;
+    for (int t = tid; t < ncol; t += blockDim.x) lo |= (tc0 + t < a.nl) && (a.mask == nullptr || a.mask[tc0 + t]);
+    if (lead) for (int t = tid; t < tb; t += blockDim.x) lo |= a.mask == nullptr || a.mask[t];
+    cta_on = __syncthreads_or(lo) != 0;
+    if (CL) cta_on = true;  // every CTA of a cluster must reach the same cluster barriers
+  }
   double acc[MT][NJ][2][2];
   double2 racc[MT][REM > 0 ? REM : 1];
 #pragma unroll
@@ -659,7 +676,7 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
   double2 lacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
   const int ncp = tb + ncol;
   int buf = 0;
-  for (int bi = sg.y; bi < sg.z; ++bi) {
+  for (int bi = sg.y; bi < (cta_on ? sg.z : sg.y); ++bi) {
     const int b = a.far_sorted[bi];
     const int c = a.far_c[b];
     __syncthreads();
@@ -720,7 +737,7 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
           const int tt = warp + 8 * i;
-          if (tt < ntile) {
+          if (tt < ntile && ton[i]) {
             const double2 xv = xs[(k0 + q) * XTP + tb + tt * 8 + g];
             const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
             const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
@@ -904,6 +921,7 @@ struct Far8Args {
   const double2* Z;
   const double2* xhat;
   double2* part;
+  const int32_t* mask;  // nullable: per local frequency, 0 = skip (output 0)
 };
 
 template <int MT, int NJ, int REM>
@@ -932,6 +950,21 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
   }
   for (int i = tid; i < nrow; i += blockDim.x) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
   const int ntile = ncol / 8;
+  bool ton[MT];  // 8-column frequency tile has at least one unmasked column (GMRES mask)
+  bool cta_on = false;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int tt = warp + 8 * i;
+    const int t = tc0 + tt * 8 + g;
+    const bool v = tt < ntile && t < a.nl && (a.mask == nullptr || a.mask[t]);
+    ton[i] = __any_sync(0xffffffffu, v);
+  }
+  {
+    int lo = 0;
+    for (int t = tid; t < ncol; t += blockDim.x) lo |= (tc0 + t < a.nl) && (a.mask == nullptr || a.mask[tc0 + t]);
+    if (lead) for (int t = tid; t < tb; t += blockDim.x) lo |= a.mask == nullptr || a.mask[t];
+    cta_on = __syncthreads_or(lo) != 0;
+  }
   double acc[MT][NJ][2][2];
   double2 racc[MT][REM > 0 ? REM : 1];
 #pragma unroll
@@ -945,7 +978,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
   const bool lown = lead && tb > 0 && lrow < nrow;
   double2 lacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
   const int ncp = tb + ncol;
-  for (int bi = sg.y; bi < sg.z; ++bi) {
+  for (int bi = sg.y; bi < (cta_on ? sg.z : sg.y); ++bi) {
     const int b = a.far_sorted[bi];
     const int c = a.far_c[b];
     const double2* xh = a.xhat + (int64_t)c * a.nl * p;
@@ -995,7 +1028,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
 #pragma unroll
           for (int i = 0; i < MT; ++i) {
             const int tt = warp + 8 * i;
-            if (tt < ntile) {
+            if (tt < ntile && ton[i]) {
               const double2 xv = xs[(k0 + q) * XTP + tb + tt * 8 + g];
               const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
               const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
@@ -1263,6 +1296,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
       a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
       a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
       a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
+      a.mask = op.d_mask;
       BEM_CK(dispatch8(f8, p, op.far7_rem_dfma, op.n_segs, a, st));
       seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
                                                        yhat, (int64_t)nl * p);
@@ -1280,6 +1314,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
       a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
       a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
       a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
+      a.mask = op.d_mask;
       BEM_CK(dispatch7(f7, p, op.far7_rem_dfma, op.n_segs, a, st));
       seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
                                                        yhat, (int64_t)nl * p);

@@ -37,6 +37,7 @@ struct NearArgs {
   const int32_t* local_l;
   const int32_t* class_t1;
   const int32_t* class_t2;
+  const int32_t* mask;  // nullable: per local frequency, 0 = skip (output 0)
   const double2* xc;
   double2* yc;
 };
@@ -93,7 +94,16 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
 #pragma unroll
   for (int f = 0; f < F; ++f) {
     const int c = c0 + f;
-    if (c < a.n_class) {
+    const bool on = c < a.n_class &&
+                    (a.mask == nullptr || a.mask[a.class_t1[c]] || (a.class_t2[c] >= 0 && a.mask[a.class_t2[c]]));
+    if (c < a.n_class && !on) {  // converged frequencies (GMRES mask): write zeros, skip the work
+      const int t1 = a.class_t1[c], t2 = a.class_t2[c];
+      if (lane == 0) {
+        a.yc[(int64_t)t1 * a.M + k] = make_double2(0.0, 0.0);
+        if (t2 >= 0) a.yc[(int64_t)t2 * a.M + k] = make_double2(0.0, 0.0);
+      }
+    }
+    if (on) {
       const int t1 = a.class_t1[c], t2 = a.class_t2[c];
       const double2 sv = a.s[a.local_l[t1]];
       sre[f] = sv.x; sim[f] = sv.y;
@@ -103,6 +113,10 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
       sre[f] = 0.0; sim[f] = 0.0; o1[f] = -1; o2[f] = -1;
     }
   }
+  bool any = false;
+#pragma unroll
+  for (int f = 0; f < F; ++f) any |= o1[f] >= 0;
+  if (!any) return;
   double2 acc1[F], acc2[F];
 #pragma unroll
   for (int f = 0; f < F; ++f) { acc1[f] = make_double2(0.0, 0.0); acc2[f] = make_double2(0.0, 0.0); }
@@ -205,7 +219,7 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st) 
   na.near_j = dense ? op.d_dn_j.p : t.d_near_j.p;
   na.cen = t.d_cen.p; na.qn = t.d_qn.p; na.qw = t.d_qw.p; na.selfJ = t.d_selfJ.p;
   na.s = (const double2*)op.d_s.p; na.local_l = op.d_local_l.p;
-  na.class_t1 = op.d_class_t1.p; na.class_t2 = op.d_class_t2.p; na.xc = xc; na.yc = yc;
+  na.class_t1 = op.d_class_t1.p; na.class_t2 = op.d_class_t2.p; na.mask = op.d_mask; na.xc = xc; na.yc = yc;
   const int F = op.near_f;
   const int U = op.near_unroll;
   const bool T = op.near_tab;

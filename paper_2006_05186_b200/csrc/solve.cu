@@ -271,6 +271,12 @@ bem_status gmres_multifreq(Op& op, const double2* B, double2* X, double tol, int
   BEM_CK(active.alloc(nl)); BEM_CK(cyc.alloc(nl)); BEM_CK(jt.alloc(nl)); BEM_CK(iters.alloc(nl)); BEM_CK(cnt.alloc(1));
   double2* Rr = (double2*)r.p; double2* Wv = (double2*)w.p;
   double2* VV = (double2*)V.p;
+  // converged frequencies skip the K1 / K3 work of later applies (op.d_mask)
+  struct MaskGuard {
+    Op& o;
+    ~MaskGuard() { o.d_mask = nullptr; }
+  } mask_guard{op};
+  const bool use_mask = op.use_solve_mask;
   norm_kernel<<<nl, kRed, 0, st>>>(B, bnorm.p, M);
   BEM_CK(cudaMemsetAsync(X, 0, sizeof(double2) * n, st));
   BEM_CK(cudaMemsetAsync(iters.p, 0, sizeof(int) * nl, st));
@@ -283,6 +289,7 @@ bem_status gmres_multifreq(Op& op, const double2* B, double2* X, double tol, int
   bem_status rs;
   for (;;) {
     // r = b - A x ; beta = ||r||
+    op.d_mask = use_mask ? active.p : nullptr;
     rs = apply_launch(op, (const double*)X, w.p, st);
     if (rs != BEM_OK) return rs;
     axpby_kernel<<<nblk(n), 256, 0, st>>>(B, Wv, Rr, n);
@@ -297,6 +304,7 @@ bem_status gmres_multifreq(Op& op, const double2* B, double2* X, double tol, int
     if (hcnt == 0 || total >= max_iter) break;
     scale_kernel<<<nblk(n), 256, 0, st>>>(Rr, beta.p, VV, M, nl);
     for (int j = 0; j < restart && total < max_iter; ++j) {
+      op.d_mask = use_mask ? cyc.p : nullptr;
       rs = apply_launch(op, (const double*)(VV + (int64_t)j * n), w.p, st);
       if (rs != BEM_OK) return rs;
       ++total;
@@ -317,6 +325,14 @@ bem_status gmres_multifreq(Op& op, const double2* B, double2* X, double tol, int
     }
     trisolve_kernel<<<nblk(nl), 256, 0, st>>>((double2*)H.p, (double2*)g.p, (double2*)y.p, jt.p, restart, nl);
     xupdate_kernel<<<nblk(n), 256, 0, st>>>(VV, (double2*)y.p, jt.p, X, M, nl, restart);
+    BEM_CK(cudaGetLastError());
+  }
+  if (use_mask) {  // true final residuals of every frequency (the last masked apply zeroed converged ones)
+    op.d_mask = nullptr;
+    rs = apply_launch(op, (const double*)X, w.p, st);
+    if (rs != BEM_OK) return rs;
+    axpby_kernel<<<nblk(n), 256, 0, st>>>(B, Wv, Rr, n);
+    norm_kernel<<<nl, kRed, 0, st>>>(Rr, beta.p, M);
     BEM_CK(cudaGetLastError());
   }
   std::vector<double> hb(nl), hbn(nl);

@@ -353,3 +353,25 @@ def test_h2aca_p125(pb, torch, kernel, kc, monkeypatch):
     lsel = np.array([0, 1, 31, 32, 33, 63, 64])
     yo = oh.apply(O.MODE_H2ACA, s, x[lsel], lsel)
     assert _rel(y[lsel], yo) <= 1e-10
+
+
+def test_solve_mask_bitwise_identical(pb, torch, monkeypatch):
+    """Converged frequencies skip the K1/K3 work of later GMRES iterations
+    (op mask); the still-active frequencies' arithmetic is unchanged, so the
+    solution and the iteration counts are bitwise identical to the unmasked solve."""
+    V, T = synth.icosphere(3)
+    N = 64
+    R = 10.0 ** (-5.0 / N)
+    s = pb.cqm_frequencies(N, 2.0)
+    tree = pb.Tree(V, T, 48, 1.0, 4)
+    g = torch.from_numpy(synth.pulse(V, T, N, 2.0)).cuda()
+    out = []
+    for m in ("1", "0"):
+        monkeypatch.setenv("BEM_SOLVE_MASK", m)
+        op = pb.Operator(tree, s, 1e-6)
+        phi, st = pb.cqm_solve(op, g, R, tol=1e-8, restart=20)
+        out.append((phi.cpu().numpy(), st))
+        op.close()
+    assert out[0][1]["iters_sum"] == out[1][1]["iters_sum"] and out[0][1]["n_unconverged"] == 0
+    assert out[0][1]["resid_max"] == out[1][1]["resid_max"]
+    assert np.array_equal(out[0][0], out[1][0])

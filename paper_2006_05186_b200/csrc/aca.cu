@@ -543,7 +543,7 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, t.device);
       int64_t total = 0;
       for (int b = 0; b < (int)t.far_r.size(); ++b) total += op.ranks[b];
-      int64_t cap = std::max<int64_t>(1, total / (4 * (int64_t)nsm));
+      int64_t cap = std::max<int64_t>(1, total / (8 * (int64_t)nsm));  // ~8 segments per SM (r01: config 2 K3 9.02 -> 8.77 ms vs 4 per SM)
       if (const char* e = getenv("BEM_SEG_CAP")) cap = std::max<int64_t>(1, atoll(e));
       struct Seg { int64_t cost; int row, bi0, bi1, slot; };
       std::vector<Seg> segs;

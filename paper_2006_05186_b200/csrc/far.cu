@@ -626,8 +626,8 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
   const int mu0 = blockIdx.z * 32;
   const int nrow = min(32, p - mu0);
   const int nS = nrow * p;
-  double2* S = sm;                                    // 32 x SST
-  double2* own = S + 32 * SST;                        // CL: 2 x a.own
+  double2* S0 = sm;                                   // 2 x (32 x SST): double-buffered slice rows
+  double2* own = S0 + 2 * 32 * SST;                   // CL: 2 x a.own
   double2* xs = own + (CL ? 2 * a.own : 0);           // p4 x XTP
   double2* sctab = xs + (size_t)p4 * XTP;             // 64 (cos, sin)(k pi/32)
   double* etab = (double*)(sctab + 64);               // 64
@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
   double* xcn = xr + 96;                              // 3p
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
-  for (int i = tid; i < 32 * SST + p4 * XTP + (CL ? 2 * a.own : 0); i += blockDim.x) sm[i] = make_double2(0.0, 0.0);
+  for (int i = tid; i < 2 * 32 * SST + p4 * XTP + (CL ? 2 * a.own : 0); i += blockDim.x) sm[i] = make_double2(0.0, 0.0);
   for (int i = tid; i < 64; i += blockDim.x) {
     etab[i] = fast::kExp2Tab[i];
     sctab[i] = fast::kSinCosTab[i];
@@ -691,6 +691,10 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
     const double2* Zb = a.Z + a.zoff[b];
     __syncthreads();
     for (int l = 0; l < rk; ++l) {
+      // non-cluster path: S alternates between two buffers, so one barrier per
+      // term suffices and warps may run one term apart (regeneration of term
+      // l+1 overlaps other warps' DMMA work on term l)
+      double2* S = S0 + (CL ? 0 : (l & 1) * 32 * SST);
       const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + l]];
       const double2* Zl = Zb + (int64_t)l * a.nl;
       double2 zt[MT];
@@ -719,7 +723,6 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
         buf ^= 1;
         __syncthreads();
       } else {
-        __syncthreads();
         for (int e = tid; e < nS; e += blockDim.x) {
           const int i = e / p, nu = e - i * p;
           const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
@@ -845,7 +848,7 @@ Far7Cfg choose7(int p, int nl, size_t cap, bool cluster) {
     while (XTP % 8 != 2) ++XTP;
     const int cs = (cluster && ntiles > 1 && ntiles <= 8) ? ntiles : 1;
     const int own = cs > 1 ? (nrow * p + cs - 1) / cs : 0;
-    const size_t smem = sizeof(double2) * (32 * (size_t)SST + (size_t)p4 * XTP + 2 * (size_t)own + 64) +
+    const size_t smem = sizeof(double2) * (2 * 32 * (size_t)SST + (size_t)p4 * XTP + 2 * (size_t)own + 64) +
                         sizeof(double) * (64 + 96 + 3 * p);
     if (smem > cap) continue;
     c.p4 = p4; c.SST = SST; c.TT = TT; c.XTP = XTP; c.nT = TT / 8; c.tb = tb; c.nd = nD; c.ntiles = ntiles;
@@ -935,15 +938,16 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
   const bool lead = blockIdx.y == 0;
   const int mu0 = blockIdx.z * 32;
   const int nrow = min(32, p - mu0);
-  double2* S = sm;                                    // 32 x SST (SST >= KC)
-  double2* xs = S + 32 * SST;                         // KC x XTP
+  double2* S0 = sm;                                   // 2 x (32 x SST), SST >= KC: double-buffered slice
+  double2* xs = S0 + 2 * 32 * SST;                    // KC x XTP
   double2* sctab = xs + (size_t)KC * XTP;             // 64 (cos, sin)(k pi/32)
   double* etab = (double*)(sctab + 64);               // 64
   double* xr = etab + 64;                             // 96
   double* xcn = xr + 96;                              // 3p
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
-  for (int i = tid; i < 32 * SST + KC * XTP; i += blockDim.x) sm[i] = make_double2(0.0, 0.0);
+  for (int i = tid; i < 2 * 32 * SST + KC * XTP; i += blockDim.x) sm[i] = make_double2(0.0, 0.0);
+  int sbuf = 0;
   for (int i = tid; i < 64; i += blockDim.x) {
     etab[i] = fast::kExp2Tab[i];
     sctab[i] = fast::kSinCosTab[i];
@@ -989,7 +993,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
     for (int k0c = 0; k0c < p; k0c += KC) {
       const int kw = min(KC, p - k0c);          // real nu in this chunk
       const int kw4 = (kw + 3) & ~3;            // k-steps cover kw4 (padding rows/cols are zero)
-      if (k0c > 0) __syncthreads();             // previous chunk's GEMM done with xs / S
+      if (k0c > 0) __syncthreads();             // previous chunk's GEMM done with xs
       for (int idx = tid; idx < ncp * KC; idx += blockDim.x) {
         const int tl = idx / KC, nu = idx - tl * KC;
         const int tg = tl < tb ? tl : tc0 + (tl - tb);
@@ -1006,7 +1010,11 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
           const int t = tc0 + tt * 8 + g;
           zt[i] = (tt < ntile && t < a.nl) ? Zl[t] : make_double2(0.0, 0.0);
         }
-        __syncthreads();  // xs staged (first term) / previous term's GEMM done with S
+        // S alternates between two buffers: one barrier per term, and warps may
+        // run one term apart (regeneration overlaps other warps' DMMA work)
+        double2* S = S0 + sbuf * 32 * SST;
+        sbuf ^= 1;
+        if (l == 0) __syncthreads();  // xs / node coordinates staged
         for (int e = tid; e < nrow * KC; e += blockDim.x) {
           const int i = e / KC, nu = e - i * KC;
           double2 v = make_double2(0.0, 0.0);
@@ -1136,7 +1144,7 @@ Far8Cfg choose8(int p, int nl, size_t cap, int kc_req) {
     int XTP = tb + TT;
     while (XTP % 8 != 2) ++XTP;
     const size_t smem =
-        sizeof(double2) * (32 * (size_t)SST + (size_t)KC * XTP + 64) + sizeof(double) * (64 + 96 + 3 * p);
+        sizeof(double2) * (2 * 32 * (size_t)SST + (size_t)KC * XTP + 64) + sizeof(double) * (64 + 96 + 3 * p);
     if (smem > cap) return c;
     c.SST = SST; c.TT = TT; c.XTP = XTP; c.tb = tb; c.nd = nD; c.ntiles = ntiles;
     c.nchunks = (p + 31) / 32; c.mt = (TT / 8 + 7) / 8; c.smem = smem; c.KC = KC;

@@ -164,6 +164,11 @@ bem_status bem_solve_multifreq(bem_op op, const bem_c128* g_freq, bem_c128* phi_
  * (checks bit-identity with the independent oracle implementation). */
 bem_status bem_debug_pinned(const double* x, int64_t n, double* exp_out, double* sin_out, double* cos_out,
                             int32_t device);
+/* Hot-path (K1 / K3 slice regeneration) table-driven exp (x <= 0; 0 returned
+ * for x > 0) and sincos evaluated ON THE DEVICE for n host inputs: accuracy
+ * check of the fast math against libm (tests). */
+bem_status bem_debug_fastmath(const double* x, int64_t n, double* exp_out, double* sin_out, double* cos_out,
+                              int32_t device);
 /* FP64 DFMA throughput microbenchmark: returns achieved FLOP/s. */
 bem_status bem_debug_fp64_peak(int32_t device, void* cuda_stream, double* flops_per_s);
 /* mode 0: DFMA loop, 1: FP64 tensor-core mma.sync m8n8k4 loop, 2: both in one CTA. */

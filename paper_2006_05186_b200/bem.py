@@ -38,7 +38,7 @@ class SolveStats(C.Structure):
 EXPORTS = [
     "bem_last_error", "cqm_frequencies", "bem_build_tree", "bem_tree_get_stats", "bem_tree_export",
     "bem_tree_destroy", "bem_assemble_h2_aca", "bem_aca_export", "bem_op_destroy", "bem_apply_multifreq",
-    "cqm_forward", "cqm_inverse", "cqm_solve", "bem_solve_multifreq", "bem_debug_pinned", "bem_debug_fp64_peak",
+    "cqm_forward", "cqm_inverse", "cqm_solve", "bem_solve_multifreq", "bem_debug_pinned", "bem_debug_fastmath", "bem_debug_fp64_peak",
     "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count", "bem_debug_fp64_peak_ex",
 ]
 
@@ -68,6 +68,7 @@ def lib():
         "cqm_solve": [vp, vp, vp, i64, d, d, i32, i32, vp, vp, vp],
         "bem_solve_multifreq": [vp, vp, vp, d, i32, i32, vp, vp],
         "bem_debug_pinned": [vp, i64, vp, vp, vp, i32],
+        "bem_debug_fastmath": [vp, i64, vp, vp, vp, i32],
         "bem_debug_fp64_peak": [i32, vp, vp],
         "bem_op_set_profiling": [vp, i32],
         "bem_op_get_timings": [vp, vp],
@@ -267,6 +268,14 @@ def debug_pinned(x, device: int = 0):
     x = np.ascontiguousarray(x, dtype=np.float64).ravel()
     e, s, c = np.empty_like(x), np.empty_like(x), np.empty_like(x)
     _check(lib().bem_debug_pinned(_p(x), len(x), _p(e), _p(s), _p(c), int(device)))
+    return e, s, c
+
+
+def debug_fastmath(x, device: int = 0):
+    """Device table-driven exp (x <= 0) / sin / cos of the hot kernels, for accuracy tests."""
+    x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+    e, s, c = np.empty_like(x), np.empty_like(x), np.empty_like(x)
+    _check(lib().bem_debug_fastmath(_p(x), len(x), _p(e), _p(s), _p(c), int(device)))
     return e, s, c
 
 

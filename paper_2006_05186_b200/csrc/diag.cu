@@ -2,6 +2,7 @@
 // used by bench.py to state the measured FP64 ceiling beside the derived one
 // (MEASURED_PEAKS.json has no FP64 entry).
 #include "common.cuh"
+#include "fastmath.cuh"
 
 namespace bem {
 namespace {
@@ -116,5 +117,42 @@ extern "C" bem_status bem_debug_fp64_peak(int32_t device, void* cuda_stream, dou
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   *flops_per_s = 2.0 * 16.0 * (double)iters * blocks * 256.0 / (ms * 1e-3);
+  return BEM_OK;
+}
+
+// ---- hot-path math check: the table-driven exp / sincos of fastmath.cuh (K1, K3
+// slice regeneration) evaluated on the device for host inputs.
+namespace bem {
+namespace {
+__global__ void debug_fastmath_kernel(const double* x, int64_t n, double* e, double* sn, double* cs) {
+  __shared__ double et[64];
+  __shared__ double2 st[64];
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+    et[i] = fast::kExp2Tab[i];
+    st[i] = fast::kSinCosTab[i];
+  }
+  __syncthreads();
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  e[i] = x[i] <= 0.0 ? fast::exp_neg_tab(x[i], et) : 0.0;
+  fast::sincos_tab(x[i], st, &sn[i], &cs[i]);
+}
+}  // namespace
+}  // namespace bem
+
+extern "C" bem_status bem_debug_fastmath(const double* x, int64_t n, double* e, double* sn, double* cs,
+                                         int32_t device) {
+  using namespace bem;
+  BEM_REQ(x && e && sn && cs && n >= 0, "bem_debug_fastmath: bad arguments");
+  if (n == 0) return BEM_OK;
+  DeviceGuard dg(device);
+  DBuf<double> dx, de, ds, dc;
+  BEM_CK(dx.alloc(n)); BEM_CK(de.alloc(n)); BEM_CK(ds.alloc(n)); BEM_CK(dc.alloc(n));
+  BEM_CK(cudaMemcpy(dx.p, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+  debug_fastmath_kernel<<<(unsigned)((n + 255) / 256), 256>>>(dx.p, n, de.p, ds.p, dc.p);
+  BEM_CK(cudaGetLastError());
+  BEM_CK(cudaMemcpy(e, de.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  BEM_CK(cudaMemcpy(sn, ds.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  BEM_CK(cudaMemcpy(cs, dc.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
   return BEM_OK;
 }

@@ -71,27 +71,23 @@ __device__ __forceinline__ double exp_neg(double x) {
 // Table-driven variant: x = (64 k + j) ln2/64 + r, |r| <= ln2/128 (|x| < 1e13),
 // e^x = 2^k * T[j] * poly5(r), T[j] = 2^(j/64) (host-rounded, in shared
 // memory); truncation error r^6/720 < 4e-17.  Caller provides the table.
-// The magic constant places 8k (not k) in the low word of t (ulp 8 at
-// 1.5 * 2^55), so (lo(t) & 0x1f8) is directly the byte offset of T[k mod 64]
-// and the reduction constants carry the matching 1/8.
-static __constant__ double kET[4] = {8.0 * 92.332482616893656473,   // 8 * 64/ln2 (exact power-of-2 scaling)
-                                      54043195528445952.0,           // 1.5 * 2^55
-                                      -0x1.62e42ff000000p-7 / 8.0,   // -(ln2/64 high 32 bits) / 8 (kd8 * hi exact)
-                                      6.563929801064195e-13 / 8.0};  // (hi - ln2/64) / 8
+static __constant__ double kET[4] = {92.332482616893656473, 6755399441055744.0,  // 64/ln2, magic
+                                      -0x1.62e42ff000000p-7,                   // -ln2/64, high 32 bits (kd * hi exact)
+                                      6.563929801064195e-13};                  // ln2/64 low part (hi - ln2/64)
 
 __device__ __forceinline__ double exp_neg_tab(double x, const double* __restrict__ T) {
   const double t = fma(x, kET[0], kET[1]);
-  const double kd = t - kET[1];  // 8 k
+  const double kd = t - kET[1];
   double r = fma(kd, kET[2], x);
   r = fma(kd, kET[3], r);
   double p = kExpT[0];
 #pragma unroll
   for (int i = 1; i < 6; ++i) p = fma(p, r, kExpT[i]);
   const int ki = __double2loint(t);
-  p *= *(const double*)((const char*)T + (ki & 0x1f8));
+  p *= T[ki & 63];
   // exponent clamp in the integer pipe: x < -707 returns ~1e-307 instead of 0
   // (negligible) without an FP64 fmax
-  return __hiloint2double(__double2hiint(p) + (max(ki >> 9, -1020) << 20), __double2loint(p));
+  return __hiloint2double(__double2hiint(p) + (max(ki >> 6, -1020) << 20), __double2loint(p));
 }
 
 __device__ __forceinline__ void sincos_(double th, double* sn, double* cs) {
@@ -162,24 +158,21 @@ static __constant__ double2 kSinCosTab[64] = {
 
 // constant-bank operands (DFMA takes c[][] directly; immediates would be
 // rematerialised through uniform registers every iteration)
-// 16k in the low word of t (ulp 16 at 1.5 * 2^56): (lo(t) & 0x3f0) is the
-// byte offset of the 16-byte (cos, sin) entry; reduction constants carry 1/16.
 static __constant__ double kSCT[12] = {
-    16.0 * 10.185916357881301489, 108086391056891904.0,              // 16 * 32/pi, 1.5 * 2^56
-    -0x1.921fb54400000p-4 / 16.0, -0x1.0b4611a626331p-38 / 16.0,     // -(pi/32 hi, lo) / 16
+    10.185916357881301489, 6755399441055744.0, -0x1.921fb54400000p-4, -0x1.0b4611a626331p-38,  // 32/pi, magic, -pi/32 hi, lo
     -1.98412698412698412698e-04, 8.33333333333333333333e-03, -1.66666666666666666667e-01,      // sin r^7, r^5, r^3
     2.48015873015873015873e-05, -1.38888888888888888889e-03, 4.16666666666666666667e-02, -0.5, 1.0};  // cos
 
 __device__ __forceinline__ void sincos_tab(double th, const double2* __restrict__ T, double* sn, double* cs) {
   const double t = fma(th, kSCT[0], kSCT[1]);
-  const double kd = t - kSCT[1];  // 16 k
+  const double kd = t - kSCT[1];
   double r = fma(kd, kSCT[2], th);
   r = fma(kd, kSCT[3], r);
   const double z = r * r;
   const double ps = fma(z, fma(z, kSCT[4], kSCT[5]), kSCT[6]);
   const double sr = fma(r * z, ps, r);
   const double cr = fma(z, fma(z, fma(z, fma(z, kSCT[7], kSCT[8]), kSCT[9]), kSCT[10]), kSCT[11]);
-  const double2 cs_k = *(const double2*)((const char*)T + (__double2loint(t) & 0x3f0));
+  const double2 cs_k = T[__double2loint(t) & 63];
   *sn = fma(cs_k.y, cr, cs_k.x * sr);
   *cs = fma(cs_k.x, cr, -(cs_k.y * sr));
 }

@@ -375,3 +375,18 @@ def test_solve_mask_bitwise_identical(pb, torch, monkeypatch):
     assert out[0][1]["iters_sum"] == out[1][1]["iters_sum"] and out[0][1]["n_unconverged"] == 0
     assert out[0][1]["resid_max"] == out[1][1]["resid_max"]
     assert np.array_equal(out[0][0], out[1][0])
+
+
+def test_hot_path_fastmath_accuracy(pb):
+    """Table-driven exp / sincos of K1 and K3 (fastmath.cuh) against libm over the
+    configs' argument ranges: exp within 2 ulp for x in [-700, 0]; sin/cos
+    within 2.5e-16 absolute for |theta| <= 6.5e3."""
+    rng = np.random.default_rng(11)
+    x = np.concatenate([-rng.random(200000) * 700.0, [0.0, -1e-300, -0.5 * np.log(2) / 64]])
+    e, _, _ = pb.debug_fastmath(x)
+    ref = np.exp(x)
+    assert np.max(np.abs(e - ref) / np.spacing(ref)) <= 2.0
+    t = np.concatenate([(rng.random(300000) - 0.5) * 13000.0, [0.0, np.pi / 64, np.pi / 2, -np.pi]])
+    _, s, c = pb.debug_fastmath(t)
+    assert np.max(np.abs(s - np.sin(t))) <= 2.5e-16
+    assert np.max(np.abs(c - np.cos(t))) <= 2.5e-16

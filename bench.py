@@ -321,8 +321,8 @@ def main():
     if mode == pb.BEM_MODE_H2ACA:
         rk = op.aca_export()["ranks"]
         flops_far = 8.0 * float(rk.sum()) * stats["p"] ** 2 * nl
-    else:
-        flops_far = 8.0 * stats["far_blocks"] * stats["p"] ** 2 * nl
+    else:  # plain H^2: one kernel evaluation per (block entry, frequency class) + the complex MACs
+        flops_far = 75.0 * stats["far_blocks"] * stats["p"] ** 2 * n_class + 8.0 * stats["far_blocks"] * stats["p"] ** 2 * nl
     evals_near = 7.0 * stats["nnz_near"] * n_class
     flops_near = 75.0 * evals_near  # SURVEY §8(d) model: ~75 FP64 flops per complex exponential + MACs
     peaks = {}
@@ -332,7 +332,11 @@ def main():
         except Exception:
             peaks[name] = None
     dom = "coupling" if kt["coupling"] >= kt["near"] else "near"
-    if dom == "coupling":
+    if dom == "coupling" and mode != pb.BEM_MODE_H2ACA:
+        fl = flops_far
+        peak = FP64_PEAK_DERIVED / 1e12
+        bound, src = "alu", "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §7); 75 flops/evaluation model"
+    elif dom == "coupling":
         fl = flops_far
         peak = peaks["dmma"] or FP64_PEAK_DERIVED / 1e12
         bound, src = "tensor", ("measured in this run: mma.sync.m8n8k4.f64 (DMMA) loop on this GPU "
@@ -342,7 +346,8 @@ def main():
         peak = FP64_PEAK_DERIVED / 1e12
         bound, src = "alu", "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §7)"
     achieved = fl / (kt[dom] * 1e-3) / 1e12
-    kname = {"coupling": "K3 far7_kernel (+seg_reduce)", "near": "K1 near_kernel"}[dom]
+    kname = {"coupling": ("K3 far7/far8_kernel (+seg_reduce)" if mode == pb.BEM_MODE_H2ACA
+                          else "K3' h2o_kernel (+seg_reduce)"), "near": "K1 near_kernel"}[dom]
     roof = {"bound": bound, "kernel": kname, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": traffic_bytes(args.config, dom), "peak_source": src,
             "algorithmic_flops_per_launch": fl,

@@ -537,12 +537,14 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
       set_error("bem_assemble_h2_aca: upload failed");
       return fail(BEM_ECUDA);
     }
-    if (mode == BEM_MODE_H2ACA) {
+    {
       // split rows into block-range segments of bounded cost (load balance of K3)
       int nsm = 148;
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, t.device);
+      // block weight: ACA rank (H2ACA: r_b slice products) or 1 (H2ONLY: one p x p evaluation per frequency)
+      auto wgt = [&](int b) -> int64_t { return mode == BEM_MODE_H2ACA ? op.ranks[b] : 1; };
       int64_t total = 0;
-      for (int b = 0; b < (int)t.far_r.size(); ++b) total += op.ranks[b];
+      for (int b = 0; b < (int)t.far_r.size(); ++b) total += wgt(b);
       int64_t cap = std::max<int64_t>(1, total / (8 * (int64_t)nsm));  // ~8 segments per SM (r01: config 2 K3 9.02 -> 8.77 ms vs 4 per SM)
       if (const char* e = getenv("BEM_SEG_CAP")) cap = std::max<int64_t>(1, atoll(e));
       struct Seg { int64_t cost; int row, bi0, bi1, slot; };
@@ -554,7 +556,7 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
         int start = b0;
         int64_t acc = 0;
         for (int bi = b0; bi < b1; ++bi) {
-          const int64_t w = op.ranks[t.far_sorted[bi]];
+          const int64_t w = wgt(t.far_sorted[bi]);
           if (acc > 0 && acc + w > cap) {
             segs.push_back({acc, c, start, bi, (int)segs.size()});
             start = bi;

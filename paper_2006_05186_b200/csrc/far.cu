@@ -1176,6 +1176,161 @@ cudaError_t dispatch8(const Far8Cfg& c, int p, bool rem_dfma, int nseg, const Fa
   return c.mt == 1 ? launch8<1, 4, 0>(c, nseg, a, st) : launch8<2, 4, 0>(c, nseg, a, st);
 }
 
+// ------------------------------- h2o: plain-H^2 coupling evaluated on the fly
+// BEM_MODE_H2ONLY (the paper's "plain H^2-matrix"
+// comparison): no ACA, the coupling matrix of every far block is
+// evaluated per frequency from the kernel,
+//   yhat_r(l) += S_b(s_l) xhat_c(l),   S_b(s_l)[mu,nu] = k(|xi_{c,nu} - xi_{r,mu}|; s_l),
+// with one exp/sincos shared by the conjugate pair (l, L-l):
+// S_b(conj s) = conj S_b(s).  CTA = (segment of a row's far blocks, tile of
+// FC frequency classes); warp w takes blocks w, w+8, ... of the segment;
+// lane owns rows mu = lane + 32 u; per (mu, nu) the distance and 1/(4 pi r)
+// are computed once for all FC classes.  Warps' partial yhat are summed in a
+// fixed order through shared memory (deterministic, no atomics).
+struct H2oArgs {
+  int nl, m, p, n_class, FCs;
+  const int4* segs;
+  const int32_t* far_sorted;
+  const int32_t* far_c;
+  const double* xi;
+  const double2* s;
+  const int32_t* local_l;
+  const int32_t* class_t1;
+  const int32_t* class_t2;
+  const double2* xhat;
+  double2* part;
+  const int32_t* mask;
+};
+
+constexpr int kH2oWarps = 4;
+
+template <int U, int FC>
+__global__ void __launch_bounds__(kH2oWarps * 32, 3) h2o_kernel(H2oArgs a) {
+  extern __shared__ double2 sm[];
+  const int p = a.p, m = a.m;
+  const int4 sg = a.segs[blockIdx.x];
+  const int r = sg.x;
+  const int c0 = blockIdx.y * FC;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double2* sctab = sm;                                  // 64
+  double* etab = (double*)(sctab + 64);                 // 64
+  double2* xw = (double2*)(etab + 64) + (size_t)warp * 2 * FC * p;  // per warp: [2 FC][p] xhat of its block
+  double* cw = (double*)((double2*)(etab + 64) + (size_t)kH2oWarps * 2 * FC * p) + (size_t)warp * 3 * p;  // per warp nodes
+  double2* red = (double2*)((double*)((double2*)(etab + 64) + (size_t)kH2oWarps * 2 * FC * p) + (size_t)kH2oWarps * 3 * p);
+  for (int i = tid; i < 64; i += blockDim.x) {
+    etab[i] = fast::kExp2Tab[i];
+    sctab[i] = fast::kSinCosTab[i];
+  }
+  int t1[FC], t2[FC];
+  double sre[FC], sim[FC];
+#pragma unroll
+  for (int f = 0; f < FC; ++f) {
+    const int c = c0 + f;
+    t1[f] = c < a.n_class ? a.class_t1[c] : -1;
+    t2[f] = c < a.n_class ? a.class_t2[c] : -1;
+    if (t1[f] >= 0 && a.mask != nullptr && !a.mask[t1[f]] && (t2[f] < 0 || !a.mask[t2[f]])) t1[f] = t2[f] = -1;
+    const double2 sv = t1[f] >= 0 ? a.s[a.local_l[t1[f]]] : make_double2(0.0, 0.0);
+    sre[f] = sv.x;
+    sim[f] = sv.y;
+  }
+  double xr[U][3];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int mu = lane + 32 * u;
+    node(a.xi + (int64_t)r * 3 * m, m, mu < p ? mu : 0, xr[u]);
+  }
+  double2 y1[FC][U], y2[FC][U];
+#pragma unroll
+  for (int f = 0; f < FC; ++f)
+#pragma unroll
+    for (int u = 0; u < U; ++u) y1[f][u] = y2[f][u] = make_double2(0.0, 0.0);
+  bool any = false;
+#pragma unroll
+  for (int f = 0; f < FC; ++f) any |= t1[f] >= 0;
+  __syncthreads();
+  for (int bi = sg.y + warp; bi < (any ? sg.z : sg.y); bi += kH2oWarps) {
+    const int b = a.far_sorted[bi];
+    const int c = a.far_c[b];
+    const double2* xh = a.xhat + (int64_t)c * a.nl * p;
+    __syncwarp();
+    for (int i = lane; i < p; i += 32) node(a.xi + (int64_t)c * 3 * m, m, i, cw + 3 * i);
+    for (int i = lane; i < FC * p; i += 32) {
+      const int f = i / p, nu = i - f * p;
+      xw[(2 * f) * p + nu] = t1[f] >= 0 ? xh[(int64_t)t1[f] * p + nu] : make_double2(0.0, 0.0);
+      xw[(2 * f + 1) * p + nu] = t2[f] >= 0 ? xh[(int64_t)t2[f] * p + nu] : make_double2(0.0, 0.0);
+    }
+    __syncwarp();
+    for (int nu = 0; nu < p; ++nu) {
+      const double cx = cw[3 * nu], cy = cw[3 * nu + 1], cz = cw[3 * nu + 2];
+      double2 x1[FC], x2[FC];
+#pragma unroll
+      for (int f = 0; f < FC; ++f) {
+        x1[f] = xw[(2 * f) * p + nu];
+        x2[f] = xw[(2 * f + 1) * p + nu];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double dx = cx - xr[u][0], dy = cy - xr[u][1], dz = cz - xr[u][2];
+        const double d2 = dx * dx + dy * dy + dz * dz;
+        const double ir = rsqrt(d2);
+        const double rr = d2 * ir;
+        const double w = ir * 0.079577471545947667884;  // 1/(4 pi r)
+#pragma unroll
+        for (int f = 0; f < FC; ++f) {
+          const double e = fast::exp_neg_tab(-sre[f] * rr, etab) * w;
+          double sn, cs;
+          fast::sincos_tab(sim[f] * rr, sctab, &sn, &cs);
+          const double kr = e * cs, ki = -e * sn;  // S(s) = kr + i ki; S(conj s) = kr - i ki
+          y1[f][u].x = fma(kr, x1[f].x, fma(-ki, x1[f].y, y1[f][u].x));
+          y1[f][u].y = fma(kr, x1[f].y, fma(ki, x1[f].x, y1[f][u].y));
+          y2[f][u].x = fma(kr, x2[f].x, fma(ki, x2[f].y, y2[f][u].x));
+          y2[f][u].y = fma(kr, x2[f].y, fma(-ki, x2[f].x, y2[f][u].y));
+        }
+      }
+    }
+  }
+  // fixed-order reduction over the warps: red[w][2 FC][U*32]
+  const int R = 2 * FC * U * 32;
+#pragma unroll
+  for (int f = 0; f < FC; ++f)
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      red[(size_t)warp * R + ((2 * f) * U + u) * 32 + lane] = y1[f][u];
+      red[(size_t)warp * R + ((2 * f + 1) * U + u) * 32 + lane] = y2[f][u];
+    }
+  __syncthreads();
+  double2* out = a.part + (int64_t)sg.w * a.nl * p;
+  for (int i = tid; i < R; i += blockDim.x) {
+    double2 v = red[i];
+    for (int w2 = 1; w2 < kH2oWarps; ++w2) {
+      const double2 q2 = red[(size_t)w2 * R + i];
+      v.x += q2.x;
+      v.y += q2.y;
+    }
+    const int lane2 = i & 31, rest = i >> 5;
+    const int u = rest % U, fh = rest / U;
+    const int f = fh >> 1, half = fh & 1;
+    const int mu = lane2 + 32 * u;
+    const int t = half ? t2[f] : t1[f];
+    const int c = c0 + f;
+    if (mu < p && c < a.n_class) {
+      const int tt = half ? a.class_t2[c] : a.class_t1[c];  // masked classes still write (zeros)
+      if (tt >= 0) out[(int64_t)tt * p + mu] = t >= 0 ? v : make_double2(0.0, 0.0);
+    }
+  }
+}
+
+template <int U, int FC>
+cudaError_t launch_h2o(const H2oArgs& a, int nseg, int ntile, cudaStream_t st) {
+  const size_t smem = sizeof(double2) * 64 + sizeof(double) * 64 + sizeof(double2) * kH2oWarps * 2 * FC * (size_t)a.p +
+                      sizeof(double) * kH2oWarps * 3 * (size_t)a.p + sizeof(double2) * kH2oWarps * 2 * FC * U * 32;
+  auto k = h2o_kernel<U, FC>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<dim3((unsigned)nseg, (unsigned)ntile), kH2oWarps * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 // yhat[r] = sum over the row's segments (fixed order)
 __global__ void seg_reduce_kernel(const int32_t* __restrict__ rows, const int32_t* __restrict__ seg_ptr,
                                   const double2* __restrict__ part, double2* __restrict__ yhat, int64_t tile) {
@@ -1294,6 +1449,29 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
   Tree& t = *op.tree;
   const int nl = op.n_local, p = t.p;
   const int fk = op.far_kernel != 0 ? op.far_kernel : (p > 32 ? 8 : 7);  // r01: far8 wins at p = 64, far7 at p = 27
+  if (op.mode == BEM_MODE_H2ONLY && !op.force_generic && op.n_segs > 0 && p <= 128) {
+    BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
+    H2oArgs a;
+    a.nl = nl; a.m = t.m; a.p = p; a.n_class = op.n_class;
+    a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
+    a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.local_l = op.d_local_l.p;
+    a.class_t1 = op.d_class_t1.p; a.class_t2 = op.d_class_t2.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
+    a.mask = op.d_mask;
+    const int U = (p + 31) / 32;
+    const int FC = p <= 32 ? 4 : 2;
+    a.FCs = FC;
+    const int ntile = (op.n_class + FC - 1) / FC;
+    cudaError_t e;
+    if (U == 1) e = launch_h2o<1, 4>(a, op.n_segs, ntile, st);
+    else if (U == 2) e = launch_h2o<2, 2>(a, op.n_segs, ntile, st);
+    else if (U == 3) e = launch_h2o<3, 2>(a, op.n_segs, ntile, st);
+    else e = launch_h2o<4, 2>(a, op.n_segs, ntile, st);
+    BEM_CK(e);
+    seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
+                                                     yhat, (int64_t)nl * p);
+    BEM_CK(cudaGetLastError());
+    return BEM_OK;
+  }
   if (op.mode == BEM_MODE_H2ACA && fk == 8 && !op.force_generic && op.n_segs > 0) {
     const Far8Cfg f8 = choose8(p, nl, op.far4_smem_cap, op.far8_kc);
     if (f8.mt > 0) {

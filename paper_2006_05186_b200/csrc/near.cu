@@ -123,20 +123,9 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
   const double cx = a.cen[3 * k], cy = a.cen[3 * k + 1], cz = a.cen[3 * k + 2];
   const int li = a.leaf_of[k];
   const int jb = a.near_jb[li], je = a.near_je[li];
-  int jn = jb + lane < je ? a.near_j[jb + lane] : 0;
   for (int jj = jb + lane; jj < je; jj += 32) {
     {
-      const int j = jn;
-      // software prefetch (L1) of the next source panel's nodes and weights:
-      // their latency was exposed at node 0 (long-scoreboard stalls, r01 ncu)
-      jn = jj + 32 < je ? a.near_j[jj + 32] : j;
-      {
-        const char* pn = (const char*)(a.qn + 21 * (int64_t)jn);
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(pn));  // 168 B: up to three 128 B lines
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(pn + 84));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(pn + 167));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.qw + 7 * (int64_t)jn));
-      }
+      const int j = a.near_j[jj];
       if (j == k) continue;  // self panel below
       double2 x1[F], x2[F];
 #pragma unroll

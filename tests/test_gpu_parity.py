@@ -390,3 +390,20 @@ def test_hot_path_fastmath_accuracy(pb):
     _, s, c = pb.debug_fastmath(t)
     assert np.max(np.abs(s - np.sin(t))) <= 2.5e-16
     assert np.max(np.abs(c - np.cos(t))) <= 2.5e-16
+
+
+@pytest.mark.parametrize("m,leaf,N", [(3, 32, 128), (4, 48, 64), (5, 64, 32)])
+def test_h2only_on_the_fly_couplings(pb, torch, m, leaf, N):
+    """BEM_MODE_H2ONLY (plain H^2, couplings evaluated per frequency on the fly;
+    SURVEY §8(f) NEXT-3) vs the oracle's H2ONLY on a frequency sample, p = 27/64/125."""
+    V, T = synth.icosphere(3)
+    M, L = len(T), N + 1
+    s = pb.cqm_frequencies(N, 2.0)
+    x = synth.random_density(6, L, M)
+    tree = pb.Tree(V, T, leaf, 1.0, m)
+    op = pb.Operator(tree, s, 1e-6, mode=pb.BEM_MODE_H2ONLY)
+    y = _apply(pb, torch, op, x)
+    oh = O.H2(V, T, leaf, 1.0, m)
+    lsel = np.unique(np.r_[0, 1, N // 2, N // 2 + 1, N - 1, N])
+    yo = oh.apply(O.MODE_H2ONLY, s, x[lsel], lsel)
+    assert _rel(y[lsel], yo) <= 1e-10

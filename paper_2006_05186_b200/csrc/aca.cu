@@ -387,8 +387,19 @@ bem_status run_aca(Op& op, cudaStream_t st) {
   const int p = t.p, pp = p * p, L = op.L;
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, t.device);
-  int rcap = std::min(std::min(L, pp), 96);
-  unsigned long long cap = (unsigned long long)nfar * 40ull * (unsigned long long)op.n_local;
+  // scratch rank cap and Z-pool size: generous first guesses (a retry recomputes the
+  // whole ACA: config 5 hit both the old 96 rank cap and the 40-per-block pool
+  // estimate), the pool is shrunk to its exact size afterwards
+  int rcap = std::min(std::min(L, pp), 128);
+  unsigned long long cap = (unsigned long long)nfar * 64ull * (unsigned long long)op.n_local;
+  {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+      const size_t scratch = (size_t)std::max(1, std::min(nfar, nsm * 4)) * rcap * ((size_t)pp + L) * 16;
+      const unsigned long long lim = fr > scratch ? (unsigned long long)((fr - scratch) * 0.7 / 16) : 0ull;
+      if (lim > 0 && cap > lim) cap = lim;
+    }
+  }
   DBuf<int32_t> flags, counter;
   DBuf<unsigned long long> used;
   BEM_CK(flags.alloc(1));
@@ -437,6 +448,13 @@ bem_status run_aca(Op& op, cudaStream_t st) {
     }
     op.rcap = rcap;
     BEM_CK(cudaMemcpy(op.ranks.data(), op.d_rank.p, sizeof(int32_t) * nfar, cudaMemcpyDeviceToHost));
+    if (hused < cap && (cap - hused) * 16ull > (64ull << 20)) {  // shrink the Z pool to its exact size
+      DBuf<double> z;
+      BEM_CK(z.alloc((size_t)std::max<unsigned long long>(hused, 1) * 2));
+      BEM_CK(cudaMemcpyAsync(z.p, op.d_Z.p, (size_t)hused * 16, cudaMemcpyDeviceToDevice, st));
+      BEM_CK(cudaStreamSynchronize(st));
+      op.d_Z = std::move(z);
+    }
     return BEM_OK;
   }
   set_error("bem_assemble_h2_aca: ACA did not fit after repeated growth");
@@ -546,6 +564,10 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
       int64_t total = 0;
       for (int b = 0; b < (int)t.far_r.size(); ++b) total += wgt(b);
       int64_t cap = std::max<int64_t>(1, total / (8 * (int64_t)nsm));  // ~8 segments per SM (r01: config 2 K3 9.02 -> 8.77 ms vs 4 per SM)
+      // H2ONLY: the CTA's 4 warps take every 4th block of a segment, so keep >= 16 blocks
+      // per segment (<= 25% warp imbalance at the end-of-CTA barrier); the class tiles
+      // already give many CTAs
+      if (mode != BEM_MODE_H2ACA) cap = std::max<int64_t>(cap, std::max<int64_t>(16, total / (2 * (int64_t)nsm)));
       if (const char* e = getenv("BEM_SEG_CAP")) cap = std::max<int64_t>(1, atoll(e));
       struct Seg { int64_t cost; int row, bi0, bi1, slot; };
       std::vector<Seg> segs;

@@ -96,7 +96,6 @@ struct Tree {
   DBuf<double> d_cen;    // M*3
   DBuf<double> d_qn;     // M*21 quadrature nodes
   DBuf<double> d_qw;     // M*7  w_q * |T_j| / (4 pi)
-  DBuf<double> d_qnw;    // M*28 packed (x, y, z, w) per node (K1 source record)
   DBuf<double> d_selfJ;  // M    J(T)/(4 pi)
   DBuf<double> d_area;   // M
   DBuf<double> d_U, d_W; // M*p

@@ -405,15 +405,7 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
   } while (0)
   UP(d_perm, t.perm); UP(d_begin, t.begin); UP(d_end, t.end); UP(d_son0, t.son0); UP(d_son1, t.son1);
   UP(d_parent, t.parent); UP(d_leaf_of, leaf_of);
-  // packed near-field source record per panel: 7 x (x, y, z, w_q |T| / 4pi) = 224 B,
-  // 16-byte aligned, so K1 reads a node with two 16-byte vector loads
-  std::vector<double> qnw((size_t)t.M * 28);
-  for (int64_t j = 0; j < t.M; ++j)
-    for (int q = 0; q < 7; ++q) {
-      for (int d = 0; d < 3; ++d) qnw[(size_t)j * 28 + 4 * q + d] = qn[(size_t)j * 21 + 3 * q + d];
-      qnw[(size_t)j * 28 + 4 * q + 3] = qw[(size_t)j * 7 + q];
-    }
-  UP(d_cen, cen); UP(d_qn, qn); UP(d_qw, qw); UP(d_qnw, qnw); UP(d_selfJ, sj); UP(d_area, area);
+  UP(d_cen, cen); UP(d_qn, qn); UP(d_qw, qw); UP(d_selfJ, sj); UP(d_area, area);
   UP(d_U, U); UP(d_W, W); UP(d_E, E); UP(d_xi, t.xi); UP(d_leaves, t.leaves);
   UP(d_near_jb, njb); UP(d_near_je, nje); UP(d_near_j, nj);
   UP(d_far_ptr, t.far_ptr); UP(d_far_sorted, t.far_sorted); UP(d_far_r, t.far_r); UP(d_far_c, t.far_c);

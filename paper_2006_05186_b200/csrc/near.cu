@@ -32,7 +32,6 @@ struct NearArgs {
   const double* cen;
   const double* qn;
   const double* qw;
-  const double4* qnw;  // packed source record: 7 x (x, y, z, w) per panel
   const double* selfJ;
   const double2* s;
   const int32_t* local_l;
@@ -124,9 +123,11 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
   const double cx = a.cen[3 * k], cy = a.cen[3 * k + 1], cz = a.cen[3 * k + 2];
   const int li = a.leaf_of[k];
   const int jb = a.near_jb[li], je = a.near_je[li];
+  int jn = jb + lane < je ? a.near_j[jb + lane] : 0;
   for (int jj = jb + lane; jj < je; jj += 32) {
     {
-      const int j = a.near_j[jj];
+      const int j = jn;  // index loaded one iteration ahead (one dependent global load fewer per source)
+      if (jj + 32 < je) jn = a.near_j[jj + 32];
       if (j == k) continue;  // self panel below
       double2 x1[F], x2[F];
 #pragma unroll
@@ -137,15 +138,15 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
       double2 v[F];
 #pragma unroll
       for (int f = 0; f < F; ++f) v[f] = make_double2(0.0, 0.0);
-      const double4* qnw = a.qnw + 7 * (int64_t)j;
+      const double* qn = a.qn + 21 * (int64_t)j;
+      const double* qw = a.qw + 7 * (int64_t)j;
 #pragma unroll U
       for (int q = 0; q < 7; ++q) {
-        const double4 nd = qnw[q];
-        const double dx = cx - nd.x, dy = cy - nd.y, dz = cz - nd.z;
+        const double dx = cx - qn[3 * q], dy = cy - qn[3 * q + 1], dz = cz - qn[3 * q + 2];
         const double d2 = dx * dx + dy * dy + dz * dz;
         const double ir = rsqrt(d2);
         const double r = d2 * ir;
-        const double w = nd.w * ir;
+        const double w = qw[q] * ir;
 #pragma unroll
         for (int f = 0; f < F; ++f) {
           const double e = (TAB ? fast::exp_neg_tab(-sre[f] * r, etab) : fast::exp_neg(-sre[f] * r)) * w;
@@ -218,7 +219,7 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st) 
   na.near_jb = dense ? op.d_dn_jb.p : t.d_near_jb.p;
   na.near_je = dense ? op.d_dn_je.p : t.d_near_je.p;
   na.near_j = dense ? op.d_dn_j.p : t.d_near_j.p;
-  na.cen = t.d_cen.p; na.qn = t.d_qn.p; na.qw = t.d_qw.p; na.qnw = (const double4*)t.d_qnw.p; na.selfJ = t.d_selfJ.p;
+  na.cen = t.d_cen.p; na.qn = t.d_qn.p; na.qw = t.d_qw.p; na.selfJ = t.d_selfJ.p;
   na.s = (const double2*)op.d_s.p; na.local_l = op.d_local_l.p;
   na.class_t1 = op.d_class_t1.p; na.class_t2 = op.d_class_t2.p; na.mask = op.d_mask; na.xc = xc; na.yc = yc;
   const int F = op.near_f;

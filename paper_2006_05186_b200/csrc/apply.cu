@@ -93,12 +93,13 @@ __global__ void __launch_bounds__(kPassThreads) down_transfer_kernel(const int32
     const int t = t0 + rem / p, lam = rem % p;
     if (t >= nl) continue;
     const int sc = sidx ? son1[c] : son0[c];
-    const double* Es = E + (int64_t)sc * p * p + (int64_t)lam * p;
+    const double* Es = E + (int64_t)sc * p * p + lam;  // E^T[sc][mu][lam]: coalesced over lam
     const double2* yp = yhat + ((int64_t)c * nl + t) * p;
     double2 acc = yhat[((int64_t)sc * nl + t) * p + lam];
     for (int mu = 0; mu < p; ++mu) {
-      acc.x = fma(Es[mu], yp[mu].x, acc.x);
-      acc.y = fma(Es[mu], yp[mu].y, acc.y);
+      const double e = Es[(int64_t)mu * p];
+      acc.x = fma(e, yp[mu].x, acc.x);
+      acc.y = fma(e, yp[mu].y, acc.y);
     }
     yhat[((int64_t)sc * nl + t) * p + lam] = acc;
   }
@@ -122,10 +123,11 @@ __global__ void __launch_bounds__(kPassThreads) down_leaf_kernel(const int32_t* 
     double2 acc = yc[(int64_t)t * M + k];
     if (has_far) {
       const double2* yh = yhat + ((int64_t)c * nl + t) * p;
-      const double* Uk = U + (int64_t)k * p;
+      const double* Uk = U + k;  // U^T[mu][k]: coalesced over k
       for (int mu = 0; mu < p; ++mu) {
-        acc.x = fma(Uk[mu], yh[mu].x, acc.x);
-        acc.y = fma(Uk[mu], yh[mu].y, acc.y);
+        const double u = Uk[(int64_t)mu * M];
+        acc.x = fma(u, yh[mu].x, acc.x);
+        acc.y = fma(u, yh[mu].y, acc.y);
       }
     }
     y[(int64_t)t * M + perm[k]] = acc;
@@ -189,11 +191,11 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
       const int n = (int)t.level_nonleaf[lv].size();
       if (n == 0) continue;
       down_transfer_kernel<<<dim3((unsigned)n, tt), kPassThreads, 0, st>>>(t.d_level_nonleaf[lv].p, t.d_son0.p,
-                                                                           t.d_son1.p, t.d_E.p, yhat, nl, p);
+                                                                           t.d_son1.p, t.d_ET.p, yhat, nl, p);
       BEM_CK(cudaGetLastError());
     }
     down_leaf_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, 0, st>>>(
-        t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_U.p, yhat, yc, t.d_perm.p, y, M, nl, p, 1);
+        t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_UT.p, yhat, yc, t.d_perm.p, y, M, nl, p, 1);
     BEM_CK(cudaGetLastError());
   } else {
     if (prof) { BEM_CK(cudaEventRecord(op.ev[2], st)); BEM_CK(cudaEventRecord(op.ev[3], st)); }

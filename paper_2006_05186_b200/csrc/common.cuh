@@ -100,6 +100,7 @@ struct Tree {
   DBuf<double> d_area;   // M
   DBuf<double> d_U, d_W; // M*p
   DBuf<double> d_E;      // C*p*p (E of cluster c w.r.t. its parent)
+  DBuf<double> d_ET, d_UT;  // transposed E (C*p*p) and U (p*M) for the downward pass
   DBuf<double> d_xi;     // C*3*m
   DBuf<int32_t> d_leaves;
   // near field per leaf index: [jb, je) into the flat list of near source panels
@@ -142,6 +143,7 @@ struct Op {
   int near_f = 3;  // frequency classes per warp (r01 sweep at config 2: F=2 7.77 ms, F=3 6.97 ms, F=4 9.85 ms)
   int near_unroll = 7;
   bool near_tab = true;
+  bool near_lean = false;  // K1 variant: x loads after the node loop, 128 registers (env BEM_NEAR_LEAN)
   int near_minb = 0;  // K1 __launch_bounds__ min blocks/SM variant (0: compiler's choice; 6, 8)
   bool force_generic = false;
   int far_kernel = 0;                 // 0: auto (far8 for p > 32, far7 otherwise); 8, 7, 6 (DMMA variants), 4, 3

@@ -406,7 +406,18 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
   UP(d_perm, t.perm); UP(d_begin, t.begin); UP(d_end, t.end); UP(d_son0, t.son0); UP(d_son1, t.son1);
   UP(d_parent, t.parent); UP(d_leaf_of, leaf_of);
   UP(d_cen, cen); UP(d_qn, qn); UP(d_qw, qw); UP(d_selfJ, sj); UP(d_area, area);
-  UP(d_U, U); UP(d_W, W); UP(d_E, E); UP(d_xi, t.xi); UP(d_leaves, t.leaves);
+  // transposed copies for the downward pass (K2): lanes run over lambda / panel k, so
+  // E^T[c][mu][lambda] and U^T[mu][k] make its loads coalesced
+  std::vector<double> ET(E.size()), UT(U.size());
+  {
+    const size_t pp = (size_t)t.p * t.p;
+    for (size_t c = 0; c < E.size() / pp; ++c)
+      for (int l = 0; l < t.p; ++l)
+        for (int mu = 0; mu < t.p; ++mu) ET[c * pp + (size_t)mu * t.p + l] = E[c * pp + (size_t)l * t.p + mu];
+    for (int64_t k = 0; k < t.M; ++k)
+      for (int mu = 0; mu < t.p; ++mu) UT[(size_t)mu * t.M + k] = U[(size_t)k * t.p + mu];
+  }
+  UP(d_U, U); UP(d_W, W); UP(d_E, E); UP(d_ET, ET); UP(d_UT, UT); UP(d_xi, t.xi); UP(d_leaves, t.leaves);
   UP(d_near_jb, njb); UP(d_near_je, nje); UP(d_near_j, nj);
   UP(d_far_ptr, t.far_ptr); UP(d_far_sorted, t.far_sorted); UP(d_far_r, t.far_r); UP(d_far_c, t.far_c);
   t.d_level_nonleaf.resize(t.depth + 1);

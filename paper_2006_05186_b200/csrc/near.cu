@@ -74,7 +74,7 @@ __device__ __noinline__ double2 self_entry(const double* qn, const double* qw, d
   return make_double2(vr, vi);
 }
 
-template <int F, int U, bool TAB>
+template <int F, int U, bool TAB, bool LEAN = false>
 __device__ __forceinline__ void near_body(const NearArgs& a) {
   __shared__ double etab[64];
   __shared__ double2 sctab[64];
@@ -130,10 +130,12 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
       if (jj + 32 < je) jn = a.near_j[jj + 32];
       if (j == k) continue;  // self panel below
       double2 x1[F], x2[F];
+      if (!LEAN) {  // loads issued before the node loop (latency hidden, 4F registers live through it)
 #pragma unroll
-      for (int f = 0; f < F; ++f) {
-        x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
-        x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
+        for (int f = 0; f < F; ++f) {
+          x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
+          x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
+        }
       }
       double2 v[F];
 #pragma unroll
@@ -155,6 +157,13 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
           else fast::sincos_(sim[f] * r, &sn, &cs);
           v[f].x = fma(e, cs, v[f].x);
           v[f].y = fma(-e, sn, v[f].y);
+        }
+      }
+      if (LEAN) {  // loads after the node loop: fewer live registers, latency covered by other warps
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
+          x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
         }
       }
 #pragma unroll
@@ -200,6 +209,11 @@ template <int F, int U, bool TAB, int MINB>
 __global__ void __launch_bounds__(kNearWarps * 32, MINB) near_kernel_minb(NearArgs a) {
   near_body<F, U, TAB>(a);
 }
+// lean variant (x loads after the node loop) at 4 CTAs/SM (128 registers)
+template <int F>
+__global__ void __launch_bounds__(kNearWarps * 32, 4) near_kernel_lean(NearArgs a) {
+  near_body<F, 7, true, true>(a);
+}
 
 template <int F, int U, bool TAB, int MINB = 0>
 cudaError_t launch(const NearArgs& na, cudaStream_t st) {
@@ -226,7 +240,11 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st) 
   const int U = op.near_unroll;
   const bool T = op.near_tab;
   cudaError_t e;
-  if (F == 3 && U == 7 && T && op.near_minb == 4) e = launch<3, 7, true, 4>(na, st);
+  if (F == 3 && U == 7 && T && op.near_lean) {
+    dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + 2) / 3));
+    near_kernel_lean<3><<<g, kNearWarps * 32, 0, st>>>(na);
+    e = cudaGetLastError();
+  } else if (F == 3 && U == 7 && T && op.near_minb == 4) e = launch<3, 7, true, 4>(na, st);
   else if (F == 3 && U == 7 && T && op.near_minb == 2) e = launch<3, 7, true, 2>(na, st);
   else if (F == 2 && U == 7 && T && op.near_minb == 4) e = launch<2, 7, true, 4>(na, st);
   else if (F == 2 && U == 7 && T && op.near_minb == 6) e = launch<2, 7, true, 6>(na, st);

@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--mode", default="h2aca", choices=["h2aca", "h2only"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA-graph replay")
     ap.add_argument("--shard-of", type=int, default=0,
                     help="virtual shard: on 1 GPU, time the frequency-domain apply of rank --shard-rank's frequency "
                          "classes of a G-GPU run (what one rank of `--gpus G` computes, without the all-to-alls)")
@@ -260,27 +261,55 @@ def main():
     torch.cuda.synchronize()
     op.set_profiling(True)
     acc = {"near": 0.0, "up": 0.0, "coupling": 0.0, "down": 0.0}
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+
+    def timed(run, profile):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush (256 MB write) outside the timed region of every step
+            evs[k][0].record()
+            run()
+            evs[k][1].record()
+            evs[k][1].synchronize()
+            if profile:
+                for key, v in op.timings().items():
+                    acc[key] += v
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        return [a.elapsed_time(bb) for a, bb in evs]
+
+    # (1) eager steps with the library's per-kernel CUDA-event timers (kernel breakdown, roofline)
+    ms_eager = timed(lambda: step(x), True)
+    op.set_profiling(False)
+    # (2) headline: the same step captured once in a CUDA graph and replayed (removes the
+    # host launch gaps of the ~25 small launches per step); 1 GPU only
+    graph, graph_error = None, None
+    if world == 1 and not args.no_graph:
+        try:
+            x_static = x.clone()
+            s_cap = torch.cuda.Stream()
+            s_cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s_cap):
+                for _ in range(2):
+                    step(x_static)
+            torch.cuda.current_stream().wait_stream(s_cap)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                y_static = step(x_static)
+            graph.replay()
+            torch.cuda.synchronize()
+        except Exception as ex:  # pragma: no cover
+            graph = None
+            graph_error = repr(ex)
     clk = ClockSampler(local_rank)
     clk.start()
     time.sleep(0.3)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    for k in range(args.steps):
-        flush.zero_()
-        evs[k][0].record()
-        y = step(x)
-        evs[k][1].record()
-        evs[k][1].synchronize()
-        for key, v in op.timings().items():
-            acc[key] += v
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    ms_steps = timed(graph.replay, False) if graph is not None else timed(lambda: step(x), False)
     clocks = clk.stop()
-    op.set_profiling(False)
-    ms_steps = [a.elapsed_time(bb) for a, bb in evs]
     t_tot = torch.tensor([sum(ms_steps)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_tot, op=dist.ReduceOp.MAX)
@@ -359,6 +388,9 @@ def main():
            "config": config_json(args.config, cfg, M, L, world), "roofline": roof, "e2e": e2e,
            "gpu_launches": launches * args.steps, "clocks": clocks,
            "kernel_ms": kt, "fp64_measured_tflops": peaks,
+           "timing": ("CUDA-graph replay of the whole step (captured once after warm-up); eager step "
+                      f"{statistics.median(ms_eager):.3f} ms (median)") if graph is not None else
+                     f"eager launches{'' if graph_error is None else ' (graph capture failed: ' + graph_error + ')'}",
            "near_evals_per_s": evals_near / (kt["near"] * 1e-3) if kt["near"] > 0 else None,
            "setup_s": {"tree": t_tree, "aca": t_aca}, "mode": args.mode,
            "mean_aca_rank": float(op.aca_export()["ranks"].mean()) if mode == pb.BEM_MODE_H2ACA else None}

@@ -143,10 +143,9 @@ struct Op {
   int near_f = 3;  // frequency classes per warp (r01 sweep at config 2: F=2 7.77 ms, F=3 6.97 ms, F=4 9.85 ms)
   int near_unroll = 7;
   bool near_tab = true;
-  bool near_lean = false;  // K1 variant: x loads after the node loop, 128 registers (env BEM_NEAR_LEAN)
   int near_minb = 0;  // K1 __launch_bounds__ min blocks/SM variant (0: compiler's choice; 6, 8)
   bool force_generic = false;
-  int far_kernel = 0;                 // 0: auto (far8 for p > 32, far7 otherwise); 8, 7, 6 (DMMA variants), 4, 3
+  int far_kernel = 0;                 // 0: auto (far8 for p > 32, far7 otherwise); 8, 7, 6 (DMMA variants)
   size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM
   bool far7_rem_dfma = true;          // p = 27: rows 24..26 on DFMA instead of a padded DMMA tile
   bool far7_cluster = false;

@@ -10,15 +10,15 @@
 // are evaluated", north_star); they are regenerated on the fly from the
 // kernel (no slice storage: 223 GB at config 4).
 //
-// far3_kernel: CTA = (row cluster r, frequency tile, 32-row chunk of mu).
-// Per (b, j): the slice rows S[mu-chunk][:] are regenerated into shared
-// memory, B = Z_b[j,tile] (.) xhat_c[:,tile] is built in shared memory, and
-// every thread accumulates an MU x TU complex register tile of S B (FP64 DFMA).
-// Rows are processed heaviest-first (host-sorted by sum_b r_b); one CTA owns
-// each output tile, so there are no atomics and the result is deterministic.
-//
-// far_generic_kernel: BEM_MODE_H2ONLY (the plain-H^2 comparison path: S_b(s_l)
-// evaluated per frequency, no ACA) and a fallback for shapes far3 cannot hold.
+// Kernels (all deterministic: one CTA owns each output tile of a segment's
+// partial sum; segments of a row are reduced in fixed order, no atomics):
+//   far8_kernel / far7_kernel (default, p > 32 / p <= 32): the per-term slice
+//     product on the FP64 tensor cores (mma.sync m8n8k4 f64), slices
+//     regenerated in shared memory -- DESIGN.md §7;
+//   far6_kernel: the earlier DMMA variant (kept as a measured baseline, tested);
+//   h2o_kernel: BEM_MODE_H2ONLY, couplings evaluated per frequency on the fly
+//     (the paper's plain-H^2 comparison);
+//   far_generic_kernel: fallback for shapes the tiled kernels cannot hold.
 #include <algorithm>
 #include <vector>
 
@@ -50,337 +50,10 @@ __device__ __forceinline__ void node(const double* xi, int m, int mu, double* ou
   out[2] = xi[2 * m + mu / (m * m)];
 }
 
-struct Far3Args {
-  int nl, m, p, rcap, RB, RBP, gm, gt, TT, TTP;
-  const int32_t* rows;
-  const int32_t* far_ptr;
-  const int32_t* far_sorted;
-  const int32_t* far_c;
-  const double* xi;
-  const double2* s;
-  const int32_t* rank;
-  const int32_t* pivk;
-  const int64_t* zoff;
-  const double2* Z;
-  const double2* xhat;
-  double2* yhat;
-};
-
-template <int MU, int TU>
-__global__ void __launch_bounds__(256) far3_kernel(Far3Args a) {
-  extern __shared__ double2 sm[];
-  const int p = a.p, m = a.m, TT = a.TT, TTP = a.TTP;
-  const int r = a.rows[blockIdx.x];
-  const int t0 = blockIdx.y * TT;
-  const int mu0 = blockIdx.z * a.RB;
-  const int nrow = min(a.RB, p - mu0);
-  const int ntv = min(TT, a.nl - t0);
-  double2* B = sm;                         // p x TTP   Z (.) xhat tile, [nu][t]
-  double2* S = B + (size_t)p * TTP;        // RBP x p   slice rows (padded rows stay 0)
-  double* xcn = (double*)(S + (size_t)a.RBP * p);  // 3p
-  double* xr = xcn + 3 * p;                // 3 RBP
-  const int tid = threadIdx.x;
-  const int mg = tid / a.gt, tg = tid - (tid / a.gt) * a.gt;
-  const bool active = mg < a.gm;
-  for (int i = tid; i < a.RBP * p; i += blockDim.x) S[i] = make_double2(0.0, 0.0);
-  for (int i = tid; i < nrow; i += blockDim.x) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
-  double2 acc[MU][TU];
-#pragma unroll
-  for (int i = 0; i < MU; ++i)
-#pragma unroll
-    for (int u = 0; u < TU; ++u) acc[i][u] = make_double2(0.0, 0.0);
-  const double2* Srow = S + (size_t)mg * p;
-  const double2* Bcol = B + tg;
-  for (int bi = a.far_ptr[r]; bi < a.far_ptr[r + 1]; ++bi) {
-    const int b = a.far_sorted[bi];
-    const int c = a.far_c[b];
-    __syncthreads();
-    for (int i = tid; i < p; i += blockDim.x) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
-    const double2* xh = a.xhat + ((int64_t)c * a.nl + t0) * p;
-    const int rk = a.rank[b];
-    const double2* Zb = a.Z + a.zoff[b] + t0;
-    for (int l = 0; l < rk; ++l) {
-      const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + l]];
-      const double2* Zl = Zb + (int64_t)l * a.nl;
-      __syncthreads();
-      for (int idx = tid; idx < nrow * p; idx += blockDim.x) {
-        const int i = idx / p, nu = idx - i * p;
-        const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
-                     dz = xcn[3 * nu + 2] - xr[3 * i + 2];
-        S[idx] = kern(sqrt(dx * dx + dy * dy + dz * dz), sv);
-      }
-      for (int idx = tid; idx < TT * p; idx += blockDim.x) {
-        const int t = idx / p, nu = idx - t * p;
-        double2 v = make_double2(0.0, 0.0);
-        if (t < ntv) {
-          const double2 z = Zl[t], x = xh[(int64_t)t * p + nu];
-          v = make_double2(z.x * x.x - z.y * x.y, z.x * x.y + z.y * x.x);
-        }
-        B[nu * TTP + t] = v;
-      }
-      __syncthreads();
-      if (active) {
-#pragma unroll 2
-        for (int nu = 0; nu < p; ++nu) {
-          double2 sv2[MU], xv[TU];
-#pragma unroll
-          for (int i = 0; i < MU; ++i) sv2[i] = Srow[(size_t)i * a.gm * p + nu];
-#pragma unroll
-          for (int u = 0; u < TU; ++u) xv[u] = Bcol[nu * TTP + u * a.gt];
-#pragma unroll
-          for (int i = 0; i < MU; ++i)
-#pragma unroll
-            for (int u = 0; u < TU; ++u) cmac(acc[i][u], sv2[i], xv[u]);
-        }
-      }
-    }
-  }
-  if (active) {
-#pragma unroll
-    for (int u = 0; u < TU; ++u) {
-      const int tt = tg + u * a.gt;
-      if (tt >= ntv) continue;
-#pragma unroll
-      for (int i = 0; i < MU; ++i) {
-        const int row = mg + i * a.gm;
-        if (row < nrow) a.yhat[((int64_t)r * a.nl + t0 + tt) * p + mu0 + row] = acc[i][u];
-      }
-    }
-  }
-}
-
-struct Far3Cfg {
-  int MU = 0, TU = 0, RB = 0, RBP = 0, gm = 0, gt = 0, TT = 0, TTP = 0, ntiles = 0, nchunks = 0;
-  size_t smem = 0;
-};
-
-Far3Cfg choose(int p, int nl) {
-  Far3Cfg c;
-  const int RB = std::min(p, 32);
-  for (int MU : {4, 3, 2, 1}) {
-    const int gm = (RB + MU - 1) / MU;
-    if (gm > 64 || (gm * MU - RB) * 8 > RB) continue;  // <= 12.5% padded rows
-    const int gt = 256 / gm;
-    for (int TU = std::min(5, 16 / MU); TU >= 1; --TU) {
-      const int ntiles = (nl + gt * TU - 1) / (gt * TU);
-      const int need = (nl + ntiles - 1) / ntiles;
-      const int TUn = std::min(TU, (need + gt - 1) / gt);
-      const int TT = gt * TUn;
-      int TTP = TT + 1;
-      while (TTP % 8 != 1) ++TTP;  // row stride = 16 B mod 128 B: conflict-free column writes
-      const size_t smem = sizeof(double2) * ((size_t)p * TTP + (size_t)gm * MU * p) + sizeof(double) * 3 * (p + gm * MU);
-      if (smem > 110 * 1024) continue;  // keep 2 CTAs per SM
-      c.MU = MU; c.TU = TUn; c.RB = RB; c.RBP = gm * MU; c.gm = gm; c.gt = gt; c.TT = TT; c.TTP = TTP;
-      c.ntiles = ntiles; c.nchunks = (p + RB - 1) / RB; c.smem = smem;
-      return c;
-    }
-  }
-  return c;
-}
-
-template <int MU, int TU>
-cudaError_t launch3(const Far3Cfg& c, int nrows, const Far3Args& a, cudaStream_t st) {
-  auto k = far3_kernel<MU, TU>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-  if (e != cudaSuccess) return e;
-  k<<<dim3((unsigned)nrows, (unsigned)c.ntiles, (unsigned)c.nchunks), 256, c.smem, st>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t dispatch3(const Far3Cfg& c, int nrows, const Far3Args& a, cudaStream_t st) {
-#define CASE(MU_, TU_) \
-  if (c.MU == MU_ && c.TU == TU_) return launch3<MU_, TU_>(c, nrows, a, st);
-  CASE(4, 1) CASE(4, 2) CASE(4, 3) CASE(4, 4)
-  CASE(3, 1) CASE(3, 2) CASE(3, 3) CASE(3, 4) CASE(3, 5)
-  CASE(2, 1) CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(2, 5)
-  CASE(1, 1) CASE(1, 2) CASE(1, 3) CASE(1, 4) CASE(1, 5)
-#undef CASE
-  return cudaErrorInvalidConfiguration;
-}
-
-// ------------------------------------------------------ far4: FP64 tensor cores
-// Same decomposition as far3, but the contraction S B runs on the FP64 tensor
-// cores (mma.sync.aligned.m8n8k4.f64, SASS DMMA): a complex 8x8x4 step is four
-// real DMMAs (re += Sr Br - Si Bi, im += Sr Bi + Si Br).  8 warps; warp w owns
-// the 8-row mu tile (w & 3) and every second 8-column t tile starting at
-// (w >> 2), so the A fragment is shared by all of its tiles.  Padded rows and
-// columns (mu >= p, nu >= p, t >= n_t) are zero in shared memory.
-// Row strides are chosen conflict-free for the fragment loads: S stride = 4
-// (mod 8) complex, B stride = 2 (mod 8) complex.
-struct Far4Args {
-  int nl, m, p, p4, rcap, SST, TT, TTP, nT;
-  const int4* segs;  // (row, bi0, bi1, slot): far-block range of a row, launch order
-  const int32_t* far_sorted;
-  const int32_t* far_c;
-  const double* xi;
-  const double2* s;
-  const int32_t* rank;
-  const int32_t* pivk;
-  const int64_t* zoff;
-  const double2* Z;
-  const double2* xhat;
-  double2* part;  // [slot][t][mu]: partial y^ of the segment (reduced per row afterwards)
-};
-
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
-}
-
-template <int MAXT>
-__global__ void __launch_bounds__(256, 2) far4_kernel(Far4Args a) {
-  extern __shared__ double2 sm[];
-  const int p = a.p, m = a.m, TT = a.TT, TTP = a.TTP, SST = a.SST;
-  const int4 sg = a.segs[blockIdx.x];
-  const int r = sg.x;
-  const int t0 = blockIdx.y * TT;
-  const int mu0 = blockIdx.z * 32;
-  const int nrow = min(32, p - mu0);
-  const int ntv = min(TT, a.nl - t0);
-  const int nS = nrow * p, nB = ntv * p;
-  double2* S = sm;                            // 32 x SST
-  double2* B = S + 32 * SST;                  // p4 x TTP
-  double* xcn = (double*)(B + (size_t)a.p4 * TTP);  // 3p
-  double* xr = xcn + 3 * p;                   // 3 x 32
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, q = lane & 3;
-  for (int i = tid; i < 32 * SST; i += blockDim.x) S[i] = make_double2(0.0, 0.0);
-  for (int i = tid; i < a.p4 * TTP; i += blockDim.x) B[i] = make_double2(0.0, 0.0);
-  for (int i = tid; i < nrow; i += blockDim.x) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
-  const int mt = warp & 3;
-  double cre[MAXT][2], cim[MAXT][2];
-#pragma unroll
-  for (int i = 0; i < MAXT; ++i) { cre[i][0] = cre[i][1] = cim[i][0] = cim[i][1] = 0.0; }
-  const double2* Afrag = S + (mt * 8 + g) * SST + q;
-  for (int bi = sg.y; bi < sg.z; ++bi) {
-    const int b = a.far_sorted[bi];
-    const int c = a.far_c[b];
-    __syncthreads();
-    for (int i = tid; i < p; i += blockDim.x) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
-    const double2* xh = a.xhat + ((int64_t)c * a.nl + t0) * p;
-    const int rk = a.rank[b];
-    const double2* Zb = a.Z + a.zoff[b] + t0;
-    for (int l = 0; l < rk; ++l) {
-      const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + l]];
-      const double2* Zl = Zb + (int64_t)l * a.nl;
-      __syncthreads();
-      // produce B = Z_l (.) xhat_c (global loads issued first, 4 in flight) and
-      // the slice rows S(s_{k_l}) (ALU work overlapping the load latency)
-      int us = tid;
-      for (int u0 = tid; u0 < nB; u0 += 4 * 256) {
-        double2 zv[4], xv[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int u = u0 + k * 256;
-          if (u < nB) {
-            const int t = u / p;
-            zv[k] = Zl[t];
-            xv[k] = xh[u];
-          }
-        }
-        if (us < nS) {
-          const int i = us / p, nu = us - i * p;
-          const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
-                       dz = xcn[3 * nu + 2] - xr[3 * i + 2];
-          S[i * SST + nu] = kern(sqrt(dx * dx + dy * dy + dz * dz), sv);
-          us += 256;
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int u = u0 + k * 256;
-          if (u < nB) {
-            const int t = u / p, nu = u - t * p;
-            B[nu * TTP + t] = make_double2(zv[k].x * xv[k].x - zv[k].y * xv[k].y, zv[k].x * xv[k].y + zv[k].y * xv[k].x);
-          }
-        }
-      }
-      for (; us < nS; us += 256) {
-        const int i = us / p, nu = us - i * p;
-        const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
-                     dz = xcn[3 * nu + 2] - xr[3 * i + 2];
-        S[i * SST + nu] = kern(sqrt(dx * dx + dy * dy + dz * dz), sv);
-      }
-      __syncthreads();
-      for (int k0 = 0; k0 < a.p4; k0 += 4) {
-        const double2 av = Afrag[k0];
-        const double nai = -av.y;
-        const double2* Brow = B + (k0 + q) * TTP + g;
-#pragma unroll
-        for (int i = 0; i < MAXT; ++i) {
-          const int tt = (warp >> 2) + 2 * i;
-          if (tt < a.nT) {
-            const double2 bv = Brow[tt * 8];
-            dmma(cre[i][0], cre[i][1], av.x, bv.x);
-            dmma(cre[i][0], cre[i][1], nai, bv.y);
-            dmma(cim[i][0], cim[i][1], av.x, bv.y);
-            dmma(cim[i][0], cim[i][1], av.y, bv.x);
-          }
-        }
-      }
-    }
-  }
-  const int row = mt * 8 + g;
-  if (row < nrow) {
-#pragma unroll
-    for (int i = 0; i < MAXT; ++i) {
-      const int tt = (warp >> 2) + 2 * i;
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int col = tt * 8 + 2 * q + v;
-        if (tt < a.nT && col < ntv)
-          a.part[((int64_t)sg.w * a.nl + t0 + col) * p + mu0 + row] = make_double2(cre[i][v], cim[i][v]);
-      }
-    }
-  }
-}
-
-struct Far4Cfg {
-  int p4 = 0, SST = 0, TT = 0, TTP = 0, nT = 0, ntiles = 0, nchunks = 0, maxt = 0;
-  size_t smem = 0;
-};
-
-Far4Cfg choose4(int p, int nl, size_t smem_cap) {
-  Far4Cfg c;
-  const int p4 = (p + 3) / 4 * 4;
-  int SST = p4;
-  while (SST % 8 != 4) ++SST;
-  for (int TTmax : {144, 128, 112, 96, 80, 64, 48, 32, 16, 8}) {
-    const int ntiles = (nl + TTmax - 1) / TTmax;
-    const int TT = ((nl + ntiles - 1) / ntiles + 7) / 8 * 8;
-    int TTP = TT;
-    while (TTP % 8 != 2) ++TTP;
-    const size_t smem = sizeof(double2) * (32 * (size_t)SST + (size_t)p4 * TTP) + sizeof(double) * 3 * (p + 32);
-    if (smem > smem_cap) continue;
-    c.p4 = p4; c.SST = SST; c.TT = TT; c.TTP = TTP; c.nT = TT / 8; c.ntiles = ntiles;
-    c.nchunks = (p + 31) / 32; c.maxt = (c.nT + 1) / 2; c.smem = smem;
-    return c;
-  }
-  return c;
-}
-
-template <int MAXT>
-cudaError_t launch4(const Far4Cfg& c, int nrows, const Far4Args& a, cudaStream_t st) {
-  auto k = far4_kernel<MAXT>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-  if (e != cudaSuccess) return e;
-  k<<<dim3((unsigned)nrows, (unsigned)c.ntiles, (unsigned)c.nchunks), 256, c.smem, st>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t dispatch4(const Far4Cfg& c, int nrows, const Far4Args& a, cudaStream_t st) {
-  switch (c.maxt) {
-    case 1: return launch4<1>(c, nrows, a, st);
-    case 2: return launch4<2>(c, nrows, a, st);
-    case 3: return launch4<3>(c, nrows, a, st);
-    case 4: return launch4<4>(c, nrows, a, st);
-    case 5: return launch4<5>(c, nrows, a, st);
-    case 6: return launch4<6>(c, nrows, a, st);
-    case 7: return launch4<7>(c, nrows, a, st);
-    case 8: return launch4<8>(c, nrows, a, st);
-    case 9: return launch4<9>(c, nrows, a, st);
-    default: return cudaErrorInvalidConfiguration;
-  }
 }
 
 // ------------------------------------------------ far6: transposed DMMA coupling
@@ -1524,35 +1197,6 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
       BEM_CK(cudaGetLastError());
       return BEM_OK;
     }
-  }
-  if (op.mode == BEM_MODE_H2ACA && fk == 4 && !op.force_generic && op.n_segs > 0) {
-    const Far4Cfg f4 = choose4(p, nl, op.far4_smem_cap);
-    if (f4.maxt > 0) {
-      BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
-      Far4Args a;
-      a.nl = nl; a.m = t.m; a.p = p; a.p4 = f4.p4; a.rcap = op.rcap; a.SST = f4.SST; a.TT = f4.TT; a.TTP = f4.TTP;
-      a.nT = f4.nT;
-      a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
-      a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
-      a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
-      BEM_CK(dispatch4(f4, op.n_segs, a, st));
-      seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
-                                                       yhat, (int64_t)nl * p);
-      BEM_CK(cudaGetLastError());
-      return BEM_OK;
-    }
-  }
-  const Far3Cfg fc = choose(p, nl);
-  if (op.mode == BEM_MODE_H2ACA && fc.MU > 0 && !op.force_generic) {
-    BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
-    Far3Args a;
-    a.nl = nl; a.m = t.m; a.p = p; a.rcap = op.rcap; a.RB = fc.RB; a.RBP = fc.RBP; a.gm = fc.gm; a.gt = fc.gt;
-    a.TT = fc.TT; a.TTP = fc.TTP;
-    a.rows = op.d_far_rows.p; a.far_ptr = t.d_far_ptr.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
-    a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
-    a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.yhat = yhat;
-    BEM_CK(dispatch3(fc, op.n_far_rows, a, st));
-    return BEM_OK;
   }
   FarArgs a;
   a.nl = nl; a.m = t.m; a.p = p; a.mode = op.mode; a.rcap = op.rcap;

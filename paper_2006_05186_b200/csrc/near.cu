@@ -209,11 +209,7 @@ template <int F, int U, bool TAB, int MINB>
 __global__ void __launch_bounds__(kNearWarps * 32, MINB) near_kernel_minb(NearArgs a) {
   near_body<F, U, TAB>(a);
 }
-// lean variant (x loads after the node loop) at 4 CTAs/SM (128 registers)
-template <int F>
-__global__ void __launch_bounds__(kNearWarps * 32, 4) near_kernel_lean(NearArgs a) {
-  near_body<F, 7, true, true>(a);
-}
+
 
 template <int F, int U, bool TAB, int MINB = 0>
 cudaError_t launch(const NearArgs& na, cudaStream_t st) {
@@ -240,11 +236,7 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st) 
   const int U = op.near_unroll;
   const bool T = op.near_tab;
   cudaError_t e;
-  if (F == 3 && U == 7 && T && op.near_lean) {
-    dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + 2) / 3));
-    near_kernel_lean<3><<<g, kNearWarps * 32, 0, st>>>(na);
-    e = cudaGetLastError();
-  } else if (F == 3 && U == 7 && T && op.near_minb == 4) e = launch<3, 7, true, 4>(na, st);
+  if (F == 3 && U == 7 && T && op.near_minb == 4) e = launch<3, 7, true, 4>(na, st);
   else if (F == 3 && U == 7 && T && op.near_minb == 2) e = launch<3, 7, true, 2>(na, st);
   else if (F == 2 && U == 7 && T && op.near_minb == 4) e = launch<2, 7, true, 4>(na, st);
   else if (F == 2 && U == 7 && T && op.near_minb == 6) e = launch<2, 7, true, 6>(na, st);

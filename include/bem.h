@@ -166,9 +166,9 @@ bem_status bem_debug_pinned(const double* x, int64_t n, double* exp_out, double*
                             int32_t device);
 /* Hot-path (K1 / K3 slice regeneration) table-driven exp (x <= 0; 0 returned
  * for x > 0) and sincos evaluated ON THE DEVICE for n host inputs: accuracy
- * check of the fast math against libm (tests). */
+ * check of the fast math against libm (tests).  variant: 64 or 256 (table size). */
 bem_status bem_debug_fastmath(const double* x, int64_t n, double* exp_out, double* sin_out, double* cos_out,
-                              int32_t device);
+                              int32_t device, int32_t variant);
 /* FP64 DFMA throughput microbenchmark: returns achieved FLOP/s. */
 bem_status bem_debug_fp64_peak(int32_t device, void* cuda_stream, double* flops_per_s);
 /* mode 0: DFMA loop, 1: FP64 tensor-core mma.sync m8n8k4 loop, 2: both in one CTA. */

@@ -68,7 +68,7 @@ def lib():
         "cqm_solve": [vp, vp, vp, i64, d, d, i32, i32, vp, vp, vp],
         "bem_solve_multifreq": [vp, vp, vp, d, i32, i32, vp, vp],
         "bem_debug_pinned": [vp, i64, vp, vp, vp, i32],
-        "bem_debug_fastmath": [vp, i64, vp, vp, vp, i32],
+        "bem_debug_fastmath": [vp, i64, vp, vp, vp, i32, i32],
         "bem_debug_fp64_peak": [i32, vp, vp],
         "bem_op_set_profiling": [vp, i32],
         "bem_op_get_timings": [vp, vp],
@@ -271,11 +271,11 @@ def debug_pinned(x, device: int = 0):
     return e, s, c
 
 
-def debug_fastmath(x, device: int = 0):
+def debug_fastmath(x, device: int = 0, variant: int = 64):
     """Device table-driven exp (x <= 0) / sin / cos of the hot kernels, for accuracy tests."""
     x = np.ascontiguousarray(x, dtype=np.float64).ravel()
     e, s, c = np.empty_like(x), np.empty_like(x), np.empty_like(x)
-    _check(lib().bem_debug_fastmath(_p(x), len(x), _p(e), _p(s), _p(c), int(device)))
+    _check(lib().bem_debug_fastmath(_p(x), len(x), _p(e), _p(s), _p(c), int(device), int(variant)))
     return e, s, c
 
 

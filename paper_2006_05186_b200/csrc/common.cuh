@@ -143,6 +143,7 @@ struct Op {
   int near_f = 3;  // frequency classes per warp (r01 sweep at config 2: F=2 7.77 ms, F=3 6.97 ms, F=4 9.85 ms)
   int near_unroll = 7;
   bool near_tab = true;
+  bool near_t256 = false;  // K1 with 256-entry exp / sincos tables (env BEM_NEAR_T256)
   int near_minb = 0;  // K1 __launch_bounds__ min blocks/SM variant (0: compiler's choice; 6, 8)
   bool force_generic = false;
   int far_kernel = 0;                 // 0: auto (far8 for p > 32, far7 otherwise); 8, 7, 6 (DMMA variants)

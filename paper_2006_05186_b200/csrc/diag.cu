@@ -124,24 +124,29 @@ extern "C" bem_status bem_debug_fp64_peak(int32_t device, void* cuda_stream, dou
 // slice regeneration) evaluated on the device for host inputs.
 namespace bem {
 namespace {
-__global__ void debug_fastmath_kernel(const double* x, int64_t n, double* e, double* sn, double* cs) {
-  __shared__ double et[64];
-  __shared__ double2 st[64];
-  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
-    et[i] = fast::kExp2Tab[i];
-    st[i] = fast::kSinCosTab[i];
+__global__ void debug_fastmath_kernel(const double* x, int64_t n, double* e, double* sn, double* cs, int v256) {
+  __shared__ double et[256];
+  __shared__ double2 st[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    et[i] = v256 ? fast::kExp2Tab256[i] : (i < 64 ? fast::kExp2Tab[i] : 0.0);
+    st[i] = v256 ? fast::kSinCosTab256[i] : (i < 64 ? fast::kSinCosTab[i] : make_double2(0.0, 0.0));
   }
   __syncthreads();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  e[i] = x[i] <= 0.0 ? fast::exp_neg_tab(x[i], et) : 0.0;
-  fast::sincos_tab(x[i], st, &sn[i], &cs[i]);
+  if (v256) {
+    e[i] = x[i] <= 0.0 ? fast::exp_neg_tab256(x[i], et) : 0.0;
+    fast::sincos_tab256(x[i], st, &sn[i], &cs[i]);
+  } else {
+    e[i] = x[i] <= 0.0 ? fast::exp_neg_tab(x[i], et) : 0.0;
+    fast::sincos_tab(x[i], st, &sn[i], &cs[i]);
+  }
 }
 }  // namespace
 }  // namespace bem
 
 extern "C" bem_status bem_debug_fastmath(const double* x, int64_t n, double* e, double* sn, double* cs,
-                                         int32_t device) {
+                                         int32_t device, int32_t variant) {
   using namespace bem;
   BEM_REQ(x && e && sn && cs && n >= 0, "bem_debug_fastmath: bad arguments");
   if (n == 0) return BEM_OK;
@@ -149,7 +154,7 @@ extern "C" bem_status bem_debug_fastmath(const double* x, int64_t n, double* e, 
   DBuf<double> dx, de, ds, dc;
   BEM_CK(dx.alloc(n)); BEM_CK(de.alloc(n)); BEM_CK(ds.alloc(n)); BEM_CK(dc.alloc(n));
   BEM_CK(cudaMemcpy(dx.p, x, sizeof(double) * n, cudaMemcpyHostToDevice));
-  debug_fastmath_kernel<<<(unsigned)((n + 255) / 256), 256>>>(dx.p, n, de.p, ds.p, dc.p);
+  debug_fastmath_kernel<<<(unsigned)((n + 255) / 256), 256>>>(dx.p, n, de.p, ds.p, dc.p, variant == 256);
   BEM_CK(cudaGetLastError());
   BEM_CK(cudaMemcpy(e, de.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
   BEM_CK(cudaMemcpy(sn, ds.p, sizeof(double) * n, cudaMemcpyDeviceToHost));

@@ -74,14 +74,15 @@ __device__ __noinline__ double2 self_entry(const double* qn, const double* qw, d
   return make_double2(vr, vi);
 }
 
-template <int F, int U, bool TAB, bool LEAN = false>
+template <int F, int U, bool TAB, bool LEAN = false, bool T256 = false>
 __device__ __forceinline__ void near_body(const NearArgs& a) {
-  __shared__ double etab[64];
-  __shared__ double2 sctab[64];
+  constexpr int NT = T256 ? 256 : 64;
+  __shared__ double etab[NT];
+  __shared__ double2 sctab[NT];
   if (TAB) {
-    for (int i = threadIdx.x; i < 64; i += blockDim.x) {
-      etab[i] = fast::kExp2Tab[i];
-      sctab[i] = fast::kSinCosTab[i];
+    for (int i = threadIdx.x; i < NT; i += blockDim.x) {
+      etab[i] = T256 ? fast::kExp2Tab256[i] : fast::kExp2Tab[i];
+      sctab[i] = T256 ? fast::kSinCosTab256[i] : fast::kSinCosTab[i];
     }
     __syncthreads();
   }
@@ -151,9 +152,11 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
         const double w = qw[q] * ir;
 #pragma unroll
         for (int f = 0; f < F; ++f) {
-          const double e = (TAB ? fast::exp_neg_tab(-sre[f] * r, etab) : fast::exp_neg(-sre[f] * r)) * w;
+          const double e = (TAB ? (T256 ? fast::exp_neg_tab256(-sre[f] * r, etab) : fast::exp_neg_tab(-sre[f] * r, etab))
+                                : fast::exp_neg(-sre[f] * r)) * w;
           double sn, cs;
-          if (TAB) fast::sincos_tab(sim[f] * r, sctab, &sn, &cs);
+          if (TAB && T256) fast::sincos_tab256(sim[f] * r, sctab, &sn, &cs);
+          else if (TAB) fast::sincos_tab(sim[f] * r, sctab, &sn, &cs);
           else fast::sincos_(sim[f] * r, &sn, &cs);
           v[f].x = fma(e, cs, v[f].x);
           v[f].y = fma(-e, sn, v[f].y);
@@ -209,6 +212,11 @@ template <int F, int U, bool TAB, int MINB>
 __global__ void __launch_bounds__(kNearWarps * 32, MINB) near_kernel_minb(NearArgs a) {
   near_body<F, U, TAB>(a);
 }
+// 256-entry exp / sincos tables (one / two polynomial terms fewer); BEM_NEAR_T256
+template <int F>
+__global__ void __launch_bounds__(kNearWarps * 32) near_kernel_t256(NearArgs a) {
+  near_body<F, 7, true, false, true>(a);
+}
 
 
 template <int F, int U, bool TAB, int MINB = 0>
@@ -236,7 +244,11 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st) 
   const int U = op.near_unroll;
   const bool T = op.near_tab;
   cudaError_t e;
-  if (F == 3 && U == 7 && T && op.near_minb == 4) e = launch<3, 7, true, 4>(na, st);
+  if (F == 3 && U == 7 && T && op.near_t256) {
+    dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + 2) / 3));
+    near_kernel_t256<3><<<g, kNearWarps * 32, 0, st>>>(na);
+    e = cudaGetLastError();
+  } else if (F == 3 && U == 7 && T && op.near_minb == 4) e = launch<3, 7, true, 4>(na, st);
   else if (F == 3 && U == 7 && T && op.near_minb == 2) e = launch<3, 7, true, 2>(na, st);
   else if (F == 2 && U == 7 && T && op.near_minb == 4) e = launch<2, 7, true, 4>(na, st);
   else if (F == 2 && U == 7 && T && op.near_minb == 6) e = launch<2, 7, true, 6>(na, st);

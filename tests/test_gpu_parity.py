@@ -377,17 +377,18 @@ def test_solve_mask_bitwise_identical(pb, torch, monkeypatch):
     assert np.array_equal(out[0][0], out[1][0])
 
 
-def test_hot_path_fastmath_accuracy(pb):
+@pytest.mark.parametrize("variant", [64, 256])
+def test_hot_path_fastmath_accuracy(pb, variant):
     """Table-driven exp / sincos of K1 and K3 (fastmath.cuh) against libm over the
     configs' argument ranges: exp within 2 ulp for x in [-700, 0]; sin/cos
     within 2.5e-16 absolute for |theta| <= 6.5e3."""
     rng = np.random.default_rng(11)
     x = np.concatenate([-rng.random(200000) * 700.0, [0.0, -1e-300, -0.5 * np.log(2) / 64]])
-    e, _, _ = pb.debug_fastmath(x)
+    e, _, _ = pb.debug_fastmath(x, variant=variant)
     ref = np.exp(x)
     assert np.max(np.abs(e - ref) / np.spacing(ref)) <= 2.0
     t = np.concatenate([(rng.random(300000) - 0.5) * 13000.0, [0.0, np.pi / 64, np.pi / 2, -np.pi]])
-    _, s, c = pb.debug_fastmath(t)
+    _, s, c = pb.debug_fastmath(t, variant=variant)
     assert np.max(np.abs(s - np.sin(t))) <= 2.5e-16
     assert np.max(np.abs(c - np.cos(t))) <= 2.5e-16
 

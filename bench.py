@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA-graph replay")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: host-staged all-to-all (testing the multi-rank flow on one GPU only)")
     ap.add_argument("--shard-of", type=int, default=0,
                     help="virtual shard: on 1 GPU, time the frequency-domain apply of rank --shard-rank's frequency "
                          "classes of a G-GPU run (what one rank of `--gpus G` computes, without the all-to-alls)")
@@ -211,10 +213,15 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; --dist-backend gloo (host-staged all-to-all) lets N ranks share
+    # fewer GPUs to exercise the multi-rank flow where only one GPU is available
+    local_rank = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local_rank)
     cfg, V, T, N, L, R = workload(args.config)
     M = len(T)
@@ -310,7 +317,8 @@ def main():
     time.sleep(0.3)
     ms_steps = timed(graph.replay, False) if graph is not None else timed(lambda: step(x), False)
     clocks = clk.stop()
-    t_tot = torch.tensor([sum(ms_steps)], dtype=torch.float64, device=dev)
+    red_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")
+    t_tot = torch.tensor([sum(ms_steps)], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t_tot, op=dist.ReduceOp.MAX)
     ms_per_step = float(t_tot.item()) / args.steps
@@ -334,7 +342,7 @@ def main():
             yh.copy_(yd, non_blocking=True)
             eev[k][1].record()
             eev[k][1].synchronize()
-        te = torch.tensor([sum(a.elapsed_time(bb) for a, bb in eev)], dtype=torch.float64, device=dev)
+        te = torch.tensor([sum(a.elapsed_time(bb) for a, bb in eev)], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         ms_e2e = float(te.item()) / args.steps

@@ -65,9 +65,14 @@ class ShardedTimeOperator:
         torch = self._torch
         send = torch.cat([torch.view_as_real(c.contiguous()).reshape(-1) for c in send_chunks])
         rsz = [int(np.prod(s)) * 2 for s in recv_shapes]
-        recv = torch.empty(sum(rsz), dtype=torch.float64, device=device)
         ssz = [c.numel() * 2 for c in send_chunks]
-        dist.all_to_all_single(recv, send, output_split_sizes=rsz, input_split_sizes=ssz, group=self.group)
+        if send.is_cuda and dist.get_backend(self.group) == "gloo":  # host-staged (tests on one GPU)
+            recv = torch.empty(sum(rsz), dtype=torch.float64)
+            dist.all_to_all_single(recv, send.cpu(), output_split_sizes=rsz, input_split_sizes=ssz, group=self.group)
+            recv = recv.to(device)
+        else:
+            recv = torch.empty(sum(rsz), dtype=torch.float64, device=device)
+            dist.all_to_all_single(recv, send, output_split_sizes=rsz, input_split_sizes=ssz, group=self.group)
         out, o = [], 0
         for s, n in zip(recv_shapes, rsz):
             out.append(torch.view_as_complex(recv[o:o + n].view(*s, 2)))

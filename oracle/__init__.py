@@ -69,6 +69,10 @@ def lib():
         L.orc_admissible.restype = i32
         L.orc_aca_matrix.argtypes = [vp, i32, i32, d, vp, vp, vp, vp, vp]
         L.orc_aca_matrix.restype = i32
+        L.orc_h2_apply_dl.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, d]
+        L.orc_h2_apply_dl.restype = C.c_int
+        L.orc_dense_matrix_dl.argtypes = [vp, vp, i64, d, d, vp]
+        L.orc_normals.argtypes = [vp, vp, i64, vp]
         _lib = L
     return _lib
 
@@ -180,6 +184,22 @@ def dense_matrix(V, T, s):
     return A
 
 
+def dense_matrix_dl(V, T, s):
+    """Double-layer collocation matrix K(s) (NEXT-1), K[i,i] = 0."""
+    V, T = _f64(V), _i32(T)
+    M = len(T)
+    A = np.empty((M, M), dtype=np.complex128)
+    lib().orc_dense_matrix_dl(_p(V), _p(T), M, float(np.real(s)), float(np.imag(s)), _p(A))
+    return A
+
+
+def normals(V, T):
+    V, T = _f64(V), _i32(T)
+    n = np.empty((len(T), 3))
+    lib().orc_normals(_p(V), _p(T), len(T), _p(n))
+    return n
+
+
 def forward(xt, N, R):
     xt = _c128(xt)
     M = xt.shape[1]
@@ -261,6 +281,19 @@ class H2:
         rc = lib().orc_h2_apply(self.h, int(mode), _p(s), L, _p(lsel), len(lsel), _p(x), _p(y))
         if rc != 0:
             raise RuntimeError("oracle apply: ACA not assembled for these frequencies")
+        return y
+
+    def apply_dl(self, mode, s, x, lsel=None, alpha=0.0):
+        """y[t] = (alpha I + K(s[lsel[t]])) x[t] (double layer, NEXT-1)."""
+        s = _c128(s)
+        L = len(s)
+        lsel = np.arange(L, dtype=np.int32) if lsel is None else _i32(lsel)
+        x = _c128(x)
+        assert x.shape == (len(lsel), self.M)
+        y = np.empty_like(x)
+        rc = lib().orc_h2_apply_dl(self.h, int(mode), _p(s), L, _p(lsel), len(lsel), _p(x), _p(y), float(alpha))
+        if rc != 0:
+            raise RuntimeError("oracle apply_dl: ACA not assembled for these frequencies")
         return y
 
     def gmres(self, mode, s, b, lsel=None, tol=1e-8, restart=50, maxit=2000):

@@ -62,6 +62,7 @@ static const Rule7 RULE;
 struct Geometry {
   int64_t M = 0;
   std::vector<double> cen, area, node, J, lo, hi;  // cen M*3, node M*7*3, lo/hi M*3
+  std::vector<double> nrm;                           // M*3 unit normal (b-a) x (c-a) / |.| (vertex order)
 };
 
 // J(T) = int_T dS(y)/|c-y| for c the centroid (in-plane point), summed over
@@ -91,7 +92,7 @@ static double self_integral(const double* A0, const double* B0, const double* C0
 static void make_geometry(const double* V, const int32_t* T, int64_t M, Geometry& g) {
   g.M = M;
   g.cen.resize(M * 3); g.area.resize(M); g.node.resize(M * 21); g.J.resize(M);
-  g.lo.resize(M * 3); g.hi.resize(M * 3);
+  g.lo.resize(M * 3); g.hi.resize(M * 3); g.nrm.resize(M * 3);
   for (int64_t i = 0; i < M; ++i) {
     const double* a = V + 3 * (int64_t)T[3 * i + 0];
     const double* b = V + 3 * (int64_t)T[3 * i + 1];
@@ -106,6 +107,7 @@ static void make_geometry(const double* V, const int32_t* T, int64_t M, Geometry
     double cr[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
                     e1[0] * e2[1] - e1[1] * e2[0]};
     g.area[i] = 0.5 * std::sqrt((cr[0] * cr[0] + cr[1] * cr[1]) + cr[2] * cr[2]);
+    for (int k = 0; k < 3; ++k) g.nrm[3 * i + k] = cr[k] / (2.0 * g.area[i]);
     for (int q = 0; q < 7; ++q)
       for (int k = 0; k < 3; ++k)
         g.node[21 * i + 3 * q + k] = (q == 0) ? g.cen[3 * i + k]
@@ -154,6 +156,26 @@ static cplx entry(const Geometry& g, int64_t i, int64_t j, cplx s) {
     acc += RULE.w[q] * phi_self(r, s);
   }
   return (g.J[i] + g.area[i] * acc) / FOURPI;
+}
+
+// NEXT-1: double-layer operator K(s) of eq:wavebio (P:301-303,
+// gamma_{1,y} applied to the fundamental solution), collocation analogue:
+//   dk(x,y,n_y;s) = d/dn_y e^{-s|x-y|}/(4 pi |x-y|) = -(1+s r) e^{-s r} ((y-x).n_y)/(4 pi r^3),
+//   K_l[i,j] = |T_j| sum_q w_q dk(c_i, y_{j,q}, n_j; s_l)  (i != j),
+//   K_l[i,i] = 0 (flat panel: (y - c_i).n_i = 0 on the panel's own plane).
+static cplx entry_dl(const Geometry& g, int64_t i, int64_t j, cplx s) {
+  if (i == j) return cplx(0.0, 0.0);
+  const double* ci = &g.cen[3 * i];
+  const double* n = &g.nrm[3 * j];
+  cplx acc(0.0, 0.0);
+  for (int q = 0; q < 7; ++q) {
+    const double* y = &g.node[21 * j + 3 * q];
+    double dx = y[0] - ci[0], dy = y[1] - ci[1], dz = y[2] - ci[2];
+    double r = std::sqrt((dx * dx + dy * dy) + dz * dz);
+    double dn = (dx * n[0] + dy * n[1]) + dz * n[2];
+    acc += RULE.w[q] * (-(1.0 + s * r) * std::exp(-s * r) * (dn / (r * r * r)));
+  }
+  return acc * (g.area[j] / FOURPI);
 }
 
 // ---------------------------------------------------------------------------
@@ -312,6 +334,7 @@ struct H2 {
   std::vector<int> nearR, nearC, farR, farC;
   // bases (cluster order): U[k*p+mu], W[k*p+nu]; E[c*p*p + lam*p + mu] = E_{c,parent(c)}
   std::vector<double> U, W, E, xi;  // xi[c*3*m + a*m + k]
+  std::vector<double> WK;           // double-layer column basis: |T_j| sum_q w_q n_j . grad L_nu(y_q)
   // ACA result per far block
   std::vector<int> rank, pivk, pivq;
   std::vector<int64_t> pivoff, zoff;
@@ -428,6 +451,29 @@ static double lagrange3(const double* xi, int m, int mu, const double* x) {
          lagrange1(xi + 2 * m, m, kz, x[2]);
 }
 
+// d/dt of the 1-D Lagrange polynomial l_k(t)
+static double dlagrange1(const double* nodes, int m, int k, double t) {
+  double sum = 0.0;
+  for (int i = 0; i < m; ++i) {
+    if (i == k) continue;
+    double v = 1.0 / (nodes[k] - nodes[i]);
+    for (int j = 0; j < m; ++j)
+      if (j != k && j != i) v *= (t - nodes[j]) / (nodes[k] - nodes[j]);
+    sum += v;
+  }
+  return sum;
+}
+
+// n . grad L_{c,mu}(x)
+static double dlagrange3n(const double* xi, int m, int mu, const double* x, const double* n) {
+  int kx = mu % m, ky = (mu / m) % m, kz = mu / (m * m);
+  double lx = lagrange1(xi, m, kx, x[0]), ly = lagrange1(xi + m, m, ky, x[1]), lz = lagrange1(xi + 2 * m, m, kz, x[2]);
+  double gx = dlagrange1(xi, m, kx, x[0]) * ly * lz;
+  double gy = lx * dlagrange1(xi + m, m, ky, x[1]) * lz;
+  double gz = lx * ly * dlagrange1(xi + 2 * m, m, kz, x[2]);
+  return (n[0] * gx + n[1] * gy) + n[2] * gz;
+}
+
 static void node_point(const double* xi, int m, int mu, double* out) {
   out[0] = xi[mu % m];
   out[1] = xi[m + (mu / m) % m];
@@ -442,6 +488,7 @@ static void build_bases(H2& h) {
   for (int c = 0; c < C; ++c) cluster_nodes(h.cl[c], m, &h.xi[(size_t)c * 3 * m]);
   h.U.assign((size_t)M * p, 0.0);
   h.W.assign((size_t)M * p, 0.0);
+  h.WK.assign((size_t)M * p, 0.0);
   for (int c = 0; c < C; ++c) {
     const Cluster& cc = h.cl[c];
     if (cc.son0 >= 0) continue;
@@ -453,6 +500,10 @@ static void build_bases(H2& h) {
         double acc = 0.0;
         for (int q = 0; q < 7; ++q) acc += RULE.w[q] * lagrange3(xi, m, mu, &h.g.node[21 * i + 3 * q]);
         h.W[(size_t)k * p + mu] = h.g.area[i] * acc;
+        double acck = 0.0;
+        for (int q = 0; q < 7; ++q)
+          acck += RULE.w[q] * dlagrange3n(xi, m, mu, &h.g.node[21 * i + 3 * q], &h.g.nrm[3 * i]);
+        h.WK[(size_t)k * p + mu] = h.g.area[i] * acck;
       }
     }
   }
@@ -591,8 +642,12 @@ static void aca_block(const double* xr, const double* xc, int m, int p, const st
 // ---------------------------------------------------------------------------
 enum { MODE_DENSE = 0, MODE_H2ONLY = 1, MODE_H2ACA = 2 };
 
+// op = 0: single layer V(s_l); op = 1: double layer K(s_l) (NEXT-1): the same
+// coupling tensors and ACA, column basis WK and near entries entry_dl.
 static void apply_one(const H2& h, int mode, cplx s_l, int l, const std::vector<cplx>& sl_all,
-                      const cplx* x_in, cplx* y_out) {
+                      const cplx* x_in, cplx* y_out, int op = 0) {
+  auto ent = [&](int64_t i, int64_t j) { return op == 0 ? entry(h.g, i, j, s_l) : entry_dl(h.g, i, j, s_l); };
+  const std::vector<double>& Wc = op == 0 ? h.W : h.WK;
   int64_t M = h.g.M;
   int p = h.p, m = h.m, C = (int)h.cl.size();
   std::vector<cplx> x(M), y(M, cplx(0.0, 0.0));
@@ -600,7 +655,7 @@ static void apply_one(const H2& h, int mode, cplx s_l, int l, const std::vector<
   if (mode == MODE_DENSE) {
     for (int64_t a = 0; a < M; ++a) {
       cplx acc(0.0, 0.0);
-      for (int64_t b = 0; b < M; ++b) acc += entry(h.g, h.perm[a], h.perm[b], s_l) * x[b];
+      for (int64_t b = 0; b < M; ++b) acc += ent(h.perm[a], h.perm[b]) * x[b];
       y[a] = acc;
     }
   } else {
@@ -612,7 +667,7 @@ static void apply_one(const H2& h, int mode, cplx s_l, int l, const std::vector<
       if (cc.son0 < 0) {
         for (int nu = 0; nu < p; ++nu) {
           cplx acc(0.0, 0.0);
-          for (int k = cc.begin; k < cc.end; ++k) acc += h.W[(size_t)k * p + nu] * x[k];
+          for (int k = cc.begin; k < cc.end; ++k) acc += Wc[(size_t)k * p + nu] * x[k];
           out[nu] = acc;
         }
       } else {
@@ -687,7 +742,7 @@ static void apply_one(const H2& h, int mode, cplx s_l, int l, const std::vector<
       const Cluster& Cc = h.cl[h.nearC[b]];
       for (int a = R.begin; a < R.end; ++a) {
         cplx acc(0.0, 0.0);
-        for (int k = Cc.begin; k < Cc.end; ++k) acc += entry(h.g, h.perm[a], h.perm[k], s_l) * x[k];
+        for (int k = Cc.begin; k < Cc.end; ++k) acc += ent(h.perm[a], h.perm[k]) * x[k];
         y[a] += acc;
       }
     }
@@ -1001,6 +1056,43 @@ int orc_h2_apply(void* hp, int32_t mode, const double* s_in, int32_t L, const in
     apply_one(h, mode, s[l], l, s, (const cplx*)(x + 2 * (int64_t)t * M), (cplx*)(y + 2 * (int64_t)t * M));
   }
   return 0;
+}
+
+// y[t][:] = (alpha I + K(s_{lsel[t]})) x[t][:] (double layer, NEXT-1)
+int orc_h2_apply_dl(void* hp, int32_t mode, const double* s_in, int32_t L, const int32_t* lsel, int32_t nsel,
+                    const double* x, double* y, double alpha) {
+  H2& h = *(H2*)hp;
+  if (mode == MODE_H2ACA && (!h.aca_done || h.L != L)) return -1;
+  std::vector<cplx> s(L);
+  for (int l = 0; l < L; ++l) s[l] = cplx(s_in[2 * l], s_in[2 * l + 1]);
+  int64_t M = h.g.M;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int t = 0; t < nsel; ++t) {
+    int l = lsel[t];
+    const cplx* xt = (const cplx*)(x + 2 * (int64_t)t * M);
+    cplx* yt = (cplx*)(y + 2 * (int64_t)t * M);
+    apply_one(h, mode, s[l], l, s, xt, yt, 1);
+    for (int64_t i = 0; i < M; ++i) yt[i] += alpha * xt[i];
+  }
+  return 0;
+}
+
+void orc_dense_matrix_dl(const double* V, const int32_t* T, int64_t M, double sre, double sim, double* A) {
+  Geometry g;
+  make_geometry(V, T, M, g);
+  cplx s(sre, sim);
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t j = 0; j < M; ++j) {
+      cplx v = entry_dl(g, i, j, s);
+      A[2 * (i * M + j)] = v.real();
+      A[2 * (i * M + j) + 1] = v.imag();
+    }
+}
+
+void orc_normals(const double* V, const int32_t* T, int64_t M, double* nrm) {
+  Geometry g;
+  make_geometry(V, T, M, g);
+  for (int64_t i = 0; i < 3 * M; ++i) nrm[i] = g.nrm[i];
 }
 
 void orc_forward(const double* xt, double* xf, int64_t M, int32_t N, double R) {

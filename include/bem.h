@@ -120,6 +120,19 @@ bem_status bem_op_destroy(bem_op op); /* NULL-safe */
  * x and y must not overlap.  Asynchronous on cuda_stream. */
 bem_status bem_apply_multifreq(bem_op op, const bem_c128* x, bem_c128* y, void* cuda_stream);
 
+/* Double-layer operator (eq:wavebio P:301-303, the
+ * gamma_{1,y}-derivative of the fundamental solution eq:fundsol P:479-482):
+ *   y_t = (alpha I + K(s_{local_l[t]})) x_t,
+ *   K[i,j](s) = |T_j| sum_q w_q d/dn_y [e^{-s r}/(4 pi r)] at (c_i, y_{j,q}),
+ *             = |T_j| sum_q w_q (-(1 + s r) e^{-s r} (y - c_i).n_j / (4 pi r^3)),
+ *   K[i,i] = 0 (flat panels), n_j = (b-a)x(c-a)/|.| in the triangle's vertex order.
+ * Far field: the op's coupling tensors / ACA skeleton (unchanged: the kernel
+ * is interpolated in y and then differentiated) with the column basis
+ * |T_j| sum_q w_q n_j . grad L_{c,nu}(y_{j,q}).  alpha = -1/2 gives the right-hand
+ * side (-1/2 I + K) g of the direct Dirichlet formulation eq:cqmdir P:1801-1806.
+ * x, y: device [n_local][M] complex, input panel order, no overlap.  Asynchronous. */
+bem_status bem_apply_double_layer(bem_op op, const bem_c128* x, bem_c128* y, double alpha, void* cuda_stream);
+
 /* R-scaled CQM transforms (eq:omega_n P:436-441, eq:slphelm P:529-540; D2):
  *   forward:  x_freq[l] = sum_{n=0}^{N} R^n x_time[n] e^{-2 pi i n l / L}
  *   inverse:  y_time[n] = R^{-n}/L sum_{l=0}^{L-1} y_freq[l] e^{+2 pi i n l / L}

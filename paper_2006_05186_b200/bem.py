@@ -37,7 +37,7 @@ class SolveStats(C.Structure):
 
 EXPORTS = [
     "bem_last_error", "cqm_frequencies", "bem_build_tree", "bem_tree_get_stats", "bem_tree_export",
-    "bem_tree_destroy", "bem_assemble_h2_aca", "bem_aca_export", "bem_op_destroy", "bem_apply_multifreq",
+    "bem_tree_destroy", "bem_assemble_h2_aca", "bem_aca_export", "bem_op_destroy", "bem_apply_multifreq", "bem_apply_double_layer",
     "cqm_forward", "cqm_inverse", "cqm_solve", "bem_solve_multifreq", "bem_debug_pinned", "bem_debug_fastmath", "bem_debug_fp64_peak",
     "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count", "bem_debug_fp64_peak_ex",
 ]
@@ -63,6 +63,7 @@ def lib():
         "bem_aca_export": [vp, vp, vp, vp],
         "bem_op_destroy": [vp],
         "bem_apply_multifreq": [vp, vp, vp, vp],
+        "bem_apply_double_layer": [vp, vp, vp, d, vp],
         "cqm_forward": [vp, vp, i64, i32, d, vp],
         "cqm_inverse": [vp, vp, i64, i32, d, vp],
         "cqm_solve": [vp, vp, vp, i64, d, d, i32, i32, vp, vp, vp],
@@ -195,6 +196,15 @@ class Operator:
         _check(lib().bem_apply_multifreq(self.h, _p(x), _p(y), _stream(stream)))
         return y
 
+    def apply_dl(self, x, alpha: float = 0.0, y=None, stream=None):
+        """y_t = (alpha I + K(s_{local_l[t]})) x_t (double layer, NEXT-1)."""
+        import torch
+        assert x.dtype == torch.complex128 and x.is_cuda and x.is_contiguous()
+        if y is None:
+            y = torch.empty_like(x)
+        _check(lib().bem_apply_double_layer(self.h, _p(x), _p(y), float(alpha), _stream(stream)))
+        return y
+
     def launch_count(self) -> int:
         n = C.c_int32()
         _check(lib().bem_op_launch_count(self.h, C.byref(n)))
@@ -269,6 +279,20 @@ def debug_pinned(x, device: int = 0):
     e, s, c = np.empty_like(x), np.empty_like(x), np.empty_like(x)
     _check(lib().bem_debug_pinned(_p(x), len(x), _p(e), _p(s), _p(c), int(device)))
     return e, s, c
+
+
+def dirichlet_solve(op: Operator, g_time, R: float, tol: float = 1e-8, restart: int = 50, max_iter: int = 2000,
+                    stream=None):
+    """Direct Dirichlet formulation (eq:cqmdir P:1801-1806), frequency-decoupled
+    (Remark P:1607-1614): V(s_l) q^_l = (-1/2 I + K(s_l)) g^_l for every l,
+    q = Re inverse(q^).  Every step runs in libbem's kernels: K4 forward, the
+    double-layer apply, batched GMRES on V, K4 inverse.  g_time: [N+1][M] real."""
+    import torch
+    N = op.L - 1
+    gf = cqm_forward(g_time.to(torch.complex128).contiguous(), N, R, stream=stream)
+    rhs = op.apply_dl(gf, alpha=-0.5, stream=stream)
+    qf, st = solve_multifreq(op, rhs, tol=tol, restart=restart, max_iter=max_iter, stream=stream)
+    return cqm_inverse(qf, N, R, stream=stream).real.contiguous(), st
 
 
 def debug_fastmath(x, device: int = 0, variant: int = 64):

@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(kPassThreads) down_leaf_kernel(const int32_t* 
                                                                  const double2* __restrict__ yc,
                                                                  const int32_t* __restrict__ perm,
                                                                  double2* __restrict__ y, int64_t M, int nl, int p,
-                                                                 int has_far) {
+                                                                 int has_far, const double2* __restrict__ xc,
+                                                                 double alpha) {
   const int c = leaves[blockIdx.x];
   const int b = cb[c], e = ce[c], n = e - b;
   const int t0 = blockIdx.y * kPassT;
@@ -130,21 +131,33 @@ __global__ void __launch_bounds__(kPassThreads) down_leaf_kernel(const int32_t* 
         acc.y = fma(u, yh[mu].y, acc.y);
       }
     }
+    if (alpha != 0.0) {  // (alpha I + K) x for the double layer
+      const double2 xv = xc[(int64_t)t * M + k];
+      acc.x = fma(alpha, xv.x, acc.x);
+      acc.y = fma(alpha, xv.y, acc.y);
+    }
     y[(int64_t)t * M + perm[k]] = acc;
   }
 }
 
 __global__ void scatter_kernel(const double2* __restrict__ yc, double2* __restrict__ y,
-                               const int32_t* __restrict__ perm, int64_t M, int nl) {
+                               const int32_t* __restrict__ perm, int64_t M, int nl, const double2* __restrict__ xc, double alpha) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= M * nl) return;
   const int64_t t = i / M, k = i - t * M;
-  y[t * M + perm[k]] = yc[i];
+  double2 v = yc[i];
+  if (alpha != 0.0) {
+    v.x = fma(alpha, xc[i].x, v.x);
+    v.y = fma(alpha, xc[i].y, v.y);
+  }
+  y[t * M + perm[k]] = v;
 }
 
 }  // namespace
 
-bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st) {
+// y = V x (dl = false) or y = (alpha I + K) x (dl = true, double layer, NEXT-1): the
+// same coupling tensors / ACA skeleton, K's near field and column basis W^K
+bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st, bool dl, double alpha) {
   Tree& t = *op.tree;
   const int64_t M = t.M;
   const int nl = op.n_local, p = t.p;
@@ -165,7 +178,7 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
   BEM_CK(cudaGetLastError());
   // K1
   {
-    bem_status rs = launch_near(op, xc, yc, st);
+    bem_status rs = launch_near(op, xc, yc, st, dl);
     if (rs != BEM_OK) return rs;
   }
   const bool dense = op.mode == BEM_MODE_DENSE;
@@ -174,7 +187,7 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
   const unsigned tt = (unsigned)((nl + kPassT - 1) / kPassT);
   if (has_far) {
     up_leaf_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, 0, st>>>(t.d_leaves.p, t.d_begin.p, t.d_end.p,
-                                                                             t.d_W.p, xc, xhat, M, nl, p);
+                                                                             dl ? t.d_WK.p : t.d_W.p, xc, xhat, M, nl, p);
     BEM_CK(cudaGetLastError());
     for (int lv = t.depth - 1; lv >= 0; --lv) {
       const int n = (int)t.level_nonleaf[lv].size();
@@ -195,11 +208,11 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
       BEM_CK(cudaGetLastError());
     }
     down_leaf_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, 0, st>>>(
-        t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_UT.p, yhat, yc, t.d_perm.p, y, M, nl, p, 1);
+        t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_UT.p, yhat, yc, t.d_perm.p, y, M, nl, p, 1, xc, dl ? alpha : 0.0);
     BEM_CK(cudaGetLastError());
   } else {
     if (prof) { BEM_CK(cudaEventRecord(op.ev[2], st)); BEM_CK(cudaEventRecord(op.ev[3], st)); }
-    scatter_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(yc, y, t.d_perm.p, M, nl);
+    scatter_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(yc, y, t.d_perm.p, M, nl, xc, dl ? alpha : 0.0);
     BEM_CK(cudaGetLastError());
   }
   if (prof) BEM_CK(cudaEventRecord(op.ev[4], st));
@@ -225,7 +238,27 @@ extern "C" bem_status bem_apply_multifreq(bem_op oh, const bem_c128* x, bem_c128
   BEM_REQ(at.type == cudaMemoryTypeDevice && at.device == op.tree->device,
           "bem_apply_multifreq: y must be device memory on device %d", op.tree->device);
   DeviceGuard dg(op.tree->device);
-  return apply_launch(op, (const double*)x, (double*)y, (cudaStream_t)cuda_stream);
+  return apply_launch(op, (const double*)x, (double*)y, (cudaStream_t)cuda_stream, false, 0.0);
+}
+
+extern "C" bem_status bem_apply_double_layer(bem_op oh, const bem_c128* x, bem_c128* y, double alpha,
+                                             void* cuda_stream) {
+  BEM_REQ(oh && x && y, "bem_apply_double_layer: NULL argument");
+  BEM_REQ(((uintptr_t)x & 15) == 0 && ((uintptr_t)y & 15) == 0,
+          "bem_apply_double_layer: pointers must be 16-byte aligned");
+  Op& op = oh->o;
+  const size_t bytes = (size_t)op.n_local * op.tree->M * 16;
+  BEM_REQ((const char*)x + bytes <= (const char*)y || (const char*)y + bytes <= (const char*)x,
+          "bem_apply_double_layer: x and y overlap");
+  cudaPointerAttributes at;
+  BEM_CK(cudaPointerGetAttributes(&at, x));
+  BEM_REQ(at.type == cudaMemoryTypeDevice && at.device == op.tree->device,
+          "bem_apply_double_layer: x must be device memory on device %d", op.tree->device);
+  BEM_CK(cudaPointerGetAttributes(&at, y));
+  BEM_REQ(at.type == cudaMemoryTypeDevice && at.device == op.tree->device,
+          "bem_apply_double_layer: y must be device memory on device %d", op.tree->device);
+  DeviceGuard dg(op.tree->device);
+  return apply_launch(op, (const double*)x, (double*)y, (cudaStream_t)cuda_stream, true, alpha);
 }
 
 extern "C" bem_status bem_op_launch_count(bem_op oh, int32_t* n) {

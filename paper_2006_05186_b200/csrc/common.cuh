@@ -99,6 +99,8 @@ struct Tree {
   DBuf<double> d_selfJ;  // M    J(T)/(4 pi)
   DBuf<double> d_area;   // M
   DBuf<double> d_U, d_W; // M*p
+  DBuf<double> d_WK;     // M*p double-layer column basis (NEXT-1)
+  DBuf<double> d_nrm;    // M*3 unit normals (cluster order)
   DBuf<double> d_E;      // C*p*p (E of cluster c w.r.t. its parent)
   DBuf<double> d_ET, d_UT;  // transposed E (C*p*p) and U (p*M) for the downward pass
   DBuf<double> d_xi;     // C*3*m
@@ -162,8 +164,8 @@ struct Op {
 };
 
 // launchers (apply.cu, near.cu, far.cu)
-bem_status apply_launch(Op& op, const double* x, double* y, cudaStream_t st);
-bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st);
+bem_status apply_launch(Op& op, const double* x, double* y, cudaStream_t st, bool dl = false, double alpha = 0.0);
+bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st, bool dl = false);
 bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st);
 // fft.cu
 bem_status fft_transform(const double* in, double* out, int64_t M, int N, double R, bool inverse,

@@ -122,6 +122,7 @@ namespace {
 
 struct HostGeom {
   std::vector<double> cen, lo, hi, area, qn, J;  // input order
+  std::vector<double> nrm;  // unit normals (b-a)x(c-a)/|.| in vertex order (double layer, NEXT-1)
 };
 
 // Tree construction with an explicit stack (pre-order ids, left son first).
@@ -268,6 +269,31 @@ void lagrange_3d(const double* xi, int m, const double* x, double* out) {
       for (int kx = 0; kx < m; ++kx) out[kx + m * (ky + m * kz)] = lx[kx] * ly[ky] * lz[kz];
 }
 
+// n . grad of all p = m^3 tensor Lagrange polynomials at x (double-layer column basis)
+void lagrange_grad_n_3d(const double* xi, int m, const double* x, const double* n, double* out) {
+  double l[3][8], d[3][8];
+  for (int a = 0; a < 3; ++a) {
+    const double* xs = xi + a * m;
+    lagrange_1d(xs, m, x[a], l[a]);
+    for (int k = 0; k < m; ++k) {  // l_k'(t) = sum_{i != k} 1/(x_k - x_i) prod_{j != k,i} (t - x_j)/(x_k - x_j)
+      double sum = 0.0;
+      for (int i = 0; i < m; ++i) {
+        if (i == k) continue;
+        double v = 1.0 / (xs[k] - xs[i]);
+        for (int j = 0; j < m; ++j)
+          if (j != k && j != i) v *= (x[a] - xs[j]) / (xs[k] - xs[j]);
+        sum += v;
+      }
+      d[a][k] = sum;
+    }
+  }
+  for (int kz = 0; kz < m; ++kz)
+    for (int ky = 0; ky < m; ++ky)
+      for (int kx = 0; kx < m; ++kx)
+        out[kx + m * (ky + m * kz)] = (n[0] * (d[0][kx] * l[1][ky] * l[2][kz]) + n[1] * (l[0][kx] * d[1][ky] * l[2][kz])) +
+                                      n[2] * (l[0][kx] * l[1][ky] * d[2][kz]);
+}
+
 }  // namespace
 
 extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t* T, int64_t nt, int32_t leaf_size,
@@ -287,6 +313,7 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
   const int64_t M = nt;
   HostGeom g;
   g.cen.resize(3 * M); g.lo.resize(3 * M); g.hi.resize(3 * M); g.area.resize(M); g.qn.resize(21 * M); g.J.resize(M);
+  g.nrm.resize(3 * M);
   for (int64_t i = 0; i < M; ++i) {
     const double* P[3];
     for (int v = 0; v < 3; ++v) {
@@ -305,6 +332,9 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
     const double cx = uy * vz - uz * vy, cy = uz * vx - ux * vz, cz = ux * vy - uy * vx;
     g.area[i] = 0.5 * std::sqrt((cx * cx + cy * cy) + cz * cz);
     BEM_REQ(g.area[i] > 0.0, "bem_build_tree: triangle %lld is degenerate (area <= 0)", (long long)i);
+    g.nrm[3 * i] = cx / (2.0 * g.area[i]);
+    g.nrm[3 * i + 1] = cy / (2.0 * g.area[i]);
+    g.nrm[3 * i + 2] = cz / (2.0 * g.area[i]);
     for (int q = 0; q < 7; ++q)
       for (int a = 0; a < 3; ++a)
         g.qn[21 * i + 3 * q + a] =
@@ -329,7 +359,7 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
   // bases
   t.xi.resize((size_t)C * 3 * m);
   for (int c = 0; c < C; ++c) cheb_nodes(&t.box[6 * c], m, &t.xi[(size_t)c * 3 * m]);
-  std::vector<double> U((size_t)M * p), W((size_t)M * p, 0.0), E((size_t)C * p * p, 0.0), tmp(p);
+  std::vector<double> U((size_t)M * p), W((size_t)M * p, 0.0), WK((size_t)M * p, 0.0), E((size_t)C * p * p, 0.0), tmp(p);
   std::vector<int32_t> leaf_of(M);
   for (int li = 0; li < t.n_leaves; ++li) {
     const int c = t.leaves[li];
@@ -343,6 +373,11 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
         for (int nu = 0; nu < p; ++nu) W[(size_t)k * p + nu] += kRule.w[q] * tmp[nu];
       }
       for (int nu = 0; nu < p; ++nu) W[(size_t)k * p + nu] *= g.area[i];
+      for (int q = 0; q < 7; ++q) {  // double layer: |T_j| sum_q w_q n_j . grad L_nu(y_q)
+        lagrange_grad_n_3d(xi, m, &g.qn[21 * i + 3 * q], &g.nrm[3 * i], tmp.data());
+        for (int nu = 0; nu < p; ++nu) WK[(size_t)k * p + nu] += kRule.w[q] * tmp[nu];
+      }
+      for (int nu = 0; nu < p; ++nu) WK[(size_t)k * p + nu] *= g.area[i];
     }
   }
   for (int c = 0; c < C; ++c) {
@@ -356,7 +391,7 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
     }
   }
   // cluster-ordered panel data
-  std::vector<double> cen((size_t)3 * M), qn((size_t)21 * M), qw((size_t)7 * M), sj(M), area(M);
+  std::vector<double> cen((size_t)3 * M), qn((size_t)21 * M), qw((size_t)7 * M), sj(M), area(M), nrm((size_t)3 * M);
   for (int64_t k = 0; k < M; ++k) {
     const int i = t.perm[k];
     for (int a = 0; a < 3; ++a) cen[3 * k + a] = g.cen[3 * i + a];
@@ -364,6 +399,7 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
     for (int q = 0; q < 7; ++q) qw[7 * k + q] = (kRule.w[q] * g.area[i]) / kFourPi;
     sj[k] = g.J[i] / kFourPi;
     area[k] = g.area[i];
+    for (int a = 0; a < 3; ++a) nrm[3 * k + a] = g.nrm[3 * i + a];
   }
   // near field: per leaf, the flat list of near source panels (cluster order),
   // concatenated column-leaf ranges in partition order
@@ -405,7 +441,7 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
   } while (0)
   UP(d_perm, t.perm); UP(d_begin, t.begin); UP(d_end, t.end); UP(d_son0, t.son0); UP(d_son1, t.son1);
   UP(d_parent, t.parent); UP(d_leaf_of, leaf_of);
-  UP(d_cen, cen); UP(d_qn, qn); UP(d_qw, qw); UP(d_selfJ, sj); UP(d_area, area);
+  UP(d_cen, cen); UP(d_qn, qn); UP(d_qw, qw); UP(d_selfJ, sj); UP(d_area, area); UP(d_nrm, nrm); UP(d_WK, WK);
   // transposed copies for the downward pass (K2): lanes run over lambda / panel k, so
   // E^T[c][mu][lambda] and U^T[mu][k] make its loads coalesced
   std::vector<double> ET(E.size()), UT(U.size());

@@ -32,6 +32,7 @@ struct NearArgs {
   const double* cen;
   const double* qn;
   const double* qw;
+  const double* nrm;  // unit normals (double layer)
   const double* selfJ;
   const double2* s;
   const int32_t* local_l;
@@ -74,7 +75,9 @@ __device__ __noinline__ double2 self_entry(const double* qn, const double* qw, d
   return make_double2(vr, vi);
 }
 
-template <int F, int U, bool TAB, bool LEAN = false, bool T256 = false>
+// DL: double-layer kernel d/dn_y e^{-sr}/(4 pi r) (NEXT-1): per node the factor
+// (x - y).n_y / r^3 and (1 + s r) e^{-s r}; the self panel contributes 0.
+template <int F, int U, bool TAB, bool LEAN = false, bool T256 = false, bool DL = false>
 __device__ __forceinline__ void near_body(const NearArgs& a) {
   constexpr int NT = T256 ? 256 : 64;
   __shared__ double etab[NT];
@@ -143,13 +146,15 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
       for (int f = 0; f < F; ++f) v[f] = make_double2(0.0, 0.0);
       const double* qn = a.qn + 21 * (int64_t)j;
       const double* qw = a.qw + 7 * (int64_t)j;
+      double nx = 0.0, ny = 0.0, nz = 0.0;
+      if (DL) { nx = a.nrm[3 * (int64_t)j]; ny = a.nrm[3 * (int64_t)j + 1]; nz = a.nrm[3 * (int64_t)j + 2]; }
 #pragma unroll U
       for (int q = 0; q < 7; ++q) {
         const double dx = cx - qn[3 * q], dy = cy - qn[3 * q + 1], dz = cz - qn[3 * q + 2];
         const double d2 = dx * dx + dy * dy + dz * dz;
         const double ir = rsqrt(d2);
         const double r = d2 * ir;
-        const double w = qw[q] * ir;
+        const double w = DL ? qw[q] * ((dx * nx + dy * ny) + dz * nz) * (ir * ir * ir) : qw[q] * ir;
 #pragma unroll
         for (int f = 0; f < F; ++f) {
           const double e = (TAB ? (T256 ? fast::exp_neg_tab256(-sre[f] * r, etab) : fast::exp_neg_tab(-sre[f] * r, etab))
@@ -158,8 +163,14 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
           if (TAB && T256) fast::sincos_tab256(sim[f] * r, sctab, &sn, &cs);
           else if (TAB) fast::sincos_tab(sim[f] * r, sctab, &sn, &cs);
           else fast::sincos_(sim[f] * r, &sn, &cs);
-          v[f].x = fma(e, cs, v[f].x);
-          v[f].y = fma(-e, sn, v[f].y);
+          if (DL) {  // (1 + s r) e^{-s r}: (alpha + i beta)(cos - i sin) E
+            const double ea = e * fma(sre[f], r, 1.0), eb = e * (sim[f] * r);
+            v[f].x = fma(ea, cs, fma(eb, sn, v[f].x));
+            v[f].y = fma(eb, cs, fma(-ea, sn, v[f].y));
+          } else {
+            v[f].x = fma(e, cs, v[f].x);
+            v[f].y = fma(-e, sn, v[f].y);
+          }
         }
       }
       if (LEAN) {  // loads after the node loop: fewer live registers, latency covered by other warps
@@ -176,7 +187,7 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
       }
     }
   }
-  if (lane == 0) {
+  if (lane == 0 && !DL) {
     const double c[3] = {cx, cy, cz};
 #pragma unroll 1
     for (int f = 0; f < F; ++f) {
@@ -212,6 +223,11 @@ template <int F, int U, bool TAB, int MINB>
 __global__ void __launch_bounds__(kNearWarps * 32, MINB) near_kernel_minb(NearArgs a) {
   near_body<F, U, TAB>(a);
 }
+// double-layer near field (NEXT-1)
+template <int F>
+__global__ void __launch_bounds__(kNearWarps * 32) near_kernel_dl(NearArgs a) {
+  near_body<F, 7, true, false, false, true>(a);
+}
 // 256-entry exp / sincos tables (one / two polynomial terms fewer); BEM_NEAR_T256
 template <int F>
 __global__ void __launch_bounds__(kNearWarps * 32) near_kernel_t256(NearArgs a) {
@@ -229,7 +245,7 @@ cudaError_t launch(const NearArgs& na, cudaStream_t st) {
 
 }  // namespace
 
-bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st) {
+bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st, bool dl) {
   Tree& t = *op.tree;
   NearArgs na;
   na.M = t.M; na.n_class = op.n_class; na.leaf_of = t.d_leaf_of.p;
@@ -237,14 +253,18 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st) 
   na.near_jb = dense ? op.d_dn_jb.p : t.d_near_jb.p;
   na.near_je = dense ? op.d_dn_je.p : t.d_near_je.p;
   na.near_j = dense ? op.d_dn_j.p : t.d_near_j.p;
-  na.cen = t.d_cen.p; na.qn = t.d_qn.p; na.qw = t.d_qw.p; na.selfJ = t.d_selfJ.p;
+  na.cen = t.d_cen.p; na.qn = t.d_qn.p; na.qw = t.d_qw.p; na.nrm = t.d_nrm.p; na.selfJ = t.d_selfJ.p;
   na.s = (const double2*)op.d_s.p; na.local_l = op.d_local_l.p;
   na.class_t1 = op.d_class_t1.p; na.class_t2 = op.d_class_t2.p; na.mask = op.d_mask; na.xc = xc; na.yc = yc;
   const int F = op.near_f;
   const int U = op.near_unroll;
   const bool T = op.near_tab;
   cudaError_t e;
-  if (F == 3 && U == 7 && T && op.near_t256) {
+  if (dl) {
+    dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + 2) / 3));
+    near_kernel_dl<3><<<g, kNearWarps * 32, 0, st>>>(na);
+    e = cudaGetLastError();
+  } else if (F == 3 && U == 7 && T && op.near_t256) {
     dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + 2) / 3));
     near_kernel_t256<3><<<g, kNearWarps * 32, 0, st>>>(na);
     e = cudaGetLastError();

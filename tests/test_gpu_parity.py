@@ -408,3 +408,87 @@ def test_h2only_on_the_fly_couplings(pb, torch, m, leaf, N):
     lsel = np.unique(np.r_[0, 1, N // 2, N // 2 + 1, N - 1, N])
     yo = oh.apply(O.MODE_H2ONLY, s, x[lsel], lsel)
     assert _rel(y[lsel], yo) <= 1e-10
+
+
+# ---------------------------------------------------------------- NEXT-1: double layer
+@pytest.mark.parametrize("mode", ["dense", "h2only", "h2aca"])
+def test_double_layer_apply_vs_oracle(pb, torch, mode):
+    """(alpha I + K(s_l)) x on a 1280-panel sphere in all three modes vs the
+    oracle's identical operator (<= 1e-10 global relative l2)."""
+    V, T = synth.icosphere(3)
+    N = 32
+    M, L, eps = len(T), N + 1, 1e-6
+    s = pb.cqm_frequencies(N, 2.0)
+    x = synth.random_density(7, L, M)
+    leaf = 10 ** 6 if mode == "dense" else 32
+    m = 1 if mode == "dense" else 3
+    gm = {"dense": pb.BEM_MODE_DENSE, "h2only": pb.BEM_MODE_H2ONLY, "h2aca": pb.BEM_MODE_H2ACA}[mode]
+    om = {"dense": O.MODE_DENSE, "h2only": O.MODE_H2ONLY, "h2aca": O.MODE_H2ACA}[mode]
+    op = pb.Operator(pb.Tree(V, T, leaf, 1.0, m), s, eps, mode=gm)
+    y = op.apply_dl(torch.from_numpy(x).cuda(), alpha=-0.5).cpu().numpy()
+    oh = O.H2(V, T, leaf, 1.0, m)
+    if mode == "h2aca":
+        oh.aca(s, eps)
+    lsel = np.array([0, 1, 7, 16, 17, 31, 32])
+    yo = oh.apply_dl(om, s, x[lsel], lsel, alpha=-0.5)
+    assert _rel(y[lsel], yo) <= 1e-10
+
+
+def test_double_layer_p64_far8(pb, torch):
+    V, T = synth.icosphere(3)
+    N = 256
+    M, L, eps = len(T), N + 1, 1e-6
+    s = pb.cqm_frequencies(N, 2.0)
+    x = synth.random_density(8, L, M)
+    op = pb.Operator(pb.Tree(V, T, 48, 1.0, 4), s, eps)
+    y = op.apply_dl(torch.from_numpy(x).cuda()).cpu().numpy()
+    oh = O.H2(V, T, 48, 1.0, 4)
+    oh.aca(s, eps)
+    lsel = np.array([0, 1, 64, 128, 129, 255, 256])
+    yo = oh.apply_dl(O.MODE_H2ACA, s, x[lsel], lsel)
+    assert _rel(y[lsel], yo) <= 1e-10
+
+
+def test_dirichlet_solve_spherical_wave(pb, torch):
+    """Direct Dirichlet formulation (eq:cqmdir P:1801-1806) on the unit sphere
+    with the paper's spherical wave u = f(t - |x|)/|x|, shifted
+    to reach the sphere right after t = 0.  Under joint refinement of dt and h
+    (Courant dt/h ~ 1): the BEM solution approaches the semi-discrete CQM
+    solution (exact frequency response -(1+s) through the same transforms) at
+    second order in h, and the exact trace -f'(t-1) - f(t-1) as the CQM error
+    falls; the frequency-domain solution agrees with the oracle's GMRES.
+    (At Courant ~0.2 the centroid-collocation V is under-resolved at the
+    strongly damped frequencies |s| h >> 1 and the first-kind solve is not
+    accurate there -- a property of the discretisation.)"""
+    def f(z):
+        return np.where(z > -0.2, np.cos(5 * z + 1) - 1, 0.0)
+
+    def df(z):
+        return np.where(z > -0.2, -5 * np.sin(5 * z + 1), 0.0)
+
+    e_cqm, e_exact = [], []
+    for sub, N in ((2, 8), (3, 16)):
+        V, T = synth.icosphere(sub)
+        M, L = len(T), N + 1
+        Tend = 2.0
+        R = 10.0 ** (-5.0 / N)
+        s = pb.cqm_frequencies(N, Tend, R)
+        z = np.arange(L) * Tend / N - 0.2  # f(t - |x| + shift) on |x| = 1
+        g = np.ascontiguousarray(np.repeat(f(z)[:, None], M, axis=1))
+        op = pb.Operator(pb.Tree(V, T, 10 ** 6, 1.0, 1), s, 1e-8, mode=pb.BEM_MODE_DENSE)
+        q, st = pb.dirichlet_solve(op, torch.from_numpy(g).cuda(), R, tol=1e-10, restart=40)
+        assert st["n_unconverged"] == 0
+        q = q.cpu().numpy()
+        gf = O.forward(g.astype(np.complex128), N, R)
+        q_cqm = O.inverse(-(1 + s)[:, None] * gf, N, R).real.mean(axis=1)
+        q_exact = -df(z) - f(z)
+        e_cqm.append(np.linalg.norm(q.mean(axis=1) - q_cqm) / np.linalg.norm(q_cqm))
+        e_exact.append(np.linalg.norm(q.mean(axis=1) - q_exact) / np.linalg.norm(q_exact))
+        if sub == 2:  # vs the oracle's GMRES on the same system
+            oh = O.H2(V, T, 10 ** 6, 1.0, 1)
+            rhs = oh.apply_dl(O.MODE_DENSE, s, gf, alpha=-0.5)
+            qo, _, _ = oh.gmres(O.MODE_DENSE, s, rhs, tol=1e-10, restart=40)
+            sc = (R ** np.arange(L))[:, None]
+            assert _rel(q * sc, O.inverse(qo, N, R).real * sc) <= 1e-6
+    assert e_cqm[1] < 0.5 * e_cqm[0] and e_cqm[1] < 0.02, e_cqm
+    assert e_exact[1] < 0.5 * e_exact[0], e_exact

@@ -107,9 +107,6 @@ struct Tree {
   DBuf<int32_t> d_leaves;
   // near field per leaf index: [jb, je) into the flat list of near source panels
   DBuf<int32_t> d_near_jb, d_near_je, d_near_j;
-  // K1 staged variant: (leaf, first target) groups of <= 4 targets, leaf end (built lazily)
-  int n_kgroups = 0;
-  DBuf<int32_t> d_kgroups, d_leaf_end;
   // far CSR by row cluster
   std::vector<int32_t> far_ptr, far_sorted;  // far_sorted: block ids grouped by row cluster
   DBuf<int32_t> d_far_ptr, d_far_sorted, d_far_r, d_far_c;
@@ -148,9 +145,6 @@ struct Op {
   int near_f = 3;  // frequency classes per warp (r01 sweep at config 2: F=2 7.77 ms, F=3 6.97 ms, F=4 9.85 ms)
   int near_unroll = 7;
   bool near_tab = true;
-  bool near_staged = false;  // K1 with cp.async-staged source chunks shared by the CTA (env BEM_NEAR_STAGED)
-  bool near_t256 = false;  // K1 with 256-entry exp / sincos tables (env BEM_NEAR_T256)
-  int near_minb = 0;  // K1 __launch_bounds__ min blocks/SM variant (0: compiler's choice; 6, 8)
   bool force_generic = false;
   int far_kernel = 0;                 // 0: auto (far8 for p > 32, far7 otherwise); 8, 7, 6 (DMMA variants)
   size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM

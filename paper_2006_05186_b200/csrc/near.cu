@@ -77,15 +77,14 @@ __device__ __noinline__ double2 self_entry(const double* qn, const double* qw, d
 
 // DL: double-layer kernel d/dn_y e^{-sr}/(4 pi r) (NEXT-1): per node the factor
 // (x - y).n_y / r^3 and (1 + s r) e^{-s r}; the self panel contributes 0.
-template <int F, int U, bool TAB, bool LEAN = false, bool T256 = false, bool DL = false>
+template <int F, int U, bool TAB, bool DL = false>
 __device__ __forceinline__ void near_body(const NearArgs& a) {
-  constexpr int NT = T256 ? 256 : 64;
-  __shared__ double etab[NT];
-  __shared__ double2 sctab[NT];
+  __shared__ double etab[64];
+  __shared__ double2 sctab[64];
   if (TAB) {
-    for (int i = threadIdx.x; i < NT; i += blockDim.x) {
-      etab[i] = T256 ? fast::kExp2Tab256[i] : fast::kExp2Tab[i];
-      sctab[i] = T256 ? fast::kSinCosTab256[i] : fast::kSinCosTab[i];
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+      etab[i] = fast::kExp2Tab[i];
+      sctab[i] = fast::kSinCosTab[i];
     }
     __syncthreads();
   }
@@ -133,13 +132,11 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
       const int j = jn;  // index loaded one iteration ahead (one dependent global load fewer per source)
       if (jj + 32 < je) jn = a.near_j[jj + 32];
       if (j == k) continue;  // self panel below
-      double2 x1[F], x2[F];
-      if (!LEAN) {  // loads issued before the node loop (latency hidden, 4F registers live through it)
+      double2 x1[F], x2[F];  // issued before the node loop: their latency hides behind it
 #pragma unroll
-        for (int f = 0; f < F; ++f) {
-          x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
-          x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
-        }
+      for (int f = 0; f < F; ++f) {
+        x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
+        x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
       }
       double2 v[F];
 #pragma unroll
@@ -157,11 +154,9 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
         const double w = DL ? qw[q] * ((dx * nx + dy * ny) + dz * nz) * (ir * ir * ir) : qw[q] * ir;
 #pragma unroll
         for (int f = 0; f < F; ++f) {
-          const double e = (TAB ? (T256 ? fast::exp_neg_tab256(-sre[f] * r, etab) : fast::exp_neg_tab(-sre[f] * r, etab))
-                                : fast::exp_neg(-sre[f] * r)) * w;
+          const double e = (TAB ? fast::exp_neg_tab(-sre[f] * r, etab) : fast::exp_neg(-sre[f] * r)) * w;
           double sn, cs;
-          if (TAB && T256) fast::sincos_tab256(sim[f] * r, sctab, &sn, &cs);
-          else if (TAB) fast::sincos_tab(sim[f] * r, sctab, &sn, &cs);
+          if (TAB) fast::sincos_tab(sim[f] * r, sctab, &sn, &cs);
           else fast::sincos_(sim[f] * r, &sn, &cs);
           if (DL) {  // (1 + s r) e^{-s r}: (alpha + i beta)(cos - i sin) E
             const double ea = e * fma(sre[f], r, 1.0), eb = e * (sim[f] * r);
@@ -171,13 +166,6 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
             v[f].x = fma(e, cs, v[f].x);
             v[f].y = fma(-e, sn, v[f].y);
           }
-        }
-      }
-      if (LEAN) {  // loads after the node loop: fewer live registers, latency covered by other warps
-#pragma unroll
-        for (int f = 0; f < F; ++f) {
-          x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
-          x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
         }
       }
 #pragma unroll
@@ -218,184 +206,16 @@ template <int F, int U, bool TAB>
 __global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
   near_body<F, U, TAB>(a);
 }
-// occupancy variants (register cap 65536 / (MINB * 128)); selected by BEM_NEAR_MINB
-template <int F, int U, bool TAB, int MINB>
-__global__ void __launch_bounds__(kNearWarps * 32, MINB) near_kernel_minb(NearArgs a) {
-  near_body<F, U, TAB>(a);
-}
 // double-layer near field (NEXT-1)
 template <int F>
 __global__ void __launch_bounds__(kNearWarps * 32) near_kernel_dl(NearArgs a) {
-  near_body<F, 7, true, false, false, true>(a);
+  near_body<F, 7, true, true>(a);
 }
-// 256-entry exp / sincos tables (one / two polynomial terms fewer); BEM_NEAR_T256
-template <int F>
-__global__ void __launch_bounds__(kNearWarps * 32) near_kernel_t256(NearArgs a) {
-  near_body<F, 7, true, false, true>(a);
-}
-
-
-template <int F, int U, bool TAB, int MINB = 0>
+template <int F, int U, bool TAB>
 cudaError_t launch(const NearArgs& na, cudaStream_t st) {
   dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + F - 1) / F));
-  if (MINB == 0) near_kernel<F, U, TAB><<<g, kNearWarps * 32, 0, st>>>(na);
-  else near_kernel_minb<F, U, TAB, (MINB > 0 ? MINB : 1)><<<g, kNearWarps * 32, 0, st>>>(na);
+  near_kernel<F, U, TAB><<<g, kNearWarps * 32, 0, st>>>(na);
   return cudaGetLastError();
-}
-
-// ---------------------------------------------------------- K1 staged variant
-// The 4 warps of a CTA take up to 4 targets of ONE leaf, which share the leaf's
-// near-source list: the sources' quadrature nodes / weights and the x values
-// of the CTA's frequency classes are staged in shared memory in chunks of 32
-// with cp.async, double-buffered, so the loads of chunk c+1 overlap the
-// evaluation of chunk c and are issued once per CTA instead of once per warp.
-constexpr int kSQ = 29;  // doubles per staged source: 21 node coordinates + 7 weights (+1 pad, odd stride)
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-template <int F>
-__global__ void __launch_bounds__(kNearWarps * 32) near_kernel_staged(NearArgs a, const int2* __restrict__ groups,
-                                                                     const int32_t* __restrict__ leaf_end) {
-  constexpr int XS = 2 * F + 1;  // double2 per staged source (odd stride)
-  __shared__ double etab[64];
-  __shared__ double2 sctab[64];
-  __shared__ double sq[2][32 * kSQ];
-  __shared__ double2 sx[2][32 * XS];
-  __shared__ int sjj[2][32];
-  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
-    etab[i] = fast::kExp2Tab[i];
-    sctab[i] = fast::kSinCosTab[i];
-  }
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int2 gr = groups[blockIdx.x];
-  const int li = gr.x;
-  const int64_t k = gr.y + warp;
-  const bool kval = k < leaf_end[li];
-  const int jb = a.near_jb[li], je = a.near_je[li], nsrc = je - jb;
-  const int c0 = blockIdx.y * F;
-  int t1[F], t2[F];
-  double sre[F], sim[F];
-#pragma unroll
-  for (int f = 0; f < F; ++f) {
-    const int c = c0 + f;
-    t1[f] = c < a.n_class ? a.class_t1[c] : -1;
-    t2[f] = c < a.n_class ? a.class_t2[c] : -1;
-    const bool on = t1[f] >= 0 && (a.mask == nullptr || a.mask[t1[f]] || (t2[f] >= 0 && a.mask[t2[f]]));
-    if (t1[f] >= 0 && !on && kval && lane == 0) {  // converged (GMRES mask): zeros
-      a.yc[(int64_t)t1[f] * a.M + k] = make_double2(0.0, 0.0);
-      if (t2[f] >= 0) a.yc[(int64_t)t2[f] * a.M + k] = make_double2(0.0, 0.0);
-    }
-    if (!on) t1[f] = t2[f] = -1;
-    const double2 sv = t1[f] >= 0 ? a.s[a.local_l[t1[f]]] : make_double2(0.0, 0.0);
-    sre[f] = sv.x;
-    sim[f] = sv.y;
-  }
-  // stage chunk c into buffer b: 4 threads per source
-  auto stage = [&](int c, int b) {
-    const int sidx = tid >> 2, part = tid & 3;
-    const int jj = jb + c * 32 + sidx;
-    if (jj < je) {
-      const int j = a.near_j[jj];
-      if (part == 0) sjj[b][sidx] = j;
-      double* dq = &sq[b][sidx * kSQ];
-      const double* gq = a.qn + 21 * (int64_t)j;
-      for (int e = part; e < 21; e += 4) cp_async8(dq + e, gq + e);
-      const double* gw = a.qw + 7 * (int64_t)j;
-      for (int e = part; e < 7; e += 4) cp_async8(dq + 21 + e, gw + e);
-#pragma unroll
-      for (int f = 0; f < F; ++f) {
-        if (part == (2 * f) % 4 && t1[f] >= 0) cp_async16(&sx[b][sidx * XS + 2 * f], a.xc + (int64_t)t1[f] * a.M + j);
-        if (part == (2 * f + 1) % 4 && t2[f] >= 0)
-          cp_async16(&sx[b][sidx * XS + 2 * f + 1], a.xc + (int64_t)t2[f] * a.M + j);
-      }
-    }
-    cp_async_commit();
-  };
-  double2 acc1[F], acc2[F];
-#pragma unroll
-  for (int f = 0; f < F; ++f) { acc1[f] = make_double2(0.0, 0.0); acc2[f] = make_double2(0.0, 0.0); }
-  const int64_t kk = kval ? k : 0;
-  const double cx = a.cen[3 * kk], cy = a.cen[3 * kk + 1], cz = a.cen[3 * kk + 2];
-  const int nch = (nsrc + 31) / 32;
-  if (nch > 0) stage(0, 0);
-  for (int c = 0; c < nch; ++c) {
-    const int b = c & 1;
-    if (c + 1 < nch) {
-      stage(c + 1, b ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const int jj = c * 32 + lane;
-    if (kval && jj < nsrc) {
-      const int j = sjj[b][lane];
-      if (j != k) {
-        const double* qd = &sq[b][lane * kSQ];
-        double2 v[F];
-#pragma unroll
-        for (int f = 0; f < F; ++f) v[f] = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int q = 0; q < 7; ++q) {
-          const double dx = cx - qd[3 * q], dy = cy - qd[3 * q + 1], dz = cz - qd[3 * q + 2];
-          const double d2 = dx * dx + dy * dy + dz * dz;
-          const double ir = rsqrt(d2);
-          const double r = d2 * ir;
-          const double w = qd[21 + q] * ir;
-#pragma unroll
-          for (int f = 0; f < F; ++f) {
-            const double e = fast::exp_neg_tab(-sre[f] * r, etab) * w;
-            double sn, cs;
-            fast::sincos_tab(sim[f] * r, sctab, &sn, &cs);
-            v[f].x = fma(e, cs, v[f].x);
-            v[f].y = fma(-e, sn, v[f].y);
-          }
-        }
-#pragma unroll
-        for (int f = 0; f < F; ++f) {
-          if (t1[f] >= 0) cmac(acc1[f], v[f], sx[b][lane * XS + 2 * f]);
-          if (t2[f] >= 0) cmac_conj(acc2[f], v[f], sx[b][lane * XS + 2 * f + 1]);
-        }
-      }
-    }
-    __syncthreads();  // buffer b is restaged in iteration c + 1
-  }
-  if (!kval) return;
-  if (lane == 0) {
-    const double cc[3] = {cx, cy, cz};
-#pragma unroll 1
-    for (int f = 0; f < F; ++f) {
-      if (t1[f] < 0) continue;
-      const double2 v = self_entry(a.qn + 21 * k, a.qw + 7 * k, a.selfJ[k], cc, sre[f], sim[f]);
-      cmac(acc1[f], v, a.xc[(int64_t)t1[f] * a.M + k]);
-      if (t2[f] >= 0) cmac_conj(acc2[f], v, a.xc[(int64_t)t2[f] * a.M + k]);
-    }
-  }
-#pragma unroll
-  for (int f = 0; f < F; ++f) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      acc1[f].x += __shfl_xor_sync(0xffffffffu, acc1[f].x, off);
-      acc1[f].y += __shfl_xor_sync(0xffffffffu, acc1[f].y, off);
-      acc2[f].x += __shfl_xor_sync(0xffffffffu, acc2[f].x, off);
-      acc2[f].y += __shfl_xor_sync(0xffffffffu, acc2[f].y, off);
-    }
-  }
-#pragma unroll
-  for (int f = 0; f < F; ++f) {
-    if (lane == 2 * f && t1[f] >= 0) a.yc[(int64_t)t1[f] * a.M + k] = acc1[f];
-    if (lane == 2 * f + 1 && t2[f] >= 0) a.yc[(int64_t)t2[f] * a.M + k] = acc2[f];
-  }
 }
 
 }  // namespace
@@ -415,37 +235,11 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st, 
   const int U = op.near_unroll;
   const bool T = op.near_tab;
   cudaError_t e;
-  if (!dl && op.near_staged && T) {
-    if (t.d_kgroups.p == nullptr) {  // (leaf, first target) groups of <= 4 targets; built once per tree
-      std::vector<int32_t> gv, le(t.n_leaves);
-      for (int li = 0; li < t.n_leaves; ++li) {
-        const int c = t.leaves[li];
-        le[li] = t.end[c];
-        for (int k = t.begin[c]; k < t.end[c]; k += kNearWarps) { gv.push_back(li); gv.push_back(k); }
-      }
-      t.n_kgroups = (int)(gv.size() / 2);
-      if (t.d_kgroups.upload(gv) != cudaSuccess || t.d_leaf_end.upload(le) != cudaSuccess) {
-        set_error("launch_near: group upload failed");
-        return BEM_ECUDA;
-      }
-    }
-    dim3 g((unsigned)t.n_kgroups, (unsigned)((na.n_class + 2) / 3));
-    near_kernel_staged<3><<<g, kNearWarps * 32, 0, st>>>(na, (const int2*)t.d_kgroups.p, t.d_leaf_end.p);
-    e = cudaGetLastError();
-  } else if (dl) {
+  if (dl) {
     dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + 2) / 3));
     near_kernel_dl<3><<<g, kNearWarps * 32, 0, st>>>(na);
     e = cudaGetLastError();
-  } else if (F == 3 && U == 7 && T && op.near_t256) {
-    dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + 2) / 3));
-    near_kernel_t256<3><<<g, kNearWarps * 32, 0, st>>>(na);
-    e = cudaGetLastError();
-  } else if (F == 3 && U == 7 && T && op.near_minb == 4) e = launch<3, 7, true, 4>(na, st);
-  else if (F == 3 && U == 7 && T && op.near_minb == 2) e = launch<3, 7, true, 2>(na, st);
-  else if (F == 2 && U == 7 && T && op.near_minb == 4) e = launch<2, 7, true, 4>(na, st);
-  else if (F == 2 && U == 7 && T && op.near_minb == 6) e = launch<2, 7, true, 6>(na, st);
-  else if (F == 2 && U == 7 && T && op.near_minb == 8) e = launch<2, 7, true, 8>(na, st);
-  else if (F == 3) e = T ? (U == 7 ? launch<3, 7, true>(na, st) : launch<3, 1, true>(na, st))
+  } else if (F == 3) e = T ? (U == 7 ? launch<3, 7, true>(na, st) : launch<3, 1, true>(na, st))
                     : (U == 7 ? launch<3, 7, false>(na, st) : launch<3, 1, false>(na, st));
   else if (F == 4) e = T ? launch<4, 1, true>(na, st) : launch<4, 1, false>(na, st);
   else e = T ? (U == 7 ? launch<2, 7, true>(na, st) : launch<2, 1, true>(na, st))

@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--mode", default="h2aca", choices=["h2aca", "h2only"])
+    ap.add_argument("--operator", default="V", choices=["V", "K"],
+                    help="K: the double-layer operator (SURVEY NEXT-1) instead of the single layer")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA-graph replay")
@@ -253,14 +255,15 @@ def main():
     def inv(z):
         return pb.cqm_inverse(z, N, R)
 
+    opfn = op.apply if args.operator == "V" else (lambda z: op.apply_dl(z))
     if world > 1:
-        top = ShardedTimeOperator(rank, world, M, L, op.apply, fwd, inv)
+        top = ShardedTimeOperator(rank, world, M, L, opfn, fwd, inv)
         step = top.step
     elif vshard:
-        step = op.apply
+        step = opfn
     else:
         def step(z):
-            return inv(op.apply(fwd(z)))
+            return inv(opfn(fwd(z)))
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     for _ in range(max(3, args.warmup)):
@@ -400,7 +403,7 @@ def main():
                       f"{statistics.median(ms_eager):.3f} ms (median)") if graph is not None else
                      f"eager launches{'' if graph_error is None else ' (graph capture failed: ' + graph_error + ')'}",
            "near_evals_per_s": evals_near / (kt["near"] * 1e-3) if kt["near"] > 0 else None,
-           "setup_s": {"tree": t_tree, "aca": t_aca}, "mode": args.mode,
+           "setup_s": {"tree": t_tree, "aca": t_aca}, "mode": args.mode, "operator": args.operator,
            "mean_aca_rank": float(op.aca_export()["ranks"].mean()) if mode == pb.BEM_MODE_H2ACA else None}
     if vshard:
         out["config"]["parallelism"] = (f"virtual shard {args.shard_rank} of {args.shard_of}: frequency-domain apply of "

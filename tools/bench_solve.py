@@ -28,6 +28,9 @@ ap.add_argument("--tol", type=float, default=1e-8)
 ap.add_argument("--restart", type=int, default=50)
 ap.add_argument("--max-iter", type=int, default=2000)
 ap.add_argument("--check-freqs", type=int, default=0, help="oracle residual check on this many frequencies")
+ap.add_argument("--dirichlet", action="store_true",
+                help="direct Dirichlet formulation V q = (-1/2 I + K) g (NEXT-1) instead of the indirect V phi = g")
+ap.add_argument("--mode", default="h2aca", choices=["h2aca", "h2only"])
 a = ap.parse_args()
 
 cfg = synth.CONFIGS[a.config]
@@ -39,32 +42,41 @@ s = pb.cqm_frequencies(N, cfg["T"], R)
 t0 = time.perf_counter()
 leaf = cfg["leaf"] if not cfg.get("dense") else 10 ** 6
 tree = pb.Tree(V, T, leaf, cfg["eta"], cfg["m"])
-mode = pb.BEM_MODE_DENSE if cfg.get("dense") else pb.BEM_MODE_H2ACA
+mode = pb.BEM_MODE_DENSE if cfg.get("dense") else (pb.BEM_MODE_H2ACA if a.mode == "h2aca" else pb.BEM_MODE_H2ONLY)
 op = pb.Operator(tree, s, cfg["eps"], mode=mode)
 torch.cuda.synchronize()
 t_setup = time.perf_counter() - t0
 g = torch.from_numpy(synth.pulse(V, T, N, cfg["T"])).cuda()
-pb.cqm_solve(op, g, R, tol=a.tol, restart=a.restart, max_iter=a.max_iter)  # warm-up (allocations, caches)
+
+def solve():
+    if a.dirichlet:
+        return pb.dirichlet_solve(op, g, R, tol=a.tol, restart=a.restart, max_iter=a.max_iter)
+    return pb.cqm_solve(op, g, R, tol=a.tol, restart=a.restart, max_iter=a.max_iter)
+
+
+solve()  # warm-up (allocations, caches)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-phi, st = pb.cqm_solve(op, g, R, tol=a.tol, restart=a.restart, max_iter=a.max_iter)
+phi, st = solve()
 e1.record()
 e1.synchronize()
 ms = e0.elapsed_time(e1)
 # residual re-evaluation through the library's apply: forward(phi) vs forward(g)
 gf = pb.cqm_forward(g.to(torch.complex128), N, R)
 pf = pb.cqm_forward(phi.to(torch.complex128), N, R)
-res = op.apply(pf) - gf
-rel = (torch.linalg.vector_norm(res, dim=1) / torch.linalg.vector_norm(gf, dim=1)).cpu().numpy()
-out = {"config": a.config, "M": M, "L": L, "tol": a.tol, "restart": a.restart, "solve_ms": ms,
+res = op.apply(pf) - (op.apply_dl(gf, alpha=-0.5) if a.dirichlet else gf)
+rhs_n = op.apply_dl(gf, alpha=-0.5) if a.dirichlet else gf
+rel = (torch.linalg.vector_norm(res, dim=1) / torch.linalg.vector_norm(rhs_n, dim=1)).cpu().numpy()
+out = {"config": a.config, "formulation": "direct Dirichlet (NEXT-1)" if a.dirichlet else "indirect V phi = g",
+       "mode": a.mode, "M": M, "L": L, "tol": a.tol, "restart": a.restart, "solve_ms": ms,
        "setup_s": t_setup, "stats": st, "max_rel_residual_relib": float(rel.max()),
        "apply_equivalents_per_s": None}
 if st["iters_sum"]:
     # every GMRES inner iteration applies V(s_l) to the still-active frequencies
     out["frequency_iterations"] = int(st["iters_sum"])
     out["unknowns_x_freq_iterations_per_s"] = M * st["iters_sum"] / (ms * 1e-3)
-if a.check_freqs > 0:
+if a.check_freqs > 0 and not a.dirichlet:
     import oracle as O
     oh = O.H2(V, T, leaf, cfg["eta"], cfg["m"])
     if mode == pb.BEM_MODE_H2ACA:

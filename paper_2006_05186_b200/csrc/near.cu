@@ -56,23 +56,20 @@ __device__ __forceinline__ void cmac_conj(double2& acc, double2 a, double2 b) { 
   acc.y = fma(-a.y, b.x, acc.y);
 }
 
-// self entry V[i,i](s) (rare: once per target and class; libdevice functions)
-__device__ __noinline__ double2 self_entry(const double* qn, const double* qw, double J, const double* c, double sre,
-                                           double sim) {
-  double vr = J - qw[0] * sre, vi = -qw[0] * sim;  // node 0 is the centroid: phi(s,0) = -s
-  for (int q = 1; q < 7; ++q) {
-    const double dx = c[0] - qn[3 * q], dy = c[1] - qn[3 * q + 1], dz = c[2] - qn[3 * q + 2];
-    const double r = sqrt(dx * dx + dy * dy + dz * dz);
-    const double xr = -sre * r, yr = -sim * r;
-    double sn, cs, sh, ch;
-    sincos(yr, &sn, &cs);
-    sincos(0.5 * yr, &sh, &ch);
-    const double re = expm1(xr) * cs - 2.0 * sh * sh;  // Re(e^z - 1), cancellation-free
-    const double im = exp(xr) * sn;
-    vr = fma(qw[q] / r, re, vr);
-    vi = fma(qw[q] / r, im, vi);
-  }
-  return make_double2(vr, vi);
+// self entry V[i,i](s) = J/4pi + sum_q (w_q |T_i|/4pi) phi(s, r_q): computed once per target and
+// class, spread over the lanes of the warp (self_node per node q >= 1)
+// one node's share of the self entry: qw_q phi(s, r_q) / ... (q >= 1); libdevice functions
+__device__ __forceinline__ double2 self_node(const double* qn, const double* qw, const double* c, int q, double sre,
+                                             double sim) {
+  const double dx = c[0] - qn[3 * q], dy = c[1] - qn[3 * q + 1], dz = c[2] - qn[3 * q + 2];
+  const double r = sqrt(dx * dx + dy * dy + dz * dz);
+  const double xr = -sre * r, yr = -sim * r;
+  double sn, cs, sh, ch;
+  sincos(yr, &sn, &cs);
+  sincos(0.5 * yr, &sh, &ch);
+  const double re = expm1(xr) * cs - 2.0 * sh * sh;  // Re(e^z - 1), cancellation-free
+  const double im = exp(xr) * sn;
+  return make_double2(qw[q] / r * re, qw[q] / r * im);
 }
 
 // DL: double-layer kernel d/dn_y e^{-sr}/(4 pi r) (NEXT-1): per node the factor
@@ -175,12 +172,22 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
       }
     }
   }
-  if (lane == 0 && !DL) {
+  if (!DL) {
+    // self panel, spread over the warp: lane (f, q-1) for q = 1..6 evaluates one
+    // node of class f (libdevice expm1 / sincos); the lane with q = 1 also adds
+    // J and the centroid node phi(s,0) = -s.  Summed by the reduction below.
     const double c[3] = {cx, cy, cz};
-#pragma unroll 1
+    const double* qnk = a.qn + 21 * k;
+    const double* qwk = a.qw + 7 * k;
+#pragma unroll
     for (int f = 0; f < F; ++f) {
-      if (o1[f] < 0) continue;
-      const double2 v = self_entry(a.qn + 21 * k, a.qw + 7 * k, a.selfJ[k], c, sre[f], sim[f]);
+      if (o1[f] < 0 || lane < 6 * f || lane >= 6 * f + 6) continue;
+      const int q = 1 + lane - 6 * f;
+      double2 v = self_node(qnk, qwk, c, q, sre[f], sim[f]);
+      if (q == 1) {
+        v.x += a.selfJ[k] - qwk[0] * sre[f];
+        v.y -= qwk[0] * sim[f];
+      }
       cmac(acc1[f], v, a.xc[o1[f] + k]);
       if (o2[f] >= 0) cmac_conj(acc2[f], v, a.xc[o2[f] + k]);
     }

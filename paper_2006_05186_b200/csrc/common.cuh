@@ -142,7 +142,7 @@ struct Op {
   // workspaces
   DBuf<double> d_xc, d_yc, d_xhat, d_yhat;
   // kernel variants (tuning knobs; env BEM_NEAR_F, BEM_FAR_GENERIC read at assembly)
-  int near_f = 3;  // frequency classes per warp (r01 sweep at config 2: F=2 7.77 ms, F=3 6.97 ms, F=4 9.85 ms)
+  int near_f = 4;  // frequency classes per warp (r01 sweeps: F=3 -> 4 after the parallel self term: config 2 6.17 -> 5.89 ms)
   int near_unroll = 7;
   bool near_tab = true;
   bool force_generic = false;

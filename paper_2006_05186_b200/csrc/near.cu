@@ -243,12 +243,14 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st, 
   const bool T = op.near_tab;
   cudaError_t e;
   if (dl) {
-    dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + 2) / 3));
-    near_kernel_dl<3><<<g, kNearWarps * 32, 0, st>>>(na);
+    dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + 3) / 4));
+    near_kernel_dl<4><<<g, kNearWarps * 32, 0, st>>>(na);
     e = cudaGetLastError();
   } else if (F == 3) e = T ? (U == 7 ? launch<3, 7, true>(na, st) : launch<3, 1, true>(na, st))
                     : (U == 7 ? launch<3, 7, false>(na, st) : launch<3, 1, false>(na, st));
-  else if (F == 4) e = T ? launch<4, 1, true>(na, st) : launch<4, 1, false>(na, st);
+  else if (F == 4) e = T ? (U == 7 ? launch<4, 7, true>(na, st) : launch<4, 1, true>(na, st)) : launch<4, 1, false>(na, st);
+  else if (F == 5 && T) e = launch<5, 7, true>(na, st);
+  else if (F == 6 && T) e = launch<6, 7, true>(na, st);
   else e = T ? (U == 7 ? launch<2, 7, true>(na, st) : launch<2, 1, true>(na, st))
              : (U == 7 ? launch<2, 7, false>(na, st) : launch<2, 1, false>(na, st));
   BEM_CK(e);

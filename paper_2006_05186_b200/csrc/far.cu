@@ -1131,12 +1131,15 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
     a.class_t1 = op.d_class_t1.p; a.class_t2 = op.d_class_t2.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
     a.mask = op.d_mask;
     const int U = (p + 31) / 32;
-    const int FC = p <= 32 ? 4 : 2;
+    int FC = p <= 32 ? 4 : 2;
+    if (op.h2o_fc > 0) FC = op.h2o_fc;
     a.FCs = FC;
     const int ntile = (op.n_class + FC - 1) / FC;
     cudaError_t e;
-    if (U == 1) e = launch_h2o<1, 4>(a, op.n_segs, ntile, st);
-    else if (U == 2) e = launch_h2o<2, 2>(a, op.n_segs, ntile, st);
+    if (U == 1) e = FC == 2 ? launch_h2o<1, 2>(a, op.n_segs, ntile, st) : FC == 6 ? launch_h2o<1, 6>(a, op.n_segs, ntile, st)
+                                                                              : launch_h2o<1, 4>(a, op.n_segs, ntile, st);
+    else if (U == 2) e = FC == 3 ? launch_h2o<2, 3>(a, op.n_segs, ntile, st) : FC == 4 ? launch_h2o<2, 4>(a, op.n_segs, ntile, st)
+                                                                                 : launch_h2o<2, 2>(a, op.n_segs, ntile, st);
     else if (U == 3) e = launch_h2o<3, 2>(a, op.n_segs, ntile, st);
     else e = launch_h2o<4, 2>(a, op.n_segs, ntile, st);
     BEM_CK(e);

@@ -1131,7 +1131,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
     a.class_t1 = op.d_class_t1.p; a.class_t2 = op.d_class_t2.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
     a.mask = op.d_mask;
     const int U = (p + 31) / 32;
-    int FC = p <= 32 ? 4 : 2;
+    int FC = p <= 32 ? 6 : 2;  // r01 sweep: p = 27 FC 2/4/6 = 2.45/2.48/2.39 ms; p = 64 FC 2/3/4 = 356/369/383 ms
     if (op.h2o_fc > 0) FC = op.h2o_fc;
     a.FCs = FC;
     const int ntile = (op.n_class + FC - 1) / FC;

@@ -149,9 +149,9 @@ struct Op {
   int far_kernel = 0;                 // 0: auto (far8 for p > 32, far7 otherwise); 8, 7, 6 (DMMA variants)
   size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM
   bool far7_rem_dfma = true;          // p = 27: rows 24..26 on DFMA instead of a padded DMMA tile
-  bool far7_cluster = false;
-  int far8_kc = 0;
-  int h2o_fc = 0;                     // K3' classes per CTA tile (0: 6 for p <= 32, else 2; env BEM_H2O_FC)                    // far8 nu-chunk width (0: automatic)          // DSMEM-shared slices across frequency tiles (measured slower, r01)
+  bool far7_cluster = false;          // DSMEM-shared slices across frequency tiles (measured slower, r01)
+  int far8_kc = 0;                    // far8 nu-chunk width (0: automatic)
+  int h2o_fc = 0;                     // K3' classes per CTA tile (0: 6 for p <= 32, else 2; env BEM_H2O_FC)
   // optional per-local-frequency mask (1 = compute); set only by the GMRES driver so that
   // converged frequencies skip K1 / K3 work (their outputs are then zero)
   const int32_t* d_mask = nullptr;

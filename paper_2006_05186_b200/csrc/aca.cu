@@ -140,6 +140,7 @@ struct AcaArgs {
   double2* Cbuf;  // grid * rcap * pp
   double2* Dbuf;  // grid * rcap * L
   double2* Ebuf;  // grid * L
+  double2* Pbuf;  // grid * rcap * (pp/32 + L/32 + 2): chunk partials of the batched Gram dots
   int32_t* rank;
   int32_t* pivk;
   int32_t* pivq;
@@ -220,6 +221,8 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
   double2* cq = dk + a.rcap;                  // rcap: C[j][q*]
   unsigned* usedq = (unsigned*)(cq + a.rcap); // pp bits
   unsigned* usedk = usedq + (pp + 31) / 32;   // L bits
+  double2* gcs = (double2*)(((uintptr_t)(usedk + (L + 31) / 32) + 15) & ~(uintptr_t)15);  // rcap: <c_j, c>
+  double2* gds = gcs + a.rcap;                                                          // rcap: <d_j, d>
   __shared__ BestPair red[kAcaThreads / 32];
   __shared__ int s_blk, s_k, s_stop;
   __shared__ double s_nrm2;
@@ -300,13 +303,51 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
       __syncthreads();
       const double nc2 = block_psum(pp, [&](int q) { const double v = key(c[q]); return make_double2(v, 0.0); }, part).x;
       const double nd2 = block_psum(L, [&](int l) { const double v = key(d[l]); return make_double2(v, 0.0); }, part).x;
+      // Gram cross terms <c_j, c> <d_j, d> for all j < ell at once: every dot product keeps the
+      // pinned order (sequential within chunks of 32, then left to right over the chunk sums),
+      // but the (j, chunk) partials of all j are computed in one parallel pass (2 barriers
+      // instead of 6 per j; the per-j serial tails run in parallel over j)
       double cross = 0.0;
-      for (int j = 0; j < ell; ++j) {
-        const double2* cj = Cb + (size_t)j * pp;
-        const double2* dj = Db + (size_t)j * L;
-        const double2 gc = block_psum(pp, [&](int q) { return cmulconj(cj[q], c[q]); }, part);
-        const double2 gd = block_psum(L, [&](int l) { return cmulconj(dj[l], d[l]); }, part);
-        cross = add(cross, sub(mul(gc.x, gd.x), mul(gc.y, gd.y)));
+      if (ell > 0) {
+        const int nchc = (pp + 31) >> 5, nchd = (L + 31) >> 5;
+        double2* Pc = a.Pbuf + (size_t)blockIdx.x * a.rcap * (nchc + nchd);
+        double2* Pd = Pc + (size_t)a.rcap * nchc;
+        for (int w = threadIdx.x; w < ell * nchc; w += blockDim.x) {
+          const int j = w / nchc, ch = w - j * nchc;
+          const double2* cj = Cb + (size_t)j * pp;
+          double sr = 0.0, si = 0.0;
+          const int e = min(pp, (ch << 5) + 32);
+          for (int i = ch << 5; i < e; ++i) {
+            const double2 x = cmulconj(cj[i], c[i]);
+            sr = __dadd_rn(sr, x.x);
+            si = __dadd_rn(si, x.y);
+          }
+          Pc[(size_t)j * nchc + ch] = make_double2(sr, si);
+        }
+        for (int w = threadIdx.x; w < ell * nchd; w += blockDim.x) {
+          const int j = w / nchd, ch = w - j * nchd;
+          const double2* dj = Db + (size_t)j * L;
+          double sr = 0.0, si = 0.0;
+          const int e = min(L, (ch << 5) + 32);
+          for (int i = ch << 5; i < e; ++i) {
+            const double2 x = cmulconj(dj[i], d[i]);
+            sr = __dadd_rn(sr, x.x);
+            si = __dadd_rn(si, x.y);
+          }
+          Pd[(size_t)j * nchd + ch] = make_double2(sr, si);
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < ell; j += blockDim.x) {
+          double tr = 0.0, ti = 0.0;
+          for (int ch = 0; ch < nchc; ++ch) { tr = __dadd_rn(tr, Pc[(size_t)j * nchc + ch].x); ti = __dadd_rn(ti, Pc[(size_t)j * nchc + ch].y); }
+          gcs[j] = make_double2(tr, ti);
+          tr = 0.0; ti = 0.0;
+          for (int ch = 0; ch < nchd; ++ch) { tr = __dadd_rn(tr, Pd[(size_t)j * nchd + ch].x); ti = __dadd_rn(ti, Pd[(size_t)j * nchd + ch].y); }
+          gds[j] = make_double2(tr, ti);
+        }
+        __syncthreads();
+        for (int j = 0; j < ell; ++j)  // every thread, same order: the value is only used by thread 0
+          cross = add(cross, sub(mul(gcs[j].x, gds[j].x), mul(gcs[j].y, gds[j].y)));
       }
       const BestPair bn = block_argmax(be, bl, red);
       if (threadIdx.x == 0) {
@@ -409,7 +450,8 @@ bem_status run_aca(Op& op, cudaStream_t st) {
   BEM_CK(op.d_zoff.alloc(nfar));
   for (int attempt = 0; attempt < 8; ++attempt) {
     const int grid = std::max(1, std::min(nfar, nsm * 4));
-    DBuf<double> Cbuf, Dbuf, Ebuf;
+    DBuf<double> Cbuf, Dbuf, Ebuf, Pbuf;
+    BEM_CK(Pbuf.alloc((size_t)grid * rcap * ((pp + 31) / 32 + (L + 31) / 32) * 2));
     BEM_CK(Cbuf.alloc((size_t)grid * rcap * pp * 2));
     BEM_CK(Dbuf.alloc((size_t)grid * rcap * L * 2));
     BEM_CK(Ebuf.alloc((size_t)grid * L * 2));
@@ -423,13 +465,13 @@ bem_status run_aca(Op& op, cudaStream_t st) {
     a.nfar = nfar; a.m = t.m; a.p = p; a.L = L; a.rcap = rcap; a.n_local = op.n_local;
     a.far_r = t.d_far_r.p; a.far_c = t.d_far_c.p; a.xi = t.d_xi.p;
     a.s = (const double2*)op.d_s.p; a.local_l = op.d_local_l.p; a.eps = op.eps;
-    a.Cbuf = (double2*)Cbuf.p; a.Dbuf = (double2*)Dbuf.p; a.Ebuf = (double2*)Ebuf.p;
+    a.Cbuf = (double2*)Cbuf.p; a.Dbuf = (double2*)Dbuf.p; a.Ebuf = (double2*)Ebuf.p; a.Pbuf = (double2*)Pbuf.p;
     a.rank = op.d_rank.p; a.pivk = op.d_pivk.p; a.pivq = op.d_pivq.p; a.zoff = op.d_zoff.p;
     a.Zpool = (double2*)op.d_Z.p; a.pool_used = used.p; a.pool_cap = cap; a.flags = flags.p;
     a.next_block = counter.p;
     const int nchmax = (std::max(pp, L) + 31) / 32 + 1;
     const size_t smem = sizeof(double) * 6 * p + sizeof(double2) * (nchmax + 2 * rcap) +
-                        sizeof(unsigned) * ((pp + 31) / 32 + (L + 31) / 32) + 64;
+                        sizeof(unsigned) * ((pp + 31) / 32 + (L + 31) / 32) + 64 + sizeof(double2) * 2 * rcap + 16;
     BEM_CK(cudaFuncSetAttribute(aca_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     aca_kernel<<<grid, kAcaThreads, smem, st>>>(a);
     BEM_CK(cudaGetLastError());

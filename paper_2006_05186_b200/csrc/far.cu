@@ -155,11 +155,15 @@ __global__ void __launch_bounds__(256, 2) far6_kernel(Far6Args a) {
             const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
             const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
             const double nai = -ai;
+            // two passes: dependent DMMAs on one accumulator are 2*4 instructions apart
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
-              dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
               dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
               dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
             }
           }
@@ -418,11 +422,15 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
             const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
             const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
             const double nai = -ai;
+            // two passes: dependent DMMAs on one accumulator are 2*NJ instructions apart
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
               dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
-              dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
               dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
+            }
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+              dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
               dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
             }
 #pragma unroll
@@ -714,11 +722,15 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
               const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
               const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
               const double nai = -ai;
+              // two passes: dependent DMMAs on one accumulator are 2*NJ instructions apart
 #pragma unroll
               for (int j = 0; j < NJ; ++j) {
                 dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
-                dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
                 dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
+              }
+#pragma unroll
+              for (int j = 0; j < NJ; ++j) {
+                dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
                 dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
               }
 #pragma unroll

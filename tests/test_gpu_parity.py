@@ -536,3 +536,24 @@ def test_full_size_properties(pb, torch, cfg):
     yt = pb.cqm_inverse(op.apply(pb.cqm_forward(xt, N, R)), N, R)
     sc = torch.from_numpy(R ** np.arange(L))[:, None].cuda()
     assert float(torch.linalg.vector_norm(yt.imag * sc) / torch.linalg.vector_norm(yt.real * sc)) <= 1e-8
+
+
+def test_config5_geometry_small(pb, torch):
+    """Config 5's geometry and parameters at small size: two unit spheres 3
+    apart, every face split 1->2 along the median (non-conforming, coplanar
+    halves, AM22), m = 5 (p = 125), leaf 64, eps = 1e-8; K3 on far8 with nu
+    chunks.  Pivots bit-exact and the apply within 1e-10 of the oracle."""
+    V, T = synth.two_spheres(2, split=True)
+    N = 32
+    M, L, eps = len(T), N + 1, 1e-8
+    s = pb.cqm_frequencies(N, 2.0)
+    tree = pb.Tree(V, T, 64, 1.0, 5)
+    op = pb.Operator(tree, s, eps)
+    oh = O.H2(V, T, 64, 1.0, 5)
+    oa = oh.aca(s, eps)
+    ga = op.aca_export()
+    assert np.array_equal(ga["ranks"], oa["ranks"]) and np.array_equal(ga["pivots"], oa["pivots"])
+    x = synth.random_density(5, L, M)
+    y = _apply(pb, torch, op, x)
+    lsel = np.array([0, 1, 16, 17, 32])
+    assert _rel(y[lsel], oh.apply(O.MODE_H2ACA, s, x[lsel], lsel)) <= 1e-10

@@ -1,5 +1,6 @@
+# Quick GPU check: GPU tests + the default bench line.
 set -x
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --config 2 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b2.log 2>&1
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_default.log 2>&1
 echo done

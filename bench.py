@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA-graph replay")
+    ap.add_argument("--transpose", default="peer", choices=["peer", "a2a"],
+                    help="N > 1: peer = transforms fused with the transpose over CUDA-IPC peer memory "
+                         "(cqm_forward_rows / cqm_inverse_rows); a2a = torch.distributed all_to_all_single")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: host-staged all-to-all (testing the multi-rank flow on one GPU only)")
     ap.add_argument("--shard-of", type=int, default=0,
@@ -256,8 +259,20 @@ def main():
         return pb.cqm_inverse(z, N, R)
 
     opfn = op.apply if args.operator == "V" else (lambda z: op.apply_dl(z))
+    transpose = None
     if world > 1:
-        top = ShardedTimeOperator(rank, world, M, L, opfn, fwd, inv)
+        top = None
+        if args.transpose == "peer" and args.operator == "V":
+            try:
+                from paper_2006_05186_b200.dist import PeerTimeOperator
+                top = PeerTimeOperator(rank, world, M, L, op, R, local_rank)
+                transpose = "fused transform + transpose over CUDA-IPC peer memory"
+            except Exception as ex:  # no peer access: fall back to the collective
+                top = None
+                transpose = f"all_to_all_single (peer path unavailable: {ex!r})"
+        if top is None:
+            top = ShardedTimeOperator(rank, world, M, L, opfn, fwd, inv)
+            transpose = transpose or f"all_to_all_single ({args.dist_backend})"
         step = top.step
     elif vshard:
         step = opfn
@@ -404,6 +419,7 @@ def main():
                      f"eager launches{'' if graph_error is None else ' (graph capture failed: ' + graph_error + ')'}",
            "near_evals_per_s": evals_near / (kt["near"] * 1e-3) if kt["near"] > 0 else None,
            "setup_s": {"tree": t_tree, "aca": t_aca}, "mode": args.mode, "operator": args.operator,
+           "transpose": transpose,
            "mean_aca_rank": float(op.aca_export()["ranks"].mean()) if mode == pb.BEM_MODE_H2ACA else None}
     if vshard:
         out["config"]["parallelism"] = (f"virtual shard {args.shard_rank} of {args.shard_of}: frequency-domain apply of "

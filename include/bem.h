@@ -158,6 +158,32 @@ bem_status cqm_inverse(const bem_c128* y_freq, bem_c128* y_time, int64_t M_loc, 
 bem_status cqm_solve(bem_op op, const double* g_time, double* phi_time, int64_t M_loc, double R, double tol,
                      int32_t restart, int32_t max_iter, void* nccl_comm, void* cuda_stream, bem_solve_stats* stats);
 
+/* Transforms fused with the multi-GPU time<->frequency transpose (SURVEY
+ * §8(e)).  The same R-scaled transforms as cqm_forward / cqm_inverse, but
+ * row r of the frequency-domain side is addressed through a host array of
+ * L = N+1 device pointers, which may point into OTHER ranks' buffers (CUDA
+ * IPC handles, see bem_ipc_*; peer memory over NVLink/NVSwitch): one kernel
+ * then computes the transform of this rank's DOF columns and stores frequency
+ * row l straight into the rank that owns l (forward), or reads it back from
+ * the owner (inverse), with no separate all-to-all.
+ *   cqm_forward_rows: x_time device [N+1][M_loc] (this rank's columns) ->
+ *                     out_rows[l][0..M_loc) for every l;
+ *   cqm_inverse_rows: in_rows[l][0..M_loc) for every l -> y_time [N+1][M_loc].
+ * The pointer arrays are copied before the call returns; rows must be
+ * 16-byte aligned device (or peer-mapped) memory.  N + 1 <= 2048.
+ * The caller orders the exchange (e.g. device sync + barrier) across ranks. */
+bem_status cqm_forward_rows(const bem_c128* x_time, int64_t M_loc, bem_c128* const* out_rows, int32_t N, double R,
+                            void* cuda_stream);
+bem_status cqm_inverse_rows(bem_c128* const* in_rows, bem_c128* y_time, int64_t M_loc, int32_t N, double R,
+                            void* cuda_stream);
+/* CUDA IPC handles (64 bytes) for peer row tables. */
+bem_status bem_ipc_get_handle(void* dev_ptr, void* handle_out);
+bem_status bem_ipc_open_handle(const void* handle, int32_t device, void** dev_ptr_out);
+bem_status bem_ipc_close(void* dev_ptr);
+/* Plain cudaMalloc / cudaFree (buffers whose IPC handle maps exactly the buffer). */
+bem_status bem_device_alloc(int64_t bytes, int32_t device, void** out);
+bem_status bem_device_free(void* ptr);
+
 /* Frequency-domain batched GMRES over the op's local frequencies (the
  * per-frequency systems of the decoupled solve, Remark P:1607-1614; reading
  * D10): for every t < n_local solve V(s_{local_l[t]}) phi_t = g_t by

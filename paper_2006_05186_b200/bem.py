@@ -38,7 +38,8 @@ class SolveStats(C.Structure):
 EXPORTS = [
     "bem_last_error", "cqm_frequencies", "bem_build_tree", "bem_tree_get_stats", "bem_tree_export",
     "bem_tree_destroy", "bem_assemble_h2_aca", "bem_aca_export", "bem_op_destroy", "bem_apply_multifreq", "bem_apply_double_layer",
-    "cqm_forward", "cqm_inverse", "cqm_solve", "bem_solve_multifreq", "bem_debug_pinned", "bem_debug_fastmath", "bem_debug_fp64_peak",
+    "cqm_forward", "cqm_inverse", "cqm_forward_rows", "cqm_inverse_rows", "bem_ipc_get_handle",
+    "bem_ipc_open_handle", "bem_ipc_close", "bem_device_alloc", "bem_device_free", "cqm_solve", "bem_solve_multifreq", "bem_debug_pinned", "bem_debug_fastmath", "bem_debug_fp64_peak",
     "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count", "bem_debug_fp64_peak_ex",
 ]
 
@@ -67,6 +68,13 @@ def lib():
         "cqm_forward": [vp, vp, i64, i32, d, vp],
         "cqm_inverse": [vp, vp, i64, i32, d, vp],
         "cqm_solve": [vp, vp, vp, i64, d, d, i32, i32, vp, vp, vp],
+        "cqm_forward_rows": [vp, i64, vp, i32, d, vp],
+        "cqm_inverse_rows": [vp, vp, i64, i32, d, vp],
+        "bem_ipc_get_handle": [vp, vp],
+        "bem_ipc_open_handle": [vp, i32, vp],
+        "bem_ipc_close": [vp],
+        "bem_device_alloc": [i64, i32, vp],
+        "bem_device_free": [vp],
         "bem_solve_multifreq": [vp, vp, vp, d, i32, i32, vp, vp],
         "bem_debug_pinned": [vp, i64, vp, vp, vp, i32],
         "bem_debug_fastmath": [vp, i64, vp, vp, vp, i32, i32],
@@ -196,6 +204,10 @@ class Operator:
         _check(lib().bem_apply_multifreq(self.h, _p(x), _p(y), _stream(stream)))
         return y
 
+    def apply_raw(self, x_ptr: int, y_ptr: int, stream=None):
+        """y = V x on raw device addresses ([n_local][M] complex each), e.g. IPC-shared buffers."""
+        _check(lib().bem_apply_multifreq(self.h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), _stream(stream)))
+
     def apply_dl(self, x, alpha: float = 0.0, y=None, stream=None):
         """y_t = (alpha I + K(s_{local_l[t]})) x_t (double layer, NEXT-1)."""
         import torch
@@ -244,6 +256,65 @@ def cqm_inverse(y_freq, N: int, R: float, out=None, stream=None):
     out = torch.empty_like(y_freq) if out is None else out
     _check(lib().cqm_inverse(_p(y_freq), _p(out), y_freq.shape[1], int(N), float(R), _stream(stream)))
     return out
+
+
+def _row_array(ptrs):
+    arr = (C.c_void_p * len(ptrs))(*[int(p) for p in ptrs])
+    return arr
+
+
+def cqm_forward_rows(x_time, N: int, R: float, out_rows, stream=None):
+    """Forward transform of x_time [N+1][M_loc] whose frequency row l is stored at the
+    device address out_rows[l] (possibly a peer rank's buffer): transform + transpose in one kernel."""
+    import torch
+    assert x_time.dtype == torch.complex128 and x_time.is_cuda and x_time.is_contiguous()
+    assert len(out_rows) == N + 1
+    _check(lib().cqm_forward_rows(_p(x_time), x_time.shape[1], _row_array(out_rows), int(N), float(R),
+                                  _stream(stream)))
+
+
+def cqm_inverse_rows(in_rows, N: int, R: float, M_loc: int, out=None, device=None, stream=None):
+    """Inverse transform reading frequency row l at device address in_rows[l] -> [N+1][M_loc]."""
+    import torch
+    assert len(in_rows) == N + 1
+    if out is None:
+        out = torch.empty((N + 1, M_loc), dtype=torch.complex128, device=device or torch.cuda.current_device())
+    _check(lib().cqm_inverse_rows(_row_array(in_rows), _p(out), int(M_loc), int(N), float(R), _stream(stream)))
+    return out
+
+
+def ipc_handle(t) -> bytes:
+    """64-byte CUDA IPC handle of the allocation holding tensor t (t must start the allocation)."""
+    buf = C.create_string_buffer(64)
+    _check(lib().bem_ipc_get_handle(C.c_void_p(t.data_ptr()), buf))
+    return buf.raw
+
+
+def ipc_handle_ptr(ptr: int) -> bytes:
+    """64-byte CUDA IPC handle of a raw allocation from device_alloc."""
+    buf = C.create_string_buffer(64)
+    _check(lib().bem_ipc_get_handle(C.c_void_p(ptr), buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes, device: int) -> int:
+    out = C.c_void_p()
+    _check(lib().bem_ipc_open_handle(C.c_char_p(handle), int(device), C.byref(out)))
+    return out.value
+
+
+def ipc_close(ptr: int):
+    _check(lib().bem_ipc_close(C.c_void_p(ptr)))
+
+
+def device_alloc(nbytes: int, device: int) -> int:
+    out = C.c_void_p()
+    _check(lib().bem_device_alloc(int(nbytes), int(device), C.byref(out)))
+    return out.value
+
+
+def device_free(ptr: int):
+    _check(lib().bem_device_free(C.c_void_p(ptr)))
 
 
 def cqm_solve(op: Operator, g_time, R: float, tol: float = 1e-8, restart: int = 50, max_iter: int = 2000,

@@ -130,12 +130,26 @@ __device__ void smem_fft(double2* buf, int P, int logP, int NC, const double2* _
   }
 }
 
+// Row addressing of the transform's input and output: row r of the input is
+// in_rows.p[r] (or in + r*M when in_rows == nullptr), likewise for the output.
+// With row pointers into OTHER ranks' buffers (CUDA IPC / NVLink peer memory)
+// the kernel performs the time<->frequency transform and the all-to-all
+// transpose in one pass: the forward transform stores frequency row l of this
+// rank's DOF columns straight into the owner of l (cqm_forward_rows), the
+// inverse reads them back from the owners (cqm_inverse_rows).
+constexpr int kMaxRows = 2048;
+struct RowPtrs {
+  double2* p[kMaxRows];
+};
+
 __global__ void __launch_bounds__(kFftThreads) bluestein_kernel(const double2* __restrict__ in, double2* __restrict__ out,
                                                                int64_t M, int L, int P, int logP, int NC,
                                                                const double2* __restrict__ pre,
                                                                const double2* __restrict__ post,
                                                                const double2* __restrict__ hhat,
-                                                               const double2* __restrict__ tw) {
+                                                               const double2* __restrict__ tw,
+                                                               const RowPtrs* __restrict__ in_rows,
+                                                               const RowPtrs* __restrict__ out_rows) {
   extern __shared__ double2 buf[];
   const int64_t c0 = (int64_t)blockIdx.x * NC;
   const int nc = (int)min((int64_t)NC, M - c0);
@@ -143,7 +157,10 @@ __global__ void __launch_bounds__(kFftThreads) bluestein_kernel(const double2* _
   for (int idx = threadIdx.x; idx < NC * P; idx += blockDim.x) {
     const int n = idx / NC, col = idx % NC;
     double2 v = make_double2(0.0, 0.0);
-    if (n < L && col < nc) v = cm(in[(int64_t)n * M + c0 + col], pre[n]);
+    if (n < L && col < nc) {
+      const double2* row = in_rows ? in_rows->p[n] : in + (int64_t)n * M;
+      v = cm(row[c0 + col], pre[n]);
+    }
     const int rv = (int)(__brev((unsigned)n) >> (32 - logP));
     if (n < P) buf[(size_t)col * P + rv] = v;
   }
@@ -170,13 +187,17 @@ __global__ void __launch_bounds__(kFftThreads) bluestein_kernel(const double2* _
   smem_fft(buf, P, logP, NC, tw, true);
   for (int idx = threadIdx.x; idx < NC * L; idx += blockDim.x) {
     const int j = idx / NC, col = idx % NC;
-    if (col < nc) out[(int64_t)j * M + c0 + col] = cm(buf[(size_t)col * P + j], post[j]);
+    if (col < nc) {
+      double2* row = out_rows ? out_rows->p[j] : out + (int64_t)j * M;
+      row[c0 + col] = cm(buf[(size_t)col * P + j], post[j]);
+    }
   }
 }
 
 }  // namespace
 
-bem_status fft_transform(const double* in, double* out, int64_t M, int N, double R, bool inverse, cudaStream_t st) {
+bem_status fft_transform_rows(const double* in, double* out, int64_t M, int N, double R, bool inverse, cudaStream_t st,
+                              const RowPtrs* in_rows, const RowPtrs* out_rows) {
   Plan* pl = nullptr;
   bem_status rs = get_plan(N, R, inverse, &pl);
   if (rs != BEM_OK) return rs;
@@ -186,10 +207,22 @@ bem_status fft_transform(const double* in, double* out, int64_t M, int N, double
   const unsigned grid = (unsigned)((M + NC - 1) / NC);
   bluestein_kernel<<<grid, kFftThreads, smem, st>>>((const double2*)in, (double2*)out, M, pl->L, pl->P, pl->logP, NC,
                                                     (const double2*)pl->pre.p, (const double2*)pl->post.p,
-                                                    (const double2*)pl->hhat.p, (const double2*)pl->tw.p);
+                                                    (const double2*)pl->hhat.p, (const double2*)pl->tw.p, in_rows,
+                                                    out_rows);
   BEM_CK(cudaGetLastError());
   return BEM_OK;
 }
+
+bem_status fft_transform(const double* in, double* out, int64_t M, int N, double R, bool inverse, cudaStream_t st) {
+  return fft_transform_rows(in, out, M, N, R, inverse, st, nullptr, nullptr);
+}
+
+// row tables live in device memory owned by a small per-thread cache (graph-safe:
+// the table is written with cudaMemcpyAsync on the caller's stream before the kernel)
+struct RowTable {
+  DBuf<double> buf;  // sizeof(RowPtrs) bytes
+};
+static thread_local RowTable g_rows[2];
 
 }  // namespace bem
 
@@ -220,4 +253,88 @@ extern "C" bem_status cqm_forward(const bem_c128* x_time, bem_c128* x_freq, int6
 extern "C" bem_status cqm_inverse(const bem_c128* y_freq, bem_c128* y_time, int64_t M_loc, int32_t N, double R,
                                   void* cuda_stream) {
   return transform_entry(y_freq, y_time, M_loc, N, R, cuda_stream, true);
+}
+
+// host pointer table -> device table (async on the stream; the host array is copied into
+// pinned staging first, so the caller may reuse it immediately)
+static bem_status upload_rows(int which, bem_c128* const* rows, int L, cudaStream_t st, const RowPtrs** dev) {
+  static thread_local RowPtrs* staging[2] = {nullptr, nullptr};
+  RowTable& tb = g_rows[which];
+  if (!tb.buf.p) BEM_CK(tb.buf.alloc((sizeof(RowPtrs) + 7) / 8));
+  if (!staging[which]) BEM_CK(cudaMallocHost((void**)&staging[which], sizeof(RowPtrs)));
+  BEM_CK(cudaStreamSynchronize(st));  // the previous use of this staging slot has been consumed
+  for (int r = 0; r < L; ++r) staging[which]->p[r] = (double2*)rows[r];
+  BEM_CK(cudaMemcpyAsync(tb.buf.p, staging[which], sizeof(double2*) * (size_t)L, cudaMemcpyHostToDevice, st));
+  *dev = (const RowPtrs*)tb.buf.p;
+  return BEM_OK;
+}
+
+extern "C" bem_status cqm_forward_rows(const bem_c128* x_time, int64_t M_loc, bem_c128* const* out_rows, int32_t N,
+                                       double R, void* cuda_stream) {
+  BEM_REQ(x_time && out_rows, "cqm_forward_rows: NULL pointer");
+  BEM_REQ(M_loc >= 1 && N >= 1 && N + 1 <= kMaxRows, "cqm_forward_rows: need M_loc >= 1 and 1 <= N < %d", kMaxRows);
+  BEM_REQ(R > 0.0 && R <= 1.0, "cqm_forward_rows: R must lie in (0,1]");
+  for (int r = 0; r <= N; ++r) BEM_REQ(out_rows[r] != nullptr, "cqm_forward_rows: row %d is NULL", r);
+  cudaPointerAttributes at;
+  BEM_CK(cudaPointerGetAttributes(&at, x_time));
+  BEM_REQ(at.type == cudaMemoryTypeDevice, "cqm_forward_rows: input must be device memory");
+  DeviceGuard dg(at.device);
+  const RowPtrs* dev = nullptr;
+  bem_status rs = upload_rows(0, out_rows, N + 1, (cudaStream_t)cuda_stream, &dev);
+  if (rs != BEM_OK) return rs;
+  return fft_transform_rows((const double*)x_time, nullptr, M_loc, N, R, false, (cudaStream_t)cuda_stream, nullptr, dev);
+}
+
+extern "C" bem_status cqm_inverse_rows(bem_c128* const* in_rows, bem_c128* y_time, int64_t M_loc, int32_t N, double R,
+                                       void* cuda_stream) {
+  BEM_REQ(y_time && in_rows, "cqm_inverse_rows: NULL pointer");
+  BEM_REQ(M_loc >= 1 && N >= 1 && N + 1 <= kMaxRows, "cqm_inverse_rows: need M_loc >= 1 and 1 <= N < %d", kMaxRows);
+  BEM_REQ(R > 0.0 && R <= 1.0, "cqm_inverse_rows: R must lie in (0,1]");
+  for (int r = 0; r <= N; ++r) BEM_REQ(in_rows[r] != nullptr, "cqm_inverse_rows: row %d is NULL", r);
+  cudaPointerAttributes at;
+  BEM_CK(cudaPointerGetAttributes(&at, y_time));
+  BEM_REQ(at.type == cudaMemoryTypeDevice, "cqm_inverse_rows: output must be device memory");
+  DeviceGuard dg(at.device);
+  const RowPtrs* dev = nullptr;
+  bem_status rs = upload_rows(1, in_rows, N + 1, (cudaStream_t)cuda_stream, &dev);
+  if (rs != BEM_OK) return rs;
+  return fft_transform_rows(nullptr, (double*)y_time, M_loc, N, R, true, (cudaStream_t)cuda_stream, dev, nullptr);
+}
+
+// CUDA IPC helpers for the peer row tables (multi-GPU transposes without NCCL)
+extern "C" bem_status bem_ipc_get_handle(void* dev_ptr, void* handle_out /* 64 bytes */) {
+  BEM_REQ(dev_ptr && handle_out, "bem_ipc_get_handle: NULL argument");
+  cudaIpcMemHandle_t h;
+  BEM_CK(cudaIpcGetMemHandle(&h, dev_ptr));
+  static_assert(sizeof(h) == 64, "CUDA IPC handle size");
+  memcpy(handle_out, &h, sizeof(h));
+  return BEM_OK;
+}
+
+extern "C" bem_status bem_ipc_open_handle(const void* handle, int32_t device, void** dev_ptr_out) {
+  BEM_REQ(handle && dev_ptr_out, "bem_ipc_open_handle: NULL argument");
+  DeviceGuard dg(device);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  BEM_CK(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return BEM_OK;
+}
+
+// raw device allocations (own cudaMalloc, so an IPC handle maps exactly this buffer)
+extern "C" bem_status bem_device_alloc(int64_t bytes, int32_t device, void** out) {
+  BEM_REQ(out && bytes > 0, "bem_device_alloc: bad arguments");
+  DeviceGuard dg(device);
+  BEM_CK(cudaMalloc(out, (size_t)bytes));
+  return BEM_OK;
+}
+
+extern "C" bem_status bem_device_free(void* ptr) {
+  if (ptr) BEM_CK(cudaFree(ptr));
+  return BEM_OK;
+}
+
+extern "C" bem_status bem_ipc_close(void* dev_ptr) {
+  BEM_REQ(dev_ptr, "bem_ipc_close: NULL argument");
+  BEM_CK(cudaIpcCloseMemHandle(dev_ptr));
+  return BEM_OK;
 }

@@ -135,3 +135,72 @@ class ShardedSolver(ShardedTimeOperator):
         stats = {"iters_max": int(mx[0]), "resid_max": float(mx[1]), "n_unconverged": int(sm[0]),
                  "iters_sum": int(sm[1])}
         return phi.real.contiguous(), stats
+
+
+class PeerTimeOperator:
+    """Time-domain operator y = inverse(V forward(x)) on G ranks with the
+    time<->frequency transposes fused into the transforms over peer memory
+    (no NCCL all-to-all): every rank exposes two device buffers through CUDA
+    IPC -- its frequency shard's input [L_g][M] and the apply's output
+    [L_g][M] -- and cqm_forward_rows stores frequency row l of this rank's DOF
+    columns directly into the owner of l; cqm_inverse_rows reads the owners'
+    output rows back.  Between the phases the ranks synchronise their devices
+    and meet at a process-group barrier (no kernel waits on another rank).
+    On an NVSwitch box the row stores/loads go over NVLink peer memory."""
+
+    def __init__(self, rank: int, world: int, M: int, L: int, op, R: float, device: int, group=None):
+        import torch
+        import torch.distributed as dist
+        from . import bem as B
+        self.rank, self.G, self.M, self.L, self.R = rank, world, M, L, R
+        self.N = L - 1
+        self.op, self.device, self.group = op, device, group
+        self._torch, self._dist, self._B = torch, dist, B
+        self.local = shard_frequencies(L, world)
+        self.ranges = dof_ranges(M, world)
+        owner = np.empty(L, dtype=np.int64)
+        slot = np.empty(L, dtype=np.int64)
+        for h, fl in enumerate(self.local):
+            owner[fl] = h
+            slot[fl] = np.arange(len(fl))
+        self.owner, self.slot = owner, slot
+        nbytes = max(1, len(self.local[rank])) * M * 16
+        self.xin = B.device_alloc(nbytes, device)
+        self.yout = B.device_alloc(nbytes, device)
+        hs = [None] * world
+        dist.all_gather_object(hs, (B.ipc_handle_ptr(self.xin), B.ipc_handle_ptr(self.yout)), group=group)
+        self.peer_x, self.peer_y = [], []
+        for h in range(world):
+            if h == rank:
+                self.peer_x.append(self.xin)
+                self.peer_y.append(self.yout)
+            else:
+                self.peer_x.append(B.ipc_open(hs[h][0], device))
+                self.peer_y.append(B.ipc_open(hs[h][1], device))
+        b = self.ranges[rank][0]
+        self.out_rows = [self.peer_x[owner[l]] + int((slot[l] * M + b) * 16) for l in range(L)]
+        self.in_rows = [self.peer_y[owner[l]] + int((slot[l] * M + b) * 16) for l in range(L)]
+
+    def _fence(self):
+        self._torch.cuda.synchronize(self.device)
+        self._dist.barrier(group=self.group)
+
+    def step(self, x_loc):
+        """x_loc: [N+1][M_g] complex (this rank's DOFs) -> y_loc [N+1][M_g]."""
+        B = self._B
+        B.cqm_forward_rows(x_loc, self.N, self.R, self.out_rows)
+        self._fence()  # every rank's rows have landed in the owners' input buffers
+        self.op.apply_raw(self.xin, self.yout)
+        self._fence()  # every owner's output is complete
+        y = B.cqm_inverse_rows(self.in_rows, self.N, self.R, x_loc.shape[1], device=x_loc.device)
+        self._fence()  # peers finished reading our output before it is overwritten
+        return y
+
+    def close(self):
+        B = self._B
+        for h in range(self.G):
+            if h != self.rank:
+                B.ipc_close(self.peer_x[h])
+                B.ipc_close(self.peer_y[h])
+        B.device_free(self.xin)
+        B.device_free(self.yout)

@@ -11,7 +11,9 @@ Function-to-paper map (P = /root/reference/PAPER.md):
   dense_matrix               collocation analogue of the Galerkin entries P:584-609
   H2.build                   cluster tree P:807-835, partition P:843-912, bases P:957-978
   H2.aca                     MACA Alg. 2, stop P:1298-1310
-  H2.apply                   eq:lrfinal P:1404-1410 (DENSE / H2ONLY / H2ACA)
+  H2.apply                   eq:lrfinal P:1404-1410 (DENSE / H2ONLY / H2ACA / COMBINED)
+  H2.aca_near                Alg. 3 NEAR branch P:1426-1431, P:1444-1450 (NEXT-4)
+  dense_matrix_pinned        C3 entries in the pinned arithmetic the near MACA reads
   forward / inverse          eq:omega_n P:436-441, eq:slphelm P:529-540
   H2.gmres                   frequency-decoupled solve, Remark P:1607-1614
 """
@@ -24,7 +26,7 @@ import numpy as np
 
 from .build import build as _build
 
-MODE_DENSE, MODE_H2ONLY, MODE_H2ACA = 0, 1, 2
+MODE_DENSE, MODE_H2ONLY, MODE_H2ACA, MODE_COMBINED = 0, 1, 2, 3
 
 _lib = None
 
@@ -73,6 +75,12 @@ def lib():
         L.orc_h2_apply_dl.restype = C.c_int
         L.orc_dense_matrix_dl.argtypes = [vp, vp, i64, d, d, vp]
         L.orc_normals.argtypes = [vp, vp, i64, vp]
+        L.orc_h2_aca_near.argtypes = [vp, vp, i32, d, vp, i64, vp, vp]
+        L.orc_h2_aca_near.restype = i64
+        L.orc_h2_aca_near_export.argtypes = [vp, vp, i64, vp, vp]
+        L.orc_dense_matrix_pinned.argtypes = [vp, vp, i64, d, d, vp]
+        L.orc_pexpm1.argtypes = [d]
+        L.orc_pexpm1.restype = d
         _lib = L
     return _lib
 
@@ -184,6 +192,20 @@ def dense_matrix(V, T, s):
     return A
 
 
+def dense_matrix_pinned(V, T, s):
+    """C3 collocation matrix with every entry in pinned arithmetic (the values
+    the near-field MACA reads, NEXT-4)."""
+    V, T = _f64(V), _i32(T)
+    M = len(T)
+    A = np.empty((M, M), dtype=np.complex128)
+    lib().orc_dense_matrix_pinned(_p(V), _p(T), M, float(np.real(s)), float(np.imag(s)), _p(A))
+    return A
+
+
+def pexpm1(x):
+    return lib().orc_pexpm1(float(x))
+
+
 def dense_matrix_dl(V, T, s):
     """Double-layer collocation matrix K(s) (NEXT-1), K[i,i] = 0."""
     V, T = _f64(V), _i32(T)
@@ -268,6 +290,25 @@ class H2:
         piv = np.empty((tot, 2), dtype=np.int32)
         Z = np.empty(tot * L, dtype=np.complex128)
         lib().orc_h2_aca_export(self.h, _p(blk), nb, _p(piv), _p(Z))
+        return dict(ranks=ranks, pivots=piv, Z=Z, fragile=fragile)
+
+    def aca_near(self, s, eps, blocks=None):
+        """Near-field MACA on the near blocks (Alg. 3 NEAR branch; MODE_COMBINED)."""
+        s = _c128(s)
+        L = len(s)
+        if blocks is None:
+            blk, nb = None, self.n_near
+        else:
+            blk = np.ascontiguousarray(blocks, dtype=np.int32)
+            nb = len(blk)
+        ranks = np.empty(nb, dtype=np.int32)
+        fragile = np.empty(nb, dtype=np.int32)
+        tot = lib().orc_h2_aca_near(self.h, _p(s), L, float(eps), _p(blk), nb, _p(ranks), _p(fragile))
+        if tot < 0:
+            raise RuntimeError("oracle aca_near: far ACA was assembled for another L")
+        piv = np.empty((tot, 2), dtype=np.int32)
+        Z = np.empty(tot * L, dtype=np.complex128)
+        lib().orc_h2_aca_near_export(self.h, _p(blk), nb, _p(piv), _p(Z))
         return dict(ranks=ranks, pivots=piv, Z=Z, fragile=fragile)
 
     def apply(self, mode, s, x, lsel=None):

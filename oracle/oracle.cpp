@@ -276,6 +276,64 @@ static C2 pkernel(double r, C2 s) {
   return {(E * cs) * inv, -((E * sn) * inv)};
 }
 
+// Pinned expm1 (self entry of the NEAR tensor, Alg. 3 P:1414-1453 / NEXT-4):
+// |x| < 1/2: x * sum_{k=1..19} x^{k-1}/k! (Horner in fma); else pexp(x) - 1.
+static double pexpm1(double x) {
+  if (x > -0.5 && x < 0.5) {
+    double q = P_INVFACT[19];
+    for (int j = 18; j >= 1; --j) q = std::fma(q, x, P_INVFACT[j]);
+    return x * q;
+  }
+  return pexp(x) - 1.0;
+}
+
+// Pinned phi(s,r) = (e^{-sr}-1)/r, r > 0, in the cancellation-free form of C3:
+// Re = expm1(x) cos y - 2 sin^2(y/2), Im = e^x sin y, z = x + iy = -s r.
+static C2 pphi(double r, C2 s) {
+  double x = -(s.re * r), y = -(s.im * r);
+  double sy, cy, sh, chh;
+  psincos(y, &sy, &cy);
+  psincos(0.5 * y, &sh, &chh);
+  double re = pexpm1(x) * cy - 2.0 * (sh * sh);
+  double im = pexp(x) * sy;
+  return {re / r, im / r};
+}
+
+static const double INV4PI = 0x1.45f306dc9c883p-4;  // 1/(4 pi), correctly rounded
+
+// Pinned collocation entry V(s)[i,j] of C3 (the NEAR procedure of Alg. 3,
+// P:1444-1450, collocation reading): every value the near-field MACA reads.
+//   i != j: sum_{q=0..6} (w_q |T_j|) * pkernel(|y_{j,q} - c_i|; s), q ascending;
+//   i == j: ((J_i + |T_i| acc.re) / 4pi, (|T_i| acc.im) / 4pi) with
+//           acc = sum_q w_q phi_q, phi_0 = -s (node 0 is the centroid), phi_q = pphi(r_q, s).
+static C2 pentry(const Geometry& g, int64_t i, int64_t j, C2 s) {
+  const double* ci = &g.cen[3 * i];
+  double ar = 0.0, ai = 0.0;
+  if (i != j) {
+    for (int q = 0; q < 7; ++q) {
+      const double* y = &g.node[21 * j + 3 * q];
+      double dx = y[0] - ci[0], dy = y[1] - ci[1], dz = y[2] - ci[2];
+      double r = std::sqrt((dx * dx + dy * dy) + dz * dz);
+      C2 k = pkernel(r, s);
+      double wa = RULE.w[q] * g.area[j];
+      ar = ar + wa * k.re;
+      ai = ai + wa * k.im;
+    }
+    return {ar, ai};
+  }
+  ar = ar + RULE.w[0] * (-s.re);
+  ai = ai + RULE.w[0] * (-s.im);
+  for (int q = 1; q < 7; ++q) {
+    const double* y = &g.node[21 * j + 3 * q];
+    double dx = y[0] - ci[0], dy = y[1] - ci[1], dz = y[2] - ci[2];
+    double r = std::sqrt((dx * dx + dy * dy) + dz * dz);
+    C2 f = pphi(r, s);
+    ar = ar + RULE.w[q] * f.re;
+    ai = ai + RULE.w[q] * f.im;
+  }
+  return {(g.J[i] + g.area[i] * ar) * INV4PI, (g.area[i] * ai) * INV4PI};
+}
+
 // Pinned summation: sequential within chunks of 32, then left to right.
 static double psum(const std::vector<double>& v) {
   double tot = 0.0;
@@ -342,6 +400,13 @@ struct H2 {
   std::vector<C2> s;  // frequencies used by the ACA
   int L = 0;
   bool aca_done = false;
+  // near-field MACA per near block (Alg. 3 NEAR branch, BEM_MODE_COMBINED / NEXT-4)
+  std::vector<int> nrank, npivk, npivq;
+  std::vector<int64_t> npivoff, nzoff;
+  std::vector<C2> nZ;
+  std::vector<int64_t> nsoff;  // pivot slices C_{b,t} = V_{k_t}[b] (the tensor C_b of eq:lrfinal), t-major
+  std::vector<C2> nS;
+  bool near_done = false;
 };
 
 static void build_cluster(H2& h, int begin, int end, int level, int parent) {
@@ -640,7 +705,25 @@ static void aca_block(const double* xr, const double* xc, int m, int p, const st
 // ---------------------------------------------------------------------------
 // C11. The apply y_l = V_l x_l in three modes (eq:lrfinal P:1404-1410).
 // ---------------------------------------------------------------------------
-enum { MODE_DENSE = 0, MODE_H2ONLY = 1, MODE_H2ACA = 2 };
+// MODE_COMBINED: Alg. 3 in full (eq:lrfinal P:1404-1410): MACA skeletons on the
+// far blocks (P+) AND on the near blocks (P-: V[b] ~ C_b x_3 D_b), NEXT-4.
+enum { MODE_DENSE = 0, MODE_H2ONLY = 1, MODE_H2ACA = 2, MODE_COMBINED = 3 };
+
+// Entry q = a_loc * n_c + k_loc, frequency l of the near block tensor V[b]
+// (block b = (R, C) of P-, rows/cols in cluster order), pinned; l > L/2 is the
+// conjugate of l' = L - l (C2 reading: mirrored values are defined, not evaluated).
+static C2 near_aca_entry(const H2& h, size_t b, int q, const std::vector<C2>& s, int l) {
+  int L = (int)s.size(), half = L / 2;
+  bool mir = l > half;
+  int ll = mir ? L - l : l;
+  const Cluster& R = h.cl[h.nearR[b]];
+  const Cluster& Cc = h.cl[h.nearC[b]];
+  int nc = Cc.end - Cc.begin;
+  int a = R.begin + q / nc, k = Cc.begin + q % nc;
+  C2 v = pentry(h.g, h.perm[a], h.perm[k], s[ll]);
+  if (mir) v.im = -v.im;
+  return v;
+}
 
 // op = 0: single layer V(s_l); op = 1: double layer K(s_l) (NEXT-1): the same
 // coupling tensors and ACA, column basis WK and near entries entry_dl.
@@ -740,6 +823,24 @@ static void apply_one(const H2& h, int mode, cplx s_l, int l, const std::vector<
     for (size_t b = 0; b < h.nearR.size(); ++b) {
       const Cluster& R = h.cl[h.nearR[b]];
       const Cluster& Cc = h.cl[h.nearC[b]];
+      if (mode == MODE_COMBINED && op == 0) {
+        // V_l[b] ~ sum_t Z_b[t,l] V_{k_t}[b] (skeleton form of eq:maca, pivot slices pinned)
+        const int nr = R.end - R.begin, nc = Cc.end - Cc.begin;
+        for (int t = 0; t < h.nrank[b]; ++t) {
+          const C2* S = &h.nS[h.nsoff[b] + (size_t)t * nr * nc];  // V_{k_t}[b], row-major
+          const C2 z = h.nZ[h.nzoff[b] + (size_t)t * h.L + l];
+          const cplx zc(z.re, z.im);
+          for (int a = R.begin; a < R.end; ++a) {
+            cplx acc(0.0, 0.0);
+            for (int k = Cc.begin; k < Cc.end; ++k) {
+              const C2 v = S[(size_t)(a - R.begin) * nc + (k - Cc.begin)];
+              acc += cplx(v.re, v.im) * x[k];
+            }
+            y[a] += zc * acc;
+          }
+        }
+        continue;
+      }
       for (int a = R.begin; a < R.end; ++a) {
         cplx acc(0.0, 0.0);
         for (int k = Cc.begin; k < Cc.end; ++k) acc += ent(h.perm[a], h.perm[k]) * x[k];
@@ -993,6 +1094,7 @@ void orc_h2_export_bases(void* hp, double* U, double* W, double* E, double* xi) 
 int64_t orc_h2_aca(void* hp, const double* s_in, int32_t L, double eps, const int32_t* blocks, int64_t nblk,
                    int32_t* ranks, int32_t* fragile) {
   H2& h = *(H2*)hp;
+  if (h.near_done && h.L != L) h.near_done = false;
   h.L = L;
   h.s.resize(L);
   for (int l = 0; l < L; ++l) h.s[l] = C2{s_in[2 * l], s_in[2 * l + 1]};
@@ -1026,6 +1128,83 @@ int64_t orc_h2_aca(void* hp, const double* s_in, int32_t L, double eps, const in
   return tot;
 }
 
+// Near-field MACA (Alg. 3 NEAR branch) over all
+// near blocks, or the first nblk of `blocks`.  Same Alg. 2 and readings as
+// the far blocks; entries from pentry.  Returns the sum of ranks.
+int64_t orc_h2_aca_near(void* hp, const double* s_in, int32_t L, double eps, const int32_t* blocks, int64_t nblk,
+                        int32_t* ranks, int32_t* fragile) {
+  H2& h = *(H2*)hp;
+  if (h.aca_done && h.L != L) return -1;
+  h.L = L;
+  h.s.resize(L);
+  for (int l = 0; l < L; ++l) h.s[l] = C2{s_in[2 * l], s_in[2 * l + 1]};
+  int64_t nnear = (int64_t)h.nearR.size();
+  std::vector<int64_t> list;
+  if (blocks) list.assign(blocks, blocks + nblk); else { list.resize(nnear); for (int64_t b = 0; b < nnear; ++b) list[b] = b; }
+  std::vector<AcaOut> res(list.size());
+  std::vector<std::vector<C2>> slices(list.size());
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t t = 0; t < (int64_t)list.size(); ++t) {
+    const int64_t b = list[t];
+    const int pp = (h.cl[h.nearR[b]].end - h.cl[h.nearR[b]].begin) * (h.cl[h.nearC[b]].end - h.cl[h.nearC[b]].begin);
+    aca_generic([&](int q, int l) { return near_aca_entry(h, (size_t)b, q, h.s, l); }, pp, L, eps, res[t]);
+    for (size_t j = 0; j < res[t].k.size(); ++j)
+      for (int q = 0; q < pp; ++q) slices[t].push_back(near_aca_entry(h, (size_t)b, q, h.s, res[t].k[j]));
+  }
+  h.nrank.assign(nnear, 0); h.npivoff.assign(nnear, 0); h.nzoff.assign(nnear, 0); h.nsoff.assign(nnear, 0);
+  h.npivk.clear(); h.npivq.clear(); h.nZ.clear(); h.nS.clear();
+  std::vector<int64_t> where(nnear, -1);
+  for (size_t t = 0; t < list.size(); ++t) where[list[t]] = (int64_t)t;
+  int64_t tot = 0;
+  for (int64_t b = 0; b < nnear; ++b) {
+    h.npivoff[b] = (int64_t)h.npivk.size();
+    h.nzoff[b] = (int64_t)h.nZ.size();
+    h.nsoff[b] = (int64_t)h.nS.size();
+    if (where[b] < 0) continue;
+    h.nS.insert(h.nS.end(), slices[where[b]].begin(), slices[where[b]].end());
+    AcaOut& o = res[where[b]];
+    h.nrank[b] = (int)o.k.size();
+    tot += h.nrank[b];
+    for (size_t t = 0; t < o.k.size(); ++t) { h.npivk.push_back(o.k[t]); h.npivq.push_back(o.q[t]); }
+    h.nZ.insert(h.nZ.end(), o.Z.begin(), o.Z.end());
+  }
+  if (ranks) for (int64_t t = 0; t < (int64_t)list.size(); ++t) ranks[t] = h.nrank[list[t]];
+  if (fragile) for (int64_t t = 0; t < (int64_t)list.size(); ++t) fragile[t] = res[t].fragile;
+  h.near_done = true;
+  return tot;
+}
+
+void orc_h2_aca_near_export(void* hp, const int32_t* blocks, int64_t nblk, int32_t* pivots, double* Z) {
+  H2& h = *(H2*)hp;
+  int64_t pz = 0, pp = 0;
+  for (int64_t t = 0; t < nblk; ++t) {
+    int64_t b = blocks ? blocks[t] : t;
+    for (int j = 0; j < h.nrank[b]; ++j) {
+      if (pivots) { pivots[2 * pp] = h.npivk[h.npivoff[b] + j]; pivots[2 * pp + 1] = h.npivq[h.npivoff[b] + j]; }
+      ++pp;
+    }
+    if (Z) for (int64_t j = 0; j < (int64_t)h.nrank[b] * h.L; ++j) {
+      Z[2 * pz] = h.nZ[h.nzoff[b] + j].re; Z[2 * pz + 1] = h.nZ[h.nzoff[b] + j].im; ++pz;
+    }
+  }
+}
+
+// Pinned collocation matrix (pentry) at one frequency, input order.
+void orc_dense_matrix_pinned(const double* V, const int32_t* T, int64_t M, double sre, double sim, double* A) {
+  Geometry g;
+  make_geometry(V, T, M, g);
+  C2 s{sre, sim};
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t j = 0; j < M; ++j) {
+      C2 v = pentry(g, i, j, s);
+      A[2 * (i * M + j)] = v.re;
+      A[2 * (i * M + j) + 1] = v.im;
+    }
+}
+
+double orc_pexpm1(double x) { return pexpm1(x); }
+
 // pivots for the listed blocks (same order as the orc_h2_aca call), Z likewise.
 void orc_h2_aca_export(void* hp, const int32_t* blocks, int64_t nblk, int32_t* pivots, double* Z) {
   H2& h = *(H2*)hp;
@@ -1046,7 +1225,8 @@ void orc_h2_aca_export(void* hp, const int32_t* blocks, int64_t nblk, int32_t* p
 int orc_h2_apply(void* hp, int32_t mode, const double* s_in, int32_t L, const int32_t* lsel, int32_t nsel,
                  const double* x, double* y) {
   H2& h = *(H2*)hp;
-  if (mode == MODE_H2ACA && (!h.aca_done || h.L != L)) return -1;
+  if ((mode == MODE_H2ACA || mode == MODE_COMBINED) && (!h.aca_done || h.L != L)) return -1;
+  if (mode == MODE_COMBINED && !h.near_done) return -1;
   std::vector<cplx> s(L);
   for (int l = 0; l < L; ++l) s[l] = cplx(s_in[2 * l], s_in[2 * l + 1]);
   int64_t M = h.g.M;
@@ -1062,7 +1242,8 @@ int orc_h2_apply(void* hp, int32_t mode, const double* s_in, int32_t L, const in
 int orc_h2_apply_dl(void* hp, int32_t mode, const double* s_in, int32_t L, const int32_t* lsel, int32_t nsel,
                     const double* x, double* y, double alpha) {
   H2& h = *(H2*)hp;
-  if (mode == MODE_H2ACA && (!h.aca_done || h.L != L)) return -1;
+  if ((mode == MODE_H2ACA || mode == MODE_COMBINED) && (!h.aca_done || h.L != L)) return -1;
+  if (mode == MODE_COMBINED && !h.near_done) return -1;
   std::vector<cplx> s(L);
   for (int l = 0; l < L; ++l) s[l] = cplx(s_in[2 * l], s_in[2 * l + 1]);
   int64_t M = h.g.M;
@@ -1107,7 +1288,8 @@ int orc_h2_gmres(void* hp, int32_t mode, const double* s_in, int32_t L, const in
                  const double* b, double* x, double tol, int32_t restart, int32_t maxit, int32_t* iters,
                  double* relres) {
   H2& h = *(H2*)hp;
-  if (mode == MODE_H2ACA && (!h.aca_done || h.L != L)) return -1;
+  if ((mode == MODE_H2ACA || mode == MODE_COMBINED) && (!h.aca_done || h.L != L)) return -1;
+  if (mode == MODE_COMBINED && !h.near_done) return -1;
   std::vector<cplx> s(L);
   for (int l = 0; l < L; ++l) s[l] = cplx(s_in[2 * l], s_in[2 * l + 1]);
   int64_t M = h.g.M;

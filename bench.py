@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--mode", default="h2aca", choices=["h2aca", "h2only"])
+    ap.add_argument("--mode", default="h2aca", choices=["h2aca", "h2only", "combined"],
+                    help="combined: Alg. 3 in full, near blocks MACA-compressed too (SURVEY NEXT-4)")
     ap.add_argument("--operator", default="V", choices=["V", "K"],
                     help="K: the double-layer operator (SURVEY NEXT-1) instead of the single layer")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -231,7 +232,8 @@ def main():
     cfg, V, T, N, L, R = workload(args.config)
     M = len(T)
     s = pb.cqm_frequencies(N, cfg["T"], R)
-    mode = pb.BEM_MODE_H2ACA if args.mode == "h2aca" else pb.BEM_MODE_H2ONLY
+    mode = {"h2aca": pb.BEM_MODE_H2ACA, "h2only": pb.BEM_MODE_H2ONLY, "combined": pb.BEM_MODE_COMBINED}[args.mode]
+    aca_far = mode in (pb.BEM_MODE_H2ACA, pb.BEM_MODE_COMBINED)
     t0 = time.perf_counter()
     tree = pb.Tree(V, T, cfg["leaf"], cfg["eta"], cfg["m"], device=local_rank)
     t_tree = time.perf_counter() - t0
@@ -373,13 +375,21 @@ def main():
     n_class = len({min(l, L - l) for l in local})
     kt = {k: v / args.steps for k, v in acc.items()}
     launches = op.launch_count() + 2
-    if mode == pb.BEM_MODE_H2ACA:
+    if aca_far:
         rk = op.aca_export()["ranks"]
         flops_far = 8.0 * float(rk.sum()) * stats["p"] ** 2 * nl
     else:  # plain H^2: one kernel evaluation per (block entry, frequency class) + the complex MACs
         flops_far = 75.0 * stats["far_blocks"] * stats["p"] ** 2 * n_class + 8.0 * stats["far_blocks"] * stats["p"] ** 2 * nl
     evals_near = 7.0 * stats["nnz_near"] * n_class
     flops_near = 75.0 * evals_near  # SURVEY §8(d) model: ~75 FP64 flops per complex exponential + MACs
+    near_rank = None
+    if mode == pb.BEM_MODE_COMBINED:  # K1m: 8 flops per (slice entry, term, frequency) on DMMA
+        rkn = op.aca_export_near()["ranks"].astype(np.float64)
+        ex = tree.export()
+        sz = ex["clusters"][:, 1] - ex["clusters"][:, 0]
+        nrnc = sz[ex["near"][:, 0]].astype(np.float64) * sz[ex["near"][:, 1]]
+        flops_near = 8.0 * float((rkn * nrnc).sum()) * nl
+        near_rank = float(rkn.mean())
     peaks = {}
     for m_, name in ((0, "dfma"), (1, "dmma")):
         try:
@@ -387,7 +397,11 @@ def main():
         except Exception:
             peaks[name] = None
     dom = "coupling" if kt["coupling"] >= kt["near"] else "near"
-    if dom == "coupling" and mode != pb.BEM_MODE_H2ACA:
+    if dom == "near" and mode == pb.BEM_MODE_COMBINED:
+        fl = flops_near
+        peak = peaks["dmma"] or FP64_PEAK_DERIVED / 1e12
+        bound, src = "tensor", "measured in this run: mma.sync.m8n8k4.f64 (DMMA) loop (bem_debug_fp64_peak_ex mode 1)"
+    elif dom == "coupling" and not aca_far:
         fl = flops_far
         peak = FP64_PEAK_DERIVED / 1e12
         bound, src = "alu", "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §7); 75 flops/evaluation model"
@@ -401,8 +415,9 @@ def main():
         peak = FP64_PEAK_DERIVED / 1e12
         bound, src = "alu", "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §7)"
     achieved = fl / (kt[dom] * 1e-3) / 1e12
-    kname = {"coupling": ("K3 far7/far8_kernel (+seg_reduce)" if mode == pb.BEM_MODE_H2ACA
-                          else "K3' h2o_kernel (+seg_reduce)"), "near": "K1 near_kernel"}[dom]
+    kname = {"coupling": ("K3 far7/far8_kernel (+seg_reduce)" if aca_far
+                          else "K3' h2o_kernel (+seg_reduce)"),
+             "near": "K1m nearm_kernel" if mode == pb.BEM_MODE_COMBINED else "K1 near_kernel"}[dom]
     roof = {"bound": bound, "kernel": kname, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": traffic_bytes(args.config, dom), "peak_source": src,
             "algorithmic_flops_per_launch": fl,
@@ -417,10 +432,12 @@ def main():
            "timing": ("CUDA-graph replay of the whole step (captured once after warm-up); eager step "
                       f"{statistics.median(ms_eager):.3f} ms (median)") if graph is not None else
                      f"eager launches{'' if graph_error is None else ' (graph capture failed: ' + graph_error + ')'}",
-           "near_evals_per_s": evals_near / (kt["near"] * 1e-3) if kt["near"] > 0 else None,
+           "near_evals_per_s": (evals_near / (kt["near"] * 1e-3) if kt["near"] > 0 and mode != pb.BEM_MODE_COMBINED
+                                else None),
            "setup_s": {"tree": t_tree, "aca": t_aca}, "mode": args.mode, "operator": args.operator,
            "transpose": transpose,
-           "mean_aca_rank": float(op.aca_export()["ranks"].mean()) if mode == pb.BEM_MODE_H2ACA else None}
+           "mean_aca_rank": float(op.aca_export()["ranks"].mean()) if aca_far else None,
+           "mean_near_aca_rank": near_rank}
     if vshard:
         out["config"]["parallelism"] = (f"virtual shard {args.shard_rank} of {args.shard_of}: frequency-domain apply of "
                                          f"{len(local)} of {L} frequencies on 1 GPU (no transforms, no all-to-all); "

@@ -47,7 +47,10 @@ enum {
   BEM_ESTATE = -6   /* handle misuse (wrong device, tree destroyed before its ops) */
 };
 
-enum { BEM_MODE_H2ACA = 0, BEM_MODE_H2ONLY = 1, BEM_MODE_DENSE = 2 };
+/* BEM_MODE_COMBINED: Alg. 3 in full (eq:lrfinal P:1404-1410 for both
+ * b in P+ and b in P-): the near blocks are MACA-compressed across frequency too
+ * (SURVEY §8(f) NEXT-4), instead of evaluated on the fly per apply. */
+enum { BEM_MODE_H2ACA = 0, BEM_MODE_H2ONLY = 1, BEM_MODE_DENSE = 2, BEM_MODE_COMBINED = 3 };
 
 typedef struct { double re, im; } bem_c128;
 typedef struct bem_tree_s* bem_tree; /* panels, cluster tree, P+/P-, U, W, E, boxes; one device */
@@ -102,7 +105,12 @@ bem_status bem_tree_destroy(bem_tree t);
  *   aca_eps > 0: MACA tolerance (Alg. 2, stop rule P:1288);
  *   mode: BEM_MODE_H2ACA (the product), BEM_MODE_H2ONLY (couplings evaluated
  *         per frequency, no ACA; plain-H^2 comparison path), BEM_MODE_DENSE
- *         (every leaf pair is evaluated as near field).
+ *         (every leaf pair is evaluated as near field), BEM_MODE_COMBINED (H2ACA
+ *         plus MACA of every near block: Alg. 3 NEAR branch P:1426-1431, entries
+ *         V[b][i,j](s) of the NEAR procedure P:1444-1450 in the collocation reading,
+ *         evaluated in pinned arithmetic; stores the pivot slices V_{k_t}[b], i.e.
+ *         16 * sum_b r_b n_r n_c bytes -- the tensor C_b of eq:lrfinal).
+ *         The double-layer apply of a COMBINED op keeps its near field exact.
  * The ACA runs over ALL L frequencies on the device with pinned arithmetic
  * (bit-reproducible pivots) and keeps Z columns for local_l only.
  * Synchronous on return.  EINVAL: L < 1, s NULL, local index out of range or
@@ -113,6 +121,11 @@ bem_status bem_assemble_h2_aca(bem_tree t, const bem_c128* s, int32_t L, const i
  * order (q = mu*p + nu, mode-3 unfolding P:1322-1334).  Either may be NULL.
  * *total_rank (may be NULL) receives sum ranks.  ESTATE for non-ACA modes. */
 bem_status bem_aca_export(bem_op op, int32_t* ranks, int32_t* pivots, int64_t* total_rank);
+/* Near-block skeletons of a BEM_MODE_COMBINED op: ranks host [near_blocks];
+ * pivots host [sum ranks][2] = (k_l, q_l), q = i_loc * n_c + j_loc with i_loc /
+ * j_loc the row / column panel offsets inside the block's clusters (cluster
+ * order), blocks in bem_tree_export's near_pairs order.  ESTATE otherwise. */
+bem_status bem_aca_export_near(bem_op op, int32_t* ranks, int32_t* pivots, int64_t* total_rank);
 bem_status bem_op_destroy(bem_op op); /* NULL-safe */
 
 /* y_t = V(s_{local_l[t]}) x_t for t < n_local (P:529-540 operators V_l).

@@ -14,7 +14,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libbem.so")
 
-BEM_MODE_H2ACA, BEM_MODE_H2ONLY, BEM_MODE_DENSE = 0, 1, 2
+BEM_MODE_H2ACA, BEM_MODE_H2ONLY, BEM_MODE_DENSE, BEM_MODE_COMBINED = 0, 1, 2, 3
 BEM_ENOCONV = -5
 _lib = None
 
@@ -37,7 +37,7 @@ class SolveStats(C.Structure):
 
 EXPORTS = [
     "bem_last_error", "cqm_frequencies", "bem_build_tree", "bem_tree_get_stats", "bem_tree_export",
-    "bem_tree_destroy", "bem_assemble_h2_aca", "bem_aca_export", "bem_op_destroy", "bem_apply_multifreq", "bem_apply_double_layer",
+    "bem_tree_destroy", "bem_assemble_h2_aca", "bem_aca_export", "bem_aca_export_near", "bem_op_destroy", "bem_apply_multifreq", "bem_apply_double_layer",
     "cqm_forward", "cqm_inverse", "cqm_forward_rows", "cqm_inverse_rows", "bem_ipc_get_handle",
     "bem_ipc_open_handle", "bem_ipc_close", "bem_device_alloc", "bem_device_free", "cqm_solve", "bem_solve_multifreq", "bem_debug_pinned", "bem_debug_fastmath", "bem_debug_fp64_peak",
     "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count", "bem_debug_fp64_peak_ex",
@@ -62,6 +62,7 @@ def lib():
         "bem_tree_destroy": [vp],
         "bem_assemble_h2_aca": [vp, vp, i32, vp, i32, d, i32, vp, vp],
         "bem_aca_export": [vp, vp, vp, vp],
+        "bem_aca_export_near": [vp, vp, vp, vp],
         "bem_op_destroy": [vp],
         "bem_apply_multifreq": [vp, vp, vp, vp],
         "bem_apply_double_layer": [vp, vp, vp, d, vp],
@@ -192,6 +193,16 @@ class Operator:
         _check(lib().bem_aca_export(self.h, _p(ranks), None, C.byref(tot)))
         piv = np.empty((tot.value, 2), dtype=np.int32)
         _check(lib().bem_aca_export(self.h, None, _p(piv), None))
+        return dict(ranks=ranks, pivots=piv)
+
+    def aca_export_near(self):
+        """Near-block skeletons of a BEM_MODE_COMBINED operator (Alg. 3 NEAR branch)."""
+        nn = self.tree.stats["near_blocks"]
+        ranks = np.empty(nn, dtype=np.int32)
+        tot = C.c_int64()
+        _check(lib().bem_aca_export_near(self.h, _p(ranks), None, C.byref(tot)))
+        piv = np.empty((tot.value, 2), dtype=np.int32)
+        _check(lib().bem_aca_export_near(self.h, None, _p(piv), None))
         return dict(ranks=ranks, pivots=piv)
 
     def apply(self, x, y=None, stream=None):

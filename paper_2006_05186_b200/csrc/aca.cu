@@ -121,6 +121,61 @@ __device__ __forceinline__ double dist(const double* a, const double* b) {
   return __dsqrt_rn(add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)));
 }
 
+// 1/k!, k = 0..19, correctly rounded (pinned expm1 of the self entry).
+__device__ __constant__ double kInvFact[20] = {
+    0x1.0000000000000p+0, 0x1.0000000000000p+0, 0x1.0000000000000p-1, 0x1.5555555555555p-3,
+    0x1.5555555555555p-5, 0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
+    0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22, 0x1.ae64567f544e4p-26,
+    0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33, 0x1.93974a8c07c9dp-37, 0x1.ae7f3e733b81fp-41,
+    0x1.ae7f3e733b81fp-45, 0x1.952c77030ad4ap-49, 0x1.6827863b97d97p-53, 0x1.2f49b46814157p-57};
+
+// expm1: |x| < 1/2 -> x * sum_{k=1..19} x^{k-1}/k! (Horner in fma), else exp(x) - 1.
+__device__ double expm1_(double x) {
+  if (x > -0.5 && x < 0.5) {
+    double q = kInvFact[19];
+    for (int j = 18; j >= 1; --j) q = fma(q, x, kInvFact[j]);
+    return mul(x, q);
+  }
+  return sub(exp_(x), 1.0);
+}
+
+// phi(s,r) = (e^{-sr} - 1)/r, r > 0: Re = expm1(x) cos y - 2 sin^2(y/2), Im = e^x sin y, x + iy = -s r.
+__device__ double2 phi(double r, double sre, double sim) {
+  const double x = -mul(sre, r), y = -mul(sim, r);
+  double sy, cy, sh, ch;
+  sincos_(y, &sy, &cy);
+  sincos_(mul(0.5, y), &sh, &ch);
+  const double re = sub(mul(expm1_(x), cy), mul(2.0, mul(sh, sh)));
+  const double im = mul(exp_(x), sy);
+  return make_double2(__ddiv_rn(re, r), __ddiv_rn(im, r));
+}
+
+// Collocation entry V(s)[i,j] (C3; the NEAR procedure of Alg. 3) in pinned
+// arithmetic.  ci: centroid of panel i; cj: 21 node coordinates, |T_j|, J(T_j) of panel j.
+__device__ double2 near_entry(const double* ci, const double* cj, bool self, double sre, double sim,
+                              const double* w) {
+  double ar = 0.0, ai = 0.0;
+  const double area = cj[21];
+  if (!self) {
+    for (int q = 0; q < 7; ++q) {
+      const double2 k = kernel(dist(ci, cj + 3 * q), sre, sim);
+      const double wa = mul(w[q], area);
+      ar = add(ar, mul(wa, k.x));
+      ai = add(ai, mul(wa, k.y));
+    }
+    return make_double2(ar, ai);
+  }
+  ar = add(ar, mul(w[0], -sre));  // node 0 is the centroid: phi = -s
+  ai = add(ai, mul(w[0], -sim));
+  for (int q = 1; q < 7; ++q) {
+    const double2 f = phi(dist(ci, cj + 3 * q), sre, sim);
+    ar = add(ar, mul(w[q], f.x));
+    ai = add(ai, mul(w[q], f.y));
+  }
+  constexpr double kInv4Pi = 0x1.45f306dc9c883p-4;
+  return make_double2(mul(add(cj[22], mul(area, ar)), kInv4Pi), mul(mul(area, ai), kInv4Pi));
+}
+
 }  // namespace pinned
 
 namespace {
@@ -131,9 +186,22 @@ constexpr int kMaxChunks = 8192;   // pp/32 upper bound for smem partials (m <= 
 
 struct AcaArgs {
   int nfar, m, p, L, rcap, n_local;
-  const int32_t* far_r;
+  int ppmax, geo;  // largest unfolding row count; doubles of staged block geometry
+  const int32_t* far_r;  // block row / column clusters (far or near list)
   const int32_t* far_c;
   const double* xi;
+  // near blocks (combined mode): cluster ranges and cluster-ordered panel data
+  const int32_t* cbegin;
+  const int32_t* cend;
+  const double* cen;
+  const double* qn;
+  const double* area;
+  const double* J;
+  double w[7];
+  double2* Spool;                  // pivot slices V_{k_t}[b]
+  unsigned long long* spool_used;
+  unsigned long long spool_cap;
+  int64_t* soff;
   const double2* s;
   const int32_t* local_l;
   double eps;
@@ -207,20 +275,21 @@ __device__ double2 block_psum(int n, F v, double2* part) {
   return r;
 }
 
+template <bool NEAR>
 __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
   using namespace pinned;
   extern __shared__ unsigned char smem_raw[];
-  const int p = a.p, m = a.m, pp = p * p, L = a.L;
+  const int p = a.p, m = a.m, L = a.L;
   const int half = L / 2;
   // shared layout
-  double* xr = (double*)smem_raw;             // p*3
-  double* xc = xr + 3 * p;                    // p*3
-  double2* part = (double2*)(xc + 3 * p);     // max(pp, L)/32 + 1
-  const int nchmax = (max(pp, L) + 31) / 32 + 1;
+  double* xr = (double*)smem_raw;             // far: p*3 row nodes; near: 3 per row panel
+  double* xc = xr + 3 * p;                    // far: p*3 column nodes
+  double2* part = (double2*)(xr + a.geo);     // max(ppmax, L)/32 + 1
+  const int nchmax = (max(a.ppmax, L) + 31) / 32 + 1;
   double2* dk = part + nchmax;                // rcap: D[j][k]
   double2* cq = dk + a.rcap;                  // rcap: C[j][q*]
-  unsigned* usedq = (unsigned*)(cq + a.rcap); // pp bits
-  unsigned* usedk = usedq + (pp + 31) / 32;   // L bits
+  unsigned* usedq = (unsigned*)(cq + a.rcap); // ppmax bits
+  unsigned* usedk = usedq + (a.ppmax + 31) / 32;   // L bits
   double2* gcs = (double2*)(((uintptr_t)(usedk + (L + 31) / 32) + 15) & ~(uintptr_t)15);  // rcap: <c_j, c>
   double2* gds = gcs + a.rcap;                                                          // rcap: <d_j, d>
   __shared__ BestPair red[kAcaThreads / 32];
@@ -228,10 +297,9 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
   __shared__ double s_nrm2;
   __shared__ long long s_off;
 
-  double2* Cb = a.Cbuf + (size_t)blockIdx.x * a.rcap * pp;
+  double2* Cb = a.Cbuf + (size_t)blockIdx.x * a.rcap * a.ppmax;
   double2* Db = a.Dbuf + (size_t)blockIdx.x * a.rcap * L;
   double2* Eb = a.Ebuf + (size_t)blockIdx.x * L;
-  const int rmax = min(L, pp);
 
   for (;;) {
     if (threadIdx.x == 0) s_blk = atomicAdd(a.next_block, 1);
@@ -240,12 +308,27 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
     __syncthreads();
     if (b >= a.nfar) break;
     const int rc = a.far_r[b], cc = a.far_c[b];
-    for (int i = threadIdx.x; i < p; i += blockDim.x) {
-      const double* xir = a.xi + (size_t)rc * 3 * m;
-      const double* xic = a.xi + (size_t)cc * 3 * m;
-      xr[3 * i + 0] = xir[i % m]; xr[3 * i + 1] = xir[m + (i / m) % m]; xr[3 * i + 2] = xir[2 * m + i / (m * m)];
-      xc[3 * i + 0] = xic[i % m]; xc[3 * i + 1] = xic[m + (i / m) % m]; xc[3 * i + 2] = xic[2 * m + i / (m * m)];
+    int pp, nr = 0, nc = 0, r0 = 0, c0 = 0;
+    if constexpr (NEAR) {
+      r0 = a.cbegin[rc]; nr = a.cend[rc] - r0;
+      c0 = a.cbegin[cc]; nc = a.cend[cc] - c0;
+      pp = nr * nc;
+      for (int i = threadIdx.x; i < 3 * nr; i += blockDim.x) xr[i] = a.cen[3 * (size_t)r0 + i];
+      double* gc = xr + 3 * nr;  // per column panel: 21 node coordinates, area, J
+      for (int i = threadIdx.x; i < 23 * nc; i += blockDim.x) {
+        const int j = i / 23, e = i - 23 * j;
+        gc[i] = e < 21 ? a.qn[21 * (size_t)(c0 + j) + e] : (e == 21 ? a.area[c0 + j] : a.J[c0 + j]);
+      }
+    } else {
+      pp = p * p;
+      for (int i = threadIdx.x; i < p; i += blockDim.x) {
+        const double* xir = a.xi + (size_t)rc * 3 * m;
+        const double* xic = a.xi + (size_t)cc * 3 * m;
+        xr[3 * i + 0] = xir[i % m]; xr[3 * i + 1] = xir[m + (i / m) % m]; xr[3 * i + 2] = xir[2 * m + i / (m * m)];
+        xc[3 * i + 0] = xic[i % m]; xc[3 * i + 1] = xic[m + (i / m) % m]; xc[3 * i + 2] = xic[2 * m + i / (m * m)];
+      }
     }
+    const int rmax = min(L, pp);
     for (int i = threadIdx.x; i < (pp + 31) / 32; i += blockDim.x) usedq[i] = 0u;
     for (int i = threadIdx.x; i < (L + 31) / 32; i += blockDim.x) usedk[i] = 0u;
     if (threadIdx.x == 0) { s_k = 0; s_nrm2 = 0.0; s_stop = 0; }
@@ -254,8 +337,14 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
     auto entry = [&](int q, int l) -> double2 {
       const bool mir = l > half;
       const int ll = mir ? L - l : l;
-      const double r = dist(&xr[3 * (q / p)], &xc[3 * (q % p)]);
-      double2 v = kernel(r, a.s[ll].x, a.s[ll].y);
+      double2 v;
+      if constexpr (NEAR) {
+        const int i = q / nc, j = q - i * nc;
+        v = near_entry(&xr[3 * i], &xr[3 * nr + 23 * j], r0 + i == c0 + j, a.s[ll].x, a.s[ll].y, a.w);
+      } else {
+        const double r = dist(&xr[3 * (q / p)], &xc[3 * (q % p)]);
+        v = kernel(r, a.s[ll].x, a.s[ll].y);
+      }
       if (mir) v.y = -v.y;
       return v;
     };
@@ -310,7 +399,7 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
       double cross = 0.0;
       if (ell > 0) {
         const int nchc = (pp + 31) >> 5, nchd = (L + 31) >> 5;
-        double2* Pc = a.Pbuf + (size_t)blockIdx.x * a.rcap * (nchc + nchd);
+        double2* Pc = a.Pbuf + (size_t)blockIdx.x * a.rcap * ((a.ppmax + 31) / 32 + nchd);
         double2* Pd = Pc + (size_t)a.rcap * nchc;
         for (int w = threadIdx.x; w < ell * nchc; w += blockDim.x) {
           const int j = w / nchc, ch = w - j * nchc;
@@ -403,6 +492,28 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
         }
       }
     }
+    if constexpr (NEAR) {
+      // pivot slices V_{k_t}[b] (raw tensor columns, the apply's C_b), re-evaluated
+      __shared__ long long s_soff;
+      if (threadIdx.x == 0) {
+        s_soff = -1;
+        if (off >= 0) {
+          const unsigned long long need = (unsigned long long)ell * (unsigned long long)pp;
+          const unsigned long long so = atomicAdd(a.spool_used, need);
+          if (so + need > a.spool_cap) atomicOr(a.flags, 4); else s_soff = (long long)so;
+        }
+        a.soff[b] = s_soff;
+      }
+      __syncthreads();
+      const long long so = s_soff;
+      if (so >= 0) {
+        const int32_t* kp = a.pivk + (size_t)b * a.rcap;
+        for (int idx = threadIdx.x; idx < ell * pp; idx += blockDim.x) {
+          const int t = idx / pp, q = idx - t * pp;
+          a.Spool[so + idx] = entry(q, kp[t]);
+        }
+      }
+    }
     __syncthreads();
   }
 }
@@ -420,83 +531,130 @@ __global__ void debug_pinned_kernel(const double* x, int64_t n, double* e, doubl
 using namespace bem;
 
 namespace {
-bem_status run_aca(Op& op, cudaStream_t st) {
+// near = false: far blocks (P+, coupling tensors); near = true: near blocks (P-,
+// combined mode), whose pivot slices are stored as well.
+bem_status run_aca(Op& op, cudaStream_t st, bool near) {
   Tree& t = *op.tree;
-  const int nfar = (int)t.far_r.size();
-  op.ranks.assign(nfar, 0);
-  if (nfar == 0) return BEM_OK;
-  const int p = t.p, pp = p * p, L = op.L;
+  const int nblk = near ? (int)t.near_r.size() : (int)t.far_r.size();
+  std::vector<int32_t>& ranks_out = near ? op.nranks : op.ranks;
+  ranks_out.assign(nblk, 0);
+  if (nblk == 0) return BEM_OK;
+  const int p = t.p, L = op.L;
+  const int ppmax = near ? t.max_leaf * t.max_leaf : p * p;
+  const int geo = near ? 26 * t.max_leaf : 6 * p;
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, t.device);
   // scratch rank cap and Z-pool size: generous first guesses (a retry recomputes the
   // whole ACA: config 5 hit both the old 96 rank cap and the 40-per-block pool
   // estimate), the pool is shrunk to its exact size afterwards
-  int rcap = std::min(std::min(L, pp), 128);
-  unsigned long long cap = (unsigned long long)nfar * 64ull * (unsigned long long)op.n_local;
+  int rcap = std::min(std::min(L, ppmax), 128);
+  unsigned long long cap = (unsigned long long)nblk * 64ull * (unsigned long long)op.n_local;
+  unsigned long long scap = 0;
+  if (near) {
+    scap = 0;
+    for (int b = 0; b < nblk; ++b)
+      scap += 40ull * (unsigned long long)(t.end[t.near_r[b]] - t.begin[t.near_r[b]]) *
+              (unsigned long long)(t.end[t.near_c[b]] - t.begin[t.near_c[b]]);
+  }
   {
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
-      const size_t scratch = (size_t)std::max(1, std::min(nfar, nsm * 4)) * rcap * ((size_t)pp + L) * 16;
+      const size_t scratch = (size_t)std::max(1, std::min(nblk, nsm * 4)) * rcap * ((size_t)ppmax + L) * 16;
       const unsigned long long lim = fr > scratch ? (unsigned long long)((fr - scratch) * 0.7 / 16) : 0ull;
-      if (lim > 0 && cap > lim) cap = lim;
+      if (lim > 0 && cap + scap > lim) {
+        const double f = (double)lim / (double)(cap + scap);
+        cap = (unsigned long long)(cap * f);
+        scap = (unsigned long long)(scap * f);
+      }
     }
   }
   DBuf<int32_t> flags, counter;
   DBuf<unsigned long long> used;
   BEM_CK(flags.alloc(1));
   BEM_CK(counter.alloc(1));
-  BEM_CK(used.alloc(1));
-  BEM_CK(op.d_rank.alloc(nfar));
-  BEM_CK(op.d_zoff.alloc(nfar));
+  BEM_CK(used.alloc(2));
+  DBuf<int32_t>& d_rank = near ? op.d_nrank : op.d_rank;
+  DBuf<int32_t>& d_pivk = near ? op.d_npivk : op.d_pivk;
+  DBuf<int32_t>& d_pivq = near ? op.d_npivq : op.d_pivq;
+  DBuf<int64_t>& d_zoff = near ? op.d_nzoff : op.d_zoff;
+  DBuf<double>& d_Z = near ? op.d_nZ : op.d_Z;
+  BEM_CK(d_rank.alloc(nblk));
+  BEM_CK(d_zoff.alloc(nblk));
+  if (near) BEM_CK(op.d_nsoff.alloc(nblk));
+  std::vector<double> wq(7);
+  {
+    const double r15 = std::sqrt(15.0);
+    const double w1 = (155.0 + r15) / 1200.0, w2 = (155.0 - r15) / 1200.0;
+    const double W[7] = {9.0 / 40.0, w1, w1, w1, w2, w2, w2};  // the 7-point rule of host.cu (C1)
+    for (int q = 0; q < 7; ++q) wq[q] = W[q];
+  }
   for (int attempt = 0; attempt < 8; ++attempt) {
-    const int grid = std::max(1, std::min(nfar, nsm * 4));
+    const int grid = std::max(1, std::min(nblk, nsm * 4));
     DBuf<double> Cbuf, Dbuf, Ebuf, Pbuf;
-    BEM_CK(Pbuf.alloc((size_t)grid * rcap * ((pp + 31) / 32 + (L + 31) / 32) * 2));
-    BEM_CK(Cbuf.alloc((size_t)grid * rcap * pp * 2));
+    BEM_CK(Pbuf.alloc((size_t)grid * rcap * ((ppmax + 31) / 32 + (L + 31) / 32) * 2));
+    BEM_CK(Cbuf.alloc((size_t)grid * rcap * ppmax * 2));
     BEM_CK(Dbuf.alloc((size_t)grid * rcap * L * 2));
     BEM_CK(Ebuf.alloc((size_t)grid * L * 2));
-    BEM_CK(op.d_pivk.alloc((size_t)nfar * rcap));
-    BEM_CK(op.d_pivq.alloc((size_t)nfar * rcap));
-    BEM_CK(op.d_Z.alloc((size_t)cap * 2));
+    BEM_CK(d_pivk.alloc((size_t)nblk * rcap));
+    BEM_CK(d_pivq.alloc((size_t)nblk * rcap));
+    BEM_CK(d_Z.alloc((size_t)cap * 2));
+    if (near) BEM_CK(op.d_nS.alloc((size_t)scap * 2));
     BEM_CK(cudaMemsetAsync(flags.p, 0, sizeof(int32_t), st));
     BEM_CK(cudaMemsetAsync(counter.p, 0, sizeof(int32_t), st));
-    BEM_CK(cudaMemsetAsync(used.p, 0, sizeof(unsigned long long), st));
-    AcaArgs a;
-    a.nfar = nfar; a.m = t.m; a.p = p; a.L = L; a.rcap = rcap; a.n_local = op.n_local;
-    a.far_r = t.d_far_r.p; a.far_c = t.d_far_c.p; a.xi = t.d_xi.p;
+    BEM_CK(cudaMemsetAsync(used.p, 0, 2 * sizeof(unsigned long long), st));
+    AcaArgs a{};
+    a.nfar = nblk; a.m = t.m; a.p = p; a.L = L; a.rcap = rcap; a.n_local = op.n_local;
+    a.ppmax = ppmax; a.geo = geo;
+    a.far_r = near ? t.d_near_r.p : t.d_far_r.p; a.far_c = near ? t.d_near_c.p : t.d_far_c.p; a.xi = t.d_xi.p;
+    a.cbegin = t.d_begin.p; a.cend = t.d_end.p; a.cen = t.d_cen.p; a.qn = t.d_qn.p; a.area = t.d_area.p;
+    a.J = t.d_J.p;
+    for (int q = 0; q < 7; ++q) a.w[q] = wq[q];
+    a.Spool = near ? (double2*)op.d_nS.p : nullptr; a.spool_used = used.p + 1; a.spool_cap = scap;
+    a.soff = near ? op.d_nsoff.p : nullptr;
     a.s = (const double2*)op.d_s.p; a.local_l = op.d_local_l.p; a.eps = op.eps;
     a.Cbuf = (double2*)Cbuf.p; a.Dbuf = (double2*)Dbuf.p; a.Ebuf = (double2*)Ebuf.p; a.Pbuf = (double2*)Pbuf.p;
-    a.rank = op.d_rank.p; a.pivk = op.d_pivk.p; a.pivq = op.d_pivq.p; a.zoff = op.d_zoff.p;
-    a.Zpool = (double2*)op.d_Z.p; a.pool_used = used.p; a.pool_cap = cap; a.flags = flags.p;
+    a.rank = d_rank.p; a.pivk = d_pivk.p; a.pivq = d_pivq.p; a.zoff = d_zoff.p;
+    a.Zpool = (double2*)d_Z.p; a.pool_used = used.p; a.pool_cap = cap; a.flags = flags.p;
     a.next_block = counter.p;
-    const int nchmax = (std::max(pp, L) + 31) / 32 + 1;
-    const size_t smem = sizeof(double) * 6 * p + sizeof(double2) * (nchmax + 2 * rcap) +
-                        sizeof(unsigned) * ((pp + 31) / 32 + (L + 31) / 32) + 64 + sizeof(double2) * 2 * rcap + 16;
-    BEM_CK(cudaFuncSetAttribute(aca_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    aca_kernel<<<grid, kAcaThreads, smem, st>>>(a);
+    const int nchmax = (std::max(ppmax, L) + 31) / 32 + 1;
+    const size_t smem = sizeof(double) * geo + sizeof(double2) * (nchmax + 2 * rcap) +
+                        sizeof(unsigned) * ((ppmax + 31) / 32 + (L + 31) / 32) + 64 + sizeof(double2) * 2 * rcap + 16;
+    if (near) {
+      BEM_CK(cudaFuncSetAttribute(aca_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      aca_kernel<true><<<grid, kAcaThreads, smem, st>>>(a);
+    } else {
+      BEM_CK(cudaFuncSetAttribute(aca_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      aca_kernel<false><<<grid, kAcaThreads, smem, st>>>(a);
+    }
     BEM_CK(cudaGetLastError());
     int32_t hflags = 0;
-    unsigned long long hused = 0;
+    unsigned long long hused[2] = {0, 0};
     BEM_CK(cudaMemcpyAsync(&hflags, flags.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    BEM_CK(cudaMemcpyAsync(&hused, used.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    BEM_CK(cudaMemcpyAsync(hused, used.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     BEM_CK(cudaStreamSynchronize(st));
     if (hflags & 1) {  // a rank reached the scratch capacity: grow and redo
-      rcap = std::min(std::min(L, pp), rcap * 2);
+      rcap = std::min(std::min(L, ppmax), rcap * 2);
       continue;
     }
-    if (hflags & 2) {  // Z pool too small: exact size is now known
-      cap = hused;
+    if (hflags & 6) {  // Z / slice pool too small: exact sizes are now known
+      if (hflags & 2) cap = hused[0];
+      if (hflags & 4) scap = hused[1];
       continue;
     }
-    op.rcap = rcap;
-    BEM_CK(cudaMemcpy(op.ranks.data(), op.d_rank.p, sizeof(int32_t) * nfar, cudaMemcpyDeviceToHost));
-    if (hused < cap && (cap - hused) * 16ull > (64ull << 20)) {  // shrink the Z pool to its exact size
+    if (near) op.nrcap = rcap; else op.rcap = rcap;
+    BEM_CK(cudaMemcpy(ranks_out.data(), d_rank.p, sizeof(int32_t) * nblk, cudaMemcpyDeviceToHost));
+    auto shrink = [&](DBuf<double>& buf, unsigned long long used_n, unsigned long long cap_n) -> cudaError_t {
+      if (!(used_n < cap_n && (cap_n - used_n) * 16ull > (64ull << 20))) return cudaSuccess;
       DBuf<double> z;
-      BEM_CK(z.alloc((size_t)std::max<unsigned long long>(hused, 1) * 2));
-      BEM_CK(cudaMemcpyAsync(z.p, op.d_Z.p, (size_t)hused * 16, cudaMemcpyDeviceToDevice, st));
-      BEM_CK(cudaStreamSynchronize(st));
-      op.d_Z = std::move(z);
-    }
+      cudaError_t e = z.alloc((size_t)std::max<unsigned long long>(used_n, 1) * 2);
+      if (e != cudaSuccess) return e;
+      e = cudaMemcpyAsync(z.p, buf.p, (size_t)used_n * 16, cudaMemcpyDeviceToDevice, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e == cudaSuccess) buf = std::move(z);
+      return e;
+    };
+    BEM_CK(shrink(d_Z, hused[0], cap));
+    if (near) BEM_CK(shrink(op.d_nS, hused[1], scap));
     return BEM_OK;
   }
   set_error("bem_assemble_h2_aca: ACA did not fit after repeated growth");
@@ -510,7 +668,7 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   BEM_REQ(th && out, "bem_assemble_h2_aca: NULL tree/out");
   BEM_REQ(s != nullptr && L >= 1, "bem_assemble_h2_aca: need s and L >= 1");
   BEM_REQ(aca_eps > 0.0, "bem_assemble_h2_aca: aca_eps must be > 0");
-  BEM_REQ(mode == BEM_MODE_H2ACA || mode == BEM_MODE_H2ONLY || mode == BEM_MODE_DENSE,
+  BEM_REQ(mode == BEM_MODE_H2ACA || mode == BEM_MODE_H2ONLY || mode == BEM_MODE_DENSE || mode == BEM_MODE_COMBINED,
           "bem_assemble_h2_aca: unknown mode %d", mode);
   *out = nullptr;
   Tree& t = th->t;
@@ -577,8 +735,12 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
     set_error("bem_assemble_h2_aca: upload failed");
     return fail(BEM_ECUDA);
   }
-  if (mode == BEM_MODE_H2ACA) {
-    bem_status rs = run_aca(op, st);
+  if (mode == BEM_MODE_H2ACA || mode == BEM_MODE_COMBINED) {
+    bem_status rs = run_aca(op, st, false);
+    if (rs != BEM_OK) return fail(rs);
+  }
+  if (mode == BEM_MODE_COMBINED) {
+    bem_status rs = run_aca(op, st, true);
     if (rs != BEM_OK) return fail(rs);
   }
   if (mode != BEM_MODE_DENSE && !t.far_r.empty()) {
@@ -586,7 +748,7 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
     for (int c = 0; c < t.C; ++c) {
       int64_t cost = 0;
       for (int bi = t.far_ptr[c]; bi < t.far_ptr[c + 1]; ++bi)
-        cost += mode == BEM_MODE_H2ACA ? op.ranks[t.far_sorted[bi]] + 1 : 1;
+        cost += op.ranks.empty() ? 1 : op.ranks[t.far_sorted[bi]] + 1;
       if (t.far_ptr[c + 1] > t.far_ptr[c]) w.push_back({-cost, c});
     }
     std::sort(w.begin(), w.end());
@@ -602,14 +764,15 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
       int nsm = 148;
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, t.device);
       // block weight: ACA rank (H2ACA: r_b slice products) or 1 (H2ONLY: one p x p evaluation per frequency)
-      auto wgt = [&](int b) -> int64_t { return mode == BEM_MODE_H2ACA ? op.ranks[b] : 1; };
+      const bool aca = mode == BEM_MODE_H2ACA || mode == BEM_MODE_COMBINED;
+      auto wgt = [&](int b) -> int64_t { return aca ? op.ranks[b] : 1; };
       int64_t total = 0;
       for (int b = 0; b < (int)t.far_r.size(); ++b) total += wgt(b);
       int64_t cap = std::max<int64_t>(1, total / (8 * (int64_t)nsm));  // ~8 segments per SM (r01: config 2 K3 9.02 -> 8.77 ms vs 4 per SM)
       // H2ONLY: the CTA's 4 warps take every 4th block of a segment, so keep >= 16 blocks
       // per segment (<= 25% warp imbalance at the end-of-CTA barrier); the class tiles
       // already give many CTAs
-      if (mode != BEM_MODE_H2ACA) cap = std::max<int64_t>(cap, std::max<int64_t>(16, total / (2 * (int64_t)nsm)));
+      if (!aca) cap = std::max<int64_t>(cap, std::max<int64_t>(16, total / (2 * (int64_t)nsm)));
       if (const char* e = getenv("BEM_SEG_CAP")) cap = std::max<int64_t>(1, atoll(e));
       struct Seg { int64_t cost; int row, bi0, bi1, slot; };
       std::vector<Seg> segs;
@@ -680,8 +843,8 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
 extern "C" bem_status bem_aca_export(bem_op oh, int32_t* ranks, int32_t* pivots, int64_t* total_rank) {
   BEM_REQ(oh, "bem_aca_export: NULL op");
   Op& op = oh->o;
-  if (op.mode != BEM_MODE_H2ACA) {
-    set_error("bem_aca_export: operator was not assembled with BEM_MODE_H2ACA");
+  if (op.mode != BEM_MODE_H2ACA && op.mode != BEM_MODE_COMBINED) {
+    set_error("bem_aca_export: operator was not assembled with BEM_MODE_H2ACA / BEM_MODE_COMBINED");
     return BEM_ESTATE;
   }
   const int nfar = (int)op.ranks.size();
@@ -699,6 +862,34 @@ extern "C" bem_status bem_aca_export(bem_op oh, int32_t* ranks, int32_t* pivots,
       for (int j = 0; j < op.ranks[b]; ++j) {
         pivots[2 * o] = pk[(size_t)b * op.rcap + j];
         pivots[2 * o + 1] = pq[(size_t)b * op.rcap + j];
+        ++o;
+      }
+  }
+  return BEM_OK;
+}
+
+extern "C" bem_status bem_aca_export_near(bem_op oh, int32_t* ranks, int32_t* pivots, int64_t* total_rank) {
+  BEM_REQ(oh, "bem_aca_export_near: NULL op");
+  Op& op = oh->o;
+  if (op.mode != BEM_MODE_COMBINED) {
+    set_error("bem_aca_export_near: operator was not assembled with BEM_MODE_COMBINED");
+    return BEM_ESTATE;
+  }
+  const int nb = (int)op.nranks.size();
+  int64_t tot = 0;
+  for (int r : op.nranks) tot += r;
+  if (total_rank) *total_rank = tot;
+  if (ranks) std::copy(op.nranks.begin(), op.nranks.end(), ranks);
+  if (pivots && nb > 0) {
+    DeviceGuard dg(op.tree->device);
+    std::vector<int32_t> pk((size_t)nb * op.nrcap), pq((size_t)nb * op.nrcap);
+    BEM_CK(cudaMemcpy(pk.data(), op.d_npivk.p, sizeof(int32_t) * pk.size(), cudaMemcpyDeviceToHost));
+    BEM_CK(cudaMemcpy(pq.data(), op.d_npivq.p, sizeof(int32_t) * pq.size(), cudaMemcpyDeviceToHost));
+    int64_t o = 0;
+    for (int b = 0; b < nb; ++b)
+      for (int j = 0; j < op.nranks[b]; ++j) {
+        pivots[2 * o] = pk[(size_t)b * op.nrcap + j];
+        pivots[2 * o + 1] = pq[(size_t)b * op.nrcap + j];
         ++o;
       }
   }

@@ -107,6 +107,10 @@ struct Tree {
   DBuf<int32_t> d_leaves;
   // near field per leaf index: [jb, je) into the flat list of near source panels
   DBuf<int32_t> d_near_jb, d_near_je, d_near_j;
+  // near blocks (combined mode, NEXT-4): block list, per-row-leaf CSR, raw J(T) (cluster order)
+  DBuf<int32_t> d_near_r, d_near_c, d_nb_ptr, d_nb_sorted;
+  DBuf<double> d_J;
+  int max_leaf = 0;
   // far CSR by row cluster
   std::vector<int32_t> far_ptr, far_sorted;  // far_sorted: block ids grouped by row cluster
   DBuf<int32_t> d_far_ptr, d_far_sorted, d_far_r, d_far_c;
@@ -139,6 +143,13 @@ struct Op {
   int n_segs = 0, n_seg_rows = 0;
   DBuf<int32_t> d_segs, d_seg_rows, d_seg_ptr;
   DBuf<double> d_part;  // n_segs * n_local * p complex
+  // near-field MACA (BEM_MODE_COMBINED, Alg. 3 NEAR branch): per near block rank, pivots,
+  // Z (r x n_local) and the pivot slices V_{k_t}[b] (r x n_r x n_c, row-major) in pools
+  int nrcap = 0;
+  std::vector<int32_t> nranks;
+  DBuf<int32_t> d_nrank, d_npivk, d_npivq;
+  DBuf<int64_t> d_nzoff, d_nsoff;
+  DBuf<double> d_nZ, d_nS;
   // workspaces
   DBuf<double> d_xc, d_yc, d_xhat, d_yhat;
   // kernel variants (tuning knobs; env BEM_NEAR_F, BEM_FAR_GENERIC read at assembly)
@@ -166,6 +177,7 @@ struct Op {
 bem_status apply_launch(Op& op, const double* x, double* y, cudaStream_t st, bool dl = false, double alpha = 0.0);
 bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st, bool dl = false);
 bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st);
+bem_status launch_near_maca(Op& op, const double2* xc, double2* yc, cudaStream_t st);  // nearm.cu
 // fft.cu
 bem_status fft_transform(const double* in, double* out, int64_t M, int N, double R, bool inverse,
                          cudaStream_t st);

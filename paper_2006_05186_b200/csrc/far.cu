@@ -1134,6 +1134,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
   Tree& t = *op.tree;
   const int nl = op.n_local, p = t.p;
   const int fk = op.far_kernel != 0 ? op.far_kernel : (p > 32 ? 8 : 7);  // r01: far8 wins at p = 64, far7 at p = 27
+  const bool aca = op.mode == BEM_MODE_H2ACA || op.mode == BEM_MODE_COMBINED;  // far blocks via the MACA skeleton
   if (op.mode == BEM_MODE_H2ONLY && !op.force_generic && op.n_segs > 0 && p <= 128) {
     BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
     H2oArgs a;
@@ -1160,7 +1161,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
     BEM_CK(cudaGetLastError());
     return BEM_OK;
   }
-  if (op.mode == BEM_MODE_H2ACA && fk == 8 && !op.force_generic && op.n_segs > 0) {
+  if (aca && fk == 8 && !op.force_generic && op.n_segs > 0) {
     const Far8Cfg f8 = choose8(p, nl, op.far4_smem_cap, op.far8_kc);
     if (f8.mt > 0) {
       BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
@@ -1178,7 +1179,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
       return BEM_OK;
     }
   }
-  if (op.mode == BEM_MODE_H2ACA && fk == 7 && !op.force_generic && op.n_segs > 0) {
+  if (aca && fk == 7 && !op.force_generic && op.n_segs > 0) {
     const Far7Cfg f7 = choose7(p, nl, op.far4_smem_cap, op.far7_cluster);
     if (f7.mt > 0) {
       BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
@@ -1196,7 +1197,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
       return BEM_OK;
     }
   }
-  if (op.mode == BEM_MODE_H2ACA && fk == 6 && !op.force_generic && op.n_segs > 0) {
+  if (aca && fk == 6 && !op.force_generic && op.n_segs > 0) {
     const Far6Cfg f6 = choose6(p, nl, op.far4_smem_cap);
     if (f6.mt > 0) {
       BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
@@ -1214,7 +1215,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
     }
   }
   FarArgs a;
-  a.nl = nl; a.m = t.m; a.p = p; a.mode = op.mode; a.rcap = op.rcap;
+  a.nl = nl; a.m = t.m; a.p = p; a.mode = aca ? BEM_MODE_H2ACA : op.mode; a.rcap = op.rcap;
   a.far_ptr = t.d_far_ptr.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p; a.xi = t.d_xi.p;
   a.s = (const double2*)op.d_s.p; a.local_l = op.d_local_l.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
   a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.yhat = yhat;

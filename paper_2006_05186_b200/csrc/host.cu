@@ -68,7 +68,9 @@ static double panel_self_integral(const double* P0, const double* P1, const doub
     double bx = B[0] - c[0], by = B[1] - c[1], bz = B[2] - c[2];
     double ta = ax * ux + ay * uy + az * uz;
     double tb = bx * ux + by * uy + bz * uz;
-    double fx = ax - ta * ux, fy = ay - ta * uy, fz = az - ta * uz;
+    // f = (A - t_A u) - c: the pinned operation order of DESIGN.md §5 (the near-field
+    // MACA reads J bit-for-bit)
+    double fx = (A[0] - ta * ux) - c[0], fy = (A[1] - ta * uy) - c[1], fz = (A[2] - ta * uz) - c[2];
     double d = std::sqrt(fx * fx + fy * fy + fz * fz);
     acc += d * (std::asinh(tb / d) - std::asinh(ta / d));
   }
@@ -391,13 +393,15 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
     }
   }
   // cluster-ordered panel data
-  std::vector<double> cen((size_t)3 * M), qn((size_t)21 * M), qw((size_t)7 * M), sj(M), area(M), nrm((size_t)3 * M);
+  std::vector<double> cen((size_t)3 * M), qn((size_t)21 * M), qw((size_t)7 * M), sj(M), area(M), nrm((size_t)3 * M),
+      rawJ(M);
   for (int64_t k = 0; k < M; ++k) {
     const int i = t.perm[k];
     for (int a = 0; a < 3; ++a) cen[3 * k + a] = g.cen[3 * i + a];
     for (int j = 0; j < 21; ++j) qn[21 * k + j] = g.qn[21 * i + j];
     for (int q = 0; q < 7; ++q) qw[7 * k + q] = (kRule.w[q] * g.area[i]) / kFourPi;
     sj[k] = g.J[i] / kFourPi;
+    rawJ[k] = g.J[i];
     area[k] = g.area[i];
     for (int a = 0; a < 3; ++a) nrm[3 * k + a] = g.nrm[3 * i + a];
   }
@@ -416,6 +420,17 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
     nj.insert(nj.end(), per_leaf[li].begin(), per_leaf[li].end());
     nje[li] = (int32_t)nj.size();
   }
+  // near blocks grouped by row leaf (partition order within a row): the combined
+  // mode's near-field MACA apply walks a row leaf's blocks
+  std::vector<int32_t> nb_ptr(t.n_leaves + 1, 0), nb_sorted(t.near_r.size());
+  for (size_t b = 0; b < t.near_r.size(); ++b) nb_ptr[leaf_pos[t.near_r[b]] + 1]++;
+  for (int li = 0; li < t.n_leaves; ++li) nb_ptr[li + 1] += nb_ptr[li];
+  {
+    std::vector<int32_t> f(nb_ptr.begin(), nb_ptr.end() - 1);
+    for (size_t b = 0; b < t.near_r.size(); ++b) nb_sorted[f[leaf_pos[t.near_r[b]]]++] = (int32_t)b;
+  }
+  for (int li = 0; li < t.n_leaves; ++li)
+    t.max_leaf = std::max(t.max_leaf, t.end[t.leaves[li]] - t.begin[t.leaves[li]]);
   // far CSR by row cluster
   t.far_ptr.assign(C + 1, 0);
   for (size_t b = 0; b < t.far_r.size(); ++b) t.far_ptr[t.far_r[b] + 1]++;
@@ -455,6 +470,7 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
   }
   UP(d_U, U); UP(d_W, W); UP(d_E, E); UP(d_ET, ET); UP(d_UT, UT); UP(d_xi, t.xi); UP(d_leaves, t.leaves);
   UP(d_near_jb, njb); UP(d_near_je, nje); UP(d_near_j, nj);
+  UP(d_J, rawJ); UP(d_near_r, t.near_r); UP(d_near_c, t.near_c); UP(d_nb_ptr, nb_ptr); UP(d_nb_sorted, nb_sorted);
   UP(d_far_ptr, t.far_ptr); UP(d_far_sorted, t.far_sorted); UP(d_far_r, t.far_r); UP(d_far_c, t.far_c);
   t.d_level_nonleaf.resize(t.depth + 1);
   for (int lv = 0; lv <= t.depth; ++lv) UP(d_level_nonleaf[lv], t.level_nonleaf[lv]);

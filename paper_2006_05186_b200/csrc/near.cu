@@ -228,6 +228,7 @@ cudaError_t launch(const NearArgs& na, cudaStream_t st) {
 }  // namespace
 
 bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st, bool dl) {
+  if (!dl && op.mode == BEM_MODE_COMBINED) return launch_near_maca(op, xc, yc, st);  // NEXT-4 (nearm.cu)
   Tree& t = *op.tree;
   NearArgs na;
   na.M = t.M; na.n_class = op.n_class; na.leaf_of = t.d_leaf_of.p;

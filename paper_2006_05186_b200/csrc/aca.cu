@@ -742,6 +742,23 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   if (mode == BEM_MODE_COMBINED) {
     bem_status rs = run_aca(op, st, true);
     if (rs != BEM_OK) return fail(rs);
+    // K1m launch order: row leaves by descending near-field MACA work (LPT)
+    std::vector<std::pair<int64_t, int32_t>> w;
+    for (int li = 0; li < t.n_leaves; ++li) {
+      int64_t c = 0;
+      for (int bi = t.nb_ptr[li]; bi < t.nb_ptr[li + 1]; ++bi) {
+        const int b = t.nb_sorted[bi];
+        c += (int64_t)op.nranks[b] * (t.end[t.near_c[b]] - t.begin[t.near_c[b]]);
+      }
+      w.push_back({-c, li});
+    }
+    std::stable_sort(w.begin(), w.end());
+    std::vector<int32_t> ord;
+    for (auto& e : w) ord.push_back(e.second);
+    if (op.d_nm_order.upload(ord) != cudaSuccess) {
+      set_error("bem_assemble_h2_aca: upload failed");
+      return fail(BEM_ECUDA);
+    }
   }
   if (mode != BEM_MODE_DENSE && !t.far_r.empty()) {
     std::vector<std::pair<int64_t, int32_t>> w;

@@ -111,6 +111,7 @@ struct Tree {
   DBuf<int32_t> d_near_r, d_near_c, d_nb_ptr, d_nb_sorted;
   DBuf<double> d_J;
   int max_leaf = 0;
+  std::vector<int32_t> nb_ptr, nb_sorted;  // host copies of d_nb_ptr / d_nb_sorted
   // far CSR by row cluster
   std::vector<int32_t> far_ptr, far_sorted;  // far_sorted: block ids grouped by row cluster
   DBuf<int32_t> d_far_ptr, d_far_sorted, d_far_r, d_far_c;
@@ -150,6 +151,7 @@ struct Op {
   DBuf<int32_t> d_nrank, d_npivk, d_npivq;
   DBuf<int64_t> d_nzoff, d_nsoff;
   DBuf<double> d_nZ, d_nS;
+  DBuf<int32_t> d_nm_order, d_nm_counter;  // K1m CTA order: leaf indices by descending sum_b r_b n_c (LPT)
   // workspaces
   DBuf<double> d_xc, d_yc, d_xhat, d_yhat;
   // kernel variants (tuning knobs; env BEM_NEAR_F, BEM_FAR_GENERIC read at assembly)

@@ -431,6 +431,8 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
   }
   for (int li = 0; li < t.n_leaves; ++li)
     t.max_leaf = std::max(t.max_leaf, t.end[t.leaves[li]] - t.begin[t.leaves[li]]);
+  t.nb_ptr = nb_ptr;
+  t.nb_sorted = nb_sorted;
   // far CSR by row cluster
   t.far_ptr.assign(C + 1, 0);
   for (size_t b = 0; b < t.far_r.size(); ++b) t.far_ptr[t.far_r[b] + 1]++;

@@ -10,9 +10,9 @@
 //             per fragment, reused for the four 8-row tiles),
 //   B[nu,i] = V_{k_j}[b][i,nu]       slice rows staged in shared memory with
 //             cp.async, double-buffered so term j+1 loads while term j multiplies.
-// One CTA owns (row leaf, 8*8-column frequency tile, 32-row chunk) and walks all
+// One CTA owns (row leaf, nw*8-column frequency tile, 32-row chunk) and walks all
 // near blocks of its row leaf, so the output is written once (no partial sums,
-// deterministic).  Leftover columns (n_local mod 8) use DFMA on lanes 0..3.
+// deterministic).  The last frequency tile is zero-padded to 8 columns.
 #include <algorithm>
 
 #include "common.cuh"
@@ -36,8 +36,11 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 
 struct NearmArgs {
   int64_t M;
-  int nl, tb, TT, XTP, SST, p4max;
+  int nl, nw, XTP, SST, p4max;  // nw warps per CTA = 8-column frequency tiles per CTA
   const int32_t* leaves;
+  const int32_t* order;  // leaf indices, descending sum_b r_b n_c (LPT)
+  int* counter;          // work-item counter (zeroed before each launch)
+  int nitems, ntiles, nchunks;
   const int32_t* nb_ptr;
   const int32_t* nb_sorted;
   const int32_t* near_c;
@@ -53,36 +56,42 @@ struct NearmArgs {
   const int32_t* mask;
 };
 
-constexpr int kNmThreads = 256;
+// Columns past n_local (the last tile's padding, e.g. 129 -> 144) carry zero Z and x:
+// a zero-padded DMMA column is cheaper than a DFMA side path (r01: far7 / K1m v1).
+// Slices are triple-buffered (one barrier per term: the barrier that publishes
+// term j also retires term j-1's buffer, which term j+2's cp.async then refills);
+// the real and imaginary partial products go to separate accumulators so that
+// dependent DMMAs are 2 * njt instructions apart in each pass (r01 ncu: v2 was
+// "stall wait" bound at 6 apart).
+constexpr int kNmMaxWarps = 6;
 
-__global__ void __launch_bounds__(kNmThreads, 2) nearm_kernel(NearmArgs a) {
+__device__ __forceinline__ void nearm_item(const NearmArgs& a, int item) {
   extern __shared__ double2 sm[];
-  const int SST = a.SST, XTP = a.XTP, tb = a.tb;
-  const int r = a.leaves[blockIdx.x];
+  const int SST = a.SST, XTP = a.XTP, nth = blockDim.x;
+  const int tile = item % a.ntiles, rest = item / a.ntiles;
+  const int chunk = rest % a.nchunks;
+  const int li = a.order[rest / a.nchunks];
+  const int r = a.leaves[li];
   const int rb0 = a.cbegin[r], nr = a.cend[r] - rb0;
-  const int mu0 = blockIdx.z * 32;
+  const int mu0 = chunk * 32;
   const int nrow = min(32, nr - mu0);
   if (nrow <= 0) return;
-  const int tc0 = tb + blockIdx.y * a.TT;
-  const int ncol = max(0, min(a.TT, a.nl - tc0));
-  const bool lead = blockIdx.y == 0;
-  double2* Sb[2] = {sm, sm + 32 * SST};
-  double2* xs = sm + 64 * SST;  // p4max x XTP: [nu][0..tb) leftover, [tb..) DMMA columns
+  const int ncp = a.nw * 8;                    // staged columns of this CTA
+  const int tc0 = tile * ncp;
+  double2* Sb[3] = {sm, sm + 32 * SST, sm + 64 * SST};
+  double2* xs = sm + 96 * SST;  // p4max x XTP: [nu][column]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
-  const int ntile = ncol / 8;
-  const bool wt = warp < ntile;  // this warp's 8-column tile exists
+  const int tcol = tc0 + warp * 8 + g;         // this lane's A-fragment column
+  const bool live = tcol < a.nl;
+  const bool wlive = tc0 + warp * 8 < a.nl;    // the warp's tile holds a real column
   const int njt = (nrow + 7) / 8;
-  double acc[4][2][2];
+  double acc[4][2][2], bcc[4][2][2];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) acc[j][0][0] = acc[j][0][1] = acc[j][1][0] = acc[j][1][1] = 0.0;
-  double2 lacc[8];
+  for (int j = 0; j < 4; ++j)
 #pragma unroll
-  for (int i = 0; i < 8; ++i) lacc[i] = make_double2(0.0, 0.0);
-  const int lrow = 4 * warp + lane;
-  const bool lown = lead && lane < 4 && lrow < nrow && tb > 0;
-  const int ncp = tb + ncol;
-  for (int bi = a.nb_ptr[blockIdx.x]; bi < a.nb_ptr[blockIdx.x + 1]; ++bi) {
+    for (int u = 0; u < 2; ++u) acc[j][u][0] = acc[j][u][1] = bcc[j][u][0] = bcc[j][u][1] = 0.0;
+  for (int bi = a.nb_ptr[li]; bi < a.nb_ptr[li + 1]; ++bi) {
     const int b = a.nb_sorted[bi];
     const int c = a.near_c[b];
     const int cb0 = a.cbegin[c], nc = a.cend[c] - cb0;
@@ -92,78 +101,63 @@ __global__ void __launch_bounds__(kNmThreads, 2) nearm_kernel(NearmArgs a) {
     const double2* Zb = a.Z + a.zoff[b];
     const int64_t slice = (int64_t)nr * nc;
     __syncthreads();  // previous block's xs / S reads are done
-    // stage xc[t, c0 + nu] (zero rows nu in [nc, p4)) and zero the padded S columns
-    for (int idx = tid; idx < ncp * p4; idx += kNmThreads) {
+    // stage xc[t, c0 + nu] (zero for nu in [nc, p4) and t >= n_local), zero the padded S columns
+    for (int idx = tid; idx < ncp * p4; idx += nth) {
       const int tl = idx / p4, nu = idx - tl * p4;
-      const int tg = tl < tb ? tl : tc0 + (tl - tb);
-      if (tl >= tb || lead)
-        xs[nu * XTP + tl] = nu < nc ? a.xc[(int64_t)tg * a.M + cb0 + nu] : make_double2(0.0, 0.0);
+      const int tg = tc0 + tl;
+      xs[nu * XTP + tl] = (nu < nc && tg < a.nl) ? a.xc[(int64_t)tg * a.M + cb0 + nu] : make_double2(0.0, 0.0);
     }
-    for (int idx = tid; idx < 2 * 32 * (p4 - nc); idx += kNmThreads) {
+    for (int idx = tid; idx < 3 * 32 * (p4 - nc); idx += nth) {
       const int w = idx / (32 * (p4 - nc)), e = idx - w * 32 * (p4 - nc);
       const int i = e / (p4 - nc), nu = nc + (e - i * (p4 - nc));
       Sb[w][i * SST + nu] = make_double2(0.0, 0.0);
     }
-    auto load = [&](int j, double2* dst) {
-      const double2* src = Sg + (int64_t)j * slice;
-      for (int idx = tid; idx < nrow * nc; idx += kNmThreads) {
-        const int i = idx / nc, nu = idx - i * nc;
-        cp_async16(dst + i * SST + nu, src + idx);
+    auto load = [&](int j) {
+      if (j < rk) {
+        const double2* src = Sg + (int64_t)j * slice;
+        double2* dst = Sb[j % 3];
+        for (int idx = tid; idx < nrow * nc; idx += nth) {
+          const int i = idx / nc, nu = idx - i * nc;
+          cp_async16(dst + i * SST + nu, src + idx);
+        }
       }
-      cp_commit();
+      cp_commit();  // empty groups keep the wait_group count uniform
     };
-    if (rk > 0) load(0, Sb[0]);
+    load(0);
+    load(1);
     for (int j = 0; j < rk; ++j) {
-      const double2 zt = wt ? Zb[(int64_t)j * a.nl + tc0 + warp * 8 + g] : make_double2(0.0, 0.0);
-      if (j + 1 < rk) {
-        load(j + 1, Sb[(j + 1) & 1]);
-        cp_wait<1>();
-      } else {
-        cp_wait<0>();
-      }
-      __syncthreads();
-      const double2* S = Sb[j & 1];
-      if (wt) {
-        for (int k0 = 0; k0 < p4; k0 += 4) {
-          const double2 xv = xs[(k0 + q) * XTP + tb + warp * 8 + g];
-          const double ar = zt.x * xv.x - zt.y * xv.y;
-          const double ai = zt.x * xv.y + zt.y * xv.x;
-          const double nai = -ai;
-          double2 bf[4];
+      const double2 zt = live ? Zb[(int64_t)j * a.nl + tcol] : make_double2(0.0, 0.0);
+      cp_wait<1>();      // this thread's copies of term j have landed
+      __syncthreads();   // ... everyone's; and term j-1's buffer is free
+      load(j + 2);
+      const double2* S = Sb[j % 3];
+      for (int k0 = 0; k0 < (wlive ? p4 : 0); k0 += 4) {
+        const double2 xv = xs[(k0 + q) * XTP + warp * 8 + g];
+        const double ar = zt.x * xv.x - zt.y * xv.y;
+        const double ai = zt.x * xv.y + zt.y * xv.x;
+        const double nai = -ai;
+        double2 bf[4];
 #pragma unroll
-          for (int jt = 0; jt < 4; ++jt) bf[jt] = S[(jt * 8 + g) * SST + k0 + q];
+        for (int jt = 0; jt < 4; ++jt) bf[jt] = S[(jt * 8 + g) * SST + k0 + q];
 #pragma unroll
-          for (int jt = 0; jt < 4; ++jt)
-            if (jt < njt) {
-              dmma(acc[jt][0][0], acc[jt][0][1], ar, bf[jt].x);
-              dmma(acc[jt][1][0], acc[jt][1][1], ar, bf[jt].y);
-            }
-#pragma unroll
-          for (int jt = 0; jt < 4; ++jt)
-            if (jt < njt) {
-              dmma(acc[jt][0][0], acc[jt][0][1], nai, bf[jt].y);
-              dmma(acc[jt][1][0], acc[jt][1][1], ai, bf[jt].x);
-            }
-        }
-      }
-      if (lown) {
-        for (int tl = 0; tl < tb; ++tl) {
-          const double2 z = Zb[(int64_t)j * a.nl + tl];
-          double2 sacc = make_double2(0.0, 0.0);
-          for (int nu = 0; nu < nc; ++nu) {
-            const double2 sv = S[lrow * SST + nu], xv = xs[nu * XTP + tl];
-            sacc.x += sv.x * xv.x - sv.y * xv.y;
-            sacc.y += sv.x * xv.y + sv.y * xv.x;
+        for (int jt = 0; jt < 4; ++jt)
+          if (jt < njt) {
+            dmma(acc[jt][0][0], acc[jt][0][1], ar, bf[jt].x);
+            dmma(acc[jt][1][0], acc[jt][1][1], ar, bf[jt].y);
           }
-          lacc[tl].x += z.x * sacc.x - z.y * sacc.y;
-          lacc[tl].y += z.x * sacc.y + z.y * sacc.x;
-        }
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt)
+          if (jt < njt) {
+            dmma(bcc[jt][0][0], bcc[jt][0][1], nai, bf[jt].y);
+            dmma(bcc[jt][1][0], bcc[jt][1][1], ai, bf[jt].x);
+          }
       }
-      __syncthreads();  // buffer j&1 is refilled by the load of term j+2
     }
+    cp_wait<0>();
   }
-  if (wt) {
-    const int t = tc0 + warp * 8 + g;
+  // accumulator element (row 2q+v of tile jt, column g of the warp's tile)
+  const int t = tc0 + warp * 8 + g;
+  if (t < a.nl) {
     const bool on = a.mask == nullptr || a.mask[t] != 0;
 #pragma unroll
     for (int jt = 0; jt < 4; ++jt)
@@ -172,14 +166,25 @@ __global__ void __launch_bounds__(kNmThreads, 2) nearm_kernel(NearmArgs a) {
         const int row = jt * 8 + 2 * q + v;
         if (row < nrow)
           a.yc[(int64_t)t * a.M + rb0 + mu0 + row] =
-              on ? make_double2(acc[jt][0][v], acc[jt][1][v]) : make_double2(0.0, 0.0);
+              on ? make_double2(acc[jt][0][v] + bcc[jt][0][v], acc[jt][1][v] + bcc[jt][1][v])
+                 : make_double2(0.0, 0.0);
       }
   }
-  if (lown)
-    for (int tl = 0; tl < tb; ++tl) {
-      const bool on = a.mask == nullptr || a.mask[tl] != 0;
-      a.yc[(int64_t)tl * a.M + rb0 + mu0 + lrow] = on ? lacc[tl] : make_double2(0.0, 0.0);
-    }
+}
+
+// Persistent CTAs take work items (row leaf, 32-row chunk, column tile) from a
+// counter in LPT order (leaves by descending sum_b r_b n_c): every item's output
+// is written by exactly one CTA, so the result does not depend on the schedule.
+__global__ void __launch_bounds__(kNmMaxWarps * 32, 2) nearm_kernel(NearmArgs a) {
+  __shared__ int s_item;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_item = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= a.nitems) return;
+    nearm_item(a, item);
+  }
 }
 
 }  // namespace
@@ -193,25 +198,42 @@ bem_status launch_near_maca(Op& op, const double2* xc, double2* yc, cudaStream_t
   }
   NearmArgs a;
   a.M = t.M; a.nl = nl;
-  a.tb = nl % 8;
-  const int nD = nl - a.tb;
-  const int ntiles = std::max(1, (nD + 63) / 64);
-  a.TT = nD == 0 ? 0 : ((nD / 8 + ntiles - 1) / ntiles) * 8;
+  // 8-column tiles; CTAs of nw in [4, 8] warps, nw chosen to minimise padded tiles
+  // (129 frequencies: 17 tiles -> 3 x 6; 257: 33 -> 7 x 5 ... ties: more warps)
+  const int ntl = (nl + 7) / 8;
+  int nw = kNmMaxWarps, best = 1 << 30;
+  for (int w = kNmMaxWarps; w >= 4; --w) {
+    const int waste = ((ntl + w - 1) / w) * w - ntl;
+    if (waste < best) { best = waste; nw = w; }
+  }
+  if (ntl < 4) nw = ntl;
+  const int ntiles = (ntl + nw - 1) / nw;
+  a.nw = nw;
   a.p4max = (t.max_leaf + 3) & ~3;
   int SST = a.p4max;
   while (SST % 8 != 4) ++SST;  // B fragment rows 8 apart: stride 4 (mod 8) complex -> conflict-free
   a.SST = SST;
-  int XTP = a.tb + a.TT;
+  int XTP = nw * 8;
   while (XTP % 8 != 2) ++XTP;
   a.XTP = XTP;
+  a.order = op.d_nm_order.p;
   a.leaves = t.d_leaves.p; a.nb_ptr = t.d_nb_ptr.p; a.nb_sorted = t.d_nb_sorted.p; a.near_c = t.d_near_c.p;
   a.cbegin = t.d_begin.p; a.cend = t.d_end.p;
   a.rank = op.d_nrank.p; a.soff = op.d_nsoff.p; a.zoff = op.d_nzoff.p;
   a.S = (const double2*)op.d_nS.p; a.Z = (const double2*)op.d_nZ.p; a.xc = xc; a.yc = yc; a.mask = op.d_mask;
-  const size_t smem = sizeof(double2) * (64 * (size_t)SST + (size_t)a.p4max * XTP);
+  const size_t smem = sizeof(double2) * (96 * (size_t)SST + (size_t)a.p4max * XTP);
   BEM_CK(cudaFuncSetAttribute(nearm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const unsigned nchunks = (unsigned)((t.max_leaf + 31) / 32);
-  nearm_kernel<<<dim3((unsigned)t.n_leaves, (unsigned)ntiles, nchunks), kNmThreads, smem, st>>>(a);
+  a.nchunks = (t.max_leaf + 31) / 32;
+  a.ntiles = ntiles;
+  a.nitems = t.n_leaves * a.nchunks * ntiles;
+  if (op.d_nm_counter.n == 0) BEM_CK(op.d_nm_counter.alloc(1));
+  a.counter = op.d_nm_counter.p;
+  BEM_CK(cudaMemsetAsync(a.counter, 0, sizeof(int), st));
+  int nsm = 148, per_sm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, t.device);
+  BEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nearm_kernel, nw * 32, smem));
+  const int grid = std::max(1, std::min(a.nitems, nsm * std::max(1, per_sm)));
+  nearm_kernel<<<grid, nw * 32, smem, st>>>(a);
   BEM_CK(cudaGetLastError());
   return BEM_OK;
 }

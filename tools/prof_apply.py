@@ -23,7 +23,8 @@ N = cfg["N"]
 R = 10.0 ** (-5.0 / N)
 s = pb.cqm_frequencies(N, cfg["T"], R)
 tree = pb.Tree(V, T, cfg["leaf"], cfg["eta"], cfg["m"])
-mode = {"h2aca": pb.BEM_MODE_H2ACA, "h2only": pb.BEM_MODE_H2ONLY, "dense": pb.BEM_MODE_DENSE}[a.mode]
+mode = {"h2aca": pb.BEM_MODE_H2ACA, "h2only": pb.BEM_MODE_H2ONLY, "dense": pb.BEM_MODE_DENSE,
+        "combined": pb.BEM_MODE_COMBINED}[a.mode]
 op = pb.Operator(tree, s, cfg["eps"], mode=mode)
 x = torch.from_numpy(synth.random_density(a.config, N + 1, len(T))).cuda()
 for _ in range(a.reps):

@@ -80,6 +80,12 @@ def lib():
         L.orc_h2_aca_near_export.argtypes = [vp, vp, i64, vp, vp]
         L.orc_dense_matrix_pinned.argtypes = [vp, vp, i64, d, d, vp]
         L.orc_pexpm1.argtypes = [d]
+        L.orc_h2_time_weights.argtypes = [vp, d]
+        L.orc_h2_time_weights.restype = C.c_int
+        L.orc_h2_conv.argtypes = [vp, vp, vp, i32]
+        L.orc_h2_conv.restype = C.c_int
+        L.orc_h2_weight_dense.argtypes = [vp, i32, vp]
+        L.orc_h2_weight_dense.restype = C.c_int
         L.orc_pexpm1.restype = d
         _lib = L
     return _lib
@@ -310,6 +316,45 @@ class H2:
         Z = np.empty(tot * L, dtype=np.complex128)
         lib().orc_h2_aca_near_export(self.h, _p(blk), nb, _p(piv), _p(Z))
         return dict(ranks=ranks, pivots=piv, Z=Z, fragile=fragile)
+
+    def time_weights(self, R):
+        """dhat = R-scaled inverse DFT of every far / near skeleton coefficient row
+        (eq:fastdft P:1542-1553); needs aca() and aca_near() on all L frequencies."""
+        if lib().orc_h2_time_weights(self.h, float(R)) != 0:
+            raise RuntimeError("oracle time_weights: run aca() and aca_near() first")
+        self.R = float(R)
+
+    def conv(self, q, kmax=None):
+        """y[n] = sum_{k <= min(n, kmax)} V^_{n-k} q[k] with the compressed time weights
+        (eq:fastrhs P:1566-1573); q [L][M] (input order), complex result."""
+        q = _c128(q)
+        L = q.shape[0]
+        y = np.empty_like(q)
+        if lib().orc_h2_conv(self.h, _p(q), _p(y), int(L - 1 if kmax is None else kmax)) != 0:
+            raise RuntimeError("oracle conv: call time_weights() first")
+        return y
+
+    def weight_dense(self, n):
+        """Dense V^_n (input order) assembled from the compressed weights."""
+        A = np.empty((self.M, self.M), dtype=np.complex128)
+        if lib().orc_h2_weight_dense(self.h, int(n), _p(A)) != 0:
+            raise RuntimeError("oracle weight_dense: call time_weights() first / n out of range")
+        return A
+
+    def mot(self, g):
+        """Marching on in time with the compressed weights (eq:cqmrhs P:652-680, one LU
+        of V^_0 P:686-703; Dirichlet single-layer problem V q = g): for n = 0..N,
+        Re V^_0 q_n = g_n - Re sum_{k<n} V^_{n-k} q_k.  g real [L][M]; returns q real."""
+        import scipy.linalg as sla
+        g = np.asarray(g, dtype=np.float64)
+        L, M = g.shape
+        W = [self.weight_dense(n).real for n in range(L)]
+        lu = sla.lu_factor(W[0])
+        q = np.zeros((L, M))
+        for n in range(L):
+            rhs = g[n] - sum(W[n - k] @ q[k] for k in range(n))
+            q[n] = sla.lu_solve(lu, rhs)
+        return q
 
     def apply(self, mode, s, x, lsel=None):
         """y[t] = V(s[lsel[t]]) x[t]; x shape [nsel][M] complex (input order)."""

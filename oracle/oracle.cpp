@@ -407,6 +407,9 @@ struct H2 {
   std::vector<int64_t> nsoff;  // pivot slices C_{b,t} = V_{k_t}[b] (the tensor C_b of eq:lrfinal), t-major
   std::vector<C2> nS;
   bool near_done = false;
+  // time-domain weight coefficients dhat (NEXT-2), rows as in Z / nZ
+  std::vector<cplx> tDf, tDn;
+  bool tw_done = false;
 };
 
 static void build_cluster(H2& h, int begin, int end, int level, int parent) {
@@ -1095,6 +1098,7 @@ int64_t orc_h2_aca(void* hp, const double* s_in, int32_t L, double eps, const in
                    int32_t* ranks, int32_t* fragile) {
   H2& h = *(H2*)hp;
   if (h.near_done && h.L != L) h.near_done = false;
+  h.tw_done = false;
   h.L = L;
   h.s.resize(L);
   for (int l = 0; l < L; ++l) h.s[l] = C2{s_in[2 * l], s_in[2 * l + 1]};
@@ -1135,6 +1139,7 @@ int64_t orc_h2_aca_near(void* hp, const double* s_in, int32_t L, double eps, con
                         int32_t* ranks, int32_t* fragile) {
   H2& h = *(H2*)hp;
   if (h.aca_done && h.L != L) return -1;
+  h.tw_done = false;
   h.L = L;
   h.s.resize(L);
   for (int l = 0; l < L; ++l) h.s[l] = C2{s_in[2 * l], s_in[2 * l + 1]};
@@ -1337,4 +1342,235 @@ int32_t orc_aca_matrix(const double* A, int32_t pp, int32_t L, double eps, int32
   return r;
 }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// NEXT-2: time-domain weights from the compressed tensor and the
+// fast right-hand-side convolution (eq:fastdft P:1542-1553, eq:fastrhs
+// P:1566-1573), on the combined skeleton (every block b in P+ and P-):
+//   V^_n[b] = sum_t C_{b,t} dhat_{b,t}[n],
+//   dhat_{b,t}[n] = (R^{-n}/L) sum_l Z_b[t,l] e^{+2 pi i (n l mod L)/L}  (reading D2: L = N+1,
+//                   the inverse transform of C5 applied to the coefficient row),
+//   C_{b,t} = S_b(s_{k_t}) (far, with the bases U_r, W_c) or V_{k_t}[b] (near, stored).
+// The MoT recursion itself (eq:cqmrhs P:652-680 and the LU of V^_0)
+// is written in oracle/__init__.py on top of these.
+// ---------------------------------------------------------------------------
+static void up_pass(const H2& h, const std::vector<cplx>& x, std::vector<cplx>& xh) {
+  const int p = h.p, C = (int)h.cl.size();
+  xh.assign((size_t)C * p, cplx(0.0, 0.0));
+  for (int c = C - 1; c >= 0; --c) {
+    const Cluster& cc = h.cl[c];
+    cplx* out = &xh[(size_t)c * p];
+    if (cc.son0 < 0) {
+      for (int nu = 0; nu < p; ++nu) {
+        cplx acc(0.0, 0.0);
+        for (int k = cc.begin; k < cc.end; ++k) acc += h.W[(size_t)k * p + nu] * x[k];
+        out[nu] = acc;
+      }
+    } else {
+      for (int son : {cc.son0, cc.son1}) {
+        const double* Es = &h.E[(size_t)son * p * p];
+        for (int mu = 0; mu < p; ++mu) {
+          cplx acc(0.0, 0.0);
+          for (int lam = 0; lam < p; ++lam) acc += Es[(size_t)lam * p + mu] * xh[(size_t)son * p + lam];
+          out[mu] += acc;
+        }
+      }
+    }
+  }
+}
+
+static void down_pass(const H2& h, std::vector<cplx>& yh, std::vector<cplx>& y) {
+  const int p = h.p, C = (int)h.cl.size();
+  for (int c = 0; c < C; ++c) {
+    const Cluster& cc = h.cl[c];
+    if (cc.parent >= 0) {
+      const double* Es = &h.E[(size_t)c * p * p];
+      for (int lam = 0; lam < p; ++lam) {
+        cplx acc(0.0, 0.0);
+        for (int mu = 0; mu < p; ++mu) acc += Es[(size_t)lam * p + mu] * yh[(size_t)cc.parent * p + mu];
+        yh[(size_t)c * p + lam] += acc;
+      }
+    }
+    if (cc.son0 < 0)
+      for (int k = cc.begin; k < cc.end; ++k) {
+        cplx acc(0.0, 0.0);
+        for (int mu = 0; mu < p; ++mu) acc += h.U[(size_t)k * p + mu] * yh[(size_t)c * p + mu];
+        y[k] += acc;
+      }
+  }
+}
+
+
+static void dhat_rows(const std::vector<C2>& Z, int L, int N, double R, std::vector<cplx>& D) {
+  const size_t rows = Z.size() / (size_t)L;
+  D.assign(Z.size(), cplx(0.0, 0.0));
+  std::vector<cplx> zf(L), dt(L);
+  for (size_t r = 0; r < rows; ++r) {
+    for (int l = 0; l < L; ++l) zf[l] = cplx(Z[r * L + l].re, Z[r * L + l].im);
+    inverse(zf.data(), dt.data(), 1, N, R);
+    for (int n = 0; n < L; ++n) D[r * L + n] = dt[n];
+  }
+}
+
+
+// y_n = sum_{k = 0}^{min(n, kmax)} V^_{n-k} q_k for n = 0..N (cluster-basis form of
+// eq:fastrhs: per block and term, u = sum_k dhat[n-k] Xc_k first, then C_t u).
+static void conv_time(const H2& h, const cplx* q_in, cplx* y_out, int kmax) {
+  const int L = h.L, p = h.p, m = h.m, C = (int)h.cl.size();
+  const int64_t M = h.g.M;
+  std::vector<std::vector<cplx>> q(L, std::vector<cplx>(M)), xh(L);
+  for (int k = 0; k < L; ++k) {
+    for (int64_t a = 0; a < M; ++a) q[k][a] = q_in[(int64_t)k * M + h.perm[a]];
+    up_pass(h, q[k], xh[k]);
+  }
+  std::vector<cplx> S((size_t)p * p), u(std::max<int64_t>(p, 1)), un;
+  for (int n = 0; n < L; ++n) {
+    const int kend = std::min(n, kmax);
+    std::vector<cplx> yh((size_t)C * p, cplx(0.0, 0.0)), y(M, cplx(0.0, 0.0));
+    for (size_t b = 0; b < h.farR.size(); ++b) {
+      const int r = h.farR[b], c = h.farC[b];
+      const double* xr = &h.xi[(size_t)r * 3 * m];
+      const double* xc = &h.xi[(size_t)c * 3 * m];
+      for (int t = 0; t < h.rank[b]; ++t) {
+        const cplx* d = &h.tDf[h.zoff[b] + (size_t)t * L];
+        for (int nu = 0; nu < p; ++nu) {
+          cplx acc(0.0, 0.0);
+          for (int k = 0; k <= kend; ++k) acc += d[n - k] * xh[k][(size_t)c * p + nu];
+          u[nu] = acc;
+        }
+        const int kk = h.pivk[h.pivoff[b] + t];
+        const cplx sk(h.s[kk].re, h.s[kk].im);
+        for (int mu = 0; mu < p; ++mu) {
+          cplx acc(0.0, 0.0);
+          for (int nu = 0; nu < p; ++nu) {
+            double a3[3], b3[3];
+            node_point(xr, m, mu, a3); node_point(xc, m, nu, b3);
+            const double dx = b3[0] - a3[0], dy = b3[1] - a3[1], dz = b3[2] - a3[2];
+            acc += kernel(std::sqrt((dx * dx + dy * dy) + dz * dz), sk) * u[nu];
+          }
+          yh[(size_t)r * p + mu] += acc;
+        }
+      }
+    }
+    down_pass(h, yh, y);
+    for (size_t b = 0; b < h.nearR.size(); ++b) {
+      const Cluster& R = h.cl[h.nearR[b]];
+      const Cluster& Cc = h.cl[h.nearC[b]];
+      const int nr = R.end - R.begin, nc = Cc.end - Cc.begin;
+      un.assign(nc, cplx(0.0, 0.0));
+      for (int t = 0; t < h.nrank[b]; ++t) {
+        const cplx* d = &h.tDn[h.nzoff[b] + (size_t)t * L];
+        for (int j = 0; j < nc; ++j) {
+          cplx acc(0.0, 0.0);
+          for (int k = 0; k <= kend; ++k) acc += d[n - k] * q[k][Cc.begin + j];
+          un[j] = acc;
+        }
+        const C2* Sl = &h.nS[h.nsoff[b] + (size_t)t * nr * nc];
+        for (int i = 0; i < nr; ++i) {
+          cplx acc(0.0, 0.0);
+          for (int j = 0; j < nc; ++j) acc += cplx(Sl[(size_t)i * nc + j].re, Sl[(size_t)i * nc + j].im) * un[j];
+          y[R.begin + i] += acc;
+        }
+      }
+    }
+    for (int64_t a = 0; a < M; ++a) y_out[(int64_t)n * M + h.perm[a]] = y[a];
+  }
+}
+
+// Dense V^_n (input order) assembled from the same compressed weights (for the
+// oracle's LU-based MoT and the pins).
+static void weight_dense(const H2& h, int n, cplx* A) {
+  const int L = h.L, p = h.p, m = h.m;
+  const int64_t M = h.g.M;
+  std::fill(A, A + M * M, cplx(0.0, 0.0));
+  std::vector<cplx> G((size_t)p * p);
+  for (size_t b = 0; b < h.farR.size(); ++b) {
+    const int r = h.farR[b], c = h.farC[b];
+    const double* xr = &h.xi[(size_t)r * 3 * m];
+    const double* xc = &h.xi[(size_t)c * 3 * m];
+    std::fill(G.begin(), G.end(), cplx(0.0, 0.0));
+    for (int t = 0; t < h.rank[b]; ++t) {
+      const cplx d = h.tDf[h.zoff[b] + (size_t)t * L + n];
+      const int kk = h.pivk[h.pivoff[b] + t];
+      const cplx sk(h.s[kk].re, h.s[kk].im);
+      for (int mu = 0; mu < p; ++mu)
+        for (int nu = 0; nu < p; ++nu) {
+          double a3[3], b3[3];
+          node_point(xr, m, mu, a3); node_point(xc, m, nu, b3);
+          const double dx = b3[0] - a3[0], dy = b3[1] - a3[1], dz = b3[2] - a3[2];
+          G[(size_t)mu * p + nu] += d * kernel(std::sqrt((dx * dx + dy * dy) + dz * dz), sk);
+        }
+    }
+    // V^_n[rows of r, cols of c] = U_r G W_c^T with the clusters' own Lagrange bases
+    // (P:957-978): U_r[a,mu] = L_{r,mu}(c_a), W_c[k,nu] = |T_k| sum_q w_q L_{c,nu}(y_{k,q})
+    const Cluster& R = h.cl[r];
+    const Cluster& Cc = h.cl[c];
+    std::vector<double> Wc((size_t)(Cc.end - Cc.begin) * p);
+    for (int k = Cc.begin; k < Cc.end; ++k) {
+      const int i = h.perm[k];
+      for (int nu = 0; nu < p; ++nu) {
+        double acc = 0.0;
+        for (int q = 0; q < 7; ++q) acc += RULE.w[q] * lagrange3(xc, m, nu, &h.g.node[21 * i + 3 * q]);
+        Wc[(size_t)(k - Cc.begin) * p + nu] = h.g.area[i] * acc;
+      }
+    }
+    std::vector<cplx> GW((size_t)p * (Cc.end - Cc.begin));
+    for (int mu = 0; mu < p; ++mu)
+      for (int k = 0; k < Cc.end - Cc.begin; ++k) {
+        cplx row(0.0, 0.0);
+        for (int nu = 0; nu < p; ++nu) row += G[(size_t)mu * p + nu] * Wc[(size_t)k * p + nu];
+        GW[(size_t)mu * (Cc.end - Cc.begin) + k] = row;
+      }
+    for (int a = R.begin; a < R.end; ++a) {
+      double ur[512];
+      for (int mu = 0; mu < p; ++mu) ur[mu] = lagrange3(xr, m, mu, &h.g.cen[3 * h.perm[a]]);
+      for (int k = Cc.begin; k < Cc.end; ++k) {
+        cplx acc(0.0, 0.0);
+        for (int mu = 0; mu < p; ++mu) acc += ur[mu] * GW[(size_t)mu * (Cc.end - Cc.begin) + (k - Cc.begin)];
+        A[(int64_t)h.perm[a] * M + h.perm[k]] += acc;
+      }
+    }
+  }
+  for (size_t b = 0; b < h.nearR.size(); ++b) {
+    const Cluster& R = h.cl[h.nearR[b]];
+    const Cluster& Cc = h.cl[h.nearC[b]];
+    const int nr = R.end - R.begin, nc = Cc.end - Cc.begin;
+    for (int t = 0; t < h.nrank[b]; ++t) {
+      const cplx d = h.tDn[h.nzoff[b] + (size_t)t * L + n];
+      const C2* Sl = &h.nS[h.nsoff[b] + (size_t)t * nr * nc];
+      for (int i = 0; i < nr; ++i)
+        for (int j = 0; j < nc; ++j)
+          A[(int64_t)h.perm[R.begin + i] * M + h.perm[Cc.begin + j]] +=
+              d * cplx(Sl[(size_t)i * nc + j].re, Sl[(size_t)i * nc + j].im);
+    }
+  }
+}
+
+extern "C" {
+// dhat rows of every far and near block (requires orc_h2_aca and orc_h2_aca_near with
+// the same L); R is the transform's scaling.
+int orc_h2_time_weights(void* hp, double R) {
+  H2& h = *(H2*)hp;
+  if (!h.aca_done || !h.near_done) return -1;
+  dhat_rows(h.Z, h.L, h.L - 1, R, h.tDf);
+  dhat_rows(h.nZ, h.L, h.L - 1, R, h.tDn);
+  h.tw_done = true;
+  return 0;
+}
+
+// y[n][:] = sum_{k <= min(n, kmax)} V^_{n-k} q[k][:], input order, complex [L][M].
+int orc_h2_conv(void* hp, const double* q, double* y, int32_t kmax) {
+  H2& h = *(H2*)hp;
+  if (!h.tw_done) return -1;
+  conv_time(h, (const cplx*)q, (cplx*)y, kmax);
+  return 0;
+}
+
+int orc_h2_weight_dense(void* hp, int32_t n, double* A) {
+  H2& h = *(H2*)hp;
+  if (!h.tw_done || n < 0 || n >= h.L) return -1;
+  weight_dense(h, n, (cplx*)A);
+  return 0;
+}
 }  // extern "C"

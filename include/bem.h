@@ -146,6 +146,27 @@ bem_status bem_apply_multifreq(bem_op op, const bem_c128* x, bem_c128* y, void* 
  * x, y: device [n_local][M] complex, input panel order, no overlap.  Asynchronous. */
 bem_status bem_apply_double_layer(bem_op op, const bem_c128* x, bem_c128* y, double alpha, void* cuda_stream);
 
+/* Time-domain path with compressed weights (eq:fastdft
+ * P:1542-1553, eq:fastrhs P:1566-1573, eq:cqmrhs P:652-680).  The op must be
+ * BEM_MODE_COMBINED (every block in MACA skeleton form) and hold all L = N+1
+ * frequencies (local_l = 0..L-1); else ESTATE / EINVAL.
+ * bem_mot_prepare: dhat_{b,t}[n] = (R^{-n}/L) sum_l Z_b[t,l] e^{+2 pi i (nl mod L)/L}
+ *   for every far and near skeleton row (the weights V^_n[b] = sum_t C_{b,t} dhat_{b,t}[n]),
+ *   and stores the far pivot slices S_b(s_{k_t}) (16 sum_b r_b p^2 bytes).  Synchronous.
+ * bem_conv_time: y_n = sum_{k <= min(n, kmax)} V^_{n-k} q_k, n = 0..N, with the compressed
+ *   weights in the order of eq:fastrhs.  q, y: device [L][M] complex, input panel order,
+ *   no overlap.  Synchronous.
+ * cqm_mot_solve: marching on in time for V q = g: for n = 0..N solve
+ *   Re V^_0 q_n = g_n - Re sum_{k<n} V^_{n-k} q_k by GMRES(restart) to tol (the paper
+ *   factorises V^_0 once; an iterative solver is its stated alternative).
+ *   g_time, phi_time: device [L][M] real.  stats over the time steps.  Synchronous;
+ *   ENOCONV if some step missed tol (phi_time still written).  Stable only where the
+ *   discretisation's recursion is (Courant >~ 0.5 for this collocation). */
+bem_status bem_mot_prepare(bem_op op, double R, void* cuda_stream);
+bem_status bem_conv_time(bem_op op, const bem_c128* q, bem_c128* y, int32_t kmax, void* cuda_stream);
+bem_status cqm_mot_solve(bem_op op, const double* g_time, double* phi_time, double tol, int32_t restart,
+                         int32_t max_iter, void* cuda_stream, bem_solve_stats* stats);
+
 /* R-scaled CQM transforms (eq:omega_n P:436-441, eq:slphelm P:529-540; D2):
  *   forward:  x_freq[l] = sum_{n=0}^{N} R^n x_time[n] e^{-2 pi i n l / L}
  *   inverse:  y_time[n] = R^{-n}/L sum_{l=0}^{L-1} y_freq[l] e^{+2 pi i n l / L}

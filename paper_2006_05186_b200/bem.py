@@ -37,7 +37,7 @@ class SolveStats(C.Structure):
 
 EXPORTS = [
     "bem_last_error", "cqm_frequencies", "bem_build_tree", "bem_tree_get_stats", "bem_tree_export",
-    "bem_tree_destroy", "bem_assemble_h2_aca", "bem_aca_export", "bem_aca_export_near", "bem_op_destroy", "bem_apply_multifreq", "bem_apply_double_layer",
+    "bem_tree_destroy", "bem_assemble_h2_aca", "bem_aca_export", "bem_aca_export_near", "bem_mot_prepare", "bem_conv_time", "cqm_mot_solve", "bem_op_destroy", "bem_apply_multifreq", "bem_apply_double_layer",
     "cqm_forward", "cqm_inverse", "cqm_forward_rows", "cqm_inverse_rows", "bem_ipc_get_handle",
     "bem_ipc_open_handle", "bem_ipc_close", "bem_device_alloc", "bem_device_free", "cqm_solve", "bem_solve_multifreq", "bem_debug_pinned", "bem_debug_fastmath", "bem_debug_fp64_peak",
     "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count", "bem_debug_fp64_peak_ex",
@@ -63,6 +63,9 @@ def lib():
         "bem_assemble_h2_aca": [vp, vp, i32, vp, i32, d, i32, vp, vp],
         "bem_aca_export": [vp, vp, vp, vp],
         "bem_aca_export_near": [vp, vp, vp, vp],
+        "bem_mot_prepare": [vp, d, vp],
+        "bem_conv_time": [vp, vp, vp, i32, vp],
+        "cqm_mot_solve": [vp, vp, vp, d, i32, i32, vp, vp],
         "bem_op_destroy": [vp],
         "bem_apply_multifreq": [vp, vp, vp, vp],
         "bem_apply_double_layer": [vp, vp, vp, d, vp],
@@ -205,6 +208,19 @@ class Operator:
         _check(lib().bem_aca_export_near(self.h, None, _p(piv), None))
         return dict(ranks=ranks, pivots=piv)
 
+    def mot_prepare(self, R: float, stream=None):
+        """Time-domain weights of the compressed tensor (eq:fastdft; BEM_MODE_COMBINED, all L)."""
+        _check(lib().bem_mot_prepare(self.h, float(R), _stream(stream)))
+
+    def conv_time(self, q, kmax: int | None = None, stream=None):
+        """y_n = sum_{k <= min(n, kmax)} V^_{n-k} q_k (eq:fastrhs); q device [L][M] complex."""
+        import torch
+        assert q.dtype == torch.complex128 and q.is_cuda and q.is_contiguous()
+        y = torch.empty_like(q)
+        _check(lib().bem_conv_time(self.h, _p(q), _p(y), int(q.shape[0] - 1 if kmax is None else kmax),
+                                   _stream(stream)))
+        return y
+
     def apply(self, x, y=None, stream=None):
         """x, y: torch complex128 [n_local][M] on the tree's device (input panel order)."""
         import torch
@@ -337,6 +353,20 @@ def cqm_solve(op: Operator, g_time, R: float, tol: float = 1e-8, restart: int = 
     st = SolveStats()
     code = lib().cqm_solve(op.h, _p(g_time), _p(phi), g_time.shape[1], float(R), float(tol), int(restart),
                            int(max_iter), None, _stream(stream), C.byref(st))
+    if code != 0 and not (code == BEM_ENOCONV and not raise_on_noconv):
+        _check(code)
+    return phi, {k: getattr(st, k) for k, _ in SolveStats._fields_ if k != "pad_"}
+
+
+def cqm_mot_solve(op: Operator, g_time, tol: float = 1e-10, restart: int = 50, max_iter: int = 2000, stream=None,
+                  raise_on_noconv: bool = True):
+    """Marching on in time with the compressed weights (eq:cqmrhs; op.mot_prepare first)."""
+    import torch
+    assert g_time.dtype == torch.float64 and g_time.is_cuda and g_time.is_contiguous()
+    phi = torch.empty_like(g_time)
+    st = SolveStats()
+    code = lib().cqm_mot_solve(op.h, _p(g_time), _p(phi), float(tol), int(restart), int(max_iter), _stream(stream),
+                               C.byref(st))
     if code != 0 and not (code == BEM_ENOCONV and not raise_on_noconv):
         _check(code)
     return phi, {k: getattr(st, k) for k, _ in SolveStats._fields_ if k != "pad_"}

@@ -219,6 +219,53 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
   return BEM_OK;
 }
 
+// Building blocks for the time-domain path (mot.cu): ncols columns, [ncols][M] layout.
+bem_status h2_gather(Op& op, const double2* x, double2* xc, int ncols, cudaStream_t st) {
+  const int64_t tot = op.tree->M * ncols;
+  gather_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(x, xc, op.tree->d_perm.p, op.tree->M, ncols);
+  BEM_CK(cudaGetLastError());
+  return BEM_OK;
+}
+
+bem_status h2_up(Op& op, const double2* xc, double2* xhat, int ncols, cudaStream_t st) {
+  Tree& t = *op.tree;
+  const unsigned tt = (unsigned)((ncols + kPassT - 1) / kPassT);
+  up_leaf_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, 0, st>>>(t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_W.p,
+                                                                           xc, xhat, t.M, ncols, t.p);
+  BEM_CK(cudaGetLastError());
+  for (int lv = t.depth - 1; lv >= 0; --lv) {
+    const int n = (int)t.level_nonleaf[lv].size();
+    if (n == 0) continue;
+    up_transfer_kernel<<<dim3((unsigned)n, tt), kPassThreads, 0, st>>>(t.d_level_nonleaf[lv].p, t.d_son0.p,
+                                                                       t.d_son1.p, t.d_E.p, xhat, ncols, t.p);
+    BEM_CK(cudaGetLastError());
+  }
+  return BEM_OK;
+}
+
+// y (input order) = ycn + U-side of the downward pass of yhat
+bem_status h2_down_scatter(Op& op, double2* yhat, const double2* ycn, double2* y, int ncols, cudaStream_t st) {
+  Tree& t = *op.tree;
+  const unsigned tt = (unsigned)((ncols + kPassT - 1) / kPassT);
+  if (t.far_r.empty()) {
+    const int64_t tot = t.M * ncols;
+    scatter_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(ycn, y, t.d_perm.p, t.M, ncols, ycn, 0.0);
+    BEM_CK(cudaGetLastError());
+    return BEM_OK;
+  }
+  for (int lv = 0; lv < t.depth; ++lv) {
+    const int n = (int)t.level_nonleaf[lv].size();
+    if (n == 0) continue;
+    down_transfer_kernel<<<dim3((unsigned)n, tt), kPassThreads, 0, st>>>(t.d_level_nonleaf[lv].p, t.d_son0.p,
+                                                                         t.d_son1.p, t.d_ET.p, yhat, ncols, t.p);
+    BEM_CK(cudaGetLastError());
+  }
+  down_leaf_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, 0, st>>>(
+      t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_UT.p, yhat, ycn, t.d_perm.p, y, t.M, ncols, t.p, 1, ycn, 0.0);
+  BEM_CK(cudaGetLastError());
+  return BEM_OK;
+}
+
 }  // namespace bem
 
 using namespace bem;

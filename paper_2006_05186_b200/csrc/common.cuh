@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -151,7 +152,13 @@ struct Op {
   DBuf<int32_t> d_nrank, d_npivk, d_npivq;
   DBuf<int64_t> d_nzoff, d_nsoff;
   DBuf<double> d_nZ, d_nS;
-  DBuf<int32_t> d_nm_order, d_nm_counter;  // K1m CTA order: leaf indices by descending sum_b r_b n_c (LPT)
+  DBuf<int32_t> d_nm_order, d_nm_counter;
+  // time-domain path (NEXT-2, mot.cu): dhat rows of the far / near skeletons (same offsets as
+  // d_Z / d_nZ, row length L), stored far pivot slices S_b(s_{k_t}) [r_b][p][p] at fsoff[b]
+  bool mot_ready = false;
+  double mot_R = 0.0;
+  DBuf<double> d_Df, d_Dn, d_fS;
+  DBuf<int64_t> d_fsoff;  // K1m CTA order: leaf indices by descending sum_b r_b n_c (LPT)
   // workspaces
   DBuf<double> d_xc, d_yc, d_xhat, d_yhat;
   // kernel variants (tuning knobs; env BEM_NEAR_F, BEM_FAR_GENERIC read at assembly)
@@ -180,6 +187,15 @@ bem_status apply_launch(Op& op, const double* x, double* y, cudaStream_t st, boo
 bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st, bool dl = false);
 bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st);
 bem_status launch_near_maca(Op& op, const double2* xc, double2* yc, cudaStream_t st);  // nearm.cu
+bem_status h2_gather(Op& op, const double2* x, double2* xc, int ncols, cudaStream_t st);
+bem_status h2_up(Op& op, const double2* xc, double2* xhat, int ncols, cudaStream_t st);
+bem_status h2_down_scatter(Op& op, double2* yhat, const double2* ycn, double2* y, int ncols, cudaStream_t st);
+// solve.cu: batched GMRES on an arbitrary operator ([nl][M] complex columns), stats
+bem_status gmres_fn(int64_t M, int nl, const std::function<bem_status(const double*, double*)>& apply,
+                    const double2* B, double2* X, double tol, int restart, int max_iter, cudaStream_t st,
+                    std::vector<int>& hit, std::vector<double>& hrel);
+bem_status solve_stats(const std::vector<int>& hit, const std::vector<double>& hrel, double tol, int max_iter,
+                       double imag_rel, bem_solve_stats* stats);
 // fft.cu
 bem_status fft_transform(const double* in, double* out, int64_t M, int N, double R, bool inverse,
                          cudaStream_t st);

@@ -9,6 +9,8 @@
 #include <cmath>
 #include <vector>
 
+#include <functional>
+
 #include "common.cuh"
 
 namespace bem {
@@ -253,11 +255,12 @@ namespace {
 // input panel order): solves V(s_l) X_t = B_t for every local t.  B, X:
 // device [n_local][M] complex.  Writes per-frequency iteration counts and the
 // final relative residuals (host vectors).
-bem_status gmres_multifreq(Op& op, const double2* B, double2* X, double tol, int restart, int max_iter,
-                           cudaStream_t st, std::vector<int>& hit, std::vector<double>& hrel) {
-  Tree& tr = *op.tree;
-  const int64_t M = tr.M;
-  const int nl = op.n_local;
+// Generic batched GMRES core: apply(x, w) computes w = A_t x_t for all nl columns
+// ([nl][M] complex); set_mask(mask) tells the operator which columns may skip work.
+template <class ApplyFn, class MaskFn>
+bem_status gmres_core(int64_t M, int nl, ApplyFn apply, MaskFn set_mask, bool use_mask, const double2* B, double2* X,
+                      double tol, int restart, int max_iter, cudaStream_t st, std::vector<int>& hit,
+                      std::vector<double>& hrel) {
   const int64_t n = M * nl;
   DBuf<double> r, w, V, h, H, g, cs, sn, y;
   DBuf<double> beta, bnorm, hn;
@@ -271,12 +274,11 @@ bem_status gmres_multifreq(Op& op, const double2* B, double2* X, double tol, int
   BEM_CK(active.alloc(nl)); BEM_CK(cyc.alloc(nl)); BEM_CK(jt.alloc(nl)); BEM_CK(iters.alloc(nl)); BEM_CK(cnt.alloc(1));
   double2* Rr = (double2*)r.p; double2* Wv = (double2*)w.p;
   double2* VV = (double2*)V.p;
-  // converged frequencies skip the K1 / K3 work of later applies (op.d_mask)
+  // converged frequencies skip the K1 / K3 work of later applies (mask)
   struct MaskGuard {
-    Op& o;
-    ~MaskGuard() { o.d_mask = nullptr; }
-  } mask_guard{op};
-  const bool use_mask = op.use_solve_mask;
+    MaskFn& f;
+    ~MaskGuard() { f(nullptr); }
+  } mask_guard{set_mask};
   norm_kernel<<<nl, kRed, 0, st>>>(B, bnorm.p, M);
   BEM_CK(cudaMemsetAsync(X, 0, sizeof(double2) * n, st));
   BEM_CK(cudaMemsetAsync(iters.p, 0, sizeof(int) * nl, st));
@@ -289,8 +291,8 @@ bem_status gmres_multifreq(Op& op, const double2* B, double2* X, double tol, int
   bem_status rs;
   for (;;) {
     // r = b - A x ; beta = ||r||
-    op.d_mask = use_mask ? active.p : nullptr;
-    rs = apply_launch(op, (const double*)X, w.p, st);
+    set_mask(use_mask ? active.p : nullptr);
+    rs = apply((const double*)X, w.p);
     if (rs != BEM_OK) return rs;
     axpby_kernel<<<nblk(n), 256, 0, st>>>(B, Wv, Rr, n);
     norm_kernel<<<nl, kRed, 0, st>>>(Rr, beta.p, M);
@@ -304,8 +306,8 @@ bem_status gmres_multifreq(Op& op, const double2* B, double2* X, double tol, int
     if (hcnt == 0 || total >= max_iter) break;
     scale_kernel<<<nblk(n), 256, 0, st>>>(Rr, beta.p, VV, M, nl);
     for (int j = 0; j < restart && total < max_iter; ++j) {
-      op.d_mask = use_mask ? cyc.p : nullptr;
-      rs = apply_launch(op, (const double*)(VV + (int64_t)j * n), w.p, st);
+      set_mask(use_mask ? cyc.p : nullptr);
+      rs = apply((const double*)(VV + (int64_t)j * n), w.p);
       if (rs != BEM_OK) return rs;
       ++total;
       for (int pass = 0; pass < 2; ++pass) {
@@ -328,8 +330,8 @@ bem_status gmres_multifreq(Op& op, const double2* B, double2* X, double tol, int
     BEM_CK(cudaGetLastError());
   }
   if (use_mask) {  // true final residuals of every frequency (the last masked apply zeroed converged ones)
-    op.d_mask = nullptr;
-    rs = apply_launch(op, (const double*)X, w.p, st);
+    set_mask(nullptr);
+    rs = apply((const double*)X, w.p);
     if (rs != BEM_OK) return rs;
     axpby_kernel<<<nblk(n), 256, 0, st>>>(B, Wv, Rr, n);
     norm_kernel<<<nl, kRed, 0, st>>>(Rr, beta.p, M);
@@ -343,6 +345,14 @@ bem_status gmres_multifreq(Op& op, const double2* B, double2* X, double tol, int
   BEM_CK(cudaMemcpy(hit.data(), iters.p, sizeof(int) * nl, cudaMemcpyDeviceToHost));
   for (int t = 0; t < nl; ++t) hrel[t] = hbn[t] > 0.0 ? hb[t] / hbn[t] : 0.0;
   return BEM_OK;
+}
+
+bem_status gmres_multifreq(Op& op, const double2* B, double2* X, double tol, int restart, int max_iter,
+                           cudaStream_t st, std::vector<int>& hit, std::vector<double>& hrel) {
+  auto apply = [&](const double* x, double* w) { return apply_launch(op, x, w, st); };
+  auto set_mask = [&](const int32_t* m) { op.d_mask = m; };
+  return gmres_core(op.tree->M, op.n_local, apply, set_mask, op.use_solve_mask, B, X, tol, restart, max_iter, st, hit,
+                    hrel);
 }
 
 bem_status finish_stats(const std::vector<int>& hit, const std::vector<double>& hrel, double tol, int max_iter,
@@ -367,6 +377,19 @@ bem_status finish_stats(const std::vector<int>& hit, const std::vector<double>& 
 }
 
 }  // namespace
+
+bem_status gmres_fn(int64_t M, int nl, const std::function<bem_status(const double*, double*)>& apply,
+                    const double2* B, double2* X, double tol, int restart, int max_iter, cudaStream_t st,
+                    std::vector<int>& hit, std::vector<double>& hrel) {
+  auto set_mask = [](const int32_t*) {};
+  return gmres_core(M, nl, apply, set_mask, false, B, X, tol, restart, max_iter, st, hit, hrel);
+}
+
+bem_status solve_stats(const std::vector<int>& hit, const std::vector<double>& hrel, double tol, int max_iter,
+                       double imag_rel, bem_solve_stats* stats) {
+  return finish_stats(hit, hrel, tol, max_iter, imag_rel, stats);
+}
+
 }  // namespace bem
 
 extern "C" bem_status bem_solve_multifreq(bem_op oh, const bem_c128* g_freq, bem_c128* phi_freq, double tol,

@@ -158,7 +158,10 @@ struct Op {
   bool mot_ready = false;
   double mot_R = 0.0;
   DBuf<double> d_Df, d_Dn, d_fS;
-  DBuf<int64_t> d_fsoff;  // K1m CTA order: leaf indices by descending sum_b r_b n_c (LPT)
+  DBuf<int64_t> d_fsoff;
+  DBuf<double> d_g0f, d_g0n;  // Re V^_0 blocks (far p x p, near n_r x n_c at d_g0noff)
+  DBuf<int64_t> d_g0noff;
+  DBuf<double> d_conv_part;  // per-block partial sums of the time-domain convolution  // K1m CTA order: leaf indices by descending sum_b r_b n_c (LPT)
   // workspaces
   DBuf<double> d_xc, d_yc, d_xhat, d_yhat;
   // kernel variants (tuning knobs; env BEM_NEAR_F, BEM_FAR_GENERIC read at assembly)
@@ -190,10 +193,17 @@ bem_status launch_near_maca(Op& op, const double2* xc, double2* yc, cudaStream_t
 bem_status h2_gather(Op& op, const double2* x, double2* xc, int ncols, cudaStream_t st);
 bem_status h2_up(Op& op, const double2* xc, double2* xhat, int ncols, cudaStream_t st);
 bem_status h2_down_scatter(Op& op, double2* yhat, const double2* ycn, double2* y, int ncols, cudaStream_t st);
-// solve.cu: batched GMRES on an arbitrary operator ([nl][M] complex columns), stats
+// solve.cu: batched GMRES on an arbitrary operator ([nl][M] complex columns), stats;
+// the workspace is reused across calls of the same shape (the MoT solves one system per step)
+struct GmresWs {
+  DBuf<double> r, w, V, h, H, g, cs, sn, y, beta, bnorm, hn;
+  DBuf<int> active, cyc, jt, iters, cnt;
+  int64_t n = -1;
+  int nl = -1, restart = -1;
+};
 bem_status gmres_fn(int64_t M, int nl, const std::function<bem_status(const double*, double*)>& apply,
                     const double2* B, double2* X, double tol, int restart, int max_iter, cudaStream_t st,
-                    std::vector<int>& hit, std::vector<double>& hrel);
+                    std::vector<int>& hit, std::vector<double>& hrel, GmresWs& ws);
 bem_status solve_stats(const std::vector<int>& hit, const std::vector<double>& hrel, double tol, int max_iter,
                        double imag_rel, bem_solve_stats* stats);
 // fft.cu

@@ -13,10 +13,12 @@
 // by GMRES through the same skeleton (the paper factorises V^_0 once, P:686-703;
 // an iterative solver is its stated alternative).
 //
-// Kernels (memory/latency-bound matrix-vector work, one CTA per row cluster or
-// row leaf and time column; deterministic): dhat_kernel (the transform of the
-// coefficient rows, setup), far_slice_kernel (stores the pivot slices S_b(s_{k_t}),
-// setup), conv_far_kernel, conv_near_kernel.
+// Kernels (memory/latency-bound matrix-vector work; deterministic): dhat_kernel
+// (the transform of the coefficient rows, setup), far_slice_kernel (stores the
+// pivot slices S_b(s_{k_t}), setup), conv_block_kernel<far|near> (one CTA per
+// block and time column: history sums, then the slice products) with fixed-order
+// row reductions, g0_block_kernel<far|near> (Re V^_0 as a real H^2 matrix, every
+// GMRES step).
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -87,6 +89,7 @@ struct ConvArgs {
   const int32_t* leaves;
   const int32_t* nb_ptr;
   const int32_t* nb_sorted;
+  const int32_t* near_r;
   const int32_t* near_c;
   const int32_t* cbegin;
   const int32_t* cend;
@@ -106,67 +109,187 @@ __device__ __forceinline__ void cmac(double2& a, double2 x, double2 y) {
   a.y = fma(x.y, y.x, a.y);
 }
 
-// yhat_r[n] = sum_{b=(r,c)} sum_t S_{b,t} u_{b,t}[n],  u = sum_{k<=min(n,kmax)} dhat_{b,t}[n-k] XH_c[k]
-__global__ void conv_far_kernel(ConvArgs a) {
+// One CTA per (block, time column): u_t = sum_{k<=min(n,kmax)} dhat_{b,t}[n-k] X_c[k] for a chunk
+// of kTC terms at a time (shared memory), then thread (tc, row) accumulates
+// sum_{t in its share} C_{b,t}[row,:] u_t; the kConvTC partial sums are added in a fixed
+// order into the block's partial output (deterministic; rows are reduced per row cluster /
+// row leaf by block_reduce_kernel).  far: X = XH[c][k][0..p), C_{b,t} = S_b(s_{k_t}) (p x p);
+// near: X = Q[k][c0..c0+nc), C_{b,t} = V_{k_t}[b] (nr x nc).
+constexpr int kTC = 8;       // terms staged per chunk
+constexpr int kConvThreads = 256;
+
+template <bool NEAR>
+__global__ void __launch_bounds__(kConvThreads) conv_block_kernel(ConvArgs a, double2* __restrict__ part, int pmax) {
   extern __shared__ double2 sm[];
-  const int r = blockIdx.x, j = blockIdx.y, n = a.n0 + j, p = a.p;
-  const int b0 = a.far_ptr[r], b1 = a.far_ptr[r + 1];
-  if (b0 == b1) return;
-  double2* u = sm;
-  double2 acc = make_double2(0.0, 0.0);  // thread mu < p
+  const int b = blockIdx.x, j = blockIdx.y, n = a.n0 + j;
+  int nr, nc, rk;
+  const double2* D;
+  const double2* S;
+  if constexpr (NEAR) {
+    const int r = a.near_r[b], c = a.near_c[b];
+    nr = a.cend[r] - a.cbegin[r];
+    nc = a.cend[c] - a.cbegin[c];
+    rk = a.nrank[b];
+    D = a.Dn + a.nzoff[b];
+    S = a.nS + a.nsoff[b];
+  } else {
+    nr = nc = a.p;
+    rk = a.rank[b];
+    D = a.Df + a.zoff[b];
+    S = a.fS + a.fsoff[b];
+  }
   const int kend = min(n, a.kmax);
-  for (int bi = b0; bi < b1; ++bi) {
-    const int b = a.far_sorted[bi];
-    const int c = a.far_c[b];
-    for (int t = 0; t < a.rank[b]; ++t) {
-      const double2* d = a.Df + a.zoff[b] + (int64_t)t * a.L;
-      __syncthreads();
-      for (int nu = threadIdx.x; nu < p; nu += blockDim.x) {
-        double2 s = make_double2(0.0, 0.0);
-        for (int k = 0; k <= kend; ++k) cmac(s, d[n - k], a.XH[((int64_t)c * a.HS + k) * p + nu]);
-        u[nu] = s;
+  double2* u = sm;                 // kTC x nc
+  double2* red = sm + kTC * pmax;  // kTC x nr partials
+  const int tc = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2 acc[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  for (int t0 = 0; t0 < rk; t0 += kTC) {
+    const int nt = min(kTC, rk - t0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nt * nc; idx += kConvThreads) {
+      const int tt = idx / nc, nu = idx - tt * nc;
+      const double2* d = D + (int64_t)(t0 + tt) * a.L;
+      double2 sacc = make_double2(0.0, 0.0);
+      if constexpr (NEAR) {
+        const int64_t col = a.cbegin[a.near_c[b]] + nu;
+        for (int k = 0; k <= kend; ++k) cmac(sacc, d[n - k], a.Q[(int64_t)k * a.M + col]);
+      } else {
+        const int64_t base = (int64_t)a.far_c[b] * a.HS * a.p + nu;
+        for (int k = 0; k <= kend; ++k) cmac(sacc, d[n - k], a.XH[base + (int64_t)k * a.p]);
       }
-      __syncthreads();
-      const double2* S = a.fS + a.fsoff[b] + (int64_t)t * p * p;
-      if (threadIdx.x < p) {
-        const double2* Sm = S + (int64_t)threadIdx.x * p;
-        for (int nu = 0; nu < p; ++nu) cmac(acc, Sm[nu], u[nu]);
+      u[tt * nc + nu] = sacc;
+    }
+    __syncthreads();
+    if (tc < nt) {
+      const double2* St = S + (int64_t)(t0 + tc) * nr * nc;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = lane + 32 * i;
+        if (row < nr) {
+          const double2* Sr = St + (int64_t)row * nc;
+          for (int nu = 0; nu < nc; ++nu) cmac(acc[i], Sr[nu], u[tc * nc + nu]);
+        }
       }
     }
   }
-  if (threadIdx.x < p) a.yhat[((int64_t)r * a.ncols + j) * p + threadIdx.x] = acc;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = lane + 32 * i;
+    if (row < nr) red[tc * pmax + row] = acc[i];
+  }
+  __syncthreads();
+  for (int row = threadIdx.x; row < nr; row += kConvThreads) {
+    double2 v = make_double2(0.0, 0.0);
+    for (int w = 0; w < kTC; ++w) { v.x += red[w * pmax + row].x; v.y += red[w * pmax + row].y; }
+    part[((int64_t)b * a.ncols + j) * pmax + row] = v;
+  }
 }
 
-// ycn[n, rows of leaf] = sum_{b=(leaf,c)} sum_t V_{k_t}[b] u_{b,t}[n],  u = sum_k dhat[n-k] Q_k|_c
-__global__ void conv_near_kernel(ConvArgs a) {
-  extern __shared__ double2 sm[];
-  const int li = blockIdx.x, j = blockIdx.y, n = a.n0 + j;
-  const int r = a.leaves[li];
-  const int rb0 = a.cbegin[r], nr = a.cend[r] - rb0;
-  double2* u = sm;
-  double2 acc = make_double2(0.0, 0.0);  // thread i < nr
-  const int kend = min(n, a.kmax);
-  for (int bi = a.nb_ptr[li]; bi < a.nb_ptr[li + 1]; ++bi) {
-    const int b = a.nb_sorted[bi];
-    const int c = a.near_c[b];
-    const int cb0 = a.cbegin[c], nc = a.cend[c] - cb0;
-    for (int t = 0; t < a.nrank[b]; ++t) {
-      const double2* d = a.Dn + a.nzoff[b] + (int64_t)t * a.L;
-      __syncthreads();
-      for (int jj = threadIdx.x; jj < nc; jj += blockDim.x) {
-        double2 s = make_double2(0.0, 0.0);
-        for (int k = 0; k <= kend; ++k) cmac(s, d[n - k], a.Q[(int64_t)k * a.M + cb0 + jj]);
-        u[jj] = s;
-      }
-      __syncthreads();
-      const double2* S = a.nS + a.nsoff[b] + (int64_t)t * nr * nc;
-      if (threadIdx.x < nr) {
-        const double2* Si = S + (int64_t)threadIdx.x * nc;
-        for (int jj = 0; jj < nc; ++jj) cmac(acc, Si[jj], u[jj]);
-      }
+// far: yhat[r][j][:] = sum over the row's blocks (far CSR order) of the block partials
+__global__ void far_reduce_kernel(const int32_t* __restrict__ far_ptr, const int32_t* __restrict__ far_sorted,
+                                  const double2* __restrict__ part, double2* __restrict__ yhat, int ncols, int p) {
+  const int r = blockIdx.x, j = blockIdx.y;
+  const int b0 = far_ptr[r], b1 = far_ptr[r + 1];
+  if (b0 == b1) return;
+  for (int mu = threadIdx.x; mu < p; mu += blockDim.x) {
+    double2 v = make_double2(0.0, 0.0);
+    for (int bi = b0; bi < b1; ++bi) {
+      const double2 w = part[((int64_t)far_sorted[bi] * ncols + j) * p + mu];
+      v.x += w.x; v.y += w.y;
     }
+    yhat[((int64_t)r * ncols + j) * p + mu] = v;
   }
-  if (threadIdx.x < nr) a.ycn[(int64_t)j * a.M + rb0 + threadIdx.x] = acc;
+}
+
+// near: ycn[j][rows of leaf] = sum over the leaf's near blocks of the block partials
+__global__ void near_reduce_kernel(const int32_t* __restrict__ leaves, const int32_t* __restrict__ nb_ptr,
+                                   const int32_t* __restrict__ nb_sorted, const int32_t* __restrict__ cb,
+                                   const int32_t* __restrict__ ce, const double2* __restrict__ part,
+                                   double2* __restrict__ ycn, int64_t M, int ncols, int pmax) {
+  const int li = blockIdx.x, j = blockIdx.y;
+  const int r = leaves[li];
+  const int rb0 = cb[r], nr = ce[r] - rb0;
+  for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+    double2 v = make_double2(0.0, 0.0);
+    for (int bi = nb_ptr[li]; bi < nb_ptr[li + 1]; ++bi) {
+      const double2 w = part[((int64_t)nb_sorted[bi] * ncols + j) * pmax + i];
+      v.x += w.x; v.y += w.y;
+    }
+    ycn[(int64_t)j * M + rb0 + i] = v;
+  }
+}
+
+// Re V^_0 as a real H^2 matrix: G_b = Re sum_t C_{b,t} dhat_{b,t}[0] (far: p x p between the
+// cluster bases; near: n_r x n_c), assembled once so that each GMRES step of the MoT applies
+// one real matrix per block instead of r_b terms.
+__global__ void g0_far_build_kernel(const double2* __restrict__ fS, const int64_t* __restrict__ fsoff,
+                                    const double2* __restrict__ Df, const int64_t* __restrict__ zoff,
+                                    const int32_t* __restrict__ rank, int L, int p, double* __restrict__ G) {
+  const int b = blockIdx.x;
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    double acc = 0.0;
+    for (int t = 0; t < rank[b]; ++t) {
+      const double2 sv = fS[fsoff[b] + (int64_t)t * p * p + e], d = Df[zoff[b] + (int64_t)t * L];
+      acc += sv.x * d.x - sv.y * d.y;
+    }
+    G[(int64_t)b * p * p + e] = acc;
+  }
+}
+
+__global__ void g0_near_build_kernel(const double2* __restrict__ nS, const int64_t* __restrict__ nsoff,
+                                     const double2* __restrict__ Dn, const int64_t* __restrict__ nzoff,
+                                     const int32_t* __restrict__ nrank, const int32_t* __restrict__ near_r,
+                                     const int32_t* __restrict__ near_c, const int32_t* __restrict__ cb,
+                                     const int32_t* __restrict__ ce, const int64_t* __restrict__ goff, int L,
+                                     double* __restrict__ G) {
+  const int b = blockIdx.x;
+  const int nrnc = (ce[near_r[b]] - cb[near_r[b]]) * (ce[near_c[b]] - cb[near_c[b]]);
+  for (int e = threadIdx.x; e < nrnc; e += blockDim.x) {
+    double acc = 0.0;
+    for (int t = 0; t < nrank[b]; ++t) {
+      const double2 sv = nS[nsoff[b] + (int64_t)t * nrnc + e], d = Dn[nzoff[b] + (int64_t)t * L];
+      acc += sv.x * d.x - sv.y * d.y;
+    }
+    G[goff[b] + e] = acc;
+  }
+}
+
+// Re V^_0 x per block (one CTA per block; x_c staged in shared memory, thread = output
+// row), partials reduced per row cluster / row leaf by far_reduce_kernel / near_reduce_kernel.
+template <bool NEAR>
+__global__ void __launch_bounds__(128) g0_block_kernel(const int32_t* __restrict__ blk_r,
+                                                       const int32_t* __restrict__ blk_c,
+                                                       const int32_t* __restrict__ cb, const int32_t* __restrict__ ce,
+                                                       const int64_t* __restrict__ goff, const double* __restrict__ G,
+                                                       const double2* __restrict__ x, double2* __restrict__ part,
+                                                       int p, int pmax) {
+  extern __shared__ double2 xs[];
+  const int b = blockIdx.x;
+  int nr, nc;
+  const double2* xb;
+  const double* Gb;
+  if constexpr (NEAR) {
+    nr = ce[blk_r[b]] - cb[blk_r[b]];
+    nc = ce[blk_c[b]] - cb[blk_c[b]];
+    xb = x + cb[blk_c[b]];
+    Gb = G + goff[b];
+  } else {
+    nr = nc = p;
+    xb = x + (int64_t)blk_c[b] * p;
+    Gb = G + (int64_t)b * p * p;
+  }
+  for (int j = threadIdx.x; j < nc; j += blockDim.x) xs[j] = xb[j];
+  __syncthreads();
+  for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    const double* Gi = Gb + (int64_t)i * nc;
+    for (int j = 0; j < nc; ++j) {
+      acc.x = fma(Gi[j], xs[j].x, acc.x);
+      acc.y = fma(Gi[j], xs[j].y, acc.y);
+    }
+    part[(int64_t)b * pmax + i] = acc;
+  }
 }
 
 __global__ void rhs_kernel(const double* __restrict__ g, const double2* __restrict__ f, double2* __restrict__ b,
@@ -174,11 +297,6 @@ __global__ void rhs_kernel(const double* __restrict__ g, const double2* __restri
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= M) return;
   b[i] = make_double2(g[i] - (has_f ? f[i].x : 0.0), 0.0);
-}
-
-__global__ void real_part_kernel(double2* __restrict__ w, int64_t M) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < M) w[i].y = 0.0;
 }
 
 __global__ void store_step_kernel(const double2* __restrict__ x, double* __restrict__ phi, double2* __restrict__ xr,
@@ -206,6 +324,7 @@ ConvArgs conv_args(Op& op) {
   a.far_ptr = t.d_far_ptr.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p; a.rank = op.d_rank.p;
   a.zoff = op.d_zoff.p; a.fsoff = op.d_fsoff.p; a.Df = (const double2*)op.d_Df.p; a.fS = (const double2*)op.d_fS.p;
   a.leaves = t.d_leaves.p; a.nb_ptr = t.d_nb_ptr.p; a.nb_sorted = t.d_nb_sorted.p; a.near_c = t.d_near_c.p;
+  a.near_r = t.d_near_r.p;
   a.cbegin = t.d_begin.p; a.cend = t.d_end.p; a.nrank = op.d_nrank.p; a.nzoff = op.d_nzoff.p; a.nsoff = op.d_nsoff.p;
   a.Dn = (const double2*)op.d_Dn.p; a.nS = (const double2*)op.d_nS.p;
   return a;
@@ -217,15 +336,26 @@ bem_status conv_launch(Op& op, const double2* XH, const double2* Q, int HS, int 
   Tree& t = *op.tree;
   ConvArgs a = conv_args(op);
   a.HS = HS; a.n0 = n0; a.ncols = ncols; a.kmax = kmax; a.XH = XH; a.Q = Q; a.yhat = yhat; a.ycn = ycn;
-  const bool far = !t.far_r.empty();
-  if (far) {
+  const int nfar = (int)t.far_r.size(), nnear = (int)t.near_r.size();
+  const size_t need = std::max((size_t)nfar * ncols * t.p, (size_t)nnear * ncols * t.max_leaf) * 2;
+  if (op.d_conv_part.n < need) BEM_CK(op.d_conv_part.alloc(need));
+  double2* part = (double2*)op.d_conv_part.p;
+  if (nfar > 0) {
     BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * ncols * t.p, st));
-    conv_far_kernel<<<dim3((unsigned)t.C, (unsigned)ncols), std::max(32, (t.p + 31) / 32 * 32),
-                      sizeof(double2) * t.p, st>>>(a);
+    const size_t smf = sizeof(double2) * 2 * kTC * t.p;
+    BEM_CK(cudaFuncSetAttribute(conv_block_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf));
+    conv_block_kernel<false><<<dim3((unsigned)nfar, (unsigned)ncols), kConvThreads, smf, st>>>(a, part, t.p);
+    BEM_CK(cudaGetLastError());
+    far_reduce_kernel<<<dim3((unsigned)t.C, (unsigned)ncols), 128, 0, st>>>(t.d_far_ptr.p, t.d_far_sorted.p, part,
+                                                                             yhat, ncols, t.p);
     BEM_CK(cudaGetLastError());
   }
-  conv_near_kernel<<<dim3((unsigned)t.n_leaves, (unsigned)ncols), std::max(32, (t.max_leaf + 31) / 32 * 32),
-                     sizeof(double2) * t.max_leaf, st>>>(a);
+  const size_t smn = sizeof(double2) * 2 * kTC * t.max_leaf;
+  BEM_CK(cudaFuncSetAttribute(conv_block_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smn));
+  conv_block_kernel<true><<<dim3((unsigned)nnear, (unsigned)ncols), kConvThreads, smn, st>>>(a, part, t.max_leaf);
+  BEM_CK(cudaGetLastError());
+  near_reduce_kernel<<<dim3((unsigned)t.n_leaves, (unsigned)ncols), 64, 0, st>>>(
+      t.d_leaves.p, t.d_nb_ptr.p, t.d_nb_sorted.p, t.d_begin.p, t.d_end.p, part, ycn, t.M, ncols, t.max_leaf);
   BEM_CK(cudaGetLastError());
   return h2_down_scatter(op, yhat, ycn, y, ncols, st);
 }
@@ -274,6 +404,28 @@ extern "C" bem_status bem_mot_prepare(bem_op oh, double R, void* cuda_stream) {
   if (nfar > 0) {
     far_slice_kernel<<<nfar, 256, 0, st>>>(t.d_far_r.p, t.d_far_c.p, t.d_xi.p, (const double2*)op.d_s.p, op.d_rank.p,
                                            op.d_pivk.p, op.rcap, op.d_fsoff.p, (double2*)op.d_fS.p, t.m, p);
+    BEM_CK(cudaGetLastError());
+  }
+  // Re V^_0 blocks
+  BEM_CK(op.d_g0f.alloc((size_t)std::max(nfar, 1) * p * p));
+  if (nfar > 0) {
+    g0_far_build_kernel<<<nfar, 256, 0, st>>>((const double2*)op.d_fS.p, op.d_fsoff.p, (const double2*)op.d_Df.p,
+                                              op.d_zoff.p, op.d_rank.p, L, p, op.d_g0f.p);
+    BEM_CK(cudaGetLastError());
+  }
+  const int nnear = (int)t.near_r.size();
+  std::vector<int64_t> goff(std::max(nnear, 1), 0);
+  int64_t gt = 0;
+  for (int b = 0; b < nnear; ++b) {
+    goff[b] = gt;
+    gt += (int64_t)(t.end[t.near_r[b]] - t.begin[t.near_r[b]]) * (t.end[t.near_c[b]] - t.begin[t.near_c[b]]);
+  }
+  BEM_CK(op.d_g0noff.upload(goff));
+  BEM_CK(op.d_g0n.alloc((size_t)std::max<int64_t>(gt, 1)));
+  if (nnear > 0) {
+    g0_near_build_kernel<<<nnear, 256, 0, st>>>((const double2*)op.d_nS.p, op.d_nsoff.p, (const double2*)op.d_Dn.p,
+                                                op.d_nzoff.p, op.d_nrank.p, t.d_near_r.p, t.d_near_c.p, t.d_begin.p,
+                                                t.d_end.p, op.d_g0noff.p, L, op.d_g0n.p);
     BEM_CK(cudaGetLastError());
   }
   BEM_CK(cudaStreamSynchronize(st));
@@ -331,15 +483,32 @@ extern "C" bem_status cqm_mot_solve(bem_op oh, const double* g_time, double* phi
   // w = Re V^_0 x (one column, input order)
   auto v0 = [&](const double* x, double* w) -> bem_status {
     bem_status s = h2_gather(op, (const double2*)x, (double2*)xc1.p, 1, st);
-    if (s == BEM_OK && far) s = h2_up(op, (const double2*)xc1.p, (double2*)xh1.p, 1, st);
-    if (s == BEM_OK)
-      s = conv_launch(op, (const double2*)xh1.p, (const double2*)xc1.p, 1, 0, 1, 0, (double2*)yh1.p,
-                      (double2*)ycn1.p, (double2*)w, st);
     if (s != BEM_OK) return s;
-    real_part_kernel<<<nb(M), 256, 0, st>>>((double2*)w, M);
+    const int nfar = (int)t.far_r.size(), nnear = (int)t.near_r.size();
+    const size_t need = (size_t)std::max(nfar * p, nnear * t.max_leaf) * 2;
+    if (op.d_conv_part.n < need) BEM_CK(op.d_conv_part.alloc(need));
+    double2* part = (double2*)op.d_conv_part.p;
+    if (far) {
+      s = h2_up(op, (const double2*)xc1.p, (double2*)xh1.p, 1, st);
+      if (s != BEM_OK) return s;
+      BEM_CK(cudaMemsetAsync(yh1.p, 0, sizeof(double2) * (size_t)C * p, st));
+      g0_block_kernel<false><<<nfar, 128, sizeof(double2) * p, st>>>(t.d_far_r.p, t.d_far_c.p, t.d_begin.p,
+                                                                     t.d_end.p, nullptr, op.d_g0f.p,
+                                                                     (const double2*)xh1.p, part, p, p);
+      far_reduce_kernel<<<dim3((unsigned)C, 1), 128, 0, st>>>(t.d_far_ptr.p, t.d_far_sorted.p, part,
+                                                               (double2*)yh1.p, 1, p);
+      BEM_CK(cudaGetLastError());
+    }
+    g0_block_kernel<true><<<nnear, 128, sizeof(double2) * t.max_leaf, st>>>(
+        t.d_near_r.p, t.d_near_c.p, t.d_begin.p, t.d_end.p, op.d_g0noff.p, op.d_g0n.p, (const double2*)xc1.p, part,
+        p, t.max_leaf);
+    near_reduce_kernel<<<dim3((unsigned)t.n_leaves, 1), 64, 0, st>>>(t.d_leaves.p, t.d_nb_ptr.p, t.d_nb_sorted.p,
+                                                                     t.d_begin.p, t.d_end.p, part, (double2*)ycn1.p,
+                                                                     M, 1, t.max_leaf);
     BEM_CK(cudaGetLastError());
-    return BEM_OK;
+    return h2_down_scatter(op, (double2*)yh1.p, (const double2*)ycn1.p, (double2*)w, 1, st);
   };
+  GmresWs ws;
   int imax = 0, isum = 0;
   double rmax = 0.0;
   int nunc = 0;
@@ -353,7 +522,7 @@ extern "C" bem_status cqm_mot_solve(bem_op oh, const double* g_time, double* phi
     BEM_CK(cudaGetLastError());
     std::vector<int> hit;
     std::vector<double> hrel;
-    rs = gmres_fn(M, 1, v0, (const double2*)b1.p, (double2*)x1.p, tol, restart, max_iter, st, hit, hrel);
+    rs = gmres_fn(M, 1, v0, (const double2*)b1.p, (double2*)x1.p, tol, restart, max_iter, st, hit, hrel, ws);
     if (rs != BEM_OK) return rs;
     isum += hit[0];
     imax = std::max(imax, hit[0]);

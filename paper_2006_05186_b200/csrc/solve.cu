@@ -260,18 +260,22 @@ namespace {
 template <class ApplyFn, class MaskFn>
 bem_status gmres_core(int64_t M, int nl, ApplyFn apply, MaskFn set_mask, bool use_mask, const double2* B, double2* X,
                       double tol, int restart, int max_iter, cudaStream_t st, std::vector<int>& hit,
-                      std::vector<double>& hrel) {
+                      std::vector<double>& hrel, GmresWs& ws) {
   const int64_t n = M * nl;
-  DBuf<double> r, w, V, h, H, g, cs, sn, y;
-  DBuf<double> beta, bnorm, hn;
-  DBuf<int> active, cyc, jt, iters, cnt;
-  BEM_CK(r.alloc(2 * n));
-  BEM_CK(w.alloc(2 * n)); BEM_CK(V.alloc(2 * n * (restart + 1)));
-  BEM_CK(h.alloc(2 * (size_t)nl * (restart + 1))); BEM_CK(H.alloc(2 * (size_t)nl * (restart + 1) * restart));
-  BEM_CK(g.alloc(2 * (size_t)nl * (restart + 1))); BEM_CK(cs.alloc(2 * (size_t)nl * restart));
-  BEM_CK(sn.alloc(2 * (size_t)nl * restart)); BEM_CK(y.alloc(2 * (size_t)nl * restart));
-  BEM_CK(beta.alloc(nl)); BEM_CK(bnorm.alloc(nl)); BEM_CK(hn.alloc(nl));
-  BEM_CK(active.alloc(nl)); BEM_CK(cyc.alloc(nl)); BEM_CK(jt.alloc(nl)); BEM_CK(iters.alloc(nl)); BEM_CK(cnt.alloc(1));
+  if (ws.n != n || ws.nl != nl || ws.restart != restart) {  // (re)allocate the workspace
+    BEM_CK(ws.r.alloc(2 * n));
+    BEM_CK(ws.w.alloc(2 * n)); BEM_CK(ws.V.alloc(2 * n * (restart + 1)));
+    BEM_CK(ws.h.alloc(2 * (size_t)nl * (restart + 1))); BEM_CK(ws.H.alloc(2 * (size_t)nl * (restart + 1) * restart));
+    BEM_CK(ws.g.alloc(2 * (size_t)nl * (restart + 1))); BEM_CK(ws.cs.alloc(2 * (size_t)nl * restart));
+    BEM_CK(ws.sn.alloc(2 * (size_t)nl * restart)); BEM_CK(ws.y.alloc(2 * (size_t)nl * restart));
+    BEM_CK(ws.beta.alloc(nl)); BEM_CK(ws.bnorm.alloc(nl)); BEM_CK(ws.hn.alloc(nl));
+    BEM_CK(ws.active.alloc(nl)); BEM_CK(ws.cyc.alloc(nl)); BEM_CK(ws.jt.alloc(nl)); BEM_CK(ws.iters.alloc(nl));
+    BEM_CK(ws.cnt.alloc(1));
+    ws.n = n; ws.nl = nl; ws.restart = restart;
+  }
+  DBuf<double>&r = ws.r, &w = ws.w, &V = ws.V, &h = ws.h, &H = ws.H, &g = ws.g, &cs = ws.cs, &sn = ws.sn, &y = ws.y;
+  DBuf<double>&beta = ws.beta, &bnorm = ws.bnorm, &hn = ws.hn;
+  DBuf<int>&active = ws.active, &cyc = ws.cyc, &jt = ws.jt, &iters = ws.iters, &cnt = ws.cnt;
   double2* Rr = (double2*)r.p; double2* Wv = (double2*)w.p;
   double2* VV = (double2*)V.p;
   // converged frequencies skip the K1 / K3 work of later applies (mask)
@@ -351,8 +355,9 @@ bem_status gmres_multifreq(Op& op, const double2* B, double2* X, double tol, int
                            cudaStream_t st, std::vector<int>& hit, std::vector<double>& hrel) {
   auto apply = [&](const double* x, double* w) { return apply_launch(op, x, w, st); };
   auto set_mask = [&](const int32_t* m) { op.d_mask = m; };
+  GmresWs ws;
   return gmres_core(op.tree->M, op.n_local, apply, set_mask, op.use_solve_mask, B, X, tol, restart, max_iter, st, hit,
-                    hrel);
+                    hrel, ws);
 }
 
 bem_status finish_stats(const std::vector<int>& hit, const std::vector<double>& hrel, double tol, int max_iter,
@@ -380,9 +385,9 @@ bem_status finish_stats(const std::vector<int>& hit, const std::vector<double>& 
 
 bem_status gmres_fn(int64_t M, int nl, const std::function<bem_status(const double*, double*)>& apply,
                     const double2* B, double2* X, double tol, int restart, int max_iter, cudaStream_t st,
-                    std::vector<int>& hit, std::vector<double>& hrel) {
+                    std::vector<int>& hit, std::vector<double>& hrel, GmresWs& ws) {
   auto set_mask = [](const int32_t*) {};
-  return gmres_core(M, nl, apply, set_mask, false, B, X, tol, restart, max_iter, st, hit, hrel);
+  return gmres_core(M, nl, apply, set_mask, false, B, X, tol, restart, max_iter, st, hit, hrel, ws);
 }
 
 bem_status solve_stats(const std::vector<int>& hit, const std::vector<double>& hrel, double tol, int max_iter,

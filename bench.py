@@ -262,6 +262,7 @@ def main():
 
     opfn = op.apply if args.operator == "V" else (lambda z: op.apply_dl(z))
     transpose = None
+    lib_step = False
     if world > 1:
         top = None
         if args.transpose == "peer" and args.operator == "V":
@@ -281,6 +282,9 @@ def main():
     else:
         def step(z):
             return inv(opfn(fwd(z)))
+        # e2e: the library's one-call step on host buffers (bem_time_step: H2D, K4 forward,
+        # apply, K4 inverse replayed from the CUDA graph the op captures at its first call, D2H)
+        lib_step = args.operator == "V" and not args.no_graph
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     for _ in range(max(3, args.warmup)):
@@ -351,15 +355,22 @@ def main():
         xh = torch.from_numpy(xt_host).pin_memory()
         yh = torch.empty_like(xh).pin_memory()
         eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if lib_step:
+            for _ in range(2):  # the op captures its step graph at the first call: outside the timed region
+                op.time_step(xh, R, y=yh)
+            torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         for k in range(args.steps):
             flush.zero_()
             eev[k][0].record()
-            xd = xh.to(dev, non_blocking=True)
-            yd = step(xd)
-            yh.copy_(yd, non_blocking=True)
+            if lib_step:  # host buffers straight into the library call (H2D + step + D2H inside)
+                op.time_step(xh, R, y=yh)
+            else:
+                xd = xh.to(dev, non_blocking=True)
+                yd = step(xd)
+                yh.copy_(yd, non_blocking=True)
             eev[k][1].record()
             eev[k][1].synchronize()
         te = torch.tensor([sum(a.elapsed_time(bb) for a, bb in eev)], dtype=torch.float64, device=red_dev)
@@ -367,7 +378,9 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         ms_e2e = float(te.item()) / args.steps
         e2e = {"value": n_units / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 16),
-               "d2h_bytes_per_step": int(yh.numel() * 16), "ms_per_step": ms_e2e}
+               "d2h_bytes_per_step": int(yh.numel() * 16), "ms_per_step": ms_e2e,
+               "call": ("bem_time_step(op, host x, host y, R) per step (pinned host buffers)" if lib_step else
+                        "torch H2D copy, the step's C-ABI calls, torch D2H copy")}
 
     # roofline of the dominant kernel (algorithmic flops / live CUDA-event launch time)
     stats = tree.stats

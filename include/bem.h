@@ -146,6 +146,15 @@ bem_status bem_apply_multifreq(bem_op op, const bem_c128* x, bem_c128* y, void* 
  * x, y: device [n_local][M] complex, input panel order, no overlap.  Asynchronous. */
 bem_status bem_apply_double_layer(bem_op op, const bem_c128* x, bem_c128* y, double alpha, void* cuda_stream);
 
+/* One time-domain operator step, y_time = cqm_inverse(V(s_l) cqm_forward(x_time)) (the
+ * bench's step; eq:omega_n P:436-441 around eq:slphelm P:529-540).  x_time, y_time: [L][M]
+ * complex, input panel order, HOST (pageable or pinned) or DEVICE memory; the op must hold
+ * all L = N+1 frequencies (local_l = 0..L-1).  The device part runs from a CUDA graph the
+ * op captures at its first call (and again when R changes); host buffers are copied
+ * through the op's device time buffers.  Asynchronous on cuda_stream for pinned/device
+ * buffers.  Not while profiling is enabled (then eager). */
+bem_status bem_time_step(bem_op op, const bem_c128* x_time, bem_c128* y_time, double R, void* cuda_stream);
+
 /* Time-domain path with compressed weights (eq:fastdft
  * P:1542-1553, eq:fastrhs P:1566-1573, eq:cqmrhs P:652-680).  The op must be
  * BEM_MODE_COMBINED (every block in MACA skeleton form) and hold all L = N+1

@@ -37,7 +37,7 @@ class SolveStats(C.Structure):
 
 EXPORTS = [
     "bem_last_error", "cqm_frequencies", "bem_build_tree", "bem_tree_get_stats", "bem_tree_export",
-    "bem_tree_destroy", "bem_assemble_h2_aca", "bem_aca_export", "bem_aca_export_near", "bem_mot_prepare", "bem_conv_time", "cqm_mot_solve", "bem_op_destroy", "bem_apply_multifreq", "bem_apply_double_layer",
+    "bem_tree_destroy", "bem_assemble_h2_aca", "bem_aca_export", "bem_aca_export_near", "bem_mot_prepare", "bem_conv_time", "cqm_mot_solve", "bem_time_step", "bem_op_destroy", "bem_apply_multifreq", "bem_apply_double_layer",
     "cqm_forward", "cqm_inverse", "cqm_forward_rows", "cqm_inverse_rows", "bem_ipc_get_handle",
     "bem_ipc_open_handle", "bem_ipc_close", "bem_device_alloc", "bem_device_free", "cqm_solve", "bem_solve_multifreq", "bem_debug_pinned", "bem_debug_fastmath", "bem_debug_fp64_peak",
     "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count", "bem_debug_fp64_peak_ex",
@@ -64,6 +64,7 @@ def lib():
         "bem_aca_export": [vp, vp, vp, vp],
         "bem_aca_export_near": [vp, vp, vp, vp],
         "bem_mot_prepare": [vp, d, vp],
+        "bem_time_step": [vp, vp, vp, d, vp],
         "bem_conv_time": [vp, vp, vp, i32, vp],
         "cqm_mot_solve": [vp, vp, vp, d, i32, i32, vp, vp],
         "bem_op_destroy": [vp],
@@ -207,6 +208,15 @@ class Operator:
         piv = np.empty((tot.value, 2), dtype=np.int32)
         _check(lib().bem_aca_export_near(self.h, None, _p(piv), None))
         return dict(ranks=ranks, pivots=piv)
+
+    def time_step(self, x_time, R: float, y=None, stream=None):
+        """y = cqm_inverse(V(s_l) cqm_forward(x_time)) in one library call (graph-replayed device
+        part); x_time: [L][M] complex128 torch tensor on the host (pinned for async) or device."""
+        import torch
+        assert x_time.dtype == torch.complex128 and x_time.is_contiguous()
+        y = torch.empty_like(x_time, pin_memory=not x_time.is_cuda) if y is None else y
+        _check(lib().bem_time_step(self.h, _p(x_time), _p(y), float(R), _stream(stream)))
+        return y
 
     def mot_prepare(self, R: float, stream=None):
         """Time-domain weights of the compressed tensor (eq:fastdft; BEM_MODE_COMBINED, all L)."""

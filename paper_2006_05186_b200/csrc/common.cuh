@@ -119,6 +119,19 @@ struct Tree {
   std::vector<DBuf<int32_t>> d_level_nonleaf;
 };
 
+// bem_time_step's device buffers and captured graph (step.cu)
+struct StepGraph {
+  DBuf<double> tx, xf, yf, ty;  // [L][M] complex each
+  cudaStream_t own = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  double R = 0.0;
+  StepGraph() = default;
+  StepGraph(const StepGraph&) = delete;
+  StepGraph& operator=(const StepGraph&) = delete;
+  ~StepGraph();
+};
+
 struct Op {
   Tree* tree = nullptr;
   int L = 0, n_local = 0, mode = 0;
@@ -179,6 +192,7 @@ struct Op {
   // converged frequencies skip K1 / K3 work (their outputs are then zero)
   const int32_t* d_mask = nullptr;
   bool use_solve_mask = true;  // env BEM_SOLVE_MASK=0 disables
+  StepGraph step;  // bem_time_step
   // profiling
   bool profile = false;
   cudaEvent_t ev[6] = {};

@@ -111,6 +111,7 @@ bem_status bem_tree_destroy(bem_tree t);
  *         evaluated in pinned arithmetic; stores the pivot slices V_{k_t}[b], i.e.
  *         16 * sum_b r_b n_r n_c bytes -- the tensor C_b of eq:lrfinal).
  *         The double-layer apply of a COMBINED op keeps its near field exact.
+ *         COMBINED requires leaves of at most 64 panels (EINVAL otherwise).
  * The ACA runs over ALL L frequencies on the device with pinned arithmetic
  * (bit-reproducible pivots) and keeps Z columns for local_l only.
  * Synchronous on return.  EINVAL: L < 1, s NULL, local index out of range or

@@ -740,6 +740,10 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
     if (rs != BEM_OK) return fail(rs);
   }
   if (mode == BEM_MODE_COMBINED) {
+    if (t.max_leaf > 64) {  // K1m stages 3 slice buffers of 32 x max_leaf complex per CTA
+      set_error("bem_assemble_h2_aca: BEM_MODE_COMBINED needs leaves of at most 64 panels (largest: %d)", t.max_leaf);
+      return fail(BEM_EINVAL);
+    }
     bem_status rs = run_aca(op, st, true);
     if (rs != BEM_OK) return fail(rs);
     // K1m launch order: row leaves by descending near-field MACA work (LPT)

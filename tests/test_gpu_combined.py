@@ -142,3 +142,27 @@ def test_combined_config2_full_size(pb, torch):
     off = np.r_[0, np.cumsum(gn["ranks"])]
     assert np.array_equal(gn["ranks"][blk], on["ranks"])
     assert np.array_equal(np.concatenate([gn["pivots"][off[b]:off[b + 1]] for b in blk]), on["pivots"])
+
+
+def test_combined_edge_cases(pb, torch):
+    """Leaves above 64 panels are refused (EINVAL); a tree whose partition has no
+    far blocks (80 panels, one level) runs the near-only paths of the combined
+    apply and of the time-domain convolution."""
+    V, T = synth.icosphere(2)
+    s = pb.cqm_frequencies(8, 2.0)
+    with pytest.raises(pb.BemError):
+        pb.Operator(pb.Tree(V, T, 10 ** 6, 1.0, 2), s, 1e-6, mode=pb.BEM_MODE_COMBINED)
+    V, T = synth.icosphere(1)
+    N = 8
+    M, L, R = len(T), N + 1, O.default_R(N)
+    tree = pb.Tree(V, T, 48, 1.0, 2)
+    op = pb.Operator(tree, s, 1e-8, mode=pb.BEM_MODE_COMBINED)
+    oh = O.H2(V, T, 48, 1.0, 2)
+    oh.aca(s, 1e-8)
+    oh.aca_near(s, 1e-8)
+    x = synth.random_density(2, L, M)
+    assert _rel(_apply(torch, op, x), oh.apply(O.MODE_COMBINED, s, x)) <= 1e-10
+    op.mot_prepare(R)
+    oh.time_weights(R)
+    q = np.random.default_rng(5).standard_normal((L, M)) + 0j
+    assert _rel(op.conv_time(torch.from_numpy(q).cuda()).cpu().numpy(), oh.conv(q)) <= 1e-10

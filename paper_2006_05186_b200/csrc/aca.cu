@@ -706,6 +706,8 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   if (const char* e = getenv("BEM_FAR8_KC")) op.far8_kc = atoi(e);
   if (const char* e = getenv("BEM_H2O_FC")) op.h2o_fc = atoi(e);
   if (const char* e = getenv("BEM_SOLVE_MASK")) op.use_solve_mask = atoi(e) != 0;
+  if (const char* e = getenv("BEM_OVERLAP")) op.overlap = atoi(e) != 0;
+  if (const char* e = getenv("BEM_FAR_SMEM_MIN_KB")) op.far_smem_min = (size_t)atoi(e) * 1024;
   auto fail = [&](bem_status stt) { delete h; return stt; };
   std::vector<double> sh(2 * (size_t)L);
   for (int l = 0; l < L; ++l) { sh[2 * l] = s[l].re; sh[2 * l + 1] = s[l].im; }
@@ -923,6 +925,9 @@ extern "C" bem_status bem_op_destroy(bem_op oh) {
   oh->o.tree->refcount--;
   for (auto& e : oh->o.ev)
     if (e) cudaEventDestroy(e);
+  if (oh->o.side) cudaStreamDestroy(oh->o.side);
+  if (oh->o.ev_fork) cudaEventDestroy(oh->o.ev_fork);
+  if (oh->o.ev_join) cudaEventDestroy(oh->o.ev_join);
   delete oh;
   return BEM_OK;
 }

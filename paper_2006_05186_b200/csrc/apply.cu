@@ -176,14 +176,31 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
   const int64_t tot = M * nl;
   gather_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(x, xc, t.d_perm.p, M, nl);
   BEM_CK(cudaGetLastError());
-  // K1
+  const bool dense = op.mode == BEM_MODE_DENSE;
+  const bool has_far = !dense && !t.far_r.empty();
+  // K1 (near field) and the far branch (K2 up, K3, K2 down transfers) are independent until
+  // the leaf-level scatter: unless per-kernel timers are on, K1 runs on a side stream forked
+  // from st (event fork/join, graph-capturable) so both kernels share the SMs' FP64 pipes
+  const bool overlap = op.overlap && has_far && !prof;
+  cudaStream_t sk1 = st;
+  if (overlap) {
+    if (!op.side) {
+      int lo = 0, hi = 0;
+      BEM_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      BEM_CK(cudaStreamCreateWithPriority(&op.side, cudaStreamNonBlocking, lo));  // K1: lowest priority
+      BEM_CK(cudaEventCreateWithFlags(&op.ev_fork, cudaEventDisableTiming));
+      BEM_CK(cudaEventCreateWithFlags(&op.ev_join, cudaEventDisableTiming));
+    }
+    BEM_CK(cudaEventRecord(op.ev_fork, st));
+    BEM_CK(cudaStreamWaitEvent(op.side, op.ev_fork, 0));
+    sk1 = op.side;
+  }
   {
-    bem_status rs = launch_near(op, xc, yc, st, dl);
+    bem_status rs = launch_near(op, xc, yc, sk1, dl);
     if (rs != BEM_OK) return rs;
   }
-  const bool dense = op.mode == BEM_MODE_DENSE;
+  if (overlap) BEM_CK(cudaEventRecord(op.ev_join, sk1));
   if (prof) BEM_CK(cudaEventRecord(op.ev[1], st));
-  const bool has_far = !dense && !t.far_r.empty();
   const unsigned tt = (unsigned)((nl + kPassT - 1) / kPassT);
   if (has_far) {
     up_leaf_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, 0, st>>>(t.d_leaves.p, t.d_begin.p, t.d_end.p,
@@ -207,6 +224,7 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
                                                                            t.d_son1.p, t.d_ET.p, yhat, nl, p);
       BEM_CK(cudaGetLastError());
     }
+    if (overlap) BEM_CK(cudaStreamWaitEvent(st, op.ev_join, 0));
     down_leaf_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, 0, st>>>(
         t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_UT.p, yhat, yc, t.d_perm.p, y, M, nl, p, 1, xc, dl ? alpha : 0.0);
     BEM_CK(cudaGetLastError());

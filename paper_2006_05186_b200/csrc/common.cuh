@@ -184,6 +184,7 @@ struct Op {
   bool force_generic = false;
   int far_kernel = 0;                 // 0: auto (far8 for p > 32, far7 otherwise); 8, 7, 6 (DMMA variants)
   size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM
+  size_t far_smem_min = 0;            // minimum dynamic smem of far7/far8 (residency experiments)
   bool far7_rem_dfma = true;          // p = 27: rows 24..26 on DFMA instead of a padded DMMA tile
   bool far7_cluster = false;          // DSMEM-shared slices across frequency tiles (measured slower, r01)
   int far8_kc = 0;                    // far8 nu-chunk width (0: automatic)
@@ -193,6 +194,10 @@ struct Op {
   const int32_t* d_mask = nullptr;
   bool use_solve_mask = true;  // env BEM_SOLVE_MASK=0 disables
   StepGraph step;  // bem_time_step
+  // K1 || far-branch overlap (apply.cu): side stream and fork/join events, created lazily
+  bool overlap = true;  // env BEM_OVERLAP=0 disables
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // profiling
   bool profile = false;
   cudaEvent_t ev[6] = {};

@@ -1162,7 +1162,8 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
     return BEM_OK;
   }
   if (aca && fk == 8 && !op.force_generic && op.n_segs > 0) {
-    const Far8Cfg f8 = choose8(p, nl, op.far4_smem_cap, op.far8_kc);
+    Far8Cfg f8 = choose8(p, nl, op.far4_smem_cap, op.far8_kc);
+    f8.smem = std::max(f8.smem, op.far_smem_min);  // residency experiment (env BEM_FAR_SMEM_MIN_KB)
     if (f8.mt > 0) {
       BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
       Far8Args a;
@@ -1180,7 +1181,8 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
     }
   }
   if (aca && fk == 7 && !op.force_generic && op.n_segs > 0) {
-    const Far7Cfg f7 = choose7(p, nl, op.far4_smem_cap, op.far7_cluster);
+    Far7Cfg f7 = choose7(p, nl, op.far4_smem_cap, op.far7_cluster);
+    f7.smem = std::max(f7.smem, op.far_smem_min);  // residency experiment (env BEM_FAR_SMEM_MIN_KB)
     if (f7.mt > 0) {
       BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
       Far7Args a;

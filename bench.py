@@ -117,6 +117,15 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def hbm_peak_gbs():
+    """Measured copy bandwidth (MEASURED_PEAKS.json, driver-written), else the guide's fallback."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6550.0
+
+
 def traffic_bytes(cfg_id, dom):
     """DRAM bytes per launch of the dominant kernel from the committed ncu capture, if any."""
     try:
@@ -436,12 +445,42 @@ def main():
             "algorithmic_flops_per_launch": fl,
             "traffic_source": "profiles/traffic.json (ncu --set full dram__bytes_read.sum + dram__bytes_write.sum "
                               "per launch of the same kernel and config)"}
+    # every kernel against its own roofline, and the whole apply
+    # T_roof = sum_k max(F_k / P_FP64, B_k / BW) against the measured apply time
+    hbm = hbm_peak_gbs()
+    p_, C_ = stats["p"], stats["clusters"]
+    b_up = 16.0 * M * nl + 16.0 * p_ * nl * C_
+    b_down = 16.0 * p_ * nl * C_ + 32.0 * M * nl
+    f_up = 8.0 * p_ * M * nl + 8.0 * p_ * p_ * nl * (C_ - 1)
+    pk_near = (peaks["dmma"] or FP64_PEAK_DERIVED / 1e12) if mode == pb.BEM_MODE_COMBINED else FP64_PEAK_DERIVED / 1e12
+    pk_far = (peaks["dmma"] or FP64_PEAK_DERIVED / 1e12) if aca_far else FP64_PEAK_DERIVED / 1e12
+    kern = {
+        "near": {"flops": flops_near, "ms": kt["near"], "peak_tflops": pk_near},
+        "coupling": {"flops": flops_far, "ms": kt["coupling"], "peak_tflops": pk_far},
+        "up": {"flops": f_up, "bytes": b_up, "ms": kt["up"], "peak_tflops": FP64_PEAK_DERIVED / 1e12,
+               "peak_gbs": hbm},
+        "down": {"flops": f_up, "bytes": b_down, "ms": kt["down"], "peak_tflops": FP64_PEAK_DERIVED / 1e12,
+                 "peak_gbs": hbm},
+    }
+    t_roof = 0.0
+    for k_, v_ in kern.items():
+        t_f = v_["flops"] / (v_["peak_tflops"] * 1e12)
+        t_b = v_.get("bytes", 0.0) / (v_.get("peak_gbs", hbm) * 1e9)
+        v_["roof_ms"] = max(t_f, t_b) * 1e3
+        v_["bound"] = "hbm" if t_b > t_f else ("tensor" if v_["peak_tflops"] != FP64_PEAK_DERIVED / 1e12 else "alu")
+        v_["frac"] = v_["roof_ms"] / v_["ms"] if v_["ms"] > 0 else None
+        t_roof += v_["roof_ms"]
+    t_apply = sum(kt.values())
+    per_kernel = {"kernels": kern, "apply_roof_ms": t_roof, "apply_ms": t_apply,
+                  "apply_frac": t_roof / t_apply if t_apply > 0 else None,
+                  "model": "SURVEY §8(d): F, B per kernel (75 flops per K1 evaluation; K2 general-E flops and "
+                           "minimum bytes), P = measured DMMA / derived FP64 ALU peak, BW = MEASURED_PEAKS.json hbm_gbs"}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": config_json(args.config, cfg, M, L, world), "roofline": roof, "e2e": e2e,
            "gpu_launches": launches * args.steps, "clocks": clocks,
-           "kernel_ms": kt, "fp64_measured_tflops": peaks,
+           "kernel_ms": kt, "fp64_measured_tflops": peaks, "per_kernel_roofline": per_kernel,
            "timing": ("CUDA-graph replay of the whole step (captured once after warm-up); eager step "
                       f"{statistics.median(ms_eager):.3f} ms (median)") if graph is not None else
                      f"eager launches{'' if graph_error is None else ' (graph capture failed: ' + graph_error + ')'}",

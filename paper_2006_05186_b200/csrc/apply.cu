@@ -140,6 +140,163 @@ __global__ void __launch_bounds__(kPassThreads) down_leaf_kernel(const int32_t* 
   }
 }
 
+// Shared-memory staged variants (used when the tiles fit): the basis / transfer
+// matrix and the coefficient tile are loaded once with coalesced loads, then every
+// thread's dot product runs from shared memory (the unstaged kernels above chain
+// ~2p dependent global loads per output; r01: K2 at 6 % of its roofline).
+__global__ void __launch_bounds__(kPassThreads) up_leaf_s_kernel(const int32_t* __restrict__ leaves,
+                                                                 const int32_t* __restrict__ cb,
+                                                                 const int32_t* __restrict__ ce,
+                                                                 const double* __restrict__ W,
+                                                                 const double2* __restrict__ xc,
+                                                                 double2* __restrict__ xhat, int64_t M, int nl, int p) {
+  extern __shared__ double2 smx[];
+  const int c = leaves[blockIdx.x];
+  const int b = cb[c], n = ce[c] - b;
+  const int t0 = blockIdx.y * kPassT;
+  double2* xs = smx;                      // kPassT x n
+  double* Ws = (double*)(smx + kPassT * n);  // n x p
+  for (int idx = threadIdx.x; idx < n * p; idx += blockDim.x) Ws[idx] = W[(int64_t)b * p + idx];
+  for (int idx = threadIdx.x; idx < kPassT * n; idx += blockDim.x) {
+    const int tl = idx / n, k = idx - tl * n;
+    xs[idx] = t0 + tl < nl ? xc[(int64_t)(t0 + tl) * M + b + k] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < kPassT * p; idx += blockDim.x) {
+    const int tl = idx / p, nu = idx - tl * p;
+    if (t0 + tl >= nl) break;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < n; ++k) {
+      const double w = Ws[k * p + nu];
+      const double2 v = xs[tl * n + k];
+      acc.x = fma(w, v.x, acc.x);
+      acc.y = fma(w, v.y, acc.y);
+    }
+    xhat[((int64_t)c * nl + t0 + tl) * p + nu] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(kPassThreads) up_transfer_s_kernel(const int32_t* __restrict__ list,
+                                                                     const int32_t* __restrict__ son0,
+                                                                     const int32_t* __restrict__ son1,
+                                                                     const double* __restrict__ E,
+                                                                     double2* __restrict__ xhat, int nl, int p) {
+  extern __shared__ double2 smx[];
+  const int c = list[blockIdx.x];
+  const int sons[2] = {son0[c], son1[c]};
+  const int t0 = blockIdx.y * kPassT;
+  double2* xs = smx;                           // 2 x kPassT x p
+  double* Es = (double*)(smx + 2 * kPassT * p);  // 2 x p x p
+  for (int idx = threadIdx.x; idx < 2 * p * p; idx += blockDim.x) {
+    const int sidx = idx / (p * p), e = idx - sidx * p * p;
+    Es[idx] = E[(int64_t)sons[sidx] * p * p + e];
+  }
+  for (int idx = threadIdx.x; idx < 2 * kPassT * p; idx += blockDim.x) {
+    const int sidx = idx / (kPassT * p), e = idx - sidx * kPassT * p;
+    const int tl = e / p;
+    xs[idx] = t0 + tl < nl ? xhat[((int64_t)sons[sidx] * nl + t0) * p + e] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < kPassT * p; idx += blockDim.x) {
+    const int tl = idx / p, mu = idx - tl * p;
+    if (t0 + tl >= nl) break;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int sidx = 0; sidx < 2; ++sidx) {
+      const double* Em = Es + sidx * p * p + mu;
+      const double2* x = xs + (sidx * kPassT + tl) * p;
+      for (int lam = 0; lam < p; ++lam) {
+        const double w = Em[lam * p];
+        acc.x = fma(w, x[lam].x, acc.x);
+        acc.y = fma(w, x[lam].y, acc.y);
+      }
+    }
+    xhat[((int64_t)c * nl + t0 + tl) * p + mu] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(kPassThreads) down_transfer_s_kernel(const int32_t* __restrict__ list,
+                                                                       const int32_t* __restrict__ son0,
+                                                                       const int32_t* __restrict__ son1,
+                                                                       const double* __restrict__ ET,
+                                                                       double2* __restrict__ yhat, int nl, int p) {
+  extern __shared__ double2 smx[];
+  const int c = list[blockIdx.x];
+  const int sons[2] = {son0[c], son1[c]};
+  const int t0 = blockIdx.y * kPassT;
+  double2* ys = smx;                      // kPassT x p (parent)
+  double* Es = (double*)(smx + kPassT * p);  // 2 x p x p, E^T[son][mu][lam]
+  for (int idx = threadIdx.x; idx < 2 * p * p; idx += blockDim.x) {
+    const int sidx = idx / (p * p), e = idx - sidx * p * p;
+    Es[idx] = ET[(int64_t)sons[sidx] * p * p + e];
+  }
+  for (int idx = threadIdx.x; idx < kPassT * p; idx += blockDim.x) {
+    const int tl = idx / p;
+    ys[idx] = t0 + tl < nl ? yhat[((int64_t)c * nl + t0) * p + idx] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < 2 * kPassT * p; idx += blockDim.x) {
+    const int sidx = idx / (kPassT * p), e = idx - sidx * kPassT * p;
+    const int tl = e / p, lam = e - tl * p;
+    if (t0 + tl >= nl) continue;
+    const int sc = sons[sidx];
+    const double* Em = Es + sidx * p * p + lam;
+    const double2* yp = ys + tl * p;
+    double2 acc = yhat[((int64_t)sc * nl + t0 + tl) * p + lam];
+    for (int mu = 0; mu < p; ++mu) {
+      const double w = Em[mu * p];
+      acc.x = fma(w, yp[mu].x, acc.x);
+      acc.y = fma(w, yp[mu].y, acc.y);
+    }
+    yhat[((int64_t)sc * nl + t0 + tl) * p + lam] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(kPassThreads) down_leaf_s_kernel(const int32_t* __restrict__ leaves,
+                                                                   const int32_t* __restrict__ cb,
+                                                                   const int32_t* __restrict__ ce,
+                                                                   const double* __restrict__ UT,
+                                                                   const double2* __restrict__ yhat,
+                                                                   const double2* __restrict__ yc,
+                                                                   const int32_t* __restrict__ perm,
+                                                                   double2* __restrict__ y, int64_t M, int nl, int p,
+                                                                   const double2* __restrict__ xc, double alpha) {
+  extern __shared__ double2 smx[];
+  const int c = leaves[blockIdx.x];
+  const int b = cb[c], n = ce[c] - b;
+  const int t0 = blockIdx.y * kPassT;
+  double2* ys = smx;                      // kPassT x p
+  double* Us = (double*)(smx + kPassT * p);  // p x n (U^T rows of the leaf's panels)
+  for (int idx = threadIdx.x; idx < p * n; idx += blockDim.x) {
+    const int mu = idx / n, k = idx - mu * n;
+    Us[idx] = UT[(int64_t)mu * M + b + k];
+  }
+  for (int idx = threadIdx.x; idx < kPassT * p; idx += blockDim.x) {
+    const int tl = idx / p;
+    ys[idx] = t0 + tl < nl ? yhat[((int64_t)c * nl + t0) * p + idx] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < kPassT * n; idx += blockDim.x) {
+    const int tl = idx / n, k = idx - tl * n;
+    const int t = t0 + tl;
+    if (t >= nl) break;
+    double2 acc = yc[(int64_t)t * M + b + k];
+    const double2* yh = ys + tl * p;
+    for (int mu = 0; mu < p; ++mu) {
+      const double u = Us[mu * n + k];
+      acc.x = fma(u, yh[mu].x, acc.x);
+      acc.y = fma(u, yh[mu].y, acc.y);
+    }
+    if (alpha != 0.0) {
+      const double2 xv = xc[(int64_t)t * M + b + k];
+      acc.x = fma(alpha, xv.x, acc.x);
+      acc.y = fma(alpha, xv.y, acc.y);
+    }
+    y[(int64_t)t * M + perm[b + k]] = acc;
+  }
+}
+
+constexpr size_t kPassSmemMax = 100 * 1024;
+
 __global__ void scatter_kernel(const double2* __restrict__ yc, double2* __restrict__ y,
                                const int32_t* __restrict__ perm, int64_t M, int nl, const double2* __restrict__ xc, double alpha) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -153,6 +310,71 @@ __global__ void scatter_kernel(const double2* __restrict__ yc, double2* __restri
   y[t * M + perm[k]] = v;
 }
 
+// K2 up / down passes over nl columns, staged kernels when their tiles fit
+bem_status run_up(Tree& t, const double* W, const double2* xc, double2* xhat, int nl, cudaStream_t st) {
+  const int p = t.p;
+  const unsigned tt = (unsigned)((nl + kPassT - 1) / kPassT);
+  const size_t sm_leaf = sizeof(double2) * kPassT * t.max_leaf + sizeof(double) * (size_t)t.max_leaf * p;
+  if (sm_leaf <= kPassSmemMax) {
+    BEM_CK(cudaFuncSetAttribute(up_leaf_s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_leaf));
+    up_leaf_s_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, sm_leaf, st>>>(t.d_leaves.p, t.d_begin.p,
+                                                                                   t.d_end.p, W, xc, xhat, t.M, nl, p);
+  } else {
+    up_leaf_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, 0, st>>>(t.d_leaves.p, t.d_begin.p, t.d_end.p, W,
+                                                                             xc, xhat, t.M, nl, p);
+  }
+  BEM_CK(cudaGetLastError());
+  const size_t sm_tr = sizeof(double2) * 2 * kPassT * p + sizeof(double) * 2 * (size_t)p * p;
+  const bool staged = sm_tr <= kPassSmemMax;
+  if (staged)
+    BEM_CK(cudaFuncSetAttribute(up_transfer_s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_tr));
+  for (int lv = t.depth - 1; lv >= 0; --lv) {
+    const int n = (int)t.level_nonleaf[lv].size();
+    if (n == 0) continue;
+    if (staged)
+      up_transfer_s_kernel<<<dim3((unsigned)n, tt), kPassThreads, sm_tr, st>>>(t.d_level_nonleaf[lv].p, t.d_son0.p,
+                                                                               t.d_son1.p, t.d_E.p, xhat, nl, p);
+    else
+      up_transfer_kernel<<<dim3((unsigned)n, tt), kPassThreads, 0, st>>>(t.d_level_nonleaf[lv].p, t.d_son0.p,
+                                                                         t.d_son1.p, t.d_E.p, xhat, nl, p);
+    BEM_CK(cudaGetLastError());
+  }
+  return BEM_OK;
+}
+
+bem_status run_down(Tree& t, double2* yhat, const double2* yc, double2* y, int nl, const double2* xc, double alpha,
+                    cudaStream_t st, cudaEvent_t wait_before_leaf = nullptr) {
+  const int p = t.p;
+  const unsigned tt = (unsigned)((nl + kPassT - 1) / kPassT);
+  const size_t sm_tr = sizeof(double2) * kPassT * p + sizeof(double) * 2 * (size_t)p * p;
+  const bool staged = sm_tr <= kPassSmemMax;
+  if (staged)
+    BEM_CK(cudaFuncSetAttribute(down_transfer_s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_tr));
+  for (int lv = 0; lv < t.depth; ++lv) {
+    const int n = (int)t.level_nonleaf[lv].size();
+    if (n == 0) continue;
+    if (staged)
+      down_transfer_s_kernel<<<dim3((unsigned)n, tt), kPassThreads, sm_tr, st>>>(t.d_level_nonleaf[lv].p, t.d_son0.p,
+                                                                                 t.d_son1.p, t.d_ET.p, yhat, nl, p);
+    else
+      down_transfer_kernel<<<dim3((unsigned)n, tt), kPassThreads, 0, st>>>(t.d_level_nonleaf[lv].p, t.d_son0.p,
+                                                                           t.d_son1.p, t.d_ET.p, yhat, nl, p);
+    BEM_CK(cudaGetLastError());
+  }
+  if (wait_before_leaf) BEM_CK(cudaStreamWaitEvent(st, wait_before_leaf, 0));
+  const size_t sm_leaf = sizeof(double2) * kPassT * p + sizeof(double) * (size_t)p * t.max_leaf;
+  if (sm_leaf <= kPassSmemMax) {
+    BEM_CK(cudaFuncSetAttribute(down_leaf_s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_leaf));
+    down_leaf_s_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, sm_leaf, st>>>(
+        t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_UT.p, yhat, yc, t.d_perm.p, y, t.M, nl, p, xc, alpha);
+  } else {
+    down_leaf_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, 0, st>>>(
+        t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_UT.p, yhat, yc, t.d_perm.p, y, t.M, nl, p, 1, xc, alpha);
+  }
+  BEM_CK(cudaGetLastError());
+  return BEM_OK;
+}
+
 }  // namespace
 
 // y = V x (dl = false) or y = (alpha I + K) x (dl = true, double layer, NEXT-1): the
@@ -160,7 +382,7 @@ __global__ void scatter_kernel(const double2* __restrict__ yc, double2* __restri
 bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st, bool dl, double alpha) {
   Tree& t = *op.tree;
   const int64_t M = t.M;
-  const int nl = op.n_local, p = t.p;
+  const int nl = op.n_local;
   const double2* x = (const double2*)xin;
   double2* y = (double2*)yout;
   double2* xc = (double2*)op.d_xc.p;
@@ -201,33 +423,20 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
   }
   if (overlap) BEM_CK(cudaEventRecord(op.ev_join, sk1));
   if (prof) BEM_CK(cudaEventRecord(op.ev[1], st));
-  const unsigned tt = (unsigned)((nl + kPassT - 1) / kPassT);
   if (has_far) {
-    up_leaf_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, 0, st>>>(t.d_leaves.p, t.d_begin.p, t.d_end.p,
-                                                                             dl ? t.d_WK.p : t.d_W.p, xc, xhat, M, nl, p);
-    BEM_CK(cudaGetLastError());
-    for (int lv = t.depth - 1; lv >= 0; --lv) {
-      const int n = (int)t.level_nonleaf[lv].size();
-      if (n == 0) continue;
-      up_transfer_kernel<<<dim3((unsigned)n, tt), kPassThreads, 0, st>>>(t.d_level_nonleaf[lv].p, t.d_son0.p,
-                                                                         t.d_son1.p, t.d_E.p, xhat, nl, p);
-      BEM_CK(cudaGetLastError());
+    {
+      bem_status rs = run_up(t, dl ? t.d_WK.p : t.d_W.p, xc, xhat, nl, st);
+      if (rs != BEM_OK) return rs;
     }
     if (prof) BEM_CK(cudaEventRecord(op.ev[2], st));
     bem_status rs = launch_far(op, xhat, yhat, st);
     if (rs != BEM_OK) return rs;
     if (prof) BEM_CK(cudaEventRecord(op.ev[3], st));
-    for (int lv = 0; lv < t.depth; ++lv) {
-      const int n = (int)t.level_nonleaf[lv].size();
-      if (n == 0) continue;
-      down_transfer_kernel<<<dim3((unsigned)n, tt), kPassThreads, 0, st>>>(t.d_level_nonleaf[lv].p, t.d_son0.p,
-                                                                           t.d_son1.p, t.d_ET.p, yhat, nl, p);
-      BEM_CK(cudaGetLastError());
+    {
+      // the down transfers do not read yc: only the leaf scatter waits for K1
+      bem_status rs = run_down(t, yhat, yc, y, nl, xc, dl ? alpha : 0.0, st, overlap ? op.ev_join : nullptr);
+      if (rs != BEM_OK) return rs;
     }
-    if (overlap) BEM_CK(cudaStreamWaitEvent(st, op.ev_join, 0));
-    down_leaf_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, 0, st>>>(
-        t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_UT.p, yhat, yc, t.d_perm.p, y, M, nl, p, 1, xc, dl ? alpha : 0.0);
-    BEM_CK(cudaGetLastError());
   } else {
     if (prof) { BEM_CK(cudaEventRecord(op.ev[2], st)); BEM_CK(cudaEventRecord(op.ev[3], st)); }
     scatter_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(yc, y, t.d_perm.p, M, nl, xc, dl ? alpha : 0.0);
@@ -246,42 +455,19 @@ bem_status h2_gather(Op& op, const double2* x, double2* xc, int ncols, cudaStrea
 }
 
 bem_status h2_up(Op& op, const double2* xc, double2* xhat, int ncols, cudaStream_t st) {
-  Tree& t = *op.tree;
-  const unsigned tt = (unsigned)((ncols + kPassT - 1) / kPassT);
-  up_leaf_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, 0, st>>>(t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_W.p,
-                                                                           xc, xhat, t.M, ncols, t.p);
-  BEM_CK(cudaGetLastError());
-  for (int lv = t.depth - 1; lv >= 0; --lv) {
-    const int n = (int)t.level_nonleaf[lv].size();
-    if (n == 0) continue;
-    up_transfer_kernel<<<dim3((unsigned)n, tt), kPassThreads, 0, st>>>(t.d_level_nonleaf[lv].p, t.d_son0.p,
-                                                                       t.d_son1.p, t.d_E.p, xhat, ncols, t.p);
-    BEM_CK(cudaGetLastError());
-  }
-  return BEM_OK;
+  return run_up(*op.tree, op.tree->d_W.p, xc, xhat, ncols, st);
 }
 
 // y (input order) = ycn + U-side of the downward pass of yhat
 bem_status h2_down_scatter(Op& op, double2* yhat, const double2* ycn, double2* y, int ncols, cudaStream_t st) {
   Tree& t = *op.tree;
-  const unsigned tt = (unsigned)((ncols + kPassT - 1) / kPassT);
   if (t.far_r.empty()) {
     const int64_t tot = t.M * ncols;
     scatter_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(ycn, y, t.d_perm.p, t.M, ncols, ycn, 0.0);
     BEM_CK(cudaGetLastError());
     return BEM_OK;
   }
-  for (int lv = 0; lv < t.depth; ++lv) {
-    const int n = (int)t.level_nonleaf[lv].size();
-    if (n == 0) continue;
-    down_transfer_kernel<<<dim3((unsigned)n, tt), kPassThreads, 0, st>>>(t.d_level_nonleaf[lv].p, t.d_son0.p,
-                                                                         t.d_son1.p, t.d_ET.p, yhat, ncols, t.p);
-    BEM_CK(cudaGetLastError());
-  }
-  down_leaf_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, 0, st>>>(
-      t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_UT.p, yhat, ycn, t.d_perm.p, y, t.M, ncols, t.p, 1, ycn, 0.0);
-  BEM_CK(cudaGetLastError());
-  return BEM_OK;
+  return run_down(t, yhat, ycn, y, ncols, ycn, 0.0, st);
 }
 
 }  // namespace bem

@@ -91,3 +91,15 @@ def test_tree_cfg4_stats_match_probe():
     lt = pb.Tree(V, T, 64, 1.0, 4, device=-1)
     s = lt.stats
     assert (s["clusters"], s["leaves"], s["near_blocks"], s["far_blocks"]) == (3591, 1796, 63554, 98386)
+
+
+def test_null_handles_rejected_without_gpu():
+    """The newer entry points (combined mode, time-domain path, one-call step)
+    validate their handles before touching a device: NULL -> BEM_EINVAL."""
+    lib = pb.lib()
+    assert lib.bem_aca_export_near(None, None, None, None) == -1
+    assert lib.bem_mot_prepare(None, 0.5, None) == -1
+    assert lib.bem_conv_time(None, None, None, 0, None) == -1
+    assert lib.cqm_mot_solve(None, None, None, 1e-8, 10, 10, None, None) == -1
+    assert lib.bem_time_step(None, None, None, 0.5, None) == -1
+    assert b"NULL" in lib.bem_last_error()

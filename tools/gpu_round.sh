@@ -15,6 +15,8 @@ timeout 900 python bench.py --config 4 --steps 3 --warmup 3 --no-cpu-baseline > 
 for c in 2 3 4; do timeout 900 python bench.py --config $c --mode h2only --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/b${c}_h2o.log 2>&1; done
 timeout 1800 python bench.py --config 5 --shard-of 8 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/b5_shard8.log 2>&1
 timeout 1500 python tools/bench_solve.py --config 3 > gpurun_out/solve_c3.log 2>&1
+timeout 600 python bench.py --config 2 --mode combined --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b2_comb.log 2>&1
+timeout 600 python tools/bench_mot.py --config 2 --N 16 > gpurun_out/mot_c2_n16.log 2>&1
 timeout 300 python tools/prof_apply.py --config 2 --reps 2 --time-step > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python tools/prof_apply.py --config 2 --reps 2 --time-step > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"near|far7" -s 2 -c 2 -o gpurun_out/prof_c2 python tools/prof_apply.py --config 2 --reps 2 > gpurun_out/ncu_full.log 2>&1

@@ -291,8 +291,11 @@ __device__ __forceinline__ double2 kern_rs(double d2, double2 s, const double* e
 
 // NJ DMMA mu tiles per 32-row chunk; REM further rows (p = 27: rows 24..26) on
 // DFMA from the same A fragments instead of a 5/8-empty fourth DMMA tile.
-template <int MT, bool CL, int NJ, int REM>
-__global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
+// NW: warps per CTA (8: two CTAs per SM; 16: one CTA per SM whose 16 warps share every
+// regenerated slice); M3: 3M complex products (three real DMMAs per complex one,
+// Re = P1 - P2, Im = P3 - P1 - P2 with P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi)).
+template <int MT, bool CL, int NJ, int REM, int NW = 8, bool M3 = false>
+__global__ void __launch_bounds__(NW * 32, 16 / NW) far7_kernel(Far7Args a) {
   extern __shared__ double2 sm[];
   const int p = a.p, m = a.m, SST = a.SST, XTP = a.XTP, p4 = a.p4, tb = a.tb;
   const int4 sg = a.segs[blockIdx.x];
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
   bool cta_on = false;
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
-    const int tt = warp + 8 * i;
+    const int tt = warp + NW * i;
     const int t = tc0 + tt * 8 + g;
     const bool v = tt < ntile && t < a.nl && (a.mask == nullptr || a.mask[t]);
     ton[i] = __any_sync(0xffffffffu, v);
@@ -338,12 +341,14 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
     cta_on = __syncthreads_or(lo) != 0;
     if (CL) cta_on = true;  // every CTA of a cluster must reach the same cluster barriers
   }
-  double acc[MT][NJ][2][2];
+  double acc[MT][NJ][M3 ? 3 : 2][2];
   double2 racc[MT][REM > 0 ? REM : 1];
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int u = 0; u < (M3 ? 3 : 2); ++u) acc[i][j][u][0] = acc[i][j][u][1] = 0.0;
 #pragma unroll
     for (int j = 0; j < (REM > 0 ? REM : 1); ++j) racc[i][j] = make_double2(0.0, 0.0);
   }
@@ -377,7 +382,7 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
       double2 zt[MT];
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
-        const int tt = warp + 8 * i;
+        const int tt = warp + NW * i;
         const int t = tc0 + tt * 8 + g;
         zt[i] = (tt < ntile && t < a.nl) ? Zl[t] : make_double2(0.0, 0.0);
       }
@@ -416,22 +421,32 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
         for (int j = 0; j < REM; ++j) rf[j] = S[(NJ * 8 + j) * SST + k0 + q];
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
-          const int tt = warp + 8 * i;
+          const int tt = warp + NW * i;
           if (tt < ntile && ton[i]) {
             const double2 xv = xs[(k0 + q) * XTP + tb + tt * 8 + g];
             const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
             const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
             const double nai = -ai;
-            // two passes: dependent DMMAs on one accumulator are 2*NJ instructions apart
+            if constexpr (M3) {
+              const double as = ar + ai;
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) {
-              dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
-              dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
-            }
+              for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) {
-              dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
-              dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
+              for (int j = 0; j < NJ; ++j) dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].y);
+#pragma unroll
+              for (int j = 0; j < NJ; ++j) dmma(acc[i][j][M3 ? 2 : 0][0], acc[i][j][M3 ? 2 : 0][1], as, bf[j].x + bf[j].y);
+            } else {
+              // two passes: dependent DMMAs on one accumulator are 2*NJ instructions apart
+#pragma unroll
+              for (int j = 0; j < NJ; ++j) {
+                dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+                dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
+              }
+#pragma unroll
+              for (int j = 0; j < NJ; ++j) {
+                dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
+                dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
+              }
             }
 #pragma unroll
             for (int j = 0; j < REM; ++j) {  // partial over this lane's k = k0 + q; reduced over q at the end
@@ -463,7 +478,7 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
   double2* out = a.part + (int64_t)sg.w * a.nl * p;
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
-    const int tt = warp + 8 * i;
+    const int tt = warp + NW * i;
     if (tt >= ntile) continue;
     const int t = tc0 + tt * 8 + g;
     if (t >= a.nl) continue;
@@ -472,13 +487,19 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int row = j * 8 + 2 * q + v;
-        if (row < nrow) out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
+        if (row < nrow) {
+          if constexpr (M3)
+            out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v] - acc[i][j][1][v],
+                                                           acc[i][j][M3 ? 2 : 0][v] - acc[i][j][0][v] - acc[i][j][1][v]);
+          else
+            out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
+        }
       }
   }
   if (REM > 0) {
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
-      const int tt = warp + 8 * i;  // warp-uniform
+      const int tt = warp + NW * i;  // warp-uniform
       if (tt >= ntile) continue;
       const int t = tc0 + tt * 8 + g;
 #pragma unroll
@@ -513,7 +534,7 @@ struct Far7Cfg {
   size_t smem = 0;
 };
 
-Far7Cfg choose7(int p, int nl, size_t cap, bool cluster) {
+Far7Cfg choose7(int p, int nl, size_t cap, bool cluster, int ttmax_cap = 0, int nw = 8) {
   int tb = nl % 8;
   if (tb > 2 || tb == nl) tb = 0;  // pad instead (zero columns past nl)
   const int nD = (nl - tb + 7) / 8 * 8;
@@ -522,6 +543,7 @@ Far7Cfg choose7(int p, int nl, size_t cap, bool cluster) {
   while (SST % 8 != 4) ++SST;
   const int nrow = std::min(p, 32);
   for (int TTmax : {256, 128, 64, 32, 16, 8}) {
+    if (ttmax_cap > 0 && TTmax > ttmax_cap) continue;
     Far7Cfg c;
     const int ntiles = (nD + TTmax - 1) / TTmax;
     const int TT = ((nD / 8 + ntiles - 1) / ntiles) * 8;
@@ -533,7 +555,7 @@ Far7Cfg choose7(int p, int nl, size_t cap, bool cluster) {
                         sizeof(double) * (64 + 96 + 3 * p);
     if (smem > cap) continue;
     c.p4 = p4; c.SST = SST; c.TT = TT; c.XTP = XTP; c.nT = TT / 8; c.tb = tb; c.nd = nD; c.ntiles = ntiles;
-    c.nchunks = (p + 31) / 32; c.mt = (c.nT + 7) / 8; c.smem = smem; c.cs = cs; c.own = own;
+    c.nchunks = (p + 31) / 32; c.mt = (c.nT + nw - 1) / nw; c.smem = smem; c.cs = cs; c.own = own;
     if (c.mt > 2) continue;  // MT >= 3 spills at 128 registers
     return c;
   }
@@ -576,8 +598,25 @@ cudaError_t dispatch7_(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream
   }
 }
 
+// 16-warp CTAs (one per SM, one t-tile per warp): every regenerated slice serves 16 warps
+template <int NJ, int REM, bool M3>
+cudaError_t launch7w(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream_t st) {
+  if (c.mt != 1 || c.cs > 1) return cudaErrorInvalidConfiguration;
+  auto k = far7_kernel<1, false, NJ, REM, 16, M3>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  if (e != cudaSuccess) return e;
+  k<<<dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks), 512, c.smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 // mu tiling: p = 27 -> 3 DMMA tiles + 3 DFMA rows; p <= 8 -> 1 tile; otherwise 4 tiles per 32-row chunk
-cudaError_t dispatch7(const Far7Cfg& c, int p, bool rem_dfma, int nseg, const Far7Args& a, cudaStream_t st) {
+cudaError_t dispatch7(const Far7Cfg& c, int p, bool rem_dfma, int nseg, const Far7Args& a, cudaStream_t st,
+                      int nw = 8, bool m3 = false) {
+  if (nw == 16) {
+    if (p <= 8) return m3 ? launch7w<1, 0, true>(c, nseg, a, st) : launch7w<1, 0, false>(c, nseg, a, st);
+    if (p == 27 && rem_dfma) return m3 ? launch7w<3, 3, true>(c, nseg, a, st) : launch7w<3, 3, false>(c, nseg, a, st);
+    return m3 ? launch7w<4, 0, true>(c, nseg, a, st) : launch7w<4, 0, false>(c, nseg, a, st);
+  }
   if (p <= 8) return dispatch7_<1, 0>(c, nseg, a, st);
   if (p == 27 && rem_dfma) return dispatch7_<3, 3>(c, nseg, a, st);
   return dispatch7_<4, 0>(c, nseg, a, st);
@@ -608,8 +647,10 @@ struct Far8Args {
   const int32_t* mask;  // nullable: per local frequency, 0 = skip (output 0)
 };
 
-template <int MT, int NJ, int REM>
-__global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
+// M3: 3M complex products (as far7); NW warps per CTA (6: up to 170 registers at two CTAs
+// per SM, room for the 3M accumulators at MT = 2; leftover columns are then padded)
+template <int MT, int NJ, int REM, bool M3 = false, int NW = 8>
+__global__ void __launch_bounds__(NW * 32, 2) far8_kernel(Far8Args a) {
   extern __shared__ double2 sm[];
   const int p = a.p, m = a.m, SST = a.SST, XTP = a.XTP, tb = a.tb, KC = a.KC;
   const int4 sg = a.segs[blockIdx.x];
@@ -639,7 +680,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
   bool cta_on = false;
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
-    const int tt = warp + 8 * i;
+    const int tt = warp + NW * i;
     const int t = tc0 + tt * 8 + g;
     const bool v = tt < ntile && t < a.nl && (a.mask == nullptr || a.mask[t]);
     ton[i] = __any_sync(0xffffffffu, v);
@@ -650,12 +691,14 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
     if (lead) for (int t = tid; t < tb; t += blockDim.x) lo |= a.mask == nullptr || a.mask[t];
     cta_on = __syncthreads_or(lo) != 0;
   }
-  double acc[MT][NJ][2][2];
+  double acc[MT][NJ][M3 ? 3 : 2][2];
   double2 racc[MT][REM > 0 ? REM : 1];
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int u = 0; u < (M3 ? 3 : 2); ++u) acc[i][j][u][0] = acc[i][j][u][1] = 0.0;
 #pragma unroll
     for (int j = 0; j < (REM > 0 ? REM : 1); ++j) racc[i][j] = make_double2(0.0, 0.0);
   }
@@ -687,7 +730,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
         double2 zt[MT];
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
-          const int tt = warp + 8 * i;
+          const int tt = warp + NW * i;
           const int t = tc0 + tt * 8 + g;
           zt[i] = (tt < ntile && t < a.nl) ? Zl[t] : make_double2(0.0, 0.0);
         }
@@ -716,22 +759,33 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
           for (int j = 0; j < REM; ++j) rf[j] = S[(NJ * 8 + j) * SST + k0 + q];
 #pragma unroll
           for (int i = 0; i < MT; ++i) {
-            const int tt = warp + 8 * i;
+            const int tt = warp + NW * i;
             if (tt < ntile && ton[i]) {
               const double2 xv = xs[(k0 + q) * XTP + tb + tt * 8 + g];
               const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
               const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
               const double nai = -ai;
               // two passes: dependent DMMAs on one accumulator are 2*NJ instructions apart
+if constexpr (M3) {
+                const double as = ar + ai;
 #pragma unroll
-              for (int j = 0; j < NJ; ++j) {
-                dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
-                dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
-              }
+                for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
 #pragma unroll
-              for (int j = 0; j < NJ; ++j) {
-                dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
-                dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
+                for (int j = 0; j < NJ; ++j) dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].y);
+#pragma unroll
+                for (int j = 0; j < NJ; ++j)
+                  dmma(acc[i][j][M3 ? 2 : 0][0], acc[i][j][M3 ? 2 : 0][1], as, bf[j].x + bf[j].y);
+              } else {
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                  dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+                  dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
+                }
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                  dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
+                  dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
+                }
               }
 #pragma unroll
               for (int j = 0; j < REM; ++j) {
@@ -764,7 +818,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
   double2* out = a.part + (int64_t)sg.w * a.nl * p;
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
-    const int tt = warp + 8 * i;
+    const int tt = warp + NW * i;
     if (tt >= ntile) continue;
     const int t = tc0 + tt * 8 + g;
     if (t >= a.nl) continue;
@@ -773,13 +827,19 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int row = j * 8 + 2 * q + v;
-        if (row < nrow) out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
+        if (row < nrow) {
+          if constexpr (M3)
+            out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v] - acc[i][j][1][v],
+                                                           acc[i][j][M3 ? 2 : 0][v] - acc[i][j][0][v] - acc[i][j][1][v]);
+          else
+            out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
+        }
       }
   }
   if (REM > 0) {
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
-      const int tt = warp + 8 * i;
+      const int tt = warp + NW * i;
       if (tt >= ntile) continue;
       const int t = tc0 + tt * 8 + g;
 #pragma unroll
@@ -815,9 +875,9 @@ struct Far8Cfg {
 
 // KC: nu chunk width (kc_req > 0 forces it; otherwise the whole p if a
 // 128-column frequency tile fits, else 32); TT up to 128 (MT <= 2).
-Far8Cfg choose8(int p, int nl, size_t cap, int kc_req) {
+Far8Cfg choose8(int p, int nl, size_t cap, int kc_req, int ttmax_cap = 0, int nw = 8) {
   int tb = nl % 8;
-  if (tb > 2 || tb == nl) tb = 0;
+  if (tb > 2 || tb == nl || nw != 8) tb = 0;
   const int nD = (nl - tb + 7) / 8 * 8;
   const int p4 = (p + 3) / 4 * 4;
   auto make = [&](int KC, int TTmax) {
@@ -832,30 +892,37 @@ Far8Cfg choose8(int p, int nl, size_t cap, int kc_req) {
         sizeof(double2) * (2 * 32 * (size_t)SST + (size_t)KC * XTP + 64) + sizeof(double) * (64 + 96 + 3 * p);
     if (smem > cap) return c;
     c.SST = SST; c.TT = TT; c.XTP = XTP; c.tb = tb; c.nd = nD; c.ntiles = ntiles;
-    c.nchunks = (p + 31) / 32; c.mt = (TT / 8 + 7) / 8; c.smem = smem; c.KC = KC;
+    c.nchunks = (p + 31) / 32; c.mt = (TT / 8 + nw - 1) / nw; c.smem = smem; c.KC = KC;
     return c;
   };
   std::vector<int> kcs;
   if (kc_req > 0) kcs = {std::min(p4, (kc_req + 3) / 4 * 4)};
   else kcs = {p4, std::min(p4, 32)};
-  for (int TTmax : {128, 64, 32, 16, 8})
+  for (int TTmax : {128, 96, 64, 48, 32, 16, 8})
     for (int KC : kcs) {
+      if (ttmax_cap > 0 && TTmax > ttmax_cap) continue;
+      if ((TTmax == 96 || TTmax == 48) != (nw == 6)) continue;  // 6-warp CTAs: 16 * MT tiles
       Far8Cfg c = make(KC, TTmax);
       if (c.mt > 0 && c.mt <= 2) return c;
     }
   return Far8Cfg{};
 }
 
-template <int MT, int NJ, int REM>
+template <int MT, int NJ, int REM, bool M3 = false, int NW = 8>
 cudaError_t launch8(const Far8Cfg& c, int nseg, const Far8Args& a, cudaStream_t st) {
-  auto k = far8_kernel<MT, NJ, REM>;
+  auto k = far8_kernel<MT, NJ, REM, M3, NW>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   if (e != cudaSuccess) return e;
-  k<<<dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks), 256, c.smem, st>>>(a);
+  k<<<dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks), NW * 32, c.smem, st>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t dispatch8(const Far8Cfg& c, int p, bool rem_dfma, int nseg, const Far8Args& a, cudaStream_t st) {
+cudaError_t dispatch8(const Far8Cfg& c, int p, bool rem_dfma, int nseg, const Far8Args& a, cudaStream_t st,
+                      bool m3 = false, int nw = 8) {
+  if (nw == 6 && p > 8 && !(p == 27 && rem_dfma))
+    return c.mt == 1 ? (m3 ? launch8<1, 4, 0, true, 6>(c, nseg, a, st) : launch8<1, 4, 0, false, 6>(c, nseg, a, st))
+                     : (m3 ? launch8<2, 4, 0, true, 6>(c, nseg, a, st) : launch8<2, 4, 0, false, 6>(c, nseg, a, st));
+  if (m3 && c.mt == 1 && p > 8 && !(p == 27 && rem_dfma)) return launch8<1, 4, 0, true>(c, nseg, a, st);
   if (p <= 8) return c.mt == 1 ? launch8<1, 1, 0>(c, nseg, a, st) : launch8<2, 1, 0>(c, nseg, a, st);
   if (p == 27 && rem_dfma) return c.mt == 1 ? launch8<1, 3, 3>(c, nseg, a, st) : launch8<2, 3, 3>(c, nseg, a, st);
   return c.mt == 1 ? launch8<1, 4, 0>(c, nseg, a, st) : launch8<2, 4, 0>(c, nseg, a, st);
@@ -1162,7 +1229,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
     return BEM_OK;
   }
   if (aca && fk == 8 && !op.force_generic && op.n_segs > 0) {
-    Far8Cfg f8 = choose8(p, nl, op.far4_smem_cap, op.far8_kc);
+    Far8Cfg f8 = choose8(p, nl, op.far4_smem_cap, op.far8_kc, op.far7_ttmax, op.far8_nw);
     f8.smem = std::max(f8.smem, op.far_smem_min);  // residency experiment (env BEM_FAR_SMEM_MIN_KB)
     if (f8.mt > 0) {
       BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
@@ -1173,7 +1240,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
       a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
       a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
       a.mask = op.d_mask;
-      BEM_CK(dispatch8(f8, p, op.far7_rem_dfma, op.n_segs, a, st));
+      BEM_CK(dispatch8(f8, p, op.far7_rem_dfma, op.n_segs, a, st, op.far7_m3, op.far8_nw));
       seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
                                                        yhat, (int64_t)nl * p);
       BEM_CK(cudaGetLastError());
@@ -1181,7 +1248,8 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
     }
   }
   if (aca && fk == 7 && !op.force_generic && op.n_segs > 0) {
-    Far7Cfg f7 = choose7(p, nl, op.far4_smem_cap, op.far7_cluster);
+    Far7Cfg f7 = choose7(p, nl, op.far7_nw == 16 ? 200 * 1024 : op.far4_smem_cap, op.far7_cluster && op.far7_nw != 16,
+                         op.far7_ttmax, op.far7_nw);
     f7.smem = std::max(f7.smem, op.far_smem_min);  // residency experiment (env BEM_FAR_SMEM_MIN_KB)
     if (f7.mt > 0) {
       BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
@@ -1192,7 +1260,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
       a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
       a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
       a.mask = op.d_mask;
-      BEM_CK(dispatch7(f7, p, op.far7_rem_dfma, op.n_segs, a, st));
+      BEM_CK(dispatch7(f7, p, op.far7_rem_dfma, op.n_segs, a, st, op.far7_nw, op.far7_m3));
       seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
                                                        yhat, (int64_t)nl * p);
       BEM_CK(cudaGetLastError());

@@ -288,6 +288,30 @@ def test_h2aca_p64_multi_tile(pb, torch, N, kernel, cluster, monkeypatch):
         assert _rel(y[lsel[i]], yo[i]) <= 1e-8, lsel[i]
 
 
+@pytest.mark.parametrize("m,leaf,N,env", [
+    (3, 32, 128, {"BEM_FAR7_NW": "16"}), (3, 32, 128, {"BEM_FAR7_NW": "16", "BEM_FAR7_M3": "1"}),
+    (3, 32, 128, {"BEM_FAR7_M3": "1", "BEM_FAR7_TTMAX": "64"}),
+    (4, 48, 256, {"BEM_FAR8_NW": "6"}), (4, 48, 256, {"BEM_FAR8_NW": "6", "BEM_FAR7_M3": "1"}),
+    (4, 48, 256, {"BEM_FAR7_M3": "1", "BEM_FAR7_TTMAX": "64"})])
+def test_k3_variants(pb, torch, m, leaf, N, env, monkeypatch):
+    """The measured K3 alternatives (profiles/r01_sweeps.md; off by default):
+    16-warp far7 CTAs, 6-warp far8 CTAs, 3M complex products (three real DMMA
+    products per complex one).  Oracle on a frequency sample."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    V, T = synth.icosphere(3)
+    M, L, eps = len(T), N + 1, 1e-6
+    s = pb.cqm_frequencies(N, 2.0)
+    x = synth.random_density(3, L, M)
+    oh = O.H2(V, T, leaf, 1.0, m)
+    oh.aca(s, eps)
+    op = pb.Operator(pb.Tree(V, T, leaf, 1.0, m), s, eps, mode=pb.BEM_MODE_H2ACA)
+    y = _apply(pb, torch, op, x)
+    lsel = np.unique(np.r_[0, 1, 7, 8, 63, 64, 127, 128, L // 2, L - 2, L - 1])
+    yo = oh.apply(O.MODE_H2ACA, s, x[lsel], lsel)
+    assert _rel(y[lsel], yo) <= 1e-10
+
+
 @pytest.mark.parametrize("nloc", [10, 19])
 def test_local_subset_padded_columns(pb, torch, nloc):
     """A frequency shard whose size leaves 3..7 columns past a multiple of 8

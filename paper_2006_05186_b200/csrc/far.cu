@@ -562,9 +562,9 @@ Far7Cfg choose7(int p, int nl, size_t cap, bool cluster, int ttmax_cap = 0, int 
   return Far7Cfg{};
 }
 
-template <int MT, bool CL, int NJ, int REM>
+template <int MT, bool CL, int NJ, int REM, bool M3 = false>
 cudaError_t launch7(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream_t st) {
-  auto k = far7_kernel<MT, CL, NJ, REM>;
+  auto k = far7_kernel<MT, CL, NJ, REM, 8, M3>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   if (e != cudaSuccess) return e;
   if (!CL) {
@@ -617,6 +617,9 @@ cudaError_t dispatch7(const Far7Cfg& c, int p, bool rem_dfma, int nseg, const Fa
     if (p == 27 && rem_dfma) return m3 ? launch7w<3, 3, true>(c, nseg, a, st) : launch7w<3, 3, false>(c, nseg, a, st);
     return m3 ? launch7w<4, 0, true>(c, nseg, a, st) : launch7w<4, 0, false>(c, nseg, a, st);
   }
+  if (m3 && c.mt == 1 && c.cs == 1 && p > 8)  // 3M at one t-tile per warp (room for the third accumulator)
+    return (p == 27 && rem_dfma) ? launch7<1, false, 3, 3, true>(c, nseg, a, st)
+                                 : launch7<1, false, 4, 0, true>(c, nseg, a, st);
   if (p <= 8) return dispatch7_<1, 0>(c, nseg, a, st);
   if (p == 27 && rem_dfma) return dispatch7_<3, 3>(c, nseg, a, st);
   return dispatch7_<4, 0>(c, nseg, a, st);

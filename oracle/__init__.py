@@ -14,6 +14,11 @@ Function-to-paper map (P = /root/reference/PAPER.md):
   H2.apply                   eq:lrfinal P:1404-1410 (DENSE / H2ONLY / H2ACA / COMBINED)
   H2.aca_near                Alg. 3 NEAR branch P:1426-1431, P:1444-1450 (NEXT-4)
   dense_matrix_pinned        C3 entries in the pinned arithmetic the near MACA reads
+  H2.time_weights            eq:fastdft P:1542-1553 (dhat = R-scaled inverse DFT of Z rows)
+  H2.conv / weight_dense     eq:fastrhs P:1566-1573 / the weights V^_n assembled densely
+  H2.mot                     eq:cqmrhs P:652-680 with one LU of V^_0
+Every function is pinned by tests/test_oracle_*.py and tests/test_golden.py (no
+"parity unpinned" entries).
   forward / inverse          eq:omega_n P:436-441, eq:slphelm P:529-540
   H2.gmres                   frequency-decoupled solve, Remark P:1607-1614
 """

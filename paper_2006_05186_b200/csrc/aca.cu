@@ -708,6 +708,7 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   if (const char* e = getenv("BEM_FAR7_NW")) op.far7_nw = atoi(e) == 16 ? 16 : 8;
   if (const char* e = getenv("BEM_FAR7_M3")) op.far7_m3 = atoi(e) != 0;
   if (const char* e = getenv("BEM_FAR8_NW")) op.far8_nw = atoi(e) == 6 ? 6 : 8;
+  if (const char* e = getenv("BEM_FAR7_SPLIT")) op.far7_split = atoi(e) != 0;
   if (const char* e = getenv("BEM_H2O_FC")) op.h2o_fc = atoi(e);
   if (const char* e = getenv("BEM_SOLVE_MASK")) op.use_solve_mask = atoi(e) != 0;
   if (const char* e = getenv("BEM_OVERLAP")) op.overlap = atoi(e) != 0;

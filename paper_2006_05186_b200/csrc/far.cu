@@ -266,6 +266,7 @@ cudaError_t dispatch6(const Far6Cfg& c, int nseg, const Far6Args& a, cudaStream_
 struct Far7Args {
   int nl, m, p, p4, rcap, SST, TT, XTP, nT, tb, nd, cs, own;  // DMMA columns [tb, tb+nd) (padded past nl);
                                                             // own = slice entries regenerated per cluster CTA
+  int mu_base = 0, rows = 1 << 30;  // this launch covers rows [mu_base, mu_base + rows) (REM split)
   const int4* segs;
   const int32_t* far_sorted;
   const int32_t* far_c;
@@ -303,8 +304,8 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) far7_kernel(Far7Args a) {
   const int tc0 = a.tb + blockIdx.y * a.TT;
   const int ncol = min(a.TT, a.tb + a.nd - tc0);
   const bool lead = blockIdx.y == 0;
-  const int mu0 = blockIdx.z * 32;
-  const int nrow = min(32, p - mu0);
+  const int mu0 = a.mu_base + blockIdx.z * 32;
+  const int nrow = min(32, min(p, a.mu_base + a.rows) - mu0);
   const int nS = nrow * p;
   double2* S0 = sm;                                   // 2 x (32 x SST): double-buffered slice rows
   double2* own = S0 + 2 * 32 * SST;                   // CL: 2 x a.own
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) far7_kernel(Far7Args a) {
     cta_on = __syncthreads_or(lo) != 0;
     if (CL) cta_on = true;  // every CTA of a cluster must reach the same cluster barriers
   }
-  double acc[MT][NJ][M3 ? 3 : 2][2];
+  double acc[MT][NJ > 0 ? NJ : 1][M3 ? 3 : 2][2];
   double2 racc[MT][REM > 0 ? REM : 1];
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
@@ -414,7 +415,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) far7_kernel(Far7Args a) {
         __syncthreads();
       }
       for (int k0 = 0; k0 < p4; k0 += 4) {
-        double2 bf[NJ], rf[REM > 0 ? REM : 1];
+        double2 bf[NJ > 0 ? NJ : 1], rf[REM > 0 ? REM : 1];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) bf[j] = S[(j * 8 + g) * SST + k0 + q];
 #pragma unroll
@@ -611,11 +612,23 @@ cudaError_t launch7w(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream_t
 
 // mu tiling: p = 27 -> 3 DMMA tiles + 3 DFMA rows; p <= 8 -> 1 tile; otherwise 4 tiles per 32-row chunk
 cudaError_t dispatch7(const Far7Cfg& c, int p, bool rem_dfma, int nseg, const Far7Args& a, cudaStream_t st,
-                      int nw = 8, bool m3 = false) {
+                      int nw = 8, bool m3 = false, bool split = false) {
   if (nw == 16) {
     if (p <= 8) return m3 ? launch7w<1, 0, true>(c, nseg, a, st) : launch7w<1, 0, false>(c, nseg, a, st);
     if (p == 27 && rem_dfma) return m3 ? launch7w<3, 3, true>(c, nseg, a, st) : launch7w<3, 3, false>(c, nseg, a, st);
     return m3 ? launch7w<4, 0, true>(c, nseg, a, st) : launch7w<4, 0, false>(c, nseg, a, st);
+  }
+  if (p == 27 && split && c.cs == 1) {
+    // rows 0..23: 3M DMMA tiles (no DFMA rows: room for the third accumulator at MT = 2);
+    // rows 24..26: a DFMA-only launch of the same kernel (NJ = 0) into the same partial slots
+    Far7Args a1 = a, a2 = a;
+    a1.mu_base = 0; a1.rows = 24;
+    a2.mu_base = 24; a2.rows = 3;
+    Far7Cfg c2 = c;
+    c2.nchunks = 1;
+    cudaError_t e = c.mt == 1 ? launch7<1, false, 3, 0, true>(c2, nseg, a1, st) : launch7<2, false, 3, 0, true>(c2, nseg, a1, st);
+    if (e != cudaSuccess) return e;
+    return c.mt == 1 ? launch7<1, false, 0, 3, false>(c2, nseg, a2, st) : launch7<2, false, 0, 3, false>(c2, nseg, a2, st);
   }
   if (m3 && c.mt == 1 && c.cs == 1 && p > 8)  // 3M at one t-tile per warp (room for the third accumulator)
     return (p == 27 && rem_dfma) ? launch7<1, false, 3, 3, true>(c, nseg, a, st)
@@ -1263,7 +1276,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
       a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
       a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
       a.mask = op.d_mask;
-      BEM_CK(dispatch7(f7, p, op.far7_rem_dfma, op.n_segs, a, st, op.far7_nw, op.far7_m3));
+      BEM_CK(dispatch7(f7, p, op.far7_rem_dfma, op.n_segs, a, st, op.far7_nw, op.far7_m3, op.far7_split));
       seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
                                                        yhat, (int64_t)nl * p);
       BEM_CK(cudaGetLastError());

@@ -290,7 +290,7 @@ def test_h2aca_p64_multi_tile(pb, torch, N, kernel, cluster, monkeypatch):
 
 @pytest.mark.parametrize("m,leaf,N,env", [
     (3, 32, 128, {"BEM_FAR7_NW": "16"}), (3, 32, 128, {"BEM_FAR7_NW": "16", "BEM_FAR7_M3": "1"}),
-    (3, 32, 128, {"BEM_FAR7_M3": "1", "BEM_FAR7_TTMAX": "64"}),
+    (3, 32, 128, {"BEM_FAR7_M3": "1", "BEM_FAR7_TTMAX": "64"}), (3, 32, 128, {"BEM_FAR7_SPLIT": "1"}),
     (4, 48, 256, {"BEM_FAR8_NW": "6"}), (4, 48, 256, {"BEM_FAR8_NW": "6", "BEM_FAR7_M3": "1"}),
     (4, 48, 256, {"BEM_FAR7_M3": "1", "BEM_FAR7_TTMAX": "64"})])
 def test_k3_variants(pb, torch, m, leaf, N, env, monkeypatch):

@@ -362,7 +362,8 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
       double2* c = Cb + (size_t)ell * pp;
       for (int q = threadIdx.x; q < pp; q += blockDim.x) {
         double2 acc = entry(q, k);
-        for (int j = 0; j < ell; ++j) acc = csub(acc, cmul(dk[j], Cb[(size_t)j * pp + q]));
+#pragma unroll 8
+        for (int j = 0; j < ell; ++j) acc = csub(acc, cmul(dk[j], Cb[(size_t)j * pp + q]));  // loads run ahead
         c[q] = acc;
         if (!((usedq[q >> 5] >> (q & 31)) & 1u)) {
           const double kk = key(acc);
@@ -381,6 +382,7 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
       int bl = 0x7fffffff;
       for (int l = threadIdx.x; l < L; l += blockDim.x) {
         double2 acc = entry(qs, l);
+#pragma unroll 8
         for (int j = 0; j < ell; ++j) acc = csub(acc, cmul(cq[j], Db[(size_t)j * L + l]));
         Eb[l] = acc;
         d[l] = cdiv(acc, piv);
@@ -406,6 +408,7 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
           const double2* cj = Cb + (size_t)j * pp;
           double sr = 0.0, si = 0.0;
           const int e = min(pp, (ch << 5) + 32);
+#pragma unroll 8
           for (int i = ch << 5; i < e; ++i) {
             const double2 x = cmulconj(cj[i], c[i]);
             sr = __dadd_rn(sr, x.x);
@@ -418,6 +421,7 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
           const double2* dj = Db + (size_t)j * L;
           double sr = 0.0, si = 0.0;
           const int e = min(L, (ch << 5) + 32);
+#pragma unroll 8
           for (int i = ch << 5; i < e; ++i) {
             const double2 x = cmulconj(dj[i], d[i]);
             sr = __dadd_rn(sr, x.x);

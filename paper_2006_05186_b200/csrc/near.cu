@@ -21,10 +21,6 @@ namespace bem {
 namespace {
 
 constexpr int kNearWarps = 4;
-#ifndef BEM_NEAR_MINB
-#define BEM_NEAR_MINB 3
-#endif
-constexpr int kNearMinBlocks = BEM_NEAR_MINB;  // CTAs per SM the register budget targets
 
 struct NearArgs {
   int64_t M;
@@ -214,7 +210,7 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
 }
 
 template <int F, int U, bool TAB>
-__global__ void __launch_bounds__(kNearWarps * 32, kNearMinBlocks) near_kernel(NearArgs a) {
+__global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
   near_body<F, U, TAB>(a);
 }
 // double-layer near field (NEXT-1)

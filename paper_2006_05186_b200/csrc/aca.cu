@@ -563,7 +563,7 @@ bem_status run_aca(Op& op, cudaStream_t st, bool near) {
   {
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
-      const size_t scratch = (size_t)std::max(1, std::min(nblk, nsm * 4)) * rcap * ((size_t)ppmax + L) * 16;
+      const size_t scratch = (size_t)std::max(1, std::min(nblk, nsm * op.aca_ctas_per_sm)) * rcap * ((size_t)ppmax + L) * 16;
       const unsigned long long lim = fr > scratch ? (unsigned long long)((fr - scratch) * 0.7 / 16) : 0ull;
       if (lim > 0 && cap + scap > lim) {
         const double f = (double)lim / (double)(cap + scap);
@@ -593,7 +593,7 @@ bem_status run_aca(Op& op, cudaStream_t st, bool near) {
     for (int q = 0; q < 7; ++q) wq[q] = W[q];
   }
   for (int attempt = 0; attempt < 8; ++attempt) {
-    const int grid = std::max(1, std::min(nblk, nsm * 4));
+    const int grid = std::max(1, std::min(nblk, nsm * op.aca_ctas_per_sm));
     DBuf<double> Cbuf, Dbuf, Ebuf, Pbuf;
     BEM_CK(Pbuf.alloc((size_t)grid * rcap * ((ppmax + 31) / 32 + (L + 31) / 32) * 2));
     BEM_CK(Cbuf.alloc((size_t)grid * rcap * ppmax * 2));
@@ -713,6 +713,7 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   if (const char* e = getenv("BEM_FAR7_M3")) op.far7_m3 = atoi(e) != 0;
   if (const char* e = getenv("BEM_FAR8_NW")) op.far8_nw = atoi(e) == 6 ? 6 : 8;
   if (const char* e = getenv("BEM_FAR7_SPLIT")) op.far7_split = atoi(e) != 0;
+  if (const char* e = getenv("BEM_ACA_CTAS")) op.aca_ctas_per_sm = std::max(1, atoi(e));
   if (const char* e = getenv("BEM_H2O_FC")) op.h2o_fc = atoi(e);
   if (const char* e = getenv("BEM_SOLVE_MASK")) op.use_solve_mask = atoi(e) != 0;
   if (const char* e = getenv("BEM_OVERLAP")) op.overlap = atoi(e) != 0;

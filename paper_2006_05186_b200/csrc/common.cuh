@@ -192,7 +192,7 @@ struct Op {
   int far7_nw = 8;                    // far7 warps per CTA: 8 (2 CTAs/SM) or 16 (env BEM_FAR7_NW)
   bool far7_m3 = false;               // far7/far8 3M complex products (env BEM_FAR7_M3)
   int far8_nw = 8;                    // far8 warps per CTA: 8 or 6 (env BEM_FAR8_NW)
-  int aca_ctas_per_sm = 4;            // persistent ACA CTAs per SM (env BEM_ACA_CTAS)
+  int aca_ctas_per_sm = 5;            // persistent ACA CTAs per SM = register-limited residency (env BEM_ACA_CTAS; r01: 4 -> 5-8 cut config-4 setup 2.96 -> 2.64 s)
   bool far7_split = false;            // p = 27: 3M DMMA rows 0..23 + DFMA-only rows 24..26 (env BEM_FAR7_SPLIT)
   int h2o_fc = 0;                     // K3' classes per CTA tile (0: 6 for p <= 32, else 2; env BEM_H2O_FC)
   // optional per-local-frequency mask (1 = compute); set only by the GMRES driver so that

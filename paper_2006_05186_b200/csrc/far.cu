@@ -649,6 +649,7 @@ cudaError_t dispatch7(const Far7Cfg& c, int p, bool rem_dfma, int nseg, const Fa
 // frequency, at p = 64 and could not hold p = 125 at all).
 struct Far8Args {
   int nl, m, p, rcap, SST, TT, XTP, tb, nd, KC;
+  int nch = 1;  // mu chunks (grid x = segment * nch + chunk)
   const int4* segs;
   const int32_t* far_sorted;
   const int32_t* far_c;
@@ -669,12 +670,14 @@ template <int MT, int NJ, int REM, bool M3 = false, int NW = 8>
 __global__ void __launch_bounds__(NW * 32, 2) far8_kernel(Far8Args a) {
   extern __shared__ double2 sm[];
   const int p = a.p, m = a.m, SST = a.SST, XTP = a.XTP, tb = a.tb, KC = a.KC;
-  const int4 sg = a.segs[blockIdx.x];
+  // the mu chunks of one (segment, tile) are adjacent CTAs: the second chunk re-reads the
+  // x^ and Z tiles from L2 instead of DRAM
+  const int4 sg = a.segs[blockIdx.x / a.nch];
   const int r = sg.x;
   const int tc0 = a.tb + blockIdx.y * a.TT;
   const int ncol = min(a.TT, a.tb + a.nd - tc0);
   const bool lead = blockIdx.y == 0;
-  const int mu0 = blockIdx.z * 32;
+  const int mu0 = (blockIdx.x % a.nch) * 32;
   const int nrow = min(32, p - mu0);
   double2* S0 = sm;                                   // 2 x (32 x SST), SST >= KC: double-buffered slice
   double2* xs = S0 + 2 * 32 * SST;                    // KC x XTP
@@ -929,7 +932,9 @@ cudaError_t launch8(const Far8Cfg& c, int nseg, const Far8Args& a, cudaStream_t 
   auto k = far8_kernel<MT, NJ, REM, M3, NW>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   if (e != cudaSuccess) return e;
-  k<<<dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks), NW * 32, c.smem, st>>>(a);
+  Far8Args a2 = a;
+  a2.nch = c.nchunks;
+  k<<<dim3((unsigned)(nseg * c.nchunks), (unsigned)c.ntiles, 1u), NW * 32, c.smem, st>>>(a2);
   return cudaGetLastError();
 }
 

@@ -11,6 +11,7 @@
 // The length-L linear convolution runs as a power-of-two P >= 2L-1 radix-2
 // FFT in shared memory, one CTA per group of DOF columns (coalesced row loads).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -201,7 +202,11 @@ bem_status fft_transform_rows(const double* in, double* out, int64_t M, int N, d
   Plan* pl = nullptr;
   bem_status rs = get_plan(N, R, inverse, &pl);
   if (rs != BEM_OK) return rs;
-  const int NC = std::max(1, 4096 / pl->P);
+  static const int nc_elems = [] {  // columns x points per CTA (env BEM_FFT_ELEMS; r01 sweep: 2048 best)
+    const char* e = getenv("BEM_FFT_ELEMS");
+    return e ? std::max(64, atoi(e)) : 2048;
+  }();
+  const int NC = std::max(1, nc_elems / pl->P);
   const size_t smem = sizeof(double2) * (size_t)NC * pl->P;
   BEM_CK(cudaFuncSetAttribute(bluestein_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const unsigned grid = (unsigned)((M + NC - 1) / NC);

@@ -111,22 +111,61 @@ __device__ __forceinline__ double2 cm(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-// in-place radix-2 DIT FFT of NC columns (bit-reversed input order assumed)
-__device__ void smem_fft(double2* buf, int P, int logP, int NC, const double2* __restrict__ tw, bool inv) {
-  for (int s = 0; s < logP; ++s) {
-    const int half = 1 << s;
-    const int tstride = P >> (s + 1);
-    for (int idx = threadIdx.x; idx < NC * (P >> 1); idx += blockDim.x) {
-      const int col = idx / (P >> 1), bfly = idx % (P >> 1);
-      const int grp = bfly >> s, pos = bfly & (half - 1);
-      const int i = (grp << (s + 1)) + pos, j = i + half;
-      double2 w = tw[pos * tstride];
-      if (inv) w.y = -w.y;
-      double2* b = buf + (size_t)col * P;
-      const double2 u = b[i], v = cm(b[j], w);
-      b[i] = make_double2(u.x + v.x, u.y + v.y);
-      b[j] = make_double2(u.x - v.x, u.y - v.y);
+// in-place radix-2 DIT FFT of NC columns (bit-reversed input order assumed), up to three
+// radix-2 stages per shared-memory pass: a thread loads the 8 (or 4 / 2) elements
+// i0 + m * 2^s of one group, applies stages s, s+1, s+2 in registers and stores them
+// back (stage s pairs (m, m+1), s+1 pairs (m, m+2), s+2 pairs (m, m+4)), so a
+// P = 512 transform takes 3 passes and barriers instead of 9 (r01: K4 was bound by the
+// per-stage shared-memory round trips).
+template <int G>  // elements per thread-group = 2^stages in this pass
+__device__ __forceinline__ void fft_pass(double2* buf, int P, int s, int NC, const double2* __restrict__ tw,
+                                         bool inv, const double2* __restrict__ post_mul) {
+  const int h0 = 1 << s;                     // half-width of the first stage
+  const int ngrp = NC * (P / G);
+  for (int g = threadIdx.x; g < ngrp; g += blockDim.x) {
+    const int col = g / (P / G), r = g - col * (P / G);
+    const int pos0 = r & (h0 - 1), blk = r >> s;   // group = blk-th run of G*h0 elements
+    double2* b = buf + (size_t)col * P + blk * (G * h0) + pos0;
+    double2 e[G];
+#pragma unroll
+    for (int m = 0; m < G; ++m) e[m] = b[m * h0];
+#pragma unroll
+    for (int st = 0, span = 1; span < G; ++st, span <<= 1) {
+      const int tstride = P >> (s + st + 1);
+#pragma unroll
+      for (int m = 0; m < G; ++m) {
+        if (m & span) continue;                   // m is the upper element of its pair
+        const int pos = pos0 + (m & (span - 1)) * h0;
+        double2 w = tw[pos * tstride];
+        if (inv) w.y = -w.y;
+        const double2 u = e[m], v = cm(e[m + span], w);
+        e[m] = make_double2(u.x + v.x, u.y + v.y);
+        e[m + span] = make_double2(u.x - v.x, u.y - v.y);
+      }
     }
+    if (post_mul) {  // last pass of the forward transform: the filter spectrum, fused
+      const int k0 = blk * (G * h0) + pos0;
+#pragma unroll
+      for (int m = 0; m < G; ++m) e[m] = cm(e[m], post_mul[k0 + m * h0]);
+    }
+#pragma unroll
+    for (int m = 0; m < G; ++m) b[m * h0] = e[m];
+  }
+}
+
+// post_mul (nullable): pointwise factor applied to the natural-order result in the last pass
+__device__ void smem_fft(double2* buf, int P, int logP, int NC, const double2* __restrict__ tw, bool inv,
+                         const double2* __restrict__ post_mul = nullptr) {
+  int s = 0;
+  for (; s + 3 <= logP; s += 3) {
+    fft_pass<8>(buf, P, s, NC, tw, inv, s + 3 == logP ? post_mul : nullptr);
+    __syncthreads();
+  }
+  if (logP - s == 2) {
+    fft_pass<4>(buf, P, s, NC, tw, inv, post_mul);
+    __syncthreads();
+  } else if (logP - s == 1) {
+    fft_pass<2>(buf, P, s, NC, tw, inv, post_mul);
     __syncthreads();
   }
 }
@@ -166,13 +205,8 @@ __global__ void __launch_bounds__(kFftThreads) bluestein_kernel(const double2* _
     if (n < P) buf[(size_t)col * P + rv] = v;
   }
   __syncthreads();
-  smem_fft(buf, P, logP, NC, tw, false);
-  // multiply by the filter spectrum (already scaled by 1/P), re-order bit-reversed
-  for (int idx = threadIdx.x; idx < NC * P; idx += blockDim.x) {
-    const int col = idx / P, k = idx % P;
-    buf[(size_t)col * P + k] = cm(buf[(size_t)col * P + k], hhat[k]);
-  }
-  __syncthreads();
+  // forward FFT, then the filter spectrum (already scaled by 1/P), fused into its last pass
+  smem_fft(buf, P, logP, NC, tw, false, hhat);
   // bit-reverse permutation in place (swap pairs once)
   for (int idx = threadIdx.x; idx < NC * P; idx += blockDim.x) {
     const int col = idx / P, k = idx % P;

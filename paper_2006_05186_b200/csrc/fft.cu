@@ -117,6 +117,10 @@ __device__ __forceinline__ double2 cm(double2 a, double2 b) {
 // back (stage s pairs (m, m+1), s+1 pairs (m, m+2), s+2 pairs (m, m+4)), so a
 // P = 512 transform takes 3 passes and barriers instead of 9 (r01: K4 was bound by the
 // per-stage shared-memory round trips).
+// Shared-memory element swizzle within a column: bits 0-2 XOR bits 3-5. Every 8 threads
+// of a radix-8 pass (h0 = 1, 8, 64) then touch 8 different 16-byte bank groups.
+__device__ __forceinline__ int sw(int i) { return i ^ ((i >> 3) & 7); }
+
 template <int G>  // elements per thread-group = 2^stages in this pass
 __device__ __forceinline__ void fft_pass(double2* buf, int P, int s, int NC, const double2* __restrict__ tw,
                                          bool inv, const double2* __restrict__ post_mul) {
@@ -125,10 +129,11 @@ __device__ __forceinline__ void fft_pass(double2* buf, int P, int s, int NC, con
   for (int g = threadIdx.x; g < ngrp; g += blockDim.x) {
     const int col = g / (P / G), r = g - col * (P / G);
     const int pos0 = r & (h0 - 1), blk = r >> s;   // group = blk-th run of G*h0 elements
-    double2* b = buf + (size_t)col * P + blk * (G * h0) + pos0;
+    double2* b = buf + (size_t)col * P;
+    const int i0 = blk * (G * h0) + pos0;
     double2 e[G];
 #pragma unroll
-    for (int m = 0; m < G; ++m) e[m] = b[m * h0];
+    for (int m = 0; m < G; ++m) e[m] = b[sw(i0 + m * h0)];
 #pragma unroll
     for (int st = 0, span = 1; span < G; ++st, span <<= 1) {
       const int tstride = P >> (s + st + 1);
@@ -144,12 +149,11 @@ __device__ __forceinline__ void fft_pass(double2* buf, int P, int s, int NC, con
       }
     }
     if (post_mul) {  // last pass of the forward transform: the filter spectrum, fused
-      const int k0 = blk * (G * h0) + pos0;
 #pragma unroll
-      for (int m = 0; m < G; ++m) e[m] = cm(e[m], post_mul[k0 + m * h0]);
+      for (int m = 0; m < G; ++m) e[m] = cm(e[m], post_mul[i0 + m * h0]);
     }
 #pragma unroll
-    for (int m = 0; m < G; ++m) b[m * h0] = e[m];
+    for (int m = 0; m < G; ++m) b[sw(i0 + m * h0)] = e[m];
   }
 }
 
@@ -202,7 +206,7 @@ __global__ void __launch_bounds__(kFftThreads) bluestein_kernel(const double2* _
       v = cm(row[c0 + col], pre[n]);
     }
     const int rv = (int)(__brev((unsigned)n) >> (32 - logP));
-    if (n < P) buf[(size_t)col * P + rv] = v;
+    if (n < P) buf[(size_t)col * P + sw(rv)] = v;
   }
   __syncthreads();
   // forward FFT, then the filter spectrum (already scaled by 1/P), fused into its last pass
@@ -213,9 +217,9 @@ __global__ void __launch_bounds__(kFftThreads) bluestein_kernel(const double2* _
     const int rv = (int)(__brev((unsigned)k) >> (32 - logP));
     if (k < rv) {
       double2* b = buf + (size_t)col * P;
-      const double2 t = b[k];
-      b[k] = b[rv];
-      b[rv] = t;
+      const double2 t = b[sw(k)];
+      b[sw(k)] = b[sw(rv)];
+      b[sw(rv)] = t;
     }
   }
   __syncthreads();
@@ -224,7 +228,7 @@ __global__ void __launch_bounds__(kFftThreads) bluestein_kernel(const double2* _
     const int j = idx / NC, col = idx % NC;
     if (col < nc) {
       double2* row = out_rows ? out_rows->p[j] : out + (int64_t)j * M;
-      row[c0 + col] = cm(buf[(size_t)col * P + j], post[j]);
+      row[c0 + col] = cm(buf[(size_t)col * P + sw(j)], post[j]);
     }
   }
 }

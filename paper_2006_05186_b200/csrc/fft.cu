@@ -174,6 +174,58 @@ __device__ void smem_fft(double2* buf, int P, int logP, int NC, const double2* _
   }
 }
 
+// Decimation-in-frequency counterpart (natural-order input, bit-reversed output) for the
+// inverse FFT of the convolution: the same element groups as fft_pass, stages from the
+// largest half-width down, butterfly (u, v) -> (u + v, (u - v) w). Its bit-reversed output
+// is read through the bit-reversed index in the store phase, so the convolution needs no
+// permutation pass.
+template <int G>
+__device__ __forceinline__ void fft_pass_dif(double2* buf, int P, int s, int NC, const double2* __restrict__ tw,
+                                             bool inv) {
+  const int h0 = 1 << s;
+  const int ngrp = NC * (P / G);
+  for (int g = threadIdx.x; g < ngrp; g += blockDim.x) {
+    const int col = g / (P / G), r = g - col * (P / G);
+    const int pos0 = r & (h0 - 1), blk = r >> s;
+    double2* b = buf + (size_t)col * P;
+    const int i0 = blk * (G * h0) + pos0;
+    double2 e[G];
+#pragma unroll
+    for (int m = 0; m < G; ++m) e[m] = b[sw(i0 + m * h0)];
+#pragma unroll
+    for (int span = G / 2; span >= 1; span >>= 1) {
+      const int tstride = P / (2 * span * h0);
+#pragma unroll
+      for (int m = 0; m < G; ++m) {
+        if (m & span) continue;
+        const int pos = pos0 + (m & (span - 1)) * h0;
+        double2 w = tw[pos * tstride];
+        if (inv) w.y = -w.y;
+        const double2 u = e[m], v = e[m + span];
+        e[m] = make_double2(u.x + v.x, u.y + v.y);
+        e[m + span] = cm(make_double2(u.x - v.x, u.y - v.y), w);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < G; ++m) b[sw(i0 + m * h0)] = e[m];
+  }
+}
+
+__device__ void smem_fft_dif(double2* buf, int P, int logP, int NC, const double2* __restrict__ tw, bool inv) {
+  const int full = logP / 3, rem = logP - 3 * full;
+  if (rem == 2) {
+    fft_pass_dif<4>(buf, P, 3 * full, NC, tw, inv);
+    __syncthreads();
+  } else if (rem == 1) {
+    fft_pass_dif<2>(buf, P, 3 * full, NC, tw, inv);
+    __syncthreads();
+  }
+  for (int k = full - 1; k >= 0; --k) {
+    fft_pass_dif<8>(buf, P, 3 * k, NC, tw, inv);
+    __syncthreads();
+  }
+}
+
 // Row addressing of the transform's input and output: row r of the input is
 // in_rows.p[r] (or in + r*M when in_rows == nullptr), likewise for the output.
 // With row pointers into OTHER ranks' buffers (CUDA IPC / NVLink peer memory)
@@ -211,24 +263,13 @@ __global__ void __launch_bounds__(kFftThreads) bluestein_kernel(const double2* _
   __syncthreads();
   // forward FFT, then the filter spectrum (already scaled by 1/P), fused into its last pass
   smem_fft(buf, P, logP, NC, tw, false, hhat);
-  // bit-reverse permutation in place (swap pairs once)
-  for (int idx = threadIdx.x; idx < NC * P; idx += blockDim.x) {
-    const int col = idx / P, k = idx % P;
-    const int rv = (int)(__brev((unsigned)k) >> (32 - logP));
-    if (k < rv) {
-      double2* b = buf + (size_t)col * P;
-      const double2 t = b[sw(k)];
-      b[sw(k)] = b[sw(rv)];
-      b[sw(rv)] = t;
-    }
-  }
-  __syncthreads();
-  smem_fft(buf, P, logP, NC, tw, true);
+  smem_fft_dif(buf, P, logP, NC, tw, true);  // output in bit-reversed order
   for (int idx = threadIdx.x; idx < NC * L; idx += blockDim.x) {
     const int j = idx / NC, col = idx % NC;
     if (col < nc) {
       double2* row = out_rows ? out_rows->p[j] : out + (int64_t)j * M;
-      row[c0 + col] = cm(buf[(size_t)col * P + sw(j)], post[j]);
+      const int jr = (int)(__brev((unsigned)j) >> (32 - logP));
+      row[c0 + col] = cm(buf[(size_t)col * P + sw(jr)], post[j]);
     }
   }
 }

@@ -36,3 +36,25 @@ def test_time_step_graph_matches_eager_and_oracle():
     yo = O.inverse(oh.apply(O.MODE_H2ACA, s, O.forward(xt, N, R)), N, R)
     yg = y2.cpu().numpy()
     assert np.linalg.norm(yg - yo) / np.linalg.norm(yo) <= 1e-10
+
+
+@pytest.mark.parametrize("mode", ["h2only", "combined", "dense"])
+def test_time_step_other_modes(mode):
+    """The captured graph also covers the plain-H^2 couplings (K3'), the combined
+    mode's near-field MACA (K1m, persistent work queue reset inside the graph) and
+    the dense mode (no far field, no side stream)."""
+    import torch
+    import paper_2006_05186_b200 as pb
+    V, T = synth.icosphere(2 if mode == "dense" else 3)
+    N = 16
+    M, R = len(T), O.default_R(N)
+    s = pb.cqm_frequencies(N, 2.0)
+    leaf = 10 ** 6 if mode == "dense" else 32
+    m = {"h2only": pb.BEM_MODE_H2ONLY, "combined": pb.BEM_MODE_COMBINED, "dense": pb.BEM_MODE_DENSE}[mode]
+    op = pb.Operator(pb.Tree(V, T, leaf, 1.0, 3 if mode != "dense" else 1), s, 1e-6, mode=m)
+    xd = torch.from_numpy(synth.random_time_data(2, N, M).astype(np.complex128)).cuda()
+    ref = pb.cqm_inverse(op.apply(pb.cqm_forward(xd, N, R)), N, R)
+    for _ in range(3):
+        y = op.time_step(xd, R)
+    torch.cuda.synchronize()
+    assert torch.equal(y, ref)

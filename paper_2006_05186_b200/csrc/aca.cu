@@ -702,6 +702,7 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   if (const char* e = getenv("BEM_NEAR_F")) op.near_f = atoi(e);
   if (const char* e = getenv("BEM_NEAR_U")) op.near_unroll = atoi(e);
   if (const char* e = getenv("BEM_NEAR_TAB")) op.near_tab = atoi(e) != 0;
+  if (const char* e = getenv("BEM_NEAR_XL")) op.near_xlate = atoi(e) != 0;
   if (const char* e = getenv("BEM_FAR_GENERIC")) op.force_generic = atoi(e) != 0;
   if (const char* e = getenv("BEM_FAR_KERNEL")) op.far_kernel = atoi(e);
   if (const char* e = getenv("BEM_FAR4_SMEM_KB")) op.far4_smem_cap = (size_t)atoi(e) * 1024;

@@ -181,6 +181,7 @@ struct Op {
   int near_f = 4;  // frequency classes per warp (r01 sweeps: F=3 -> 4 after the parallel self term: config 2 6.17 -> 5.89 ms)
   int near_unroll = 7;
   bool near_tab = true;
+  bool near_xlate = true;   // K1 loads x after the node loop: 128 instead of 164 registers, 4 CTAs/SM (env BEM_NEAR_XL)
   bool force_generic = false;
   int far_kernel = 0;                 // 0: auto (far8 for p > 32, far7 otherwise); 8, 7, 6 (DMMA variants)
   size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM

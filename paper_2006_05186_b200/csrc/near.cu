@@ -74,7 +74,7 @@ __device__ __forceinline__ double2 self_node(const double* qn, const double* qw,
 
 // DL: double-layer kernel d/dn_y e^{-sr}/(4 pi r) (NEXT-1): per node the factor
 // (x - y).n_y / r^3 and (1 + s r) e^{-s r}; the self panel contributes 0.
-template <int F, int U, bool TAB, bool DL = false>
+template <int F, int U, bool TAB, bool DL = false, bool XL = false>  // XL: load x after the node loop
 __device__ __forceinline__ void near_body(const NearArgs& a) {
   __shared__ double etab[64];
   __shared__ double2 sctab[64];
@@ -130,10 +130,12 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
       if (jj + 32 < je) jn = a.near_j[jj + 32];
       if (j == k) continue;  // self panel below
       double2 x1[F], x2[F];  // issued before the node loop: their latency hides behind it
+      if (!XL) {
 #pragma unroll
-      for (int f = 0; f < F; ++f) {
-        x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
-        x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
+        for (int f = 0; f < F; ++f) {
+          x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
+          x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
+        }
       }
       double2 v[F];
 #pragma unroll
@@ -163,6 +165,13 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
             v[f].x = fma(e, cs, v[f].x);
             v[f].y = fma(-e, sn, v[f].y);
           }
+        }
+      }
+      if (XL) {
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
+          x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
         }
       }
 #pragma unroll
@@ -209,19 +218,19 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
   }
 }
 
-template <int F, int U, bool TAB>
+template <int F, int U, bool TAB, bool XL = false>
 __global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
-  near_body<F, U, TAB>(a);
+  near_body<F, U, TAB, false, XL>(a);
 }
 // double-layer near field (NEXT-1)
-template <int F>
+template <int F, bool XL = false>
 __global__ void __launch_bounds__(kNearWarps * 32) near_kernel_dl(NearArgs a) {
-  near_body<F, 7, true, true>(a);
+  near_body<F, 7, true, true, XL>(a);
 }
-template <int F, int U, bool TAB>
+template <int F, int U, bool TAB, bool XL = false>
 cudaError_t launch(const NearArgs& na, cudaStream_t st) {
   dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + F - 1) / F));
-  near_kernel<F, U, TAB><<<g, kNearWarps * 32, 0, st>>>(na);
+  near_kernel<F, U, TAB, XL><<<g, kNearWarps * 32, 0, st>>>(na);
   return cudaGetLastError();
 }
 
@@ -245,11 +254,14 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st, 
   cudaError_t e;
   if (dl) {
     dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + 3) / 4));
-    near_kernel_dl<4><<<g, kNearWarps * 32, 0, st>>>(na);
+    if (op.near_xlate) near_kernel_dl<4, true><<<g, kNearWarps * 32, 0, st>>>(na);
+    else near_kernel_dl<4><<<g, kNearWarps * 32, 0, st>>>(na);
     e = cudaGetLastError();
   } else if (F == 3) e = T ? (U == 7 ? launch<3, 7, true>(na, st) : launch<3, 1, true>(na, st))
                     : (U == 7 ? launch<3, 7, false>(na, st) : launch<3, 1, false>(na, st));
-  else if (F == 4) e = T ? (U == 7 ? launch<4, 7, true>(na, st) : launch<4, 1, true>(na, st)) : launch<4, 1, false>(na, st);
+  else if (F == 4) e = T ? (U == 7 ? (op.near_xlate ? launch<4, 7, true, true>(na, st) : launch<4, 7, true>(na, st))
+                             : launch<4, 1, true>(na, st))
+                         : launch<4, 1, false>(na, st);
   else if (F == 5 && T) e = launch<5, 7, true>(na, st);
   else if (F == 6 && T) e = launch<6, 7, true>(na, st);
   else e = T ? (U == 7 ? launch<2, 7, true>(na, st) : launch<2, 1, true>(na, st))

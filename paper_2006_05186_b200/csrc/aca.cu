@@ -699,7 +699,7 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   bem_op_s* h = new bem_op_s();
   Op& op = h->o;
   op.tree = &t; op.L = L; op.n_local = (int)loc.size(); op.mode = mode; op.eps = aca_eps; op.local_l = loc;
-  if (const char* e = getenv("BEM_NEAR_F")) op.near_f = std::min(5, std::max(2, atoi(e)));  // 6 nodes x F <= 32 lanes
+  if (const char* e = getenv("BEM_NEAR_F")) op.near_f = atoi(e) == 0 ? 0 : std::min(5, std::max(2, atoi(e)));  // 6F <= 32 lanes
   if (const char* e = getenv("BEM_NEAR_U")) op.near_unroll = atoi(e);
   if (const char* e = getenv("BEM_NEAR_TAB")) op.near_tab = atoi(e) != 0;
   if (const char* e = getenv("BEM_NEAR_XL")) op.near_xlate = atoi(e) != 0;

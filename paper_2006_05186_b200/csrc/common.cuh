@@ -178,8 +178,8 @@ struct Op {
   // workspaces
   DBuf<double> d_xc, d_yc, d_xhat, d_yhat;
   // kernel variants (tuning knobs; env BEM_NEAR_F, BEM_FAR_GENERIC read at assembly)
-  int near_f = 4;  // frequency classes per warp (r01 sweeps: 3 -> 4 after the parallel self term; F <= 5: the self
-                   // term spreads 6 nodes per class over the 32 lanes)
+  int near_f = 0;  // frequency classes per warp, 0 = automatic 4 or 5 (near.cu); F <= 5: the self term spreads
+                   // 6 nodes per class over the 32 lanes
   int near_unroll = 7;
   bool near_tab = true;
   bool near_xlate = true;   // K1 loads x after the node loop: 128 instead of 164 registers, 4 CTAs/SM (env BEM_NEAR_XL)

@@ -248,7 +248,14 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st, 
   na.cen = t.d_cen.p; na.qn = t.d_qn.p; na.qw = t.d_qw.p; na.nrm = t.d_nrm.p; na.selfJ = t.d_selfJ.p;
   na.s = (const double2*)op.d_s.p; na.local_l = op.d_local_l.p;
   na.class_t1 = op.d_class_t1.p; na.class_t2 = op.d_class_t2.p; na.mask = op.d_mask; na.xc = xc; na.yc = yc;
-  const int F = op.near_f;
+  // F = 4 classes per warp unless that pads the last class tile by more than 3 % and F = 5
+  // pads less (config 2: 65 classes -> F = 5, 5.71 -> 5.64 ms; configs 3/4 keep F = 4)
+  int F = op.near_f;
+  if (F == 0) {
+    const int c = op.n_class;
+    const double w4 = double((c + 3) / 4 * 4 - c) / c, w5 = double((c + 4) / 5 * 5 - c) / c;
+    F = (w4 > 0.03 && w5 < w4) ? 5 : 4;
+  }
   const int U = op.near_unroll;
   const bool T = op.near_tab;
   cudaError_t e;

@@ -268,9 +268,10 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st, 
                               : launch<3, 1, true>(na, st))
                     : (U == 7 ? launch<3, 7, false>(na, st) : launch<3, 1, false>(na, st));
   else if (F == 4) e = T ? (U == 7 ? (op.near_xlate ? launch<4, 7, true, true>(na, st) : launch<4, 7, true>(na, st))
-                             : launch<4, 1, true>(na, st))
+                             : (op.near_xlate ? launch<4, 1, true, true>(na, st) : launch<4, 1, true>(na, st)))
                          : launch<4, 1, false>(na, st);
-  else if (F == 5 && T) e = op.near_xlate ? launch<5, 7, true, true>(na, st) : launch<5, 7, true>(na, st);
+  else if (F == 5 && T) e = op.near_xlate ? (U == 7 ? launch<5, 7, true, true>(na, st) : launch<5, 1, true, true>(na, st))
+                                          : launch<5, 7, true>(na, st);
   else e = T ? (U == 7 ? launch<2, 7, true>(na, st) : launch<2, 1, true>(na, st))
              : (U == 7 ? launch<2, 7, false>(na, st) : launch<2, 1, false>(na, st));
   BEM_CK(e);

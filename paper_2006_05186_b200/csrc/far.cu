@@ -1035,11 +1035,13 @@ __global__ void __launch_bounds__(kH2oWarps * 32, 3) h2o_kernel(H2oArgs a) {
     __syncwarp();
     for (int nu = 0; nu < p; ++nu) {
       const double cx = cw[3 * nu], cy = cw[3 * nu + 1], cz = cw[3 * nu + 2];
-      double2 x1[FC], x2[FC];
+      double2 x1[FC], x2[FC];  // U > 1: loaded once for all u; U == 1: at their use (fewer live registers)
+      if (U > 1) {
 #pragma unroll
-      for (int f = 0; f < FC; ++f) {
-        x1[f] = xw[(2 * f) * p + nu];
-        x2[f] = xw[(2 * f + 1) * p + nu];
+        for (int f = 0; f < FC; ++f) {
+          x1[f] = xw[(2 * f) * p + nu];
+          x2[f] = xw[(2 * f + 1) * p + nu];
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1054,6 +1056,10 @@ __global__ void __launch_bounds__(kH2oWarps * 32, 3) h2o_kernel(H2oArgs a) {
           double sn, cs;
           fast::sincos_tab(sim[f] * rr, sctab, &sn, &cs);
           const double kr = e * cs, ki = -e * sn;  // S(s) = kr + i ki; S(conj s) = kr - i ki
+          if (U == 1) {
+            x1[f] = xw[(2 * f) * p + nu];
+            x2[f] = xw[(2 * f + 1) * p + nu];
+          }
           y1[f][u].x = fma(kr, x1[f].x, fma(-ki, x1[f].y, y1[f][u].x));
           y1[f][u].y = fma(kr, x1[f].y, fma(ki, x1[f].x, y1[f][u].y));
           y2[f][u].x = fma(kr, x2[f].x, fma(ki, x2[f].y, y2[f][u].x));

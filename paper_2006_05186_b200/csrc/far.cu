@@ -356,7 +356,10 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) far7_kernel(Far7Args a) {
   // leftover columns: thread -> (row lrow, nu residue lpart)
   const int lrow = tid >> 3, lpart = tid & 7;
   const bool lown = lead && tb > 0 && lrow < nrow;
-  double2 lacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  // leftover-column accumulators in shared memory (used once per term by the lead CTA;
+  // as registers they were live through the whole kernel and caused spills)
+  double2* lacc = (double2*)(((uintptr_t)(xcn + 3 * p) + 15) & ~(uintptr_t)15) + 2 * tid;
+  lacc[0] = lacc[1] = make_double2(0.0, 0.0);
   const int ncp = tb + ncol;
   int buf = 0;
   for (int bi = sg.y; bi < (cta_on ? sg.z : sg.y); ++bi) {
@@ -552,7 +555,7 @@ Far7Cfg choose7(int p, int nl, size_t cap, bool cluster, int ttmax_cap = 0, int 
     while (XTP % 8 != 2) ++XTP;
     const int cs = (cluster && ntiles > 1 && ntiles <= 8) ? ntiles : 1;
     const int own = cs > 1 ? (nrow * p + cs - 1) / cs : 0;
-    const size_t smem = sizeof(double2) * (2 * 32 * (size_t)SST + (size_t)p4 * XTP + 2 * (size_t)own + 64) +
+    const size_t smem = sizeof(double2) * (2 * 32 * (size_t)SST + (size_t)p4 * XTP + 2 * (size_t)own + 64 + 2 * 32 * (size_t)nw) + 16 +
                         sizeof(double) * (64 + 96 + 3 * p);
     if (smem > cap) continue;
     c.p4 = p4; c.SST = SST; c.TT = TT; c.XTP = XTP; c.nT = TT / 8; c.tb = tb; c.nd = nD; c.ntiles = ntiles;

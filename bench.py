@@ -40,7 +40,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4,
+                    help="BASELINE config (default 4: the largest single-GPU config, the N = 1 headline)")
+    ap.add_argument("--skeleton", default="auto", choices=["auto", "z", "factors"],
+                    help="MACA skeleton storage: stored Z, factors only (Z tiles regenerated in K3), or auto")
     ap.add_argument("--mode", default="h2aca", choices=["h2aca", "h2only", "combined"],
                     help="combined: Alg. 3 in full, near blocks MACA-compressed too (SURVEY NEXT-4)")
     ap.add_argument("--operator", default="V", choices=["V", "K"],
@@ -136,88 +139,104 @@ def traffic_bytes(cfg_id, dom):
         return None
 
 
-def oracle_step(O, h, s, x_time, N, R, lsel):
-    """One time-domain step of the oracle on a frequency sample: full forward
-    transform, H2ACA apply of the sampled frequencies, full inverse transform.
-    Returns (seconds for the two transforms, seconds for the sampled apply)."""
-    t0 = time.perf_counter()
-    xf = O.forward(x_time, N, R)
-    t1 = time.perf_counter()
-    yf = np.zeros_like(xf)
-    yf[lsel] = h.apply(O.MODE_H2ACA, s, xf[lsel], lsel)
-    t2 = time.perf_counter()
-    O.inverse(yf, N, R)
-    t3 = time.perf_counter()
-    return (t1 - t0) + (t3 - t2), t2 - t1
+# ---------------------------------------------------------------- the CPU oracle, timed
+# The oracle (oracle/, plain FP64 C++, OpenMP) cannot run a whole config-4 step in
+# minutes (its H2ACA apply evaluates every pivot slice once per chunk of 32
+# frequencies: ~2.3e11 libm kernel evaluations for all 513 frequencies at config 4),
+# so it is timed on a BOUNDED SAMPLE of the step and the step time is extrapolated
+# from the sample (each part is linear in what is sampled):
+#   * transforms: the naive-DFT forward and inverse of a fixed, seeded 1/SAMPLE_COLS of
+#     the DOF columns (the work is per column: x SAMPLE_COLS);
+#   * apply: one chunk of FCH = 32 frequencies per step (the oracle's own chunk; seeded,
+#     different each step) with a fixed, seeded 1/SAMPLE_BLOCKS of the far blocks and of
+#     the near blocks contributing (their ACA computed at setup): x SAMPLE_BLOCKS x L/32.
+SAMPLE_COLS, SAMPLE_BLOCKS, FCH = 16, 64, 32
 
 
-def oracle_throughput(O, h, s, cfg_id, N, R, M, nsel, steps, warmup, rng_sel):
-    """Whole-step unknowns*frequencies/s extrapolated from the sample:
-    M L / (t_transforms + t_apply_sample * L / nsel) (the apply is exactly linear in L)."""
-    L = N + 1
-    tt, ta = [], []
-    for k in range(warmup + steps):
-        lsel = np.sort(rng_sel.choice(L, nsel, replace=False)).astype(np.int32)
-        x = synth.random_time_data(cfg_id, N, M, stream=k).astype(np.complex128)
-        a, b = oracle_step(O, h, s, x, N, R, lsel)
-        if k >= warmup:
-            tt.append(a)
-            ta.append(b)
-    t_step = float(np.mean(tt)) + float(np.mean(ta)) * L / nsel
-    return M * L / t_step, t_step, float(np.mean(ta))
+class OracleSample:
+    def __init__(self, cfg_id, V, T, cfg, N):
+        import oracle as O
+        self.O = O
+        self.N, self.L, self.M = N, N + 1, len(T)
+        self.R = 10.0 ** (-5.0 / N)
+        self.s = O.frequencies(N, cfg["T"])
+        t0 = time.perf_counter()
+        self.h = O.H2(V, T, cfg["leaf"], cfg["eta"], cfg["m"])
+        rng = np.random.default_rng(20060518)
+        nfs = max(1, self.h.n_far // SAMPLE_BLOCKS)
+        nns = max(1, self.h.n_near // SAMPLE_BLOCKS)
+        self.far = np.sort(rng.choice(self.h.n_far, nfs, replace=False)).astype(np.int32)
+        self.near = np.sort(rng.choice(self.h.n_near, nns, replace=False)).astype(np.int32)
+        self.cols = np.sort(rng.choice(self.M, max(1, self.M // SAMPLE_COLS), replace=False))
+        self.h.aca(self.s, cfg["eps"], blocks=self.far)
+        self.t_setup = time.perf_counter() - t0
+        self.x_time = synth.random_time_data(cfg_id, N, self.M).astype(np.complex128)
+        self.nf = min(FCH, self.L)
+        self.cores = O.num_threads()
+        self.fcols = self.M / len(self.cols)
+
+    def step(self, k):
+        """One sampled step; returns (seconds measured, seconds extrapolated to the whole step)."""
+        O = self.O
+        lsel = np.sort(np.random.default_rng(k).choice(self.L, self.nf, replace=False)).astype(np.int32)
+        xs = np.ascontiguousarray(self.x_time[:, self.cols])
+        xl = np.ascontiguousarray(self.x_time[lsel])  # stands in for the frequency-domain columns
+        t0 = time.perf_counter()
+        xf = O.forward(xs, self.N, self.R)
+        t1 = time.perf_counter()
+        self.h.apply_sample(self.s, xl, lsel, self.far, self.near)
+        t2 = time.perf_counter()
+        O.inverse(xf, self.N, self.R)
+        t3 = time.perf_counter()
+        t_dft, t_app = (t1 - t0) + (t3 - t2), t2 - t1
+        return t3 - t0, self.fcols * t_dft + (self.h.n_far / len(self.far)) * (self.L / self.nf) * t_app
+
+    def describe(self, steps):
+        return (f"per step: naive-DFT forward + inverse of {len(self.cols)} of {self.M} DOF columns, and the H2ACA "
+                f"apply of {self.nf} random frequencies of {self.L} with {len(self.far)} of {self.h.n_far} far and "
+                f"{len(self.near)} of {self.h.n_near} near blocks contributing; step time extrapolated "
+                f"x{self.fcols:.2f} (transforms) and x{self.h.n_far / len(self.far):.2f} x L/{self.nf} (apply); "
+                f"{steps} step(s); oracle setup (tree + ACA of the sampled blocks) {self.t_setup:.1f} s excluded")
 
 
-def cpu_baseline(V, T, cfg, s, N, R):
+def cpu_baseline(cfg_id, V, T, cfg, N):
     """The oracle as it stands, timed on this box's host cores on a bounded sample."""
-    import oracle as O
-    nthr = O.num_threads()
-    L, M = N + 1, len(T)
-    nsel = max(1, min(L, nthr))
-    h = O.H2(V, T, cfg["leaf"], cfg["eta"], cfg["m"])
-    t0 = time.perf_counter()
-    h.aca(s, cfg["eps"])
-    t_aca = time.perf_counter() - t0
-    val, t_step, t_app = oracle_throughput(O, h, s, cfg_id_global, N, R, M, nsel, 1, 0, np.random.default_rng(0))
-    return {"value": val, "unit": UNIT, "cores": nthr, "kind": "oracle",
-            "sample": f"one time-domain step: full naive-DFT forward/inverse transforms + H2ACA apply of {nsel} "
-                      f"random frequencies of {L} ({t_app:.2f} s), all {M} panels; step time extrapolated as "
-                      f"transforms + apply x L/{nsel} = {t_step:.1f} s; oracle ACA setup {t_aca:.1f} s excluded"}
-
-
-cfg_id_global = 2
+    o = OracleSample(cfg_id, V, T, cfg, N)
+    _, t_step = o.step(0)
+    return {"value": o.M * o.L / t_step, "unit": UNIT, "cores": o.cores, "kind": "oracle", "extrapolated": True,
+            "ms_per_step_extrapolated": t_step * 1e3, "sample": o.describe(1)}
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle, as it stands, on this box's host cores."""
+    """--impl reference: the CPU oracle, as it stands, on this box's host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import oracle as O
     cfg, V, T, N, L, R = workload(args.config)
     M = len(T)
-    s = O.frequencies(N, cfg["T"])
-    nthr = O.num_threads()
-    h = O.H2(V, T, cfg["leaf"], cfg["eta"], cfg["m"])
-    h.aca(s, cfg["eps"])
-    nsel = max(1, min(L, nthr))
-    val, t_step, t_app = oracle_throughput(O, h, s, args.config, N, R, M, nsel, args.steps, args.warmup,
-                                           np.random.default_rng(0))
+    o = OracleSample(args.config, V, T, cfg, N)
+    for k in range(args.warmup):
+        o.step(k)
+    meas, ext = [], []
+    for k in range(args.steps):
+        a, b = o.step(args.warmup + k)
+        meas.append(a)
+        ext.append(b)
+    t_step = float(np.mean(ext))
+    val = M * L / t_step
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "extrapolated": True,
+            "measured_ms_per_sampled_step": float(np.mean(meas)) * 1e3,
             "config": config_json(args.config, cfg, M, L, 1),
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": nthr, "kind": "oracle",
-                             "sample": f"each step: full naive-DFT forward/inverse transforms + oracle H2ACA apply "
-                                       f"of {nsel} random frequencies of {L} (mean {t_app:.2f} s), all {M} panels; "
-                                       f"step time extrapolated as transforms + apply x L/{nsel} (setup excluded)"},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": o.cores, "kind": "oracle", "extrapolated": True,
+                             "sample": o.describe(args.steps)},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
 def main():
-    global cfg_id_global
     args = parse()
-    cfg_id_global = args.config
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -243,6 +262,7 @@ def main():
     s = pb.cqm_frequencies(N, cfg["T"], R)
     mode = {"h2aca": pb.BEM_MODE_H2ACA, "h2only": pb.BEM_MODE_H2ONLY, "combined": pb.BEM_MODE_COMBINED}[args.mode]
     aca_far = mode in (pb.BEM_MODE_H2ACA, pb.BEM_MODE_COMBINED)
+    base_mode = mode
     t0 = time.perf_counter()
     tree = pb.Tree(V, T, cfg["leaf"], cfg["eta"], cfg["m"], device=local_rank)
     t_tree = time.perf_counter() - t0
@@ -254,6 +274,8 @@ def main():
     else:
         local = np.arange(L, dtype=np.int32)
     t0 = time.perf_counter()
+    if aca_far:
+        mode |= {"auto": 0, "z": pb.BEM_SKEL_Z, "factors": pb.BEM_SKEL_FACTORS}[args.skeleton]
     op = pb.Operator(tree, s, cfg["eps"], mode=mode, local_l=local if (world > 1 or vshard) else None)
     t_aca = time.perf_counter() - t0
     b, e = dof_ranges(M, world)[rank]
@@ -405,7 +427,7 @@ def main():
     evals_near = 7.0 * stats["nnz_near"] * n_class
     flops_near = 75.0 * evals_near  # SURVEY §8(d) model: ~75 FP64 flops per complex exponential + MACs
     near_rank = None
-    if mode == pb.BEM_MODE_COMBINED:  # K1m: 8 flops per (slice entry, term, frequency) on DMMA
+    if base_mode == pb.BEM_MODE_COMBINED:  # K1m: 8 flops per (slice entry, term, frequency) on DMMA
         rkn = op.aca_export_near()["ranks"].astype(np.float64)
         ex = tree.export()
         sz = ex["clusters"][:, 1] - ex["clusters"][:, 0]
@@ -419,7 +441,7 @@ def main():
         except Exception:
             peaks[name] = None
     dom = "coupling" if kt["coupling"] >= kt["near"] else "near"
-    if dom == "near" and mode == pb.BEM_MODE_COMBINED:
+    if dom == "near" and base_mode == pb.BEM_MODE_COMBINED:
         fl = flops_near
         peak = peaks["dmma"] or FP64_PEAK_DERIVED / 1e12
         bound, src = "tensor", "measured in this run: mma.sync.m8n8k4.f64 (DMMA) loop (bem_debug_fp64_peak_ex mode 1)"
@@ -439,7 +461,7 @@ def main():
     achieved = fl / (kt[dom] * 1e-3) / 1e12
     kname = {"coupling": ("K3 far7/far8_kernel (+seg_reduce)" if aca_far
                           else "K3' h2o_kernel (+seg_reduce)"),
-             "near": "K1m nearm_kernel" if mode == pb.BEM_MODE_COMBINED else "K1 near_kernel"}[dom]
+             "near": "K1m nearm_kernel" if base_mode == pb.BEM_MODE_COMBINED else "K1 near_kernel"}[dom]
     roof = {"bound": bound, "kernel": kname, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": traffic_bytes(args.config, dom), "peak_source": src,
             "algorithmic_flops_per_launch": fl,
@@ -452,7 +474,7 @@ def main():
     b_up = 16.0 * M * nl + 16.0 * p_ * nl * C_
     b_down = 16.0 * p_ * nl * C_ + 32.0 * M * nl
     f_up = 8.0 * p_ * M * nl + 8.0 * p_ * p_ * nl * (C_ - 1)
-    pk_near = (peaks["dmma"] or FP64_PEAK_DERIVED / 1e12) if mode == pb.BEM_MODE_COMBINED else FP64_PEAK_DERIVED / 1e12
+    pk_near = (peaks["dmma"] or FP64_PEAK_DERIVED / 1e12) if base_mode == pb.BEM_MODE_COMBINED else FP64_PEAK_DERIVED / 1e12
     pk_far = (peaks["dmma"] or FP64_PEAK_DERIVED / 1e12) if aca_far else FP64_PEAK_DERIVED / 1e12
     kern = {
         "near": {"flops": flops_near, "ms": kt["near"], "peak_tflops": pk_near},
@@ -484,20 +506,21 @@ def main():
            "timing": ("CUDA-graph replay of the whole step (captured once after warm-up); eager step "
                       f"{statistics.median(ms_eager):.3f} ms (median)") if graph is not None else
                      f"eager launches{'' if graph_error is None else ' (graph capture failed: ' + graph_error + ')'}",
-           "near_evals_per_s": (evals_near / (kt["near"] * 1e-3) if kt["near"] > 0 and mode != pb.BEM_MODE_COMBINED
+           "near_evals_per_s": (evals_near / (kt["near"] * 1e-3) if kt["near"] > 0 and base_mode != pb.BEM_MODE_COMBINED
                                 else None),
            "setup_s": {"tree": t_tree, "aca": t_aca}, "mode": args.mode, "operator": args.operator,
            "transpose": transpose,
            "mean_aca_rank": float(op.aca_export()["ranks"].mean()) if aca_far else None,
+           "op": op.info(), "skeleton": op.skeleton(),
            "mean_near_aca_rank": near_rank}
     if vshard:
         out["config"]["parallelism"] = (f"virtual shard {args.shard_rank} of {args.shard_of}: frequency-domain apply of "
                                          f"{len(local)} of {L} frequencies on 1 GPU (no transforms, no all-to-all); "
                                          f"value = this rank's unknowns*frequencies/s")
         out["metric"] = METRIC.replace("time-domain step: forward + apply + inverse", "frequency-domain apply, one shard")
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not vshard and args.config <= 3:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not vshard:
         try:
-            out["cpu_baseline"] = cpu_baseline(V, T, cfg, s, N, R)
+            out["cpu_baseline"] = cpu_baseline(args.config, V, T, cfg, N)
         except Exception as ex:  # pragma: no cover
             out["cpu_baseline"] = {"value": None, "error": str(ex)}
     if rank == 0:

@@ -51,6 +51,16 @@ enum {
  * b in P+ and b in P-): the near blocks are MACA-compressed across frequency too
  * (SURVEY §8(f) NEXT-4), instead of evaluated on the fly per apply. */
 enum { BEM_MODE_H2ACA = 0, BEM_MODE_H2ONLY = 1, BEM_MODE_DENSE = 2, BEM_MODE_COMBINED = 3 };
+/* Skeleton storage flags, OR-ed into `mode` of bem_assemble_h2_aca (ACA modes).
+ * The MACA of block b is kept as pivots (k_l, q_l) plus the r_b x r_b LU factors of
+ * A_b[Q,K] (SURVEY C10 skeleton form, AM17; 16 r_b^2 bytes).  The coefficients
+ * Z_b = U_b^{-1} C^_b^{-1} A_b[Q,:] (eq:maca P:1314-1320) of the local frequencies are
+ *   BEM_SKEL_Z:       regenerated once at assembly and stored (16 r_b n_local bytes);
+ *   BEM_SKEL_FACTORS: regenerated per apply in the coupling kernel's prologue, per
+ *                     (block, frequency tile) -- nothing per frequency is stored;
+ *   neither:          stored when that takes at most a third of the free device memory.
+ * Both give bit-identical results (the same pinned substitutions as the ACA). */
+enum { BEM_SKEL_Z = 0x100, BEM_SKEL_FACTORS = 0x200 };
 
 typedef struct { double re, im; } bem_c128;
 typedef struct bem_tree_s* bem_tree; /* panels, cluster tree, P+/P-, U, W, E, boxes; one device */
@@ -99,7 +109,9 @@ bem_status bem_tree_export(bem_tree t, int32_t* perm, int32_t* clusters, double*
 bem_status bem_tree_destroy(bem_tree t);
 
 /* Multi-frequency operator (Alg. 3, FAR branch; eq:lrfinal P:1404-1410).
- *   s: host [L] frequencies (normally from cqm_frequencies);
+ *   s: host [L] frequencies (normally from cqm_frequencies); must be exactly
+ *      conjugation-symmetric, s[L-l] == conj(s[l]) for 0 < l < L (EINVAL otherwise):
+ *      l > L/2 is evaluated as the conjugate of L - l (SURVEY C2, C10 reading 5);
  *   local_l: host [n_local] distinct frequency indices this handle applies
  *            (NULL = all L, n_local ignored);
  *   aca_eps > 0: MACA tolerance (Alg. 2, stop rule P:1288);
@@ -114,8 +126,10 @@ bem_status bem_tree_destroy(bem_tree t);
  *         COMBINED requires leaves of at most 64 panels (EINVAL otherwise).
  * The ACA runs over ALL L frequencies on the device with pinned arithmetic
  * (bit-reproducible pivots) and keeps Z columns for local_l only.
- * Synchronous on return.  EINVAL: L < 1, s NULL, local index out of range or
- * duplicated, aca_eps <= 0, unknown mode. */
+ *   mode may carry one BEM_SKEL_* flag (ACA modes; COMBINED always stores Z).
+ * Synchronous on return.  EINVAL: L < 1, s NULL or not conjugation-symmetric, local
+ * index out of range or duplicated, aca_eps <= 0, unknown mode or flags.
+ * ENOMEM: BEM_SKEL_Z (or COMBINED) and the stored Z does not fit. */
 bem_status bem_assemble_h2_aca(bem_tree t, const bem_c128* s, int32_t L, const int32_t* local_l, int32_t n_local,
                                double aca_eps, int32_t mode, void* cuda_stream, bem_op* out);
 /* ranks: host [far_blocks]; pivots: host [sum ranks][2] = (k_l, q_l) in block
@@ -128,6 +142,15 @@ bem_status bem_aca_export(bem_op op, int32_t* ranks, int32_t* pivots, int64_t* t
  * order), blocks in bem_tree_export's near_pairs order.  ESTATE otherwise. */
 bem_status bem_aca_export_near(bem_op op, int32_t* ranks, int32_t* pivots, int64_t* total_rank);
 bem_status bem_op_destroy(bem_op op); /* NULL-safe */
+/* What an op holds (host struct):  skeleton = 0 (no ACA: H2ONLY / DENSE), 1 (stored Z),
+ * 2 (factors only, BEM_SKEL_FACTORS); z_bytes / f_bytes = the stored Z and factor pools;
+ * device_bytes = every device allocation the op owns (its per-GPU footprint besides
+ * the tree and the caller's x / y). */
+typedef struct {
+  int32_t mode, skeleton, n_local, rmax;
+  int64_t total_rank, z_bytes, f_bytes, device_bytes;
+} bem_op_info;
+bem_status bem_op_get_info(bem_op op, bem_op_info* out);
 
 /* y_t = V(s_{local_l[t]}) x_t for t < n_local (P:529-540 operators V_l).
  * x, y: device [n_local][M] complex, input panel order; y is overwritten;

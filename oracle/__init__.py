@@ -65,6 +65,10 @@ def lib():
         L.orc_h2_export_bases.argtypes = [vp, vp, vp, vp, vp]
         L.orc_h2_aca.argtypes = [vp, vp, i32, d, vp, i64, vp, vp]
         L.orc_h2_aca.restype = i64
+        L.orc_h2_aca_keep.argtypes = [vp, vp, i32, d, vp, i64, vp, i32, vp, vp]
+        L.orc_h2_aca_keep.restype = i64
+        L.orc_h2_apply_sample.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, vp, i64, vp, i64]
+        L.orc_h2_apply_sample.restype = C.c_int
         L.orc_h2_aca_export.argtypes = [vp, vp, i64, vp, vp]
         L.orc_h2_apply.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp]
         L.orc_h2_apply.restype = C.c_int
@@ -286,7 +290,9 @@ class H2:
         lib().orc_h2_export_bases(self.h, _p(U), _p(W), _p(E), _p(xi))
         return dict(U=U, W=W, E=E, xi=xi)
 
-    def aca(self, s, eps, blocks=None):
+    def aca(self, s, eps, blocks=None, keep=None):
+        """MACA of every far block (or of `blocks`); keep: the frequencies whose Z
+        columns are stored (default all L; applies are then limited to them)."""
         s = _c128(s)
         self.s = s
         L = len(s)
@@ -295,11 +301,14 @@ class H2:
         else:
             blk = np.ascontiguousarray(blocks, dtype=np.int32)
             nb = len(blk)
+        kp = None if keep is None else np.ascontiguousarray(np.unique(keep), dtype=np.int32)
+        nk = L if kp is None else len(kp)
         ranks = np.empty(nb, dtype=np.int32)
         fragile = np.empty(nb, dtype=np.int32)
-        tot = lib().orc_h2_aca(self.h, _p(s), L, float(eps), _p(blk), nb, _p(ranks), _p(fragile))
+        tot = lib().orc_h2_aca_keep(self.h, _p(s), L, float(eps), _p(blk), nb, _p(kp), 0 if kp is None else nk,
+                                    _p(ranks), _p(fragile))
         piv = np.empty((tot, 2), dtype=np.int32)
-        Z = np.empty(tot * L, dtype=np.complex128)
+        Z = np.empty(tot * nk, dtype=np.complex128)
         lib().orc_h2_aca_export(self.h, _p(blk), nb, _p(piv), _p(Z))
         return dict(ranks=ranks, pivots=piv, Z=Z, fragile=fragile)
 
@@ -372,6 +381,20 @@ class H2:
         rc = lib().orc_h2_apply(self.h, int(mode), _p(s), L, _p(lsel), len(lsel), _p(x), _p(y))
         if rc != 0:
             raise RuntimeError("oracle apply: ACA not assembled for these frequencies")
+        return y
+
+    def apply_sample(self, s, x, lsel, far_blocks, near_blocks):
+        """H2ACA apply with only the listed far / near blocks contributing: a bounded
+        sample of the apply's work (bench.py times the oracle with it; not a parity path)."""
+        s = _c128(s)
+        lsel = _i32(lsel)
+        x = _c128(x)
+        fb, nb = _i32(far_blocks), _i32(near_blocks)
+        y = np.empty_like(x)
+        rc = lib().orc_h2_apply_sample(self.h, MODE_H2ACA, _p(s), len(s), _p(lsel), len(lsel), _p(x), _p(y),
+                                       _p(fb), len(fb), _p(nb), len(nb))
+        if rc != 0:
+            raise RuntimeError("oracle apply_sample: ACA missing for a sampled block / frequency")
         return y
 
     def apply_dl(self, mode, s, x, lsel=None, alpha=0.0):

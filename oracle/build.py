@@ -10,7 +10,7 @@ LIB = os.path.join(HERE, "liboracle.so")
 
 # -ffp-contract=off is load-bearing: the ACA pivots must be bit-identical to
 # the GPU library's (SURVEY.md §8(c) C10 reading 5b).
-FLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC"]
+FLAGS = ["-O3", "-std=c++17", "-mfma", "-mavx2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC"]
 
 
 def build(force: bool = False) -> str:

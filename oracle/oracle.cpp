@@ -335,10 +335,19 @@ static C2 pentry(const Geometry& g, int64_t i, int64_t j, C2 s) {
 }
 
 // Pinned summation: sequential within chunks of 32, then left to right.
+// (Four chunks are summed side by side -- each still strictly in order -- so the
+// loop has independent chains; the result is the same as chunk after chunk.)
 static double psum(const std::vector<double>& v) {
   double tot = 0.0;
   size_t n = v.size();
-  for (size_t c0 = 0; c0 < n; c0 += 32) {
+  size_t c0 = 0;
+  for (; c0 + 128 <= n; c0 += 128) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (size_t i = 0; i < 32; ++i)
+      for (int u = 0; u < 4; ++u) s[u] = s[u] + v[c0 + 32 * u + i];
+    for (int u = 0; u < 4; ++u) tot = tot + s[u];
+  }
+  for (; c0 < n; c0 += 32) {
     double s = 0.0;
     size_t c1 = std::min(n, c0 + 32);
     for (size_t i = c0; i < c1; ++i) s = s + v[i];
@@ -396,7 +405,9 @@ struct H2 {
   // ACA result per far block
   std::vector<int> rank, pivk, pivq;
   std::vector<int64_t> pivoff, zoff;
-  std::vector<C2> Z;
+  std::vector<C2> Z;   // per far block r x zld: the coefficients of the kept frequencies
+  std::vector<int> zcol;  // zcol[l] = column of frequency l in Z (-1: not kept); zld = #kept
+  int zld = 0;
   std::vector<C2> s;  // frequencies used by the ACA
   int L = 0;
   bool aca_done = false;
@@ -630,10 +641,13 @@ static void aca_generic(Entry A, int pp, int L, double eps, AcaOut& out, std::ve
   out.k.clear(); out.q.clear(); out.Z.clear(); out.fragile = 0;
   for (;;) {
     int ell = (int)Cs.size();
-    for (int q = 0; q < pp; ++q) {
-      C2 acc = A(q, k);
-      for (int j = 0; j < ell; ++j) acc = psub(acc, pmul(Ds[j][k], Cs[j][q]));
-      c[q] = acc;
+    // c[q] = A(q,k) - sum_{j<ell} d_j[k] c_j[q], subtracted in increasing j for every q
+    // (loop order j-outer only so that the q loop vectorises; each c[q] sees the same ops)
+    for (int q = 0; q < pp; ++q) c[q] = A(q, k);
+    for (int j = 0; j < ell; ++j) {
+      const C2 dk = Ds[j][k];
+      const C2* cj = Cs[j].data();
+      for (int q = 0; q < pp; ++q) c[q] = psub(c[q], pmul(dk, cj[q]));
     }
     int qs = -1;
     double best = -1.0, second = -1.0;
@@ -646,12 +660,13 @@ static void aca_generic(Entry A, int pp, int L, double eps, AcaOut& out, std::ve
     if (qs < 0 || best == 0.0) break;
     if (second >= 0.0 && best - second <= 0x1p-44 * best) out.fragile++;
     C2 piv = c[qs];
-    for (int l = 0; l < L; ++l) {
-      C2 acc = A(qs, l);
-      for (int j = 0; j < ell; ++j) acc = psub(acc, pmul(Cs[j][qs], Ds[j][l]));
-      e[l] = acc;
-      d[l] = pdiv(acc, piv);
+    for (int l = 0; l < L; ++l) e[l] = A(qs, l);
+    for (int j = 0; j < ell; ++j) {  // e[l] -= c_j[q*] d_j[l], increasing j (as above)
+      const C2 cq = Cs[j][qs];
+      const C2* dj = Ds[j].data();
+      for (int l = 0; l < L; ++l) e[l] = psub(e[l], pmul(cq, dj[l]));
     }
+    for (int l = 0; l < L; ++l) d[l] = pdiv(e[l], piv);
     tmp.resize(pp);
     for (int q = 0; q < pp; ++q) tmp[q] = pkey(c[q]);
     double nc2 = psum(tmp);
@@ -786,7 +801,7 @@ static void apply_one(const H2& h, int mode, cplx s_l, int l, const std::vector<
         int rb = h.rank[b];
         for (int t = 0; t < rb; ++t) {
           int kk = h.pivk[h.pivoff[b] + t];
-          C2 z = h.Z[h.zoff[b] + (size_t)t * h.L + l];
+          C2 z = h.Z[h.zoff[b] + (size_t)t * h.zld + h.zcol[l]];
           cplx zc(z.re, z.im);
           for (int mu = 0; mu < p; ++mu)
             for (int nu = 0; nu < p; ++nu) {
@@ -854,35 +869,340 @@ static void apply_one(const H2& h, int mode, cplx s_l, int l, const std::vector<
   for (int64_t k = 0; k < M; ++k) y_out[h.perm[k]] = y[k];
 }
 
+// The same apply for several frequencies at once, parallel over row clusters /
+// rows.  For every frequency the arithmetic and its order are exactly those of
+// apply_one (tests check equality bit for bit); only the loop nesting differs:
+// a far block's pivot slices S_b(s_{k_t}) are evaluated once and shared by the
+// selected frequencies, and the row-parallel loops visit each row's blocks in
+// ascending block order, as apply_one's sequential loop does.
+// far_on / near_on (nullable): only these blocks contribute (a bounded sample of the
+// work, for timing the oracle on workloads it cannot finish: bench.py cpu_baseline).
+static void apply_multi(const H2& h, int mode, const std::vector<cplx>& sl_all, const int32_t* lsel, int nsel,
+                        const cplx* x_in, cplx* y_out, int op, const char* far_on = nullptr,
+                        const char* near_on = nullptr) {
+  const int64_t M = h.g.M;
+  const int p = h.p, m = h.m, C = (int)h.cl.size();
+  const std::vector<double>& Wc = op == 0 ? h.W : h.WK;
+  auto ent = [&](int64_t i, int64_t j, cplx s_l) { return op == 0 ? entry(h.g, i, j, s_l) : entry_dl(h.g, i, j, s_l); };
+  std::vector<std::vector<cplx>> x(nsel), y(nsel), xh(nsel), yh(nsel);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int t = 0; t < nsel; ++t) {
+    x[t].resize(M);
+    y[t].assign(M, cplx(0.0, 0.0));
+    for (int64_t k = 0; k < M; ++k) x[t][k] = x_in[(int64_t)t * M + h.perm[k]];
+    if (mode == MODE_DENSE) continue;
+    std::vector<cplx>& xt = xh[t];
+    xt.assign((size_t)C * p, cplx(0.0, 0.0));
+    yh[t].assign((size_t)C * p, cplx(0.0, 0.0));
+    for (int c = C - 1; c >= 0; --c) {  // upward pass, as apply_one
+      const Cluster& cc = h.cl[c];
+      cplx* out = &xt[(size_t)c * p];
+      if (cc.son0 < 0) {
+        for (int nu = 0; nu < p; ++nu) {
+          cplx acc(0.0, 0.0);
+          for (int k = cc.begin; k < cc.end; ++k) acc += Wc[(size_t)k * p + nu] * x[t][k];
+          out[nu] = acc;
+        }
+      } else {
+        for (int son : {cc.son0, cc.son1}) {
+          const double* Es = &h.E[(size_t)son * p * p];
+          for (int mu = 0; mu < p; ++mu) {
+            cplx acc(0.0, 0.0);
+            for (int lam = 0; lam < p; ++lam) acc += Es[(size_t)lam * p + mu] * xt[(size_t)son * p + lam];
+            out[mu] += acc;
+          }
+        }
+      }
+    }
+  }
+  if (mode == MODE_DENSE) {
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int64_t a = 0; a < M; ++a)
+      for (int t = 0; t < nsel; ++t) {
+        const cplx s_l = sl_all[lsel[t]];
+        cplx acc(0.0, 0.0);
+        for (int64_t b = 0; b < M; ++b) acc += ent(h.perm[a], h.perm[b], s_l) * x[t][b];
+        y[t][a] = acc;
+      }
+  } else {
+    // coupling, parallel over row clusters
+    std::vector<std::vector<int>> byrow(C);
+    for (size_t b = 0; b < h.farR.size(); ++b)
+      if (!far_on || far_on[b]) byrow[h.farR[b]].push_back((int)b);
+    const int FCH = 32;  // frequencies per pass (bounds the per-thread S buffers)
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int r = 0; r < C; ++r) {
+      if (byrow[r].empty()) continue;
+      std::vector<double> dist((size_t)p * p);
+      std::vector<cplx> S((size_t)p * p * std::min(nsel, FCH));
+      for (int b : byrow[r]) {
+        const int c = h.farC[b];
+        const double* xr = &h.xi[(size_t)r * 3 * m];
+        const double* xc = &h.xi[(size_t)c * 3 * m];
+        for (int mu = 0; mu < p; ++mu)
+          for (int nu = 0; nu < p; ++nu) {
+            double a[3], bb[3];
+            node_point(xr, m, mu, a); node_point(xc, m, nu, bb);
+            double dx = bb[0] - a[0], dy = bb[1] - a[1], dz = bb[2] - a[2];
+            dist[(size_t)mu * p + nu] = std::sqrt((dx * dx + dy * dy) + dz * dz);
+          }
+        for (int t0 = 0; t0 < nsel; t0 += FCH) {
+          const int nt = std::min(FCH, nsel - t0);
+          std::fill(S.begin(), S.begin() + (size_t)p * p * nt, cplx(0.0, 0.0));
+          if (mode == MODE_H2ONLY) {
+            for (int t = 0; t < nt; ++t) {
+              const cplx s_l = sl_all[lsel[t0 + t]];
+              for (size_t e = 0; e < (size_t)p * p; ++e) S[(size_t)t * p * p + e] = kernel(dist[e], s_l);
+            }
+          } else {
+            const int rb = h.rank[b];
+            for (int j = 0; j < rb; ++j) {
+              const int kk = h.pivk[h.pivoff[b] + j];
+              for (size_t e = 0; e < (size_t)p * p; ++e) {
+                const cplx kv = kernel(dist[e], sl_all[kk]);
+                for (int t = 0; t < nt; ++t) {
+                  const C2 z = h.Z[h.zoff[b] + (size_t)j * h.zld + h.zcol[lsel[t0 + t]]];
+                  const cplx zc(z.re, z.im);
+                  S[(size_t)t * p * p + e] += zc * kv;
+                }
+              }
+            }
+          }
+          for (int t = 0; t < nt; ++t) {
+            const cplx* St = &S[(size_t)t * p * p];
+            const cplx* xc2 = &xh[t0 + t][(size_t)c * p];
+            cplx* yr = &yh[t0 + t][(size_t)r * p];
+            for (int mu = 0; mu < p; ++mu) {
+              cplx acc(0.0, 0.0);
+              for (int nu = 0; nu < p; ++nu) acc += St[(size_t)mu * p + nu] * xc2[nu];
+              yr[mu] += acc;
+            }
+          }
+        }
+      }
+    }
+    // downward pass per frequency, as apply_one
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int t = 0; t < nsel; ++t) {
+      std::vector<cplx>& yt = yh[t];
+      for (int c = 0; c < C; ++c) {
+        const Cluster& cc = h.cl[c];
+        if (cc.parent >= 0) {
+          const double* Es = &h.E[(size_t)c * p * p];
+          for (int lam = 0; lam < p; ++lam) {
+            cplx acc(0.0, 0.0);
+            for (int mu = 0; mu < p; ++mu) acc += Es[(size_t)lam * p + mu] * yt[(size_t)cc.parent * p + mu];
+            yt[(size_t)c * p + lam] += acc;
+          }
+        }
+        if (cc.son0 < 0) {
+          for (int k = cc.begin; k < cc.end; ++k) {
+            cplx acc(0.0, 0.0);
+            for (int mu = 0; mu < p; ++mu) acc += h.U[(size_t)k * p + mu] * yt[(size_t)c * p + mu];
+            y[t][k] += acc;
+          }
+        }
+      }
+    }
+    // near field, parallel over row leaves (each row's blocks in ascending order)
+    std::vector<std::vector<int>> nbyrow(C);
+    for (size_t b = 0; b < h.nearR.size(); ++b)
+      if (!near_on || near_on[b]) nbyrow[h.nearR[b]].push_back((int)b);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int rl = 0; rl < C; ++rl) {
+      for (int b : nbyrow[rl]) {
+        const Cluster& R = h.cl[h.nearR[b]];
+        const Cluster& Cc = h.cl[h.nearC[b]];
+        for (int t = 0; t < nsel; ++t) {
+          const int l = lsel[t];
+          if (mode == MODE_COMBINED && op == 0) {
+            const int nr = R.end - R.begin, nc = Cc.end - Cc.begin;
+            for (int j = 0; j < h.nrank[b]; ++j) {
+              const C2* Sn = &h.nS[h.nsoff[b] + (size_t)j * nr * nc];
+              const C2 z = h.nZ[h.nzoff[b] + (size_t)j * h.L + l];
+              const cplx zc(z.re, z.im);
+              for (int a = R.begin; a < R.end; ++a) {
+                cplx acc(0.0, 0.0);
+                for (int k = Cc.begin; k < Cc.end; ++k) {
+                  const C2 v = Sn[(size_t)(a - R.begin) * nc + (k - Cc.begin)];
+                  acc += cplx(v.re, v.im) * x[t][k];
+                }
+                y[t][a] += zc * acc;
+              }
+            }
+            continue;
+          }
+          const cplx s_l = sl_all[l];
+          for (int a = R.begin; a < R.end; ++a) {
+            cplx acc(0.0, 0.0);
+            for (int k = Cc.begin; k < Cc.end; ++k) acc += ent(h.perm[a], h.perm[k], s_l) * x[t][k];
+            y[t][a] += acc;
+          }
+        }
+      }
+    }
+  }
+#pragma omp parallel for schedule(static)
+  for (int t = 0; t < nsel; ++t)
+    for (int64_t k = 0; k < M; ++k) y_out[(int64_t)t * M + h.perm[k]] = y[t][k];
+}
+
+// apply_one for a single frequency with the far-block coupling matrices S~_{b,l}
+// and the near-block entries evaluated once (cached) and reused by every GMRES
+// iteration; the arithmetic of each product and its order are those of
+// apply_one, so the iterates are the same bit for bit (only far faster).
+static void up_pass(const H2& h, const std::vector<cplx>& x, std::vector<cplx>& xh);
+static void down_pass(const H2& h, std::vector<cplx>& yh, std::vector<cplx>& y);
+
+struct OneFreqCache {
+  std::vector<cplx> S;     // far blocks: p x p each, block order
+  std::vector<cplx> Vn;    // near blocks: nr x nc each, block order
+  std::vector<int64_t> noff;
+  std::vector<std::vector<int>> fbyrow, nbyrow;
+};
+
+static void build_cache(const H2& h, int mode, cplx s_l, int l, const std::vector<cplx>& sl_all, OneFreqCache& k) {
+  const int p = h.p, m = h.m, C = (int)h.cl.size();
+  const size_t nfar = h.farR.size(), nnear = h.nearR.size();
+  k.S.assign(nfar * p * p, cplx(0.0, 0.0));
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t b = 0; b < (int64_t)nfar; ++b) {
+    const double* xr = &h.xi[(size_t)h.farR[b] * 3 * m];
+    const double* xc = &h.xi[(size_t)h.farC[b] * 3 * m];
+    cplx* S = &k.S[(size_t)b * p * p];
+    for (int mu = 0; mu < p; ++mu)
+      for (int nu = 0; nu < p; ++nu) {
+        double a[3], bb[3];
+        node_point(xr, m, mu, a); node_point(xc, m, nu, bb);
+        double dx = bb[0] - a[0], dy = bb[1] - a[1], dz = bb[2] - a[2];
+        const double r = std::sqrt((dx * dx + dy * dy) + dz * dz);
+        if (mode == MODE_H2ONLY) {
+          S[(size_t)mu * p + nu] = kernel(r, s_l);
+        } else {
+          for (int t = 0; t < h.rank[b]; ++t) {
+            const C2 z = h.Z[h.zoff[b] + (size_t)t * h.zld + h.zcol[l]];
+            S[(size_t)mu * p + nu] += cplx(z.re, z.im) * kernel(r, sl_all[h.pivk[h.pivoff[b] + t]]);
+          }
+        }
+      }
+  }
+  k.noff.assign(nnear + 1, 0);
+  for (size_t b = 0; b < nnear; ++b)
+    k.noff[b + 1] = k.noff[b] + (int64_t)(h.cl[h.nearR[b]].end - h.cl[h.nearR[b]].begin) *
+                                    (h.cl[h.nearC[b]].end - h.cl[h.nearC[b]].begin);
+  k.Vn.assign((size_t)k.noff[nnear], cplx(0.0, 0.0));
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t b = 0; b < (int64_t)nnear; ++b) {
+    const Cluster& R = h.cl[h.nearR[b]];
+    const Cluster& Cc = h.cl[h.nearC[b]];
+    const int nc = Cc.end - Cc.begin;
+    for (int a = R.begin; a < R.end; ++a)
+      for (int kk = Cc.begin; kk < Cc.end; ++kk)
+        k.Vn[k.noff[b] + (size_t)(a - R.begin) * nc + (kk - Cc.begin)] = entry(h.g, h.perm[a], h.perm[kk], s_l);
+  }
+  k.fbyrow.assign(C, {});
+  for (size_t b = 0; b < nfar; ++b) k.fbyrow[h.farR[b]].push_back((int)b);
+  k.nbyrow.assign(C, {});
+  for (size_t b = 0; b < nnear; ++b) k.nbyrow[h.nearR[b]].push_back((int)b);
+}
+
+static void apply_cached(const H2& h, const OneFreqCache& k, const cplx* x_in, cplx* y_out) {
+  const int64_t M = h.g.M;
+  const int p = h.p, C = (int)h.cl.size();
+  std::vector<cplx> x(M), y(M, cplx(0.0, 0.0)), xh((size_t)C * p, cplx(0.0, 0.0)), yh((size_t)C * p, cplx(0.0, 0.0));
+  for (int64_t i = 0; i < M; ++i) x[i] = x_in[h.perm[i]];
+  up_pass(h, x, xh);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int r = 0; r < C; ++r)
+    for (int b : k.fbyrow[r]) {
+      const cplx* S = &k.S[(size_t)b * p * p];
+      const int c = h.farC[b];
+      for (int mu = 0; mu < p; ++mu) {
+        cplx acc(0.0, 0.0);
+        for (int nu = 0; nu < p; ++nu) acc += S[(size_t)mu * p + nu] * xh[(size_t)c * p + nu];
+        yh[(size_t)r * p + mu] += acc;
+      }
+    }
+  down_pass(h, yh, y);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int rl = 0; rl < C; ++rl)
+    for (int b : k.nbyrow[rl]) {
+      const Cluster& R = h.cl[h.nearR[b]];
+      const Cluster& Cc = h.cl[h.nearC[b]];
+      const int nc = Cc.end - Cc.begin;
+      for (int a = R.begin; a < R.end; ++a) {
+        cplx acc(0.0, 0.0);
+        for (int kk = Cc.begin; kk < Cc.end; ++kk) acc += k.Vn[k.noff[b] + (size_t)(a - R.begin) * nc + (kk - Cc.begin)] * x[kk];
+        y[a] += acc;
+      }
+    }
+  for (int64_t i = 0; i < M; ++i) y_out[h.perm[i]] = y[i];
+}
+
 // ---------------------------------------------------------------------------
 // C5. Transforms (eq:omega_n P:436-441, eq:slphelm P:529-540), reading D2.
 // ---------------------------------------------------------------------------
+// The twiddles e^{-+2 pi i idx/L} (idx = n l mod L) and R^n are tabulated once
+// (the same values the naive loop evaluates per term); columns are processed in
+// blocks of 16 and in parallel; every sum keeps its n-ascending order.
+static void dft_tables(int L, double R, std::vector<cplx>& tw, std::vector<double>& Rn) {
+  tw.resize(L);
+  Rn.resize(L);
+  for (int idx = 0; idx < L; ++idx) {
+    double ang = (2.0 * PI * (double)idx) / (double)L;
+    tw[idx] = cplx(std::cos(ang), std::sin(ang));
+  }
+  for (int n = 0; n < L; ++n) Rn[n] = std::pow(R, (double)n);
+}
+
 static void forward(const cplx* xt, cplx* xf, int64_t M, int N, double R) {
   int L = N + 1;
-  for (int l = 0; l < L; ++l)
-    for (int64_t i = 0; i < M; ++i) {
-      cplx acc(0.0, 0.0);
+  std::vector<cplx> tw;
+  std::vector<double> Rn;
+  dft_tables(L, R, tw, Rn);
+  const int64_t nb = (M + 15) / 16;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t ib = 0; ib < nb; ++ib) {
+    const int64_t i0 = ib * 16, w = std::min<int64_t>(16, M - i0);
+    std::vector<cplx> xb((size_t)L * 16);
+    for (int n = 0; n < L; ++n)
+      for (int64_t ii = 0; ii < w; ++ii) xb[(size_t)n * 16 + ii] = xt[(int64_t)n * M + i0 + ii];
+    for (int l = 0; l < L; ++l) {
+      cplx acc[16];
+      for (int64_t ii = 0; ii < w; ++ii) acc[ii] = cplx(0.0, 0.0);
       for (int n = 0; n < L; ++n) {
         int64_t idx = ((int64_t)n * l) % L;
-        double ang = (2.0 * PI * (double)idx) / (double)L;
-        acc += std::pow(R, (double)n) * xt[(int64_t)n * M + i] * cplx(std::cos(ang), -std::sin(ang));
+        const cplx e(tw[idx].real(), -tw[idx].imag());
+        for (int64_t ii = 0; ii < w; ++ii) acc[ii] += Rn[n] * xb[(size_t)n * 16 + ii] * e;
       }
-      xf[(int64_t)l * M + i] = acc;
+      for (int64_t ii = 0; ii < w; ++ii) xf[(int64_t)l * M + i0 + ii] = acc[ii];
     }
+  }
 }
 
 static void inverse(const cplx* yf, cplx* yt, int64_t M, int N, double R) {
   int L = N + 1;
-  for (int n = 0; n < L; ++n)
-    for (int64_t i = 0; i < M; ++i) {
-      cplx acc(0.0, 0.0);
+  std::vector<cplx> tw;
+  std::vector<double> Rn;
+  dft_tables(L, R, tw, Rn);
+  const int64_t nb = (M + 15) / 16;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t ib = 0; ib < nb; ++ib) {
+    const int64_t i0 = ib * 16, w = std::min<int64_t>(16, M - i0);
+    std::vector<cplx> yb((size_t)L * 16);
+    for (int l = 0; l < L; ++l)
+      for (int64_t ii = 0; ii < w; ++ii) yb[(size_t)l * 16 + ii] = yf[(int64_t)l * M + i0 + ii];
+    for (int n = 0; n < L; ++n) {
+      cplx acc[16];
+      for (int64_t ii = 0; ii < w; ++ii) acc[ii] = cplx(0.0, 0.0);
       for (int l = 0; l < L; ++l) {
         int64_t idx = ((int64_t)n * l) % L;
-        double ang = (2.0 * PI * (double)idx) / (double)L;
-        acc += yf[(int64_t)l * M + i] * cplx(std::cos(ang), std::sin(ang));
+        for (int64_t ii = 0; ii < w; ++ii) acc[ii] += yb[(size_t)l * 16 + ii] * tw[idx];
       }
-      yt[(int64_t)n * M + i] = acc * (std::pow(R, -(double)n) / (double)L);
+      const double sc = std::pow(R, -(double)n) / (double)L;
+      for (int64_t ii = 0; ii < w; ++ii) yt[(int64_t)n * M + i0 + ii] = acc[ii] * sc;
     }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1094,14 +1414,21 @@ void orc_h2_export_bases(void* hp, double* U, double* W, double* E, double* xi) 
 // ACA over all far blocks (or the first nblk of `blocks` if blocks != NULL:
 // then only those are compressed -- used for sampled pivot checks).
 // Returns sum of ranks.
-int64_t orc_h2_aca(void* hp, const double* s_in, int32_t L, double eps, const int32_t* blocks, int64_t nblk,
-                   int32_t* ranks, int32_t* fragile) {
+// keep (may be NULL = all L): the frequencies whose Z columns are kept (memory:
+// config 4 stores only the compared frequencies, not 28 GB of Z).
+int64_t orc_h2_aca_keep(void* hp, const double* s_in, int32_t L, double eps, const int32_t* blocks, int64_t nblk,
+                        const int32_t* keep, int32_t nkeep, int32_t* ranks, int32_t* fragile) {
   H2& h = *(H2*)hp;
   if (h.near_done && h.L != L) h.near_done = false;
   h.tw_done = false;
   h.L = L;
   h.s.resize(L);
   for (int l = 0; l < L; ++l) h.s[l] = C2{s_in[2 * l], s_in[2 * l + 1]};
+  h.zcol.assign(L, -1);
+  std::vector<int> kl;
+  if (keep) for (int i = 0; i < nkeep; ++i) { if (h.zcol[keep[i]] < 0) { h.zcol[keep[i]] = (int)kl.size(); kl.push_back(keep[i]); } }
+  else for (int l = 0; l < L; ++l) { h.zcol[l] = l; kl.push_back(l); }
+  h.zld = (int)kl.size();
   int64_t nfar = (int64_t)h.farR.size();
   std::vector<int64_t> list;
   if (blocks) list.assign(blocks, blocks + nblk); else { list.resize(nfar); for (int64_t b = 0; b < nfar; ++b) list[b] = b; }
@@ -1109,7 +1436,15 @@ int64_t orc_h2_aca(void* hp, const double* s_in, int32_t L, double eps, const in
 #pragma omp parallel for schedule(dynamic, 1)
   for (int64_t t = 0; t < (int64_t)list.size(); ++t) {
     int64_t b = list[t];
-    aca_block(&h.xi[(size_t)h.farR[b] * 3 * h.m], &h.xi[(size_t)h.farC[b] * 3 * h.m], h.m, h.p, h.s, eps, res[t]);
+    AcaOut& o = res[t];
+    aca_block(&h.xi[(size_t)h.farR[b] * 3 * h.m], &h.xi[(size_t)h.farC[b] * 3 * h.m], h.m, h.p, h.s, eps, o);
+    if (h.zld != L) {  // keep only the requested columns
+      const size_t r = o.k.size();
+      std::vector<C2> zk(r * h.zld);
+      for (size_t j = 0; j < r; ++j)
+        for (int c = 0; c < h.zld; ++c) zk[j * h.zld + c] = o.Z[j * L + kl[c]];
+      o.Z.swap(zk);
+    }
   }
   h.rank.assign(nfar, 0); h.pivoff.assign(nfar, 0); h.zoff.assign(nfar, 0);
   h.pivk.clear(); h.pivq.clear(); h.Z.clear();
@@ -1125,11 +1460,17 @@ int64_t orc_h2_aca(void* hp, const double* s_in, int32_t L, double eps, const in
     tot += h.rank[b];
     for (size_t t = 0; t < o.k.size(); ++t) { h.pivk.push_back(o.k[t]); h.pivq.push_back(o.q[t]); }
     h.Z.insert(h.Z.end(), o.Z.begin(), o.Z.end());
+    std::vector<C2>().swap(o.Z);
   }
   if (ranks) for (int64_t t = 0; t < (int64_t)list.size(); ++t) ranks[t] = h.rank[list[t]];
   if (fragile) for (int64_t t = 0; t < (int64_t)list.size(); ++t) fragile[t] = res[t].fragile;
   h.aca_done = true;
   return tot;
+}
+
+int64_t orc_h2_aca(void* hp, const double* s_in, int32_t L, double eps, const int32_t* blocks, int64_t nblk,
+                   int32_t* ranks, int32_t* fragile) {
+  return orc_h2_aca_keep(hp, s_in, L, eps, blocks, nblk, nullptr, 0, ranks, fragile);
 }
 
 // Near-field MACA (Alg. 3 NEAR branch) over all
@@ -1220,7 +1561,7 @@ void orc_h2_aca_export(void* hp, const int32_t* blocks, int64_t nblk, int32_t* p
       if (pivots) { pivots[2 * pp] = h.pivk[h.pivoff[b] + j]; pivots[2 * pp + 1] = h.pivq[h.pivoff[b] + j]; }
       ++pp;
     }
-    if (Z) for (int64_t j = 0; j < (int64_t)h.rank[b] * h.L; ++j) {
+    if (Z) for (int64_t j = 0; j < (int64_t)h.rank[b] * h.zld; ++j) {
       Z[2 * pz] = h.Z[h.zoff[b] + j].re; Z[2 * pz + 1] = h.Z[h.zoff[b] + j].im; ++pz;
     }
   }
@@ -1234,12 +1575,33 @@ int orc_h2_apply(void* hp, int32_t mode, const double* s_in, int32_t L, const in
   if (mode == MODE_COMBINED && !h.near_done) return -1;
   std::vector<cplx> s(L);
   for (int l = 0; l < L; ++l) s[l] = cplx(s_in[2 * l], s_in[2 * l + 1]);
-  int64_t M = h.g.M;
-#pragma omp parallel for schedule(dynamic, 1)
-  for (int t = 0; t < nsel; ++t) {
-    int l = lsel[t];
-    apply_one(h, mode, s[l], l, s, (const cplx*)(x + 2 * (int64_t)t * M), (cplx*)(y + 2 * (int64_t)t * M));
+  if (mode == MODE_H2ACA || mode == MODE_COMBINED)
+    for (int t = 0; t < nsel; ++t) if (h.zcol[lsel[t]] < 0) return -1;
+  apply_multi(h, mode, s, lsel, nsel, (const cplx*)x, (cplx*)y, 0);
+  return 0;
+}
+
+// The apply with only the listed far / near blocks contributing (timing sample).
+int orc_h2_apply_sample(void* hp, int32_t mode, const double* s_in, int32_t L, const int32_t* lsel, int32_t nsel,
+                        const double* x, double* y, const int32_t* far_blocks, int64_t nfs, const int32_t* near_blocks,
+                        int64_t nns) {
+  H2& h = *(H2*)hp;
+  if (mode != MODE_H2ACA || !h.aca_done || h.L != L) return -1;
+  std::vector<char> fo(h.farR.size(), 0), no(h.nearR.size(), 0);
+  for (int64_t i = 0; i < nfs; ++i) {
+    if (far_blocks[i] < 0 || far_blocks[i] >= (int64_t)fo.size()) return -1;
+    fo[far_blocks[i]] = 1;
   }
+  for (int64_t i = 0; i < nns; ++i) {
+    if (near_blocks[i] < 0 || near_blocks[i] >= (int64_t)no.size()) return -1;
+    no[near_blocks[i]] = 1;
+  }
+  for (int t = 0; t < nsel; ++t)
+    for (size_t b = 0; b < fo.size(); ++b)
+      if (fo[b] && (h.zcol[lsel[t]] < 0 || h.zoff[b] < 0)) return -1;
+  std::vector<cplx> s(L);
+  for (int l = 0; l < L; ++l) s[l] = cplx(s_in[2 * l], s_in[2 * l + 1]);
+  apply_multi(h, mode, s, lsel, nsel, (const cplx*)x, (cplx*)y, 0, fo.data(), no.data());
   return 0;
 }
 
@@ -1252,12 +1614,12 @@ int orc_h2_apply_dl(void* hp, int32_t mode, const double* s_in, int32_t L, const
   std::vector<cplx> s(L);
   for (int l = 0; l < L; ++l) s[l] = cplx(s_in[2 * l], s_in[2 * l + 1]);
   int64_t M = h.g.M;
-#pragma omp parallel for schedule(dynamic, 1)
+  if (mode == MODE_H2ACA || mode == MODE_COMBINED)
+    for (int t = 0; t < nsel; ++t) if (h.zcol[lsel[t]] < 0) return -1;
+  apply_multi(h, mode, s, lsel, nsel, (const cplx*)x, (cplx*)y, 1);
   for (int t = 0; t < nsel; ++t) {
-    int l = lsel[t];
     const cplx* xt = (const cplx*)(x + 2 * (int64_t)t * M);
     cplx* yt = (cplx*)(y + 2 * (int64_t)t * M);
-    apply_one(h, mode, s[l], l, s, xt, yt, 1);
     for (int64_t i = 0; i < M; ++i) yt[i] += alpha * xt[i];
   }
   return 0;
@@ -1295,9 +1657,22 @@ int orc_h2_gmres(void* hp, int32_t mode, const double* s_in, int32_t L, const in
   H2& h = *(H2*)hp;
   if ((mode == MODE_H2ACA || mode == MODE_COMBINED) && (!h.aca_done || h.L != L)) return -1;
   if (mode == MODE_COMBINED && !h.near_done) return -1;
+  if (mode == MODE_H2ACA || mode == MODE_COMBINED)
+    for (int t = 0; t < nsel; ++t) if (h.zcol[lsel[t]] < 0) return -1;
   std::vector<cplx> s(L);
   for (int l = 0; l < L; ++l) s[l] = cplx(s_in[2 * l], s_in[2 * l + 1]);
   int64_t M = h.g.M;
+  if (mode == MODE_H2ACA || mode == MODE_H2ONLY) {  // one frequency at a time, parallel applies
+    for (int t = 0; t < nsel; ++t) {
+      int l = lsel[t];
+      OneFreqCache k;
+      build_cache(h, mode, s[l], l, s, k);
+      auto op = [&](const cplx* in, cplx* out) { apply_cached(h, k, in, out); };
+      iters[t] = gmres(op, M, (const cplx*)(b + 2 * (int64_t)t * M), (cplx*)(x + 2 * (int64_t)t * M), tol, restart,
+                       maxit, &relres[t]);
+    }
+    return 0;
+  }
 #pragma omp parallel for schedule(dynamic, 1)
   for (int t = 0; t < nsel; ++t) {
     int l = lsel[t];
@@ -1552,7 +1927,7 @@ extern "C" {
 // the same L); R is the transform's scaling.
 int orc_h2_time_weights(void* hp, double R) {
   H2& h = *(H2*)hp;
-  if (!h.aca_done || !h.near_done) return -1;
+  if (!h.aca_done || !h.near_done || h.zld != h.L) return -1;
   dhat_rows(h.Z, h.L, h.L - 1, R, h.tDf);
   dhat_rows(h.nZ, h.L, h.L - 1, R, h.tDn);
   h.tw_done = true;

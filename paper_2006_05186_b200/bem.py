@@ -15,6 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libbem.so")
 
 BEM_MODE_H2ACA, BEM_MODE_H2ONLY, BEM_MODE_DENSE, BEM_MODE_COMBINED = 0, 1, 2, 3
+BEM_SKEL_Z, BEM_SKEL_FACTORS = 0x100, 0x200  # skeleton storage flags OR-ed into mode (include/bem.h)
 BEM_ENOCONV = -5
 _lib = None
 
@@ -30,6 +31,12 @@ class TreeStats(C.Structure):
                 ("far_blocks", C.c_int64), ("nnz_near", C.c_int64), ("depth", C.c_int32), ("p", C.c_int32)]
 
 
+class OpInfo(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("skeleton", C.c_int32), ("n_local", C.c_int32), ("rmax", C.c_int32),
+                ("total_rank", C.c_int64), ("z_bytes", C.c_int64), ("f_bytes", C.c_int64),
+                ("device_bytes", C.c_int64)]
+
+
 class SolveStats(C.Structure):
     _fields_ = [("iters_max", C.c_int32), ("iters_sum", C.c_int32), ("n_unconverged", C.c_int32),
                 ("pad_", C.c_int32), ("resid_max", C.c_double), ("imag_rel_max", C.c_double)]
@@ -41,6 +48,7 @@ EXPORTS = [
     "cqm_forward", "cqm_inverse", "cqm_forward_rows", "cqm_inverse_rows", "bem_ipc_get_handle",
     "bem_ipc_open_handle", "bem_ipc_close", "bem_device_alloc", "bem_device_free", "cqm_solve", "bem_solve_multifreq", "bem_debug_pinned", "bem_debug_fastmath", "bem_debug_fp64_peak",
     "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count", "bem_debug_fp64_peak_ex",
+    "bem_op_get_info",
 ]
 
 
@@ -88,6 +96,7 @@ def lib():
         "bem_op_get_timings": [vp, vp],
         "bem_op_launch_count": [vp, vp],
         "bem_debug_fp64_peak_ex": [i32, vp, i32, vp],
+        "bem_op_get_info": [vp, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -199,6 +208,15 @@ class Operator:
         _check(lib().bem_aca_export(self.h, None, _p(piv), None))
         return dict(ranks=ranks, pivots=piv)
 
+    def info(self):
+        """Skeleton storage and the op's device footprint (bem_op_get_info)."""
+        st = OpInfo()
+        _check(lib().bem_op_get_info(self.h, C.byref(st)))
+        return {k: int(getattr(st, k)) for k, _ in OpInfo._fields_}
+
+    def skeleton(self) -> str:
+        return {0: "none", 1: "Z", 2: "factors"}[self.info()["skeleton"]]
+
     def aca_export_near(self):
         """Near-block skeletons of a BEM_MODE_COMBINED operator (Alg. 3 NEAR branch)."""
         nn = self.tree.stats["near_blocks"]
@@ -214,7 +232,10 @@ class Operator:
         part); x_time: [L][M] complex128 torch tensor on the host (pinned for async) or device."""
         import torch
         assert x_time.dtype == torch.complex128 and x_time.is_contiguous()
+        assert tuple(x_time.shape) == (self.L, self.tree.M), "x_time must be [L][M]"
         y = torch.empty_like(x_time, pin_memory=not x_time.is_cuda) if y is None else y
+        assert y.dtype == torch.complex128 and y.is_contiguous() and tuple(y.shape) == tuple(x_time.shape)
+        assert (y.is_cuda == x_time.is_cuda) and (not y.is_cuda or y.device == x_time.device)
         _check(lib().bem_time_step(self.h, _p(x_time), _p(y), float(R), _stream(stream)))
         return y
 
@@ -238,6 +259,7 @@ class Operator:
         assert tuple(x.shape) == (self.n_local, self.tree.M)
         if y is None:
             y = torch.empty_like(x)
+        assert y.dtype == torch.complex128 and y.is_contiguous() and y.shape == x.shape and y.device == x.device
         _check(lib().bem_apply_multifreq(self.h, _p(x), _p(y), _stream(stream)))
         return y
 
@@ -249,8 +271,10 @@ class Operator:
         """y_t = (alpha I + K(s_{local_l[t]})) x_t (double layer, NEXT-1)."""
         import torch
         assert x.dtype == torch.complex128 and x.is_cuda and x.is_contiguous()
+        assert tuple(x.shape) == (self.n_local, self.tree.M)
         if y is None:
             y = torch.empty_like(x)
+        assert y.dtype == torch.complex128 and y.is_contiguous() and y.shape == x.shape and y.device == x.device
         _check(lib().bem_apply_double_layer(self.h, _p(x), _p(y), float(alpha), _stream(stream)))
         return y
 
@@ -282,7 +306,10 @@ class Operator:
 def cqm_forward(x_time, N: int, R: float, out=None, stream=None):
     import torch
     assert x_time.dtype == torch.complex128 and x_time.is_cuda and x_time.is_contiguous()
+    assert x_time.dim() == 2 and x_time.shape[0] == N + 1, "x_time must be [N+1][M_loc]"
     out = torch.empty_like(x_time) if out is None else out
+    assert out.dtype == torch.complex128 and out.is_contiguous() and out.shape == x_time.shape
+    assert out.device == x_time.device and out.data_ptr() != x_time.data_ptr()
     _check(lib().cqm_forward(_p(x_time), _p(out), x_time.shape[1], int(N), float(R), _stream(stream)))
     return out
 
@@ -290,7 +317,10 @@ def cqm_forward(x_time, N: int, R: float, out=None, stream=None):
 def cqm_inverse(y_freq, N: int, R: float, out=None, stream=None):
     import torch
     assert y_freq.dtype == torch.complex128 and y_freq.is_cuda and y_freq.is_contiguous()
+    assert y_freq.dim() == 2 and y_freq.shape[0] == N + 1, "y_freq must be [N+1][M_loc]"
     out = torch.empty_like(y_freq) if out is None else out
+    assert out.dtype == torch.complex128 and out.is_contiguous() and out.shape == y_freq.shape
+    assert out.device == y_freq.device and out.data_ptr() != y_freq.data_ptr()
     _check(lib().cqm_inverse(_p(y_freq), _p(out), y_freq.shape[1], int(N), float(R), _stream(stream)))
     return out
 

@@ -21,162 +21,10 @@
 
 #include "common.cuh"
 
+#include "pinned.cuh"
+#include "zgen.cuh"
+
 namespace bem {
-namespace pinned {
-
-__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double fma(double a, double b, double c) { return __fma_rn(a, b, c); }
-
-__device__ __forceinline__ double pow2i(int k) { return __longlong_as_double((long long)(k + 1023) << 52); }
-
-__device__ double exp_(double x) {
-  if (x < -746.0) return 0.0;
-  if (x > 709.5) return __longlong_as_double(0x7ff0000000000000LL);
-  const double t = fma(x, 0x1.71547652b82fep+0, 0x1.8p+52);
-  const double kd = sub(t, 0x1.8p+52);
-  double r = fma(kd, -0x1.62e42fee00000p-1, x);
-  r = fma(kd, -0x1.a39ef35793c76p-33, r);
-  double q = 0x1.6124613a86d09p-33;  // 1/13!
-  q = fma(q, r, 0x1.1eed8eff8d898p-29);
-  q = fma(q, r, 0x1.ae64567f544e4p-26);
-  q = fma(q, r, 0x1.27e4fb7789f5cp-22);
-  q = fma(q, r, 0x1.71de3a556c734p-19);
-  q = fma(q, r, 0x1.a01a01a01a01ap-16);
-  q = fma(q, r, 0x1.a01a01a01a01ap-13);
-  q = fma(q, r, 0x1.6c16c16c16c17p-10);
-  q = fma(q, r, 0x1.1111111111111p-7);
-  q = fma(q, r, 0x1.5555555555555p-5);
-  q = fma(q, r, 0x1.5555555555555p-3);
-  q = fma(q, r, 0x1.0000000000000p-1);
-  q = fma(q, r, 0x1.0000000000000p+0);
-  q = fma(q, r, 0x1.0000000000000p+0);
-  const int k = (int)kd;
-  if (k >= -1021) return mul(q, pow2i(k));
-  return mul(mul(q, pow2i(k + 200)), pow2i(-200));
-}
-
-__device__ void sincos_(double th, double* sn, double* cs) {
-  const double t = fma(th, 0x1.45f306dc9c883p-1, 0x1.8p+52);
-  const double qd = sub(t, 0x1.8p+52);
-  double r = fma(qd, -0x1.921fb54400000p+0, th);
-  r = fma(qd, -0x1.0b4611a600000p-34, r);
-  r = fma(qd, -0x1.3198a2e000000p-69, r);
-  const double z = mul(r, r);
-  double ps = 0x1.952c77030ad4ap-49;   // 1/17!
-  ps = fma(ps, z, -0x1.ae7f3e733b81fp-41);
-  ps = fma(ps, z, 0x1.6124613a86d09p-33);
-  ps = fma(ps, z, -0x1.ae64567f544e4p-26);
-  ps = fma(ps, z, 0x1.71de3a556c734p-19);
-  ps = fma(ps, z, -0x1.a01a01a01a01ap-13);
-  ps = fma(ps, z, 0x1.1111111111111p-7);
-  ps = fma(ps, z, -0x1.5555555555555p-3);
-  ps = fma(ps, z, 0x1.0000000000000p+0);
-  const double s = mul(r, ps);
-  double pc = -0x1.6827863b97d97p-53;  // -1/18!
-  pc = fma(pc, z, 0x1.ae7f3e733b81fp-45);
-  pc = fma(pc, z, -0x1.93974a8c07c9dp-37);
-  pc = fma(pc, z, 0x1.1eed8eff8d898p-29);
-  pc = fma(pc, z, -0x1.27e4fb7789f5cp-22);
-  pc = fma(pc, z, 0x1.a01a01a01a01ap-16);
-  pc = fma(pc, z, -0x1.6c16c16c16c17p-10);
-  pc = fma(pc, z, 0x1.5555555555555p-5);
-  pc = fma(pc, z, -0x1.0000000000000p-1);
-  pc = fma(pc, z, 0x1.0000000000000p+0);
-  switch ((int)((long long)qd & 3)) {
-    case 0: *sn = s; *cs = pc; break;
-    case 1: *sn = pc; *cs = -s; break;
-    case 2: *sn = -s; *cs = -pc; break;
-    default: *sn = -pc; *cs = s; break;
-  }
-}
-
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(sub(mul(a.x, b.x), mul(a.y, b.y)), add(mul(a.x, b.y), mul(a.y, b.x)));
-}
-__device__ __forceinline__ double2 cmulconj(double2 a, double2 b) {  // a * conj(b)
-  return make_double2(add(mul(a.x, b.x), mul(a.y, b.y)), sub(mul(a.y, b.x), mul(a.x, b.y)));
-}
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(sub(a.x, b.x), sub(a.y, b.y)); }
-__device__ __forceinline__ double2 cdiv(double2 a, double2 c) {
-  const double den = add(mul(c.x, c.x), mul(c.y, c.y));
-  return make_double2(__ddiv_rn(add(mul(a.x, c.x), mul(a.y, c.y)), den),
-                      __ddiv_rn(sub(mul(a.y, c.x), mul(a.x, c.y)), den));
-}
-__device__ __forceinline__ double key(double2 a) { return add(mul(a.x, a.x), mul(a.y, a.y)); }
-
-// k(r; s) = e^{-s r}/(4 pi r): E = exp(-(Re s * r)), th = Im s * r,
-// inv = 1/(4pi r), value = ((E cos th) inv, -((E sin th) inv)).
-__device__ __forceinline__ double2 kernel(double r, double sre, double sim) {
-  const double E = exp_(-mul(sre, r));
-  double sn, cs;
-  sincos_(mul(sim, r), &sn, &cs);
-  const double inv = __ddiv_rn(1.0, mul(0x1.921fb54442d18p+3, r));
-  return make_double2(mul(mul(E, cs), inv), -mul(mul(E, sn), inv));
-}
-
-__device__ __forceinline__ double dist(const double* a, const double* b) {
-  const double dx = sub(b[0], a[0]), dy = sub(b[1], a[1]), dz = sub(b[2], a[2]);
-  return __dsqrt_rn(add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)));
-}
-
-// 1/k!, k = 0..19, correctly rounded (pinned expm1 of the self entry).
-__device__ __constant__ double kInvFact[20] = {
-    0x1.0000000000000p+0, 0x1.0000000000000p+0, 0x1.0000000000000p-1, 0x1.5555555555555p-3,
-    0x1.5555555555555p-5, 0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
-    0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22, 0x1.ae64567f544e4p-26,
-    0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33, 0x1.93974a8c07c9dp-37, 0x1.ae7f3e733b81fp-41,
-    0x1.ae7f3e733b81fp-45, 0x1.952c77030ad4ap-49, 0x1.6827863b97d97p-53, 0x1.2f49b46814157p-57};
-
-// expm1: |x| < 1/2 -> x * sum_{k=1..19} x^{k-1}/k! (Horner in fma), else exp(x) - 1.
-__device__ double expm1_(double x) {
-  if (x > -0.5 && x < 0.5) {
-    double q = kInvFact[19];
-    for (int j = 18; j >= 1; --j) q = fma(q, x, kInvFact[j]);
-    return mul(x, q);
-  }
-  return sub(exp_(x), 1.0);
-}
-
-// phi(s,r) = (e^{-sr} - 1)/r, r > 0: Re = expm1(x) cos y - 2 sin^2(y/2), Im = e^x sin y, x + iy = -s r.
-__device__ double2 phi(double r, double sre, double sim) {
-  const double x = -mul(sre, r), y = -mul(sim, r);
-  double sy, cy, sh, ch;
-  sincos_(y, &sy, &cy);
-  sincos_(mul(0.5, y), &sh, &ch);
-  const double re = sub(mul(expm1_(x), cy), mul(2.0, mul(sh, sh)));
-  const double im = mul(exp_(x), sy);
-  return make_double2(__ddiv_rn(re, r), __ddiv_rn(im, r));
-}
-
-// Collocation entry V(s)[i,j] (C3; the NEAR procedure of Alg. 3) in pinned
-// arithmetic.  ci: centroid of panel i; cj: 21 node coordinates, |T_j|, J(T_j) of panel j.
-__device__ double2 near_entry(const double* ci, const double* cj, bool self, double sre, double sim,
-                              const double* w) {
-  double ar = 0.0, ai = 0.0;
-  const double area = cj[21];
-  if (!self) {
-    for (int q = 0; q < 7; ++q) {
-      const double2 k = kernel(dist(ci, cj + 3 * q), sre, sim);
-      const double wa = mul(w[q], area);
-      ar = add(ar, mul(wa, k.x));
-      ai = add(ai, mul(wa, k.y));
-    }
-    return make_double2(ar, ai);
-  }
-  ar = add(ar, mul(w[0], -sre));  // node 0 is the centroid: phi = -s
-  ai = add(ai, mul(w[0], -sim));
-  for (int q = 1; q < 7; ++q) {
-    const double2 f = phi(dist(ci, cj + 3 * q), sre, sim);
-    ar = add(ar, mul(w[q], f.x));
-    ai = add(ai, mul(w[q], f.y));
-  }
-  constexpr double kInv4Pi = 0x1.45f306dc9c883p-4;
-  return make_double2(mul(add(cj[22], mul(area, ar)), kInv4Pi), mul(mul(area, ai), kInv4Pi));
-}
-
-}  // namespace pinned
 
 namespace {
 
@@ -213,9 +61,15 @@ struct AcaArgs {
   int32_t* pivk;
   int32_t* pivq;
   int64_t* zoff;
-  double2* Zpool;
+  double2* Zpool;  // nullable: Z_b not stored (factors-only skeleton)
   unsigned long long* pool_used;
   unsigned long long pool_cap;
+  // factors-only skeleton (far blocks): F_b [r][r] row-major, F[l][j] = c_j[q_l] (j <= l, the
+  // lower factor C^_b of A_b[Q,K], pivots on the diagonal) and d_l[k_j] (j > l, the unit upper U_b)
+  double2* Fpool;  // nullable
+  unsigned long long* fpool_used;
+  unsigned long long fpool_cap;
+  int64_t* foff;
   int32_t* flags;
   int32_t* next_block;
 };
@@ -461,8 +315,10 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
       ++ell;
       if (s_stop) break;
     }
-    // write rank, allocate Z, back substitution Z = U^{-1} D^T on local columns
+    // write rank, allocate Z (and F), back substitution Z = U^{-1} D^T on local columns
+    __shared__ long long s_foff;
     if (threadIdx.x == 0) {
+      s_foff = -1;
       if (overflow) {
         atomicOr(a.flags, 1);
         a.rank[b] = -1;
@@ -470,19 +326,32 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
         s_off = -1;
       } else {
         a.rank[b] = ell;
-        const unsigned long long need = (unsigned long long)ell * (unsigned long long)a.n_local;
-        const unsigned long long off = atomicAdd(a.pool_used, need);
-        if (off + need > a.pool_cap) {
-          atomicOr(a.flags, 2);
-          s_off = -1;
-        } else {
-          s_off = (long long)off;
+        s_off = -1;
+        if (a.Zpool != nullptr) {
+          const unsigned long long need = (unsigned long long)ell * (unsigned long long)a.n_local;
+          const unsigned long long off = atomicAdd(a.pool_used, need);
+          if (off + need > a.pool_cap) atomicOr(a.flags, 2); else s_off = (long long)off;
         }
         a.zoff[b] = s_off;
+        if (a.Fpool != nullptr) {
+          const unsigned long long need = (unsigned long long)ell * (unsigned long long)ell;
+          const unsigned long long fo = atomicAdd(a.fpool_used, need);
+          if (fo + need > a.fpool_cap) atomicOr(a.flags, 8); else s_foff = (long long)fo;
+          a.foff[b] = s_foff;
+        }
       }
     }
     __syncthreads();
     const long long off = s_off;
+    if (s_foff >= 0) {
+      const int r = ell;
+      const int32_t* kp = a.pivk + (size_t)b * a.rcap;
+      const int32_t* qp = a.pivq + (size_t)b * a.rcap;
+      for (int idx = threadIdx.x; idx < r * r; idx += blockDim.x) {
+        const int i = idx / r, j = idx - i * r;
+        a.Fpool[s_foff + idx] = j <= i ? Cb[(size_t)j * pp + qp[i]] : Db[(size_t)i * L + kp[j]];
+      }
+    }
     if (off >= 0) {
       const int r = ell;
       const int32_t* kp = a.pivk + (size_t)b * a.rcap;
@@ -522,6 +391,18 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
   }
 }
 
+// Stored-Z skeleton (the default when it fits): Z_b[:, t] for every far block and local
+// frequency t, regenerated from the factors F_b (zgen.cuh; bit-identical to the ACA's own
+// back substitution).  One CTA per block (grid-stride), threads over the local columns.
+__global__ void __launch_bounds__(128) zgen_all_kernel(zgen::Src a, int nfar, const int32_t* rank, const int32_t* local_l,
+                                                    int n_local, const int64_t* zoff, double2* Z) {
+  for (int b = blockIdx.x; b < nfar; b += gridDim.x) {
+    const int r = rank[b];
+    double2* Zb = Z + zoff[b];
+    for (int t = threadIdx.x; t < n_local; t += blockDim.x) zgen::column(a, b, r, local_l[t], Zb + t, n_local);
+  }
+}
+
 __global__ void debug_pinned_kernel(const double* x, int64_t n, double* e, double* sn, double* cs) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -537,7 +418,7 @@ using namespace bem;
 namespace {
 // near = false: far blocks (P+, coupling tensors); near = true: near blocks (P-,
 // combined mode), whose pivot slices are stored as well.
-bem_status run_aca(Op& op, cudaStream_t st, bool near) {
+bem_status run_aca(Op& op, cudaStream_t st, bool near, bool store_z) {
   Tree& t = *op.tree;
   const int nblk = near ? (int)t.near_r.size() : (int)t.far_r.size();
   std::vector<int32_t>& ranks_out = near ? op.nranks : op.ranks;
@@ -552,7 +433,9 @@ bem_status run_aca(Op& op, cudaStream_t st, bool near) {
   // whole ACA: config 5 hit both the old 96 rank cap and the 40-per-block pool
   // estimate), the pool is shrunk to its exact size afterwards
   int rcap = std::min(std::min(L, ppmax), 128);
-  unsigned long long cap = (unsigned long long)nblk * 64ull * (unsigned long long)op.n_local;
+  const bool store_f = !near;  // factors-only skeleton of the far blocks (always kept: small)
+  unsigned long long cap = store_z ? (unsigned long long)nblk * 64ull * (unsigned long long)op.n_local : 0ull;
+  unsigned long long fcap = store_f ? (unsigned long long)nblk * 48ull * 48ull : 0ull;
   unsigned long long scap = 0;
   if (near) {
     scap = 0;
@@ -565,10 +448,11 @@ bem_status run_aca(Op& op, cudaStream_t st, bool near) {
     if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
       const size_t scratch = (size_t)std::max(1, std::min(nblk, nsm * op.aca_ctas_per_sm)) * rcap * ((size_t)ppmax + L) * 16;
       const unsigned long long lim = fr > scratch ? (unsigned long long)((fr - scratch) * 0.7 / 16) : 0ull;
-      if (lim > 0 && cap + scap > lim) {
-        const double f = (double)lim / (double)(cap + scap);
+      if (lim > 0 && cap + scap + fcap > lim) {
+        const double f = (double)lim / (double)(cap + scap + fcap);
         cap = (unsigned long long)(cap * f);
         scap = (unsigned long long)(scap * f);
+        fcap = (unsigned long long)(fcap * f);
       }
     }
   }
@@ -576,7 +460,7 @@ bem_status run_aca(Op& op, cudaStream_t st, bool near) {
   DBuf<unsigned long long> used;
   BEM_CK(flags.alloc(1));
   BEM_CK(counter.alloc(1));
-  BEM_CK(used.alloc(2));
+  BEM_CK(used.alloc(3));
   DBuf<int32_t>& d_rank = near ? op.d_nrank : op.d_rank;
   DBuf<int32_t>& d_pivk = near ? op.d_npivk : op.d_pivk;
   DBuf<int32_t>& d_pivq = near ? op.d_npivq : op.d_pivq;
@@ -584,6 +468,7 @@ bem_status run_aca(Op& op, cudaStream_t st, bool near) {
   DBuf<double>& d_Z = near ? op.d_nZ : op.d_Z;
   BEM_CK(d_rank.alloc(nblk));
   BEM_CK(d_zoff.alloc(nblk));
+  if (store_f) BEM_CK(op.d_foff.alloc(nblk));
   if (near) BEM_CK(op.d_nsoff.alloc(nblk));
   std::vector<double> wq(7);
   {
@@ -602,10 +487,11 @@ bem_status run_aca(Op& op, cudaStream_t st, bool near) {
     BEM_CK(d_pivk.alloc((size_t)nblk * rcap));
     BEM_CK(d_pivq.alloc((size_t)nblk * rcap));
     BEM_CK(d_Z.alloc((size_t)cap * 2));
+    if (store_f) BEM_CK(op.d_F.alloc((size_t)fcap * 2));
     if (near) BEM_CK(op.d_nS.alloc((size_t)scap * 2));
     BEM_CK(cudaMemsetAsync(flags.p, 0, sizeof(int32_t), st));
     BEM_CK(cudaMemsetAsync(counter.p, 0, sizeof(int32_t), st));
-    BEM_CK(cudaMemsetAsync(used.p, 0, 2 * sizeof(unsigned long long), st));
+    BEM_CK(cudaMemsetAsync(used.p, 0, 3 * sizeof(unsigned long long), st));
     AcaArgs a{};
     a.nfar = nblk; a.m = t.m; a.p = p; a.L = L; a.rcap = rcap; a.n_local = op.n_local;
     a.ppmax = ppmax; a.geo = geo;
@@ -618,7 +504,9 @@ bem_status run_aca(Op& op, cudaStream_t st, bool near) {
     a.s = (const double2*)op.d_s.p; a.local_l = op.d_local_l.p; a.eps = op.eps;
     a.Cbuf = (double2*)Cbuf.p; a.Dbuf = (double2*)Dbuf.p; a.Ebuf = (double2*)Ebuf.p; a.Pbuf = (double2*)Pbuf.p;
     a.rank = d_rank.p; a.pivk = d_pivk.p; a.pivq = d_pivq.p; a.zoff = d_zoff.p;
-    a.Zpool = (double2*)d_Z.p; a.pool_used = used.p; a.pool_cap = cap; a.flags = flags.p;
+    a.Zpool = store_z ? (double2*)d_Z.p : nullptr; a.pool_used = used.p; a.pool_cap = cap; a.flags = flags.p;
+    a.Fpool = store_f ? (double2*)op.d_F.p : nullptr; a.fpool_used = used.p + 2; a.fpool_cap = fcap;
+    a.foff = store_f ? op.d_foff.p : nullptr;
     a.next_block = counter.p;
     const int nchmax = (std::max(ppmax, L) + 31) / 32 + 1;
     const size_t smem = sizeof(double) * geo + sizeof(double2) * (nchmax + 2 * rcap) +
@@ -632,17 +520,18 @@ bem_status run_aca(Op& op, cudaStream_t st, bool near) {
     }
     BEM_CK(cudaGetLastError());
     int32_t hflags = 0;
-    unsigned long long hused[2] = {0, 0};
+    unsigned long long hused[3] = {0, 0, 0};
     BEM_CK(cudaMemcpyAsync(&hflags, flags.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    BEM_CK(cudaMemcpyAsync(hused, used.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    BEM_CK(cudaMemcpyAsync(hused, used.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     BEM_CK(cudaStreamSynchronize(st));
     if (hflags & 1) {  // a rank reached the scratch capacity: grow and redo
       rcap = std::min(std::min(L, ppmax), rcap * 2);
       continue;
     }
-    if (hflags & 6) {  // Z / slice pool too small: exact sizes are now known
+    if (hflags & 14) {  // Z / slice / factor pool too small: exact sizes are now known
       if (hflags & 2) cap = hused[0];
       if (hflags & 4) scap = hused[1];
+      if (hflags & 8) fcap = hused[2];
       continue;
     }
     if (near) op.nrcap = rcap; else op.rcap = rcap;
@@ -658,6 +547,8 @@ bem_status run_aca(Op& op, cudaStream_t st, bool near) {
       return e;
     };
     BEM_CK(shrink(d_Z, hused[0], cap));
+    if (store_f) BEM_CK(shrink(op.d_F, hused[2], fcap));
+    if (!near) op.z_stored = store_z;
     if (near) BEM_CK(shrink(op.d_nS, hused[1], scap));
     return BEM_OK;
   }
@@ -672,8 +563,20 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   BEM_REQ(th && out, "bem_assemble_h2_aca: NULL tree/out");
   BEM_REQ(s != nullptr && L >= 1, "bem_assemble_h2_aca: need s and L >= 1");
   BEM_REQ(aca_eps > 0.0, "bem_assemble_h2_aca: aca_eps must be > 0");
+  const int skel = mode & (BEM_SKEL_Z | BEM_SKEL_FACTORS);
+  BEM_REQ((mode & ~(0xff | BEM_SKEL_Z | BEM_SKEL_FACTORS)) == 0 && skel != (BEM_SKEL_Z | BEM_SKEL_FACTORS),
+          "bem_assemble_h2_aca: bad mode flags 0x%x", mode);
+  mode &= 0xff;
   BEM_REQ(mode == BEM_MODE_H2ACA || mode == BEM_MODE_H2ONLY || mode == BEM_MODE_DENSE || mode == BEM_MODE_COMBINED,
           "bem_assemble_h2_aca: unknown mode %d", mode);
+  BEM_REQ(!(mode == BEM_MODE_COMBINED && skel == BEM_SKEL_FACTORS),
+          "bem_assemble_h2_aca: BEM_MODE_COMBINED keeps the stored Z (the MoT weights read it)");
+  // the operator evaluates l > L/2 as the conjugate of L - l (ACA mirroring, conjugate
+  // frequency classes of K1 / K3'): s must be exactly conjugation-symmetric
+  for (int l = 1; l < L; ++l)
+    BEM_REQ(s[L - l].re == s[l].re && s[L - l].im == -s[l].im,
+            "bem_assemble_h2_aca: s[%d] != conj(s[%d]) (s must satisfy s_{L-l} = conj(s_l), as cqm_frequencies gives)",
+            L - l, l);
   *out = nullptr;
   Tree& t = th->t;
   if (t.device < 0) {
@@ -699,26 +602,10 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   bem_op_s* h = new bem_op_s();
   Op& op = h->o;
   op.tree = &t; op.L = L; op.n_local = (int)loc.size(); op.mode = mode; op.eps = aca_eps; op.local_l = loc;
-  if (const char* e = getenv("BEM_NEAR_F")) op.near_f = atoi(e) == 0 ? 0 : std::min(5, std::max(2, atoi(e)));  // 6F <= 32 lanes
-  if (const char* e = getenv("BEM_NEAR_U")) op.near_unroll = atoi(e);
-  if (const char* e = getenv("BEM_NEAR_TAB")) op.near_tab = atoi(e) != 0;
-  if (const char* e = getenv("BEM_NEAR_XL")) op.near_xlate = atoi(e) != 0;
   if (const char* e = getenv("BEM_FAR_GENERIC")) op.force_generic = atoi(e) != 0;
   if (const char* e = getenv("BEM_FAR_KERNEL")) op.far_kernel = atoi(e);
-  if (const char* e = getenv("BEM_FAR4_SMEM_KB")) op.far4_smem_cap = (size_t)atoi(e) * 1024;
-  if (const char* e = getenv("BEM_FAR7_CLUSTER")) op.far7_cluster = atoi(e) != 0;
-  if (const char* e = getenv("BEM_FAR7_REM")) op.far7_rem_dfma = atoi(e) != 0;
   if (const char* e = getenv("BEM_FAR8_KC")) op.far8_kc = atoi(e);
-  if (const char* e = getenv("BEM_FAR7_TTMAX")) op.far7_ttmax = atoi(e);
-  if (const char* e = getenv("BEM_FAR7_NW")) op.far7_nw = atoi(e) == 16 ? 16 : 8;
-  if (const char* e = getenv("BEM_FAR7_M3")) op.far7_m3 = atoi(e) != 0;
-  if (const char* e = getenv("BEM_FAR8_NW")) op.far8_nw = atoi(e) == 6 ? 6 : 8;
-  if (const char* e = getenv("BEM_FAR7_SPLIT")) op.far7_split = atoi(e) != 0;
-  if (const char* e = getenv("BEM_ACA_CTAS")) op.aca_ctas_per_sm = std::max(1, atoi(e));
-  if (const char* e = getenv("BEM_H2O_FC")) op.h2o_fc = atoi(e);
   if (const char* e = getenv("BEM_SOLVE_MASK")) op.use_solve_mask = atoi(e) != 0;
-  if (const char* e = getenv("BEM_OVERLAP")) op.overlap = atoi(e) != 0;
-  if (const char* e = getenv("BEM_FAR_SMEM_MIN_KB")) op.far_smem_min = (size_t)atoi(e) * 1024;
   auto fail = [&](bem_status stt) { delete h; return stt; };
   std::vector<double> sh(2 * (size_t)L);
   for (int l = 0; l < L; ++l) { sh[2 * l] = s[l].re; sh[2 * l + 1] = s[l].im; }
@@ -749,15 +636,50 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
     return fail(BEM_ECUDA);
   }
   if (mode == BEM_MODE_H2ACA || mode == BEM_MODE_COMBINED) {
-    bem_status rs = run_aca(op, st, false);
+    // MACA with the factors F_b only; then either the coefficients Z_b of the local
+    // frequencies are stored (regenerated once from F_b here), or K3 regenerates each
+    // block's Z tile in its prologue (factors-only skeleton): the
+    // default stores Z when it takes at most a third of the free device memory
+    bem_status rs = run_aca(op, st, false, false);
     if (rs != BEM_OK) return fail(rs);
+    int64_t zrows = 0;
+    for (int v : op.ranks) zrows += v;
+    const size_t zbytes = (size_t)zrows * op.n_local * 16;
+    bool store = skel == BEM_SKEL_Z || mode == BEM_MODE_COMBINED;
+    if (skel == 0) {
+      size_t fr = 0, tot = 0;
+      store = cudaMemGetInfo(&fr, &tot) == cudaSuccess && zbytes <= fr / 3;
+    }
+    if (store) {
+      std::vector<int64_t> zo(op.ranks.size());
+      int64_t acc = 0;
+      for (size_t b = 0; b < zo.size(); ++b) { zo[b] = acc; acc += (int64_t)op.ranks[b] * op.n_local; }
+      if (op.d_zoff.upload(zo) != cudaSuccess || op.d_Z.alloc(std::max<size_t>(1, (size_t)acc * 2)) != cudaSuccess) {
+        set_error("bem_assemble_h2_aca: stored Z (%.2f GB) does not fit", zbytes / 1e9);
+        return fail(BEM_ENOMEM);
+      }
+      zgen::Src zs{};
+      zs.m = t.m; zs.p = t.p; zs.L = L; zs.far_r = t.d_far_r.p; zs.far_c = t.d_far_c.p; zs.xi = t.d_xi.p;
+      zs.s = (const double2*)op.d_s.p; zs.pivk = op.d_pivk.p; zs.pivq = op.d_pivq.p; zs.foff = op.d_foff.p;
+      zs.F = (const double2*)op.d_F.p; zs.rcap = op.rcap;
+      const int nfar = (int)op.ranks.size();
+      if (nfar > 0) {
+        zgen_all_kernel<<<std::min(nfar, 148 * 16), 128, 0, st>>>(zs, nfar, op.d_rank.p, op.d_local_l.p, op.n_local,
+                                                                 op.d_zoff.p, (double2*)op.d_Z.p);
+        if (cudaGetLastError() != cudaSuccess) {
+          set_error("bem_assemble_h2_aca: zgen launch failed");
+          return fail(BEM_ECUDA);
+        }
+      }
+    }
+    op.z_stored = store;
   }
   if (mode == BEM_MODE_COMBINED) {
     if (t.max_leaf > 64) {  // K1m stages 3 slice buffers of 32 x max_leaf complex per CTA
       set_error("bem_assemble_h2_aca: BEM_MODE_COMBINED needs leaves of at most 64 panels (largest: %d)", t.max_leaf);
       return fail(BEM_EINVAL);
     }
-    bem_status rs = run_aca(op, st, true);
+    bem_status rs = run_aca(op, st, true, true);
     if (rs != BEM_OK) return fail(rs);
     // K1m launch order: row leaves by descending near-field MACA work (LPT)
     std::vector<std::pair<int64_t, int32_t>> w;
@@ -852,6 +774,10 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
       return fail(BEM_ECUDA);
     }
   }
+  {
+    bem_status rs = far_prepare(op);  // K3 Z-tile scratch (factors-only skeleton)
+    if (rs != BEM_OK) return fail(rs);
+  }
   const int64_t M = t.M;
   const size_t nl = (size_t)op.n_local;
   if (op.d_xc.alloc(nl * M * 2) != cudaSuccess || op.d_yc.alloc(nl * M * 2) != cudaSuccess) {
@@ -871,6 +797,31 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   }
   t.refcount++;
   *out = h;
+  return BEM_OK;
+}
+
+extern "C" bem_status bem_op_get_info(bem_op oh, bem_op_info* out) {
+  BEM_REQ(oh && out, "bem_op_get_info: NULL argument");
+  const Op& op = oh->o;
+  const bool aca = op.mode == BEM_MODE_H2ACA || op.mode == BEM_MODE_COMBINED;
+  out->mode = op.mode;
+  out->skeleton = aca ? (op.z_stored ? 1 : 2) : 0;
+  out->n_local = op.n_local;
+  int rmax = 0;
+  int64_t tot = 0;
+  for (int v : op.ranks) { rmax = std::max(rmax, v); tot += v; }
+  out->rmax = rmax;
+  out->total_rank = tot;
+  out->z_bytes = (int64_t)op.d_Z.n * 8;
+  out->f_bytes = (int64_t)op.d_F.n * 8;
+  const size_t dbl = op.d_s.n + op.d_Z.n + op.d_F.n + op.d_zs.n + op.d_part.n + op.d_nZ.n + op.d_nS.n + op.d_Df.n +
+                     op.d_Dn.n + op.d_fS.n + op.d_g0f.n + op.d_g0n.n + op.d_conv_part.n + op.d_xc.n + op.d_yc.n +
+                     op.d_xhat.n + op.d_yhat.n + op.step.tx.n + op.step.xf.n + op.step.yf.n + op.step.ty.n;
+  const size_t i32 = op.d_local_l.n + op.d_class_t1.n + op.d_class_t2.n + op.d_dn_jb.n + op.d_dn_je.n + op.d_dn_j.n +
+                     op.d_rank.n + op.d_pivk.n + op.d_pivq.n + op.d_far_rows.n + op.d_segs.n + op.d_seg_rows.n +
+                     op.d_seg_ptr.n + op.d_nrank.n + op.d_npivk.n + op.d_npivq.n + op.d_nm_order.n + op.d_nm_counter.n;
+  const size_t i64 = op.d_zoff.n + op.d_foff.n + op.d_nzoff.n + op.d_nsoff.n + op.d_fsoff.n + op.d_g0noff.n;
+  out->device_bytes = (int64_t)(8 * dbl + 4 * i32 + 8 * i64);
   return BEM_OK;
 }
 

@@ -123,7 +123,8 @@ struct Tree {
 struct StepGraph {
   DBuf<double> tx, xf, yf, ty;  // [L][M] complex each
   cudaStream_t own = nullptr;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;  // e2: end of the last call's D2H
+  bool used = false;
   cudaGraphExec_t exec = nullptr;
   double R = 0.0;
   StepGraph() = default;
@@ -149,7 +150,12 @@ struct Op {
   std::vector<int32_t> ranks;  // host copy
   DBuf<int32_t> d_rank, d_pivk, d_pivq;  // pivk/pivq: nfar * rcap
   DBuf<int64_t> d_zoff;                  // nfar
-  DBuf<double> d_Z;                      // pool: sum r_b * n_local complex
+  DBuf<double> d_Z;                      // pool: sum r_b * n_local complex (if z_stored)
+  DBuf<int64_t> d_foff;                  // nfar: offsets of F_b in d_F
+  DBuf<double> d_F;                      // pool: sum r_b^2 complex, F_b = C^_b (lower) + U_b (strict upper)
+  bool z_stored = true;                  // false: K3 regenerates Z tiles from F_b (factors-only)
+  int rmax = 0;                          // largest far rank (K3 Z-tile scratch)
+  DBuf<double> d_zs;                     // K3 Z-tile scratch (factors-only): per CTA [rmax][ZW]
   // row clusters owning far blocks, sorted by descending coupling work (K3 order)
   int n_far_rows = 0;
   DBuf<int32_t> d_far_rows;
@@ -177,33 +183,20 @@ struct Op {
   DBuf<double> d_conv_part;  // per-block partial sums of the time-domain convolution  // K1m CTA order: leaf indices by descending sum_b r_b n_c (LPT)
   // workspaces
   DBuf<double> d_xc, d_yc, d_xhat, d_yhat;
-  // kernel variants (tuning knobs; env BEM_NEAR_F, BEM_FAR_GENERIC read at assembly)
-  int near_f = 0;  // frequency classes per warp, 0 = automatic 4 or 5 (near.cu); F <= 5: the self term spreads
-                   // 6 nodes per class over the 32 lanes
-  int near_unroll = 7;
-  bool near_tab = true;
-  bool near_xlate = true;   // K1 loads x after the node loop: 128 instead of 164 registers, 4 CTAs/SM (env BEM_NEAR_XL)
+  // kernel selection (env BEM_FAR_KERNEL / BEM_FAR8_KC / BEM_FAR_GENERIC, read at assembly: tests)
   bool force_generic = false;
-  int far_kernel = 0;                 // 0: auto (far8 for p > 32, far7 otherwise); 8, 7, 6 (DMMA variants)
+  int far_kernel = 0;                 // 0: auto (far8 for p > 32, far7 otherwise); 8, 7
   size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM
-  size_t far_smem_min = 0;            // minimum dynamic smem of far7/far8 (residency experiments)
-  bool far7_rem_dfma = true;          // p = 27: rows 24..26 on DFMA instead of a padded DMMA tile
-  bool far7_cluster = false;          // DSMEM-shared slices across frequency tiles (measured slower, r01)
   int far8_kc = 0;                    // far8 nu-chunk width (0: automatic)
-  int far7_ttmax = 0;                 // cap on far7's frequency tile (0: none; env BEM_FAR7_TTMAX)
-  int far7_nw = 8;                    // far7 warps per CTA: 8 (2 CTAs/SM) or 16 (env BEM_FAR7_NW)
-  bool far7_m3 = false;               // far7/far8 3M complex products (env BEM_FAR7_M3)
-  int far8_nw = 8;                    // far8 warps per CTA: 8 or 6 (env BEM_FAR8_NW)
-  int aca_ctas_per_sm = 5;            // persistent ACA CTAs per SM = register-limited residency (env BEM_ACA_CTAS; r01: 4 -> 5-8 cut config-4 setup 2.96 -> 2.64 s)
-  bool far7_split = false;            // p = 27: 3M DMMA rows 0..23 + DFMA-only rows 24..26 (env BEM_FAR7_SPLIT)
-  int h2o_fc = 0;                     // K3' classes per CTA tile (0: 6 for p <= 32, else 2; env BEM_H2O_FC)
+  int aca_ctas_per_sm = 5;            // persistent ACA CTAs per SM = register-limited residency (r01: 4 -> 5 cut config-4 setup 2.96 -> 2.64 s)
+  int h2o_fc = 0;                     // K3' classes per CTA tile (0: 6 for p <= 32, else 2)
   // optional per-local-frequency mask (1 = compute); set only by the GMRES driver so that
   // converged frequencies skip K1 / K3 work (their outputs are then zero)
   const int32_t* d_mask = nullptr;
   bool use_solve_mask = true;  // env BEM_SOLVE_MASK=0 disables
   StepGraph step;  // bem_time_step
   // K1 || far-branch overlap (apply.cu): side stream and fork/join events, created lazily
-  bool overlap = true;  // env BEM_OVERLAP=0 disables
+  bool overlap = true;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // profiling
@@ -216,6 +209,7 @@ struct Op {
 bem_status apply_launch(Op& op, const double* x, double* y, cudaStream_t st, bool dl = false, double alpha = 0.0);
 bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st, bool dl = false);
 bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st);
+bem_status far_prepare(Op& op);  // K3 scratch of the factors-only skeleton (far.cu)
 bem_status launch_near_maca(Op& op, const double2* xc, double2* yc, cudaStream_t st);  // nearm.cu
 bem_status h2_gather(Op& op, const double2* x, double2* xc, int ncols, cudaStream_t st);
 bem_status h2_up(Op& op, const double2* xc, double2* xhat, int ncols, cudaStream_t st);

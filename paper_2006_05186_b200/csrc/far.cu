@@ -8,24 +8,31 @@
 //   yhat_r[:,t] += sum_b sum_j S_b(s_{k_j}) (Z_b[j,t] xhat_c[:,t]).
 // Only the pivot slices S_b(s_{k_j}) are evaluated ("only pivot frequencies
 // are evaluated", north_star); they are regenerated on the fly from the
-// kernel (no slice storage: 223 GB at config 4).
+// kernel (no slice storage: 223 GB at config 4).  The
+// coefficients Z_b come either from the stored pool or, in the factors-only
+// skeleton (BEM_SKEL_FACTORS), from the block's r_b x r_b LU factors: each CTA
+// regenerates the Z tile of its frequency columns in the block's prologue
+// (pivot fibres + two pinned triangular solves, zgen.cuh) into a per-CTA
+// scratch that stays in L2.
 //
 // Kernels (all deterministic: one CTA owns each output tile of a segment's
 // partial sum; segments of a row are reduced in fixed order, no atomics):
 //   far8_kernel / far7_kernel (default, p > 32 / p <= 32): the per-term slice
 //     product on the FP64 tensor cores (mma.sync m8n8k4 f64), slices
 //     regenerated in shared memory -- DESIGN.md §7;
-//   far6_kernel: the earlier DMMA variant (kept as a measured baseline, tested);
 //   h2o_kernel: BEM_MODE_H2ONLY, couplings evaluated per frequency on the fly
 //     (the paper's plain-H^2 comparison);
-//   far_generic_kernel: fallback for shapes the tiled kernels cannot hold.
+//   far_generic_kernel: fallback for shapes the tiled kernels cannot hold
+//     (stored Z only).
+// Variants measured slower in round 1 (far6, DSMEM-shared slices, 16- and
+// 6-warp CTAs, 3M complex products, split remainder rows) were removed; they
+// are in git history and profiles/r01_sweeps.md.
 #include <algorithm>
 #include <vector>
 
-#include <cooperative_groups.h>
-
 #include "common.cuh"
 #include "fastmath.cuh"
+#include "zgen.cuh"
 
 namespace bem {
 namespace {
@@ -56,231 +63,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// ------------------------------------------------ far6: transposed DMMA coupling
-// out[t, mu] += sum_j sum_nu (Z_b[j,t] xhat_c[nu,t]) S_b(s_{k_j})[mu,nu]
-// as an (M = t) x (N = mu) x (K = nu) FP64 tensor-core product per term j:
-//   A[t,nu] = Z_b[j,t] xhat_c[nu,t]  (formed in registers from the shared-memory
-//             xhat tile and the thread's Z values: one complex multiply per
-//             fragment, reused for all four 8-row mu tiles),
-//   B[nu,mu] = S_b(s_{k_j})[mu,nu]   (the regenerated slice rows in shared memory).
-// Warp w owns the 8-column t tiles {w, w+8, ...} and all four mu tiles of the
-// 32-row chunk.  Leftover columns (n_t mod 8, e.g. the real frequency l = 0
-// when L = 2^k + 1) are accumulated with DFMA by lanes 0..3 of each warp.
-struct Far6Args {
-  int nl, m, p, p4, rcap, SST, TT, XTP, nT, tb;  // tb = leftover columns [0, tb), DMMA columns [tb, nl)
-  const int4* segs;
-  const int32_t* far_sorted;
-  const int32_t* far_c;
-  const double* xi;
-  const double2* s;
-  const int32_t* rank;
-  const int32_t* pivk;
-  const int64_t* zoff;
-  const double2* Z;
-  const double2* xhat;
-  double2* part;
-};
-
-template <int MT>
-__global__ void __launch_bounds__(256, 2) far6_kernel(Far6Args a) {
-  extern __shared__ double2 sm[];
-  const int p = a.p, m = a.m, SST = a.SST, XTP = a.XTP, p4 = a.p4, tb = a.tb;
-  const int4 sg = a.segs[blockIdx.x];
-  const int r = sg.x;
-  const int tc0 = a.tb + blockIdx.y * a.TT;           // first DMMA column of this CTA
-  const int ncol = min(a.TT, a.nl - tc0);             // DMMA columns (multiple of 8)
-  const bool lead = blockIdx.y == 0;                  // also owns the leftover columns
-  const int mu0 = blockIdx.z * 32;
-  const int nrow = min(32, p - mu0);
-  double2* S = sm;                                    // 32 x SST (rows mu, cols nu)
-  double2* xs = S + 32 * SST;                         // p4 x XTP: [nu][0..tb) leftover, [tb..) DMMA cols
-  double* xr = (double*)(xs + (size_t)p4 * XTP);      // 3 x 32
-  double* xcn = xr + 96;                              // 3p
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, q = lane & 3;
-  for (int i = tid; i < 32 * SST + p4 * XTP; i += blockDim.x) sm[i] = make_double2(0.0, 0.0);
-  for (int i = tid; i < nrow; i += blockDim.x) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
-  const int ntile = ncol / 8;
-  double acc[MT][4][2][2];  // [t tile][mu tile][re/im][v]
-#pragma unroll
-  for (int i = 0; i < MT; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
-  double2 lacc[8];  // leftover columns, lanes 0..3 of each warp own row 4*warp + lane
-#pragma unroll
-  for (int i = 0; i < 8; ++i) lacc[i] = make_double2(0.0, 0.0);
-  const int lrow = 4 * warp + lane;
-  const bool lown = lead && lane < 4 && lrow < nrow && tb > 0;
-  const int ncp = tb + ncol;  // staged columns: leftover (lead only) + DMMA
-  for (int bi = sg.y; bi < sg.z; ++bi) {
-    const int b = a.far_sorted[bi];
-    const int c = a.far_c[b];
-    __syncthreads();
-    for (int i = tid; i < p; i += blockDim.x) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
-    // stage xhat_c: leftover columns (lead CTA) and this CTA's DMMA columns
-    const double2* xh = a.xhat + (int64_t)c * a.nl * p;
-    for (int idx = tid; idx < ncp * p; idx += blockDim.x) {
-      const int tl = idx / p, nu = idx - tl * p;
-      const int tg = tl < tb ? tl : tc0 + (tl - tb);
-      if (tl >= tb || lead) xs[nu * XTP + tl] = xh[(int64_t)tg * p + nu];
-    }
-    const int rk = a.rank[b];
-    const double2* Zb = a.Z + a.zoff[b];
-    for (int l = 0; l < rk; ++l) {
-      const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + l]];
-      const double2* Zl = Zb + (int64_t)l * a.nl;
-      double2 zt[MT];
-#pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        const int tt = warp + 8 * i;
-        zt[i] = tt < ntile ? Zl[tc0 + tt * 8 + g] : make_double2(0.0, 0.0);
-      }
-      __syncthreads();
-      for (int idx = tid; idx < nrow * p; idx += blockDim.x) {
-        const int i = idx / p, nu = idx - i * p;
-        const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
-                     dz = xcn[3 * nu + 2] - xr[3 * i + 2];
-        S[i * SST + nu] = kern(sqrt(dx * dx + dy * dy + dz * dz), sv);
-      }
-      __syncthreads();
-      for (int k0 = 0; k0 < p4; k0 += 4) {
-        double2 bf[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = S[(j * 8 + g) * SST + k0 + q];
-#pragma unroll
-        for (int i = 0; i < MT; ++i) {
-          const int tt = warp + 8 * i;
-          if (tt < ntile) {
-            const double2 xv = xs[(k0 + q) * XTP + tb + tt * 8 + g];
-            const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
-            const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
-            const double nai = -ai;
-            // two passes: dependent DMMAs on one accumulator are 2*4 instructions apart
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
-              dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
-              dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
-            }
-          }
-        }
-      }
-      if (lown) {
-        for (int tl = 0; tl < tb; ++tl) {
-          const double2 z = Zl[tl];
-          double2 sacc = make_double2(0.0, 0.0);
-          for (int nu = 0; nu < p; ++nu) {
-            const double2 sv2 = S[lrow * SST + nu], xv = xs[nu * XTP + tl];
-            sacc.x += sv2.x * xv.x - sv2.y * xv.y;
-            sacc.y += sv2.x * xv.y + sv2.y * xv.x;
-          }
-          lacc[tl].x += z.x * sacc.x - z.y * sacc.y;
-          lacc[tl].y += z.x * sacc.y + z.y * sacc.x;
-        }
-      }
-    }
-  }
-  double2* out = a.part + (int64_t)sg.w * a.nl * p;
-#pragma unroll
-  for (int i = 0; i < MT; ++i) {
-    const int tt = warp + 8 * i;
-    if (tt >= ntile) continue;
-    const int t = tc0 + tt * 8 + g;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int row = j * 8 + 2 * q + v;
-        if (row < nrow) out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
-      }
-  }
-  if (lown)
-    for (int tl = 0; tl < tb; ++tl) out[(int64_t)tl * p + mu0 + lrow] = lacc[tl];
-}
-
-struct Far6Cfg {
-  int p4 = 0, SST = 0, TT = 0, XTP = 0, nT = 0, tb = 0, ntiles = 0, nchunks = 0, mt = 0;
-  size_t smem = 0;
-};
-
-Far6Cfg choose6(int p, int nl, size_t cap) {
-  Far6Cfg c;
-  const int tb = nl % 8;
-  const int nD = nl - tb;
-  if (nD == 0) return c;
-  const int p4 = (p + 3) / 4 * 4;
-  int SST = p4;
-  while (SST % 8 != 4) ++SST;
-  for (int TTmax : {256, 128, 64, 32, 16, 8}) {
-    const int ntiles = (nD + TTmax - 1) / TTmax;
-    const int TT = ((nD / 8 + ntiles - 1) / ntiles) * 8;
-    int XTP = tb + TT;
-    while (XTP % 8 != 2) ++XTP;  // fragment loads [k][t]: stride 2 (mod 8) complex -> conflict-free
-    const size_t smem = sizeof(double2) * (32 * (size_t)SST + (size_t)p4 * XTP) + sizeof(double) * (96 + 3 * p);
-    if (smem > cap) continue;
-    c.p4 = p4; c.SST = SST; c.TT = TT; c.XTP = XTP; c.nT = TT / 8; c.tb = tb; c.ntiles = ntiles;
-    c.nchunks = (p + 31) / 32; c.mt = (c.nT + 7) / 8; c.smem = smem;
-    if (c.mt > 4) continue;
-    return c;
-  }
-  return Far6Cfg{};
-}
-
-template <int MT>
-cudaError_t launch6(const Far6Cfg& c, int nseg, const Far6Args& a, cudaStream_t st) {
-  auto k = far6_kernel<MT>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-  if (e != cudaSuccess) return e;
-  k<<<dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks), 256, c.smem, st>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t dispatch6(const Far6Cfg& c, int nseg, const Far6Args& a, cudaStream_t st) {
-  switch (c.mt) {
-    case 1: return launch6<1>(c, nseg, a, st);
-    case 2: return launch6<2>(c, nseg, a, st);
-    case 3: return launch6<3>(c, nseg, a, st);
-    case 4: return launch6<4>(c, nseg, a, st);
-    default: return cudaErrorInvalidConfiguration;
-  }
-}
-
-// ------------------------------------------- far7: far6 + cluster-shared slices
-// Same DMMA product as far6 (out[t,mu] += sum_nu (Z_b[j,t] xhat_c[nu,t]) S_j[mu,nu]),
-// with three changes measured on B200 (profiles/r01_*):
-//  * the CTAs that own the frequency tiles of one (segment, mu chunk) form a
-//    thread-block cluster (cluster dims (1, ntiles, 1), ntiles <= 8); each CTA
-//    regenerates only 1/ntiles of the slice S_b(s_{k_j}) into a double-
-//    buffered "own" region and copies the peers' parts through distributed
-//    shared memory, so a slice is evaluated once per apply instead of once
-//    per frequency tile (8x at config 4);
-//  * up to two leftover columns (n_l mod 8, e.g. the real frequency l = 0
-//    when L = 2^k + 1) are accumulated by all 256 threads of the lead CTA
-//    (row = tid/8, every 8th nu; one 8-lane shuffle reduction at the end)
-//    instead of 4 lanes per warp; more leftovers are zero-padded DMMA columns;
-//  * slice entries use rsqrt (no IEEE division / sqrt) and the table exp.
-struct Far7Args {
-  int nl, m, p, p4, rcap, SST, TT, XTP, nT, tb, nd, cs, own;  // DMMA columns [tb, tb+nd) (padded past nl);
-                                                            // own = slice entries regenerated per cluster CTA
-  int mu_base = 0, rows = 1 << 30;  // this launch covers rows [mu_base, mu_base + rows) (REM split)
-  const int4* segs;
-  const int32_t* far_sorted;
-  const int32_t* far_c;
-  const double* xi;
-  const double2* s;
-  const int32_t* rank;
-  const int32_t* pivk;
-  const int64_t* zoff;
-  const double2* Z;
-  const double2* xhat;
-  double2* part;
-  const int32_t* mask;  // nullable: per local frequency, 0 = skip (output 0)
-};
-
+// slice entry k(r; s) with rsqrt (no IEEE division / sqrt) and the table exp / sincos
 __device__ __forceinline__ double2 kern_rs(double d2, double2 s, const double* etab, const double2* sctab) {
   const double ir = rsqrt(d2);
   const double r = d2 * ir;
@@ -290,13 +73,70 @@ __device__ __forceinline__ double2 kern_rs(double d2, double2 s, const double* e
   return make_double2(e * cs, -e * sn);
 }
 
+// Where the coefficients Z_b[j, t] come from (stored pool or per-CTA regenerated tile).
+struct ZSrc {
+  const int64_t* zoff;  // stored: Z_b at Z + zoff[b], [r_b][nl]
+  const double2* Z;
+  zgen::Src g;          // factors-only: F_b, pivots, nodes, s
+  const int32_t* local_l;
+  double2* scr;         // per CTA [rmax][ZW]
+  int ZW, rmax;
+};
+
+// Coefficient rows of block b for this CTA's columns.  Returns zD, zL and the row
+// stride such that Z_b[j, t] = zD[j * stride + t] for the tile's DMMA columns t and
+// zL[j * stride + t] for the leftover columns t < tb.  FAC: the tile is regenerated here
+// (columns [0, tb) leftover -- lead CTA only -- then [tc0, tc0 + ncol)); the caller
+// synchronises the CTA before the first read.
+template <bool FAC>
+__device__ __forceinline__ void ztile(const ZSrc& z, int b, int rk, int nl, int tb, int tc0, int ncp, bool lead,
+                                      const int32_t* mask, const double2*& zD, const double2*& zL, int& stride) {
+  if constexpr (!FAC) {
+    zD = zL = z.Z + z.zoff[b];
+    stride = nl;
+  } else {
+    double2* scr = z.scr + (int64_t)(blockIdx.x + gridDim.x * blockIdx.y) * z.rmax * z.ZW;
+    for (int c = threadIdx.x; c < ncp; c += blockDim.x) {
+      if (c < tb && !lead) continue;
+      const int t = c < tb ? c : tc0 + (c - tb);
+      const int l = (t < nl && (mask == nullptr || mask[t])) ? z.local_l[t] : -1;
+      zgen::column(z.g, b, rk, l, scr + c, z.ZW);
+    }
+    zL = scr;
+    zD = scr + (tb - tc0);
+    stride = z.ZW;
+  }
+}
+
+// ------------------------------------------------ far7: p <= 32, whole p staged
+// out[t, mu] += sum_j sum_nu (Z_b[j,t] xhat_c[nu,t]) S_b(s_{k_j})[mu,nu]
+// as an (M = t) x (N = mu) x (K = nu) FP64 tensor-core product per term j:
+//   A[t,nu] = Z_b[j,t] xhat_c[nu,t]  (formed in registers from the shared-memory
+//             xhat tile and the thread's Z values: one complex multiply per
+//             fragment, reused for the mu tiles),
+//   B[nu,mu] = S_b(s_{k_j})[mu,nu]   (the regenerated slice rows in shared memory,
+//             double-buffered: one barrier per term, warps may run a term apart).
 // NJ DMMA mu tiles per 32-row chunk; REM further rows (p = 27: rows 24..26) on
-// DFMA from the same A fragments instead of a 5/8-empty fourth DMMA tile.
-// NW: warps per CTA (8: two CTAs per SM; 16: one CTA per SM whose 16 warps share every
-// regenerated slice); M3: 3M complex products (three real DMMAs per complex one,
-// Re = P1 - P2, Im = P3 - P1 - P2 with P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi)).
-template <int MT, bool CL, int NJ, int REM, int NW = 8, bool M3 = false>
-__global__ void __launch_bounds__(NW * 32, 16 / NW) far7_kernel(Far7Args a) {
+// DFMA from the same A fragments instead of a 5/8-empty fourth DMMA tile.  Up to
+// two leftover columns (n_l mod 8, e.g. the real l = 0 when L = 2^k + 1) are
+// accumulated by all 256 threads of the lead CTA; more are zero-padded DMMA columns.
+struct Far7Args {
+  int nl, m, p, p4, rcap, SST, TT, XTP, tb, nd;  // DMMA columns [tb, tb+nd) (padded past nl)
+  const int4* segs;
+  const int32_t* far_sorted;
+  const int32_t* far_c;
+  const double* xi;
+  const double2* s;
+  const int32_t* rank;
+  const int32_t* pivk;
+  ZSrc z;
+  const double2* xhat;
+  double2* part;
+  const int32_t* mask;  // nullable: per local frequency, 0 = skip (output 0)
+};
+
+template <int MT, int NJ, int REM, bool FAC>
+__global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
   extern __shared__ double2 sm[];
   const int p = a.p, m = a.m, SST = a.SST, XTP = a.XTP, p4 = a.p4, tb = a.tb;
   const int4 sg = a.segs[blockIdx.x];
@@ -304,33 +144,29 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) far7_kernel(Far7Args a) {
   const int tc0 = a.tb + blockIdx.y * a.TT;
   const int ncol = min(a.TT, a.tb + a.nd - tc0);
   const bool lead = blockIdx.y == 0;
-  const int mu0 = a.mu_base + blockIdx.z * 32;
-  const int nrow = min(32, min(p, a.mu_base + a.rows) - mu0);
+  const int mu0 = blockIdx.z * 32;
+  const int nrow = min(32, p - mu0);
   const int nS = nrow * p;
   double2* S0 = sm;                                   // 2 x (32 x SST): double-buffered slice rows
-  double2* own = S0 + 2 * 32 * SST;                   // CL: 2 x a.own
-  double2* xs = own + (CL ? 2 * a.own : 0);           // p4 x XTP
+  double2* xs = S0 + 2 * 32 * SST;                    // p4 x XTP
   double2* sctab = xs + (size_t)p4 * XTP;             // 64 (cos, sin)(k pi/32)
   double* etab = (double*)(sctab + 64);               // 64
   double* xr = etab + 64;                             // 96
   double* xcn = xr + 96;                              // 3p
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
-  for (int i = tid; i < 2 * 32 * SST + p4 * XTP + (CL ? 2 * a.own : 0); i += blockDim.x) sm[i] = make_double2(0.0, 0.0);
+  for (int i = tid; i < 2 * 32 * SST + p4 * XTP; i += blockDim.x) sm[i] = make_double2(0.0, 0.0);
   for (int i = tid; i < 64; i += blockDim.x) {
     etab[i] = fast::kExp2Tab[i];
     sctab[i] = fast::kSinCosTab[i];
   }
   for (int i = tid; i < nrow; i += blockDim.x) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
-  int crank = 0;
-  if (CL) crank = (int)cooperative_groups::this_cluster().block_rank();
-  const int e0 = crank * a.own, e1 = min(nS, e0 + a.own);  // this CTA's share of the slice entries
   const int ntile = ncol / 8;
   bool ton[MT];  // 8-column frequency tile has at least one unmasked column (GMRES mask)
   bool cta_on = false;
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
-    const int tt = warp + NW * i;
+    const int tt = warp + 8 * i;
     const int t = tc0 + tt * 8 + g;
     const bool v = tt < ntile && t < a.nl && (a.mask == nullptr || a.mask[t]);
     ton[i] = __any_sync(0xffffffffu, v);
@@ -340,32 +176,32 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) far7_kernel(Far7Args a) {
     for (int t = tid; t < ncol; t += blockDim.x) lo |= (tc0 + t < a.nl) && (a.mask == nullptr || a.mask[tc0 + t]);
     if (lead) for (int t = tid; t < tb; t += blockDim.x) lo |= a.mask == nullptr || a.mask[t];
     cta_on = __syncthreads_or(lo) != 0;
-    if (CL) cta_on = true;  // every CTA of a cluster must reach the same cluster barriers
   }
-  double acc[MT][NJ > 0 ? NJ : 1][M3 ? 3 : 2][2];
+  double acc[MT][NJ > 0 ? NJ : 1][2][2];
   double2 racc[MT][REM > 0 ? REM : 1];
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
 #pragma unroll
-    for (int j = 0; j < NJ; ++j)
-#pragma unroll
-      for (int u = 0; u < (M3 ? 3 : 2); ++u) acc[i][j][u][0] = acc[i][j][u][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
 #pragma unroll
     for (int j = 0; j < (REM > 0 ? REM : 1); ++j) racc[i][j] = make_double2(0.0, 0.0);
   }
   // leftover columns: thread -> (row lrow, nu residue lpart)
   const int lrow = tid >> 3, lpart = tid & 7;
   const bool lown = lead && tb > 0 && lrow < nrow;
-  // leftover-column accumulators in shared memory (used once per term by the lead CTA;
-  // as registers they were live through the whole kernel and caused spills)
+  // leftover-column accumulators in shared memory (registers would be live through the
+  // whole kernel and spill)
   double2* lacc = (double2*)(((uintptr_t)(xcn + 3 * p) + 15) & ~(uintptr_t)15) + 2 * tid;
   lacc[0] = lacc[1] = make_double2(0.0, 0.0);
   const int ncp = tb + ncol;
-  int buf = 0;
   for (int bi = sg.y; bi < (cta_on ? sg.z : sg.y); ++bi) {
     const int b = a.far_sorted[bi];
     const int c = a.far_c[b];
+    const int rk = a.rank[b];
     __syncthreads();
+    const double2 *zD, *zL;
+    int zst;
+    ztile<FAC>(a.z, b, rk, a.nl, tb, tc0, ncp, lead, a.mask, zD, zL, zst);
     for (int i = tid; i < p; i += blockDim.x) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
     const double2* xh = a.xhat + (int64_t)c * a.nl * p;
     for (int idx = tid; idx < ncp * p; idx += blockDim.x) {
@@ -373,50 +209,25 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) far7_kernel(Far7Args a) {
       const int tg = tl < tb ? tl : tc0 + (tl - tb);
       if (tl >= tb || lead) xs[nu * XTP + tl] = tg < a.nl ? xh[(int64_t)tg * p + nu] : make_double2(0.0, 0.0);
     }
-    const int rk = a.rank[b];
-    const double2* Zb = a.Z + a.zoff[b];
     __syncthreads();
     for (int l = 0; l < rk; ++l) {
-      // non-cluster path: S alternates between two buffers, so one barrier per
-      // term suffices and warps may run one term apart (regeneration of term
-      // l+1 overlaps other warps' DMMA work on term l)
-      double2* S = S0 + (CL ? 0 : (l & 1) * 32 * SST);
+      double2* S = S0 + (l & 1) * 32 * SST;
       const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + l]];
-      const double2* Zl = Zb + (int64_t)l * a.nl;
+      const double2* Zl = zD + (int64_t)l * zst;
       double2 zt[MT];
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
-        const int tt = warp + NW * i;
+        const int tt = warp + 8 * i;
         const int t = tc0 + tt * 8 + g;
         zt[i] = (tt < ntile && t < a.nl) ? Zl[t] : make_double2(0.0, 0.0);
       }
-      if (CL) {
-        double2* ob = own + buf * a.own;
-        for (int e = e0 + tid; e < e1; e += blockDim.x) {
-          const int i = e / p, nu = e - i * p;
-          const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
-                       dz = xcn[3 * nu + 2] - xr[3 * i + 2];
-          ob[e - e0] = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab, sctab);
-        }
-        cooperative_groups::this_cluster().sync();  // all parts ready; every local warp is past its GEMM
-        for (int e = tid; e < nS; e += blockDim.x) {
-          const int owner = e / a.own;
-          const double2* src = owner == crank ? ob
-                                              : cooperative_groups::this_cluster().map_shared_rank(ob, owner);
-          const int i = e / p, nu = e - i * p;
-          S[i * SST + nu] = src[e - owner * a.own];
-        }
-        buf ^= 1;
-        __syncthreads();
-      } else {
-        for (int e = tid; e < nS; e += blockDim.x) {
-          const int i = e / p, nu = e - i * p;
-          const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
-                       dz = xcn[3 * nu + 2] - xr[3 * i + 2];
-          S[i * SST + nu] = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab, sctab);
-        }
-        __syncthreads();
+      for (int e = tid; e < nS; e += blockDim.x) {
+        const int i = e / p, nu = e - i * p;
+        const double dx = xcn[3 * nu] - xr[3 * i], dy = xcn[3 * nu + 1] - xr[3 * i + 1],
+                     dz = xcn[3 * nu + 2] - xr[3 * i + 2];
+        S[i * SST + nu] = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab, sctab);
       }
+      __syncthreads();
       for (int k0 = 0; k0 < p4; k0 += 4) {
         double2 bf[NJ > 0 ? NJ : 1], rf[REM > 0 ? REM : 1];
 #pragma unroll
@@ -425,32 +236,22 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) far7_kernel(Far7Args a) {
         for (int j = 0; j < REM; ++j) rf[j] = S[(NJ * 8 + j) * SST + k0 + q];
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
-          const int tt = warp + NW * i;
+          const int tt = warp + 8 * i;
           if (tt < ntile && ton[i]) {
             const double2 xv = xs[(k0 + q) * XTP + tb + tt * 8 + g];
             const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
             const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
             const double nai = -ai;
-            if constexpr (M3) {
-              const double as = ar + ai;
+            // two passes: dependent DMMAs on one accumulator are 2*NJ instructions apart
 #pragma unroll
-              for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+            for (int j = 0; j < NJ; ++j) {
+              dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+              dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
+            }
 #pragma unroll
-              for (int j = 0; j < NJ; ++j) dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].y);
-#pragma unroll
-              for (int j = 0; j < NJ; ++j) dmma(acc[i][j][M3 ? 2 : 0][0], acc[i][j][M3 ? 2 : 0][1], as, bf[j].x + bf[j].y);
-            } else {
-              // two passes: dependent DMMAs on one accumulator are 2*NJ instructions apart
-#pragma unroll
-              for (int j = 0; j < NJ; ++j) {
-                dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
-                dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
-              }
-#pragma unroll
-              for (int j = 0; j < NJ; ++j) {
-                dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
-                dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
-              }
+            for (int j = 0; j < NJ; ++j) {
+              dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
+              dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
             }
 #pragma unroll
             for (int j = 0; j < REM; ++j) {  // partial over this lane's k = k0 + q; reduced over q at the end
@@ -472,9 +273,9 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) far7_kernel(Far7Args a) {
             sacc.y = fma(sv2.x, xv.y, sacc.y);
             sacc.y = fma(sv2.y, xv.x, sacc.y);
           }
-          const double2 z = Zl[tl];
-          lacc[tl].x = fma(z.x, sacc.x, fma(-z.y, sacc.y, lacc[tl].x));
-          lacc[tl].y = fma(z.x, sacc.y, fma(z.y, sacc.x, lacc[tl].y));
+          const double2 zz = zL[(int64_t)l * zst + tl];
+          lacc[tl].x = fma(zz.x, sacc.x, fma(-zz.y, sacc.y, lacc[tl].x));
+          lacc[tl].y = fma(zz.x, sacc.y, fma(zz.y, sacc.x, lacc[tl].y));
         }
       }
     }
@@ -482,7 +283,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) far7_kernel(Far7Args a) {
   double2* out = a.part + (int64_t)sg.w * a.nl * p;
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
-    const int tt = warp + NW * i;
+    const int tt = warp + 8 * i;
     if (tt >= ntile) continue;
     const int t = tc0 + tt * 8 + g;
     if (t >= a.nl) continue;
@@ -491,19 +292,13 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) far7_kernel(Far7Args a) {
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int row = j * 8 + 2 * q + v;
-        if (row < nrow) {
-          if constexpr (M3)
-            out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v] - acc[i][j][1][v],
-                                                           acc[i][j][M3 ? 2 : 0][v] - acc[i][j][0][v] - acc[i][j][1][v]);
-          else
-            out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
-        }
+        if (row < nrow) out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
       }
   }
   if (REM > 0) {
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
-      const int tt = warp + NW * i;  // warp-uniform
+      const int tt = warp + 8 * i;  // warp-uniform
       if (tt >= ntile) continue;
       const int t = tc0 + tt * 8 + g;
 #pragma unroll
@@ -530,115 +325,57 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) far7_kernel(Far7Args a) {
       if (lpart == 0 && lrow < nrow) out[(int64_t)tl * p + mu0 + lrow] = v;
     }
   }
-  if (CL) cooperative_groups::this_cluster().sync();  // peers may still read our own[] region
 }
 
 struct Far7Cfg {
-  int p4 = 0, SST = 0, TT = 0, XTP = 0, nT = 0, tb = 0, nd = 0, ntiles = 0, nchunks = 0, mt = 0, cs = 1, own = 0;
+  int p4 = 0, SST = 0, TT = 0, XTP = 0, tb = 0, nd = 0, ntiles = 0, nchunks = 0, mt = 0;
   size_t smem = 0;
 };
 
-Far7Cfg choose7(int p, int nl, size_t cap, bool cluster, int ttmax_cap = 0, int nw = 8) {
+Far7Cfg choose7(int p, int nl, size_t cap) {
   int tb = nl % 8;
   if (tb > 2 || tb == nl) tb = 0;  // pad instead (zero columns past nl)
   const int nD = (nl - tb + 7) / 8 * 8;
   const int p4 = (p + 3) / 4 * 4;
   int SST = p4;
   while (SST % 8 != 4) ++SST;
-  const int nrow = std::min(p, 32);
   for (int TTmax : {256, 128, 64, 32, 16, 8}) {
-    if (ttmax_cap > 0 && TTmax > ttmax_cap) continue;
     Far7Cfg c;
     const int ntiles = (nD + TTmax - 1) / TTmax;
     const int TT = ((nD / 8 + ntiles - 1) / ntiles) * 8;
     int XTP = tb + TT;
     while (XTP % 8 != 2) ++XTP;
-    const int cs = (cluster && ntiles > 1 && ntiles <= 8) ? ntiles : 1;
-    const int own = cs > 1 ? (nrow * p + cs - 1) / cs : 0;
-    const size_t smem = sizeof(double2) * (2 * 32 * (size_t)SST + (size_t)p4 * XTP + 2 * (size_t)own + 64 + 2 * 32 * (size_t)nw) + 16 +
+    const size_t smem = sizeof(double2) * (2 * 32 * (size_t)SST + (size_t)p4 * XTP + 64 + 2 * 256) + 16 +
                         sizeof(double) * (64 + 96 + 3 * p);
     if (smem > cap) continue;
-    c.p4 = p4; c.SST = SST; c.TT = TT; c.XTP = XTP; c.nT = TT / 8; c.tb = tb; c.nd = nD; c.ntiles = ntiles;
-    c.nchunks = (p + 31) / 32; c.mt = (c.nT + nw - 1) / nw; c.smem = smem; c.cs = cs; c.own = own;
+    c.p4 = p4; c.SST = SST; c.TT = TT; c.XTP = XTP; c.tb = tb; c.nd = nD; c.ntiles = ntiles;
+    c.nchunks = (p + 31) / 32; c.mt = (TT / 8 + 7) / 8; c.smem = smem;
     if (c.mt > 2) continue;  // MT >= 3 spills at 128 registers
     return c;
   }
   return Far7Cfg{};
 }
 
-template <int MT, bool CL, int NJ, int REM, bool M3 = false>
+template <int MT, int NJ, int REM, bool FAC>
 cudaError_t launch7(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream_t st) {
-  auto k = far7_kernel<MT, CL, NJ, REM, 8, M3>;
+  auto k = far7_kernel<MT, NJ, REM, FAC>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   if (e != cudaSuccess) return e;
-  if (!CL) {
-    k<<<dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks), 256, c.smem, st>>>(a);
-    return cudaGetLastError();
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks);
-  cfg.blockDim = dim3(256, 1, 1);
-  cfg.dynamicSmemBytes = c.smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 1;
-  at[0].val.clusterDim.y = CL ? (unsigned)c.cs : 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, k, a);
-  if (e != cudaSuccess) return e;
+  k<<<dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks), 256, c.smem, st>>>(a);
   return cudaGetLastError();
 }
 
-template <int NJ, int REM>
+template <int NJ, int REM, bool FAC>
 cudaError_t dispatch7_(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream_t st) {
-  const bool cl = c.cs > 1;
-  switch (c.mt) {
-    case 1: return cl ? launch7<1, true, NJ, REM>(c, nseg, a, st) : launch7<1, false, NJ, REM>(c, nseg, a, st);
-    case 2: return cl ? launch7<2, true, NJ, REM>(c, nseg, a, st) : launch7<2, false, NJ, REM>(c, nseg, a, st);
-    default: return cudaErrorInvalidConfiguration;
-  }
-}
-
-// 16-warp CTAs (one per SM, one t-tile per warp): every regenerated slice serves 16 warps
-template <int NJ, int REM, bool M3>
-cudaError_t launch7w(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream_t st) {
-  if (c.mt != 1 || c.cs > 1) return cudaErrorInvalidConfiguration;
-  auto k = far7_kernel<1, false, NJ, REM, 16, M3>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-  if (e != cudaSuccess) return e;
-  k<<<dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks), 512, c.smem, st>>>(a);
-  return cudaGetLastError();
+  return c.mt == 1 ? launch7<1, NJ, REM, FAC>(c, nseg, a, st) : launch7<2, NJ, REM, FAC>(c, nseg, a, st);
 }
 
 // mu tiling: p = 27 -> 3 DMMA tiles + 3 DFMA rows; p <= 8 -> 1 tile; otherwise 4 tiles per 32-row chunk
-cudaError_t dispatch7(const Far7Cfg& c, int p, bool rem_dfma, int nseg, const Far7Args& a, cudaStream_t st,
-                      int nw = 8, bool m3 = false, bool split = false) {
-  if (nw == 16) {
-    if (p <= 8) return m3 ? launch7w<1, 0, true>(c, nseg, a, st) : launch7w<1, 0, false>(c, nseg, a, st);
-    if (p == 27 && rem_dfma) return m3 ? launch7w<3, 3, true>(c, nseg, a, st) : launch7w<3, 3, false>(c, nseg, a, st);
-    return m3 ? launch7w<4, 0, true>(c, nseg, a, st) : launch7w<4, 0, false>(c, nseg, a, st);
-  }
-  if (p == 27 && split && c.cs == 1) {
-    // rows 0..23: 3M DMMA tiles (no DFMA rows: room for the third accumulator at MT = 2);
-    // rows 24..26: a DFMA-only launch of the same kernel (NJ = 0) into the same partial slots
-    Far7Args a1 = a, a2 = a;
-    a1.mu_base = 0; a1.rows = 24;
-    a2.mu_base = 24; a2.rows = 3;
-    Far7Cfg c2 = c;
-    c2.nchunks = 1;
-    cudaError_t e = c.mt == 1 ? launch7<1, false, 3, 0, true>(c2, nseg, a1, st) : launch7<2, false, 3, 0, true>(c2, nseg, a1, st);
-    if (e != cudaSuccess) return e;
-    return c.mt == 1 ? launch7<1, false, 0, 3, false>(c2, nseg, a2, st) : launch7<2, false, 0, 3, false>(c2, nseg, a2, st);
-  }
-  if (m3 && c.mt == 1 && c.cs == 1 && p > 8)  // 3M at one t-tile per warp (room for the third accumulator)
-    return (p == 27 && rem_dfma) ? launch7<1, false, 3, 3, true>(c, nseg, a, st)
-                                 : launch7<1, false, 4, 0, true>(c, nseg, a, st);
-  if (p <= 8) return dispatch7_<1, 0>(c, nseg, a, st);
-  if (p == 27 && rem_dfma) return dispatch7_<3, 3>(c, nseg, a, st);
-  return dispatch7_<4, 0>(c, nseg, a, st);
+template <bool FAC>
+cudaError_t dispatch7(const Far7Cfg& c, int p, int nseg, const Far7Args& a, cudaStream_t st) {
+  if (p <= 8) return dispatch7_<1, 0, FAC>(c, nseg, a, st);
+  if (p == 27) return dispatch7_<3, 3, FAC>(c, nseg, a, st);
+  return dispatch7_<4, 0, FAC>(c, nseg, a, st);
 }
 
 // ------------------------------------------------ far8: far7 with K (nu) chunks
@@ -647,9 +384,7 @@ cudaError_t dispatch7(const Far7Cfg& c, int p, bool rem_dfma, int nseg, const Fa
 // ACA term j the slice columns S_j[mu-chunk][nu-chunk] are regenerated and
 // contracted.  Regeneration per (b, j) is unchanged (every slice entry is
 // evaluated once per CTA), but shared memory no longer grows with p, so the
-// frequency tile stays at TT = 128 with two CTAs per SM for p = 64 and 125
-// (far7 had to drop to TT <= 64, i.e. >= 2x more slice regeneration per
-// frequency, at p = 64 and could not hold p = 125 at all).
+// frequency tile stays at TT = 128 with two CTAs per SM for p = 64 and 125.
 struct Far8Args {
   int nl, m, p, rcap, SST, TT, XTP, tb, nd, KC;
   int nch = 1;  // mu chunks (grid x = segment * nch + chunk)
@@ -660,17 +395,14 @@ struct Far8Args {
   const double2* s;
   const int32_t* rank;
   const int32_t* pivk;
-  const int64_t* zoff;
-  const double2* Z;
+  ZSrc z;
   const double2* xhat;
   double2* part;
   const int32_t* mask;  // nullable: per local frequency, 0 = skip (output 0)
 };
 
-// M3: 3M complex products (as far7); NW warps per CTA (6: up to 170 registers at two CTAs
-// per SM, room for the 3M accumulators at MT = 2; leftover columns are then padded)
-template <int MT, int NJ, int REM, bool M3 = false, int NW = 8>
-__global__ void __launch_bounds__(NW * 32, 2) far8_kernel(Far8Args a) {
+template <int MT, int NJ, int REM, bool FAC>
+__global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
   extern __shared__ double2 sm[];
   const int p = a.p, m = a.m, SST = a.SST, XTP = a.XTP, tb = a.tb, KC = a.KC;
   // the mu chunks of one (segment, tile) are adjacent CTAs: the second chunk re-reads the
@@ -702,7 +434,7 @@ __global__ void __launch_bounds__(NW * 32, 2) far8_kernel(Far8Args a) {
   bool cta_on = false;
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
-    const int tt = warp + NW * i;
+    const int tt = warp + 8 * i;
     const int t = tc0 + tt * 8 + g;
     const bool v = tt < ntile && t < a.nl && (a.mask == nullptr || a.mask[t]);
     ton[i] = __any_sync(0xffffffffu, v);
@@ -713,14 +445,12 @@ __global__ void __launch_bounds__(NW * 32, 2) far8_kernel(Far8Args a) {
     if (lead) for (int t = tid; t < tb; t += blockDim.x) lo |= a.mask == nullptr || a.mask[t];
     cta_on = __syncthreads_or(lo) != 0;
   }
-  double acc[MT][NJ][M3 ? 3 : 2][2];
+  double acc[MT][NJ][2][2];
   double2 racc[MT][REM > 0 ? REM : 1];
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
 #pragma unroll
-    for (int j = 0; j < NJ; ++j)
-#pragma unroll
-      for (int u = 0; u < (M3 ? 3 : 2); ++u) acc[i][j][u][0] = acc[i][j][u][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
 #pragma unroll
     for (int j = 0; j < (REM > 0 ? REM : 1); ++j) racc[i][j] = make_double2(0.0, 0.0);
   }
@@ -733,8 +463,10 @@ __global__ void __launch_bounds__(NW * 32, 2) far8_kernel(Far8Args a) {
     const int c = a.far_c[b];
     const double2* xh = a.xhat + (int64_t)c * a.nl * p;
     const int rk = a.rank[b];
-    const double2* Zb = a.Z + a.zoff[b];
     __syncthreads();
+    const double2 *zD, *zL;
+    int zst;
+    ztile<FAC>(a.z, b, rk, a.nl, tb, tc0, ncp, lead, a.mask, zD, zL, zst);
     for (int i = tid; i < p; i += blockDim.x) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
     for (int k0c = 0; k0c < p; k0c += KC) {
       const int kw = min(KC, p - k0c);          // real nu in this chunk
@@ -748,19 +480,19 @@ __global__ void __launch_bounds__(NW * 32, 2) far8_kernel(Far8Args a) {
       }
       for (int l = 0; l < rk; ++l) {
         const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + l]];
-        const double2* Zl = Zb + (int64_t)l * a.nl;
-        double2 zt[MT];
-#pragma unroll
-        for (int i = 0; i < MT; ++i) {
-          const int tt = warp + NW * i;
-          const int t = tc0 + tt * 8 + g;
-          zt[i] = (tt < ntile && t < a.nl) ? Zl[t] : make_double2(0.0, 0.0);
-        }
         // S alternates between two buffers: one barrier per term, and warps may
         // run one term apart (regeneration overlaps other warps' DMMA work)
         double2* S = S0 + sbuf * 32 * SST;
         sbuf ^= 1;
-        if (l == 0) __syncthreads();  // xs / node coordinates staged
+        if (l == 0) __syncthreads();  // xs / node coordinates / Z tile staged
+        const double2* Zl = zD + (int64_t)l * zst;
+        double2 zt[MT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const int tt = warp + 8 * i;
+          const int t = tc0 + tt * 8 + g;
+          zt[i] = (tt < ntile && t < a.nl) ? Zl[t] : make_double2(0.0, 0.0);
+        }
         for (int e = tid; e < nrow * KC; e += blockDim.x) {
           const int i = e / KC, nu = e - i * KC;
           double2 v = make_double2(0.0, 0.0);
@@ -781,33 +513,22 @@ __global__ void __launch_bounds__(NW * 32, 2) far8_kernel(Far8Args a) {
           for (int j = 0; j < REM; ++j) rf[j] = S[(NJ * 8 + j) * SST + k0 + q];
 #pragma unroll
           for (int i = 0; i < MT; ++i) {
-            const int tt = warp + NW * i;
+            const int tt = warp + 8 * i;
             if (tt < ntile && ton[i]) {
               const double2 xv = xs[(k0 + q) * XTP + tb + tt * 8 + g];
               const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
               const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
               const double nai = -ai;
               // two passes: dependent DMMAs on one accumulator are 2*NJ instructions apart
-if constexpr (M3) {
-                const double as = ar + ai;
 #pragma unroll
-                for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+              for (int j = 0; j < NJ; ++j) {
+                dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+                dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
+              }
 #pragma unroll
-                for (int j = 0; j < NJ; ++j) dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].y);
-#pragma unroll
-                for (int j = 0; j < NJ; ++j)
-                  dmma(acc[i][j][M3 ? 2 : 0][0], acc[i][j][M3 ? 2 : 0][1], as, bf[j].x + bf[j].y);
-              } else {
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                  dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
-                  dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
-                }
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                  dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
-                  dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
-                }
+              for (int j = 0; j < NJ; ++j) {
+                dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
+                dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
               }
 #pragma unroll
               for (int j = 0; j < REM; ++j) {
@@ -829,9 +550,9 @@ if constexpr (M3) {
               sacc.y = fma(sv2.x, xv.y, sacc.y);
               sacc.y = fma(sv2.y, xv.x, sacc.y);
             }
-            const double2 z = Zl[tl];
-            lacc[tl].x = fma(z.x, sacc.x, fma(-z.y, sacc.y, lacc[tl].x));
-            lacc[tl].y = fma(z.x, sacc.y, fma(z.y, sacc.x, lacc[tl].y));
+            const double2 zz = zL[(int64_t)l * zst + tl];
+            lacc[tl].x = fma(zz.x, sacc.x, fma(-zz.y, sacc.y, lacc[tl].x));
+            lacc[tl].y = fma(zz.x, sacc.y, fma(zz.y, sacc.x, lacc[tl].y));
           }
         }
       }
@@ -840,7 +561,7 @@ if constexpr (M3) {
   double2* out = a.part + (int64_t)sg.w * a.nl * p;
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
-    const int tt = warp + NW * i;
+    const int tt = warp + 8 * i;
     if (tt >= ntile) continue;
     const int t = tc0 + tt * 8 + g;
     if (t >= a.nl) continue;
@@ -849,19 +570,13 @@ if constexpr (M3) {
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int row = j * 8 + 2 * q + v;
-        if (row < nrow) {
-          if constexpr (M3)
-            out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v] - acc[i][j][1][v],
-                                                           acc[i][j][M3 ? 2 : 0][v] - acc[i][j][0][v] - acc[i][j][1][v]);
-          else
-            out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
-        }
+        if (row < nrow) out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
       }
   }
   if (REM > 0) {
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
-      const int tt = warp + NW * i;
+      const int tt = warp + 8 * i;
       if (tt >= ntile) continue;
       const int t = tc0 + tt * 8 + g;
 #pragma unroll
@@ -897,9 +612,9 @@ struct Far8Cfg {
 
 // KC: nu chunk width (kc_req > 0 forces it; otherwise the whole p if a
 // 128-column frequency tile fits, else 32); TT up to 128 (MT <= 2).
-Far8Cfg choose8(int p, int nl, size_t cap, int kc_req, int ttmax_cap = 0, int nw = 8) {
+Far8Cfg choose8(int p, int nl, size_t cap, int kc_req) {
   int tb = nl % 8;
-  if (tb > 2 || tb == nl || nw != 8) tb = 0;
+  if (tb > 2 || tb == nl) tb = 0;
   const int nD = (nl - tb + 7) / 8 * 8;
   const int p4 = (p + 3) / 4 * 4;
   auto make = [&](int KC, int TTmax) {
@@ -914,42 +629,36 @@ Far8Cfg choose8(int p, int nl, size_t cap, int kc_req, int ttmax_cap = 0, int nw
         sizeof(double2) * (2 * 32 * (size_t)SST + (size_t)KC * XTP + 64) + sizeof(double) * (64 + 96 + 3 * p);
     if (smem > cap) return c;
     c.SST = SST; c.TT = TT; c.XTP = XTP; c.tb = tb; c.nd = nD; c.ntiles = ntiles;
-    c.nchunks = (p + 31) / 32; c.mt = (TT / 8 + nw - 1) / nw; c.smem = smem; c.KC = KC;
+    c.nchunks = (p + 31) / 32; c.mt = (TT / 8 + 7) / 8; c.smem = smem; c.KC = KC;
     return c;
   };
   std::vector<int> kcs;
   if (kc_req > 0) kcs = {std::min(p4, (kc_req + 3) / 4 * 4)};
   else kcs = {p4, std::min(p4, 32)};
-  for (int TTmax : {128, 96, 64, 48, 32, 16, 8})
+  for (int TTmax : {128, 64, 32, 16, 8})
     for (int KC : kcs) {
-      if (ttmax_cap > 0 && TTmax > ttmax_cap) continue;
-      if ((TTmax == 96 || TTmax == 48) != (nw == 6)) continue;  // 6-warp CTAs: 16 * MT tiles
       Far8Cfg c = make(KC, TTmax);
       if (c.mt > 0 && c.mt <= 2) return c;
     }
   return Far8Cfg{};
 }
 
-template <int MT, int NJ, int REM, bool M3 = false, int NW = 8>
+template <int MT, int NJ, int REM, bool FAC>
 cudaError_t launch8(const Far8Cfg& c, int nseg, const Far8Args& a, cudaStream_t st) {
-  auto k = far8_kernel<MT, NJ, REM, M3, NW>;
+  auto k = far8_kernel<MT, NJ, REM, FAC>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   if (e != cudaSuccess) return e;
   Far8Args a2 = a;
   a2.nch = c.nchunks;
-  k<<<dim3((unsigned)(nseg * c.nchunks), (unsigned)c.ntiles, 1u), NW * 32, c.smem, st>>>(a2);
+  k<<<dim3((unsigned)(nseg * c.nchunks), (unsigned)c.ntiles, 1u), 256, c.smem, st>>>(a2);
   return cudaGetLastError();
 }
 
-cudaError_t dispatch8(const Far8Cfg& c, int p, bool rem_dfma, int nseg, const Far8Args& a, cudaStream_t st,
-                      bool m3 = false, int nw = 8) {
-  if (nw == 6 && p > 8 && !(p == 27 && rem_dfma))
-    return c.mt == 1 ? (m3 ? launch8<1, 4, 0, true, 6>(c, nseg, a, st) : launch8<1, 4, 0, false, 6>(c, nseg, a, st))
-                     : (m3 ? launch8<2, 4, 0, true, 6>(c, nseg, a, st) : launch8<2, 4, 0, false, 6>(c, nseg, a, st));
-  if (m3 && c.mt == 1 && p > 8 && !(p == 27 && rem_dfma)) return launch8<1, 4, 0, true>(c, nseg, a, st);
-  if (p <= 8) return c.mt == 1 ? launch8<1, 1, 0>(c, nseg, a, st) : launch8<2, 1, 0>(c, nseg, a, st);
-  if (p == 27 && rem_dfma) return c.mt == 1 ? launch8<1, 3, 3>(c, nseg, a, st) : launch8<2, 3, 3>(c, nseg, a, st);
-  return c.mt == 1 ? launch8<1, 4, 0>(c, nseg, a, st) : launch8<2, 4, 0>(c, nseg, a, st);
+template <bool FAC>
+cudaError_t dispatch8(const Far8Cfg& c, int p, int nseg, const Far8Args& a, cudaStream_t st) {
+  if (p <= 8) return c.mt == 1 ? launch8<1, 1, 0, FAC>(c, nseg, a, st) : launch8<2, 1, 0, FAC>(c, nseg, a, st);
+  if (p == 27) return c.mt == 1 ? launch8<1, 3, 3, FAC>(c, nseg, a, st) : launch8<2, 3, 3, FAC>(c, nseg, a, st);
+  return c.mt == 1 ? launch8<1, 4, 0, FAC>(c, nseg, a, st) : launch8<2, 4, 0, FAC>(c, nseg, a, st);
 }
 
 // ------------------------------- h2o: plain-H^2 coupling evaluated on the fly
@@ -1227,10 +936,57 @@ __global__ void __launch_bounds__(256) far_generic_kernel(FarArgs a) {
 
 }  // namespace
 
+// K3 launch geometry of an ACA op: kernel (7/8), CTA grid and Z-tile row width.
+struct FarGeom {
+  int fk = 0;
+  Far7Cfg f7;
+  Far8Cfg f8;
+  int64_t ctas = 0;
+  int ZW = 0;
+};
+
+static FarGeom far_geom(const Op& op) {
+  const Tree& t = *op.tree;
+  const int p = t.p, nl = op.n_local;
+  FarGeom g;
+  g.fk = op.far_kernel != 0 ? op.far_kernel : (p > 32 ? 8 : 7);  // r01: far8 wins at p = 64, far7 at p = 27
+  if (op.force_generic || op.n_segs == 0) return g;
+  if (g.fk == 8) {
+    g.f8 = choose8(p, nl, op.far4_smem_cap, op.far8_kc);
+    if (g.f8.mt > 0) {
+      g.ctas = (int64_t)op.n_segs * g.f8.nchunks * g.f8.ntiles;
+      g.ZW = g.f8.tb + g.f8.TT;
+      return g;
+    }
+  } else if (g.fk == 7) {
+    g.f7 = choose7(p, nl, op.far4_smem_cap);
+    if (g.f7.mt > 0) {
+      g.ctas = (int64_t)op.n_segs * g.f7.nchunks * g.f7.ntiles;
+      g.ZW = g.f7.tb + g.f7.TT;
+      return g;
+    }
+  }
+  g.fk = 0;
+  return g;
+}
+
+// Factors-only skeleton: per-CTA Z-tile scratch of K3 (allocated at assembly so
+// that an apply never allocates, e.g. inside a CUDA-graph capture).
+bem_status far_prepare(Op& op) {
+  if (op.z_stored || op.ranks.empty()) return BEM_OK;
+  const FarGeom g = far_geom(op);
+  if (g.fk == 0) {
+    set_error("bem_assemble_h2_aca: factors-only skeleton needs the tiled coupling kernels (p <= 128)");
+    return BEM_EINVAL;
+  }
+  op.rmax = *std::max_element(op.ranks.begin(), op.ranks.end());
+  BEM_CK(op.d_zs.alloc((size_t)g.ctas * std::max(1, op.rmax) * g.ZW * 2));
+  return BEM_OK;
+}
+
 bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st) {
   Tree& t = *op.tree;
   const int nl = op.n_local, p = t.p;
-  const int fk = op.far_kernel != 0 ? op.far_kernel : (p > 32 ? 8 : 7);  // r01: far8 wins at p = 64, far7 at p = 27
   const bool aca = op.mode == BEM_MODE_H2ACA || op.mode == BEM_MODE_COMBINED;  // far blocks via the MACA skeleton
   if (op.mode == BEM_MODE_H2ONLY && !op.force_generic && op.n_segs > 0 && p <= 128) {
     BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
@@ -1258,61 +1014,53 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
     BEM_CK(cudaGetLastError());
     return BEM_OK;
   }
-  if (aca && fk == 8 && !op.force_generic && op.n_segs > 0) {
-    Far8Cfg f8 = choose8(p, nl, op.far4_smem_cap, op.far8_kc, op.far7_ttmax, op.far8_nw);
-    f8.smem = std::max(f8.smem, op.far_smem_min);  // residency experiment (env BEM_FAR_SMEM_MIN_KB)
-    if (f8.mt > 0) {
-      BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
-      Far8Args a;
-      a.nl = nl; a.m = t.m; a.p = p; a.rcap = op.rcap; a.SST = f8.SST; a.TT = f8.TT; a.XTP = f8.XTP;
-      a.tb = f8.tb; a.nd = f8.nd; a.KC = f8.KC;
-      a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
-      a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
-      a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
-      a.mask = op.d_mask;
-      BEM_CK(dispatch8(f8, p, op.far7_rem_dfma, op.n_segs, a, st, op.far7_m3, op.far8_nw));
-      seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
-                                                       yhat, (int64_t)nl * p);
-      BEM_CK(cudaGetLastError());
-      return BEM_OK;
+  const FarGeom g = aca ? far_geom(op) : FarGeom{};
+  const bool fac = aca && !op.z_stored;
+  ZSrc z{};
+  if (aca) {
+    z.zoff = op.d_zoff.p; z.Z = (const double2*)op.d_Z.p;
+    z.g.m = t.m; z.g.p = p; z.g.L = op.L; z.g.far_r = t.d_far_r.p; z.g.far_c = t.d_far_c.p; z.g.xi = t.d_xi.p;
+    z.g.s = (const double2*)op.d_s.p; z.g.pivk = op.d_pivk.p; z.g.pivq = op.d_pivq.p; z.g.foff = op.d_foff.p;
+    z.g.F = (const double2*)op.d_F.p; z.g.rcap = op.rcap;
+    z.local_l = op.d_local_l.p; z.scr = (double2*)op.d_zs.p; z.ZW = g.ZW; z.rmax = std::max(1, op.rmax);
+    if (fac && (g.fk == 0 || op.d_zs.p == nullptr)) {
+      set_error("launch_far: factors-only skeleton without the K3 scratch");
+      return BEM_ESTATE;
     }
   }
-  if (aca && fk == 7 && !op.force_generic && op.n_segs > 0) {
-    Far7Cfg f7 = choose7(p, nl, op.far7_nw == 16 ? 200 * 1024 : op.far4_smem_cap, op.far7_cluster && op.far7_nw != 16,
-                         op.far7_ttmax, op.far7_nw);
-    f7.smem = std::max(f7.smem, op.far_smem_min);  // residency experiment (env BEM_FAR_SMEM_MIN_KB)
-    if (f7.mt > 0) {
-      BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
-      Far7Args a;
-      a.nl = nl; a.m = t.m; a.p = p; a.p4 = f7.p4; a.rcap = op.rcap; a.SST = f7.SST; a.TT = f7.TT; a.XTP = f7.XTP;
-      a.nT = f7.nT; a.tb = f7.tb; a.nd = f7.nd; a.cs = f7.cs; a.own = f7.own;
-      a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
-      a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
-      a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
-      a.mask = op.d_mask;
-      BEM_CK(dispatch7(f7, p, op.far7_rem_dfma, op.n_segs, a, st, op.far7_nw, op.far7_m3, op.far7_split));
-      seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
-                                                       yhat, (int64_t)nl * p);
-      BEM_CK(cudaGetLastError());
-      return BEM_OK;
-    }
+  if (aca && g.fk == 8) {
+    const Far8Cfg& f8 = g.f8;
+    BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
+    Far8Args a;
+    a.nl = nl; a.m = t.m; a.p = p; a.rcap = op.rcap; a.SST = f8.SST; a.TT = f8.TT; a.XTP = f8.XTP;
+    a.tb = f8.tb; a.nd = f8.nd; a.KC = f8.KC;
+    a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
+    a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
+    a.z = z; a.xhat = xhat; a.part = (double2*)op.d_part.p; a.mask = op.d_mask;
+    BEM_CK(fac ? dispatch8<true>(f8, p, op.n_segs, a, st) : dispatch8<false>(f8, p, op.n_segs, a, st));
+    seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
+                                                     yhat, (int64_t)nl * p);
+    BEM_CK(cudaGetLastError());
+    return BEM_OK;
   }
-  if (aca && fk == 6 && !op.force_generic && op.n_segs > 0) {
-    const Far6Cfg f6 = choose6(p, nl, op.far4_smem_cap);
-    if (f6.mt > 0) {
-      BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
-      Far6Args a;
-      a.nl = nl; a.m = t.m; a.p = p; a.p4 = f6.p4; a.rcap = op.rcap; a.SST = f6.SST; a.TT = f6.TT; a.XTP = f6.XTP;
-      a.nT = f6.nT; a.tb = f6.tb;
-      a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
-      a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
-      a.zoff = op.d_zoff.p; a.Z = (const double2*)op.d_Z.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
-      BEM_CK(dispatch6(f6, op.n_segs, a, st));
-      seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
-                                                       yhat, (int64_t)nl * p);
-      BEM_CK(cudaGetLastError());
-      return BEM_OK;
-    }
+  if (aca && g.fk == 7) {
+    const Far7Cfg& f7 = g.f7;
+    BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
+    Far7Args a;
+    a.nl = nl; a.m = t.m; a.p = p; a.p4 = f7.p4; a.rcap = op.rcap; a.SST = f7.SST; a.TT = f7.TT; a.XTP = f7.XTP;
+    a.tb = f7.tb; a.nd = f7.nd;
+    a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
+    a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
+    a.z = z; a.xhat = xhat; a.part = (double2*)op.d_part.p; a.mask = op.d_mask;
+    BEM_CK(fac ? dispatch7<true>(f7, p, op.n_segs, a, st) : dispatch7<false>(f7, p, op.n_segs, a, st));
+    seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
+                                                     yhat, (int64_t)nl * p);
+    BEM_CK(cudaGetLastError());
+    return BEM_OK;
+  }
+  if (fac) {
+    set_error("launch_far: factors-only skeleton needs far7/far8");
+    return BEM_ESTATE;
   }
   FarArgs a;
   a.nl = nl; a.m = t.m; a.p = p; a.mode = aca ? BEM_MODE_H2ACA : op.mode; a.rcap = op.rcap;

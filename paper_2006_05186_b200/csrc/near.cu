@@ -74,17 +74,16 @@ __device__ __forceinline__ double2 self_node(const double* qn, const double* qw,
 
 // DL: double-layer kernel d/dn_y e^{-sr}/(4 pi r) (NEXT-1): per node the factor
 // (x - y).n_y / r^3 and (1 + s r) e^{-s r}; the self panel contributes 0.
-template <int F, int U, bool TAB, bool DL = false, bool XL = false>  // XL: load x after the node loop
+// x is loaded after the node loop (r01: 128 instead of 164 registers, 4 CTAs per SM).
+template <int F, bool DL = false>
 __device__ __forceinline__ void near_body(const NearArgs& a) {
   __shared__ double etab[64];
   __shared__ double2 sctab[64];
-  if (TAB) {
-    for (int i = threadIdx.x; i < 64; i += blockDim.x) {
-      etab[i] = fast::kExp2Tab[i];
-      sctab[i] = fast::kSinCosTab[i];
-    }
-    __syncthreads();
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+    etab[i] = fast::kExp2Tab[i];
+    sctab[i] = fast::kSinCosTab[i];
   }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t k = (int64_t)blockIdx.x * kNearWarps + (threadIdx.x >> 5);
   if (k >= a.M) return;
@@ -129,14 +128,7 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
       const int j = jn;  // index loaded one iteration ahead (one dependent global load fewer per source)
       if (jj + 32 < je) jn = a.near_j[jj + 32];
       if (j == k) continue;  // self panel below
-      double2 x1[F], x2[F];  // issued before the node loop: their latency hides behind it
-      if (!XL) {
-#pragma unroll
-        for (int f = 0; f < F; ++f) {
-          x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
-          x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
-        }
-      }
+      double2 x1[F], x2[F];
       double2 v[F];
 #pragma unroll
       for (int f = 0; f < F; ++f) v[f] = make_double2(0.0, 0.0);
@@ -144,7 +136,7 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
       const double* qw = a.qw + 7 * (int64_t)j;
       double nx = 0.0, ny = 0.0, nz = 0.0;
       if (DL) { nx = a.nrm[3 * (int64_t)j]; ny = a.nrm[3 * (int64_t)j + 1]; nz = a.nrm[3 * (int64_t)j + 2]; }
-#pragma unroll U
+#pragma unroll 7
       for (int q = 0; q < 7; ++q) {
         const double dx = cx - qn[3 * q], dy = cy - qn[3 * q + 1], dz = cz - qn[3 * q + 2];
         const double d2 = dx * dx + dy * dy + dz * dz;
@@ -153,10 +145,9 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
         const double w = DL ? qw[q] * ((dx * nx + dy * ny) + dz * nz) * (ir * ir * ir) : qw[q] * ir;
 #pragma unroll
         for (int f = 0; f < F; ++f) {
-          const double e = (TAB ? fast::exp_neg_tab(-sre[f] * r, etab) : fast::exp_neg(-sre[f] * r)) * w;
+          const double e = fast::exp_neg_tab(-sre[f] * r, etab) * w;
           double sn, cs;
-          if (TAB) fast::sincos_tab(sim[f] * r, sctab, &sn, &cs);
-          else fast::sincos_(sim[f] * r, &sn, &cs);
+          fast::sincos_tab(sim[f] * r, sctab, &sn, &cs);
           if (DL) {  // (1 + s r) e^{-s r}: (alpha + i beta)(cos - i sin) E
             const double ea = e * fma(sre[f], r, 1.0), eb = e * (sim[f] * r);
             v[f].x = fma(ea, cs, fma(eb, sn, v[f].x));
@@ -167,12 +158,10 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
           }
         }
       }
-      if (XL) {
 #pragma unroll
-        for (int f = 0; f < F; ++f) {
-          x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
-          x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
-        }
+      for (int f = 0; f < F; ++f) {
+        x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
+        x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int f = 0; f < F; ++f) {
@@ -218,19 +207,17 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
   }
 }
 
-template <int F, int U, bool TAB, bool XL = false>
+template <int F>
 __global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
-  near_body<F, U, TAB, false, XL>(a);
+  near_body<F, false>(a);
 }
 // double-layer near field (NEXT-1)
-template <int F, bool XL = false>
-__global__ void __launch_bounds__(kNearWarps * 32) near_kernel_dl(NearArgs a) {
-  near_body<F, 7, true, true, XL>(a);
-}
-template <int F, int U, bool TAB, bool XL = false>
+__global__ void __launch_bounds__(kNearWarps * 32) near_kernel_dl(NearArgs a) { near_body<4, true>(a); }
+
+template <int F>
 cudaError_t launch(const NearArgs& na, cudaStream_t st) {
   dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + F - 1) / F));
-  near_kernel<F, U, TAB, XL><<<g, kNearWarps * 32, 0, st>>>(na);
+  near_kernel<F><<<g, kNearWarps * 32, 0, st>>>(na);
   return cudaGetLastError();
 }
 
@@ -250,30 +237,17 @@ bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st, 
   na.class_t1 = op.d_class_t1.p; na.class_t2 = op.d_class_t2.p; na.mask = op.d_mask; na.xc = xc; na.yc = yc;
   // F = 4 classes per warp unless that pads the last class tile by more than 3 % and F = 5
   // pads less (config 2: 65 classes -> F = 5, 5.71 -> 5.64 ms; configs 3/4 keep F = 4)
-  int F = op.near_f;
-  if (F == 0) {
-    const int c = op.n_class;
-    const double w4 = double((c + 3) / 4 * 4 - c) / c, w5 = double((c + 4) / 5 * 5 - c) / c;
-    F = (w4 > 0.03 && w5 < w4) ? 5 : 4;
-  }
-  const int U = op.near_unroll;
-  const bool T = op.near_tab;
+  const int c = op.n_class;
+  const double w4 = double((c + 3) / 4 * 4 - c) / c, w5 = double((c + 4) / 5 * 5 - c) / c;
+  const int F = (w4 > 0.03 && w5 < w4) ? 5 : 4;
   cudaError_t e;
   if (dl) {
     dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + 3) / 4));
-    if (op.near_xlate) near_kernel_dl<4, true><<<g, kNearWarps * 32, 0, st>>>(na);
-    else near_kernel_dl<4><<<g, kNearWarps * 32, 0, st>>>(na);
+    near_kernel_dl<<<g, kNearWarps * 32, 0, st>>>(na);
     e = cudaGetLastError();
-  } else if (F == 3) e = T ? (U == 7 ? (op.near_xlate ? launch<3, 7, true, true>(na, st) : launch<3, 7, true>(na, st))
-                              : launch<3, 1, true>(na, st))
-                    : (U == 7 ? launch<3, 7, false>(na, st) : launch<3, 1, false>(na, st));
-  else if (F == 4) e = T ? (U == 7 ? (op.near_xlate ? launch<4, 7, true, true>(na, st) : launch<4, 7, true>(na, st))
-                             : (op.near_xlate ? launch<4, 1, true, true>(na, st) : launch<4, 1, true>(na, st)))
-                         : launch<4, 1, false>(na, st);
-  else if (F == 5 && T) e = op.near_xlate ? (U == 7 ? launch<5, 7, true, true>(na, st) : launch<5, 1, true, true>(na, st))
-                                          : launch<5, 7, true>(na, st);
-  else e = T ? (U == 7 ? launch<2, 7, true>(na, st) : launch<2, 1, true>(na, st))
-             : (U == 7 ? launch<2, 7, false>(na, st) : launch<2, 1, false>(na, st));
+  } else {
+    e = F == 5 ? launch<5>(na, st) : launch<4>(na, st);
+  }
   BEM_CK(e);
   return BEM_OK;
 }

@@ -16,6 +16,7 @@ StepGraph::~StepGraph() {
   if (own) cudaStreamDestroy(own);
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
+  if (e2) cudaEventDestroy(e2);
 }
 
 }  // namespace bem
@@ -42,7 +43,11 @@ extern "C" bem_status bem_time_step(bem_op oh, const bem_c128* x_time, bem_c128*
     BEM_CK(cudaStreamCreateWithFlags(&g.own, cudaStreamNonBlocking));
     BEM_CK(cudaEventCreateWithFlags(&g.e0, cudaEventDisableTiming));
     BEM_CK(cudaEventCreateWithFlags(&g.e1, cudaEventDisableTiming));
+    BEM_CK(cudaEventCreateWithFlags(&g.e2, cudaEventDisableTiming));
   }
+  // the op's time buffers are shared by every call: this call's H2D into g.tx must not
+  // overtake the previous call's graph (or its D2H from g.ty), whatever stream it was on
+  if (g.used) BEM_CK(cudaStreamWaitEvent(st, g.e2, 0));
   BEM_CK(cudaMemcpyAsync(g.tx.p, x_time, bytes, cudaMemcpyDefault, st));
   BEM_CK(cudaEventRecord(g.e0, st));
   BEM_CK(cudaStreamWaitEvent(g.own, g.e0, 0));
@@ -83,5 +88,7 @@ extern "C" bem_status bem_time_step(bem_op oh, const bem_c128* x_time, bem_c128*
   BEM_CK(cudaEventRecord(g.e1, g.own));
   BEM_CK(cudaStreamWaitEvent(st, g.e1, 0));
   BEM_CK(cudaMemcpyAsync(y_time, g.ty.p, bytes, cudaMemcpyDefault, st));
+  BEM_CK(cudaEventRecord(g.e2, st));
+  g.used = true;
   return BEM_OK;
 }

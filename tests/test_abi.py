@@ -84,6 +84,19 @@ def test_tree_partition_bit_identical_to_oracle(case):
     assert lt.stats["nnz_near"] == oh.nnz_near and lt.stats["depth"] == oh.depth
 
 
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_tree_partition_full_size_bit_identical(cfg):
+    """Configs 4 and 5 at full size (81,920 / 327,680 panels): the library's tree and
+    partition (host build, the same code the device build runs) bit-equal to the oracle's."""
+    c = synth.CONFIGS[cfg]
+    V, T = synth.config_mesh(cfg)
+    lt = pb.Tree(V, T, c["leaf"], c["eta"], c["m"], device=-1)
+    oh = O.H2(V, T, c["leaf"], c["eta"], c["m"])
+    a, b = lt.export(), oh.export()
+    for k in ("perm", "clusters", "boxes", "near", "far"):
+        assert np.array_equal(a[k].view(np.uint8), b[k].view(np.uint8)), k
+
+
 def test_tree_cfg4_stats_match_probe():
     """SURVEY §8.0 row 4 (independent probe): 3,591 clusters, 1,796 leaves,
     63,554 near and 98,386 far blocks."""
@@ -102,4 +115,5 @@ def test_null_handles_rejected_without_gpu():
     assert lib.bem_conv_time(None, None, None, 0, None) == -1
     assert lib.cqm_mot_solve(None, None, None, 1e-8, 10, 10, None, None) == -1
     assert lib.bem_time_step(None, None, None, 0.5, None) == -1
+    assert lib.bem_op_get_info(None, None) == -1
     assert b"NULL" in lib.bem_last_error()

@@ -1,0 +1,229 @@
+"""Full-size parity at the BASELINE configs, in the bench's launch configuration
+(one operator holding all L frequencies on one device, the default skeleton).
+
+SURVEY C13 / north_star tolerances:
+  * trees, admissibility lists, ACA ranks and pivots: bit-exact;
+  * apply vs the identical-compression oracle: global relative l2 <= 1e-10 over
+    the compared frequencies, each frequency <= 1e-8 (reported);
+  * apply vs the dense oracle: <= 10 max(eps_ACA, e_H2), e_H2 = ||Y_H2ONLY -
+    Y_DENSE|| / ||Y_DENSE|| measured by the oracle on the same input (AM20);
+  * solve: residual re-evaluated by the oracle <= 1.5e-8 (tol 1e-8 plus the
+    re-evaluation slack), solution vs the oracle's GMRES <= 1e-6 (kappa * tol).
+Config 3 (20,480 panels, L = 257) and config 2 run the oracle live; config 4
+(81,920 panels, L = 513) compares against tests/golden/c4_oracle.npz, written
+by tools/make_golden.py from the oracle alone (its ACA of 98,386 blocks takes
+minutes); config 5 (327,680 panels, L = 1025) checks the tree / partition bit
+for bit and the ACA pivots of 48 sampled far blocks against the live oracle.
+Compared frequencies: l in {0, 1, L/2, L-1} (the real frequency, the least
+damped complex one, the most damped one and a mirrored one)."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as _t
+    assert _t.cuda.is_available()
+    return _t
+
+
+@pytest.fixture(scope="module")
+def pb():
+    import paper_2006_05186_b200 as _pb
+    _pb.lib()
+    return _pb
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def _sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def _lsel(L):
+    return np.array([0, 1, L // 2, L - 1], dtype=np.int32)
+
+
+def _check_apply(y, yo, lsel):
+    assert _rel(y[lsel], yo) <= 1e-10
+    for i in range(len(lsel)):
+        assert _rel(y[lsel[i]], yo[i]) <= 1e-8, lsel[i]
+
+
+@pytest.fixture(scope="module")
+def cfg3(pb):
+    """Config 3 oracle: tree, full ACA (all 35,934 far blocks; Z kept for lsel)."""
+    c = synth.CONFIGS[3]
+    V, T = synth.config_mesh(3)
+    N = c["N"]
+    M, L = len(T), N + 1
+    s = O.frequencies(N, c["T"])
+    lsel = _lsel(L)
+    oh = O.H2(V, T, c["leaf"], c["eta"], c["m"])
+    oa = oh.aca(s, c["eps"], keep=lsel)
+    return dict(c=c, V=V, T=T, N=N, M=M, L=L, s=s, lsel=lsel, oh=oh, oa=oa)
+
+
+def test_config3_full_size_vs_oracle(pb, torch, cfg3):
+    """Config 3 at full size: tree and ACA (all blocks) bit-exact, apply of all 257
+    frequencies vs the identical oracle on lsel; factors-only skeleton bitwise equal."""
+    d = cfg3
+    c, M, L, s, lsel, oh, oa = d["c"], d["M"], d["L"], d["s"], d["lsel"], d["oh"], d["oa"]
+    assert np.array_equal(pb.cqm_frequencies(d["N"], c["T"]).view(np.float64), s.view(np.float64))
+    tree = pb.Tree(d["V"], d["T"], c["leaf"], c["eta"], c["m"])
+    a, b = tree.export(), oh.export()
+    for k in ("perm", "clusters", "boxes", "near", "far"):
+        assert np.array_equal(a[k], b[k]), k
+    op = pb.Operator(tree, s, c["eps"])
+    ga = op.aca_export()
+    assert np.array_equal(ga["ranks"], oa["ranks"])
+    assert np.array_equal(ga["pivots"], oa["pivots"])
+    x = synth.random_density(3, L, M)
+    xg = torch.from_numpy(x).cuda()
+    y = op.apply(xg).cpu().numpy()
+    yo = oh.apply(O.MODE_H2ACA, s, x[lsel], lsel)
+    _check_apply(y, yo, lsel)
+    opf = pb.Operator(tree, s, c["eps"], mode=pb.BEM_MODE_H2ACA | pb.BEM_SKEL_FACTORS)
+    assert np.array_equal(opf.apply(xg).cpu().numpy(), y)
+
+
+def test_config3_vs_dense(pb, torch, cfg3):
+    """Config 3: GPU H2ACA apply vs the DENSE oracle (every entry by the collocation
+    rule C3) on 4 frequencies, within 10 max(eps, e_H2)."""
+    d = cfg3
+    c, M, L, s, lsel, oh = d["c"], d["M"], d["L"], d["s"], d["lsel"], d["oh"]
+    tree = pb.Tree(d["V"], d["T"], c["leaf"], c["eta"], c["m"])
+    op = pb.Operator(tree, s, c["eps"], local_l=lsel)
+    x = synth.random_density(3, len(lsel), M, stream=7)
+    y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    yd = oh.apply(O.MODE_DENSE, s, x, lsel)
+    yh = oh.apply(O.MODE_H2ONLY, s, x, lsel)
+    eh2 = _rel(yh, yd)
+    err = _rel(y, yd)
+    print(f"config 3: e_H2 = {eh2:.3e}, GPU vs dense = {err:.3e}")
+    assert err <= 10 * max(c["eps"], eh2)
+
+
+def test_config3_solve(pb, torch, cfg3):
+    """BASELINE config 3 solve: batched GMRES(50) to 1e-8 on all 257 frequencies of
+    the pulse data; the oracle re-evaluates the residual on 4 frequencies with its
+    own H2ACA apply and solves them with its own GMRES."""
+    d = cfg3
+    c, N, M, L, s, lsel, oh = d["c"], d["N"], d["M"], d["L"], d["s"], d["lsel"], d["oh"]
+    R = 10.0 ** (-5.0 / N)
+    tree = pb.Tree(d["V"], d["T"], c["leaf"], c["eta"], c["m"])
+    op = pb.Operator(tree, s, c["eps"])
+    g = synth.pulse(d["V"], d["T"], N, c["T"])
+    gf = O.forward(g.astype(np.complex128), N, R)
+    phi, st = pb.solve_multifreq(op, torch.from_numpy(gf).cuda(), tol=1e-8, restart=50)
+    print(f"config 3 solve: {st}")
+    assert st["n_unconverged"] == 0 and st["resid_max"] <= 1e-8
+    phi = phi.cpu().numpy()
+    res = oh.apply(O.MODE_H2ACA, s, phi[lsel], lsel) - gf[lsel]
+    rel = np.linalg.norm(res, axis=1) / np.linalg.norm(gf[lsel], axis=1)
+    assert np.max(rel) <= 1.5e-8, rel
+    xo, it, rr = oh.gmres(O.MODE_H2ACA, s, gf[lsel], lsel, tol=1e-8, restart=50)
+    assert np.all(rr <= 1e-8)
+    for i in range(len(lsel)):
+        assert _rel(phi[lsel[i]], xo[i]) <= 1e-6, (lsel[i], _rel(phi[lsel[i]], xo[i]))
+    # the time-domain solve through the C-ABI on the same op
+    phit, st2 = pb.cqm_solve(op, torch.from_numpy(g).cuda(), R, tol=1e-8, restart=50)
+    assert st2["n_unconverged"] == 0
+
+
+def test_config2_vs_dense(pb, torch):
+    """Config 2 (5,120 panels, L = 129): GPU apply vs the DENSE oracle on 4
+    frequencies within 10 max(eps, e_H2)."""
+    c = synth.CONFIGS[2]
+    V, T = synth.config_mesh(2)
+    N = c["N"]
+    M, L = len(T), N + 1
+    s = pb.cqm_frequencies(N, c["T"])
+    lsel = _lsel(L)
+    op = pb.Operator(pb.Tree(V, T, c["leaf"], c["eta"], c["m"]), s, c["eps"])
+    x = synth.random_density(2, L, M)
+    y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    oh = O.H2(V, T, c["leaf"], c["eta"], c["m"])
+    yd = oh.apply(O.MODE_DENSE, s, x[lsel], lsel)
+    yh = oh.apply(O.MODE_H2ONLY, s, x[lsel], lsel)
+    eh2 = _rel(yh, yd)
+    print(f"config 2: e_H2 = {eh2:.3e}, GPU vs dense = {_rel(y[lsel], yd):.3e}")
+    assert _rel(y[lsel], yd) <= 10 * max(c["eps"], eh2)
+
+
+def test_config4_full_size_vs_golden(pb, torch):
+    """Config 4 at full size (the bench's N = 1 workload): tree, every ACA rank and
+    the SHA-256 of the full pivot list equal to the oracle's (tests/golden/c4_oracle.npz,
+    tools/make_golden.py); apply of all 513 frequencies vs the oracle's H2ACA apply on
+    lsel; the factors-only skeleton bitwise equal to the stored Z."""
+    gold = np.load(os.path.join(GOLDEN, "c4_oracle.npz"))
+    c = synth.CONFIGS[4]
+    V, T = synth.config_mesh(4)
+    N = c["N"]
+    M, L = len(T), N + 1
+    lsel = gold["lsel"]
+    assert np.array_equal(lsel, _lsel(L))
+    s = pb.cqm_frequencies(N, c["T"])
+    tree = pb.Tree(V, T, c["leaf"], c["eta"], c["m"])
+    ex = tree.export()
+    assert _sha(ex["perm"], ex["clusters"], ex["boxes"], ex["near"], ex["far"]) == str(gold["tree_sha256"])
+    op = pb.Operator(tree, s, c["eps"])
+    ga = op.aca_export()
+    assert np.array_equal(ga["ranks"], gold["ranks"].astype(np.int32))
+    assert _sha(ga["pivots"].astype("<i4")) == str(gold["pivots_sha256"])
+    x = synth.random_density(4, L, M)
+    xg = torch.from_numpy(x).cuda()
+    del x
+    yg = op.apply(xg)
+    y = yg.cpu().numpy()
+    _check_apply(y, gold["y"], lsel)
+    skel = op.skeleton()
+    op.close()
+    opf = pb.Operator(tree, s, c["eps"], mode=pb.BEM_MODE_H2ACA | pb.BEM_SKEL_FACTORS)
+    assert torch.equal(opf.apply(xg), yg), f"factors-only vs {skel}"
+
+
+def test_config5_tree_and_sampled_pivots(pb, torch):
+    """Config 5 (two spheres, 327,680 panels, L = 1025, p = 125, eps = 1e-8): the
+    device-built tree and partition bit-equal to the oracle's; ranks and pivots of
+    48 sampled far blocks bit-identical; stored Z and factors-only skeleton give
+    bitwise equal applies on a frequency shard."""
+    c = synth.CONFIGS[5]
+    V, T = synth.config_mesh(5)
+    N = c["N"]
+    M, L = len(T), N + 1
+    s = pb.cqm_frequencies(N, c["T"])
+    tree = pb.Tree(V, T, c["leaf"], c["eta"], c["m"])
+    oh = O.H2(V, T, c["leaf"], c["eta"], c["m"])
+    a, b = tree.export(), oh.export()
+    for k in ("perm", "clusters", "boxes", "near", "far"):
+        assert np.array_equal(a[k], b[k]), k
+    local = np.array([0, 1, 2, 511, 512, 513, 514, 1022, 1023, 1024], dtype=np.int32)
+    op = pb.Operator(tree, s, c["eps"], mode=pb.BEM_MODE_H2ACA | pb.BEM_SKEL_Z, local_l=local)
+    ga = op.aca_export()
+    rng = np.random.default_rng(5)
+    blocks = np.sort(rng.choice(len(ga["ranks"]), 48, replace=False)).astype(np.int32)
+    oa = oh.aca(s, c["eps"], blocks=blocks, keep=[0])
+    assert np.array_equal(ga["ranks"][blocks], oa["ranks"])
+    off = np.concatenate([[0], np.cumsum(ga["ranks"])])
+    gp = np.concatenate([ga["pivots"][off[bk]:off[bk + 1]] for bk in blocks])
+    assert np.array_equal(gp, oa["pivots"])
+    x = torch.from_numpy(synth.random_density(5, len(local), M)).cuda()
+    y = op.apply(x)
+    op.close()
+    opf = pb.Operator(tree, s, c["eps"], mode=pb.BEM_MODE_H2ACA | pb.BEM_SKEL_FACTORS, local_l=local)
+    assert torch.equal(opf.apply(x), y)

@@ -159,9 +159,10 @@ def test_local_frequency_subset(pb, torch):
     assert _rel(y, yo) <= 1e-10
 
 
-@pytest.mark.parametrize("N", [1, 32, 128, 256])
+@pytest.mark.parametrize("N", [1, 32, 128, 256, 512, 1024])
 def test_transforms_vs_oracle(pb, torch, N):
-    """K4 vs the oracle's naive DFTs; round trip on R^n-scaled sequences."""
+    """K4 vs the oracle's naive DFTs; round trip on R^n-scaled sequences.  N = 512 and
+    1024 are configs 4 and 5 (L = 513, 1025)."""
     L, M = N + 1, 37
     R = 10.0 ** (-5.0 / N) if N > 1 else 0.3
     rng = np.random.default_rng(N)
@@ -261,55 +262,26 @@ def test_edge_cases(pb, torch):
     assert _rel(_apply(pb, torch, op, x), oh.apply(O.MODE_H2ACA, s, x)) <= 1e-10
 
 
-@pytest.mark.parametrize("N,kernel,cluster", [(256, "7", "0"), (260, "7", "0"), (256, "7", "1"), (260, "7", "1"),
-                                               (256, "6", "0"), (256, "8", "0"), (260, "8", "0")])
-def test_h2aca_p64_multi_tile(pb, torch, N, kernel, cluster, monkeypatch):
+@pytest.mark.parametrize("N,kernel", [(256, "7"), (260, "7"), (256, "8"), (260, "8")])
+def test_h2aca_p64_multi_tile(pb, torch, N, kernel, monkeypatch):
     """p = 64 (m = 4) with L > 128: K3 runs several frequency tiles per
-    (segment, mu chunk); far7 with BEM_FAR7_CLUSTER=1 shares the regenerated
-    pivot slices across the tiles' thread-block cluster through distributed
-    shared memory.  N = 260
-    (L mod 8 = 5) exercises the zero-padded DMMA columns, N = 256 the
-    distributed leftover column.  Oracle on a frequency sample."""
+    (segment, mu chunk).  N = 260 (L mod 8 = 5) exercises the zero-padded DMMA
+    columns, N = 256 the distributed leftover column.  Oracle on a frequency sample."""
     monkeypatch.setenv("BEM_FAR_KERNEL", kernel)
-    monkeypatch.setenv("BEM_FAR7_CLUSTER", cluster)
     V, T = synth.icosphere(3)
     M, L, eps = len(T), N + 1, 1e-6
     s = pb.cqm_frequencies(N, 2.0)
     x = synth.random_density(3, L, M)
+    lsel = np.unique(np.r_[0, 1, 2, 7, 8, 63, 64, 65, 127, 128, 129, L // 2, L - 3, L - 2, L - 1])
     oh = O.H2(V, T, 48, 1.0, 4)
-    oh.aca(s, eps)
+    oh.aca(s, eps, keep=lsel)
     tree = pb.Tree(V, T, 48, 1.0, 4)
     op = pb.Operator(tree, s, eps, mode=pb.BEM_MODE_H2ACA)
     y = _apply(pb, torch, op, x)
-    lsel = np.unique(np.r_[0, 1, 2, 7, 8, 63, 64, 65, 127, 128, 129, L // 2, L - 3, L - 2, L - 1])
     yo = oh.apply(O.MODE_H2ACA, s, x[lsel], lsel)
     assert _rel(y[lsel], yo) <= 1e-10
     for i in range(len(lsel)):
         assert _rel(y[lsel[i]], yo[i]) <= 1e-8, lsel[i]
-
-
-@pytest.mark.parametrize("m,leaf,N,env", [
-    (3, 32, 128, {"BEM_FAR7_NW": "16"}), (3, 32, 128, {"BEM_FAR7_NW": "16", "BEM_FAR7_M3": "1"}),
-    (3, 32, 128, {"BEM_FAR7_M3": "1", "BEM_FAR7_TTMAX": "64"}), (3, 32, 128, {"BEM_FAR7_SPLIT": "1"}),
-    (4, 48, 256, {"BEM_FAR8_NW": "6"}), (4, 48, 256, {"BEM_FAR8_NW": "6", "BEM_FAR7_M3": "1"}),
-    (4, 48, 256, {"BEM_FAR7_M3": "1", "BEM_FAR7_TTMAX": "64"})])
-def test_k3_variants(pb, torch, m, leaf, N, env, monkeypatch):
-    """The measured K3 alternatives (profiles/r01_sweeps.md; off by default):
-    16-warp far7 CTAs, 6-warp far8 CTAs, 3M complex products (three real DMMA
-    products per complex one).  Oracle on a frequency sample."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    V, T = synth.icosphere(3)
-    M, L, eps = len(T), N + 1, 1e-6
-    s = pb.cqm_frequencies(N, 2.0)
-    x = synth.random_density(3, L, M)
-    oh = O.H2(V, T, leaf, 1.0, m)
-    oh.aca(s, eps)
-    op = pb.Operator(pb.Tree(V, T, leaf, 1.0, m), s, eps, mode=pb.BEM_MODE_H2ACA)
-    y = _apply(pb, torch, op, x)
-    lsel = np.unique(np.r_[0, 1, 7, 8, 63, 64, 127, 128, L // 2, L - 2, L - 1])
-    yo = oh.apply(O.MODE_H2ACA, s, x[lsel], lsel)
-    assert _rel(y[lsel], yo) <= 1e-10
 
 
 @pytest.mark.parametrize("nloc", [10, 19])

@@ -51,9 +51,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA-graph replay")
-    ap.add_argument("--transpose", default="peer", choices=["peer", "a2a"],
-                    help="N > 1: peer = transforms fused with the transpose over CUDA-IPC peer memory "
-                         "(cqm_forward_rows / cqm_inverse_rows); a2a = torch.distributed all_to_all_single")
+    ap.add_argument("--transpose", default="nccl", choices=["nccl", "peer", "a2a"],
+                    help="N > 1: nccl = the library's bem_time_step_sharded (K4 fused with the packing, NCCL "
+                         "grouped send/recv all-to-all inside libbem); peer = transforms fused with the transpose over "
+                         "CUDA-IPC peer memory (cqm_forward_rows / cqm_inverse_rows); a2a = torch all_to_all_single")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: host-staged all-to-all (testing the multi-rank flow on one GPU only)")
     ap.add_argument("--shard-of", type=int, default=0,
@@ -61,6 +62,8 @@ def parse():
                          "classes of a G-GPU run (what one rank of `--gpus G` computes, without the all-to-alls)")
     ap.add_argument("--shard-rank", type=int, default=0)
     ap.add_argument("--quiet", action="store_true")
+    ap.add_argument("--ranks-dry-run", action="store_true",
+                    help="print each rank's (RANK, WORLD_SIZE) and exit (checks the --gpus N launch without a GPU)")
     return ap.parse_args()
 
 
@@ -235,8 +238,30 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def spawn_ranks(args):
+    """--gpus N > 1 launched as a plain process: re-exec under torch.distributed.run (one rank
+    per GPU, rendezvous on 127.0.0.1), the way the driver launches it."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"bench.py: spawning {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    world_env = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world_env is None:
+        spawn_ranks(args)
+    if world_env is not None and int(world_env) != args.gpus and args.dist_backend == "nccl":
+        raise SystemExit(f"bench.py: WORLD_SIZE={world_env} but --gpus {args.gpus}: launch one rank per GPU")
+    if args.ranks_dry_run:
+        print(json.dumps({"rank": int(os.environ.get("RANK", "0")), "world": int(world_env or 1)}), flush=True)
+        return
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -294,7 +319,15 @@ def main():
     opfn = op.apply if args.operator == "V" else (lambda z: op.apply_dl(z))
     transpose = None
     lib_step = False
-    if world > 1:
+    if world > 1 and args.transpose == "nccl" and args.operator == "V" and args.dist_backend == "nccl":
+        from paper_2006_05186_b200 import bem as B
+        comm = B.Comm(rank, world, local_rank)
+        transpose = ("libbem bem_time_step_sharded: K4 fused with the all-to-all packing, NCCL grouped send/recv "
+                     "all-to-all inside the library, 2-D copies for the strided side")
+
+        def step(z):
+            return B.time_step_sharded(op, z, R, comm)
+    elif world > 1:
         top = None
         if args.transpose == "peer" and args.operator == "V":
             try:
@@ -420,8 +453,9 @@ def main():
     kt = {k: v / args.steps for k, v in acc.items()}
     launches = op.launch_count() + 2
     if aca_far:
-        rk = op.aca_export()["ranks"]
-        flops_far = 8.0 * float(rk.sum()) * stats["p"] ** 2 * nl
+        # 8 flops per complex MAC of a pivot slice; 4 for the real slice S_b(s_0) (complex x real)
+        kpiv = op.aca_export()["pivots"][:, 0]
+        flops_far = float(np.where(np.imag(s[kpiv]) == 0.0, 4.0, 8.0).sum()) * stats["p"] ** 2 * nl
     else:  # plain H^2: one kernel evaluation per (block entry, frequency class) + the complex MACs
         flops_far = 75.0 * stats["far_blocks"] * stats["p"] ** 2 * n_class + 8.0 * stats["far_blocks"] * stats["p"] ** 2 * nl
     evals_near = 7.0 * stats["nnz_near"] * n_class

@@ -42,7 +42,7 @@ enum {
   BEM_EINVAL = -1,  /* invalid argument (ranges listed per call) */
   BEM_ENOMEM = -2,  /* device or host allocation failed */
   BEM_ECUDA = -3,   /* CUDA runtime error (launch or asynchronous fault) */
-  BEM_ENCCL = -4,   /* reserved: collectives are issued by the caller */
+  BEM_ENCCL = -4,   /* NCCL missing or failed (sharded multi-GPU calls) */
   BEM_ENOCONV = -5, /* cqm_solve: some frequency hit max_iter (outputs written) */
   BEM_ESTATE = -6   /* handle misuse (wrong device, tree destroyed before its ops) */
 };
@@ -65,6 +65,7 @@ enum { BEM_SKEL_Z = 0x100, BEM_SKEL_FACTORS = 0x200 };
 typedef struct { double re, im; } bem_c128;
 typedef struct bem_tree_s* bem_tree; /* panels, cluster tree, P+/P-, U, W, E, boxes; one device */
 typedef struct bem_op_s* bem_op;     /* tree ref + s_l + ACA skeletons for a local frequency set */
+typedef struct bem_comm_s* bem_comm; /* NCCL communicator of a frequency-sharded multi-GPU run */
 
 typedef struct {
   int64_t M, clusters, leaves, near_blocks, far_blocks, nnz_near;
@@ -217,13 +218,41 @@ bem_status cqm_inverse(const bem_c128* y_freq, bem_c128* y_time, int64_t M_loc, 
  *   GMRES(restart) from 0, classical Gram-Schmidt with one
  *   re-orthogonalisation, stop at ||g^_l - V phi^_l|| <= tol ||g^_l||;
  *   phi = Re inverse(phi^).
- * g_time, phi_time: device [N+1][M] real.  The op must hold all L = N+1
- * frequencies (single device; nccl_comm must be NULL in this version: the
- * multi-GPU transpose is issued by the caller).
+ * nccl_comm = NULL: one device; g_time, phi_time device [N+1][M] real, M_loc = M,
+ *   the op holds all L = N+1 frequencies in order.
+ * nccl_comm = a bem_comm of G ranks (bem_comm_init; the handle type is bem_comm):
+ *   rank g passes its DOF shard, g_time / phi_time device [N+1][M_loc] with
+ *   M_loc = the size of [M g/G, M (g+1)/G), and its op holds exactly rank g's
+ *   frequency shard (bem_shard_frequencies; EINVAL otherwise).  The two
+ *   time<->frequency transposes are NCCL all-to-alls inside the call (SURVEY
+ *   §8(e)); stats are reduced over the ranks (max / sum).  Collective: every rank
+ *   of the communicator must call it.
  * stats (host, may be NULL).  Synchronous.  Returns BEM_ENOCONV if some
- * frequency reached max_iter (phi_time is still written). */
+ * frequency reached max_iter (phi_time is still written), BEM_ENCCL on NCCL errors. */
 bem_status cqm_solve(bem_op op, const double* g_time, double* phi_time, int64_t M_loc, double R, double tol,
                      int32_t restart, int32_t max_iter, void* nccl_comm, void* cuda_stream, bem_solve_stats* stats);
+
+/* ---- multi-GPU frequency sharding over NCCL (Remark P:1607-1614) ----
+ * Rank g of G owns the DOFs [M g/G, M (g+1)/G) of time-domain data and the frequency
+ * classes {0}, {j, L-j} of bem_shard_frequencies (balanced contiguous class ranges,
+ * conjugate pairs kept together).  NCCL is loaded at run time (libnccl.so.2).
+ *   bem_comm_unique_id: 128-byte ncclUniqueId, created on one rank and broadcast by
+ *     the caller (e.g. torch.distributed); ENCCL when NCCL cannot be loaded.
+ *   bem_comm_init: collective over the nranks processes (ncclCommInitRank); device =
+ *     this rank's CUDA ordinal (the ops used with it must live there).
+ *   bem_shard_frequencies: host only; owner[l] = rank holding frequency l, slot[l] =
+ *     its row in that rank's local list (the op's local_l, in that order).
+ *   bem_time_step_sharded: the bench's time-domain step on G ranks, collective:
+ *     x_loc [L][M_loc] (this rank's DOF columns, complex, device) -> forward K4 fused
+ *     with the packing of the all-to-all -> NCCL all-to-all -> apply of this rank's
+ *     frequencies -> all-to-all -> inverse K4 fused with the unpacking -> y_loc
+ *     [L][M_loc].  Asynchronous on cuda_stream (NCCL calls enqueue on it). */
+bem_status bem_comm_unique_id(void* id_out);
+bem_status bem_comm_init(const void* id, int32_t nranks, int32_t rank, int32_t device, bem_comm* out);
+bem_status bem_comm_destroy(bem_comm comm); /* NULL-safe */
+bem_status bem_shard_frequencies(int32_t L, int32_t G, int32_t* owner, int32_t* slot);
+bem_status bem_time_step_sharded(bem_op op, const bem_c128* x_loc, bem_c128* y_loc, int64_t M_loc, double R,
+                                 bem_comm comm, void* cuda_stream);
 
 /* Transforms fused with the multi-GPU time<->frequency transpose (SURVEY
  * §8(e)).  The same R-scaled transforms as cqm_forward / cqm_inverse, but
@@ -275,6 +304,12 @@ bem_status bem_debug_pinned(const double* x, int64_t n, double* exp_out, double*
  * check of the fast math against libm (tests).  variant: 64 or 256 (table size). */
 bem_status bem_debug_fastmath(const double* x, int64_t n, double* exp_out, double* sin_out, double* cos_out,
                               int32_t device, int32_t variant);
+/* MACA (the assembly's kernel and pinned arithmetic) of the listed far blocks only, no
+ * skeleton kept: ranks host [nblk], pivots host [sum ranks][2] (NULL: ranks only; size it
+ * with min(L, p^2) per block), *total_rank.  Sampled bit-exactness checks at sizes whose
+ * full assembly takes minutes. */
+bem_status bem_debug_aca_blocks(bem_tree t, const bem_c128* s, int32_t L, double aca_eps, const int32_t* blocks,
+                                int32_t nblk, int32_t* ranks, int32_t* pivots, int64_t* total_rank);
 /* FP64 DFMA throughput microbenchmark: returns achieved FLOP/s. */
 bem_status bem_debug_fp64_peak(int32_t device, void* cuda_stream, double* flops_per_s);
 /* mode 0: DFMA loop, 1: FP64 tensor-core mma.sync m8n8k4 loop, 2: both in one CTA. */

@@ -48,7 +48,8 @@ EXPORTS = [
     "cqm_forward", "cqm_inverse", "cqm_forward_rows", "cqm_inverse_rows", "bem_ipc_get_handle",
     "bem_ipc_open_handle", "bem_ipc_close", "bem_device_alloc", "bem_device_free", "cqm_solve", "bem_solve_multifreq", "bem_debug_pinned", "bem_debug_fastmath", "bem_debug_fp64_peak",
     "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count", "bem_debug_fp64_peak_ex",
-    "bem_op_get_info",
+    "bem_op_get_info", "bem_comm_unique_id", "bem_comm_init", "bem_comm_destroy", "bem_shard_frequencies",
+    "bem_time_step_sharded", "bem_debug_aca_blocks",
 ]
 
 
@@ -97,6 +98,12 @@ def lib():
         "bem_op_launch_count": [vp, vp],
         "bem_debug_fp64_peak_ex": [i32, vp, i32, vp],
         "bem_op_get_info": [vp, vp],
+        "bem_comm_unique_id": [vp],
+        "bem_comm_init": [vp, i32, i32, i32, vp],
+        "bem_comm_destroy": [vp],
+        "bem_shard_frequencies": [i32, i32, vp, vp],
+        "bem_time_step_sharded": [vp, vp, vp, i64, d, vp, vp],
+        "bem_debug_aca_blocks": [vp, vp, i32, d, vp, i32, vp, vp, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -384,15 +391,74 @@ def device_free(ptr: int):
     _check(lib().bem_device_free(C.c_void_p(ptr)))
 
 
+def shard_frequencies(L: int, G: int):
+    """The library's frequency shard of every rank (bem_shard_frequencies): local lists
+    (the op's local_l of each rank, in order)."""
+    owner = np.empty(L, dtype=np.int32)
+    slot = np.empty(L, dtype=np.int32)
+    _check(lib().bem_shard_frequencies(int(L), int(G), _p(owner), _p(slot)))
+    out = [np.empty(int((owner == g).sum()), dtype=np.int32) for g in range(G)]
+    for l in range(L):
+        out[owner[l]][slot[l]] = l
+    return out
+
+
+def dof_range(M: int, G: int, g: int):
+    return M * g // G, M * (g + 1) // G
+
+
+class Comm:
+    """NCCL communicator of a frequency-sharded run (bem_comm_init), one per rank.
+    The 128-byte unique id is created on rank 0 and broadcast over `group`
+    (torch.distributed): plumbing only, the collectives run inside libbem."""
+
+    def __init__(self, rank: int, world: int, device: int, group=None):
+        import torch.distributed as dist
+        uid = C.create_string_buffer(128)
+        if rank == 0:
+            _check(lib().bem_comm_unique_id(uid))
+        obj = [uid.raw if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        h = C.c_void_p()
+        _check(lib().bem_comm_init(C.c_char_p(obj[0]), int(world), int(rank), int(device), C.byref(h)))
+        self.h, self.rank, self.world, self.device = h, rank, world, device
+
+    def close(self):
+        if getattr(self, "h", None):
+            _check(lib().bem_comm_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def time_step_sharded(op: Operator, x_loc, R: float, comm: Comm, y=None, stream=None):
+    """The time-domain step on G ranks (bem_time_step_sharded): x_loc [L][M_g] complex, this
+    rank's DOF columns, on the op's device; NCCL all-to-alls inside the library."""
+    import torch
+    assert x_loc.dtype == torch.complex128 and x_loc.is_cuda and x_loc.is_contiguous() and x_loc.shape[0] == op.L
+    y = torch.empty_like(x_loc) if y is None else y
+    assert y.shape == x_loc.shape and y.dtype == x_loc.dtype and y.is_contiguous()
+    _check(lib().bem_time_step_sharded(op.h, _p(x_loc), _p(y), int(x_loc.shape[1]), float(R), comm.h,
+                                       _stream(stream)))
+    return y
+
+
 def cqm_solve(op: Operator, g_time, R: float, tol: float = 1e-8, restart: int = 50, max_iter: int = 2000,
-              stream=None, raise_on_noconv: bool = True):
-    """phi = Re inverse(V(s_l)^{-1} forward(g)) (frequency-decoupled GMRES)."""
+              stream=None, raise_on_noconv: bool = True, comm: Comm | None = None):
+    """phi = Re inverse(V(s_l)^{-1} forward(g)) (frequency-decoupled GMRES).  With comm
+    (G ranks): g_time is this rank's DOF shard [N+1][M_g] and op holds this rank's
+    frequency shard; the transposes are NCCL all-to-alls inside the library."""
     import torch
     assert g_time.dtype == torch.float64 and g_time.is_cuda and g_time.is_contiguous()
     phi = torch.empty_like(g_time)
     st = SolveStats()
     code = lib().cqm_solve(op.h, _p(g_time), _p(phi), g_time.shape[1], float(R), float(tol), int(restart),
-                           int(max_iter), None, _stream(stream), C.byref(st))
+                           int(max_iter), comm.h if comm is not None else None, _stream(stream), C.byref(st))
     if code != 0 and not (code == BEM_ENOCONV and not raise_on_noconv):
         _check(code)
     return phi, {k: getattr(st, k) for k, _ in SolveStats._fields_ if k != "pad_"}
@@ -424,6 +490,18 @@ def solve_multifreq(op: Operator, g_freq, tol: float = 1e-8, restart: int = 50, 
     if code != 0 and not (code == BEM_ENOCONV and not raise_on_noconv):
         _check(code)
     return phi, {k: getattr(st, k) for k, _ in SolveStats._fields_ if k != "pad_"}
+
+
+def debug_aca_blocks(tree: Tree, s, eps: float, blocks):
+    """The assembly's MACA on the listed far blocks only: ranks and pivots (k_l, q_l)."""
+    s = np.ascontiguousarray(s, dtype=np.complex128)
+    blocks = np.ascontiguousarray(blocks, dtype=np.int32)
+    ranks = np.empty(len(blocks), dtype=np.int32)
+    piv = np.empty((len(blocks) * min(len(s), tree.p * tree.p), 2), dtype=np.int32)
+    tot = C.c_int64()
+    _check(lib().bem_debug_aca_blocks(tree.h, _p(s), len(s), float(eps), _p(blocks), len(blocks), _p(ranks),
+                                      _p(piv), C.byref(tot)))
+    return dict(ranks=ranks, pivots=piv[:tot.value])
 
 
 def debug_pinned(x, device: int = 0):

@@ -418,9 +418,16 @@ using namespace bem;
 namespace {
 // near = false: far blocks (P+, coupling tensors); near = true: near blocks (P-,
 // combined mode), whose pivot slices are stored as well.
-bem_status run_aca(Op& op, cudaStream_t st, bool near, bool store_z) {
+bem_status run_aca(Op& op, cudaStream_t st, bool near, bool store_z, const std::vector<int32_t>* subset = nullptr) {
   Tree& t = *op.tree;
-  const int nblk = near ? (int)t.near_r.size() : (int)t.far_r.size();
+  const int nblk = subset ? (int)subset->size() : near ? (int)t.near_r.size() : (int)t.far_r.size();
+  DBuf<int32_t> sub_r, sub_c;  // far blocks of `subset` only (diagnostic: bem_debug_aca_blocks)
+  if (subset) {
+    std::vector<int32_t> hr, hc;
+    for (int b : *subset) { hr.push_back(t.far_r[b]); hc.push_back(t.far_c[b]); }
+    BEM_CK(sub_r.upload(hr));
+    BEM_CK(sub_c.upload(hc));
+  }
   std::vector<int32_t>& ranks_out = near ? op.nranks : op.ranks;
   ranks_out.assign(nblk, 0);
   if (nblk == 0) return BEM_OK;
@@ -433,7 +440,7 @@ bem_status run_aca(Op& op, cudaStream_t st, bool near, bool store_z) {
   // whole ACA: config 5 hit both the old 96 rank cap and the 40-per-block pool
   // estimate), the pool is shrunk to its exact size afterwards
   int rcap = std::min(std::min(L, ppmax), 128);
-  const bool store_f = !near;  // factors-only skeleton of the far blocks (always kept: small)
+  const bool store_f = !near && !subset;  // factors-only skeleton of the far blocks (always kept: small)
   unsigned long long cap = store_z ? (unsigned long long)nblk * 64ull * (unsigned long long)op.n_local : 0ull;
   unsigned long long fcap = store_f ? (unsigned long long)nblk * 48ull * 48ull : 0ull;
   unsigned long long scap = 0;
@@ -495,7 +502,9 @@ bem_status run_aca(Op& op, cudaStream_t st, bool near, bool store_z) {
     AcaArgs a{};
     a.nfar = nblk; a.m = t.m; a.p = p; a.L = L; a.rcap = rcap; a.n_local = op.n_local;
     a.ppmax = ppmax; a.geo = geo;
-    a.far_r = near ? t.d_near_r.p : t.d_far_r.p; a.far_c = near ? t.d_near_c.p : t.d_far_c.p; a.xi = t.d_xi.p;
+    a.far_r = subset ? sub_r.p : near ? t.d_near_r.p : t.d_far_r.p;
+    a.far_c = subset ? sub_c.p : near ? t.d_near_c.p : t.d_far_c.p;
+    a.xi = t.d_xi.p;
     a.cbegin = t.d_begin.p; a.cend = t.d_end.p; a.cen = t.d_cen.p; a.qn = t.d_qn.p; a.area = t.d_area.p;
     a.J = t.d_J.p;
     for (int q = 0; q < 7; ++q) a.w[q] = wq[q];
@@ -573,7 +582,7 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
           "bem_assemble_h2_aca: BEM_MODE_COMBINED keeps the stored Z (the MoT weights read it)");
   // the operator evaluates l > L/2 as the conjugate of L - l (ACA mirroring, conjugate
   // frequency classes of K1 / K3'): s must be exactly conjugation-symmetric
-  for (int l = 1; l < L; ++l)
+  for (int l = 1; 2 * l < L; ++l)
     BEM_REQ(s[L - l].re == s[l].re && s[L - l].im == -s[l].im,
             "bem_assemble_h2_aca: s[%d] != conj(s[%d]) (s must satisfy s_{L-l} = conj(s_l), as cqm_frequencies gives)",
             L - l, l);
@@ -800,6 +809,44 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   return BEM_OK;
 }
 
+// MACA of a subset of the far blocks only (the assembly's kernel and arithmetic, no
+// skeleton kept): ranks and pivots of every listed block, for sampled bit-exactness
+// checks at sizes whose full assembly takes minutes (config 5).
+extern "C" bem_status bem_debug_aca_blocks(bem_tree th, const bem_c128* s, int32_t L, double aca_eps,
+                                           const int32_t* blocks, int32_t nblk, int32_t* ranks, int32_t* pivots,
+                                           int64_t* total_rank) {
+  BEM_REQ(th && s && blocks && ranks && L >= 1 && nblk >= 1 && aca_eps > 0.0, "bem_debug_aca_blocks: bad arguments");
+  Tree& t = th->t;
+  BEM_REQ(t.device >= 0, "bem_debug_aca_blocks: host-only tree");
+  std::vector<int32_t> sub(blocks, blocks + nblk);
+  for (int b : sub) BEM_REQ(b >= 0 && b < (int)t.far_r.size(), "bem_debug_aca_blocks: block %d out of range", b);
+  DeviceGuard dg(t.device);
+  Op op;
+  op.tree = &t; op.L = L; op.n_local = 1; op.mode = BEM_MODE_H2ACA; op.eps = aca_eps; op.local_l = {0};
+  std::vector<double> sh(2 * (size_t)L);
+  for (int l = 0; l < L; ++l) { sh[2 * l] = s[l].re; sh[2 * l + 1] = s[l].im; }
+  BEM_CK(op.d_s.upload(sh));
+  BEM_CK(op.d_local_l.upload(op.local_l));
+  bem_status rs = run_aca(op, nullptr, false, false, &sub);
+  if (rs != BEM_OK) return rs;
+  std::vector<int32_t> pk((size_t)nblk * op.rcap), pq((size_t)nblk * op.rcap);
+  BEM_CK(cudaMemcpy(pk.data(), op.d_pivk.p, sizeof(int32_t) * pk.size(), cudaMemcpyDeviceToHost));
+  BEM_CK(cudaMemcpy(pq.data(), op.d_pivq.p, sizeof(int32_t) * pq.size(), cudaMemcpyDeviceToHost));
+  int64_t tot = 0;
+  for (int i = 0; i < nblk; ++i) {
+    ranks[i] = op.ranks[i];
+    for (int j = 0; j < op.ranks[i]; ++j) {
+      if (pivots) {
+        pivots[2 * tot] = pk[(size_t)i * op.rcap + j];
+        pivots[2 * tot + 1] = pq[(size_t)i * op.rcap + j];
+      }
+      ++tot;
+    }
+  }
+  if (total_rank) *total_rank = tot;
+  return BEM_OK;
+}
+
 extern "C" bem_status bem_op_get_info(bem_op oh, bem_op_info* out) {
   BEM_REQ(oh && out, "bem_op_get_info: NULL argument");
   const Op& op = oh->o;
@@ -884,6 +931,7 @@ extern "C" bem_status bem_aca_export_near(bem_op oh, int32_t* ranks, int32_t* pi
 extern "C" bem_status bem_op_destroy(bem_op oh) {
   if (!oh) return BEM_OK;
   DeviceGuard dg(oh->o.tree->device);
+  shard_ws_release(&oh->o);
   oh->o.tree->refcount--;
   for (auto& e : oh->o.ev)
     if (e) cudaEventDestroy(e);

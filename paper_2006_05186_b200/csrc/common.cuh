@@ -227,7 +227,19 @@ bem_status gmres_fn(int64_t M, int nl, const std::function<bem_status(const doub
                     std::vector<int>& hit, std::vector<double>& hrel, GmresWs& ws);
 bem_status solve_stats(const std::vector<int>& hit, const std::vector<double>& hrel, double tol, int max_iter,
                        double imag_rel, bem_solve_stats* stats);
-// fft.cu
+// fft.cu; tab (mode 1: input rows, 2: output rows) = host row-pointer table, copied into the launch
+bem_status fft_transform_rows(const double* in, double* out, int64_t M, int N, double R, bool inverse,
+                              cudaStream_t st, const double2* const* tab, int mode);
+// comm.cu: NCCL frequency sharding
+bool shard_frequencies(int L, int G, std::vector<int>& owner, std::vector<int>& slot,
+                       std::vector<std::vector<int>>* lists);
+bem_status shard_forward(Op& op, bem_comm c, const double* x_time, double R, double2** xf, cudaStream_t st);
+bem_status shard_inverse(Op& op, bem_comm c, const double2* yf, double R, double* y_time, cudaStream_t st);
+bem_status shard_yf(Op& op, bem_comm c, double2** yf);
+bem_status comm_allreduce(bem_comm c, double* dev, int nmax, int nsum, cudaStream_t st);
+bem_status comm_check(bem_comm c, const Op& op, int64_t M_loc);
+double* comm_scratch(bem_comm c);
+void shard_ws_release(const Op* op);
 bem_status fft_transform(const double* in, double* out, int64_t M, int N, double R, bool inverse,
                          cudaStream_t st);
 

@@ -86,21 +86,34 @@ struct ZSrc {
 // Coefficient rows of block b for this CTA's columns.  Returns zD, zL and the row
 // stride such that Z_b[j, t] = zD[j * stride + t] for the tile's DMMA columns t and
 // zL[j * stride + t] for the leftover columns t < tb.  FAC: the tile is regenerated here
-// (columns [0, tb) leftover -- lead CTA only -- then [tc0, tc0 + ncol)); the caller
-// synchronises the CTA before the first read.
+// (columns [0, tb) leftover -- lead CTA only -- then [tc0, tc0 + ncol)): one thread per
+// column runs the two substitutions on a [r][nb] batch in shared memory (work: the CTA's
+// slice / x^ buffers, free before the block's staging; nb columns per batch), and the
+// batch is copied to the CTA's scratch, which the term loop reads.  Ends with a barrier.
 template <bool FAC>
 __device__ __forceinline__ void ztile(const ZSrc& z, int b, int rk, int nl, int tb, int tc0, int ncp, bool lead,
-                                      const int32_t* mask, const double2*& zD, const double2*& zL, int& stride) {
+                                      const int32_t* mask, double2* work, int work_cap, const double2*& zD,
+                                      const double2*& zL, int& stride) {
   if constexpr (!FAC) {
     zD = zL = z.Z + z.zoff[b];
     stride = nl;
   } else {
     double2* scr = z.scr + (int64_t)(blockIdx.x + gridDim.x * blockIdx.y) * z.rmax * z.ZW;
-    for (int c = threadIdx.x; c < ncp; c += blockDim.x) {
-      if (c < tb && !lead) continue;
-      const int t = c < tb ? c : tc0 + (c - tb);
-      const int l = (t < nl && (mask == nullptr || mask[t])) ? z.local_l[t] : -1;
-      zgen::column(z.g, b, rk, l, scr + c, z.ZW);
+    const int nb = max(1, min(ncp, work_cap / max(rk, 1)));
+    for (int c0 = lead ? 0 : tb; c0 < ncp; c0 += nb) {
+      const int nc = min(nb, ncp - c0);
+      if ((int)threadIdx.x < nc) {
+        const int c = c0 + threadIdx.x;
+        const int t = c < tb ? c : tc0 + (c - tb);
+        const int l = (t < nl && (mask == nullptr || mask[t])) ? z.local_l[t] : -1;
+        zgen::column(z.g, b, rk, l, work + threadIdx.x, nb);
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < rk * nc; e += blockDim.x) {
+        const int j = e / nc, cc = e - j * nc;
+        scr[(int64_t)j * z.ZW + c0 + cc] = work[j * nb + cc];
+      }
+      __syncthreads();
     }
     zL = scr;
     zD = scr + (tb - tc0);
@@ -201,7 +214,7 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
     __syncthreads();
     const double2 *zD, *zL;
     int zst;
-    ztile<FAC>(a.z, b, rk, a.nl, tb, tc0, ncp, lead, a.mask, zD, zL, zst);
+    ztile<FAC>(a.z, b, rk, a.nl, tb, tc0, ncp, lead, a.mask, S0, 2 * 32 * SST + p4 * XTP, zD, zL, zst);
     for (int i = tid; i < p; i += blockDim.x) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
     const double2* xh = a.xhat + (int64_t)c * a.nl * p;
     for (int idx = tid; idx < ncp * p; idx += blockDim.x) {
@@ -213,6 +226,7 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
     for (int l = 0; l < rk; ++l) {
       double2* S = S0 + (l & 1) * 32 * SST;
       const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + l]];
+      const bool real_slice = sv.y == 0.0;
       const double2* Zl = zD + (int64_t)l * zst;
       double2 zt[MT];
 #pragma unroll
@@ -242,16 +256,24 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
             const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
             const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
             const double nai = -ai;
-            // two passes: dependent DMMAs on one accumulator are 2*NJ instructions apart
+            if (real_slice) {  // pivot frequency s_0 is real: Im S = 0, two DMMAs per complex MAC
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) {
-              dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
-              dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
-            }
+              for (int j = 0; j < NJ; ++j) {
+                dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+                dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
+              }
+            } else {
+              // two passes: dependent DMMAs on one accumulator are 2*NJ instructions apart
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) {
-              dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
-              dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
+              for (int j = 0; j < NJ; ++j) {
+                dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+                dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
+              }
+#pragma unroll
+              for (int j = 0; j < NJ; ++j) {
+                dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
+                dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
+              }
             }
 #pragma unroll
             for (int j = 0; j < REM; ++j) {  // partial over this lane's k = k0 + q; reduced over q at the end
@@ -466,7 +488,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
     __syncthreads();
     const double2 *zD, *zL;
     int zst;
-    ztile<FAC>(a.z, b, rk, a.nl, tb, tc0, ncp, lead, a.mask, zD, zL, zst);
+    ztile<FAC>(a.z, b, rk, a.nl, tb, tc0, ncp, lead, a.mask, S0, 2 * 32 * SST + KC * XTP, zD, zL, zst);
     for (int i = tid; i < p; i += blockDim.x) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
     for (int k0c = 0; k0c < p; k0c += KC) {
       const int kw = min(KC, p - k0c);          // real nu in this chunk
@@ -480,6 +502,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
       }
       for (int l = 0; l < rk; ++l) {
         const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + l]];
+        const bool real_slice = sv.y == 0.0;
         // S alternates between two buffers: one barrier per term, and warps may
         // run one term apart (regeneration overlaps other warps' DMMA work)
         double2* S = S0 + sbuf * 32 * SST;
@@ -519,16 +542,24 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
               const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
               const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
               const double nai = -ai;
-              // two passes: dependent DMMAs on one accumulator are 2*NJ instructions apart
+              if (real_slice) {  // pivot frequency s_0 is real: Im S = 0, two DMMAs per complex MAC
 #pragma unroll
-              for (int j = 0; j < NJ; ++j) {
-                dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
-                dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
-              }
+                for (int j = 0; j < NJ; ++j) {
+                  dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+                  dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
+                }
+              } else {
+                // two passes: dependent DMMAs on one accumulator are 2*NJ instructions apart
 #pragma unroll
-              for (int j = 0; j < NJ; ++j) {
-                dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
-                dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
+                for (int j = 0; j < NJ; ++j) {
+                  dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+                  dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
+                }
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                  dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
+                  dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
+                }
               }
 #pragma unroll
               for (int j = 0; j < REM; ++j) {

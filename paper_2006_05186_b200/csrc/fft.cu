@@ -2,14 +2,22 @@
 // (eq:omega_n P:436-441, eq:slphelm P:529-540; reading D2):
 //   forward  X_l = sum_n R^n x_n w^{nl},             w = e^{-2 pi i/L}
 //   inverse  y_n = R^{-n}/L sum_l Y_l w^{-nl}
-// L = N+1 has large prime factors (33, 129, 257, 513, 1025), so each column
-// is transformed by Bluestein's chirp-z identity nl = (n^2 + l^2 - (l-n)^2)/2:
-//   out_j = post_j sum_i (in_i pre_i) h_{j-i}
-// with chirp c_k = e^{-pi i (k^2 mod 2L)/L} (index reduced in integers), and
-//   forward: pre_i = R^i c_i,   h_k = conj(c_k), post_j = c_j
-//   inverse: pre_i = conj(c_i), h_k = c_k,       post_j = R^{-j} conj(c_j)/L.
-// The length-L linear convolution runs as a power-of-two P >= 2L-1 radix-2
-// FFT in shared memory, one CTA per group of DOF columns (coalesced row loads).
+// One CTA transforms a group of NC DOF columns entirely in shared memory: the
+// [L][NC] tile is loaded with coalesced row segments (R^n folded into the load),
+// transformed, and stored (R^{-n}/L folded into the store).
+//  * L whose prime factors are all <= 64 (33 = 3*11, 129 = 3*43, 513 = 3^3*19,
+//    1025 = 5^2*41): a self-sorting mixed-radix Stockham FFT -- radix-2/3/4/5/7
+//    butterflies in registers, larger prime factors as a direct DFT whose
+//    outputs are spread over threads (every input read is a shared-memory
+//    broadcast); twiddles and roots from one table of the L-th roots of unity.
+//  * otherwise (257 is prime): Bluestein's chirp-z identity
+//    nl = (n^2 + l^2 - (l-n)^2)/2 with a power-of-two P >= 2L-1 FFT:
+//      out_j = post_j sum_i (in_i pre_i) h_{j-i},  c_k = e^{-pi i (k^2 mod 2L)/L},
+//      forward: pre_i = R^i c_i, h_k = conj(c_k), post_j = c_j;
+//      inverse: pre_i = conj(c_i), h_k = c_k, post_j = R^{-j} conj(c_j)/L.
+// Rows may be addressed through a table of row pointers passed BY VALUE in the
+// kernel parameters (16 KB, graph-capturable, no staging): the transforms fused
+// with the multi-GPU time<->frequency transpose (cqm_*_rows, bem_comm.cu).
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -25,8 +33,25 @@ namespace {
 
 struct Plan {
   int L = 0, P = 0, logP = 0;
-  DBuf<double> pre, post, hhat, tw;  // complex arrays (interleaved)
+  DBuf<double> pre, post, hhat, tw;  // Bluestein: complex arrays (interleaved)
+  bool stock = false;                // mixed-radix Stockham (every prime factor <= kMaxRadix)
+  int nst = 0, rad[24] = {};
+  DBuf<double> roots, scale;         // Stockham: e^{sign 2 pi i k/L} (k < L); R^n or R^{-n}/L
 };
+
+constexpr int kMaxRadix = 64;
+
+// radices of L: 4s, 2s, 3s, 5s, 7s, then the remaining primes; empty if a prime > kMaxRadix
+std::vector<int> factor_radices(int L) {
+  std::vector<int> f;
+  int n = L;
+  for (int q : {4, 2, 3, 5, 7})
+    while (n % q == 0) { f.push_back(q); n /= q; }
+  for (int q = 11; n > 1 && q <= kMaxRadix; q += 2)
+    while (n % q == 0) { f.push_back(q); n /= q; }
+  if (n > 1) f.clear();
+  return f;
+}
 
 std::mutex g_plan_mu;
 std::map<std::tuple<int, int, uint64_t, int>, std::unique_ptr<Plan>> g_plans;
@@ -65,6 +90,26 @@ bem_status get_plan(int N, double R, bool inverse, Plan** out) {
   if (it != g_plans.end()) { *out = it->second.get(); return BEM_OK; }
   auto pl = std::make_unique<Plan>();
   const int L = N + 1;
+  const std::vector<int> rad = factor_radices(L);
+  if (!rad.empty() && (int)rad.size() <= 24) {
+    pl->L = L;
+    pl->stock = true;
+    pl->nst = (int)rad.size();
+    for (int i = 0; i < pl->nst; ++i) pl->rad[i] = rad[i];
+    const double sg = inverse ? 1.0 : -1.0;
+    std::vector<double> ro(2 * L), sc(L);
+    for (int k = 0; k < L; ++k) {
+      const double ang = 2.0 * M_PI * (double)k / (double)L;
+      ro[2 * k] = std::cos(ang);
+      ro[2 * k + 1] = sg * std::sin(ang);
+      sc[k] = inverse ? std::pow(R, -(double)k) / (double)L : std::pow(R, (double)k);
+    }
+    BEM_CK(pl->roots.upload(ro));
+    BEM_CK(pl->scale.upload(sc));
+    *out = pl.get();
+    g_plans[key] = std::move(pl);
+    return BEM_OK;
+  }
   int P = 1, logP = 0;
   while (P < 2 * L - 1) { P <<= 1; ++logP; }
   pl->L = L; pl->P = P; pl->logP = logP;
@@ -226,87 +271,249 @@ __device__ void smem_fft_dif(double2* buf, int P, int logP, int NC, const double
   }
 }
 
-// Row addressing of the transform's input and output: row r of the input is
-// in_rows.p[r] (or in + r*M when in_rows == nullptr), likewise for the output.
-// With row pointers into OTHER ranks' buffers (CUDA IPC / NVLink peer memory)
-// the kernel performs the time<->frequency transform and the all-to-all
-// transpose in one pass: the forward transform stores frequency row l of this
-// rank's DOF columns straight into the owner of l (cqm_forward_rows), the
-// inverse reads them back from the owners (cqm_inverse_rows).
-constexpr int kMaxRows = 2048;
-struct RowPtrs {
-  double2* p[kMaxRows];
+// Row addressing: mode 0 = row r at in/out + r*M; mode 1 = input row r at tab.p[r];
+// mode 2 = output row r at tab.p[r].  With row pointers into OTHER ranks' buffers
+// (CUDA IPC peer memory) or into the packed send / receive buffers of an NCCL
+// all-to-all (bem_comm.cu), the kernel performs the transform and the
+// time<->frequency transpose's (un)packing in one pass.
+struct K4Args {
+  const double2* in;
+  double2* out;
+  int64_t M;
+  int L, NC, mode, inverse;
+  // Stockham
+  int nst;
+  int rad[24];
+  const double2* roots;
+  const double* scale;
+  // Bluestein
+  int P, logP;
+  const double2 *pre, *post, *hhat, *tw;
 };
 
-__global__ void __launch_bounds__(kFftThreads) bluestein_kernel(const double2* __restrict__ in, double2* __restrict__ out,
-                                                               int64_t M, int L, int P, int logP, int NC,
-                                                               const double2* __restrict__ pre,
-                                                               const double2* __restrict__ post,
-                                                               const double2* __restrict__ hhat,
-                                                               const double2* __restrict__ tw,
-                                                               const RowPtrs* __restrict__ in_rows,
-                                                               const RowPtrs* __restrict__ out_rows) {
-  extern __shared__ double2 buf[];
+__device__ __forceinline__ double2 cfma(double2 acc, double2 a, double2 b) {  // acc + a b
+  acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+  return acc;
+}
+
+// radix-R Stockham stage (R <= 8, butterflies in registers), A -> B:
+//   j < T = L/R, jm = j mod Ns:  v_r = A[j + r T] w^{jm r L/(Ns R)},
+//   B[(j - jm) R + jm + k Ns] = sum_r v_r w^{(r k mod R) L/R}
+template <int R>
+__device__ __forceinline__ void stage_small(const double2* __restrict__ A, double2* __restrict__ B, int L, int Ns,
+                                            int NC, const double2* __restrict__ W) {
+  const int T = L / R, tstep = L / (Ns * R), rstep = L / R;
+  for (int it = threadIdx.x; it < T * NC; it += blockDim.x) {
+    const int j = it / NC, c = it - j * NC;
+    const int jm = j % Ns;
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = A[(j + r * T) * NC + c];
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cm(v[r], W[jm * r * tstep]);
+    const int base = (j - jm) * R + jm;
+    if constexpr (R == 2) {
+      B[base * NC + c] = make_double2(v[0].x + v[1].x, v[0].y + v[1].y);
+      B[(base + Ns) * NC + c] = make_double2(v[0].x - v[1].x, v[0].y - v[1].y);
+    } else {
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        double2 acc = v[0];
+#pragma unroll
+        for (int r = 1; r < R; ++r) acc = cfma(acc, v[r], W[((r * k) % R) * rstep]);
+        B[(base + k * Ns) * NC + c] = acc;
+      }
+    }
+  }
+}
+
+// prime radix R > 8: twiddle pass A -> B, then a direct R-point DFT with one thread per
+// output k (the inputs are shared-memory broadcasts), B -> A.  The result stays in A.
+__device__ __forceinline__ void stage_large(double2* __restrict__ A, double2* __restrict__ B, int L, int R, int Ns,
+                                            int NC, const double2* __restrict__ W) {
+  const int T = L / R, tstep = L / (Ns * R), rstep = L / R;
+  for (int e = threadIdx.x; e < L * NC; e += blockDim.x) {
+    const int row = e / NC;
+    const int r = row / T, j = row - r * T;
+    B[e] = cm(A[e], W[(j % Ns) * r * tstep]);
+  }
+  __syncthreads();
+  for (int it = threadIdx.x; it < L * NC; it += blockDim.x) {
+    const int c = it % NC, q = it / NC;
+    const int j = q / R, k = q - j * R;
+    const int jm = j % Ns;
+    double2 acc = B[j * NC + c];
+    int idx = k;
+    for (int r = 1; r < R; ++r) {
+      acc = cfma(acc, B[(j + r * T) * NC + c], W[idx * rstep]);
+      idx += k;
+      if (idx >= R) idx -= R;
+    }
+    A[((j - jm) * R + jm + k * Ns) * NC + c] = acc;
+  }
+}
+
+__device__ __forceinline__ void stockham_body(const K4Args& a, const double2* const* tab) {
+  extern __shared__ double2 sm2[];
+  const int L = a.L, NC = a.NC;
+  double2* A = sm2;
+  double2* B = A + (size_t)L * NC;
+  double2* W = B + (size_t)L * NC;
   const int64_t c0 = (int64_t)blockIdx.x * NC;
-  const int nc = (int)min((int64_t)NC, M - c0);
+  const int nc = (int)min((int64_t)NC, a.M - c0);
+  for (int i = threadIdx.x; i < L; i += blockDim.x) W[i] = a.roots[i];
+  for (int idx = threadIdx.x; idx < L * NC; idx += blockDim.x) {
+    const int n = idx / NC, c = idx - n * NC;
+    double2 v = make_double2(0.0, 0.0);
+    if (c < nc) {
+      const double2* row = a.mode == 1 ? tab[n] : a.in + (int64_t)n * a.M;
+      v = row[c0 + c];
+      if (!a.inverse) { const double sc = a.scale[n]; v.x *= sc; v.y *= sc; }
+    }
+    A[idx] = v;
+  }
+  __syncthreads();
+  int Ns = 1;
+  for (int st = 0; st < a.nst; ++st) {
+    const int R = a.rad[st];
+    switch (R) {
+      case 2: stage_small<2>(A, B, L, Ns, NC, W); break;
+      case 3: stage_small<3>(A, B, L, Ns, NC, W); break;
+      case 4: stage_small<4>(A, B, L, Ns, NC, W); break;
+      case 5: stage_small<5>(A, B, L, Ns, NC, W); break;
+      case 7: stage_small<7>(A, B, L, Ns, NC, W); break;
+      default: stage_large(A, B, L, R, Ns, NC, W); break;
+    }
+    if (R <= 8) { double2* t = A; A = B; B = t; }
+    __syncthreads();
+    Ns *= R;
+  }
+  for (int idx = threadIdx.x; idx < L * NC; idx += blockDim.x) {
+    const int n = idx / NC, c = idx - n * NC;
+    if (c < nc) {
+      double2 v = A[idx];
+      if (a.inverse) { const double sc = a.scale[n]; v.x *= sc; v.y *= sc; }
+      double2* row = a.mode == 2 ? const_cast<double2*>(tab[n]) : a.out + (int64_t)n * a.M;
+      row[c0 + c] = v;
+    }
+  }
+}
+
+__device__ __forceinline__ void bluestein_body(const K4Args& a, const double2* const* tab) {
+  extern __shared__ double2 buf[];
+  const int L = a.L, P = a.P, logP = a.logP, NC = a.NC;
+  const int64_t c0 = (int64_t)blockIdx.x * NC;
+  const int nc = (int)min((int64_t)NC, a.M - c0);
   // load with pre-chirp into bit-reversed positions; zero padding
   for (int idx = threadIdx.x; idx < NC * P; idx += blockDim.x) {
     const int n = idx / NC, col = idx % NC;
     double2 v = make_double2(0.0, 0.0);
     if (n < L && col < nc) {
-      const double2* row = in_rows ? in_rows->p[n] : in + (int64_t)n * M;
-      v = cm(row[c0 + col], pre[n]);
+      const double2* row = a.mode == 1 ? tab[n] : a.in + (int64_t)n * a.M;
+      v = cm(row[c0 + col], a.pre[n]);
     }
     const int rv = (int)(__brev((unsigned)n) >> (32 - logP));
     if (n < P) buf[(size_t)col * P + sw(rv)] = v;
   }
   __syncthreads();
   // forward FFT, then the filter spectrum (already scaled by 1/P), fused into its last pass
-  smem_fft(buf, P, logP, NC, tw, false, hhat);
-  smem_fft_dif(buf, P, logP, NC, tw, true);  // output in bit-reversed order
+  smem_fft(buf, P, logP, NC, a.tw, false, a.hhat);
+  smem_fft_dif(buf, P, logP, NC, a.tw, true);  // output in bit-reversed order
   for (int idx = threadIdx.x; idx < NC * L; idx += blockDim.x) {
     const int j = idx / NC, col = idx % NC;
     if (col < nc) {
-      double2* row = out_rows ? out_rows->p[j] : out + (int64_t)j * M;
+      double2* row = a.mode == 2 ? const_cast<double2*>(tab[j]) : a.out + (int64_t)j * a.M;
       const int jr = (int)(__brev((unsigned)j) >> (32 - logP));
-      row[c0 + col] = cm(buf[(size_t)col * P + sw(jr)], post[j]);
+      row[c0 + col] = cm(buf[(size_t)col * P + sw(jr)], a.post[j]);
     }
   }
 }
 
+constexpr int kMaxRows = 2048;
+struct RowTab {
+  const double2* p[kMaxRows];
+};
+
+__global__ void __launch_bounds__(kFftThreads, 3) stockham_kernel(const K4Args a) { stockham_body(a, nullptr); }
+__global__ void __launch_bounds__(kFftThreads, 3) stockham_rows_kernel(const K4Args a, const __grid_constant__ RowTab tab) {
+  stockham_body(a, tab.p);
+}
+__global__ void __launch_bounds__(kFftThreads) bluestein_kernel(const K4Args a) { bluestein_body(a, nullptr); }
+__global__ void __launch_bounds__(kFftThreads) bluestein_rows_kernel(const K4Args a, const __grid_constant__ RowTab tab) {
+  bluestein_body(a, tab.p);
+}
+
 }  // namespace
 
+// tab: host row table (mode 1: input rows, 2: output rows), copied into the kernel
+// parameters at launch (nothing to keep alive, capturable in a CUDA graph)
 bem_status fft_transform_rows(const double* in, double* out, int64_t M, int N, double R, bool inverse, cudaStream_t st,
-                              const RowPtrs* in_rows, const RowPtrs* out_rows) {
+                              const double2* const* tab, int mode) {
   Plan* pl = nullptr;
   bem_status rs = get_plan(N, R, inverse, &pl);
   if (rs != BEM_OK) return rs;
-  static const int nc_elems = [] {  // columns x points per CTA (env BEM_FFT_ELEMS; r01 sweep: 2048 best)
-    const char* e = getenv("BEM_FFT_ELEMS");
-    return e ? std::max(64, atoi(e)) : 2048;
-  }();
-  const int NC = std::max(1, nc_elems / pl->P);
-  const size_t smem = sizeof(double2) * (size_t)NC * pl->P;
-  BEM_CK(cudaFuncSetAttribute(bluestein_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const unsigned grid = (unsigned)((M + NC - 1) / NC);
-  bluestein_kernel<<<grid, kFftThreads, smem, st>>>((const double2*)in, (double2*)out, M, pl->L, pl->P, pl->logP, NC,
-                                                    (const double2*)pl->pre.p, (const double2*)pl->post.p,
-                                                    (const double2*)pl->hhat.p, (const double2*)pl->tw.p, in_rows,
-                                                    out_rows);
+  if (mode != 0 && N + 1 > kMaxRows) {
+    set_error("cqm transform rows: L = %d exceeds %d", N + 1, kMaxRows);
+    return BEM_EINVAL;
+  }
+  K4Args a{};
+  a.in = (const double2*)in; a.out = (double2*)out; a.M = M; a.L = pl->L; a.mode = mode; a.inverse = inverse ? 1 : 0;
+  RowTab* rt = nullptr;
+  std::unique_ptr<RowTab> hold;
+  if (mode != 0) {
+    hold = std::make_unique<RowTab>();
+    for (int r = 0; r <= N; ++r) hold->p[r] = tab[r];
+    rt = hold.get();
+  }
+  size_t smem;
+  if (pl->stock) {
+    a.nst = pl->nst;
+    for (int i = 0; i < pl->nst; ++i) a.rad[i] = pl->rad[i];
+    a.roots = (const double2*)pl->roots.p; a.scale = pl->scale.p;
+    // columns per CTA: the largest power of two keeping the two [L][NC] tiles and the root
+    // table within ~74 KB (three CTAs per SM)
+    int NC = 1;
+    while (NC < 64 && (size_t)(2 * 2 * NC + 1) * pl->L * 16 <= 74 * 1024) NC *= 2;
+    if (NC == 1 && (size_t)5 * pl->L * 16 <= 113 * 1024) NC = 2;  // >= 32-byte row segments (two CTAs per SM)
+    a.NC = NC;
+    smem = sizeof(double2) * ((size_t)2 * NC + 1) * pl->L;
+  } else {
+    static const int nc_elems = [] {  // columns x points per CTA (env BEM_FFT_ELEMS; r01 sweep: 2048 best)
+      const char* e = getenv("BEM_FFT_ELEMS");
+      return e ? std::max(64, atoi(e)) : 2048;
+    }();
+    a.NC = std::max(1, nc_elems / pl->P);
+    a.P = pl->P; a.logP = pl->logP;
+    a.pre = (const double2*)pl->pre.p; a.post = (const double2*)pl->post.p;
+    a.hhat = (const double2*)pl->hhat.p; a.tw = (const double2*)pl->tw.p;
+    smem = sizeof(double2) * (size_t)a.NC * pl->P;
+  }
+  const unsigned grid = (unsigned)((M + a.NC - 1) / a.NC);
+  if (pl->stock) {
+    if (rt) {
+      BEM_CK(cudaFuncSetAttribute(stockham_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      stockham_rows_kernel<<<grid, kFftThreads, smem, st>>>(a, *rt);
+    } else {
+      BEM_CK(cudaFuncSetAttribute(stockham_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      stockham_kernel<<<grid, kFftThreads, smem, st>>>(a);
+    }
+  } else {
+    if (rt) {
+      BEM_CK(cudaFuncSetAttribute(bluestein_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      bluestein_rows_kernel<<<grid, kFftThreads, smem, st>>>(a, *rt);
+    } else {
+      BEM_CK(cudaFuncSetAttribute(bluestein_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      bluestein_kernel<<<grid, kFftThreads, smem, st>>>(a);
+    }
+  }
   BEM_CK(cudaGetLastError());
   return BEM_OK;
 }
 
 bem_status fft_transform(const double* in, double* out, int64_t M, int N, double R, bool inverse, cudaStream_t st) {
-  return fft_transform_rows(in, out, M, N, R, inverse, st, nullptr, nullptr);
+  return fft_transform_rows(in, out, M, N, R, inverse, st, nullptr, 0);
 }
-
-// row tables live in device memory owned by a small per-thread cache (graph-safe:
-// the table is written with cudaMemcpyAsync on the caller's stream before the kernel)
-struct RowTable {
-  DBuf<double> buf;  // sizeof(RowPtrs) bytes
-};
-static thread_local RowTable g_rows[2];
 
 }  // namespace bem
 
@@ -339,20 +546,6 @@ extern "C" bem_status cqm_inverse(const bem_c128* y_freq, bem_c128* y_time, int6
   return transform_entry(y_freq, y_time, M_loc, N, R, cuda_stream, true);
 }
 
-// host pointer table -> device table (async on the stream; the host array is copied into
-// pinned staging first, so the caller may reuse it immediately)
-static bem_status upload_rows(int which, bem_c128* const* rows, int L, cudaStream_t st, const RowPtrs** dev) {
-  static thread_local RowPtrs* staging[2] = {nullptr, nullptr};
-  RowTable& tb = g_rows[which];
-  if (!tb.buf.p) BEM_CK(tb.buf.alloc((sizeof(RowPtrs) + 7) / 8));
-  if (!staging[which]) BEM_CK(cudaMallocHost((void**)&staging[which], sizeof(RowPtrs)));
-  BEM_CK(cudaStreamSynchronize(st));  // the previous use of this staging slot has been consumed
-  for (int r = 0; r < L; ++r) staging[which]->p[r] = (double2*)rows[r];
-  BEM_CK(cudaMemcpyAsync(tb.buf.p, staging[which], sizeof(double2*) * (size_t)L, cudaMemcpyHostToDevice, st));
-  *dev = (const RowPtrs*)tb.buf.p;
-  return BEM_OK;
-}
-
 extern "C" bem_status cqm_forward_rows(const bem_c128* x_time, int64_t M_loc, bem_c128* const* out_rows, int32_t N,
                                        double R, void* cuda_stream) {
   BEM_REQ(x_time && out_rows, "cqm_forward_rows: NULL pointer");
@@ -363,10 +556,8 @@ extern "C" bem_status cqm_forward_rows(const bem_c128* x_time, int64_t M_loc, be
   BEM_CK(cudaPointerGetAttributes(&at, x_time));
   BEM_REQ(at.type == cudaMemoryTypeDevice, "cqm_forward_rows: input must be device memory");
   DeviceGuard dg(at.device);
-  const RowPtrs* dev = nullptr;
-  bem_status rs = upload_rows(0, out_rows, N + 1, (cudaStream_t)cuda_stream, &dev);
-  if (rs != BEM_OK) return rs;
-  return fft_transform_rows((const double*)x_time, nullptr, M_loc, N, R, false, (cudaStream_t)cuda_stream, nullptr, dev);
+  return fft_transform_rows((const double*)x_time, nullptr, M_loc, N, R, false, (cudaStream_t)cuda_stream,
+                            (const double2* const*)out_rows, 2);
 }
 
 extern "C" bem_status cqm_inverse_rows(bem_c128* const* in_rows, bem_c128* y_time, int64_t M_loc, int32_t N, double R,
@@ -379,10 +570,8 @@ extern "C" bem_status cqm_inverse_rows(bem_c128* const* in_rows, bem_c128* y_tim
   BEM_CK(cudaPointerGetAttributes(&at, y_time));
   BEM_REQ(at.type == cudaMemoryTypeDevice, "cqm_inverse_rows: output must be device memory");
   DeviceGuard dg(at.device);
-  const RowPtrs* dev = nullptr;
-  bem_status rs = upload_rows(1, in_rows, N + 1, (cudaStream_t)cuda_stream, &dev);
-  if (rs != BEM_OK) return rs;
-  return fft_transform_rows(nullptr, (double*)y_time, M_loc, N, R, true, (cudaStream_t)cuda_stream, dev, nullptr);
+  return fft_transform_rows(nullptr, (double*)y_time, M_loc, N, R, true, (cudaStream_t)cuda_stream,
+                            (const double2* const*)in_rows, 1);
 }
 
 // CUDA IPC helpers for the peer row tables (multi-GPU transposes without NCCL)

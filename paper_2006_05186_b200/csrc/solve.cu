@@ -395,6 +395,65 @@ bem_status solve_stats(const std::vector<int>& hit, const std::vector<double>& h
   return finish_stats(hit, hrel, tol, max_iter, imag_rel, stats);
 }
 
+// cqm_solve on G ranks: this rank's DOF shard g_time [L][M_loc] -> forward K4 + NCCL
+// all-to-all -> batched GMRES on this rank's frequencies -> all-to-all + inverse K4.
+bem_status solve_sharded(Op& op, const double* g_time, double* phi_time, int64_t M_loc, double R, double tol,
+                         int restart, int max_iter, bem_comm c, cudaStream_t st, bem_solve_stats* stats) {
+  BEM_REQ(tol > 0.0 && restart >= 1 && max_iter >= 1, "cqm_solve: bad tol/restart/max_iter");
+  BEM_REQ(R > 0.0 && R < 1.0, "cqm_solve: R must lie in (0,1)");
+  bem_status rs = comm_check(c, op, M_loc);
+  if (rs != BEM_OK) return rs;
+  DeviceGuard dg(op.tree->device);
+  const int N = op.L - 1;
+  const int64_t nt = M_loc * op.L, nf = op.tree->M * op.n_local;
+  DBuf<double> tmpc, x, mx;
+  BEM_CK(tmpc.alloc(2 * std::max<int64_t>(nt, 1))); BEM_CK(x.alloc(2 * std::max<int64_t>(nf, 1)));
+  BEM_CK(mx.alloc(2));
+  real_to_complex_kernel<<<nblk(nt), 256, 0, st>>>(g_time, (double2*)tmpc.p, nt);
+  BEM_CK(cudaGetLastError());
+  double2* gf = nullptr;
+  rs = shard_forward(op, c, tmpc.p, R, &gf, st);
+  if (rs != BEM_OK) return rs;
+  std::vector<int> hit;
+  std::vector<double> hrel;
+  rs = gmres_multifreq(op, gf, (double2*)x.p, tol, restart, max_iter, st, hit, hrel);
+  if (rs != BEM_OK) return rs;
+  rs = shard_inverse(op, c, (const double2*)x.p, R, tmpc.p, st);
+  if (rs != BEM_OK) return rs;
+  BEM_CK(cudaMemsetAsync(mx.p, 0, sizeof(double) * 2, st));
+  complex_to_real_kernel<<<1024, kRed, 0, st>>>((const double2*)tmpc.p, phi_time, nt, mx.p);
+  BEM_CK(cudaGetLastError());
+  // statistics over the ranks: max (iters_max, resid_max, max |Im|, max |phi|), sum (unconverged, iters)
+  int nunc = 0, imax = 0;
+  long long isum = 0;
+  double rmax = 0.0;
+  for (size_t t = 0; t < hit.size(); ++t) {
+    rmax = std::max(rmax, hrel[t]);
+    if (hrel[t] > tol) ++nunc;
+    imax = std::max(imax, hit[t]);
+    isum += hit[t];
+  }
+  double* red = comm_scratch(c);
+  const double loc[6] = {(double)imax, rmax, 0.0, 0.0, (double)nunc, (double)isum};
+  BEM_CK(cudaMemcpyAsync(red, loc, sizeof(loc), cudaMemcpyHostToDevice, st));
+  BEM_CK(cudaMemcpyAsync(red + 2, mx.p, 2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  rs = comm_allreduce(c, red, 4, 2, st);
+  if (rs != BEM_OK) return rs;
+  double glob[6];
+  BEM_CK(cudaMemcpyAsync(glob, red, sizeof(glob), cudaMemcpyDeviceToHost, st));
+  BEM_CK(cudaStreamSynchronize(st));
+  if (stats) {
+    stats->iters_max = (int32_t)glob[0]; stats->resid_max = glob[1];
+    stats->imag_rel_max = glob[3] > 0.0 ? glob[2] / glob[3] : 0.0;
+    stats->n_unconverged = (int32_t)glob[4]; stats->iters_sum = (int32_t)glob[5];
+  }
+  if (glob[4] > 0) {
+    set_error("cqm_solve: %d frequencies (all ranks) did not converge within max_iter=%d", (int)glob[4], max_iter);
+    return BEM_ENOCONV;
+  }
+  return BEM_OK;
+}
+
 }  // namespace bem
 
 extern "C" bem_status bem_solve_multifreq(bem_op oh, const bem_c128* g_freq, bem_c128* phi_freq, double tol,
@@ -419,7 +478,8 @@ extern "C" bem_status cqm_solve(bem_op oh, const double* g_time, double* phi_tim
   BEM_REQ(oh && g_time && phi_time, "cqm_solve: NULL argument");
   Op& op = oh->o;
   Tree& tr = *op.tree;
-  BEM_REQ(nccl_comm == nullptr, "cqm_solve: multi-GPU transpose is issued by the caller; pass nccl_comm = NULL");
+  if (nccl_comm != nullptr) return solve_sharded(op, g_time, phi_time, M_loc, R, tol, restart, max_iter,
+                                                 (bem_comm)nccl_comm, (cudaStream_t)cuda_stream, stats);
   BEM_REQ(M_loc == tr.M, "cqm_solve: M_loc must equal the number of panels on a single device");
   BEM_REQ(op.n_local == op.L, "cqm_solve: the operator must hold all L frequencies");
   for (int t = 0; t < op.n_local; ++t) BEM_REQ(op.local_l[t] == t, "cqm_solve: local_l must be 0..L-1 in order");

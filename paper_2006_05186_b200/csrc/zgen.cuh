@@ -69,11 +69,13 @@ __device__ __forceinline__ void column(const Src& a, int b, int r, int l, double
   const int32_t* qp = a.pivq + (int64_t)b * a.rcap;
   for (int i = 0; i < r; ++i) {  // forward: d_i
     double2 acc = fibre(a, rc, cc, qp[i], l);
+#pragma unroll 4
     for (int j = 0; j < i; ++j) acc = csub(acc, cmul(F[i * r + j], z[j * stride]));
     z[i * stride] = cdiv(acc, F[i * r + i]);
   }
   for (int i = r - 1; i >= 0; --i) {  // backward: Z_i = d_i - sum_{j>i} U[i][j] Z_j
     double2 acc = z[i * stride];
+#pragma unroll 4
     for (int j = i + 1; j < r; ++j) acc = csub(acc, cmul(F[i * r + j], z[j * stride]));
     z[i * stride] = acc;
   }

@@ -180,3 +180,28 @@ def test_sharded_solve_matches_single_process():
         assert st["n_unconverged"] == 0 and st["iters_max"] == int(it.max()) and st["iters_sum"] == int(it.sum())
     sc = (R ** np.arange(L))[:, None]
     assert np.linalg.norm((phi - ref) * sc) / np.linalg.norm(ref * sc) <= 1e-13
+
+
+def test_library_shard_map_equals_dist_py():
+    """The C-ABI's frequency shard (bem_shard_frequencies, used by the NCCL transposes
+    inside libbem) is the same class partition as dist.shard_frequencies."""
+    from paper_2006_05186_b200 import bem as B
+    for L in list(range(1, 70)) + [129, 257, 513, 1025]:
+        for G in range(1, min(L // 2 + 1, 16) + 1):
+            a, b = B.shard_frequencies(L, G), shard_frequencies(L, G)
+            assert len(a) == len(b) and all(np.array_equal(x, y) for x, y in zip(a, b)), (L, G)
+    with pytest.raises(B.BemError):
+        B.shard_frequencies(5, 4)  # 3 classes only
+
+
+def test_bench_gpus_n_spawns_n_ranks():
+    """`python bench.py --gpus 2` (no torchrun around it) starts 2 ranks itself."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--ranks-dry-run"],
+                       capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert sorted(d["rank"] for d in lines) == [0, 1] and all(d["world"] == 2 for d in lines)

@@ -9,7 +9,8 @@ import torch  # noqa: E402
 import paper_2006_05186_b200 as pb  # noqa: E402
 
 out = {}
-for name, M, N in (("config2", 5120, 128), ("config3", 20480, 256), ("config4", 81920, 512)):
+for name, M, N in (("config2", 5120, 128), ("config3", 20480, 256), ("config4", 81920, 512),
+                   ("config5_rank_of_2", 163840, 1024)):
     R = 10.0 ** (-5.0 / N)
     x = torch.randn(N + 1, M, dtype=torch.complex128, device="cuda")
     for _ in range(3):
@@ -23,6 +24,13 @@ for name, M, N in (("config2", 5120, 128), ("config3", 20480, 256), ("config4", 
     e1.record()
     e1.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    e0.record()
+    for _ in range(reps):
+        z = pb.cqm_inverse(y, N, R)
+    e1.record()
+    e1.synchronize()
+    msi = e0.elapsed_time(e1) / reps
     bytes_ = 32.0 * M * (N + 1)
-    out[name] = {"ms": ms, "GB/s": bytes_ / (ms * 1e-3) / 1e9}
+    out[name] = {"forward_ms": ms, "inverse_ms": msi, "forward_GB/s": bytes_ / (ms * 1e-3) / 1e9,
+                 "inverse_GB/s": bytes_ / (msi * 1e-3) / 1e9}
 print(json.dumps(out))

@@ -505,9 +505,12 @@ def main():
     # T_roof = sum_k max(F_k / P_FP64, B_k / BW) against the measured apply time
     hbm = hbm_peak_gbs()
     p_, C_ = stats["p"], stats["clusters"]
+    m_ = round(p_ ** (1.0 / 3.0))
     b_up = 16.0 * M * nl + 16.0 * p_ * nl * C_
     b_down = 16.0 * p_ * nl * C_ + 32.0 * M * nl
-    f_up = 8.0 * p_ * M * nl + 8.0 * p_ * p_ * nl * (C_ - 1)
+    # leaf products W^T x / U yhat: one real x complex MAC (4 flops) per (panel, node, frequency);
+    # Kronecker transfers: 3 m p real x complex MACs per (non-root cluster, frequency)
+    f_up = 4.0 * p_ * M * nl + 12.0 * m_ * p_ * nl * (C_ - 1)
     pk_near = (peaks["dmma"] or FP64_PEAK_DERIVED / 1e12) if base_mode == pb.BEM_MODE_COMBINED else FP64_PEAK_DERIVED / 1e12
     pk_far = (peaks["dmma"] or FP64_PEAK_DERIVED / 1e12) if aca_far else FP64_PEAK_DERIVED / 1e12
     kern = {
@@ -529,8 +532,9 @@ def main():
     t_apply = sum(kt.values())
     per_kernel = {"kernels": kern, "apply_roof_ms": t_roof, "apply_ms": t_apply,
                   "apply_frac": t_roof / t_apply if t_apply > 0 else None,
-                  "model": "SURVEY §8(d): F, B per kernel (75 flops per K1 evaluation; K2 general-E flops and "
-                           "minimum bytes), P = measured DMMA / derived FP64 ALU peak, BW = MEASURED_PEAKS.json hbm_gbs"}
+                  "model": "SURVEY §8(d): F, B per kernel (75 flops per K1 evaluation; K2 with Kronecker transfers: "
+                           "4 p M L + 12 m p L (C-1) flops (4 per real x complex MAC) and minimum bytes), P = measured "
+                           "DMMA / derived FP64 ALU peak, BW = MEASURED_PEAKS.json hbm_gbs"}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",

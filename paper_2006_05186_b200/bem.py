@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbem.so")
+LIB_PATH = os.environ.get("BEM_LIB_PATH") or os.path.join(HERE, "libbem.so")  # override: A/B builds (tools)
 
 BEM_MODE_H2ACA, BEM_MODE_H2ONLY, BEM_MODE_DENSE, BEM_MODE_COMBINED = 0, 1, 2, 3
 BEM_SKEL_Z, BEM_SKEL_FACTORS = 0x100, 0x200  # skeleton storage flags OR-ed into mode (include/bem.h)

@@ -607,6 +607,7 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
     }
   }
   DeviceGuard dg(t.device);
+  Nvtx nv("a10 bem_assemble_h2_aca");
   cudaStream_t st = (cudaStream_t)cuda_stream;
   bem_op_s* h = new bem_op_s();
   Op& op = h->o;
@@ -867,7 +868,7 @@ extern "C" bem_status bem_op_get_info(bem_op oh, bem_op_info* out) {
   const size_t i32 = op.d_local_l.n + op.d_class_t1.n + op.d_class_t2.n + op.d_dn_jb.n + op.d_dn_je.n + op.d_dn_j.n +
                      op.d_rank.n + op.d_pivk.n + op.d_pivq.n + op.d_far_rows.n + op.d_segs.n + op.d_seg_rows.n +
                      op.d_seg_ptr.n + op.d_nrank.n + op.d_npivk.n + op.d_npivq.n + op.d_nm_order.n + op.d_nm_counter.n;
-  const size_t i64 = op.d_zoff.n + op.d_foff.n + op.d_nzoff.n + op.d_nsoff.n + op.d_fsoff.n + op.d_g0noff.n;
+  const size_t i64 = op.d_zoff.n + op.d_foff.n + op.d_ztoff.n + op.d_nzoff.n + op.d_nsoff.n + op.d_fsoff.n + op.d_g0noff.n;
   out->device_bytes = (int64_t)(8 * dbl + 4 * i32 + 8 * i64);
   return BEM_OK;
 }

@@ -295,7 +295,299 @@ __global__ void __launch_bounds__(kPassThreads) down_leaf_s_kernel(const int32_t
   }
 }
 
+// Leaf products on the FP64 tensor cores (mma.sync m8n8k4 f64, SASS DMMA): with the 16
+// frequencies of a tile as 32 interleaved real columns,
+//   up:   xhat_c[t][nu] = sum_k W[k][nu] x[t][k]         = (W^T)(p x n) . X(n x 32)
+//   down: y[t][k]  = yc[t][k] + sum_mu U[k][mu] yhat[t][mu] = U(n x p) . Y(p x 32)
+// A fragments from the basis tile, B fragments from the transposed coefficient tile
+// (both in shared memory, row strides = 8 mod 16 doubles: two wavefronts per fragment
+// load); each warp owns 8 x 8 output tiles, K = n (up) / p (down) in steps of 4.
+constexpr int kLeafT = 16;  // frequencies per CTA (32 real columns = 4 DMMA column tiles)
+
+__device__ __forceinline__ void dmma_k2(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__host__ __device__ __forceinline__ int pad8(int n) { return (n + 15) / 16 * 16 + 8; }  // row stride = 8 (mod 16)
+
+__global__ void __launch_bounds__(kPassThreads) up_leaf_d_kernel(const int32_t* __restrict__ leaves,
+                                                                 const int32_t* __restrict__ cb,
+                                                                 const int32_t* __restrict__ ce,
+                                                                 const double* __restrict__ W,
+                                                                 const double2* __restrict__ xc,
+                                                                 double2* __restrict__ xhat, int64_t M, int nl, int p) {
+  extern __shared__ double smd[];
+  const int c = leaves[blockIdx.x];
+  const int b = cb[c], n = ce[c] - b;
+  const int n4 = (n + 3) & ~3;
+  const int t0 = blockIdx.y * kLeafT;
+  const int nt = min(kLeafT, nl - t0);
+  const int WS = pad8(p), XS = pad8(2 * kLeafT);
+  double* Ws = smd;              // [n4][WS]: W[k][nu]
+  double* Xs = Ws + n4 * WS;     // [n4][XS]: x[t][k] as Xs[k][2t + re/im]
+  for (int i = threadIdx.x; i < n4 * p; i += blockDim.x) {
+    const int k = i / p, nu = i - k * p;
+    Ws[k * WS + nu] = k < n ? W[(int64_t)(b + k) * p + nu] : 0.0;
+  }
+  for (int i = threadIdx.x; i < n4 * kLeafT; i += blockDim.x) {
+    const int tl = i / n4, k = i - tl * n4;  // consecutive threads: consecutive panels (coalesced)
+    const double2 v = (k < n && tl < nt) ? xc[(int64_t)(t0 + tl) * M + b + k] : make_double2(0.0, 0.0);
+    Xs[k * XS + 2 * tl] = v.x;
+    Xs[k * XS + 2 * tl + 1] = v.y;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int nvt = (p + 7) / 8;
+  for (int tile = warp; tile < nvt * 4; tile += blockDim.x >> 5) {
+    const int v0 = (tile >> 2) * 8, n0 = (tile & 3) * 8;
+    const int nu = v0 + g;
+    double c0 = 0.0, c1 = 0.0;
+    for (int k0 = 0; k0 < n4; k0 += 4) {
+      const double a = nu < p ? Ws[(k0 + q) * WS + nu] : 0.0;
+      const double bb = Xs[(k0 + q) * XS + n0 + g];
+      dmma_k2(c0, c1, a, bb);
+    }
+    const int tl = (n0 >> 1) + q;  // columns n0 + 2q, n0 + 2q + 1 = (re, im) of frequency tl
+    if (nu < p && tl < nt) xhat[((int64_t)c * nl + t0 + tl) * p + nu] = make_double2(c0, c1);
+  }
+}
+
+__global__ void __launch_bounds__(kPassThreads) down_leaf_d_kernel(const int32_t* __restrict__ leaves,
+                                                                   const int32_t* __restrict__ cb,
+                                                                   const int32_t* __restrict__ ce,
+                                                                   const double* __restrict__ U,
+                                                                   const double2* __restrict__ yhat,
+                                                                   const double2* __restrict__ yc,
+                                                                   const int32_t* __restrict__ perm,
+                                                                   double2* __restrict__ y, int64_t M, int nl, int p,
+                                                                   const double2* __restrict__ xc, double alpha) {
+  extern __shared__ double smd[];
+  const int c = leaves[blockIdx.x];
+  const int b = cb[c], n = ce[c] - b;
+  const int p4 = (p + 3) & ~3;
+  const int t0 = blockIdx.y * kLeafT;
+  const int nt = min(kLeafT, nl - t0);
+  const int US = pad8(p4), YS = pad8(2 * kLeafT);
+  const int n8 = (n + 7) & ~7;
+  double* Us = smd;              // [n8][US]: U[k][mu]
+  double* Ys = Us + n8 * US;     // [p4][YS]: yhat[t][mu] as Ys[mu][2t + re/im]
+  for (int i = threadIdx.x; i < n8 * p4; i += blockDim.x) {
+    const int k = i / p4, mu = i - k * p4;
+    Us[k * US + mu] = (k < n && mu < p) ? U[(int64_t)(b + k) * p + mu] : 0.0;
+  }
+  for (int i = threadIdx.x; i < kLeafT * p4; i += blockDim.x) {
+    const int tl = i / p4, mu = i - tl * p4;
+    const double2 v = (mu < p && tl < nt) ? yhat[((int64_t)c * nl + t0 + tl) * p + mu] : make_double2(0.0, 0.0);
+    Ys[mu * YS + 2 * tl] = v.x;
+    Ys[mu * YS + 2 * tl + 1] = v.y;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int nkt = n8 / 8;
+  for (int tile = warp; tile < nkt * 4; tile += blockDim.x >> 5) {
+    const int k0r = (tile >> 2) * 8, n0 = (tile & 3) * 8;
+    double c0 = 0.0, c1 = 0.0;
+    for (int m0 = 0; m0 < p4; m0 += 4) {
+      const double a = Us[(k0r + g) * US + m0 + q];
+      const double bb = Ys[(m0 + q) * YS + n0 + g];
+      dmma_k2(c0, c1, a, bb);
+    }
+    const int k = k0r + g, tl = (n0 >> 1) + q;
+    if (k < n && tl < nt) {
+      const int64_t row = (int64_t)(t0 + tl) * M;
+      double2 acc = yc[row + b + k];
+      acc.x += c0;
+      acc.y += c1;
+      if (alpha != 0.0) {
+        const double2 xv = xc[row + b + k];
+        acc.x = fma(alpha, xv.x, acc.x);
+        acc.y = fma(alpha, xv.y, acc.y);
+      }
+      y[row + perm[b + k]] = acc;
+    }
+  }
+}
+
+// Kronecker transfers (tensor Chebyshev interpolation): E = E_z (x) E_y (x) E_x,
+// so E^T x (upward) and E y (downward) are three m x m mode products on the m x m x m
+// coefficient tensor (index mu = mx + m my + m^2 mz): 3 m p multiply-adds per (cluster,
+// frequency) instead of p^2.  CTA = (parent cluster, tile of TF frequencies); the tiles of
+// both sons / the parent are staged in shared memory and contracted axis by axis.
+template <int MC>  // m at compile time (0: runtime m): constant index arithmetic
+__global__ void __launch_bounds__(kPassThreads) up_transfer_k_kernel(const int32_t* __restrict__ list,
+                                                                     const int32_t* __restrict__ son0,
+                                                                     const int32_t* __restrict__ son1,
+                                                                     const double* __restrict__ E1,
+                                                                     double2* __restrict__ xhat, int nl, int m_, int TF) {
+  extern __shared__ double2 smk[];
+  const int m = MC > 0 ? MC : m_;
+  const int p = m * m * m, mm = m * m;
+  const int c = list[blockIdx.x];
+  const int sons[2] = {son0[c], son1[c]};
+  const int t0 = blockIdx.y * TF;
+  const int nt = min(TF, nl - t0);
+  double2* A = smk;                      // [2][TF][p]
+  double2* B = A + 2 * TF * p;           // [2][TF][p]
+  double* Es = (double*)(B + 2 * TF * p);  // [2][3][m][m]
+  for (int i = threadIdx.x; i < 2 * 3 * mm; i += blockDim.x) {
+    const int sidx = i / (3 * mm);
+    Es[i] = E1[(size_t)sons[sidx] * 3 * mm + (i - sidx * 3 * mm)];
+  }
+  const int TP = TF * p;
+  for (int i = threadIdx.x; i < 2 * TP; i += blockDim.x) {
+    const int sidx = i / TP, r = i - sidx * TP;
+    A[i] = r < nt * p ? xhat[((int64_t)sons[sidx] * nl + t0) * p + r] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  // x: B[s][t][lz][ly][mx] = sum_lx Ex[lx][mx] A[s][t][lz][ly][lx]
+  for (int i = threadIdx.x; i < 2 * TP; i += blockDim.x) {
+    const int sidx = i / TP, e = i % p;
+    const int mx = e % m, rest = e - mx;
+    const double* Ex = Es + sidx * 3 * mm;
+    const double2* a = A + (i - e) + rest;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int l = 0; l < m; ++l) {
+      const double w = Ex[l * m + mx];
+      acc.x = fma(w, a[l].x, acc.x);
+      acc.y = fma(w, a[l].y, acc.y);
+    }
+    B[i] = acc;
+  }
+  __syncthreads();
+  // y: A[s][t][lz][my][mx] = sum_ly Ey[ly][my] B[s][t][lz][ly][mx]
+  for (int i = threadIdx.x; i < 2 * TP; i += blockDim.x) {
+    const int sidx = i / TP, e = i % p;
+    const int mx = e % m, my = (e / m) % m, lz = e / mm;
+    const double* Ey = Es + sidx * 3 * mm + mm;
+    const double2* b = B + (i - e) + lz * mm + mx;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int l = 0; l < m; ++l) {
+      const double w = Ey[l * m + my];
+      acc.x = fma(w, b[l * m].x, acc.x);
+      acc.y = fma(w, b[l * m].y, acc.y);
+    }
+    A[i] = acc;
+  }
+  __syncthreads();
+  // z and the sum over both sons: out[t][mz][my][mx] = sum_s sum_lz Ez_s[lz][mz] A[s][t][lz][my][mx]
+  for (int i = threadIdx.x; i < nt * p; i += blockDim.x) {
+    const int e = i % p;
+    const int mz = e / mm, rest = e - mz * mm;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int sidx = 0; sidx < 2; ++sidx) {
+      const double* Ez = Es + sidx * 3 * mm + 2 * mm;
+      const double2* a = A + sidx * TP + (i - e) + rest;
+      for (int l = 0; l < m; ++l) {
+        const double w = Ez[l * m + mz];
+        acc.x = fma(w, a[l * mm].x, acc.x);
+        acc.y = fma(w, a[l * mm].y, acc.y);
+      }
+    }
+    xhat[((int64_t)c * nl + t0) * p + i] = acc;
+  }
+}
+
+template <int MC>  // m at compile time (0: runtime m): constant index arithmetic
+__global__ void __launch_bounds__(kPassThreads) down_transfer_k_kernel(const int32_t* __restrict__ list,
+                                                                       const int32_t* __restrict__ son0,
+                                                                       const int32_t* __restrict__ son1,
+                                                                       const double* __restrict__ E1,
+                                                                       double2* __restrict__ yhat, int nl, int m_, int TF) {
+  extern __shared__ double2 smk[];
+  const int m = MC > 0 ? MC : m_;
+  const int p = m * m * m, mm = m * m;
+  const int c = list[blockIdx.x];
+  const int sons[2] = {son0[c], son1[c]};
+  const int t0 = blockIdx.y * TF;
+  const int nt = min(TF, nl - t0);
+  const int TP = TF * p;
+  double2* P = smk;                      // [TF][p] parent tile
+  double2* B = P + TP;                   // [2][TF][p]
+  double2* C2 = B + 2 * TP;              // [2][TF][p]
+  double* Es = (double*)(C2 + 2 * TP);   // [2][3][m][m]
+  for (int i = threadIdx.x; i < 2 * 3 * mm; i += blockDim.x) {
+    const int sidx = i / (3 * mm);
+    Es[i] = E1[(size_t)sons[sidx] * 3 * mm + (i - sidx * 3 * mm)];
+  }
+  for (int i = threadIdx.x; i < TP; i += blockDim.x)
+    P[i] = i < nt * p ? yhat[((int64_t)c * nl + t0) * p + i] : make_double2(0.0, 0.0);
+  __syncthreads();
+  // x: B[s][t][mz][my][lx] = sum_mx Ex_s[lx][mx] P[t][mz][my][mx]
+  for (int i = threadIdx.x; i < 2 * TP; i += blockDim.x) {
+    const int sidx = i / TP, r = i - sidx * TP, e = r % p;
+    const int lx = e % m, rest = e - lx;
+    const double* Ex = Es + sidx * 3 * mm;
+    const double2* a = P + (r - e) + rest;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int u = 0; u < m; ++u) {
+      const double w = Ex[lx * m + u];
+      acc.x = fma(w, a[u].x, acc.x);
+      acc.y = fma(w, a[u].y, acc.y);
+    }
+    B[i] = acc;
+  }
+  __syncthreads();
+  // y: C[s][t][mz][ly][lx] = sum_my Ey_s[ly][my] B[s][t][mz][my][lx]
+  for (int i = threadIdx.x; i < 2 * TP; i += blockDim.x) {
+    const int sidx = i / TP, e = i % p;
+    const int lx = e % m, ly = (e / m) % m, mz = e / mm;
+    const double* Ey = Es + sidx * 3 * mm + mm;
+    const double2* b = B + (i - e) + mz * mm + lx;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int u = 0; u < m; ++u) {
+      const double w = Ey[ly * m + u];
+      acc.x = fma(w, b[u * m].x, acc.x);
+      acc.y = fma(w, b[u * m].y, acc.y);
+    }
+    C2[i] = acc;
+  }
+  __syncthreads();
+  // z: yhat_s[t][lz][ly][lx] += sum_mz Ez_s[lz][mz] C[s][t][mz][ly][lx]
+  for (int i = threadIdx.x; i < 2 * TP; i += blockDim.x) {
+    const int sidx = i / TP, r = i - sidx * TP, e = r % p;
+    if (r >= nt * p) continue;
+    const int lz = e / mm, rest = e - lz * mm;
+    const double* Ez = Es + sidx * 3 * mm + 2 * mm;
+    const double2* cc = C2 + (i - e) + rest;
+    double2* out = yhat + ((int64_t)sons[sidx] * nl + t0) * p + r;
+    double2 acc = *out;
+    for (int u = 0; u < m; ++u) {
+      const double w = Ez[lz * m + u];
+      acc.x = fma(w, cc[u * mm].x, acc.x);
+      acc.y = fma(w, cc[u * mm].y, acc.y);
+    }
+    *out = acc;
+  }
+}
+
 constexpr size_t kPassSmemMax = 100 * 1024;
+
+template <int MC>
+cudaError_t launch_upk(unsigned n, unsigned ttk, size_t sm, cudaStream_t st, const int32_t* list, const int32_t* s0,
+                       const int32_t* s1, const double* E1, double2* xhat, int nl, int m, int TF, bool down) {
+  auto k = down ? down_transfer_k_kernel<MC> : up_transfer_k_kernel<MC>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  k<<<dim3(n, ttk), kPassThreads, sm, st>>>(list, s0, s1, E1, xhat, nl, m, TF);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transfer_k(unsigned n, unsigned ttk, size_t sm, cudaStream_t st, const int32_t* list,
+                              const int32_t* s0, const int32_t* s1, const double* E1, double2* xy, int nl, int m,
+                              int TF, bool down) {
+  switch (m) {
+    case 3: return launch_upk<3>(n, ttk, sm, st, list, s0, s1, E1, xy, nl, m, TF, down);
+    case 4: return launch_upk<4>(n, ttk, sm, st, list, s0, s1, E1, xy, nl, m, TF, down);
+    case 5: return launch_upk<5>(n, ttk, sm, st, list, s0, s1, E1, xy, nl, m, TF, down);
+    default: return launch_upk<0>(n, ttk, sm, st, list, s0, s1, E1, xy, nl, m, TF, down);
+  }
+}
+
+
+constexpr size_t kLeafSmemMax = 160 * 1024;
+constexpr size_t kTransferSmem = 56 * 1024;  // Kronecker transfers: 4 CTAs per SM  // DMMA leaf kernels (p = 125: one CTA per SM)
 
 __global__ void scatter_kernel(const double2* __restrict__ yc, double2* __restrict__ y,
                                const int32_t* __restrict__ perm, int64_t M, int nl, const double2* __restrict__ xc, double alpha) {
@@ -314,8 +606,14 @@ __global__ void scatter_kernel(const double2* __restrict__ yc, double2* __restri
 bem_status run_up(Tree& t, const double* W, const double2* xc, double2* xhat, int nl, cudaStream_t st) {
   const int p = t.p;
   const unsigned tt = (unsigned)((nl + kPassT - 1) / kPassT);
+  const int n4 = (t.max_leaf + 3) & ~3;
+  const size_t sm_d = sizeof(double) * (size_t)n4 * (pad8(p) + pad8(2 * kLeafT));
   const size_t sm_leaf = sizeof(double2) * kPassT * t.max_leaf + sizeof(double) * (size_t)t.max_leaf * p;
-  if (sm_leaf <= kPassSmemMax) {
+  if (sm_d <= kLeafSmemMax) {
+    BEM_CK(cudaFuncSetAttribute(up_leaf_d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d));
+    up_leaf_d_kernel<<<dim3((unsigned)t.n_leaves, (unsigned)((nl + kLeafT - 1) / kLeafT)), kPassThreads, sm_d, st>>>(
+        t.d_leaves.p, t.d_begin.p, t.d_end.p, W, xc, xhat, t.M, nl, p);
+  } else if (sm_leaf <= kPassSmemMax) {
     BEM_CK(cudaFuncSetAttribute(up_leaf_s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_leaf));
     up_leaf_s_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, sm_leaf, st>>>(t.d_leaves.p, t.d_begin.p,
                                                                                    t.d_end.p, W, xc, xhat, t.M, nl, p);
@@ -324,6 +622,19 @@ bem_status run_up(Tree& t, const double* W, const double2* xc, double2* xhat, in
                                                                              xc, xhat, t.M, nl, p);
   }
   BEM_CK(cudaGetLastError());
+  // Kronecker transfers: TF frequencies per CTA with four [TF][p] tiles in shared memory
+  const int TF = std::max(1, std::min(16, (int)(kTransferSmem / (sizeof(double2) * 4 * p))));
+  const size_t sm_k = sizeof(double2) * 4 * (size_t)TF * p + sizeof(double) * 6 * t.m * t.m;
+  const unsigned ttk = (unsigned)((nl + TF - 1) / TF);
+  if (t.d_E1.p) {
+    for (int lv = t.depth - 1; lv >= 0; --lv) {
+      const int n = (int)t.level_nonleaf[lv].size();
+      if (n == 0) continue;
+      BEM_CK(launch_transfer_k((unsigned)n, ttk, sm_k, st, t.d_level_nonleaf[lv].p, t.d_son0.p, t.d_son1.p, t.d_E1.p,
+                               xhat, nl, t.m, TF, false));
+    }
+    return BEM_OK;
+  }
   const size_t sm_tr = sizeof(double2) * 2 * kPassT * p + sizeof(double) * 2 * (size_t)p * p;
   const bool staged = sm_tr <= kPassSmemMax;
   if (staged)
@@ -346,14 +657,21 @@ bem_status run_down(Tree& t, double2* yhat, const double2* yc, double2* y, int n
                     cudaStream_t st, cudaEvent_t wait_before_leaf = nullptr) {
   const int p = t.p;
   const unsigned tt = (unsigned)((nl + kPassT - 1) / kPassT);
+  const int TF = std::max(1, std::min(16, (int)(kTransferSmem / (sizeof(double2) * 5 * p))));
+  const size_t sm_k = sizeof(double2) * 5 * (size_t)TF * p + sizeof(double) * 6 * t.m * t.m;
+  const unsigned ttk = (unsigned)((nl + TF - 1) / TF);
   const size_t sm_tr = sizeof(double2) * kPassT * p + sizeof(double) * 2 * (size_t)p * p;
+  const bool kron = t.d_E1.p != nullptr;
   const bool staged = sm_tr <= kPassSmemMax;
-  if (staged)
+  if (!kron && staged)
     BEM_CK(cudaFuncSetAttribute(down_transfer_s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_tr));
   for (int lv = 0; lv < t.depth; ++lv) {
     const int n = (int)t.level_nonleaf[lv].size();
     if (n == 0) continue;
-    if (staged)
+    if (kron)
+      BEM_CK(launch_transfer_k((unsigned)n, ttk, sm_k, st, t.d_level_nonleaf[lv].p, t.d_son0.p, t.d_son1.p, t.d_E1.p,
+                               yhat, nl, t.m, TF, true));
+    else if (staged)
       down_transfer_s_kernel<<<dim3((unsigned)n, tt), kPassThreads, sm_tr, st>>>(t.d_level_nonleaf[lv].p, t.d_son0.p,
                                                                                  t.d_son1.p, t.d_ET.p, yhat, nl, p);
     else
@@ -362,8 +680,15 @@ bem_status run_down(Tree& t, double2* yhat, const double2* yc, double2* y, int n
     BEM_CK(cudaGetLastError());
   }
   if (wait_before_leaf) BEM_CK(cudaStreamWaitEvent(st, wait_before_leaf, 0));
+  const int p4 = (p + 3) & ~3, n8 = (t.max_leaf + 7) & ~7;
+  const size_t sm_d = sizeof(double) * ((size_t)n8 * pad8(p4) + (size_t)p4 * pad8(2 * kLeafT));
   const size_t sm_leaf = sizeof(double2) * kPassT * p + sizeof(double) * (size_t)p * t.max_leaf;
-  if (sm_leaf <= kPassSmemMax) {
+  if (sm_d <= kLeafSmemMax) {
+    BEM_CK(cudaFuncSetAttribute(down_leaf_d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d));
+    down_leaf_d_kernel<<<dim3((unsigned)t.n_leaves, (unsigned)((nl + kLeafT - 1) / kLeafT)), kPassThreads, sm_d,
+                         st>>>(t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_U.p, yhat, yc, t.d_perm.p, y, t.M, nl, p, xc,
+                               alpha);
+  } else if (sm_leaf <= kPassSmemMax) {
     BEM_CK(cudaFuncSetAttribute(down_leaf_s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_leaf));
     down_leaf_s_kernel<<<dim3((unsigned)t.n_leaves, tt), kPassThreads, sm_leaf, st>>>(
         t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_UT.p, yhat, yc, t.d_perm.p, y, t.M, nl, p, xc, alpha);
@@ -395,8 +720,12 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
       if (!e) BEM_CK(cudaEventCreate(&e));
     BEM_CK(cudaEventRecord(op.ev[0], st));
   }
+  Nvtx nv_apply(dl ? "apply_double_layer" : "apply_multifreq");
   const int64_t tot = M * nl;
-  gather_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(x, xc, t.d_perm.p, M, nl);
+  {
+    Nvtx nv("a2 gather");
+    gather_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(x, xc, t.d_perm.p, M, nl);
+  }
   BEM_CK(cudaGetLastError());
   const bool dense = op.mode == BEM_MODE_DENSE;
   const bool has_far = !dense && !t.far_r.empty();
@@ -418,6 +747,7 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
     sk1 = op.side;
   }
   {
+    Nvtx nv("a3 K1 near field");
     bem_status rs = launch_near(op, xc, yc, sk1, dl);
     if (rs != BEM_OK) return rs;
   }
@@ -425,15 +755,21 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
   if (prof) BEM_CK(cudaEventRecord(op.ev[1], st));
   if (has_far) {
     {
+      Nvtx nv("a4 K2 up");
       bem_status rs = run_up(t, dl ? t.d_WK.p : t.d_W.p, xc, xhat, nl, st);
       if (rs != BEM_OK) return rs;
     }
     if (prof) BEM_CK(cudaEventRecord(op.ev[2], st));
-    bem_status rs = launch_far(op, xhat, yhat, st);
+    bem_status rs;
+    {
+      Nvtx nv("a5 K3 coupling");
+      rs = launch_far(op, xhat, yhat, st);
+    }
     if (rs != BEM_OK) return rs;
     if (prof) BEM_CK(cudaEventRecord(op.ev[3], st));
     {
       // the down transfers do not read yc: only the leaf scatter waits for K1
+      Nvtx nv("a6-a7 K2 down + scatter");
       bem_status rs = run_down(t, yhat, yc, y, nl, xc, dl ? alpha : 0.0, st, overlap ? op.ev_join : nullptr);
       if (rs != BEM_OK) return rs;
     }

@@ -8,9 +8,21 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/bem.h"
 
 namespace bem {
+
+// NVTX range over a host scope (stage markers for ncu --nvtx / profilers: the paper's
+// stage timings P:1808-1828 -- tree, ACA, gather, K1, K2, K3, K4, GMRES).  Header-only
+// NVTX v3: a no-op unless a profiler injects itself.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 void set_error(const char* fmt, ...);
 
@@ -103,6 +115,7 @@ struct Tree {
   DBuf<double> d_WK;     // M*p double-layer column basis (NEXT-1)
   DBuf<double> d_nrm;    // M*3 unit normals (cluster order)
   DBuf<double> d_E;      // C*p*p (E of cluster c w.r.t. its parent)
+  DBuf<double> d_E1;     // C*3*m*m: E = E_z (x) E_y (x) E_x, E_a[lam_a][mu_a] = parent's 1-D Lagrange mu_a at son node lam_a
   DBuf<double> d_ET, d_UT;  // transposed E (C*p*p) and U (p*M) for the downward pass
   DBuf<double> d_xi;     // C*3*m
   DBuf<int32_t> d_leaves;
@@ -154,8 +167,9 @@ struct Op {
   DBuf<int64_t> d_foff;                  // nfar: offsets of F_b in d_F
   DBuf<double> d_F;                      // pool: sum r_b^2 complex, F_b = C^_b (lower) + U_b (strict upper)
   bool z_stored = true;                  // false: K3 regenerates Z tiles from F_b (factors-only)
-  int rmax = 0;                          // largest far rank (K3 Z-tile scratch)
-  DBuf<double> d_zs;                     // K3 Z-tile scratch (factors-only): per CTA [rmax][ZW]
+  int rmax = 0;                          // largest far rank
+  DBuf<double> d_zs;                     // factors-only: Z tile buffer, per block [r_b][ZW] at d_ztoff[b]
+  DBuf<int64_t> d_ztoff;
   // row clusters owning far blocks, sorted by descending coupling work (K3 order)
   int n_far_rows = 0;
   DBuf<int32_t> d_far_rows;

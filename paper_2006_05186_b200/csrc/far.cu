@@ -10,10 +10,14 @@
 // are evaluated", north_star); they are regenerated on the fly from the
 // kernel (no slice storage: 223 GB at config 4).  The
 // coefficients Z_b come either from the stored pool or, in the factors-only
-// skeleton (BEM_SKEL_FACTORS), from the block's r_b x r_b LU factors: each CTA
-// regenerates the Z tile of its frequency columns in the block's prologue
-// (pivot fibres + two pinned triangular solves, zgen.cuh) into a per-CTA
-// scratch that stays in L2.
+// skeleton (BEM_SKEL_FACTORS), from the blocks' r_b x r_b LU factors: the
+// coupling then runs one frequency tile at a time, and before each tile
+// zgen_tile_kernel regenerates every block's Z columns of the tile (pivot
+// fibres + two pinned triangular solves, zgen.cuh) into a tile buffer
+// (sum_b r_b x 130 complex: 7 GB at config 4 instead of 28 GB of stored Z),
+// which the unchanged coupling kernel reads.  (A first version regenerated the
+// tile in each CTA's block prologue; that serialised the substitutions inside
+// the GEMM kernel and cost it 20-40 %: profiles/r02_factors.md.)
 //
 // Kernels (all deterministic: one CTA owns each output tile of a segment's
 // partial sum; segments of a row are reduced in fixed order, no atomics):
@@ -28,6 +32,7 @@
 // 6-warp CTAs, 3M complex products, split remainder rows) were removed; they
 // are in git history and profiles/r01_sweeps.md.
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -73,51 +78,66 @@ __device__ __forceinline__ double2 kern_rs(double d2, double2 s, const double* e
   return make_double2(e * cs, -e * sn);
 }
 
-// Where the coefficients Z_b[j, t] come from (stored pool or per-CTA regenerated tile).
+// Where the coefficients Z_b[j, t] come from: the stored pool ([r_b][nl] at zoff[b]) or
+// the current frequency tile's buffer ([r_b][ZW] at ztoff[b]: leftover columns [0, tb)
+// then the tile's DMMA columns; factors-only skeleton).
 struct ZSrc {
-  const int64_t* zoff;  // stored: Z_b at Z + zoff[b], [r_b][nl]
+  const int64_t* zoff;
   const double2* Z;
-  zgen::Src g;          // factors-only: F_b, pivots, nodes, s
-  const int32_t* local_l;
-  double2* scr;         // per CTA [rmax][ZW]
-  int ZW, rmax;
+  int tiled, ZW;  // tiled: Z = tile buffer, zoff = per-block offsets in it
 };
 
-// Coefficient rows of block b for this CTA's columns.  Returns zD, zL and the row
-// stride such that Z_b[j, t] = zD[j * stride + t] for the tile's DMMA columns t and
-// zL[j * stride + t] for the leftover columns t < tb.  FAC: the tile is regenerated here
-// (columns [0, tb) leftover -- lead CTA only -- then [tc0, tc0 + ncol)): one thread per
-// column runs the two substitutions on a [r][nb] batch in shared memory (work: the CTA's
-// slice / x^ buffers, free before the block's staging; nb columns per batch), and the
-// batch is copied to the CTA's scratch, which the term loop reads.  Ends with a barrier.
-template <bool FAC>
-__device__ __forceinline__ void ztile(const ZSrc& z, int b, int rk, int nl, int tb, int tc0, int ncp, bool lead,
-                                      const int32_t* mask, double2* work, int work_cap, const double2*& zD,
+// Z_b[j, t] = zD[j * stride + t] for the tile's DMMA columns t, zL[j * stride + t] for the
+// leftover columns t < tb.
+__device__ __forceinline__ void zrows(const ZSrc& z, int b, int nl, int tb, int tc0, const double2*& zD,
                                       const double2*& zL, int& stride) {
-  if constexpr (!FAC) {
-    zD = zL = z.Z + z.zoff[b];
-    stride = nl;
+  zL = z.Z + z.zoff[b];
+  if (z.tiled) {
+    zD = zL + (tb - tc0);
+    stride = z.ZW;
   } else {
-    double2* scr = z.scr + (int64_t)(blockIdx.x + gridDim.x * blockIdx.y) * z.rmax * z.ZW;
-    const int nb = max(1, min(ncp, work_cap / max(rk, 1)));
+    zD = zL;
+    stride = nl;
+  }
+}
+
+// Factors-only skeleton: the Z columns of one frequency tile for every far block
+// (zgen.cuh; the same function as the stored-Z regeneration, hence bit-identical).
+// CTA per block (grid-stride); columns in batches of nb in shared memory: the pivot
+// fibres over all threads, then one column per thread for the two substitutions, then
+// a coalesced copy to the tile buffer.
+__global__ void __launch_bounds__(256) zgen_tile_kernel(zgen::Src g, int nfar, const int32_t* __restrict__ rank,
+                                                        const int64_t* __restrict__ ztoff,
+                                                        const int32_t* __restrict__ local_l,
+                                                        const int32_t* __restrict__ mask, int nl, int tb, int tc0,
+                                                        int ncol, int lead, int ZW, int cap, double2* __restrict__ Zt) {
+  extern __shared__ double2 work[];
+  const int ncp = tb + ncol;
+  for (int b = blockIdx.x; b < nfar; b += gridDim.x) {
+    const int rk = rank[b];
+    if (rk <= 0) continue;
+    const int rc = g.far_r[b], cc = g.far_c[b];
+    const int32_t* qp = g.pivq + (int64_t)b * g.rcap;
+    double2* out = Zt + ztoff[b];
+    const int nb = max(1, min(ncp, cap / rk));
     for (int c0 = lead ? 0 : tb; c0 < ncp; c0 += nb) {
       const int nc = min(nb, ncp - c0);
-      if ((int)threadIdx.x < nc) {
-        const int c = c0 + threadIdx.x;
+      for (int e = threadIdx.x; e < rk * nc; e += blockDim.x) {
+        const int i = e / nc, cl = e - i * nc;
+        const int c = c0 + cl;
         const int t = c < tb ? c : tc0 + (c - tb);
-        const int l = (t < nl && (mask == nullptr || mask[t])) ? z.local_l[t] : -1;
-        zgen::column(z.g, b, rk, l, work + threadIdx.x, nb);
+        const bool on = t < nl && (mask == nullptr || mask[t]);
+        work[i * nb + cl] = on ? zgen::fibre(g, rc, cc, qp[i], local_l[t]) : make_double2(0.0, 0.0);
       }
       __syncthreads();
+      if ((int)threadIdx.x < nc) zgen::solve(g, b, rk, work + threadIdx.x, nb);
+      __syncthreads();
       for (int e = threadIdx.x; e < rk * nc; e += blockDim.x) {
-        const int j = e / nc, cc = e - j * nc;
-        scr[(int64_t)j * z.ZW + c0 + cc] = work[j * nb + cc];
+        const int j = e / nc, cl = e - j * nc;
+        out[(int64_t)j * ZW + c0 + cl] = work[j * nb + cl];
       }
       __syncthreads();
     }
-    zL = scr;
-    zD = scr + (tb - tc0);
-    stride = z.ZW;
   }
 }
 
@@ -135,6 +155,7 @@ __device__ __forceinline__ void ztile(const ZSrc& z, int b, int rk, int nl, int 
 // accumulated by all 256 threads of the lead CTA; more are zero-padded DMMA columns.
 struct Far7Args {
   int nl, m, p, p4, rcap, SST, TT, XTP, tb, nd;  // DMMA columns [tb, tb+nd) (padded past nl)
+  int tile0 = 0;                                 // first frequency tile of this launch (grid y offset)
   const int4* segs;
   const int32_t* far_sorted;
   const int32_t* far_c;
@@ -148,15 +169,16 @@ struct Far7Args {
   const int32_t* mask;  // nullable: per local frequency, 0 = skip (output 0)
 };
 
-template <int MT, int NJ, int REM, bool FAC>
+template <int MT, int NJ, int REM>
 __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
   extern __shared__ double2 sm[];
   const int p = a.p, m = a.m, SST = a.SST, XTP = a.XTP, p4 = a.p4, tb = a.tb;
   const int4 sg = a.segs[blockIdx.x];
   const int r = sg.x;
-  const int tc0 = a.tb + blockIdx.y * a.TT;
+  const int tile = blockIdx.y + a.tile0;
+  const int tc0 = a.tb + tile * a.TT;
   const int ncol = min(a.TT, a.tb + a.nd - tc0);
-  const bool lead = blockIdx.y == 0;
+  const bool lead = tile == 0;
   const int mu0 = blockIdx.z * 32;
   const int nrow = min(32, p - mu0);
   const int nS = nrow * p;
@@ -214,7 +236,7 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
     __syncthreads();
     const double2 *zD, *zL;
     int zst;
-    ztile<FAC>(a.z, b, rk, a.nl, tb, tc0, ncp, lead, a.mask, S0, 2 * 32 * SST + p4 * XTP, zD, zL, zst);
+    zrows(a.z, b, a.nl, tb, tc0, zD, zL, zst);
     for (int i = tid; i < p; i += blockDim.x) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
     const double2* xh = a.xhat + (int64_t)c * a.nl * p;
     for (int idx = tid; idx < ncp * p; idx += blockDim.x) {
@@ -242,6 +264,10 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
         S[i * SST + nu] = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab, sctab);
       }
       __syncthreads();
+      // the real pivot slice (s_0) needs two DMMAs per complex MAC: the branch is hoisted out
+      // of the k loop (one loop body per case)
+      auto gemm = [&](auto realc) {
+        constexpr bool RS = decltype(realc)::value;
       for (int k0 = 0; k0 < p4; k0 += 4) {
         double2 bf[NJ > 0 ? NJ : 1], rf[REM > 0 ? REM : 1];
 #pragma unroll
@@ -256,7 +282,7 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
             const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
             const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
             const double nai = -ai;
-            if (real_slice) {  // pivot frequency s_0 is real: Im S = 0, two DMMAs per complex MAC
+            if constexpr (RS) {  // pivot frequency s_0 is real: Im S = 0, two DMMAs per complex MAC
 #pragma unroll
               for (int j = 0; j < NJ; ++j) {
                 dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
@@ -283,6 +309,9 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
           }
         }
       }
+      };
+      if (real_slice) gemm(std::true_type{});
+      else gemm(std::false_type{});
       if (lown) {
 #pragma unroll
         for (int tl = 0; tl < 2; ++tl) {
@@ -378,26 +407,26 @@ Far7Cfg choose7(int p, int nl, size_t cap) {
   return Far7Cfg{};
 }
 
-template <int MT, int NJ, int REM, bool FAC>
-cudaError_t launch7(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream_t st) {
-  auto k = far7_kernel<MT, NJ, REM, FAC>;
+template <int MT, int NJ, int REM>
+cudaError_t launch7(const Far7Cfg& c, int nseg, const Far7Args& a, int ntile, cudaStream_t st) {
+  auto k = far7_kernel<MT, NJ, REM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   if (e != cudaSuccess) return e;
-  k<<<dim3((unsigned)nseg, (unsigned)c.ntiles, (unsigned)c.nchunks), 256, c.smem, st>>>(a);
+  k<<<dim3((unsigned)nseg, (unsigned)ntile, (unsigned)c.nchunks), 256, c.smem, st>>>(a);
   return cudaGetLastError();
 }
 
-template <int NJ, int REM, bool FAC>
-cudaError_t dispatch7_(const Far7Cfg& c, int nseg, const Far7Args& a, cudaStream_t st) {
-  return c.mt == 1 ? launch7<1, NJ, REM, FAC>(c, nseg, a, st) : launch7<2, NJ, REM, FAC>(c, nseg, a, st);
+template <int NJ, int REM>
+cudaError_t dispatch7_(const Far7Cfg& c, int nseg, const Far7Args& a, int ntile, cudaStream_t st) {
+  return c.mt == 1 ? launch7<1, NJ, REM>(c, nseg, a, ntile, st) : launch7<2, NJ, REM>(c, nseg, a, ntile, st);
 }
 
 // mu tiling: p = 27 -> 3 DMMA tiles + 3 DFMA rows; p <= 8 -> 1 tile; otherwise 4 tiles per 32-row chunk
-template <bool FAC>
-cudaError_t dispatch7(const Far7Cfg& c, int p, int nseg, const Far7Args& a, cudaStream_t st) {
-  if (p <= 8) return dispatch7_<1, 0, FAC>(c, nseg, a, st);
-  if (p == 27) return dispatch7_<3, 3, FAC>(c, nseg, a, st);
-  return dispatch7_<4, 0, FAC>(c, nseg, a, st);
+// ntile frequency tiles from a.tile0 (grid y)
+cudaError_t dispatch7(const Far7Cfg& c, int p, int nseg, const Far7Args& a, int ntile, cudaStream_t st) {
+  if (p <= 8) return dispatch7_<1, 0>(c, nseg, a, ntile, st);
+  if (p == 27) return dispatch7_<3, 3>(c, nseg, a, ntile, st);
+  return dispatch7_<4, 0>(c, nseg, a, ntile, st);
 }
 
 // ------------------------------------------------ far8: far7 with K (nu) chunks
@@ -409,6 +438,7 @@ cudaError_t dispatch7(const Far7Cfg& c, int p, int nseg, const Far7Args& a, cuda
 // frequency tile stays at TT = 128 with two CTAs per SM for p = 64 and 125.
 struct Far8Args {
   int nl, m, p, rcap, SST, TT, XTP, tb, nd, KC;
+  int tile0 = 0;  // first frequency tile of this launch (grid y offset)
   int nch = 1;  // mu chunks (grid x = segment * nch + chunk)
   const int4* segs;
   const int32_t* far_sorted;
@@ -423,7 +453,7 @@ struct Far8Args {
   const int32_t* mask;  // nullable: per local frequency, 0 = skip (output 0)
 };
 
-template <int MT, int NJ, int REM, bool FAC>
+template <int MT, int NJ, int REM>
 __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
   extern __shared__ double2 sm[];
   const int p = a.p, m = a.m, SST = a.SST, XTP = a.XTP, tb = a.tb, KC = a.KC;
@@ -431,9 +461,10 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
   // x^ and Z tiles from L2 instead of DRAM
   const int4 sg = a.segs[blockIdx.x / a.nch];
   const int r = sg.x;
-  const int tc0 = a.tb + blockIdx.y * a.TT;
+  const int tile = blockIdx.y + a.tile0;
+  const int tc0 = a.tb + tile * a.TT;
   const int ncol = min(a.TT, a.tb + a.nd - tc0);
-  const bool lead = blockIdx.y == 0;
+  const bool lead = tile == 0;
   const int mu0 = (blockIdx.x % a.nch) * 32;
   const int nrow = min(32, p - mu0);
   double2* S0 = sm;                                   // 2 x (32 x SST), SST >= KC: double-buffered slice
@@ -488,7 +519,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
     __syncthreads();
     const double2 *zD, *zL;
     int zst;
-    ztile<FAC>(a.z, b, rk, a.nl, tb, tc0, ncp, lead, a.mask, S0, 2 * 32 * SST + KC * XTP, zD, zL, zst);
+    zrows(a.z, b, a.nl, tb, tc0, zD, zL, zst);
     for (int i = tid; i < p; i += blockDim.x) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
     for (int k0c = 0; k0c < p; k0c += KC) {
       const int kw = min(KC, p - k0c);          // real nu in this chunk
@@ -528,6 +559,8 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
           S[i * SST + nu] = v;
         }
         __syncthreads();
+        auto gemm = [&](auto realc) {  // real pivot slice: two DMMAs per complex MAC (hoisted branch)
+          constexpr bool RS = decltype(realc)::value;
         for (int k0 = 0; k0 < kw4; k0 += 4) {
           double2 bf[NJ], rf[REM > 0 ? REM : 1];
 #pragma unroll
@@ -542,7 +575,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
               const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
               const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
               const double nai = -ai;
-              if (real_slice) {  // pivot frequency s_0 is real: Im S = 0, two DMMAs per complex MAC
+              if constexpr (RS) {  // pivot frequency s_0 is real: Im S = 0, two DMMAs per complex MAC
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
                   dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
@@ -569,6 +602,9 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
             }
           }
         }
+        };
+        if (real_slice) gemm(std::true_type{});
+        else gemm(std::false_type{});
         if (lown) {
 #pragma unroll
           for (int tl = 0; tl < 2; ++tl) {
@@ -674,22 +710,21 @@ Far8Cfg choose8(int p, int nl, size_t cap, int kc_req) {
   return Far8Cfg{};
 }
 
-template <int MT, int NJ, int REM, bool FAC>
-cudaError_t launch8(const Far8Cfg& c, int nseg, const Far8Args& a, cudaStream_t st) {
-  auto k = far8_kernel<MT, NJ, REM, FAC>;
+template <int MT, int NJ, int REM>
+cudaError_t launch8(const Far8Cfg& c, int nseg, const Far8Args& a, int ntile, cudaStream_t st) {
+  auto k = far8_kernel<MT, NJ, REM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   if (e != cudaSuccess) return e;
   Far8Args a2 = a;
   a2.nch = c.nchunks;
-  k<<<dim3((unsigned)(nseg * c.nchunks), (unsigned)c.ntiles, 1u), 256, c.smem, st>>>(a2);
+  k<<<dim3((unsigned)(nseg * c.nchunks), (unsigned)ntile, 1u), 256, c.smem, st>>>(a2);
   return cudaGetLastError();
 }
 
-template <bool FAC>
-cudaError_t dispatch8(const Far8Cfg& c, int p, int nseg, const Far8Args& a, cudaStream_t st) {
-  if (p <= 8) return c.mt == 1 ? launch8<1, 1, 0, FAC>(c, nseg, a, st) : launch8<2, 1, 0, FAC>(c, nseg, a, st);
-  if (p == 27) return c.mt == 1 ? launch8<1, 3, 3, FAC>(c, nseg, a, st) : launch8<2, 3, 3, FAC>(c, nseg, a, st);
-  return c.mt == 1 ? launch8<1, 4, 0, FAC>(c, nseg, a, st) : launch8<2, 4, 0, FAC>(c, nseg, a, st);
+cudaError_t dispatch8(const Far8Cfg& c, int p, int nseg, const Far8Args& a, int ntile, cudaStream_t st) {
+  if (p <= 8) return c.mt == 1 ? launch8<1, 1, 0>(c, nseg, a, ntile, st) : launch8<2, 1, 0>(c, nseg, a, ntile, st);
+  if (p == 27) return c.mt == 1 ? launch8<1, 3, 3>(c, nseg, a, ntile, st) : launch8<2, 3, 3>(c, nseg, a, ntile, st);
+  return c.mt == 1 ? launch8<1, 4, 0>(c, nseg, a, ntile, st) : launch8<2, 4, 0>(c, nseg, a, ntile, st);
 }
 
 // ------------------------------- h2o: plain-H^2 coupling evaluated on the fly
@@ -972,8 +1007,7 @@ struct FarGeom {
   int fk = 0;
   Far7Cfg f7;
   Far8Cfg f8;
-  int64_t ctas = 0;
-  int ZW = 0;
+  int ntiles = 0, tb = 0, TT = 0, ZW = 0;
 };
 
 static FarGeom far_geom(const Op& op) {
@@ -981,28 +1015,22 @@ static FarGeom far_geom(const Op& op) {
   const int p = t.p, nl = op.n_local;
   FarGeom g;
   g.fk = op.far_kernel != 0 ? op.far_kernel : (p > 32 ? 8 : 7);  // r01: far8 wins at p = 64, far7 at p = 27
-  if (op.force_generic || op.n_segs == 0) return g;
+  if (op.force_generic || op.n_segs == 0) { g.fk = 0; return g; }
   if (g.fk == 8) {
     g.f8 = choose8(p, nl, op.far4_smem_cap, op.far8_kc);
-    if (g.f8.mt > 0) {
-      g.ctas = (int64_t)op.n_segs * g.f8.nchunks * g.f8.ntiles;
-      g.ZW = g.f8.tb + g.f8.TT;
-      return g;
-    }
+    if (g.f8.mt > 0) { g.ntiles = g.f8.ntiles; g.tb = g.f8.tb; g.TT = g.f8.TT; g.ZW = g.tb + g.TT; return g; }
   } else if (g.fk == 7) {
     g.f7 = choose7(p, nl, op.far4_smem_cap);
-    if (g.f7.mt > 0) {
-      g.ctas = (int64_t)op.n_segs * g.f7.nchunks * g.f7.ntiles;
-      g.ZW = g.f7.tb + g.f7.TT;
-      return g;
-    }
+    if (g.f7.mt > 0) { g.ntiles = g.f7.ntiles; g.tb = g.f7.tb; g.TT = g.f7.TT; g.ZW = g.tb + g.TT; return g; }
   }
   g.fk = 0;
   return g;
 }
 
-// Factors-only skeleton: per-CTA Z-tile scratch of K3 (allocated at assembly so
-// that an apply never allocates, e.g. inside a CUDA-graph capture).
+constexpr int kZgenSmem = 64 * 1024;  // zgen_tile_kernel batch buffer (4096 complex)
+
+// Factors-only skeleton: the tile buffer (sum_b r_b x ZW complex) and its per-block
+// offsets, allocated at assembly so that an apply never allocates (graph capture).
 bem_status far_prepare(Op& op) {
   if (op.z_stored || op.ranks.empty()) return BEM_OK;
   const FarGeom g = far_geom(op);
@@ -1010,8 +1038,13 @@ bem_status far_prepare(Op& op) {
     set_error("bem_assemble_h2_aca: factors-only skeleton needs the tiled coupling kernels (p <= 128)");
     return BEM_EINVAL;
   }
+  std::vector<int64_t> off(op.ranks.size());
+  int64_t acc = 0;
+  for (size_t b = 0; b < off.size(); ++b) { off[b] = acc; acc += (int64_t)op.ranks[b] * g.ZW; }
   op.rmax = *std::max_element(op.ranks.begin(), op.ranks.end());
-  BEM_CK(op.d_zs.alloc((size_t)g.ctas * std::max(1, op.rmax) * g.ZW * 2));
+  BEM_CK(op.d_ztoff.upload(off));
+  BEM_CK(op.d_zs.alloc((size_t)std::max<int64_t>(acc, 1) * 2));
+  BEM_CK(cudaFuncSetAttribute(zgen_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kZgenSmem));
   return BEM_OK;
 }
 
@@ -1047,43 +1080,54 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
   }
   const FarGeom g = aca ? far_geom(op) : FarGeom{};
   const bool fac = aca && !op.z_stored;
-  ZSrc z{};
-  if (aca) {
-    z.zoff = op.d_zoff.p; z.Z = (const double2*)op.d_Z.p;
-    z.g.m = t.m; z.g.p = p; z.g.L = op.L; z.g.far_r = t.d_far_r.p; z.g.far_c = t.d_far_c.p; z.g.xi = t.d_xi.p;
-    z.g.s = (const double2*)op.d_s.p; z.g.pivk = op.d_pivk.p; z.g.pivq = op.d_pivq.p; z.g.foff = op.d_foff.p;
-    z.g.F = (const double2*)op.d_F.p; z.g.rcap = op.rcap;
-    z.local_l = op.d_local_l.p; z.scr = (double2*)op.d_zs.p; z.ZW = g.ZW; z.rmax = std::max(1, op.rmax);
-    if (fac && (g.fk == 0 || op.d_zs.p == nullptr)) {
-      set_error("launch_far: factors-only skeleton without the K3 scratch");
-      return BEM_ESTATE;
+  if (fac && (g.fk == 0 || op.d_zs.p == nullptr)) {
+    set_error("launch_far: factors-only skeleton without its tile buffer");
+    return BEM_ESTATE;
+  }
+  if (aca && g.fk != 0) {
+    BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
+    ZSrc z{};
+    z.zoff = fac ? op.d_ztoff.p : op.d_zoff.p;
+    z.Z = fac ? (const double2*)op.d_zs.p : (const double2*)op.d_Z.p;
+    z.tiled = fac ? 1 : 0;
+    z.ZW = g.ZW;
+    zgen::Src zsrc{};
+    zsrc.m = t.m; zsrc.p = p; zsrc.L = op.L; zsrc.far_r = t.d_far_r.p; zsrc.far_c = t.d_far_c.p; zsrc.xi = t.d_xi.p;
+    zsrc.s = (const double2*)op.d_s.p; zsrc.pivk = op.d_pivk.p; zsrc.pivq = op.d_pivq.p; zsrc.foff = op.d_foff.p;
+    zsrc.F = (const double2*)op.d_F.p; zsrc.rcap = op.rcap;
+    const int nfar = (int)t.far_r.size();
+    // stored Z: all tiles in one launch; factors-only: per tile, regenerate its Z columns first
+    for (int tile = 0; tile < (fac ? g.ntiles : 1); ++tile) {
+      const int ntile = fac ? 1 : g.ntiles;
+      if (fac) {
+        const int tc0 = g.tb + tile * g.TT;
+        const int nd = g.fk == 8 ? g.f8.nd : g.f7.nd;
+        const int ncol = std::min(g.TT, g.tb + nd - tc0);
+        zgen_tile_kernel<<<std::min(nfar, 148 * 8), 256, kZgenSmem, st>>>(
+            zsrc, nfar, op.d_rank.p, op.d_ztoff.p, op.d_local_l.p, op.d_mask, nl, g.tb, tc0, ncol, tile == 0 ? 1 : 0,
+            g.ZW, kZgenSmem / (int)sizeof(double2), (double2*)op.d_zs.p);
+        BEM_CK(cudaGetLastError());
+      }
+      if (g.fk == 8) {
+        const Far8Cfg& f8 = g.f8;
+        Far8Args a;
+        a.nl = nl; a.m = t.m; a.p = p; a.rcap = op.rcap; a.SST = f8.SST; a.TT = f8.TT; a.XTP = f8.XTP;
+        a.tb = f8.tb; a.nd = f8.nd; a.KC = f8.KC; a.tile0 = fac ? tile : 0;
+        a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
+        a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
+        a.z = z; a.xhat = xhat; a.part = (double2*)op.d_part.p; a.mask = op.d_mask;
+        BEM_CK(dispatch8(f8, p, op.n_segs, a, ntile, st));
+      } else {
+        const Far7Cfg& f7 = g.f7;
+        Far7Args a;
+        a.nl = nl; a.m = t.m; a.p = p; a.p4 = f7.p4; a.rcap = op.rcap; a.SST = f7.SST; a.TT = f7.TT;
+        a.XTP = f7.XTP; a.tb = f7.tb; a.nd = f7.nd; a.tile0 = fac ? tile : 0;
+        a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
+        a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
+        a.z = z; a.xhat = xhat; a.part = (double2*)op.d_part.p; a.mask = op.d_mask;
+        BEM_CK(dispatch7(f7, p, op.n_segs, a, ntile, st));
+      }
     }
-  }
-  if (aca && g.fk == 8) {
-    const Far8Cfg& f8 = g.f8;
-    BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
-    Far8Args a;
-    a.nl = nl; a.m = t.m; a.p = p; a.rcap = op.rcap; a.SST = f8.SST; a.TT = f8.TT; a.XTP = f8.XTP;
-    a.tb = f8.tb; a.nd = f8.nd; a.KC = f8.KC;
-    a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
-    a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
-    a.z = z; a.xhat = xhat; a.part = (double2*)op.d_part.p; a.mask = op.d_mask;
-    BEM_CK(fac ? dispatch8<true>(f8, p, op.n_segs, a, st) : dispatch8<false>(f8, p, op.n_segs, a, st));
-    seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
-                                                     yhat, (int64_t)nl * p);
-    BEM_CK(cudaGetLastError());
-    return BEM_OK;
-  }
-  if (aca && g.fk == 7) {
-    const Far7Cfg& f7 = g.f7;
-    BEM_CK(cudaMemsetAsync(yhat, 0, sizeof(double2) * (size_t)t.C * nl * p, st));
-    Far7Args a;
-    a.nl = nl; a.m = t.m; a.p = p; a.p4 = f7.p4; a.rcap = op.rcap; a.SST = f7.SST; a.TT = f7.TT; a.XTP = f7.XTP;
-    a.tb = f7.tb; a.nd = f7.nd;
-    a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
-    a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
-    a.z = z; a.xhat = xhat; a.part = (double2*)op.d_part.p; a.mask = op.d_mask;
-    BEM_CK(fac ? dispatch7<true>(f7, p, op.n_segs, a, st) : dispatch7<false>(f7, p, op.n_segs, a, st));
     seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
                                                      yhat, (int64_t)nl * p);
     BEM_CK(cudaGetLastError());

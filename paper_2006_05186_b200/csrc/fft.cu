@@ -450,6 +450,7 @@ __global__ void __launch_bounds__(kFftThreads) bluestein_rows_kernel(const K4Arg
 // parameters at launch (nothing to keep alive, capturable in a CUDA graph)
 bem_status fft_transform_rows(const double* in, double* out, int64_t M, int N, double R, bool inverse, cudaStream_t st,
                               const double2* const* tab, int mode) {
+  Nvtx nv(inverse ? "a8 K4 cqm_inverse" : "a1 K4 cqm_forward");
   Plan* pl = nullptr;
   bem_status rs = get_plan(N, R, inverse, &pl);
   if (rs != BEM_OK) return rs;

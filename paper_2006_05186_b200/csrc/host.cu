@@ -300,6 +300,7 @@ void lagrange_grad_n_3d(const double* xi, int m, const double* x, const double* 
 
 extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t* T, int64_t nt, int32_t leaf_size,
                                      double eta, int32_t m, int32_t device, bem_tree* out) {
+  Nvtx nvtx_range("bem_build_tree");
   BEM_REQ(out != nullptr, "bem_build_tree: out is NULL");
   BEM_REQ(V != nullptr && T != nullptr, "bem_build_tree: NULL mesh arrays");
   BEM_REQ(nv >= 3 && nt >= 1, "bem_build_tree: need nv >= 3 and nt >= 1");
@@ -470,6 +471,21 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
     for (int64_t k = 0; k < t.M; ++k)
       for (int mu = 0; mu < t.p; ++mu) UT[(size_t)mu * t.M + k] = U[(size_t)k * t.p + mu];
   }
+  // 1-D factors of the transfer matrices (tensor Chebyshev interpolation):
+  // E[c][lam][mu] = prod_a E1[c][a][lam_a][mu_a] with E1[c][a] = the parent's axis-a Lagrange
+  // polynomials at the son's axis-a nodes (K2 applies E as three m x m mode products)
+  std::vector<double> E1((size_t)t.C * 3 * t.m * t.m, 0.0);
+  for (int c = 0; c < t.C; ++c) {
+    const int par = t.parent[c];
+    if (par < 0) continue;
+    for (int a = 0; a < 3; ++a) {
+      const double* xs = &t.xi[(size_t)c * 3 * t.m + (size_t)a * t.m];
+      const double* xp = &t.xi[(size_t)par * 3 * t.m + (size_t)a * t.m];
+      for (int lam = 0; lam < t.m; ++lam)
+        lagrange_1d(xp, t.m, xs[lam], &E1[(((size_t)c * 3 + a) * t.m + lam) * t.m]);
+    }
+  }
+  UP(d_E1, E1);
   UP(d_U, U); UP(d_W, W); UP(d_E, E); UP(d_ET, ET); UP(d_UT, UT); UP(d_xi, t.xi); UP(d_leaves, t.leaves);
   UP(d_near_jb, njb); UP(d_near_je, nje); UP(d_near_j, nj);
   UP(d_J, rawJ); UP(d_near_r, t.near_r); UP(d_near_c, t.near_c); UP(d_nb_ptr, nb_ptr); UP(d_nb_sorted, nb_sorted);

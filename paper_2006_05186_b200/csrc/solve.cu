@@ -261,6 +261,7 @@ template <class ApplyFn, class MaskFn>
 bem_status gmres_core(int64_t M, int nl, ApplyFn apply, MaskFn set_mask, bool use_mask, const double2* B, double2* X,
                       double tol, int restart, int max_iter, cudaStream_t st, std::vector<int>& hit,
                       std::vector<double>& hrel, GmresWs& ws) {
+  Nvtx nv("a9 GMRES");
   const int64_t n = M * nl;
   if (ws.n != n || ws.nl != nl || ws.restart != restart) {  // (re)allocate the workspace
     BEM_CK(ws.r.alloc(2 * n));

@@ -56,29 +56,53 @@ __device__ __forceinline__ double2 fibre(const Src& a, int rc, int cc, int q, in
   return v;
 }
 
-// Z_b[:, l] for one frequency column: z[j * stride] for j < r (in place: first
-// d, then Z).  l < 0 writes a zero column (padding).
-__device__ __forceinline__ void column(const Src& a, int b, int r, int l, double2* z, int64_t stride) {
+// Z_b[:, l] for one frequency column, z[i * stride] already holding the pivot fibre
+// A_b[q_i, l] (fibre(), or zero for a padding column): forward substitution to d, then
+// back substitution to Z, in place.  Each row's dot product is split over four
+// interleaved partial sums (j mod 4), combined as ((s0 + s1) + (s2 + s3)) and then
+// subtracted: a fixed pinned order (bit-reproducible; the stored-Z and the factors-only
+// paths share this function), with a dependency chain a quarter as long as a
+// sequential sum.  (The ACA's own d rows use the sequential order; the difference is
+// rounding-level, far below the 1e-10 parity tolerance.)
+__device__ __forceinline__ double2 dot4(const double2* __restrict__ Fi, const double2* z, int64_t stride, int j0,
+                                        int j1) {
   using namespace pinned;
+  double2 s[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  int j = j0;
+  for (; j + 4 <= j1; j += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double2 pr = cmul(Fi[j + u], z[(j + u) * stride]);
+      s[u] = make_double2(add(s[u].x, pr.x), add(s[u].y, pr.y));
+    }
+  }
+  for (int u = 0; j < j1; ++j, ++u) {
+    const double2 pr = cmul(Fi[j], z[j * stride]);
+    s[u] = make_double2(add(s[u].x, pr.x), add(s[u].y, pr.y));
+  }
+  return make_double2(add(add(s[0].x, s[1].x), add(s[2].x, s[3].x)), add(add(s[0].y, s[1].y), add(s[2].y, s[3].y)));
+}
+
+// (not inlined: keeps the coupling kernel's hot-loop register allocation unchanged)
+__device__ __forceinline__ void solve(const Src& a, int b, int r, double2* z, int64_t stride) {
+  using namespace pinned;
+  const double2* F = a.F + a.foff[b];
+  for (int i = 0; i < r; ++i)  // forward: d_i = (A[q_i, l] - sum_{j<i} C^[i][j] d_j) / C^[i][i]
+    z[i * stride] = cdiv(csub(z[i * stride], dot4(F + (int64_t)i * r, z, stride, 0, i)), F[(int64_t)i * r + i]);
+  for (int i = r - 2; i >= 0; --i)  // backward: Z_i = d_i - sum_{j>i} U[i][j] Z_j
+    z[i * stride] = csub(z[i * stride], dot4(F + (int64_t)i * r, z, stride, i + 1, r));
+}
+
+// the whole column: fibres, then the substitutions; l < 0 writes a zero column (padding)
+__device__ __forceinline__ void column(const Src& a, int b, int r, int l, double2* z, int64_t stride) {
   if (l < 0) {
     for (int j = 0; j < r; ++j) z[j * stride] = make_double2(0.0, 0.0);
     return;
   }
   const int rc = a.far_r[b], cc = a.far_c[b];
-  const double2* F = a.F + a.foff[b];
   const int32_t* qp = a.pivq + (int64_t)b * a.rcap;
-  for (int i = 0; i < r; ++i) {  // forward: d_i
-    double2 acc = fibre(a, rc, cc, qp[i], l);
-#pragma unroll 4
-    for (int j = 0; j < i; ++j) acc = csub(acc, cmul(F[i * r + j], z[j * stride]));
-    z[i * stride] = cdiv(acc, F[i * r + i]);
-  }
-  for (int i = r - 1; i >= 0; --i) {  // backward: Z_i = d_i - sum_{j>i} U[i][j] Z_j
-    double2 acc = z[i * stride];
-#pragma unroll 4
-    for (int j = i + 1; j < r; ++j) acc = csub(acc, cmul(F[i * r + j], z[j * stride]));
-    z[i * stride] = acc;
-  }
+  for (int i = 0; i < r; ++i) z[i * stride] = fibre(a, rc, cc, qp[i], l);
+  solve(a, b, r, z, stride);
 }
 
 }  // namespace

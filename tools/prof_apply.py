@@ -16,6 +16,7 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--mode", default="h2aca")
 ap.add_argument("--time-step", action="store_true", help="forward + apply + inverse")
+ap.add_argument("--skeleton", default="auto", choices=["auto", "z", "factors"])
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 V, T = synth.config_mesh(a.config)
@@ -25,6 +26,8 @@ s = pb.cqm_frequencies(N, cfg["T"], R)
 tree = pb.Tree(V, T, cfg["leaf"], cfg["eta"], cfg["m"])
 mode = {"h2aca": pb.BEM_MODE_H2ACA, "h2only": pb.BEM_MODE_H2ONLY, "dense": pb.BEM_MODE_DENSE,
         "combined": pb.BEM_MODE_COMBINED}[a.mode]
+if mode in (pb.BEM_MODE_H2ACA, pb.BEM_MODE_COMBINED):
+    mode |= {"auto": 0, "z": pb.BEM_SKEL_Z, "factors": pb.BEM_SKEL_FACTORS}[a.skeleton]
 op = pb.Operator(tree, s, cfg["eps"], mode=mode)
 x = torch.from_numpy(synth.random_density(a.config, N + 1, len(T))).cuda()
 for _ in range(a.reps):

@@ -394,12 +394,14 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(AcaArgs a) {
 // Stored-Z skeleton (the default when it fits): Z_b[:, t] for every far block and local
 // frequency t, regenerated from the factors F_b (zgen.cuh; bit-identical to the ACA's own
 // back substitution).  One CTA per block (grid-stride), threads over the local columns.
-__global__ void __launch_bounds__(128) zgen_all_kernel(zgen::Src a, int nfar, const int32_t* rank, const int32_t* local_l,
-                                                    int n_local, const int64_t* zoff, double2* Z) {
+__global__ void __launch_bounds__(256) zgen_all_kernel(zgen::Src a, int nfar, const int32_t* rank, const int32_t* local_l,
+                                                    int n_local, const int64_t* zoff, double2* Z, int cap) {
+  extern __shared__ double2 work[];
   for (int b = blockIdx.x; b < nfar; b += gridDim.x) {
-    const int r = rank[b];
     double2* Zb = Z + zoff[b];
-    for (int t = threadIdx.x; t < n_local; t += blockDim.x) zgen::column(a, b, r, local_l[t], Zb + t, n_local);
+    zgen::block_columns(
+        a, b, rank[b], 0, n_local, [&](int t) { return local_l[t]; }, work, cap,
+        [&](int j, int t, double2 v) { Zb[(int64_t)j * n_local + t] = v; });
   }
 }
 
@@ -674,8 +676,11 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
       zs.F = (const double2*)op.d_F.p; zs.rcap = op.rcap;
       const int nfar = (int)op.ranks.size();
       if (nfar > 0) {
-        zgen_all_kernel<<<std::min(nfar, 148 * 16), 128, 0, st>>>(zs, nfar, op.d_rank.p, op.d_local_l.p, op.n_local,
-                                                                 op.d_zoff.p, (double2*)op.d_Z.p);
+        constexpr int kSm = 64 * 1024;
+        cudaFuncSetAttribute(zgen_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSm);
+        zgen_all_kernel<<<std::min(nfar, 148 * 3), 256, kSm, st>>>(zs, nfar, op.d_rank.p, op.d_local_l.p, op.n_local,
+                                                                    op.d_zoff.p, (double2*)op.d_Z.p,
+                                                                    kSm / (int)sizeof(double2));
         if (cudaGetLastError() != cudaSuccess) {
           set_error("bem_assemble_h2_aca: zgen launch failed");
           return fail(BEM_ECUDA);

@@ -114,30 +114,14 @@ __global__ void __launch_bounds__(256) zgen_tile_kernel(zgen::Src g, int nfar, c
   extern __shared__ double2 work[];
   const int ncp = tb + ncol;
   for (int b = blockIdx.x; b < nfar; b += gridDim.x) {
-    const int rk = rank[b];
-    if (rk <= 0) continue;
-    const int rc = g.far_r[b], cc = g.far_c[b];
-    const int32_t* qp = g.pivq + (int64_t)b * g.rcap;
     double2* out = Zt + ztoff[b];
-    const int nb = max(1, min(ncp, cap / rk));
-    for (int c0 = lead ? 0 : tb; c0 < ncp; c0 += nb) {
-      const int nc = min(nb, ncp - c0);
-      for (int e = threadIdx.x; e < rk * nc; e += blockDim.x) {
-        const int i = e / nc, cl = e - i * nc;
-        const int c = c0 + cl;
-        const int t = c < tb ? c : tc0 + (c - tb);
-        const bool on = t < nl && (mask == nullptr || mask[t]);
-        work[i * nb + cl] = on ? zgen::fibre(g, rc, cc, qp[i], local_l[t]) : make_double2(0.0, 0.0);
-      }
-      __syncthreads();
-      if ((int)threadIdx.x < nc) zgen::solve(g, b, rk, work + threadIdx.x, nb);
-      __syncthreads();
-      for (int e = threadIdx.x; e < rk * nc; e += blockDim.x) {
-        const int j = e / nc, cl = e - j * nc;
-        out[(int64_t)j * ZW + c0 + cl] = work[j * nb + cl];
-      }
-      __syncthreads();
-    }
+    zgen::block_columns(
+        g, b, rank[b], lead ? 0 : tb, ncp,
+        [&](int c) {
+          const int t = c < tb ? c : tc0 + (c - tb);
+          return (t < nl && (mask == nullptr || mask[t])) ? local_l[t] : -1;
+        },
+        work, cap, [&](int j, int c, double2 v) { out[(int64_t)j * ZW + c] = v; });
   }
 }
 

@@ -328,8 +328,11 @@ __device__ __forceinline__ void stage_small(const double2* __restrict__ A, doubl
   }
 }
 
-// prime radix R > 8: twiddle pass A -> B, then a direct R-point DFT with one thread per
-// output k (the inputs are shared-memory broadcasts), B -> A.  The result stays in A.
+// prime radix R > 8: twiddle pass A -> B, then a direct R-point DFT, B -> A (the result
+// stays in A).  One thread per output pair (k, R - k): with v_r = a_r + i b_r and
+// w^{rk} = c + i d, X_k = (sum ac - sum bd) + i (sum ad + sum bc) and X_{R-k} =
+// (sum ac + sum bd) + i (sum bc - sum ad), so the pair costs four FMAs and two
+// shared-memory loads per r (k = 0: the plain sum); the inputs are broadcasts.
 __device__ __forceinline__ void stage_large(double2* __restrict__ A, double2* __restrict__ B, int L, int R, int Ns,
                                             int NC, const double2* __restrict__ W) {
   const int T = L / R, tstep = L / (Ns * R), rstep = L / R;
@@ -339,18 +342,37 @@ __device__ __forceinline__ void stage_large(double2* __restrict__ A, double2* __
     B[e] = cm(A[e], W[(j % Ns) * r * tstep]);
   }
   __syncthreads();
-  for (int it = threadIdx.x; it < L * NC; it += blockDim.x) {
+  const int H = (R + 1) / 2;  // k = 0 and the pairs (k, R - k), k = 1..(R-1)/2 (R odd)
+  for (int it = threadIdx.x; it < T * H * NC; it += blockDim.x) {
     const int c = it % NC, q = it / NC;
-    const int j = q / R, k = q - j * R;
+    const int j = q / H, k = q - j * H;
     const int jm = j % Ns;
-    double2 acc = B[j * NC + c];
+    const double2* b = B + j * NC + c;
+    double2* out = A + ((j - jm) * R + jm) * NC + c;
+    if (k == 0) {
+      double2 acc = b[0];
+      for (int r = 1; r < R; ++r) {
+        const double2 v = b[r * T * NC];
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+      out[0] = acc;
+      continue;
+    }
+    const double2 v0 = b[0];
+    double sac = v0.x, sbd = 0.0, sad = 0.0, sbc = v0.y;
     int idx = k;
     for (int r = 1; r < R; ++r) {
-      acc = cfma(acc, B[(j + r * T) * NC + c], W[idx * rstep]);
+      const double2 v = b[r * T * NC], w = W[idx * rstep];
+      sac = fma(v.x, w.x, sac);
+      sbd = fma(v.y, w.y, sbd);
+      sad = fma(v.x, w.y, sad);
+      sbc = fma(v.y, w.x, sbc);
       idx += k;
       if (idx >= R) idx -= R;
     }
-    A[((j - jm) * R + jm + k * Ns) * NC + c] = acc;
+    out[(int64_t)k * Ns * NC] = make_double2(sac - sbd, sad + sbc);
+    out[(int64_t)(R - k) * Ns * NC] = make_double2(sac + sbd, sbc - sad);
   }
 }
 

@@ -11,10 +11,11 @@
 //   d_l = (A_b[q_l, l] - sum_{j<l} C^_b[l][j] d_j) / C^_b[l][l],
 // and Z_b[:, l] = U_b^{-1} d[:, l] (back substitution), so that
 //   A_b[:, l] ~= sum_j Z_b[j, l] A_b[:, k_j]      (eq:maca, skeleton form).
-// Both substitutions run in the ACA's pinned arithmetic and operation order
-// (pinned.cuh; aca.cu computes exactly these d_l and Z), and the fibre entries
-// are the pinned kernel of the ACA with the same conjugate mirroring, so the
-// regenerated Z is bit-identical to the one the ACA itself would store.
+// Both substitutions run in the ACA's pinned arithmetic (pinned.cuh) and the fibre
+// entries are the pinned kernel of the ACA with the same conjugate mirroring; the
+// forward substitution keeps the ACA's term order, so d is bit-identical to the
+// ACA's; the back substitution subtracts in decreasing j (the oracle: increasing j),
+// a rounding-level difference far below the 1e-10 parity tolerance.
 #pragma once
 #include "pinned.cuh"
 
@@ -56,53 +57,61 @@ __device__ __forceinline__ double2 fibre(const Src& a, int rc, int cc, int q, in
   return v;
 }
 
-// Z_b[:, l] for one frequency column, z[i * stride] already holding the pivot fibre
-// A_b[q_i, l] (fibre(), or zero for a padding column): forward substitution to d, then
-// back substitution to Z, in place.  Each row's dot product is split over four
-// interleaved partial sums (j mod 4), combined as ((s0 + s1) + (s2 + s3)) and then
-// subtracted: a fixed pinned order (bit-reproducible; the stored-Z and the factors-only
-// paths share this function), with a dependency chain a quarter as long as a
-// sequential sum.  (The ACA's own d rows use the sequential order; the difference is
-// rounding-level, far below the 1e-10 parity tolerance.)
-__device__ __forceinline__ double2 dot4(const double2* __restrict__ Fi, const double2* z, int64_t stride, int j0,
-                                        int j1) {
+// Z_b for a set of frequency columns, computed by the whole CTA (every thread calls it):
+// columns in batches of nb = cap / r in the shared buffer work [r][nb]:
+//   1. the pivot fibres A_b[q_i, l] of the batch, spread over all threads;
+//   2. forward substitution, right-looking: after step j the rows i > j have subtracted
+//      C^[i][j] d_j, so each d_i accumulates its terms in increasing j -- exactly the
+//      ACA's own order (aca.cu computes the same d); one barrier per step;
+//   3. back substitution, right-looking: Z_j is final once the rows j' > j have been
+//      subtracted (in decreasing j'), then every row i < j subtracts U[i][j] Z_j;
+//   4. out(j, c, Z_b[j, c]) for every row j and column c of the batch.
+// col_l(c) = the global frequency of column c, or -1 for a zero (padding / masked)
+// column.  The stored-Z regeneration (aca.cu) and the factors-only tile pass (far.cu)
+// both call this function, so the two skeleton modes agree bit for bit.
+template <class ColFn, class OutFn>
+__device__ __forceinline__ void block_columns(const Src& a, int b, int r, int c_begin, int c_end, ColFn col_l,
+                                              double2* work, int cap, OutFn out) {
   using namespace pinned;
-  double2 s[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-  int j = j0;
-  for (; j + 4 <= j1; j += 4) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double2 pr = cmul(Fi[j + u], z[(j + u) * stride]);
-      s[u] = make_double2(add(s[u].x, pr.x), add(s[u].y, pr.y));
-    }
-  }
-  for (int u = 0; j < j1; ++j, ++u) {
-    const double2 pr = cmul(Fi[j], z[j * stride]);
-    s[u] = make_double2(add(s[u].x, pr.x), add(s[u].y, pr.y));
-  }
-  return make_double2(add(add(s[0].x, s[1].x), add(s[2].x, s[3].x)), add(add(s[0].y, s[1].y), add(s[2].y, s[3].y)));
-}
-
-// (not inlined: keeps the coupling kernel's hot-loop register allocation unchanged)
-__device__ __forceinline__ void solve(const Src& a, int b, int r, double2* z, int64_t stride) {
-  using namespace pinned;
-  const double2* F = a.F + a.foff[b];
-  for (int i = 0; i < r; ++i)  // forward: d_i = (A[q_i, l] - sum_{j<i} C^[i][j] d_j) / C^[i][i]
-    z[i * stride] = cdiv(csub(z[i * stride], dot4(F + (int64_t)i * r, z, stride, 0, i)), F[(int64_t)i * r + i]);
-  for (int i = r - 2; i >= 0; --i)  // backward: Z_i = d_i - sum_{j>i} U[i][j] Z_j
-    z[i * stride] = csub(z[i * stride], dot4(F + (int64_t)i * r, z, stride, i + 1, r));
-}
-
-// the whole column: fibres, then the substitutions; l < 0 writes a zero column (padding)
-__device__ __forceinline__ void column(const Src& a, int b, int r, int l, double2* z, int64_t stride) {
-  if (l < 0) {
-    for (int j = 0; j < r; ++j) z[j * stride] = make_double2(0.0, 0.0);
-    return;
-  }
+  if (r <= 0) return;
   const int rc = a.far_r[b], cc = a.far_c[b];
+  const double2* F = a.F + a.foff[b];
   const int32_t* qp = a.pivq + (int64_t)b * a.rcap;
-  for (int i = 0; i < r; ++i) z[i * stride] = fibre(a, rc, cc, qp[i], l);
-  solve(a, b, r, z, stride);
+  const int nb = max(1, min(c_end - c_begin, cap / r));
+  for (int c0 = c_begin; c0 < c_end; c0 += nb) {
+    const int nc = min(nb, c_end - c0);
+    for (int e = threadIdx.x; e < r * nc; e += blockDim.x) {
+      const int i = e / nc, cl = e - i * nc;
+      const int l = col_l(c0 + cl);
+      work[i * nb + cl] = l >= 0 ? fibre(a, rc, cc, qp[i], l) : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    for (int cl = threadIdx.x; cl < nc; cl += blockDim.x) work[cl] = cdiv(work[cl], F[0]);
+    __syncthreads();
+    for (int j = 0; j + 1 < r; ++j) {  // forward: rows i > j subtract C^[i][j] d_j; row j+1 then divides
+      const int n = (r - j - 1) * nc;
+      for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        const int i = j + 1 + e / nc, cl = e % nc;
+        double2 v = csub(work[i * nb + cl], cmul(F[(int64_t)i * r + j], work[j * nb + cl]));
+        if (i == j + 1) v = cdiv(v, F[(int64_t)i * r + i]);
+        work[i * nb + cl] = v;
+      }
+      __syncthreads();
+    }
+    for (int j = r - 1; j >= 1; --j) {  // backward: rows i < j subtract U[i][j] Z_j
+      const int n = j * nc;
+      for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        const int i = e / nc, cl = e % nc;
+        work[i * nb + cl] = csub(work[i * nb + cl], cmul(F[(int64_t)i * r + j], work[j * nb + cl]));
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < r * nc; e += blockDim.x) {
+      const int jj = e / nc, cl = e - jj * nc;
+      out(jj, c0 + cl, work[jj * nb + cl]);
+    }
+    __syncthreads();
+  }
 }
 
 }  // namespace

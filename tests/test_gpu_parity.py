@@ -262,7 +262,7 @@ def test_edge_cases(pb, torch):
     assert _rel(_apply(pb, torch, op, x), oh.apply(O.MODE_H2ACA, s, x)) <= 1e-10
 
 
-@pytest.mark.parametrize("N,kernel", [(256, "7"), (260, "7"), (256, "8"), (260, "8")])
+@pytest.mark.parametrize("N,kernel", [(256, "7"), (260, "7"), (256, "8"), (260, "8"), (256, "9"), (260, "9")])
 def test_h2aca_p64_multi_tile(pb, torch, N, kernel, monkeypatch):
     """p = 64 (m = 4) with L > 128: K3 runs several frequency tiles per
     (segment, mu chunk).  N = 260 (L mod 8 = 5) exercises the zero-padded DMMA
@@ -328,7 +328,7 @@ def test_solve_multifreq_local_shard(pb, torch):
     assert _rel(phi, xo) <= 1e-6
 
 
-@pytest.mark.parametrize("kernel,kc", [("8", "0"), ("8", "32"), ("8", "20"), ("7", "0")])
+@pytest.mark.parametrize("kernel,kc", [("8", "0"), ("8", "32"), ("8", "20"), ("7", "0"), ("9", "0")])
 def test_h2aca_p125(pb, torch, kernel, kc, monkeypatch):
     """p = 125 (m = 5, config 5's order): far8 contracts nu in chunks
     (KC = 32 automatically, 20 forced: ragged last chunk 5), far7 whole p."""

@@ -376,8 +376,24 @@ def main():
             dist.barrier()
         return [a.elapsed_time(bb) for a, bb in evs]
 
-    # (1) eager steps with the library's per-kernel CUDA-event timers (kernel breakdown, roofline)
-    ms_eager = timed(lambda: step(x), True)
+    # (1) eager steps with the library's per-kernel CUDA-event timers (kernel breakdown, roofline);
+    # on one GPU the two K4 transforms are bracketed by events of their own
+    k4_ms = []
+    if world == 1 and not vshard and args.operator == "V":
+        def step_prof(z):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e[0].record()
+            xf = fwd(z)
+            e[1].record()
+            yf = opfn(xf)
+            e[2].record()
+            y = inv(yf)
+            e[3].record()
+            k4_ms.append(e)
+            return y
+        ms_eager = timed(lambda: step_prof(x), True)
+    else:
+        ms_eager = timed(lambda: step(x), True)
     op.set_profiling(False)
     # (2) headline: the same step captured once in a CUDA graph and replayed (removes the
     # host launch gaps of the ~25 small launches per step); 1 GPU only
@@ -493,7 +509,7 @@ def main():
         peak = FP64_PEAK_DERIVED / 1e12
         bound, src = "alu", "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §7)"
     achieved = fl / (kt[dom] * 1e-3) / 1e12
-    kname = {"coupling": ("K3 far7/far8_kernel (+seg_reduce)" if aca_far
+    kname = {"coupling": ("K3 far9 (p > 32) / far7 (p <= 32) coupling kernel (+seg_reduce)" if aca_far
                           else "K3' h2o_kernel (+seg_reduce)"),
              "near": "K1m nearm_kernel" if base_mode == pb.BEM_MODE_COMBINED else "K1 near_kernel"}[dom]
     roof = {"bound": bound, "kernel": kname, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -521,6 +537,11 @@ def main():
         "down": {"flops": f_up, "bytes": b_down, "ms": kt["down"], "peak_tflops": FP64_PEAK_DERIVED / 1e12,
                  "peak_gbs": hbm},
     }
+    if k4_ms:  # K4 forward + inverse: 32 M L bytes each (read + write of complex128 [L][M]), HBM-bound
+        torch.cuda.synchronize()
+        t_k4 = statistics.mean(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in k4_ms)
+        kern["k4"] = {"flops": 0.0, "bytes": 2 * 32.0 * M * nl, "ms": t_k4, "peak_tflops": FP64_PEAK_DERIVED / 1e12,
+                      "peak_gbs": hbm}
     t_roof = 0.0
     for k_, v_ in kern.items():
         t_f = v_["flops"] / (v_["peak_tflops"] * 1e12)
@@ -528,8 +549,9 @@ def main():
         v_["roof_ms"] = max(t_f, t_b) * 1e3
         v_["bound"] = "hbm" if t_b > t_f else ("tensor" if v_["peak_tflops"] != FP64_PEAK_DERIVED / 1e12 else "alu")
         v_["frac"] = v_["roof_ms"] / v_["ms"] if v_["ms"] > 0 else None
-        t_roof += v_["roof_ms"]
-    t_apply = sum(kt.values())
+        if k_ != "k4":
+            t_roof += v_["roof_ms"]
+    t_apply = sum(kt.values())  # the apply's kernels (K4 reported separately)
     per_kernel = {"kernels": kern, "apply_roof_ms": t_roof, "apply_ms": t_apply,
                   "apply_frac": t_roof / t_apply if t_apply > 0 else None,
                   "model": "SURVEY §8(d): F, B per kernel (75 flops per K1 evaluation; K2 with Kronecker transfers: "

@@ -437,8 +437,13 @@ struct Far8Args {
   const int32_t* mask;  // nullable: per local frequency, 0 = skip (output 0)
 };
 
-template <int MT, int NJ, int REM>
+// M3: three real DMMA products per complex one (P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi);
+// Re = P1 - P2, Im = P3 - P1 - P2): 25 % fewer DMMAs for a third accumulator, which fits
+// at NJ = 2 (16-row mu chunks); the real slice S_b(s_0) takes P1 and P3 only.
+template <int MT, int NJ, int REM, bool M3 = false>
 __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
+  constexpr int RW = NJ * 8 + REM;  // mu rows per CTA
+  constexpr int NA = M3 ? 3 : 2;    // accumulators per (tile, mu tile)
   extern __shared__ double2 sm[];
   const int p = a.p, m = a.m, SST = a.SST, XTP = a.XTP, tb = a.tb, KC = a.KC;
   // the mu chunks of one (segment, tile) are adjacent CTAs: the second chunk re-reads the
@@ -449,17 +454,17 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
   const int tc0 = a.tb + tile * a.TT;
   const int ncol = min(a.TT, a.tb + a.nd - tc0);
   const bool lead = tile == 0;
-  const int mu0 = (blockIdx.x % a.nch) * 32;
-  const int nrow = min(32, p - mu0);
-  double2* S0 = sm;                                   // 2 x (32 x SST), SST >= KC: double-buffered slice
-  double2* xs = S0 + 2 * 32 * SST;                    // KC x XTP
+  const int mu0 = (blockIdx.x % a.nch) * RW;
+  const int nrow = min(RW, p - mu0);
+  double2* S0 = sm;                                   // 2 x (RW x SST), SST >= KC: double-buffered slice
+  double2* xs = S0 + 2 * RW * SST;                    // KC x XTP
   double2* sctab = xs + (size_t)KC * XTP;             // 64 (cos, sin)(k pi/32)
   double* etab = (double*)(sctab + 64);               // 64
   double* xr = etab + 64;                             // 96
   double* xcn = xr + 96;                              // 3p
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
-  for (int i = tid; i < 2 * 32 * SST + KC * XTP; i += blockDim.x) sm[i] = make_double2(0.0, 0.0);
+  for (int i = tid; i < 2 * RW * SST + KC * XTP; i += blockDim.x) sm[i] = make_double2(0.0, 0.0);
   int sbuf = 0;
   for (int i = tid; i < 64; i += blockDim.x) {
     etab[i] = fast::kExp2Tab[i];
@@ -482,12 +487,14 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
     if (lead) for (int t = tid; t < tb; t += blockDim.x) lo |= a.mask == nullptr || a.mask[t];
     cta_on = __syncthreads_or(lo) != 0;
   }
-  double acc[MT][NJ][2][2];
+  double acc[MT][NJ][NA][2];
   double2 racc[MT][REM > 0 ? REM : 1];
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int u = 0; u < NA; ++u) acc[i][j][u][0] = acc[i][j][u][1] = 0.0;
 #pragma unroll
     for (int j = 0; j < (REM > 0 ? REM : 1); ++j) racc[i][j] = make_double2(0.0, 0.0);
   }
@@ -520,7 +527,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
         const bool real_slice = sv.y == 0.0;
         // S alternates between two buffers: one barrier per term, and warps may
         // run one term apart (regeneration overlaps other warps' DMMA work)
-        double2* S = S0 + sbuf * 32 * SST;
+        double2* S = S0 + sbuf * RW * SST;
         sbuf ^= 1;
         if (l == 0) __syncthreads();  // xs / node coordinates / Z tile staged
         const double2* Zl = zD + (int64_t)l * zst;
@@ -559,7 +566,23 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
               const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
               const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
               const double nai = -ai;
-              if constexpr (RS) {  // pivot frequency s_0 is real: Im S = 0, two DMMAs per complex MAC
+              if constexpr (M3) {
+                const double as = ar + ai;
+                if constexpr (RS) {
+#pragma unroll
+                  for (int j = 0; j < NJ; ++j) {
+                    dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+                    dmma(acc[i][j][NA - 1][0], acc[i][j][NA - 1][1], as, bf[j].x);
+                  }
+                } else {
+#pragma unroll
+                  for (int j = 0; j < NJ; ++j) {
+                    dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
+                    dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].y);
+                    dmma(acc[i][j][NA - 1][0], acc[i][j][NA - 1][1], as, bf[j].x + bf[j].y);
+                  }
+                }
+              } else if constexpr (RS) {  // pivot frequency s_0 is real: Im S = 0, two DMMAs per complex MAC
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
                   dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
@@ -621,7 +644,13 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int row = j * 8 + 2 * q + v;
-        if (row < nrow) out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
+        if (row < nrow) {
+          if constexpr (M3)
+            out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v] - acc[i][j][1][v],
+                                                           acc[i][j][NA - 1][v] - acc[i][j][0][v] - acc[i][j][1][v]);
+          else
+            out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
+        }
       }
   }
   if (REM > 0) {
@@ -640,231 +669,6 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
         if (q == 0 && t < a.nl && NJ * 8 + j < nrow) out[(int64_t)t * p + mu0 + NJ * 8 + j] = v;
       }
     }
-  }
-  if (lead && tb > 0) {
-#pragma unroll
-    for (int tl = 0; tl < 2; ++tl) {
-      if (tl >= tb) break;
-      double2 v = lacc[tl];
-#pragma unroll
-      for (int off = 1; off < 8; off <<= 1) {
-        v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
-        v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
-      }
-      if (lpart == 0 && lrow < nrow) out[(int64_t)tl * p + mu0 + lrow] = v;
-    }
-  }
-}
-
-// ------------------------------------------------ far9: warp-specialised far8 (p > 32)
-// The same per-term DMMA product as far8, with the slice regeneration moved to
-// dedicated producer warps: 4 producer warps regenerate S_b(s_{k_j})[mu-chunk][nu-chunk]
-// into a 3-stage ring in shared memory while 12 consumer warps run the DMMA loop on the
-// previous stages; named barriers FULL[s] (producers arrive, consumers wait) and
-// EMPTY[s] (consumers arrive, producers wait) order the ring -- no CTA-wide barrier per
-// term.  One CTA per SM (512 threads, 128 registers), 12 x 16 = 192 frequency columns
-// per CTA (far8: 128), so every regenerated slice entry serves 1.4x more columns.
-constexpr int kF9Cons = 12, kF9Prod = 4, kF9Stages = 3;
-constexpr int kF9BarCons = 1, kF9BarProd = 2, kF9BarFull = 3, kF9BarEmpty = 3 + kF9Stages;
-
-__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void bar_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-__global__ void __launch_bounds__((kF9Cons + kF9Prod) * 32, 1) far9_kernel(Far8Args a) {
-  constexpr int MT = 2, NJ = 4, NT = (kF9Cons + kF9Prod) * 32, NC = kF9Cons * 32, NP = kF9Prod * 32;
-  extern __shared__ double2 sm[];
-  const int p = a.p, m = a.m, SST = a.SST, XTP = a.XTP, tb = a.tb, KC = a.KC;
-  const int4 sg = a.segs[blockIdx.x / a.nch];
-  const int r = sg.x;
-  const int tile = blockIdx.y + a.tile0;
-  const int tc0 = a.tb + tile * a.TT;
-  const int ncol = min(a.TT, a.tb + a.nd - tc0);
-  const bool lead = tile == 0;
-  const int mu0 = (blockIdx.x % a.nch) * 32;
-  const int nrow = min(32, p - mu0);
-  double2* Sring = sm;                                  // kF9Stages x (32 x SST)
-  double2* xs = Sring + kF9Stages * 32 * SST;           // KC x XTP
-  double2* sctab = xs + (size_t)KC * XTP;               // 64 (cos, sin)(k pi/32)
-  double* etab = (double*)(sctab + 64);                 // 64
-  double* xr = etab + 64;                               // 96
-  double* xcn = xr + 96;                                // 3p (producers)
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < kF9Stages * 32 * SST + KC * XTP; i += NT) sm[i] = make_double2(0.0, 0.0);
-  for (int i = tid; i < 64; i += NT) {
-    etab[i] = fast::kExp2Tab[i];
-    sctab[i] = fast::kSinCosTab[i];
-  }
-  for (int i = tid; i < nrow; i += NT) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
-  const int ntile = ncol / 8;
-  bool cta_on;
-  {
-    int lo = 0;
-    for (int t = tid; t < ncol; t += NT) lo |= (tc0 + t < a.nl) && (a.mask == nullptr || a.mask[tc0 + t]);
-    if (lead) for (int t = tid; t < tb; t += NT) lo |= a.mask == nullptr || a.mask[t];
-    cta_on = __syncthreads_or(lo) != 0;
-  }
-  double2* out = a.part + (int64_t)sg.w * a.nl * p;
-  if (warp >= kF9Cons) {  // ---------------- producers: slice regeneration into the ring
-    const int ptid = tid - NC;
-    int it = 0;
-    for (int bi = sg.y; bi < (cta_on ? sg.z : sg.y); ++bi) {
-      const int b = a.far_sorted[bi];
-      const int c = a.far_c[b];
-      const int rk = a.rank[b];
-      bar_sync(kF9BarProd, NP);  // every producer is done with the previous block's nodes
-      for (int i = ptid; i < p; i += NP) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
-      bar_sync(kF9BarProd, NP);
-      for (int k0c = 0; k0c < p; k0c += KC) {
-        const int kw = min(KC, p - k0c);
-        for (int l = 0; l < rk; ++l, ++it) {
-          const int st = it % kF9Stages;
-          if (it >= kF9Stages) bar_sync(kF9BarEmpty + st, NT);  // consumers released the stage
-          const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + l]];
-          double2* S = Sring + st * 32 * SST;
-          for (int e = ptid; e < 32 * KC; e += NP) {
-            const int i = e / KC, nu = e - i * KC;
-            double2 v = make_double2(0.0, 0.0);
-            if (nu < kw && i < nrow) {
-              const int nn = k0c + nu;
-              const double dx = xcn[3 * nn] - xr[3 * i], dy = xcn[3 * nn + 1] - xr[3 * i + 1],
-                           dz = xcn[3 * nn + 2] - xr[3 * i + 2];
-              v = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab, sctab);
-            }
-            S[i * SST + nu] = v;
-          }
-          bar_arrive(kF9BarFull + st, NT);
-        }
-      }
-    }
-    for (int d = max(0, it - kF9Stages); d < it; ++d) bar_sync(kF9BarEmpty + d % kF9Stages, NT);  // drain
-    return;
-  }
-  // ---------------- consumers: DMMA product of the staged x^ tile with the ring's slices
-  const int g = lane >> 2, q = lane & 3;
-  bool ton[MT];
-#pragma unroll
-  for (int i = 0; i < MT; ++i) {
-    const int tt = warp + kF9Cons * i;
-    const int t = tc0 + tt * 8 + g;
-    const bool v = tt < ntile && t < a.nl && (a.mask == nullptr || a.mask[t]);
-    ton[i] = __any_sync(0xffffffffu, v);
-  }
-  double acc[MT][NJ][2][2];
-#pragma unroll
-  for (int i = 0; i < MT; ++i)
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
-  const int lrow = tid >> 3, lpart = tid & 7;  // leftover columns: rows 0..47 over the consumers
-  const bool lown = lead && tb > 0 && lrow < nrow;
-  double2 lacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-  const int ncp = tb + ncol;
-  int it = 0;
-  for (int bi = sg.y; bi < (cta_on ? sg.z : sg.y); ++bi) {
-    const int b = a.far_sorted[bi];
-    const int c = a.far_c[b];
-    const double2* xh = a.xhat + (int64_t)c * a.nl * p;
-    const int rk = a.rank[b];
-    const double2 *zD, *zL;
-    int zst;
-    zrows(a.z, b, a.nl, tb, tc0, zD, zL, zst);
-    for (int k0c = 0; k0c < p; k0c += KC) {
-      const int kw = min(KC, p - k0c);
-      const int kw4 = (kw + 3) & ~3;
-      bar_sync(kF9BarCons, NC);  // every consumer is done with the previous x^ tile
-      for (int idx = tid; idx < ncp * KC; idx += NC) {
-        const int tl = idx / KC, nu = idx - tl * KC;
-        const int tg = tl < tb ? tl : tc0 + (tl - tb);
-        if (tl >= tb || lead)
-          xs[nu * XTP + tl] = (nu < kw && tg < a.nl) ? xh[(int64_t)tg * p + k0c + nu] : make_double2(0.0, 0.0);
-      }
-      bar_sync(kF9BarCons, NC);
-      for (int l = 0; l < rk; ++l, ++it) {
-        const int st = it % kF9Stages;
-        const bool real_slice = a.s[a.pivk[(int64_t)b * a.rcap + l]].y == 0.0;
-        const double2* Zl = zD + (int64_t)l * zst;
-        double2 zt[MT];
-#pragma unroll
-        for (int i = 0; i < MT; ++i) {
-          const int tt = warp + kF9Cons * i;
-          const int t = tc0 + tt * 8 + g;
-          zt[i] = (tt < ntile && t < a.nl) ? Zl[t] : make_double2(0.0, 0.0);
-        }
-        bar_sync(kF9BarFull + st, NT);  // the stage's slice is written
-        const double2* S = Sring + st * 32 * SST;
-        auto gemm = [&](auto realc) {
-          constexpr bool RS = decltype(realc)::value;
-          for (int k0 = 0; k0 < kw4; k0 += 4) {
-            double2 bf[NJ];
-#pragma unroll
-            for (int j = 0; j < NJ; ++j) bf[j] = S[(j * 8 + g) * SST + k0 + q];
-#pragma unroll
-            for (int i = 0; i < MT; ++i) {
-              const int tt = warp + kF9Cons * i;
-              if (tt < ntile && ton[i]) {
-                const double2 xv = xs[(k0 + q) * XTP + tb + tt * 8 + g];
-                const double ar = zt[i].x * xv.x - zt[i].y * xv.y;
-                const double ai = zt[i].x * xv.y + zt[i].y * xv.x;
-                const double nai = -ai;
-                if constexpr (RS) {
-#pragma unroll
-                  for (int j = 0; j < NJ; ++j) {
-                    dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
-                    dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
-                  }
-                } else {
-#pragma unroll
-                  for (int j = 0; j < NJ; ++j) {
-                    dmma(acc[i][j][0][0], acc[i][j][0][1], ar, bf[j].x);
-                    dmma(acc[i][j][1][0], acc[i][j][1][1], ar, bf[j].y);
-                  }
-#pragma unroll
-                  for (int j = 0; j < NJ; ++j) {
-                    dmma(acc[i][j][0][0], acc[i][j][0][1], nai, bf[j].y);
-                    dmma(acc[i][j][1][0], acc[i][j][1][1], ai, bf[j].x);
-                  }
-                }
-              }
-            }
-          }
-        };
-        if (real_slice) gemm(std::true_type{});
-        else gemm(std::false_type{});
-        if (lown) {
-#pragma unroll
-          for (int tl = 0; tl < 2; ++tl) {
-            if (tl >= tb) break;
-            double2 sacc = make_double2(0.0, 0.0);
-            for (int nu = lpart; nu < kw; nu += 8) {
-              const double2 sv2 = S[lrow * SST + nu], xv = xs[nu * XTP + tl];
-              sacc.x = fma(sv2.x, xv.x, sacc.x);
-              sacc.x = fma(-sv2.y, xv.y, sacc.x);
-              sacc.y = fma(sv2.x, xv.y, sacc.y);
-              sacc.y = fma(sv2.y, xv.x, sacc.y);
-            }
-            const double2 zz = zL[(int64_t)l * zst + tl];
-            lacc[tl].x = fma(zz.x, sacc.x, fma(-zz.y, sacc.y, lacc[tl].x));
-            lacc[tl].y = fma(zz.x, sacc.y, fma(zz.y, sacc.x, lacc[tl].y));
-          }
-        }
-        bar_arrive(kF9BarEmpty + st, NT);  // this warp is done reading the stage
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < MT; ++i) {
-    const int tt = warp + kF9Cons * i;
-    if (tt >= ntile) continue;
-    const int t = tc0 + tt * 8 + g;
-    if (t >= a.nl) continue;
-#pragma unroll
-    for (int j = 0; j < NJ; ++j)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int row = j * 8 + 2 * q + v;
-        if (row < nrow) out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
-      }
   }
   if (lead && tb > 0) {
 #pragma unroll
@@ -919,49 +723,21 @@ Far8Cfg choose8(int p, int nl, size_t cap, int kc_req) {
   return Far8Cfg{};
 }
 
-// far9 geometry: KC = 32, a 3-stage slice ring, frequency tiles of <= 192 columns
-Far8Cfg choose9(int p, int nl) {
-  Far8Cfg c;
-  if (p <= 32) return c;
-  int tb = nl % 8;
-  if (tb > 2 || tb == nl) tb = 0;
-  const int nD = (nl - tb + 7) / 8 * 8;
-  const int KC = 32;
-  int SST = KC;
-  while (SST % 8 != 4) ++SST;
-  const int ntiles = (nD + 16 * kF9Cons - 1) / (16 * kF9Cons);
-  const int TT = ((nD / 8 + ntiles - 1) / ntiles) * 8;
-  int XTP = tb + TT;
-  while (XTP % 8 != 2) ++XTP;
-  const size_t smem = sizeof(double2) * ((size_t)kF9Stages * 32 * SST + (size_t)KC * XTP + 64) +
-                      sizeof(double) * (64 + 96 + 3 * (size_t)p);
-  if (smem > 200 * 1024) return c;
-  c.SST = SST; c.TT = TT; c.XTP = XTP; c.tb = tb; c.nd = nD; c.ntiles = ntiles;
-  c.nchunks = (p + 31) / 32; c.mt = 2; c.smem = smem; c.KC = KC;
-  return c;
-}
-
-cudaError_t launch9(const Far8Cfg& c, int nseg, const Far8Args& a, int ntile, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(far9_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-  if (e != cudaSuccess) return e;
-  Far8Args a2 = a;
-  a2.nch = c.nchunks;
-  far9_kernel<<<dim3((unsigned)(nseg * c.nchunks), (unsigned)ntile, 1u), (kF9Cons + kF9Prod) * 32, c.smem, st>>>(a2);
-  return cudaGetLastError();
-}
-
-template <int MT, int NJ, int REM>
+template <int MT, int NJ, int REM, bool M3 = false>
 cudaError_t launch8(const Far8Cfg& c, int nseg, const Far8Args& a, int ntile, cudaStream_t st) {
-  auto k = far8_kernel<MT, NJ, REM>;
+  auto k = far8_kernel<MT, NJ, REM, M3>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   if (e != cudaSuccess) return e;
   Far8Args a2 = a;
-  a2.nch = c.nchunks;
-  k<<<dim3((unsigned)(nseg * c.nchunks), (unsigned)ntile, 1u), 256, c.smem, st>>>(a2);
+  a2.nch = (a.p + NJ * 8 + REM - 1) / (NJ * 8 + REM);  // mu chunks of NJ * 8 + REM rows
+  k<<<dim3((unsigned)(nseg * a2.nch), (unsigned)ntile, 1u), 256, c.smem, st>>>(a2);
   return cudaGetLastError();
 }
 
-cudaError_t dispatch8(const Far8Cfg& c, int p, int nseg, const Far8Args& a, int ntile, cudaStream_t st) {
+cudaError_t dispatch8(const Far8Cfg& c, int p, int nseg, const Far8Args& a, int ntile, cudaStream_t st,
+                      bool m3 = false) {
+  if (m3 && p > 8 && p != 27)
+    return c.mt == 1 ? launch8<1, 2, 0, true>(c, nseg, a, ntile, st) : launch8<2, 2, 0, true>(c, nseg, a, ntile, st);
   if (p <= 8) return c.mt == 1 ? launch8<1, 1, 0>(c, nseg, a, ntile, st) : launch8<2, 1, 0>(c, nseg, a, ntile, st);
   if (p == 27) return c.mt == 1 ? launch8<1, 3, 3>(c, nseg, a, ntile, st) : launch8<2, 3, 3>(c, nseg, a, ntile, st);
   return c.mt == 1 ? launch8<1, 4, 0>(c, nseg, a, ntile, st) : launch8<2, 4, 0>(c, nseg, a, ntile, st);
@@ -1254,13 +1030,8 @@ static FarGeom far_geom(const Op& op) {
   const Tree& t = *op.tree;
   const int p = t.p, nl = op.n_local;
   FarGeom g;
-  g.fk = op.far_kernel != 0 ? op.far_kernel : (p > 32 ? 9 : 7);  // far9 (warp-specialised) for p > 32
+  g.fk = op.far_kernel != 0 ? op.far_kernel : (p > 32 ? 8 : 7);  // r01: far8 wins at p = 64, far7 at p = 27
   if (op.force_generic || op.n_segs == 0) { g.fk = 0; return g; }
-  if (g.fk == 9) {
-    g.f8 = choose9(p, nl);
-    if (g.f8.mt > 0) { g.ntiles = g.f8.ntiles; g.tb = g.f8.tb; g.TT = g.f8.TT; g.ZW = g.tb + g.TT; return g; }
-    g.fk = 8;
-  }
   if (g.fk == 8) {
     g.f8 = choose8(p, nl, op.far4_smem_cap, op.far8_kc);
     if (g.f8.mt > 0) { g.ntiles = g.f8.ntiles; g.tb = g.f8.tb; g.TT = g.f8.TT; g.ZW = g.tb + g.TT; return g; }
@@ -1353,7 +1124,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
             g.ZW, kZgenSmem / (int)sizeof(double2), (double2*)op.d_zs.p);
         BEM_CK(cudaGetLastError());
       }
-      if (g.fk == 8 || g.fk == 9) {
+      if (g.fk == 8) {
         const Far8Cfg& f8 = g.f8;
         Far8Args a;
         a.nl = nl; a.m = t.m; a.p = p; a.rcap = op.rcap; a.SST = f8.SST; a.TT = f8.TT; a.XTP = f8.XTP;
@@ -1361,7 +1132,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
         a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
         a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
         a.z = z; a.xhat = xhat; a.part = (double2*)op.d_part.p; a.mask = op.d_mask;
-        BEM_CK(g.fk == 9 ? launch9(f8, op.n_segs, a, ntile, st) : dispatch8(f8, p, op.n_segs, a, ntile, st));
+        BEM_CK(dispatch8(f8, p, op.n_segs, a, ntile, st, op.far8_m3));
       } else {
         const Far7Cfg& f7 = g.f7;
         Far7Args a;

@@ -376,6 +376,45 @@ __device__ __forceinline__ void stage_large(double2* __restrict__ A, double2* __
   }
 }
 
+// prime radix 11 <= R <= 23 with the butterfly in registers: one thread per (j, column)
+// loads its R twiddled inputs once and forms every output pair (k, R - k) from them
+// (the roots are shared-memory broadcasts); A -> B like the small stages.
+template <int R>
+__device__ __forceinline__ void stage_prime_reg(const double2* __restrict__ A, double2* __restrict__ B, int L, int Ns,
+                                                int NC, const double2* __restrict__ W) {
+  const int T = L / R, tstep = L / (Ns * R), rstep = L / R;
+  for (int it = threadIdx.x; it < T * NC; it += blockDim.x) {
+    const int j = it / NC, c = it - j * NC;
+    const int jm = j % Ns;
+    double2 v[R];
+    v[0] = A[j * NC + c];
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cm(A[(j + r * T) * NC + c], W[jm * r * tstep]);
+    double2* out = B + ((j - jm) * R + jm) * NC + c;
+    double2 s0 = v[0];
+#pragma unroll
+    for (int r = 1; r < R; ++r) { s0.x += v[r].x; s0.y += v[r].y; }
+    out[0] = s0;
+#pragma unroll 1
+    for (int k = 1; k <= R / 2; ++k) {
+      double sac = v[0].x, sbd = 0.0, sad = 0.0, sbc = v[0].y;
+      int idx = k;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const double2 w = W[idx * rstep];
+        sac = fma(v[r].x, w.x, sac);
+        sbd = fma(v[r].y, w.y, sbd);
+        sad = fma(v[r].x, w.y, sad);
+        sbc = fma(v[r].y, w.x, sbc);
+        idx += k;
+        if (idx >= R) idx -= R;
+      }
+      out[(int64_t)k * Ns * NC] = make_double2(sac - sbd, sad + sbc);
+      out[(int64_t)(R - k) * Ns * NC] = make_double2(sac + sbd, sbc - sad);
+    }
+  }
+}
+
 __device__ __forceinline__ void stockham_body(const K4Args& a, const double2* const* tab) {
   extern __shared__ double2 sm2[];
   const int L = a.L, NC = a.NC;
@@ -405,9 +444,14 @@ __device__ __forceinline__ void stockham_body(const K4Args& a, const double2* co
       case 4: stage_small<4>(A, B, L, Ns, NC, W); break;
       case 5: stage_small<5>(A, B, L, Ns, NC, W); break;
       case 7: stage_small<7>(A, B, L, Ns, NC, W); break;
+      case 11: stage_prime_reg<11>(A, B, L, Ns, NC, W); break;
+      case 13: stage_prime_reg<13>(A, B, L, Ns, NC, W); break;
+      case 17: stage_prime_reg<17>(A, B, L, Ns, NC, W); break;
+      case 19: stage_prime_reg<19>(A, B, L, Ns, NC, W); break;
+      case 23: stage_prime_reg<23>(A, B, L, Ns, NC, W); break;
       default: stage_large(A, B, L, R, Ns, NC, W); break;
     }
-    if (R <= 8) { double2* t = A; A = B; B = t; }
+    if (R <= 23) { double2* t = A; A = B; B = t; }
     __syncthreads();
     Ns *= R;
   }
@@ -457,8 +501,8 @@ struct RowTab {
   const double2* p[kMaxRows];
 };
 
-__global__ void __launch_bounds__(kFftThreads, 3) stockham_kernel(const K4Args a) { stockham_body(a, nullptr); }
-__global__ void __launch_bounds__(kFftThreads, 3) stockham_rows_kernel(const K4Args a, const __grid_constant__ RowTab tab) {
+__global__ void __launch_bounds__(kFftThreads, 2) stockham_kernel(const K4Args a) { stockham_body(a, nullptr); }
+__global__ void __launch_bounds__(kFftThreads, 2) stockham_rows_kernel(const K4Args a, const __grid_constant__ RowTab tab) {
   stockham_body(a, tab.p);
 }
 __global__ void __launch_bounds__(kFftThreads) bluestein_kernel(const K4Args a) { bluestein_body(a, nullptr); }

@@ -35,9 +35,8 @@ def _rel(a, b):
 @pytest.mark.parametrize("m,leaf,N,eps,kernel", [
     (3, 32, 128, 1e-6, "0"),   # p = 27: far7, 3 DMMA row tiles + DFMA rows, leftover column l = 0
     (3, 32, 130, 1e-6, "8"),   # p = 27 on far8, padded DMMA columns (L mod 8 = 3)
-    (4, 48, 256, 1e-6, "0"),   # p = 64: far9 (warp-specialised), 2 frequency tiles
-    (4, 48, 256, 1e-6, "8"),   # p = 64: far8, 3 frequency tiles
-    (5, 64, 64, 1e-8, "0"),    # p = 125: far9 with nu chunks
+    (4, 48, 256, 1e-6, "0"),   # p = 64: far8, 3 frequency tiles
+    (5, 64, 64, 1e-8, "0"),    # p = 125: far8 with nu chunks
 ])
 def test_factors_vs_stored_bitwise_and_oracle(pb, torch, m, leaf, N, eps, kernel, monkeypatch):
     monkeypatch.setenv("BEM_FAR_KERNEL", kernel)

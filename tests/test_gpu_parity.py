@@ -262,12 +262,14 @@ def test_edge_cases(pb, torch):
     assert _rel(_apply(pb, torch, op, x), oh.apply(O.MODE_H2ACA, s, x)) <= 1e-10
 
 
-@pytest.mark.parametrize("N,kernel", [(256, "7"), (260, "7"), (256, "8"), (260, "8"), (256, "9"), (260, "9")])
-def test_h2aca_p64_multi_tile(pb, torch, N, kernel, monkeypatch):
+@pytest.mark.parametrize("N,kernel,m3", [(256, "7", "0"), (260, "7", "0"), (256, "8", "0"), (260, "8", "0"),
+                                          (256, "8", "1"), (260, "8", "1")])
+def test_h2aca_p64_multi_tile(pb, torch, N, kernel, m3, monkeypatch):
     """p = 64 (m = 4) with L > 128: K3 runs several frequency tiles per
     (segment, mu chunk).  N = 260 (L mod 8 = 5) exercises the zero-padded DMMA
     columns, N = 256 the distributed leftover column.  Oracle on a frequency sample."""
     monkeypatch.setenv("BEM_FAR_KERNEL", kernel)
+    monkeypatch.setenv("BEM_FAR8_M3", m3)  # 3M complex products at 16-row mu chunks
     V, T = synth.icosphere(3)
     M, L, eps = len(T), N + 1, 1e-6
     s = pb.cqm_frequencies(N, 2.0)
@@ -328,12 +330,14 @@ def test_solve_multifreq_local_shard(pb, torch):
     assert _rel(phi, xo) <= 1e-6
 
 
-@pytest.mark.parametrize("kernel,kc", [("8", "0"), ("8", "32"), ("8", "20"), ("7", "0"), ("9", "0")])
-def test_h2aca_p125(pb, torch, kernel, kc, monkeypatch):
+@pytest.mark.parametrize("kernel,kc,m3", [("8", "0", "0"), ("8", "32", "0"), ("8", "20", "0"), ("7", "0", "0"),
+                                          ("8", "0", "1"), ("8", "20", "1")])
+def test_h2aca_p125(pb, torch, kernel, kc, m3, monkeypatch):
     """p = 125 (m = 5, config 5's order): far8 contracts nu in chunks
     (KC = 32 automatically, 20 forced: ragged last chunk 5), far7 whole p."""
     monkeypatch.setenv("BEM_FAR_KERNEL", kernel)
     monkeypatch.setenv("BEM_FAR8_KC", kc)
+    monkeypatch.setenv("BEM_FAR8_M3", m3)
     V, T = synth.icosphere(3)
     N = 64
     M, L, eps = len(T), N + 1, 1e-8

@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(kPassThreads) up_leaf_d_kernel(const int32_t* 
   for (int i = threadIdx.x; i < n4 * kLeafT; i += blockDim.x) {
     const int tl = i / n4, k = i - tl * n4;  // consecutive threads: consecutive panels (coalesced)
     const double2 v = (k < n && tl < nt) ? xc[(int64_t)(t0 + tl) * M + b + k] : make_double2(0.0, 0.0);
+    BEM_DASSERT(k < n4 && 2 * tl + 1 < XS);
     Xs[k * XS + 2 * tl] = v.x;
     Xs[k * XS + 2 * tl + 1] = v.y;
   }
@@ -380,6 +381,7 @@ __global__ void __launch_bounds__(kPassThreads) down_leaf_d_kernel(const int32_t
   for (int i = threadIdx.x; i < kLeafT * p4; i += blockDim.x) {
     const int tl = i / p4, mu = i - tl * p4;
     const double2 v = (mu < p && tl < nt) ? yhat[((int64_t)c * nl + t0 + tl) * p + mu] : make_double2(0.0, 0.0);
+    BEM_DASSERT(mu < p4 && 2 * tl + 1 < YS);
     Ys[mu * YS + 2 * tl] = v.x;
     Ys[mu * YS + 2 * tl + 1] = v.y;
   }
@@ -397,6 +399,7 @@ __global__ void __launch_bounds__(kPassThreads) down_leaf_d_kernel(const int32_t
     const int k = k0r + g, tl = (n0 >> 1) + q;
     if (k < n && tl < nt) {
       const int64_t row = (int64_t)(t0 + tl) * M;
+      BEM_DASSERT(b + k < M && perm[b + k] >= 0 && perm[b + k] < M);
       double2 acc = yc[row + b + k];
       acc.x += c0;
       acc.y += c1;

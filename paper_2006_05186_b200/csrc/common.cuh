@@ -14,6 +14,25 @@
 
 namespace bem {
 
+// Device-side bounds checks, compiled in only for the checked build
+// (`python -m paper_2006_05186_b200.build --checked` -> libbem_checked.so): the
+// memory-safety evidence on this pool, where compute-sanitizer is not available.
+#ifdef BEM_CHECKS
+#include <cstdio>
+#define BEM_DASSERT(c)                                                                                 \
+  do {                                                                                                 \
+    if (!(c)) {                                                                                        \
+      printf("BEM_DASSERT failed %s:%d: %s (block %d, thread %d)\n", __FILE__, __LINE__, #c, blockIdx.x, \
+             threadIdx.x);                                                                             \
+      __trap();                                                                                        \
+    }                                                                                                  \
+  } while (0)
+#else
+#define BEM_DASSERT(c) \
+  do {                 \
+  } while (0)
+#endif
+
 // NVTX range over a host scope (stage markers for ncu --nvtx / profilers: the paper's
 // stage timings P:1808-1828 -- tree, ACA, gather, K1, K2, K3, K4, GMRES).  Header-only
 // NVTX v3: a no-op unless a profiler injects itself.

@@ -85,6 +85,7 @@ struct ZSrc {
   const int64_t* zoff;
   const double2* Z;
   int tiled, ZW;  // tiled: Z = tile buffer, zoff = per-block offsets in it
+  int64_t zn;     // elements of Z (bounds checks)
 };
 
 // Z_b[j, t] = zD[j * stride + t] for the tile's DMMA columns t, zL[j * stride + t] for the
@@ -110,11 +111,13 @@ __global__ void __launch_bounds__(256) zgen_tile_kernel(zgen::Src g, int nfar, c
                                                         const int64_t* __restrict__ ztoff,
                                                         const int32_t* __restrict__ local_l,
                                                         const int32_t* __restrict__ mask, int nl, int tb, int tc0,
-                                                        int ncol, int lead, int ZW, int cap, double2* __restrict__ Zt) {
+                                                        int ncol, int lead, int ZW, int cap, double2* __restrict__ Zt,
+                                                        int64_t zt_n) {
   extern __shared__ double2 work[];
   const int ncp = tb + ncol;
   for (int b = blockIdx.x; b < nfar; b += gridDim.x) {
     double2* out = Zt + ztoff[b];
+    BEM_DASSERT(ztoff[b] + (int64_t)rank[b] * ZW <= zt_n);
     zgen::block_columns(
         g, b, rank[b], lead ? 0 : tb, ncp,
         [&](int c) {
@@ -139,6 +142,7 @@ __global__ void __launch_bounds__(256) zgen_tile_kernel(zgen::Src g, int nfar, c
 // accumulated by all 256 threads of the lead CTA; more are zero-padded DMMA columns.
 struct Far7Args {
   int nl, m, p, p4, rcap, SST, TT, XTP, tb, nd;  // DMMA columns [tb, tb+nd) (padded past nl)
+  int64_t part_n = 0;                            // elements of part (bounds checks)
   int tile0 = 0;                                 // first frequency tile of this launch (grid y offset)
   const int4* segs;
   const int32_t* far_sorted;
@@ -226,6 +230,7 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
     for (int idx = tid; idx < ncp * p; idx += blockDim.x) {
       const int tl = idx / p, nu = idx - tl * p;
       const int tg = tl < tb ? tl : tc0 + (tl - tb);
+      BEM_DASSERT(nu < p4 && tl < XTP);
       if (tl >= tb || lead) xs[nu * XTP + tl] = tg < a.nl ? xh[(int64_t)tg * p + nu] : make_double2(0.0, 0.0);
     }
     __syncthreads();
@@ -239,6 +244,7 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
       for (int i = 0; i < MT; ++i) {
         const int tt = warp + 8 * i;
         const int t = tc0 + tt * 8 + g;
+        BEM_DASSERT(!(tt < ntile && t < a.nl) || (Zl + t >= a.z.Z && Zl + t < a.z.Z + a.z.zn));
         zt[i] = (tt < ntile && t < a.nl) ? Zl[t] : make_double2(0.0, 0.0);
       }
       for (int e = tid; e < nS; e += blockDim.x) {
@@ -327,7 +333,10 @@ __global__ void __launch_bounds__(256, 2) far7_kernel(Far7Args a) {
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int row = j * 8 + 2 * q + v;
-        if (row < nrow) out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
+        if (row < nrow) {
+          BEM_DASSERT((out - a.part) + (int64_t)t * p + mu0 + row < a.part_n);
+          out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v], acc[i][j][1][v]);
+        }
       }
   }
   if (REM > 0) {
@@ -422,6 +431,7 @@ cudaError_t dispatch7(const Far7Cfg& c, int p, int nseg, const Far7Args& a, int 
 // frequency tile stays at TT = 128 with two CTAs per SM for p = 64 and 125.
 struct Far8Args {
   int nl, m, p, rcap, SST, TT, XTP, tb, nd, KC;
+  int64_t part_n = 0;  // elements of part (bounds checks)
   int tile0 = 0;  // first frequency tile of this launch (grid y offset)
   int nch = 1;  // mu chunks (grid x = segment * nch + chunk)
   const int4* segs;
@@ -519,6 +529,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
       for (int idx = tid; idx < ncp * KC; idx += blockDim.x) {
         const int tl = idx / KC, nu = idx - tl * KC;
         const int tg = tl < tb ? tl : tc0 + (tl - tb);
+        BEM_DASSERT(nu < KC && tl < XTP);
         if (tl >= tb || lead)
           xs[nu * XTP + tl] = (nu < kw && tg < a.nl) ? xh[(int64_t)tg * p + k0c + nu] : make_double2(0.0, 0.0);
       }
@@ -536,7 +547,9 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
         for (int i = 0; i < MT; ++i) {
           const int tt = warp + 8 * i;
           const int t = tc0 + tt * 8 + g;
-          zt[i] = (tt < ntile && t < a.nl) ? Zl[t] : make_double2(0.0, 0.0);
+          BEM_DASSERT(!(tt < ntile && t < a.nl) || (Zl + t >= a.z.Z && Zl + t < a.z.Z + a.z.zn));
+          BEM_DASSERT(!(tt < ntile && t < a.nl) || (Zl + t >= a.z.Z && Zl + t < a.z.Z + a.z.zn));
+        zt[i] = (tt < ntile && t < a.nl) ? Zl[t] : make_double2(0.0, 0.0);
         }
         for (int e = tid; e < nrow * KC; e += blockDim.x) {
           const int i = e / KC, nu = e - i * KC;
@@ -547,6 +560,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
                          dz = xcn[3 * nn + 2] - xr[3 * i + 2];
             v = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab, sctab);
           }
+          BEM_DASSERT(i < RW && nu < SST);
           S[i * SST + nu] = v;
         }
         __syncthreads();
@@ -645,6 +659,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
       for (int v = 0; v < 2; ++v) {
         const int row = j * 8 + 2 * q + v;
         if (row < nrow) {
+          BEM_DASSERT((out - a.part) + (int64_t)t * p + mu0 + row < a.part_n);
           if constexpr (M3)
             out[(int64_t)t * p + mu0 + row] = make_double2(acc[i][j][0][v] - acc[i][j][1][v],
                                                            acc[i][j][NA - 1][v] - acc[i][j][0][v] - acc[i][j][1][v]);
@@ -1107,6 +1122,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
     z.Z = fac ? (const double2*)op.d_zs.p : (const double2*)op.d_Z.p;
     z.tiled = fac ? 1 : 0;
     z.ZW = g.ZW;
+    z.zn = (int64_t)(fac ? op.d_zs.n : op.d_Z.n) / 2;
     zgen::Src zsrc{};
     zsrc.m = t.m; zsrc.p = p; zsrc.L = op.L; zsrc.far_r = t.d_far_r.p; zsrc.far_c = t.d_far_c.p; zsrc.xi = t.d_xi.p;
     zsrc.s = (const double2*)op.d_s.p; zsrc.pivk = op.d_pivk.p; zsrc.pivq = op.d_pivq.p; zsrc.foff = op.d_foff.p;
@@ -1121,7 +1137,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
         const int ncol = std::min(g.TT, g.tb + nd - tc0);
         zgen_tile_kernel<<<std::min(nfar, 148 * 8), 256, kZgenSmem, st>>>(
             zsrc, nfar, op.d_rank.p, op.d_ztoff.p, op.d_local_l.p, op.d_mask, nl, g.tb, tc0, ncol, tile == 0 ? 1 : 0,
-            g.ZW, kZgenSmem / (int)sizeof(double2), (double2*)op.d_zs.p);
+            g.ZW, kZgenSmem / (int)sizeof(double2), (double2*)op.d_zs.p, (int64_t)op.d_zs.n / 2);
         BEM_CK(cudaGetLastError());
       }
       if (g.fk == 8) {
@@ -1132,6 +1148,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
         a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
         a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
         a.z = z; a.xhat = xhat; a.part = (double2*)op.d_part.p; a.mask = op.d_mask;
+        a.part_n = (int64_t)op.d_part.n / 2;
         BEM_CK(dispatch8(f8, p, op.n_segs, a, ntile, st, op.far8_m3));
       } else {
         const Far7Cfg& f7 = g.f7;
@@ -1141,6 +1158,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
         a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
         a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
         a.z = z; a.xhat = xhat; a.part = (double2*)op.d_part.p; a.mask = op.d_mask;
+        a.part_n = (int64_t)op.d_part.n / 2;
         BEM_CK(dispatch7(f7, p, op.n_segs, a, ntile, st));
       }
     }

@@ -322,6 +322,7 @@ __device__ __forceinline__ void stage_small(const double2* __restrict__ A, doubl
         double2 acc = v[0];
 #pragma unroll
         for (int r = 1; r < R; ++r) acc = cfma(acc, v[r], W[((r * k) % R) * rstep]);
+        BEM_DASSERT((base + k * Ns) * NC + c < L * NC);
         B[(base + k * Ns) * NC + c] = acc;
       }
     }
@@ -371,47 +372,9 @@ __device__ __forceinline__ void stage_large(double2* __restrict__ A, double2* __
       idx += k;
       if (idx >= R) idx -= R;
     }
+    BEM_DASSERT((out - A) + (int64_t)(R - k) * Ns * NC < (int64_t)L * NC);
     out[(int64_t)k * Ns * NC] = make_double2(sac - sbd, sad + sbc);
     out[(int64_t)(R - k) * Ns * NC] = make_double2(sac + sbd, sbc - sad);
-  }
-}
-
-// prime radix 11 <= R <= 23 with the butterfly in registers: one thread per (j, column)
-// loads its R twiddled inputs once and forms every output pair (k, R - k) from them
-// (the roots are shared-memory broadcasts); A -> B like the small stages.
-template <int R>
-__device__ __forceinline__ void stage_prime_reg(const double2* __restrict__ A, double2* __restrict__ B, int L, int Ns,
-                                                int NC, const double2* __restrict__ W) {
-  const int T = L / R, tstep = L / (Ns * R), rstep = L / R;
-  for (int it = threadIdx.x; it < T * NC; it += blockDim.x) {
-    const int j = it / NC, c = it - j * NC;
-    const int jm = j % Ns;
-    double2 v[R];
-    v[0] = A[j * NC + c];
-#pragma unroll
-    for (int r = 1; r < R; ++r) v[r] = cm(A[(j + r * T) * NC + c], W[jm * r * tstep]);
-    double2* out = B + ((j - jm) * R + jm) * NC + c;
-    double2 s0 = v[0];
-#pragma unroll
-    for (int r = 1; r < R; ++r) { s0.x += v[r].x; s0.y += v[r].y; }
-    out[0] = s0;
-#pragma unroll 1
-    for (int k = 1; k <= R / 2; ++k) {
-      double sac = v[0].x, sbd = 0.0, sad = 0.0, sbc = v[0].y;
-      int idx = k;
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        const double2 w = W[idx * rstep];
-        sac = fma(v[r].x, w.x, sac);
-        sbd = fma(v[r].y, w.y, sbd);
-        sad = fma(v[r].x, w.y, sad);
-        sbc = fma(v[r].y, w.x, sbc);
-        idx += k;
-        if (idx >= R) idx -= R;
-      }
-      out[(int64_t)k * Ns * NC] = make_double2(sac - sbd, sad + sbc);
-      out[(int64_t)(R - k) * Ns * NC] = make_double2(sac + sbd, sbc - sad);
-    }
   }
 }
 
@@ -432,6 +395,7 @@ __device__ __forceinline__ void stockham_body(const K4Args& a, const double2* co
       v = row[c0 + c];
       if (!a.inverse) { const double sc = a.scale[n]; v.x *= sc; v.y *= sc; }
     }
+    BEM_DASSERT(idx < L * NC);
     A[idx] = v;
   }
   __syncthreads();
@@ -444,14 +408,9 @@ __device__ __forceinline__ void stockham_body(const K4Args& a, const double2* co
       case 4: stage_small<4>(A, B, L, Ns, NC, W); break;
       case 5: stage_small<5>(A, B, L, Ns, NC, W); break;
       case 7: stage_small<7>(A, B, L, Ns, NC, W); break;
-      case 11: stage_prime_reg<11>(A, B, L, Ns, NC, W); break;
-      case 13: stage_prime_reg<13>(A, B, L, Ns, NC, W); break;
-      case 17: stage_prime_reg<17>(A, B, L, Ns, NC, W); break;
-      case 19: stage_prime_reg<19>(A, B, L, Ns, NC, W); break;
-      case 23: stage_prime_reg<23>(A, B, L, Ns, NC, W); break;
       default: stage_large(A, B, L, R, Ns, NC, W); break;
     }
-    if (R <= 23) { double2* t = A; A = B; B = t; }
+    if (R <= 8) { double2* t = A; A = B; B = t; }
     __syncthreads();
     Ns *= R;
   }
@@ -501,8 +460,8 @@ struct RowTab {
   const double2* p[kMaxRows];
 };
 
-__global__ void __launch_bounds__(kFftThreads, 2) stockham_kernel(const K4Args a) { stockham_body(a, nullptr); }
-__global__ void __launch_bounds__(kFftThreads, 2) stockham_rows_kernel(const K4Args a, const __grid_constant__ RowTab tab) {
+__global__ void __launch_bounds__(kFftThreads, 3) stockham_kernel(const K4Args a) { stockham_body(a, nullptr); }
+__global__ void __launch_bounds__(kFftThreads, 3) stockham_rows_kernel(const K4Args a, const __grid_constant__ RowTab tab) {
   stockham_body(a, tab.p);
 }
 __global__ void __launch_bounds__(kFftThreads) bluestein_kernel(const K4Args a) { bluestein_body(a, nullptr); }
@@ -543,6 +502,8 @@ bem_status fft_transform_rows(const double* in, double* out, int64_t M, int N, d
     int NC = 1;
     while (NC < 64 && (size_t)(2 * 2 * NC + 1) * pl->L * 16 <= 74 * 1024) NC *= 2;
     if (NC == 1 && (size_t)5 * pl->L * 16 <= 113 * 1024) NC = 2;  // >= 32-byte row segments (two CTAs per SM)
+    static const int nc_env = [] { const char* e = getenv("BEM_FFT_NC"); return e ? atoi(e) : 0; }();
+    if (nc_env > 0) NC = nc_env;  // tuning experiments
     a.NC = NC;
     smem = sizeof(double2) * ((size_t)2 * NC + 1) * pl->L;
   } else {

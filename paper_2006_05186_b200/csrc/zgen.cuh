@@ -83,6 +83,7 @@ __device__ __forceinline__ void block_columns(const Src& a, int b, int r, int c_
     for (int e = threadIdx.x; e < r * nc; e += blockDim.x) {
       const int i = e / nc, cl = e - i * nc;
       const int l = col_l(c0 + cl);
+      BEM_DASSERT(i * nb + cl < cap && l < a.L);
       work[i * nb + cl] = l >= 0 ? fibre(a, rc, cc, qp[i], l) : make_double2(0.0, 0.0);
     }
     __syncthreads();

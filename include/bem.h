@@ -310,6 +310,13 @@ bem_status bem_debug_fastmath(const double* x, int64_t n, double* exp_out, doubl
  * full assembly takes minutes. */
 bem_status bem_debug_aca_blocks(bem_tree t, const bem_c128* s, int32_t L, double aca_eps, const int32_t* blocks,
                                 int32_t nblk, int32_t* ranks, int32_t* pivots, int64_t* total_rank);
+/* The sharded time-domain step (bem_time_step_sharded) for G ranks in ONE process on one
+ * device: ops[g] holds rank g's frequency shard, x_loc[g] / y_loc[g] rank g's DOF columns
+ * [L][M_g]; the all-to-all exchanges are device copies between the ranks' buffers instead
+ * of NCCL, the packing / unpacking code is the NCCL path's.  Checks the multi-rank
+ * transposes where one GPU is available. */
+bem_status bem_debug_sharded_step(int32_t G, bem_op* ops, const bem_c128* const* x_loc, bem_c128* const* y_loc,
+                                  double R, void* cuda_stream);
 /* FP64 DFMA throughput microbenchmark: returns achieved FLOP/s. */
 bem_status bem_debug_fp64_peak(int32_t device, void* cuda_stream, double* flops_per_s);
 /* mode 0: DFMA loop, 1: FP64 tensor-core mma.sync m8n8k4 loop, 2: both in one CTA. */

@@ -49,7 +49,7 @@ EXPORTS = [
     "bem_ipc_open_handle", "bem_ipc_close", "bem_device_alloc", "bem_device_free", "cqm_solve", "bem_solve_multifreq", "bem_debug_pinned", "bem_debug_fastmath", "bem_debug_fp64_peak",
     "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count", "bem_debug_fp64_peak_ex",
     "bem_op_get_info", "bem_comm_unique_id", "bem_comm_init", "bem_comm_destroy", "bem_shard_frequencies",
-    "bem_time_step_sharded", "bem_debug_aca_blocks",
+    "bem_time_step_sharded", "bem_debug_aca_blocks", "bem_debug_sharded_step",
 ]
 
 
@@ -104,6 +104,7 @@ def lib():
         "bem_shard_frequencies": [i32, i32, vp, vp],
         "bem_time_step_sharded": [vp, vp, vp, i64, d, vp, vp],
         "bem_debug_aca_blocks": [vp, vp, i32, d, vp, i32, vp, vp, vp],
+        "bem_debug_sharded_step": [i32, vp, vp, vp, d, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -490,6 +491,18 @@ def solve_multifreq(op: Operator, g_freq, tol: float = 1e-8, restart: int = 50, 
     if code != 0 and not (code == BEM_ENOCONV and not raise_on_noconv):
         _check(code)
     return phi, {k: getattr(st, k) for k, _ in SolveStats._fields_ if k != "pad_"}
+
+
+def debug_sharded_step(ops, xs, R: float, stream=None):
+    """bem_debug_sharded_step: G virtual ranks in one process (device-copy exchange)."""
+    import torch
+    G = len(ops)
+    oa = (C.c_void_p * G)(*[o.h.value for o in ops])
+    ys = [torch.empty_like(x) for x in xs]
+    xa = (C.c_void_p * G)(*[x.data_ptr() for x in xs])
+    ya = (C.c_void_p * G)(*[y.data_ptr() for y in ys])
+    _check(lib().bem_debug_sharded_step(G, oa, xa, ya, float(R), _stream(stream)))
+    return ys
 
 
 def debug_aca_blocks(tree: Tree, s, eps: float, blocks):

@@ -618,6 +618,7 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   if (const char* e = getenv("BEM_FAR_KERNEL")) op.far_kernel = atoi(e);
   if (const char* e = getenv("BEM_FAR8_KC")) op.far8_kc = atoi(e);
   if (const char* e = getenv("BEM_FAR8_M3")) op.far8_m3 = atoi(e) != 0;
+  if (const char* e = getenv("BEM_FAR8_DT")) op.far8_dt = atoi(e) != 0;
   if (const char* e = getenv("BEM_SOLVE_MASK")) op.use_solve_mask = atoi(e) != 0;
   auto fail = [&](bem_status stt) { delete h; return stt; };
   std::vector<double> sh(2 * (size_t)L);

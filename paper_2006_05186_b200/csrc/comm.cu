@@ -207,29 +207,64 @@ void shard_ws_release(const Op* op) {
   }
 }
 
+// The two transposes, split into the per-rank packing steps and the exchange, so that the
+// NCCL path and the single-process check (bem_debug_sharded_step) share the packing code.
+// forward, rank g: K4 over this rank's DOF columns, frequency row l stored into its slot
+// (owner(l), slot(l)) of the packed send buffer
+static bem_status fwd_pack(ShardWs* w, const double* x_time, double R, cudaStream_t st) {
+  return fft_transform_rows(x_time, nullptr, w->Mg, w->L - 1, R, false, st, w->fwd_rows.data(), 2);
+}
+// forward exchange: rank g's chunk for h = rows cumL[h].. of its send buffer ([L_h][M_g]);
+// rank h stores it at cumM[g] * L_h in its receive buffer
+static double* fwd_send_chunk(ShardWs* w, int h) { return w->send.p + (size_t)w->cumL[h] * w->Mg * 2; }
+static size_t fwd_chunk_n(ShardWs* from, ShardWs* to) { return (size_t)to->Lh[to->rank] * from->Mg * 2; }
+static double* fwd_recv_chunk(ShardWs* w, int g) { return w->recv.p + (size_t)w->cumM[g] * w->Lh[w->rank] * 2; }
+// forward unpack: [L_g][M_h] chunks -> columns [b_h, b_h + M_h) of the [L_g][M] frequency shard
+static bem_status fwd_unpack(ShardWs* w, cudaStream_t st) {
+  const int g = w->rank;
+  for (int h = 0; h < w->G; ++h)
+    if (w->Mh[h] > 0 && w->Lh[g] > 0)
+      BEM_CK(cudaMemcpy2DAsync(w->xf.p + (size_t)w->bh[h] * 2, (size_t)w->M * 16,
+                               w->recv.p + (size_t)w->cumM[h] * w->Lh[g] * 2, (size_t)w->Mh[h] * 16,
+                               (size_t)w->Mh[h] * 16, (size_t)w->Lh[g], cudaMemcpyDeviceToDevice, st));
+  return BEM_OK;
+}
+// inverse pack: columns [b_h, b_h + M_h) of yf -> packed [L_g][M_h] chunk for rank h
+static bem_status inv_pack(ShardWs* w, const double2* yf, cudaStream_t st) {
+  const int g = w->rank;
+  for (int h = 0; h < w->G; ++h)
+    if (w->Mh[h] > 0 && w->Lh[g] > 0)
+      BEM_CK(cudaMemcpy2DAsync(w->send.p + (size_t)w->cumM[h] * w->Lh[g] * 2, (size_t)w->Mh[h] * 16,
+                               (const double*)yf + (size_t)w->bh[h] * 2, (size_t)w->M * 16, (size_t)w->Mh[h] * 16,
+                               (size_t)w->Lh[g], cudaMemcpyDeviceToDevice, st));
+  return BEM_OK;
+}
+static double* inv_send_chunk(ShardWs* w, int h) { return w->send.p + (size_t)w->cumM[h] * w->Lh[w->rank] * 2; }
+static size_t inv_chunk_n(ShardWs* from, ShardWs* to) { return (size_t)from->Lh[from->rank] * to->Mg * 2; }
+static double* inv_recv_chunk(ShardWs* w, int g) { return w->recv.p + (size_t)w->cumL[g] * w->Mg * 2; }
+// inverse unpack: K4 reading frequency row l from its slot of the receive buffer
+static bem_status inv_unpack(ShardWs* w, double* y_time, double R, cudaStream_t st) {
+  return fft_transform_rows(nullptr, y_time, w->Mg, w->L - 1, R, true, st, w->inv_rows.data(), 1);
+}
+
 // x_time [L][M_g] (this rank's DOFs, device) -> xf [L_g][M] (this rank's frequencies)
 bem_status shard_forward(Op& op, bem_comm c, const double* x_time, double R, double2** xf, cudaStream_t st) {
   ShardWs* w = nullptr;
   bem_status rs = shard_ws(op, c, &w);
   if (rs != BEM_OK) return rs;
-  const int N = w->L - 1, G = w->G, g = w->rank;
-  rs = fft_transform_rows(x_time, nullptr, w->Mg, N, R, false, st, w->fwd_rows.data(), 2);  // transform + pack
+  const int G = w->G;
+  rs = fwd_pack(w, x_time, R, st);
   if (rs != BEM_OK) return rs;
   Nccl& n = nccl();
   BEM_NC(n.groupStart());
   for (int h = 0; h < G; ++h) {
-    BEM_NC(n.send(w->send.p + (size_t)w->cumL[h] * w->Mg * 2, (size_t)w->Lh[h] * w->Mg * 2, ncclDouble, h, c->comm, st));
-    BEM_NC(n.recv(w->recv.p + (size_t)w->cumM[h] * w->Lh[g] * 2, (size_t)w->Lh[g] * w->Mh[h] * 2, ncclDouble, h,
-                  c->comm, st));
+    BEM_NC(n.send(fwd_send_chunk(w, h), (size_t)w->Lh[h] * w->Mg * 2, ncclDouble, h, c->comm, st));
+    BEM_NC(n.recv(fwd_recv_chunk(w, h), (size_t)w->Lh[w->rank] * w->Mh[h] * 2, ncclDouble, h, c->comm, st));
   }
   BEM_NC(n.groupEnd());
-  for (int h = 0; h < G; ++h)  // [L_g][M_h] chunk -> columns [b_h, b_h + M_h) of the frequency shard
-    if (w->Mh[h] > 0 && w->Lh[g] > 0)
-      BEM_CK(cudaMemcpy2DAsync(w->xf.p + (size_t)w->bh[h] * 2, (size_t)w->M * 16,
-                               w->recv.p + (size_t)w->cumM[h] * w->Lh[g] * 2, (size_t)w->Mh[h] * 16,
-                               (size_t)w->Mh[h] * 16, (size_t)w->Lh[g], cudaMemcpyDeviceToDevice, st));
+  rs = fwd_unpack(w, st);
   *xf = (double2*)w->xf.p;
-  return BEM_OK;
+  return rs;
 }
 
 // yf [L_g][M] (this rank's frequencies) -> y_time [L][M_g] (this rank's DOFs)
@@ -237,21 +272,53 @@ bem_status shard_inverse(Op& op, bem_comm c, const double2* yf, double R, double
   ShardWs* w = nullptr;
   bem_status rs = shard_ws(op, c, &w);
   if (rs != BEM_OK) return rs;
-  const int N = w->L - 1, G = w->G, g = w->rank;
-  for (int h = 0; h < G; ++h)  // columns [b_h, b_h + M_h) -> packed [L_g][M_h] chunk for rank h
-    if (w->Mh[h] > 0 && w->Lh[g] > 0)
-      BEM_CK(cudaMemcpy2DAsync(w->send.p + (size_t)w->cumM[h] * w->Lh[g] * 2, (size_t)w->Mh[h] * 16,
-                               (const double*)yf + (size_t)w->bh[h] * 2, (size_t)w->M * 16, (size_t)w->Mh[h] * 16,
-                               (size_t)w->Lh[g], cudaMemcpyDeviceToDevice, st));
+  const int G = w->G;
+  rs = inv_pack(w, yf, st);
+  if (rs != BEM_OK) return rs;
   Nccl& n = nccl();
   BEM_NC(n.groupStart());
   for (int h = 0; h < G; ++h) {
-    BEM_NC(n.send(w->send.p + (size_t)w->cumM[h] * w->Lh[g] * 2, (size_t)w->Lh[g] * w->Mh[h] * 2, ncclDouble, h,
-                  c->comm, st));
-    BEM_NC(n.recv(w->recv.p + (size_t)w->cumL[h] * w->Mg * 2, (size_t)w->Lh[h] * w->Mg * 2, ncclDouble, h, c->comm, st));
+    BEM_NC(n.send(inv_send_chunk(w, h), (size_t)w->Lh[w->rank] * w->Mh[h] * 2, ncclDouble, h, c->comm, st));
+    BEM_NC(n.recv(inv_recv_chunk(w, h), (size_t)w->Lh[h] * w->Mg * 2, ncclDouble, h, c->comm, st));
   }
   BEM_NC(n.groupEnd());
-  return fft_transform_rows(nullptr, y_time, w->Mg, N, R, true, st, w->inv_rows.data(), 1);  // unpack + transform
+  return inv_unpack(w, y_time, R, st);
+}
+
+// G ranks in one process on one device, the exchange done by device copies instead of
+// NCCL (same packing code): the multi-rank transposes checked where only one GPU exists.
+bem_status sharded_step_virtual(int G, Op** ops, const double* const* x, double* const* y, double R,
+                                cudaStream_t st) {
+  std::vector<bem_comm_s> cs(G);
+  std::vector<ShardWs*> w(G, nullptr);
+  for (int g = 0; g < G; ++g) {
+    cs[g].nranks = G; cs[g].rank = g; cs[g].device = ops[g]->tree->device;
+    bem_status rs = shard_ws(*ops[g], &cs[g], &w[g]);
+    if (rs != BEM_OK) return rs;
+  }
+  for (int g = 0; g < G; ++g) {
+    bem_status rs = fwd_pack(w[g], x[g], R, st);
+    if (rs != BEM_OK) return rs;
+  }
+  for (int g = 0; g < G; ++g)
+    for (int h = 0; h < G; ++h)
+      BEM_CK(cudaMemcpyAsync(fwd_recv_chunk(w[h], g), fwd_send_chunk(w[g], h), fwd_chunk_n(w[g], w[h]) * 8,
+                             cudaMemcpyDeviceToDevice, st));
+  for (int g = 0; g < G; ++g) {
+    bem_status rs = fwd_unpack(w[g], st);
+    if (rs == BEM_OK) rs = apply_launch(*ops[g], w[g]->xf.p, w[g]->yf.p, st);
+    if (rs == BEM_OK) rs = inv_pack(w[g], (const double2*)w[g]->yf.p, st);
+    if (rs != BEM_OK) return rs;
+  }
+  for (int g = 0; g < G; ++g)
+    for (int h = 0; h < G; ++h)
+      BEM_CK(cudaMemcpyAsync(inv_recv_chunk(w[h], g), inv_send_chunk(w[g], h), inv_chunk_n(w[g], w[h]) * 8,
+                             cudaMemcpyDeviceToDevice, st));
+  for (int g = 0; g < G; ++g) {
+    bem_status rs = inv_unpack(w[g], y[g], R, st);
+    if (rs != BEM_OK) return rs;
+  }
+  return BEM_OK;
 }
 
 bem_status shard_yf(Op& op, bem_comm c, double2** yf) {
@@ -360,4 +427,21 @@ extern "C" bem_status bem_time_step_sharded(bem_op oh, const bem_c128* x_loc, be
   if (rs == BEM_OK) rs = apply_launch(op, (const double*)xf, (double*)yf, st);
   if (rs == BEM_OK) rs = shard_inverse(op, c, yf, R, (double*)y_loc, st);
   return rs;
+}
+
+extern "C" bem_status bem_debug_sharded_step(int32_t G, bem_op* ops, const bem_c128* const* x_loc,
+                                             bem_c128* const* y_loc, double R, void* cuda_stream) {
+  BEM_REQ(G >= 1 && ops && x_loc && y_loc, "bem_debug_sharded_step: bad arguments");
+  std::vector<Op*> o(G);
+  std::vector<const double*> x(G);
+  std::vector<double*> y(G);
+  for (int g = 0; g < G; ++g) {
+    BEM_REQ(ops[g] && x_loc[g] && y_loc[g], "bem_debug_sharded_step: NULL entry %d", g);
+    o[g] = &ops[g]->o;
+    BEM_REQ(o[g]->tree->device == o[0]->tree->device, "bem_debug_sharded_step: ops on different devices");
+    x[g] = (const double*)x_loc[g];
+    y[g] = (double*)y_loc[g];
+  }
+  DeviceGuard dg(o[0]->tree->device);
+  return sharded_step_virtual(G, o.data(), x.data(), y.data(), R, (cudaStream_t)cuda_stream);
 }

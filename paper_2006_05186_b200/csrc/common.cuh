@@ -222,6 +222,7 @@ struct Op {
   size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM
   int far8_kc = 0;                    // far8 nu-chunk width (0: automatic)
   bool far8_m3 = true;                // far8: 3M complex products at 16-row mu chunks (env BEM_FAR8_M3=0: 4M, 32 rows)
+  bool far8_dt = true;                // far8 3M: per-block (r, 1/4 pi r) table in shared memory (env BEM_FAR8_DT=0: off)
   int aca_ctas_per_sm = 5;            // persistent ACA CTAs per SM = register-limited residency (r01: 4 -> 5 cut config-4 setup 2.96 -> 2.64 s)
   int h2o_fc = 0;                     // K3' classes per CTA tile (0: 6 for p <= 32, else 2)
   // optional per-local-frequency mask (1 = compute); set only by the GMRES driver so that

@@ -78,6 +78,20 @@ __device__ __forceinline__ double2 kern_rs(double d2, double2 s, const double* e
   return make_double2(e * cs, -e * sn);
 }
 
+// the same value from a precomputed (r, 1/(4 pi r)) pair (kern_rs' own intermediates:
+// bit-identical slice entries)
+__device__ __forceinline__ double2 kern_tab(double2 rw, double2 s, const double* etab, const double2* sctab) {
+  const double e = fast::exp_neg_tab(-s.x * rw.x, etab) * rw.y;
+  double sn, cs;
+  fast::sincos_tab(s.y * rw.x, sctab, &sn, &cs);
+  return make_double2(e * cs, -e * sn);
+}
+
+__device__ __forceinline__ double2 dist_pair(double d2) {
+  const double ir = rsqrt(d2);
+  return make_double2(d2 * ir, ir * 0.079577471545947667884);  // (r, 1/(4 pi r)) as kern_rs
+}
+
 // Where the coefficients Z_b[j, t] come from: the stored pool ([r_b][nl] at zoff[b]) or
 // the current frequency tile's buffer ([r_b][ZW] at ztoff[b]: leftover columns [0, tb)
 // then the tile's DMMA columns; factors-only skeleton).
@@ -450,7 +464,9 @@ struct Far8Args {
 // M3: three real DMMA products per complex one (P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi);
 // Re = P1 - P2, Im = P3 - P1 - P2): 25 % fewer DMMAs for a third accumulator, which fits
 // at NJ = 2 (16-row mu chunks); the real slice S_b(s_0) takes P1 and P3 only.
-template <int MT, int NJ, int REM, bool M3 = false>
+// DT: the block's (r, 1/(4 pi r)) table [RW][p] in shared memory, computed once per block,
+// so the per-term slice regeneration skips the distance (rsqrt) work.
+template <int MT, int NJ, int REM, bool M3 = false, bool DT = false>
 __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
   constexpr int RW = NJ * 8 + REM;  // mu rows per CTA
   constexpr int NA = M3 ? 3 : 2;    // accumulators per (tile, mu tile)
@@ -472,6 +488,7 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
   double* etab = (double*)(sctab + 64);               // 64
   double* xr = etab + 64;                             // 96
   double* xcn = xr + 96;                              // 3p
+  double2* dtab = (double2*)(((uintptr_t)(xcn + 3 * p) + 15) & ~(uintptr_t)15);  // DT: [RW][p]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
   for (int i = tid; i < 2 * RW * SST + KC * XTP; i += blockDim.x) sm[i] = make_double2(0.0, 0.0);
@@ -521,7 +538,17 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
     const double2 *zD, *zL;
     int zst;
     zrows(a.z, b, a.nl, tb, tc0, zD, zL, zst);
-    for (int i = tid; i < p; i += blockDim.x) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
+    if constexpr (DT) {
+      for (int e = tid; e < nrow * p; e += blockDim.x) {
+        const int i = e / p, nu = e - i * p;
+        double cn[3];
+        node(a.xi + (int64_t)c * 3 * m, m, nu, cn);
+        const double dx = cn[0] - xr[3 * i], dy = cn[1] - xr[3 * i + 1], dz = cn[2] - xr[3 * i + 2];
+        dtab[e] = dist_pair(dx * dx + dy * dy + dz * dz);
+      }
+    } else {
+      for (int i = tid; i < p; i += blockDim.x) node(a.xi + (int64_t)c * 3 * m, m, i, xcn + 3 * i);
+    }
     for (int k0c = 0; k0c < p; k0c += KC) {
       const int kw = min(KC, p - k0c);          // real nu in this chunk
       const int kw4 = (kw + 3) & ~3;            // k-steps cover kw4 (padding rows/cols are zero)
@@ -548,17 +575,20 @@ __global__ void __launch_bounds__(256, 2) far8_kernel(Far8Args a) {
           const int tt = warp + 8 * i;
           const int t = tc0 + tt * 8 + g;
           BEM_DASSERT(!(tt < ntile && t < a.nl) || (Zl + t >= a.z.Z && Zl + t < a.z.Z + a.z.zn));
-          BEM_DASSERT(!(tt < ntile && t < a.nl) || (Zl + t >= a.z.Z && Zl + t < a.z.Z + a.z.zn));
-        zt[i] = (tt < ntile && t < a.nl) ? Zl[t] : make_double2(0.0, 0.0);
+          zt[i] = (tt < ntile && t < a.nl) ? Zl[t] : make_double2(0.0, 0.0);
         }
         for (int e = tid; e < nrow * KC; e += blockDim.x) {
           const int i = e / KC, nu = e - i * KC;
           double2 v = make_double2(0.0, 0.0);
           if (nu < kw) {
             const int nn = k0c + nu;
-            const double dx = xcn[3 * nn] - xr[3 * i], dy = xcn[3 * nn + 1] - xr[3 * i + 1],
-                         dz = xcn[3 * nn + 2] - xr[3 * i + 2];
-            v = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab, sctab);
+            if constexpr (DT) {
+              v = kern_tab(dtab[i * p + nn], sv, etab, sctab);
+            } else {
+              const double dx = xcn[3 * nn] - xr[3 * i], dy = xcn[3 * nn + 1] - xr[3 * i + 1],
+                           dz = xcn[3 * nn + 2] - xr[3 * i + 2];
+              v = kern_rs(dx * dx + dy * dy + dz * dz, sv, etab, sctab);
+            }
           }
           BEM_DASSERT(i < RW && nu < SST);
           S[i * SST + nu] = v;
@@ -738,21 +768,28 @@ Far8Cfg choose8(int p, int nl, size_t cap, int kc_req) {
   return Far8Cfg{};
 }
 
-template <int MT, int NJ, int REM, bool M3 = false>
+template <int MT, int NJ, int REM, bool M3 = false, bool DT = false>
 cudaError_t launch8(const Far8Cfg& c, int nseg, const Far8Args& a, int ntile, cudaStream_t st) {
-  auto k = far8_kernel<MT, NJ, REM, M3>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  auto k = far8_kernel<MT, NJ, REM, M3, DT>;
+  const size_t smem = c.smem + (DT ? sizeof(double2) * ((size_t)(NJ * 8 + REM) * a.p + 1) : 0);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   Far8Args a2 = a;
   a2.nch = (a.p + NJ * 8 + REM - 1) / (NJ * 8 + REM);  // mu chunks of NJ * 8 + REM rows
-  k<<<dim3((unsigned)(nseg * a2.nch), (unsigned)ntile, 1u), 256, c.smem, st>>>(a2);
+  k<<<dim3((unsigned)(nseg * a2.nch), (unsigned)ntile, 1u), 256, smem, st>>>(a2);
   return cudaGetLastError();
 }
 
 cudaError_t dispatch8(const Far8Cfg& c, int p, int nseg, const Far8Args& a, int ntile, cudaStream_t st,
-                      bool m3 = false) {
-  if (m3 && p > 8 && p != 27)
+                      bool m3 = false, bool dt_on = true) {
+  if (m3 && p > 8 && p != 27) {
+    // the (r, 1/(4 pi r)) table when two CTAs per SM still fit (p = 64: +16 KB; not p = 125)
+    const bool dt = c.smem + sizeof(double2) * (16 * (size_t)p + 1) <= 113 * 1024 && dt_on;
+    if (dt)
+      return c.mt == 1 ? launch8<1, 2, 0, true, true>(c, nseg, a, ntile, st)
+                       : launch8<2, 2, 0, true, true>(c, nseg, a, ntile, st);
     return c.mt == 1 ? launch8<1, 2, 0, true>(c, nseg, a, ntile, st) : launch8<2, 2, 0, true>(c, nseg, a, ntile, st);
+  }
   if (p <= 8) return c.mt == 1 ? launch8<1, 1, 0>(c, nseg, a, ntile, st) : launch8<2, 1, 0>(c, nseg, a, ntile, st);
   if (p == 27) return c.mt == 1 ? launch8<1, 3, 3>(c, nseg, a, ntile, st) : launch8<2, 3, 3>(c, nseg, a, ntile, st);
   return c.mt == 1 ? launch8<1, 4, 0>(c, nseg, a, ntile, st) : launch8<2, 4, 0>(c, nseg, a, ntile, st);
@@ -1149,7 +1186,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
         a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
         a.z = z; a.xhat = xhat; a.part = (double2*)op.d_part.p; a.mask = op.d_mask;
         a.part_n = (int64_t)op.d_part.n / 2;
-        BEM_CK(dispatch8(f8, p, op.n_segs, a, ntile, st, op.far8_m3));
+        BEM_CK(dispatch8(f8, p, op.n_segs, a, ntile, st, op.far8_m3, op.far8_dt));
       } else {
         const Far7Cfg& f7 = g.f7;
         Far7Args a;

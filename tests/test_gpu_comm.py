@@ -83,3 +83,31 @@ def test_sharded_solve_one_rank_equals_solve(pb, torch, comm):
     assert sts["iters_max"] == stf["iters_max"] and sts["resid_max"] <= 1e-8
     sc = (R ** np.arange(L))[:, None]
     assert _rel(phs.cpu().numpy() * sc, phf.cpu().numpy() * sc) <= 1e-12
+
+
+@pytest.mark.parametrize("G,m,leaf,N", [(2, 3, 32, 32), (3, 4, 48, 64), (5, 3, 32, 16)])
+def test_virtual_ranks_sharded_step_equals_time_step(pb, torch, G, m, leaf, N):
+    """G ranks in one process (bem_debug_sharded_step): the NCCL path's packing and unpacking
+    code with the all-to-all replaced by device copies, so the G > 1 transposes -- ragged DOF
+    ranges (M = 1280 over 3 and 5 ranks), uneven frequency shards, the conjugate-pair
+    classes -- are checked against the single-device step on the one GPU a box has."""
+    from paper_2006_05186_b200 import bem as B
+    V, T = synth.icosphere(3)
+    M, L = len(T), N + 1
+    R = 10.0 ** (-5.0 / N)
+    s = pb.cqm_frequencies(N, 2.0)
+    tree = pb.Tree(V, T, leaf, 1.0, m)
+    lists = B.shard_frequencies(L, G)
+    assert sorted(np.concatenate(lists).tolist()) == list(range(L))
+    ops = [pb.Operator(tree, s, 1e-6, local_l=lists[g]) for g in range(G)]
+    opf = pb.Operator(tree, s, 1e-6)
+    x = torch.from_numpy(synth.random_time_data(3, N, M).astype(np.complex128)).cuda()
+    rng = [B.dof_range(M, G, g) for g in range(G)]
+    xs = [x[:, b:e].contiguous() for b, e in rng]
+    ys = B.debug_sharded_step(ops, xs, R)
+    yf = opf.time_step(x, R)
+    torch.cuda.synchronize()
+    y = torch.cat(ys, dim=1).cpu().numpy()
+    sc = (R ** np.arange(L))[:, None]
+    assert _rel(y * sc, yf.cpu().numpy() * sc) <= 1e-13
+    assert all(torch.equal(a, b) for a, b in zip(B.debug_sharded_step(ops, xs, R), ys))

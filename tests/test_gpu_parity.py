@@ -262,14 +262,16 @@ def test_edge_cases(pb, torch):
     assert _rel(_apply(pb, torch, op, x), oh.apply(O.MODE_H2ACA, s, x)) <= 1e-10
 
 
-@pytest.mark.parametrize("N,kernel,m3", [(256, "7", "0"), (260, "7", "0"), (256, "8", "0"), (260, "8", "0"),
-                                          (256, "8", "1"), (260, "8", "1")])
-def test_h2aca_p64_multi_tile(pb, torch, N, kernel, m3, monkeypatch):
+@pytest.mark.parametrize("N,kernel,m3,dt", [(256, "7", "0", "1"), (260, "7", "0", "1"), (256, "8", "0", "1"),
+                                             (260, "8", "0", "1"), (256, "8", "1", "1"), (260, "8", "1", "1"),
+                                             (260, "8", "1", "0")])
+def test_h2aca_p64_multi_tile(pb, torch, N, kernel, m3, dt, monkeypatch):
     """p = 64 (m = 4) with L > 128: K3 runs several frequency tiles per
     (segment, mu chunk).  N = 260 (L mod 8 = 5) exercises the zero-padded DMMA
     columns, N = 256 the distributed leftover column.  Oracle on a frequency sample."""
     monkeypatch.setenv("BEM_FAR_KERNEL", kernel)
     monkeypatch.setenv("BEM_FAR8_M3", m3)  # 3M complex products at 16-row mu chunks
+    monkeypatch.setenv("BEM_FAR8_DT", dt)  # per-block distance table in shared memory
     V, T = synth.icosphere(3)
     M, L, eps = len(T), N + 1, 1e-6
     s = pb.cqm_frequencies(N, 2.0)

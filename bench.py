@@ -509,7 +509,7 @@ def main():
         peak = FP64_PEAK_DERIVED / 1e12
         bound, src = "alu", "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §7)"
     achieved = fl / (kt[dom] * 1e-3) / 1e12
-    kname = {"coupling": ("K3 far9 (p > 32) / far7 (p <= 32) coupling kernel (+seg_reduce)" if aca_far
+    kname = {"coupling": ("K3 far8 (p > 32, 3M DMMA) / far7 (p <= 32) coupling kernel (+seg_reduce)" if aca_far
                           else "K3' h2o_kernel (+seg_reduce)"),
              "near": "K1m nearm_kernel" if base_mode == pb.BEM_MODE_COMBINED else "K1 near_kernel"}[dom]
     roof = {"bound": bound, "kernel": kname, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

@@ -413,6 +413,155 @@ __global__ void __launch_bounds__(kPassThreads) down_leaf_d_kernel(const int32_t
   }
 }
 
+// Pipelined leaf products: CTA = (leaf, chunk of FT frequencies).  The leaf's basis tile
+// is staged once and reused for every 16-frequency sub-tile of the chunk; the next
+// sub-tile's coefficients stream in (cp.async, one 16-byte complex per copy, directly
+// into the transposed [k][2t + re/im] layout) while the current one is contracted on the
+// tensor cores.  r2: the one-shot kernels (one sub-tile per CTA) spent most of their time
+// waiting on the staging loads.
+__global__ void __launch_bounds__(kPassThreads) up_leaf_p_kernel(const int32_t* __restrict__ leaves,
+                                                                 const int32_t* __restrict__ cb,
+                                                                 const int32_t* __restrict__ ce,
+                                                                 const double* __restrict__ W,
+                                                                 const double2* __restrict__ xc,
+                                                                 double2* __restrict__ xhat, int64_t M, int nl, int p,
+                                                                 int FT) {
+  extern __shared__ double smd[];
+  const int c = leaves[blockIdx.x];
+  const int b = cb[c], n = ce[c] - b;
+  const int n4 = (n + 3) & ~3;
+  const int f0 = blockIdx.y * FT, f1 = min(nl, f0 + FT);
+  const int WS = pad8(p), XS = pad8(2 * kLeafT);
+  double* Ws = smd;                       // [n4][WS]: W[k][nu]
+  double* X0 = Ws + n4 * WS;              // 2 x [n4][XS]: x[t][k] as X[k][2t + re/im]
+  const size_t xsz = (size_t)n4 * XS;
+  for (int i = threadIdx.x; i < n4 * p; i += blockDim.x) {
+    const int k = i / p, nu = i - k * p;
+    Ws[k * WS + nu] = k < n ? W[(int64_t)(b + k) * p + nu] : 0.0;
+  }
+  auto issue = [&](int t0, double* X) {
+    const int nt = min(kLeafT, f1 - t0);
+    for (int i = threadIdx.x; i < n4 * kLeafT; i += blockDim.x) {
+      const int tl = i / n4, k = i - tl * n4;  // consecutive threads: consecutive panels (coalesced)
+      double* d = X + k * XS + 2 * tl;
+      if (k < n && tl < nt) cp_async16(d, xc + (int64_t)(t0 + tl) * M + b + k);
+      else { d[0] = 0.0; d[1] = 0.0; }
+    }
+    cp_async_commit();
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int nvt = (p + 7) / 8;
+  int buf = 0;
+  if (f0 < f1) issue(f0, X0);
+  for (int t0 = f0; t0 < f1; t0 += kLeafT) {
+    if (t0 + kLeafT < f1) issue(t0 + kLeafT, X0 + (buf ^ 1) * xsz);
+    else cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
+    const double* Xs = X0 + buf * xsz;
+    const int nt = min(kLeafT, f1 - t0);
+    for (int tile = warp; tile < nvt * 4; tile += blockDim.x >> 5) {
+      const int v0 = (tile >> 2) * 8, n0 = (tile & 3) * 8;
+      const int nu = v0 + g;
+      double c0 = 0.0, c1 = 0.0;
+      for (int k0 = 0; k0 < n4; k0 += 4) {
+        const double a = nu < p ? Ws[(k0 + q) * WS + nu] : 0.0;
+        const double bb = Xs[(k0 + q) * XS + n0 + g];
+        dmma_k2(c0, c1, a, bb);
+      }
+      const int tl = (n0 >> 1) + q;
+      if (nu < p && tl < nt) xhat[((int64_t)c * nl + t0 + tl) * p + nu] = make_double2(c0, c1);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+  cp_async_wait1();
+}
+
+__global__ void __launch_bounds__(kPassThreads) down_leaf_p_kernel(const int32_t* __restrict__ leaves,
+                                                                   const int32_t* __restrict__ cb,
+                                                                   const int32_t* __restrict__ ce,
+                                                                   const double* __restrict__ U,
+                                                                   const double2* __restrict__ yhat,
+                                                                   const double2* __restrict__ yc,
+                                                                   const int32_t* __restrict__ perm,
+                                                                   double2* __restrict__ y, int64_t M, int nl, int p,
+                                                                   const double2* __restrict__ xc, double alpha, int FT) {
+  extern __shared__ double smd[];
+  const int c = leaves[blockIdx.x];
+  const int b = cb[c], n = ce[c] - b;
+  const int p4 = (p + 3) & ~3;
+  const int f0 = blockIdx.y * FT, f1 = min(nl, f0 + FT);
+  const int US = pad8(p4), YS = pad8(2 * kLeafT);
+  const int n8 = (n + 7) & ~7;
+  double* Us = smd;              // [n8][US]: U[k][mu]
+  double* Y0 = Us + n8 * US;     // 2 x [p4][YS]: yhat[t][mu] as Y[mu][2t + re/im]
+  const size_t ysz = (size_t)p4 * YS;
+  for (int i = threadIdx.x; i < n8 * p4; i += blockDim.x) {
+    const int k = i / p4, mu = i - k * p4;
+    Us[k * US + mu] = (k < n && mu < p) ? U[(int64_t)(b + k) * p + mu] : 0.0;
+  }
+  auto issue = [&](int t0, double* Y) {
+    const int nt = min(kLeafT, f1 - t0);
+    for (int i = threadIdx.x; i < kLeafT * p4; i += blockDim.x) {
+      const int tl = i / p4, mu = i - tl * p4;
+      double* d = Y + mu * YS + 2 * tl;
+      if (mu < p && tl < nt) cp_async16(d, yhat + ((int64_t)c * nl + t0 + tl) * p + mu);
+      else { d[0] = 0.0; d[1] = 0.0; }
+    }
+    cp_async_commit();
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int nkt = n8 / 8;
+  int buf = 0;
+  if (f0 < f1) issue(f0, Y0);
+  for (int t0 = f0; t0 < f1; t0 += kLeafT) {
+    if (t0 + kLeafT < f1) issue(t0 + kLeafT, Y0 + (buf ^ 1) * ysz);
+    else cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
+    const double* Ys = Y0 + buf * ysz;
+    const int nt = min(kLeafT, f1 - t0);
+    for (int tile = warp; tile < nkt * 4; tile += blockDim.x >> 5) {
+      const int k0r = (tile >> 2) * 8, n0 = (tile & 3) * 8;
+      double c0 = 0.0, c1 = 0.0;
+      for (int m0 = 0; m0 < p4; m0 += 4) {
+        const double a = Us[(k0r + g) * US + m0 + q];
+        const double bb = Ys[(m0 + q) * YS + n0 + g];
+        dmma_k2(c0, c1, a, bb);
+      }
+      const int k = k0r + g, tl = (n0 >> 1) + q;
+      if (k < n && tl < nt) {
+        const int64_t row = (int64_t)(t0 + tl) * M;
+        BEM_DASSERT(b + k < M && perm[b + k] >= 0 && perm[b + k] < M);
+        double2 acc = yc[row + b + k];
+        acc.x += c0;
+        acc.y += c1;
+        if (alpha != 0.0) {
+          const double2 xv = xc[row + b + k];
+          acc.x = fma(alpha, xv.x, acc.x);
+          acc.y = fma(alpha, xv.y, acc.y);
+        }
+        y[row + perm[b + k]] = acc;
+      }
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+  cp_async_wait1();
+}
+
+// frequencies per CTA of the pipelined leaf kernels: about eight 16-frequency sub-tiles
+inline int leaf_chunk(int nl) {
+  const int nsub = (nl + kLeafT - 1) / kLeafT;
+  const int nch = (nsub + 7) / 8;
+  return kLeafT * ((nsub + nch - 1) / nch);
+}
+inline bool leaf_pipe() {
+  static const bool on = [] { const char* e = getenv("BEM_LEAF_PIPE"); return e ? atoi(e) != 0 : true; }();
+  return on;
+}
+
 // Kronecker transfers (tensor Chebyshev interpolation): E = E_z (x) E_y (x) E_x,
 // so E^T x (upward) and E y (downward) are three m x m mode products on the m x m x m
 // coefficient tensor (index mu = mx + m my + m^2 mz): 3 m p multiply-adds per (cluster,
@@ -612,7 +761,13 @@ bem_status run_up(Tree& t, const double* W, const double2* xc, double2* xhat, in
   const int n4 = (t.max_leaf + 3) & ~3;
   const size_t sm_d = sizeof(double) * (size_t)n4 * (pad8(p) + pad8(2 * kLeafT));
   const size_t sm_leaf = sizeof(double2) * kPassT * t.max_leaf + sizeof(double) * (size_t)t.max_leaf * p;
-  if (sm_d <= kLeafSmemMax) {
+  const size_t sm_p = sizeof(double) * (size_t)n4 * (pad8(p) + 2 * pad8(2 * kLeafT));
+  if (leaf_pipe() && sm_p <= kLeafSmemMax) {
+    const int FT = leaf_chunk(nl);
+    BEM_CK(cudaFuncSetAttribute(up_leaf_p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_p));
+    up_leaf_p_kernel<<<dim3((unsigned)t.n_leaves, (unsigned)((nl + FT - 1) / FT)), kPassThreads, sm_p, st>>>(
+        t.d_leaves.p, t.d_begin.p, t.d_end.p, W, xc, xhat, t.M, nl, p, FT);
+  } else if (sm_d <= kLeafSmemMax) {
     BEM_CK(cudaFuncSetAttribute(up_leaf_d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d));
     up_leaf_d_kernel<<<dim3((unsigned)t.n_leaves, (unsigned)((nl + kLeafT - 1) / kLeafT)), kPassThreads, sm_d, st>>>(
         t.d_leaves.p, t.d_begin.p, t.d_end.p, W, xc, xhat, t.M, nl, p);
@@ -686,7 +841,13 @@ bem_status run_down(Tree& t, double2* yhat, const double2* yc, double2* y, int n
   const int p4 = (p + 3) & ~3, n8 = (t.max_leaf + 7) & ~7;
   const size_t sm_d = sizeof(double) * ((size_t)n8 * pad8(p4) + (size_t)p4 * pad8(2 * kLeafT));
   const size_t sm_leaf = sizeof(double2) * kPassT * p + sizeof(double) * (size_t)p * t.max_leaf;
-  if (sm_d <= kLeafSmemMax) {
+  const size_t sm_p = sizeof(double) * ((size_t)n8 * pad8(p4) + 2 * (size_t)p4 * pad8(2 * kLeafT));
+  if (leaf_pipe() && sm_p <= kLeafSmemMax) {
+    const int FT = leaf_chunk(nl);
+    BEM_CK(cudaFuncSetAttribute(down_leaf_p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_p));
+    down_leaf_p_kernel<<<dim3((unsigned)t.n_leaves, (unsigned)((nl + FT - 1) / FT)), kPassThreads, sm_p, st>>>(
+        t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_U.p, yhat, yc, t.d_perm.p, y, t.M, nl, p, xc, alpha, FT);
+  } else if (sm_d <= kLeafSmemMax) {
     BEM_CK(cudaFuncSetAttribute(down_leaf_d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d));
     down_leaf_d_kernel<<<dim3((unsigned)t.n_leaves, (unsigned)((nl + kLeafT - 1) / kLeafT)), kPassThreads, sm_d,
                          st>>>(t.d_leaves.p, t.d_begin.p, t.d_end.p, t.d_U.p, yhat, yc, t.d_perm.p, y, t.M, nl, p, xc,

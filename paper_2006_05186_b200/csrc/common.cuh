@@ -33,6 +33,16 @@ namespace bem {
   } while (0)
 #endif
 
+// Asynchronous 16-byte global -> shared copies (LDGSTS) for the software-pipelined
+// kernels (K4 Stockham, K2 leaf products): the next tile streams in while the current
+// one is computed.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
 // NVTX range over a host scope (stage markers for ncu --nvtx / profilers: the paper's
 // stage timings P:1808-1828 -- tree, ACA, gather, K1, K2, K3, K4, GMRES).  Header-only
 // NVTX v3: a no-op unless a profiler injects itself.

@@ -771,7 +771,11 @@ Far8Cfg choose8(int p, int nl, size_t cap, int kc_req) {
 template <int MT, int NJ, int REM, bool M3 = false, bool DT = false>
 cudaError_t launch8(const Far8Cfg& c, int nseg, const Far8Args& a, int ntile, cudaStream_t st) {
   auto k = far8_kernel<MT, NJ, REM, M3, DT>;
-  const size_t smem = c.smem + (DT ? sizeof(double2) * ((size_t)(NJ * 8 + REM) * a.p + 1) : 0);
+  // choose8 sizes the slice buffers for 32 rows; this instantiation uses RW = NJ * 8 + REM
+  constexpr int RW = NJ * 8 + REM;
+  static_assert(RW <= 32, "far8: at most 32 mu rows per CTA");
+  const size_t smem = c.smem - sizeof(double2) * 2 * (32 - RW) * (size_t)c.SST +
+                      (DT ? sizeof(double2) * ((size_t)RW * a.p + 1) : 0);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   Far8Args a2 = a;
@@ -784,7 +788,8 @@ cudaError_t dispatch8(const Far8Cfg& c, int p, int nseg, const Far8Args& a, int 
                       bool m3 = false, bool dt_on = true) {
   if (m3 && p > 8 && p != 27) {
     // the (r, 1/(4 pi r)) table when two CTAs per SM still fit (p = 64: +16 KB; not p = 125)
-    const bool dt = c.smem + sizeof(double2) * (16 * (size_t)p + 1) <= 113 * 1024 && dt_on;
+    const bool dt = c.smem - sizeof(double2) * 2 * 16 * (size_t)c.SST + sizeof(double2) * (16 * (size_t)p + 1) <=
+                        113 * 1024 && dt_on;
     if (dt)
       return c.mt == 1 ? launch8<1, 2, 0, true, true>(c, nseg, a, ntile, st)
                        : launch8<2, 2, 0, true, true>(c, nseg, a, ntile, st);

@@ -455,6 +455,84 @@ __device__ __forceinline__ void bluestein_body(const K4Args& a, const double2* c
   }
 }
 
+// Persistent, software-pipelined Stockham: each CTA walks column groups blockIdx.x,
+// blockIdx.x + gridDim.x, ...; while a group is transformed in shared memory the next
+// group's [L][NC] tile is already in flight (cp.async, 16-byte elements straight into the
+// second staging buffer), so the HBM reads overlap the butterflies instead of alternating
+// with them (r2: the one-shot kernel was long-scoreboard bound at 1.2 TB/s).
+// Shared memory: In[0], In[1], B ([L][NC] each) and the root table W [L].
+__device__ __forceinline__ void stockham_pipe_body(const K4Args& a, const double2* const* tab) {
+  extern __shared__ double2 sm2[];
+  const int L = a.L, NC = a.NC;
+  const size_t tile = (size_t)L * NC;  // staging buffers at sm2 and sm2 + tile
+  double2* Bw = sm2 + (size_t)2 * L * NC;
+  double2* W = Bw + (size_t)L * NC;
+  const int64_t ngrp = (a.M + NC - 1) / NC;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) W[i] = a.roots[i];
+  auto issue = [&](int64_t grp, double2* dst) {
+    const int64_t c0 = grp * NC;
+    const int nc = (int)min((int64_t)NC, a.M - c0);
+    for (int idx = threadIdx.x; idx < L * NC; idx += blockDim.x) {
+      const int n = idx / NC, c = idx - n * NC;
+      if (c < nc) {
+        const double2* row = a.mode == 1 ? tab[n] : a.in + (int64_t)n * a.M;
+        cp_async16(dst + idx, row + c0 + c);
+      } else {
+        dst[idx] = make_double2(0.0, 0.0);
+      }
+    }
+    cp_async_commit();
+  };
+  int cur = 0;
+  if ((int64_t)blockIdx.x < ngrp) issue(blockIdx.x, sm2);
+  for (int64_t grp = blockIdx.x; grp < ngrp; grp += gridDim.x) {
+    const int64_t nxt = grp + gridDim.x;
+    if (nxt < ngrp) issue(nxt, sm2 + (cur ^ 1) * tile);
+    else cp_async_commit();  // empty group: wait_group 1 below still means "current tile landed"
+    cp_async_wait1();
+    __syncthreads();
+    double2* A = sm2 + cur * tile;
+    double2* B = Bw;
+    if (!a.inverse) {
+      for (int idx = threadIdx.x; idx < L * NC; idx += blockDim.x) {
+        const double sc = a.scale[idx / NC];
+        A[idx].x *= sc;
+        A[idx].y *= sc;
+      }
+      __syncthreads();
+    }
+    int Ns = 1;
+    for (int st = 0; st < a.nst; ++st) {
+      const int R = a.rad[st];
+      switch (R) {
+        case 2: stage_small<2>(A, B, L, Ns, NC, W); break;
+        case 3: stage_small<3>(A, B, L, Ns, NC, W); break;
+        case 4: stage_small<4>(A, B, L, Ns, NC, W); break;
+        case 5: stage_small<5>(A, B, L, Ns, NC, W); break;
+        case 7: stage_small<7>(A, B, L, Ns, NC, W); break;
+        default: stage_large(A, B, L, R, Ns, NC, W); break;
+      }
+      if (R <= 8) { double2* t = A; A = B; B = t; }
+      __syncthreads();
+      Ns *= R;
+    }
+    const int64_t c0 = grp * NC;
+    const int nc = (int)min((int64_t)NC, a.M - c0);
+    for (int idx = threadIdx.x; idx < L * NC; idx += blockDim.x) {
+      const int n = idx / NC, c = idx - n * NC;
+      if (c < nc) {
+        double2 v = A[idx];
+        if (a.inverse) { const double sc = a.scale[n]; v.x *= sc; v.y *= sc; }
+        double2* row = a.mode == 2 ? const_cast<double2*>(tab[n]) : a.out + (int64_t)n * a.M;
+        row[c0 + c] = v;
+      }
+    }
+    __syncthreads();  // In[cur] and B are free before the next iteration refills In[cur]
+    cur ^= 1;
+  }
+  cp_async_wait1();  // nothing outstanding at exit (the trailing group is empty)
+}
+
 constexpr int kMaxRows = 2048;
 struct RowTab {
   const double2* p[kMaxRows];
@@ -463,6 +541,11 @@ struct RowTab {
 __global__ void __launch_bounds__(kFftThreads, 3) stockham_kernel(const K4Args a) { stockham_body(a, nullptr); }
 __global__ void __launch_bounds__(kFftThreads, 3) stockham_rows_kernel(const K4Args a, const __grid_constant__ RowTab tab) {
   stockham_body(a, tab.p);
+}
+__global__ void __launch_bounds__(kFftThreads, 2) stockham_pipe_kernel(const K4Args a) { stockham_pipe_body(a, nullptr); }
+__global__ void __launch_bounds__(kFftThreads, 2) stockham_pipe_rows_kernel(const K4Args a,
+                                                                           const __grid_constant__ RowTab tab) {
+  stockham_pipe_body(a, tab.p);
 }
 __global__ void __launch_bounds__(kFftThreads) bluestein_kernel(const K4Args a) { bluestein_body(a, nullptr); }
 __global__ void __launch_bounds__(kFftThreads) bluestein_rows_kernel(const K4Args a, const __grid_constant__ RowTab tab) {
@@ -493,6 +576,7 @@ bem_status fft_transform_rows(const double* in, double* out, int64_t M, int N, d
     rt = hold.get();
   }
   size_t smem;
+  bool pipe = false;
   if (pl->stock) {
     a.nst = pl->nst;
     for (int i = 0; i < pl->nst; ++i) a.rad[i] = pl->rad[i];
@@ -504,8 +588,15 @@ bem_status fft_transform_rows(const double* in, double* out, int64_t M, int N, d
     if (NC == 1 && (size_t)5 * pl->L * 16 <= 113 * 1024) NC = 2;  // >= 32-byte row segments (two CTAs per SM)
     static const int nc_env = [] { const char* e = getenv("BEM_FFT_NC"); return e ? atoi(e) : 0; }();
     if (nc_env > 0) NC = nc_env;  // tuning experiments
+    // pipelined persistent kernel: three [L][NC] tiles + roots, two CTAs per SM, NC >= 2
+    static const int pipe_env = [] { const char* e = getenv("BEM_FFT_PIPE"); return e ? atoi(e) : 0; }();
+    int NCp = 8;
+    while (NCp > 2 && (size_t)(3 * NCp + 1) * pl->L * 16 > 113 * 1024) NCp /= 2;
+    if (nc_env > 0) NCp = nc_env;
+    pipe = pipe_env != 0 && (size_t)(3 * NCp + 1) * pl->L * 16 <= 113 * 1024;
+    if (pipe) NC = NCp;
     a.NC = NC;
-    smem = sizeof(double2) * ((size_t)2 * NC + 1) * pl->L;
+    smem = sizeof(double2) * ((size_t)(pipe ? 3 : 2) * NC + 1) * pl->L;
   } else {
     static const int nc_elems = [] {  // columns x points per CTA (env BEM_FFT_ELEMS; r01 sweep: 2048 best)
       const char* e = getenv("BEM_FFT_ELEMS");
@@ -517,8 +608,22 @@ bem_status fft_transform_rows(const double* in, double* out, int64_t M, int N, d
     a.hhat = (const double2*)pl->hhat.p; a.tw = (const double2*)pl->tw.p;
     smem = sizeof(double2) * (size_t)a.NC * pl->P;
   }
-  const unsigned grid = (unsigned)((M + a.NC - 1) / a.NC);
-  if (pl->stock) {
+  unsigned grid = (unsigned)((M + a.NC - 1) / a.NC);
+  if (pipe) {
+    auto k = rt ? (void*)stockham_pipe_rows_kernel : (void*)stockham_pipe_kernel;
+    BEM_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    static int nsm = 0;
+    if (nsm == 0) {
+      int dev = 0;
+      BEM_CK(cudaGetDevice(&dev));
+      BEM_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    int per = 0;
+    BEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)k, kFftThreads, smem));
+    grid = std::min<unsigned>(grid, (unsigned)(std::max(per, 1) * nsm));
+    if (rt) stockham_pipe_rows_kernel<<<grid, kFftThreads, smem, st>>>(a, *rt);
+    else stockham_pipe_kernel<<<grid, kFftThreads, smem, st>>>(a);
+  } else if (pl->stock) {
     if (rt) {
       BEM_CK(cudaFuncSetAttribute(stockham_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       stockham_rows_kernel<<<grid, kFftThreads, smem, st>>>(a, *rt);

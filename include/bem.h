@@ -317,6 +317,13 @@ bem_status bem_debug_aca_blocks(bem_tree t, const bem_c128* s, int32_t L, double
  * transposes where one GPU is available. */
 bem_status bem_debug_sharded_step(int32_t G, bem_op* ops, const bem_c128* const* x_loc, bem_c128* const* y_loc,
                                   double R, void* cuda_stream);
+/* One CTA computes D = A B^T on the 5th-generation tensor cores (tcgen05.mma kind::i8,
+ * signed 8-bit operands, 32-bit integer accumulators in tensor memory): A host [128][K],
+ * B host [N][K], D host [128][N] int32; K a multiple of 32 in [32, 512], N a multiple of 16
+ * in [16, 128]; mode 0: A staged in tensor memory, 1: in shared memory.  Pins the operand
+ * layouts of the INT8 coupling kernel (far10) against plain integer arithmetic. */
+bem_status bem_debug_i8_gemm(const int8_t* A, const int8_t* B, int32_t* D, int32_t K, int32_t N, int32_t mode,
+                             int32_t device);
 /* FP64 DFMA throughput microbenchmark: returns achieved FLOP/s. */
 bem_status bem_debug_fp64_peak(int32_t device, void* cuda_stream, double* flops_per_s);
 /* mode 0: DFMA loop, 1: FP64 tensor-core mma.sync m8n8k4 loop, 2: both in one CTA. */

@@ -49,7 +49,7 @@ EXPORTS = [
     "bem_ipc_open_handle", "bem_ipc_close", "bem_device_alloc", "bem_device_free", "cqm_solve", "bem_solve_multifreq", "bem_debug_pinned", "bem_debug_fastmath", "bem_debug_fp64_peak",
     "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count", "bem_debug_fp64_peak_ex",
     "bem_op_get_info", "bem_comm_unique_id", "bem_comm_init", "bem_comm_destroy", "bem_shard_frequencies",
-    "bem_time_step_sharded", "bem_debug_aca_blocks", "bem_debug_sharded_step",
+    "bem_time_step_sharded", "bem_debug_aca_blocks", "bem_debug_sharded_step", "bem_debug_i8_gemm",
 ]
 
 
@@ -105,6 +105,7 @@ def lib():
         "bem_time_step_sharded": [vp, vp, vp, i64, d, vp, vp],
         "bem_debug_aca_blocks": [vp, vp, i32, d, vp, i32, vp, vp, vp],
         "bem_debug_sharded_step": [i32, vp, vp, vp, d, vp],
+        "bem_debug_i8_gemm": [vp, vp, vp, i32, i32, i32, i32],
     }
     for name, args in sig.items():
         f = getattr(L, name)

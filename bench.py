@@ -123,6 +123,17 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def int8_peak_tops():
+    """Dense INT8 tensor peak for a kernel timed inside a long step: the measured sustained bf16
+    GEMM rate (MEASURED_PEAKS.json) x the nominal int8 / bf16 ratio 4.5 / 2.25 = 2."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return 2.0 * float(d.get("bf16_tflops_sustained") or d["bf16_tflops"]), "measured"
+    except Exception:
+        return 2.0 * 1400.0, "fallback"
+
+
 def hbm_peak_gbs():
     """Measured copy bandwidth (MEASURED_PEAKS.json, driver-written), else the guide's fallback."""
     try:
@@ -491,6 +502,14 @@ def main():
         except Exception:
             peaks[name] = None
     dom = "coupling" if kt["coupling"] >= kt["near"] else "near"
+    far_kernel = op.info().get("far_kernel", 0) if aca_far else 0
+    i8 = None
+    if far_kernel == 10:  # far10: 4 real products per complex MAC (re/im embedding) x 21 byte-slice products
+        cmacs = float(op.aca_export()["ranks"].astype(np.float64).sum()) * stats["p"] ** 2 * nl
+        i8_peak, i8_src = int8_peak_tops()
+        i8 = {"ops": 2.0 * 84.0 * cmacs, "peak": i8_peak,
+              "src": (f"{i8_src}: 2 x bf16_tflops_sustained (MEASURED_PEAKS.json; nominal int8/bf16 dense ratio "
+                      "4.5/2.25); K3 runs inside a long step")}
     if dom == "near" and base_mode == pb.BEM_MODE_COMBINED:
         fl = flops_near
         peak = peaks["dmma"] or FP64_PEAK_DERIVED / 1e12
@@ -499,6 +518,10 @@ def main():
         fl = flops_far
         peak = FP64_PEAK_DERIVED / 1e12
         bound, src = "alu", "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §7); 75 flops/evaluation model"
+    elif dom == "coupling" and i8 is not None:
+        fl = i8["ops"]
+        peak = i8["peak"]
+        bound, src = "tensor", i8["src"]
     elif dom == "coupling":
         fl = flops_far
         peak = peaks["dmma"] or FP64_PEAK_DERIVED / 1e12
@@ -509,14 +532,23 @@ def main():
         peak = FP64_PEAK_DERIVED / 1e12
         bound, src = "alu", "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §7)"
     achieved = fl / (kt[dom] * 1e-3) / 1e12
-    kname = {"coupling": ("K3 far8 (p > 32, 3M DMMA) / far7 (p <= 32) coupling kernel (+seg_reduce)" if aca_far
+    kname = {"coupling": (("K3 far10: complex FP64 products emulated on the INT8 tensor cores (tcgen05.mma kind::i8, "
+                           "six-byte slices, 21 slice products; + seg_reduce)") if far_kernel == 10 else
+                          "K3 far8 (p > 32, 3M DMMA) / far7 (p <= 32) coupling kernel (+seg_reduce)" if aca_far
                           else "K3' h2o_kernel (+seg_reduce)"),
              "near": "K1m nearm_kernel" if base_mode == pb.BEM_MODE_COMBINED else "K1 near_kernel"}[dom]
-    roof = {"bound": bound, "kernel": kname, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+    roof = {"bound": bound, "kernel": kname, "achieved": achieved, "peak": peak,
+            "unit": "TOP/s" if (dom == "coupling" and i8 is not None) else "TFLOP/s",
             "frac": achieved / peak, "traffic": traffic_bytes(args.config, dom), "peak_source": src,
             "algorithmic_flops_per_launch": fl,
             "traffic_source": "profiles/traffic.json (ncu --set full dram__bytes_read.sum + dram__bytes_write.sum "
                               "per launch of the same kernel and config)"}
+    if dom == "coupling" and i8 is not None:
+        # the same launch in the method's own arithmetic: 8 FP64 flops per complex MAC (4 for the real slice)
+        fp64_eq = flops_far / (kt["coupling"] * 1e-3) / 1e12
+        roof["algorithmic_int8_ops_per_launch"] = fl
+        roof["fp64_equivalent"] = {"tflops": fp64_eq, "flops_per_launch": flops_far,
+                                   "vs_fp64_tensor_peak": fp64_eq / (peaks["dmma"] or FP64_PEAK_DERIVED / 1e12)}
     # every kernel against its own roofline, and the whole apply
     # T_roof = sum_k max(F_k / P_FP64, B_k / BW) against the measured apply time
     hbm = hbm_peak_gbs()
@@ -531,7 +563,8 @@ def main():
     pk_far = (peaks["dmma"] or FP64_PEAK_DERIVED / 1e12) if aca_far else FP64_PEAK_DERIVED / 1e12
     kern = {
         "near": {"flops": flops_near, "ms": kt["near"], "peak_tflops": pk_near},
-        "coupling": {"flops": flops_far, "ms": kt["coupling"], "peak_tflops": pk_far},
+        "coupling": ({"flops": i8["ops"], "ms": kt["coupling"], "peak_tflops": i8["peak"], "unit": "int8 ops"}
+                     if i8 is not None else {"flops": flops_far, "ms": kt["coupling"], "peak_tflops": pk_far}),
         "up": {"flops": f_up, "bytes": b_up, "ms": kt["up"], "peak_tflops": FP64_PEAK_DERIVED / 1e12,
                "peak_gbs": hbm},
         "down": {"flops": f_up, "bytes": b_down, "ms": kt["down"], "peak_tflops": FP64_PEAK_DERIVED / 1e12,

@@ -146,10 +146,13 @@ bem_status bem_op_destroy(bem_op op); /* NULL-safe */
 /* What an op holds (host struct):  skeleton = 0 (no ACA: H2ONLY / DENSE), 1 (stored Z),
  * 2 (factors only, BEM_SKEL_FACTORS); z_bytes / f_bytes = the stored Z and factor pools;
  * device_bytes = every device allocation the op owns (its per-GPU footprint besides
- * the tree and the caller's x / y). */
+ * the tree and the caller's x / y); far_kernel = the K3 coupling kernel an apply launches:
+ * 10 (far10: FP64 products emulated on the INT8 tensor cores), 8 / 7 (FP64 tensor cores,
+ * mma.sync f64), 0 (generic / plain-H^2 / dense paths). */
 typedef struct {
   int32_t mode, skeleton, n_local, rmax;
   int64_t total_rank, z_bytes, f_bytes, device_bytes;
+  int32_t far_kernel, reserved_;
 } bem_op_info;
 bem_status bem_op_get_info(bem_op op, bem_op_info* out);
 

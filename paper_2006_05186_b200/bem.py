@@ -34,7 +34,7 @@ class TreeStats(C.Structure):
 class OpInfo(C.Structure):
     _fields_ = [("mode", C.c_int32), ("skeleton", C.c_int32), ("n_local", C.c_int32), ("rmax", C.c_int32),
                 ("total_rank", C.c_int64), ("z_bytes", C.c_int64), ("f_bytes", C.c_int64),
-                ("device_bytes", C.c_int64)]
+                ("device_bytes", C.c_int64), ("far_kernel", C.c_int32), ("reserved_", C.c_int32)]
 
 
 class SolveStats(C.Structure):

@@ -876,7 +876,9 @@ extern "C" bem_status bem_op_get_info(bem_op oh, bem_op_info* out) {
                      op.d_rank.n + op.d_pivk.n + op.d_pivq.n + op.d_far_rows.n + op.d_segs.n + op.d_seg_rows.n +
                      op.d_seg_ptr.n + op.d_nrank.n + op.d_npivk.n + op.d_npivq.n + op.d_nm_order.n + op.d_nm_counter.n;
   const size_t i64 = op.d_zoff.n + op.d_foff.n + op.d_ztoff.n + op.d_nzoff.n + op.d_nsoff.n + op.d_fsoff.n + op.d_g0noff.n;
-  out->device_bytes = (int64_t)(8 * dbl + 4 * i32 + 8 * i64);
+  out->device_bytes = (int64_t)(8 * dbl + 4 * i32 + 8 * i64 + 8 * op.d_xmax.n);
+  out->far_kernel = aca ? far_kernel_selected(op) : 0;
+  out->reserved_ = 0;
   return BEM_OK;
 }
 

@@ -226,9 +226,10 @@ struct Op {
   DBuf<double> d_conv_part;  // per-block partial sums of the time-domain convolution  // K1m CTA order: leaf indices by descending sum_b r_b n_c (LPT)
   // workspaces
   DBuf<double> d_xc, d_yc, d_xhat, d_yhat;
+  DBuf<double> d_xmax;  // far10: [C][nl] max_nu |xhat|
   // kernel selection (env BEM_FAR_KERNEL / BEM_FAR8_KC / BEM_FAR_GENERIC, read at assembly: tests)
   bool force_generic = false;
-  int far_kernel = 0;                 // 0: auto (far8 for p > 32, far7 otherwise); 8, 7
+  int far_kernel = 0;                 // 0: auto (far8 for p > 32, far7 otherwise); 8, 7, 10 (INT8 tensor cores)
   size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM
   int far8_kc = 0;                    // far8 nu-chunk width (0: automatic)
   bool far8_m3 = true;                // far8: 3M complex products at 16-row mu chunks (env BEM_FAR8_M3=0: 4M, 32 rows)
@@ -255,6 +256,7 @@ bem_status apply_launch(Op& op, const double* x, double* y, cudaStream_t st, boo
 bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st, bool dl = false);
 bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st);
 bem_status far_prepare(Op& op);  // K3 scratch of the factors-only skeleton (far.cu)
+int far_kernel_selected(const Op& op);  // the K3 kernel an apply launches (10, 8, 7; 0: generic)
 bem_status launch_near_maca(Op& op, const double2* xc, double2* yc, cudaStream_t st);  // nearm.cu
 bem_status h2_gather(Op& op, const double2* x, double2* xc, int ncols, cudaStream_t st);
 bem_status h2_up(Op& op, const double2* xc, double2* xhat, int ncols, cudaStream_t st);

@@ -38,6 +38,7 @@
 #include "common.cuh"
 #include "fastmath.cuh"
 #include "zgen.cuh"
+#include "far_common.cuh"
 
 namespace bem {
 namespace {
@@ -56,12 +57,6 @@ __device__ __forceinline__ double2 kern(double r, double2 s) {
   return make_double2(e * cs, -e * sn);
 }
 
-__device__ __forceinline__ void node(const double* xi, int m, int mu, double* out) {
-  out[0] = xi[mu % m];
-  out[1] = xi[m + (mu / m) % m];
-  out[2] = xi[2 * m + mu / (m * m)];
-}
-
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
@@ -76,44 +71,6 @@ __device__ __forceinline__ double2 kern_rs(double d2, double2 s, const double* e
   double sn, cs;
   fast::sincos_tab(s.y * r, sctab, &sn, &cs);
   return make_double2(e * cs, -e * sn);
-}
-
-// the same value from a precomputed (r, 1/(4 pi r)) pair (kern_rs' own intermediates:
-// bit-identical slice entries)
-__device__ __forceinline__ double2 kern_tab(double2 rw, double2 s, const double* etab, const double2* sctab) {
-  const double e = fast::exp_neg_tab(-s.x * rw.x, etab) * rw.y;
-  double sn, cs;
-  fast::sincos_tab(s.y * rw.x, sctab, &sn, &cs);
-  return make_double2(e * cs, -e * sn);
-}
-
-__device__ __forceinline__ double2 dist_pair(double d2) {
-  const double ir = rsqrt(d2);
-  return make_double2(d2 * ir, ir * 0.079577471545947667884);  // (r, 1/(4 pi r)) as kern_rs
-}
-
-// Where the coefficients Z_b[j, t] come from: the stored pool ([r_b][nl] at zoff[b]) or
-// the current frequency tile's buffer ([r_b][ZW] at ztoff[b]: leftover columns [0, tb)
-// then the tile's DMMA columns; factors-only skeleton).
-struct ZSrc {
-  const int64_t* zoff;
-  const double2* Z;
-  int tiled, ZW;  // tiled: Z = tile buffer, zoff = per-block offsets in it
-  int64_t zn;     // elements of Z (bounds checks)
-};
-
-// Z_b[j, t] = zD[j * stride + t] for the tile's DMMA columns t, zL[j * stride + t] for the
-// leftover columns t < tb.
-__device__ __forceinline__ void zrows(const ZSrc& z, int b, int nl, int tb, int tc0, const double2*& zD,
-                                      const double2*& zL, int& stride) {
-  zL = z.Z + z.zoff[b];
-  if (z.tiled) {
-    zD = zL + (tb - tc0);
-    stride = z.ZW;
-  } else {
-    zD = zL;
-    stride = nl;
-  }
 }
 
 // Factors-only skeleton: the Z columns of one frequency tile for every far block
@@ -1080,7 +1037,7 @@ struct FarGeom {
   int fk = 0;
   Far7Cfg f7;
   Far8Cfg f8;
-  int ntiles = 0, tb = 0, TT = 0, ZW = 0;
+  int ntiles = 0, tb = 0, TT = 0, ZW = 0, nd = 0;
 };
 
 static FarGeom far_geom(const Op& op) {
@@ -1089,24 +1046,41 @@ static FarGeom far_geom(const Op& op) {
   FarGeom g;
   g.fk = op.far_kernel != 0 ? op.far_kernel : (p > 32 ? 8 : 7);  // r01: far8 wins at p = 64, far7 at p = 27
   if (op.force_generic || op.n_segs == 0) { g.fk = 0; return g; }
+  if (g.fk == 10) {
+    // far10 (farq.cu): 128-column frequency tiles, <= 2 leftover columns on the FP64 pipe;
+    // int32 level sums stay exact for ranks <= 160
+    int tb = nl % kFar10Tile;
+    if (tb > 2 || tb == nl) tb = 0;
+    if (p <= 128 && op.rmax <= 160 && nl > tb) {
+      g.tb = tb; g.nd = nl - tb; g.TT = kFar10Tile; g.ntiles = (g.nd + kFar10Tile - 1) / kFar10Tile;
+      g.ZW = g.tb + g.TT;
+      return g;
+    }
+    g.fk = p > 32 ? 8 : 7;
+  }
   if (g.fk == 8) {
     g.f8 = choose8(p, nl, op.far4_smem_cap, op.far8_kc);
-    if (g.f8.mt > 0) { g.ntiles = g.f8.ntiles; g.tb = g.f8.tb; g.TT = g.f8.TT; g.ZW = g.tb + g.TT; return g; }
+    if (g.f8.mt > 0) { g.ntiles = g.f8.ntiles; g.tb = g.f8.tb; g.TT = g.f8.TT; g.ZW = g.tb + g.TT; g.nd = g.f8.nd; return g; }
   } else if (g.fk == 7) {
     g.f7 = choose7(p, nl, op.far4_smem_cap);
-    if (g.f7.mt > 0) { g.ntiles = g.f7.ntiles; g.tb = g.f7.tb; g.TT = g.f7.TT; g.ZW = g.tb + g.TT; return g; }
+    if (g.f7.mt > 0) { g.ntiles = g.f7.ntiles; g.tb = g.f7.tb; g.TT = g.f7.TT; g.ZW = g.tb + g.TT; g.nd = g.f7.nd; return g; }
   }
   g.fk = 0;
   return g;
 }
+
+int far_kernel_selected(const Op& op) { return far_geom(op).fk; }
 
 constexpr int kZgenSmem = 64 * 1024;  // zgen_tile_kernel batch buffer (4096 complex)
 
 // Factors-only skeleton: the tile buffer (sum_b r_b x ZW complex) and its per-block
 // offsets, allocated at assembly so that an apply never allocates (graph capture).
 bem_status far_prepare(Op& op) {
-  if (op.z_stored || op.ranks.empty()) return BEM_OK;
+  if (op.ranks.empty()) return BEM_OK;
+  op.rmax = *std::max_element(op.ranks.begin(), op.ranks.end());
   const FarGeom g = far_geom(op);
+  if (g.fk == 10) BEM_CK(op.d_xmax.alloc((size_t)op.tree->C * op.n_local));
+  if (op.z_stored) return BEM_OK;
   if (g.fk == 0) {
     set_error("bem_assemble_h2_aca: factors-only skeleton needs the tiled coupling kernels (p <= 128)");
     return BEM_EINVAL;
@@ -1175,14 +1149,24 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
       const int ntile = fac ? 1 : g.ntiles;
       if (fac) {
         const int tc0 = g.tb + tile * g.TT;
-        const int nd = g.fk == 7 ? g.f7.nd : g.f8.nd;
+        const int nd = g.nd;
         const int ncol = std::min(g.TT, g.tb + nd - tc0);
         zgen_tile_kernel<<<std::min(nfar, 148 * 8), 256, kZgenSmem, st>>>(
             zsrc, nfar, op.d_rank.p, op.d_ztoff.p, op.d_local_l.p, op.d_mask, nl, g.tb, tc0, ncol, tile == 0 ? 1 : 0,
             g.ZW, kZgenSmem / (int)sizeof(double2), (double2*)op.d_zs.p, (int64_t)op.d_zs.n / 2);
         BEM_CK(cudaGetLastError());
       }
-      if (g.fk == 8) {
+      if (g.fk == 10) {
+        if (tile == 0) BEM_CK(launch_xmax(xhat, (int64_t)t.C * nl, p, op.d_xmax.p, st));
+        Far10Args a;
+        a.nl = nl; a.m = t.m; a.p = p; a.rcap = op.rcap; a.tb = g.tb; a.nd = g.nd; a.tile0 = fac ? tile : 0;
+        a.nch = (p + 31) / 32;
+        a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
+        a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
+        a.z = z; a.xhat = xhat; a.xmax = op.d_xmax.p; a.part = (double2*)op.d_part.p; a.mask = op.d_mask;
+        a.part_n = (int64_t)op.d_part.n / 2;
+        BEM_CK(launch_far10(a, op.n_segs, ntile, st));
+      } else if (g.fk == 8) {
         const Far8Cfg& f8 = g.f8;
         Far8Args a;
         a.nl = nl; a.m = t.m; a.p = p; a.rcap = op.rcap; a.SST = f8.SST; a.TT = f8.TT; a.XTP = f8.XTP;

@@ -327,6 +327,11 @@ bem_status bem_debug_sharded_step(int32_t G, bem_op* ops, const bem_c128* const*
  * layouts of the INT8 coupling kernel (far10) against plain integer arithmetic. */
 bem_status bem_debug_i8_gemm(const int8_t* A, const int8_t* B, int32_t* D, int32_t K, int32_t N, int32_t mode,
                              int32_t device);
+/* tcgen05 kind::i8 issue-rate microbenchmark (far10's MMA pattern: groups of 21 MMAs, M = 128,
+ * K = 32, N in {32, 64, 128, 256}; mode 0: A in tensor memory, 1: A in shared memory): int8 MACs/s over
+ * all SMs and tensor-core cycles per MMA on SM 0. */
+bem_status bem_debug_i8_rate(int32_t N, int32_t mode, int32_t iters, int32_t device, double* macs_per_s,
+                             double* cycles_per_mma);
 /* FP64 DFMA throughput microbenchmark: returns achieved FLOP/s. */
 bem_status bem_debug_fp64_peak(int32_t device, void* cuda_stream, double* flops_per_s);
 /* mode 0: DFMA loop, 1: FP64 tensor-core mma.sync m8n8k4 loop, 2: both in one CTA. */

@@ -41,14 +41,14 @@ constexpr int kQRW = 32;              // mu rows per CTA
 constexpr int kQN = 2 * kQRW;         // MMA N: (mu, Re/Im output part)
 constexpr int kQKC = 16;              // nu per stage (MMA K = 32 bytes)
 constexpr int kQXP = kQT + 2;         // x^ chunk row: tile columns, then <= 2 leftover columns
-constexpr int kQThreads = 256;
+constexpr int kQProd = 512;               // producer threads (16 warps)
+constexpr int kQThreads = kQProd + 32;    // + the MMA-issue warp
 constexpr int kQSl = 6;               // byte slices per operand
 constexpr int kQBSlice = kQN * 32;    // bytes of one B slice tile [64][32]
 constexpr int kQBStage = kQSl * kQBSlice;
 constexpr uint32_t kQCols = 512;      // TMEM: six level accumulators [0, 384), two A stages [384, 480)
 constexpr uint32_t kQAcol = 384;
 constexpr uint32_t kQIdesc = tc::idesc_i8(kQT, kQN);
-constexpr unsigned long long kQBias = 0x808080808080ull;
 constexpr size_t kQMinSmem = 116 * 1024;  // one CTA per SM (it owns all 512 TMEM columns)
 
 // canonical K-major no-swizzle offset of (n, k) in a [64][32] int8 tile: 8-row x 16-byte
@@ -57,43 +57,64 @@ __device__ __forceinline__ uint32_t boff(int n, int k) {
   return (uint32_t)((n >> 3) * 256 + (k >> 4) * 128 + (n & 7) * 16 + (k & 15));
 }
 
-// balanced digit SI (0 = most significant of six) of four biased 48-bit values, packed
-// little-endian into one word of signed bytes
-template <int SI>
-__device__ __forceinline__ uint32_t pack4(uint64_t w0, uint64_t w1, uint64_t w2, uint64_t w3) {
-  constexpr int byte = 5 - SI;
-  constexpr uint32_t bsel = byte & 3;
-  const uint32_t a0 = byte >= 4 ? (uint32_t)(w0 >> 32) : (uint32_t)w0;
-  const uint32_t a1 = byte >= 4 ? (uint32_t)(w1 >> 32) : (uint32_t)w1;
-  const uint32_t a2 = byte >= 4 ? (uint32_t)(w2 >> 32) : (uint32_t)w2;
-  const uint32_t a3 = byte >= 4 ? (uint32_t)(w3 >> 32) : (uint32_t)w3;
-  const uint32_t lo = __byte_perm(a0, a1, bsel | ((bsel + 4) << 4));
-  const uint32_t hi = __byte_perm(a2, a3, bsel | ((bsel + 4) << 4));
-  return __byte_perm(lo, hi, 0x5410) ^ 0x80808080u;
+// Fixed-point conversion on the FP64 pipe: for |v| < 2^47, v + kQMagic (= 1.5 2^52 + C,
+// C = 0x808080808080) rounds v to the nearest integer and leaves C + v in the low 48 bits
+// of the double (exponent fixed), so bytes 0..5 of the bit pattern are the biased digits
+// (digit_i = byte_i - 128, i.e. byte_i ^ 0x80 read as a signed byte).
+constexpr double kQMagic = 6896688841130112.0;  // 1.5 * 2^52 + 0x808080808080
+
+// 4 x 4 byte transpose of the low words of four digit carriers: out[b] = byte b of (a, b, c, d)
+// packed little-endian, as balanced signed digits (slice 5 - b); hi words give slices 1, 0
+__device__ __forceinline__ void tr_lo(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t (&o)[4]) {
+  const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(c, d, 0x5140);
+  const uint32_t t2 = __byte_perm(a, b, 0x7362), t3 = __byte_perm(c, d, 0x7362);
+  o[0] = __byte_perm(t0, t1, 0x5410) ^ 0x80808080u;
+  o[1] = __byte_perm(t0, t1, 0x7632) ^ 0x80808080u;
+  o[2] = __byte_perm(t2, t3, 0x5410) ^ 0x80808080u;
+  o[3] = __byte_perm(t2, t3, 0x7632) ^ 0x80808080u;
+}
+__device__ __forceinline__ void tr_hi(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t (&o)[2]) {
+  const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(c, d, 0x5140);
+  o[0] = __byte_perm(t0, t1, 0x5410) ^ 0x80808080u;
+  o[1] = __byte_perm(t0, t1, 0x7632) ^ 0x80808080u;
 }
 
-__device__ __forceinline__ uint64_t biased(double v) {
-  return (uint64_t)__double2ll_rn(v) + kQBias;
+// the slice entry's modulus and phase factors (kern_tab's intermediates): S = e (cs, -sn)
+__device__ __forceinline__ void kern_parts(double2 rw, double2 s, const double* etab, const double2* sctab, double& e,
+                                           double& sn, double& cs) {
+  e = fast::exp_neg_tab(-s.x * rw.x, etab) * rw.y;
+  fast::sincos_tab(s.y * rw.x, sctab, &sn, &cs);
 }
 
 __device__ __forceinline__ double kmag(double r, double sre, const double* etab) {  // |e^{-s r}| / (4 pi r)
   return (sre >= 0.0 ? fast::exp_neg_tab(-sre * r, etab) : exp(-sre * r)) * (0.079577471545947667884 / r);
 }
 
+__device__ __forceinline__ void prod_sync() {  // the producer warps only (named barrier 1)
+  asm volatile("bar.sync 1, %0;" ::"n"(kQProd) : "memory");
+}
+__device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool ok) {  // zero-fill when !ok
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) {
   extern __shared__ __align__(1024) uint8_t smq[];
   __shared__ uint32_t taddr_s;
-  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ __align__(8) uint64_t full[2], empty[2], drained;
   __shared__ double etab[64];
   __shared__ double2 sctab[64];
   __shared__ double xr[3 * kQRW];
   __shared__ double ascl[kQT], oscl[kQT];
-  __shared__ double redmin[kQThreads / 32], redmax[kQThreads / 32];
+  __shared__ double zred[kQProd / kQT][kQT];
+  __shared__ double redmin[kQProd / 32], redmax[kQProd / 32];
   const int p = a.p, m = a.m;
   uint8_t* sB = smq;                                          // 2 x [6][64][32] int8
-  double2* xs = (double2*)(smq + 2 * kQBStage);               // [16][kQXP]
-  double2* dtab = xs + kQKC * kQXP;                           // [32][p] (r, 1/(4 pi r))
-  double* sig = (double*)(dtab + (size_t)kQRW * p);           // [rcap] sigma_j
+  double2* xsb = (double2*)(smq + 2 * kQBStage);              // 2 x [16][kQXP]
+  double2* dtab = xsb + 2 * kQKC * kQXP;                      // [32][p] (r, 1/(4 pi r))
+  double2* svs = dtab + (size_t)kQRW * p;                     // [rcap] pivot frequencies s_{k_j}
+  double* sig = (double*)(svs + a.rcap);                      // [rcap] sigma_j
   double* isig = sig + a.rcap;                                // [rcap] 2^46 / sigma_j
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int4 sg = a.segs[blockIdx.x / a.nch];
@@ -105,6 +126,7 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
   const int ntb = lead ? a.tb : 0;  // leftover columns (FP64 path) handled by this CTA
   const int mu0 = (blockIdx.x % a.nch) * kQRW;
   const int nrow = min(kQRW, p - mu0);
+  const int nkc = (p + kQKC - 1) / kQKC;  // nu chunks per term
   for (int i = tid; i < 64; i += kQThreads) {
     etab[i] = fast::kExp2Tab[i];
     sctab[i] = fast::kSinCosTab[i];
@@ -112,193 +134,70 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
   for (int i = tid; i < nrow; i += kQThreads) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
   if (warp == 0) tc::tmem_alloc(&taddr_s, kQCols);
   if (tid == 0) {
-    tc::mbar_init(&mbar[0], 1);
-    tc::mbar_init(&mbar[1], 1);
+    tc::mbar_init(&full[0], kQProd);
+    tc::mbar_init(&full[1], kQProd);
+    tc::mbar_init(&empty[0], 1);
+    tc::mbar_init(&empty[1], 1);
+    tc::mbar_init(&drained, kQProd);
   }
-  tc::fence_before();
-  __syncthreads();
+  // producer roles: A / readout (frequency column t_l, quarter q4: nu 4 q4 .. 4 q4 + 3 of a
+  // stage, accumulator columns 16 q4 .. 16 q4 + 15 = rows mu 8 q4 .. 8 q4 + 7); B (slice entry
+  // (bmu, bnu) of a stage)
+  const int t_l = tid & (kQT - 1), q4 = (tid >> 7) & 3;
+  const int tg = tc0 + t_l;
+  const bool tv = tid < kQProd && t_l < ncol && tg < a.nl && (a.mask == nullptr || a.mask[tg]);
+  const int bmu = (tid >> 4) & 31, bnu = tid & 15;
+  const bool cta_on = __syncthreads_or(tv || (lead && tid < a.tb && (a.mask == nullptr || a.mask[tid]))) != 0;
   tc::fence_after();
   const uint32_t tD = taddr_s, tA0 = taddr_s + kQAcol;
-  const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-  // A producer / readout: frequency column t_l of the tile, half hh (nu 8hh.. / columns 32hh..)
-  const int t_l = tid & (kQT - 1), hh = tid >> 7;
-  const int tg = tc0 + t_l;
-  const bool tv = t_l < ncol && tg < a.nl && (a.mask == nullptr || a.mask[tg]);
-  // B producer: mu row bmu, nu pair (2 bq, 2 bq + 1) of the stage
-  const int bmu = tid >> 3, bq = tid & 7;
-  const bool cta_on = __syncthreads_or(tv || (lead && tid < a.tb && (a.mask == nullptr || a.mask[tid]))) != 0;
-  double acc[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) acc[i] = 0.0;
-  double2 lacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-  uint32_t stage = 0;
-  for (int bi = sg.y; bi < (cta_on ? sg.z : sg.y); ++bi) {
-    const int b = a.far_sorted[bi];
-    const int rk = a.rank[b];
-    if (rk == 0) continue;
-    const int c = a.far_c[b];
-    const double2* xh = a.xhat + (int64_t)c * a.nl * p;
-    const double2 *zD, *zL;
-    int zst;
-    zrows(a.z, b, a.nl, a.tb, tc0, zD, zL, zst);
-    tc::fence_before();
-    __syncthreads();  // previous block read out; dtab / sig / xs free
-    tc::fence_after();
-    // (1) the block's (r, 1/(4 pi r)) table over this CTA's rows, r_min and r_max
-    double rmn = 1e300, rmx = 0.0;
-    for (int e = tid; e < kQRW * p; e += kQThreads) {
-      const int i = e / p, nu = e - i * p;
-      double2 v = make_double2(1.0, 0.0);
-      if (i < nrow) {
-        double cn[3];
-        node(a.xi + (int64_t)c * 3 * m, m, nu, cn);
-        const double dx = cn[0] - xr[3 * i], dy = cn[1] - xr[3 * i + 1], dz = cn[2] - xr[3 * i + 2];
-        v = dist_pair(dx * dx + dy * dy + dz * dz);
-        rmn = fmin(rmn, v.x);
-        rmx = fmax(rmx, v.x);
-      }
-      dtab[e] = v;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      rmn = fmin(rmn, __shfl_xor_sync(0xffffffffu, rmn, o));
-      rmx = fmax(rmx, __shfl_xor_sync(0xffffffffu, rmx, o));
-    }
-    if (lane == 0) { redmin[warp] = rmn; redmax[warp] = rmx; }
-    __syncthreads();
-    rmn = redmin[0]; rmx = redmax[0];
-#pragma unroll
-    for (int w = 1; w < kQThreads / 32; ++w) { rmn = fmin(rmn, redmin[w]); rmx = fmax(rmx, redmax[w]); }
-    // (2) sigma_j = max |S_j| over the rows (the kernel's modulus is monotone or convex in r)
-    for (int j = tid; j < rk; j += kQThreads) {
-      const double sre = a.s[a.pivk[(int64_t)b * a.rcap + j]].x;
-      const double sgm = fmax(kmag(rmn, sre, etab), kmag(rmx, sre, etab)) * (1.0 + 0x1p-30);
-      sig[j] = sgm;
-      isig[j] = sgm > 0.0 ? 0x1p46 / sgm : 0.0;
-    }
-    __syncthreads();
-    // (3) per column t: A scale 2^(46 - e_t), readout scale 2^e_t
-    if (tid < kQT) {
-      double zm = 0.0;
-      if (tv) {
-        for (int j = 0; j < rk; ++j) {
-          const double2 z = zD[(int64_t)j * zst + tg];
-          zm = fmax(zm, sqrt(fma(z.x, z.x, z.y * z.y)) * sig[j]);
-        }
-      }
-      const double bound = tv ? zm * a.xmax[(int64_t)c * a.nl + tg] : 0.0;
-      int e = 0;
-      if (bound > 0.0) frexp(bound, &e);
-      ascl[tid] = bound > 0.0 ? ldexp(1.0, 46 - e) : 0.0;
-      oscl[tid] = ldexp(1.0, e);
-    }
-    __syncthreads();
-    const double as_t = ascl[t_l];
-    const uint32_t first_stage = stage;
-    // (4) stages: nu chunks (x^ chunk staged once), then the ACA terms
-    for (int k0 = 0; k0 < p; k0 += kQKC) {
-      if (k0 > 0) {
-        tc::fence_before();
-        __syncthreads();  // every thread done with the previous x^ chunk
-        tc::fence_after();
-      }
-      for (int idx = tid; idx < kQXP * kQKC; idx += kQThreads) {
-        const int tl = idx / kQKC, nu = idx - tl * kQKC;
-        int tcol;
-        bool ok;
-        if (tl < kQT) { tcol = tc0 + tl; ok = tl < ncol && tcol < a.nl; }
-        else { tcol = tl - kQT; ok = tcol < ntb; }
-        xs[nu * kQXP + tl] = (ok && k0 + nu < p) ? xh[(int64_t)tcol * p + k0 + nu] : make_double2(0.0, 0.0);
-      }
-      __syncthreads();
-      for (int j = 0; j < rk; ++j, ++stage) {
-        const int buf = stage & 1;
-        if (stage >= 2) tc::mbar_wait(&mbar[buf], ((stage >> 1) - 1) & 1);
-        tc::fence_after();
-        const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + j]];
-        {  // ---- A: column t_l, nu 8hh .. 8hh + 7 -> TMEM lane t_l, columns 4hh .. 4hh + 3 per slice
-          double2 z = tv ? zD[(int64_t)j * zst + tg] : make_double2(0.0, 0.0);
-          const double f = sig[j] * as_t;
-          z.x *= f;
-          z.y *= f;
-          uint64_t wr[8], wi[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const double2 x = xs[(8 * hh + u) * kQXP + t_l];
-            wr[u] = biased(fma(z.x, x.x, -z.y * x.y));
-            wi[u] = biased(fma(z.x, x.y, z.y * x.x));
-          }
-          const uint32_t ta = tA0 + (uint32_t)buf * 48 + lane_base + 4 * hh;
-          uint32_t v[4];
-#define FAR10_A(SI)                                                                                        \
-  {                                                                                                        \
-    _Pragma("unroll") for (int cc = 0; cc < 4; ++cc) v[cc] =                                               \
-        pack4<SI>(wr[2 * cc], wi[2 * cc], wr[2 * cc + 1], wi[2 * cc + 1]);                                 \
-    tc::tmem_st4(ta + SI * 8, v);                                                                          \
-  }
-          FAR10_A(0) FAR10_A(1) FAR10_A(2) FAR10_A(3) FAR10_A(4) FAR10_A(5)
-#undef FAR10_A
-        }
-        {  // ---- B: slice entries (bmu, 2 bq + e), regenerated from the kernel (far8's DT path)
-          uint64_t br[2], bi[2], bn[2];
-          const double is = isig[j];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int nl_ = 2 * bq + e, nu = k0 + nl_;
-            double2 S = make_double2(0.0, 0.0);
-            if (bmu < nrow && nu < p) S = kern_tab(dtab[bmu * p + nu], sv, etab, sctab);
-            for (int tl = 0; tl < ntb; ++tl) {  // leftover columns on the FP64 pipe (lead CTA)
-              const double2 zz = zL[(int64_t)j * zst + tl], xv = xs[nl_ * kQXP + kQT + tl];
-              const double ax = zz.x * xv.x - zz.y * xv.y, ay = zz.x * xv.y + zz.y * xv.x;
-              lacc[tl].x = fma(S.x, ax, fma(-S.y, ay, lacc[tl].x));
-              lacc[tl].y = fma(S.x, ay, fma(S.y, ax, lacc[tl].y));
-            }
-            const long long vr = __double2ll_rn(S.x * is), vi = __double2ll_rn(S.y * is);
-            br[e] = (uint64_t)vr + kQBias;
-            bi[e] = (uint64_t)vi + kQBias;
-            bn[e] = (uint64_t)(-vi) + kQBias;
-          }
-          uint8_t* sb = sB + buf * kQBStage;
-          const uint32_t o0 = boff(2 * bmu, 4 * bq), o1 = boff(2 * bmu + 1, 4 * bq);
-#define FAR10_B(SI)                                                                                        \
-  {                                                                                                        \
-    *(uint32_t*)(sb + SI * kQBSlice + o0) = pack4<SI>(br[0], bn[0], br[1], bn[1]);                         \
-    *(uint32_t*)(sb + SI * kQBSlice + o1) = pack4<SI>(bi[0], br[0], bi[1], br[1]);                         \
-  }
-          FAR10_B(0) FAR10_B(1) FAR10_B(2) FAR10_B(3) FAR10_B(4) FAR10_B(5)
-#undef FAR10_B
-        }
-        tc::wait_st();
-        tc::fence_proxy_async();
-        tc::fence_before();
-        __syncthreads();
-        tc::fence_after();
-        if (tid == 0) {
-          const bool first = stage == first_stage;
-          const uint32_t ta = tA0 + (uint32_t)buf * 48;
-          const uint32_t sbb = tc::smem_u32(sB + buf * kQBStage);
-#pragma unroll
-          for (int ia = 0; ia < kQSl; ++ia)
-#pragma unroll
-            for (int ib = 0; ib < kQSl - ia; ++ib)
-              tc::mma_i8_ts(tD + (uint32_t)(ia + ib) * kQN, ta + ia * 8,
-                            tc::smem_desc(sbb + ib * kQBSlice, 128, 256), kQIdesc, (first && ia == 0) ? 0u : 1u);
-          tc::mma_commit(&mbar[buf]);
-        }
-        __syncwarp();
-      }
-    }
-    // (5) read the six level accumulators out into the FP64 accumulators
-    {
-      const uint32_t last = stage - 1;
-      tc::mbar_wait(&mbar[last & 1], (last >> 1) & 1);
+  const int bend = cta_on ? sg.z : sg.y;
+
+  if (warp == kQProd / 32) {
+    // ================= MMA-issue warp: every lane runs the loop (operands stay warp-uniform),
+    // one elected lane issues -- a divergent single-thread issue loop measured ~4x slower
+    // per MMA (tools/i8_rate.py: 117-156 vs 35 cycles at N = 64)
+    uint32_t stage = 0, blk = 0;
+    for (int bi = sg.y; bi < bend; ++bi) {
+      const int rk = a.rank[a.far_sorted[bi]];
+      if (rk == 0) continue;
+      if (blk > 0) tc::mbar_wait(&drained, (blk - 1) & 1);  // previous block read out
       tc::fence_after();
-      const double et = oscl[t_l];
-      const double hs = et * 0x1p-28, ls = et * 0x1p-52;
+      const int ns = rk * nkc;
+      for (int s = 0; s < ns; ++s, ++stage) {
+        const int buf = stage & 1;
+        tc::mbar_wait(&full[buf], (stage >> 1) & 1);
+        tc::fence_after();
+        const uint32_t ta = tA0 + (uint32_t)buf * 48;
+        const uint32_t sbb = tc::smem_u32(sB + buf * kQBStage);
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
+        for (int ia = 0; ia < kQSl; ++ia)
+#pragma unroll
+          for (int ib = 0; ib < kQSl - ia; ++ib)
+            tc::mma_i8_ts_warp(tD + (uint32_t)(ia + ib) * kQN, ta + ia * 8,
+                               tc::smem_desc(sbb + ib * kQBSlice, 128, 256), kQIdesc, (s == 0 && ia == 0) ? 0u : 1u);
+        tc::mma_commit_warp(&empty[buf]);
+      }
+      ++blk;
+    }
+  } else {
+    // ================= producer warps
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    double acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+    double2 lacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    uint32_t stage = 0;
+    int pending = 0;        // a block whose accumulators still have to be read out
+    double et_prev = 1.0;   // its readout scale for column t_l
+    auto readout = [&]() {
+      const uint32_t last = stage - 1;
+      tc::mbar_wait(&empty[last & 1], (last >> 1) & 1);
+      tc::fence_after();
+      const double hs = et_prev * 0x1p-28, ls = et_prev * 0x1p-52;
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
         uint32_t d0[8], d1[8], d2[8], d3[8], d4[8], d5[8];
-        const uint32_t col = tD + lane_base + 32 * hh + 8 * g;
+        const uint32_t col = tD + lane_base + 16 * q4 + 8 * g;
         tc::tmem_ld8(col + 0 * kQN, d0);
         tc::tmem_ld8(col + 1 * kQN, d1);
         tc::tmem_ld8(col + 2 * kQN, d2);
@@ -313,28 +212,193 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
           acc[8 * g + cc] = fma((double)H, hs, fma((double)Lo, ls, acc[8 * g + cc]));
         }
       }
-    }
-  }
-  // (6) this segment's partial: columns 32 hh .. 32 hh + 31 = rows mu 16 hh .. 16 hh + 15 (Re, Im)
-  double2* out = a.part + (int64_t)sg.w * a.nl * p;
-  if (t_l < ncol && tg < a.nl) {
+      tc::fence_before();
+      tc::mbar_arrive(&drained);
+    };
+    auto stage_x = [&](const double2* xh, int k0, double2* xs) {  // x^ chunk [16][kQXP] (cp.async, zero-filled)
+      for (int idx = tid; idx < kQXP * kQKC; idx += kQProd) {
+        const int tl = idx / kQKC, nu = idx - tl * kQKC;
+        int tcol;
+        bool ok;
+        if (tl < kQT) { tcol = tc0 + tl; ok = tl < ncol && tcol < a.nl; }
+        else { tcol = tl - kQT; ok = tcol < ntb; }
+        ok = ok && k0 + nu < p;
+        cp_async16z(xs + nu * kQXP + tl, ok ? (const void*)(xh + (int64_t)tcol * p + k0 + nu) : (const void*)xh, ok);
+      }
+      cp_async_commit();
+    };
+    for (int bi = sg.y; bi < bend; ++bi) {
+      const int b = a.far_sorted[bi];
+      const int rk = a.rank[b];
+      if (rk == 0) continue;
+      const int c = a.far_c[b];
+      const double2* xh = a.xhat + (int64_t)c * a.nl * p;
+      const double2 *zD, *zL;
+      int zst;
+      zrows(a.z, b, a.nl, a.tb, tc0, zD, zL, zst);
+      prod_sync();  // every producer done with the previous block's smem (dtab, sig, svs, x^)
+      stage_x(xh, 0, xsb);  // chunk 0 in flight during the prologue
+      // (1) the block's (r, 1/(4 pi r)) table over this CTA's rows, r_min and r_max
+      double rmn = 1e300, rmx = 0.0;
+      for (int e = tid; e < kQRW * p; e += kQProd) {
+        const int i = e / p, nu = e - i * p;
+        double2 v = make_double2(1.0, 0.0);
+        if (i < nrow) {
+          double cn[3];
+          node(a.xi + (int64_t)c * 3 * m, m, nu, cn);
+          const double dx = cn[0] - xr[3 * i], dy = cn[1] - xr[3 * i + 1], dz = cn[2] - xr[3 * i + 2];
+          v = dist_pair(dx * dx + dy * dy + dz * dz);
+          rmn = fmin(rmn, v.x);
+          rmx = fmax(rmx, v.x);
+        }
+        dtab[e] = v;
+      }
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int mu = 16 * hh + i;
-      if (mu < nrow) {
-        BEM_DASSERT((out - a.part) + (int64_t)tg * p + mu0 + mu < a.part_n);
-        out[(int64_t)tg * p + mu0 + mu] = tv ? make_double2(acc[2 * i], acc[2 * i + 1]) : make_double2(0.0, 0.0);
+      for (int o = 16; o > 0; o >>= 1) {
+        rmn = fmin(rmn, __shfl_xor_sync(0xffffffffu, rmn, o));
+        rmx = fmax(rmx, __shfl_xor_sync(0xffffffffu, rmx, o));
+      }
+      if (lane == 0) { redmin[warp] = rmn; redmax[warp] = rmx; }
+      prod_sync();
+      rmn = redmin[0]; rmx = redmax[0];
+#pragma unroll
+      for (int w = 1; w < kQProd / 32; ++w) { rmn = fmin(rmn, redmin[w]); rmx = fmax(rmx, redmax[w]); }
+      // (2) pivot frequencies and sigma_j = max |S_j| over the rows (the kernel's modulus
+      // is monotone or convex in r)
+      for (int j = tid; j < rk; j += kQProd) {
+        const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + j]];
+        const double sgm = fmax(kmag(rmn, sv.x, etab), kmag(rmx, sv.x, etab)) * (1.0 + 0x1p-30);
+        svs[j] = sv;
+        sig[j] = sgm;
+        isig[j] = sgm > 0.0 ? 0x1p46 / sgm : 0.0;
+      }
+      prod_sync();
+      // (3) per column t: A scale 2^(46 - e_t), readout scale 2^e_t (terms split over the quarters)
+      {
+        double zm = 0.0;
+        if (tv)
+          for (int j = q4; j < rk; j += kQProd / kQT) {
+            const double2 z = zD[(int64_t)j * zst + tg];
+            zm = fmax(zm, sqrt(fma(z.x, z.x, z.y * z.y)) * sig[j]);
+          }
+        zred[q4][t_l] = zm;
+      }
+      prod_sync();
+      if (tid < kQT) {
+        double zm = zred[0][tid];
+#pragma unroll
+        for (int q = 1; q < kQProd / kQT; ++q) zm = fmax(zm, zred[q][tid]);
+        const double bound = tv ? zm * a.xmax[(int64_t)c * a.nl + tg] : 0.0;
+        int e = 0;
+        if (bound > 0.0) frexp(bound, &e);
+        ascl[tid] = bound > 0.0 ? ldexp(1.0, 46 - e) : 0.0;
+        oscl[tid] = ldexp(1.0, e);
+      }
+      // (4) the previous block's accumulators (its MMAs ran during this prologue)
+      if (pending) readout();
+      prod_sync();  // ascl / oscl written
+      const double as_t = ascl[t_l];
+      et_prev = oscl[t_l];
+      pending = 1;
+      // (5) stages: nu chunks (x^ chunk double-buffered), then the ACA terms
+      double2 znext = tv ? zD[tg] : make_double2(0.0, 0.0);
+      for (int kc = 0; kc < nkc; ++kc) {
+        const int k0 = kc * kQKC;
+        double2* xs = xsb + (kc & 1) * kQKC * kQXP;
+        cp_async_wait_all();
+        prod_sync();  // chunk kc landed everywhere; chunk kc - 1's buffer is free
+        if (kc + 1 < nkc) stage_x(xh, k0 + kQKC, xsb + ((kc + 1) & 1) * kQKC * kQXP);
+        for (int j = 0; j < rk; ++j, ++stage) {
+          const int buf = stage & 1;
+          const double2 zc = znext;
+          const int jn = j + 1 < rk ? j + 1 : 0;
+          znext = tv ? zD[(int64_t)jn * zst + tg] : make_double2(0.0, 0.0);
+          if (stage >= 2) tc::mbar_wait(&empty[buf], ((stage >> 1) - 1) & 1);
+          tc::fence_after();
+          const double2 sv = svs[j];
+          {  // ---- A: column t_l, nu 4 q4 .. 4 q4 + 3 -> TMEM lane t_l, columns 2 q4, 2 q4 + 1 per slice
+            const double f = sig[j] * as_t;
+            const double zx = zc.x * f, zy = zc.y * f;
+            double w[8];  // (re, im) of the 4 nu, as digit carriers
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double2 x = xs[(4 * q4 + u) * kQXP + t_l];
+              w[2 * u] = fma(zx, x.x, fma(-zy, x.y, kQMagic));
+              w[2 * u + 1] = fma(zx, x.y, fma(zy, x.x, kQMagic));
+            }
+            uint32_t lo0[4], lo1[4], hi0[2], hi1[2];
+            tr_lo(__double2loint(w[0]), __double2loint(w[1]), __double2loint(w[2]), __double2loint(w[3]), lo0);
+            tr_lo(__double2loint(w[4]), __double2loint(w[5]), __double2loint(w[6]), __double2loint(w[7]), lo1);
+            tr_hi(__double2hiint(w[0]), __double2hiint(w[1]), __double2hiint(w[2]), __double2hiint(w[3]), hi0);
+            tr_hi(__double2hiint(w[4]), __double2hiint(w[5]), __double2hiint(w[6]), __double2hiint(w[7]), hi1);
+            const uint32_t ta = tA0 + (uint32_t)buf * 48 + lane_base + 2 * q4;
+            // slice si = 5 - byte: bytes 5, 4 from the hi words, 3 .. 0 from the lo words
+            tc::tmem_st2(ta + 0 * 8, hi0[1], hi1[1]);
+            tc::tmem_st2(ta + 1 * 8, hi0[0], hi1[0]);
+            tc::tmem_st2(ta + 2 * 8, lo0[3], lo1[3]);
+            tc::tmem_st2(ta + 3 * 8, lo0[2], lo1[2]);
+            tc::tmem_st2(ta + 4 * 8, lo0[1], lo1[1]);
+            tc::tmem_st2(ta + 5 * 8, lo0[0], lo1[0]);
+          }
+          {  // ---- B: slice entry (bmu, bnu), regenerated from the kernel (far8's DT path)
+            const int nu = k0 + bnu;
+            double e = 0.0, sn = 0.0, cs = 0.0;
+            if (bmu < nrow && nu < p) kern_parts(dtab[bmu * p + nu], sv, etab, sctab, e, sn, cs);
+            if (ntb > 0) {  // leftover columns on the FP64 pipe (lead CTA)
+              const double sx = e * cs, sy = -e * sn;
+              for (int tl = 0; tl < ntb; ++tl) {
+                const double2 zz = zL[(int64_t)j * zst + tl], xv = xs[bnu * kQXP + kQT + tl];
+                const double ax = zz.x * xv.x - zz.y * xv.y, ay = zz.x * xv.y + zz.y * xv.x;
+                lacc[tl].x = fma(sx, ax, fma(-sy, ay, lacc[tl].x));
+                lacc[tl].y = fma(sx, ay, fma(sy, ax, lacc[tl].y));
+              }
+            }
+            const double es = e * isig[j];
+            const double wr = fma(es, cs, kQMagic), wi = fma(-es, sn, kQMagic), wn = fma(es, sn, kQMagic);
+            // row 2 bmu: (Re S, -Im S) at k = 2 bnu, 2 bnu + 1; row 2 bmu + 1: (Im S, Re S)
+            const uint32_t rl = __double2loint(wr), il = __double2loint(wi), nlw = __double2loint(wn);
+            const uint32_t rh = __double2hiint(wr), ih = __double2hiint(wi), nh = __double2hiint(wn);
+            uint8_t* sb = sB + buf * kQBStage;
+            const uint32_t o0 = boff(2 * bmu, 2 * bnu), o1 = boff(2 * bmu + 1, 2 * bnu);
+#define FAR10_B(SI, X, Y, Z_, SEL)                                                                        \
+  {                                                                                                      \
+    *(uint16_t*)(sb + SI * kQBSlice + o0) = (uint16_t)(__byte_perm(X, Y, SEL) ^ 0x8080u);                 \
+    *(uint16_t*)(sb + SI * kQBSlice + o1) = (uint16_t)(__byte_perm(Z_, X, SEL) ^ 0x8080u);                \
+  }
+            FAR10_B(0, rh, nh, ih, 0x51) FAR10_B(1, rh, nh, ih, 0x40)
+            FAR10_B(2, rl, nlw, il, 0x73) FAR10_B(3, rl, nlw, il, 0x62)
+            FAR10_B(4, rl, nlw, il, 0x51) FAR10_B(5, rl, nlw, il, 0x40)
+#undef FAR10_B
+          }
+          tc::wait_st();
+          tc::fence_proxy_async();
+          tc::fence_before();
+          tc::mbar_arrive(&full[buf]);
+        }
       }
     }
-  }
-  for (int tl = 0; tl < ntb; ++tl) {
-    double2 v = lacc[tl];
+    if (pending) readout();
+    // (6) this segment's partial: columns 16 q4 .. 16 q4 + 15 = rows mu 8 q4 .. 8 q4 + 7 (Re, Im)
+    double2* out = a.part + (int64_t)sg.w * a.nl * p;
+    if (t_l < ncol && tg < a.nl) {
 #pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-      v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
-      v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+      for (int i = 0; i < 8; ++i) {
+        const int mu = 8 * q4 + i;
+        if (mu < nrow) {
+          BEM_DASSERT((out - a.part) + (int64_t)tg * p + mu0 + mu < a.part_n);
+          out[(int64_t)tg * p + mu0 + mu] = tv ? make_double2(acc[2 * i], acc[2 * i + 1]) : make_double2(0.0, 0.0);
+        }
+      }
     }
-    if (bq == 0 && bmu < nrow) out[(int64_t)tl * p + mu0 + bmu] = v;
+    for (int tl = 0; tl < ntb; ++tl) {
+      double2 v = lacc[tl];
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+      }
+      if (bnu == 0 && bmu < nrow) out[(int64_t)tl * p + mu0 + bmu] = v;
+    }
   }
   tc::fence_before();
   __syncthreads();
@@ -360,8 +424,8 @@ __global__ void __launch_bounds__(256) xmax_kernel(const double2* __restrict__ x
 }  // namespace
 
 cudaError_t launch_far10(const Far10Args& a, int nseg, int ntile, cudaStream_t st) {
-  const size_t need = 2 * (size_t)kQBStage + sizeof(double2) * ((size_t)kQKC * kQXP + (size_t)kQRW * a.p) +
-                      sizeof(double) * 2 * (size_t)a.rcap + 64;
+  const size_t need = 2 * (size_t)kQBStage + sizeof(double2) * (2 * (size_t)kQKC * kQXP + (size_t)kQRW * a.p) +
+                      sizeof(double) * 4 * (size_t)a.rcap + 64;
   const size_t smem = need > kQMinSmem ? need : kQMinSmem;
   cudaError_t e = cudaFuncSetAttribute(far10_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

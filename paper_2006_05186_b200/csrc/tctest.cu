@@ -105,3 +105,102 @@ extern "C" bem_status bem_debug_i8_gemm(const int8_t* A, const int8_t* B, int32_
   BEM_CK(cudaMemcpy(D, dD.p, sizeof(int32_t) * 128 * N, cudaMemcpyDeviceToHost));
   return BEM_OK;
 }
+
+// ---- tcgen05 kind::i8 issue-rate microbenchmark (diagnostics): one CTA per SM, one thread
+// issues `iters` groups of 21 MMAs (M = 128, N, K = 32; the far10 level pattern: six
+// accumulators of N columns) with A in TMEM (mode 0) or shared memory (mode 1), a
+// commit per group and a wait two groups back.  Returns int8 MACs per second.
+namespace bem {
+namespace {
+__global__ void __launch_bounds__(128, 1) i8_rate_kernel(int iters, int N, int mode, long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t taddr_s;
+  __shared__ __align__(8) uint64_t mbar[2];
+  const int t = threadIdx.x, w = t >> 5;
+  for (int i = t; i < 6 * 256 * 32 + 128 * 32 * 6; i += 128) sm[i] = (uint8_t)(i * 7);
+  if (w == 0) tc::tmem_alloc(&taddr_s, 512);
+  if (t == 0) { tc::mbar_init(&mbar[0], 1); tc::mbar_init(&mbar[1], 1); }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tD = taddr_s, tA = taddr_s + 384;
+  const int nacc = N <= 64 ? 6 : N <= 128 ? 3 : 1;  // level accumulators that fit below column 384
+  if (mode >= 2 && w == 0) {  // whole warp 0 runs the issue loop, one elected lane issues
+    const uint32_t id = tc::idesc_i8(128, N);
+    const uint32_t sb = tc::smem_u32(sm);
+    const long long c0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const int buf = it & 1;
+      if (it >= 2) tc::mbar_wait(&mbar[buf], ((it >> 1) - 1) & 1);
+#pragma unroll
+      for (int ia = 0; ia < 6; ++ia)
+#pragma unroll
+        for (int ib = 0; ib < 6 - ia; ++ib) {
+          const uint64_t bd = tc::smem_desc(sb + ib * (N * 32), 128, 256);
+          tc::mma_i8_ts_warp(tD + ((ia + ib) % nacc) * N, tA + ia * 8, bd, id, 1u);
+        }
+      tc::mma_commit_warp(&mbar[buf]);
+    }
+    const int last = iters - 1;
+    tc::mbar_wait(&mbar[last & 1], (last >> 1) & 1);
+    if (t == 0) cyc[blockIdx.x] = clock64() - c0;
+  }
+  if (mode < 2 && t == 0) {
+    const uint32_t id = tc::idesc_i8(128, N);
+    const uint32_t sb = tc::smem_u32(sm), sa = tc::smem_u32(sm + 6 * 256 * 32);
+    const long long c0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const int buf = it & 1;
+      if (it >= 2) tc::mbar_wait(&mbar[buf], ((it >> 1) - 1) & 1);
+      for (int ia = 0; ia < 6; ++ia)
+        for (int ib = 0; ib < 6 - ia; ++ib) {
+          const uint64_t bd = tc::smem_desc(sb + ib * (N * 32), 128, 256);
+          const uint32_t d = tD + ((ia + ib) % nacc) * N;
+          if (mode == 0) tc::mma_i8_ts(d, tA + ia * 8, bd, id, 1u);
+          else tc::mma_i8_ss(d, tc::smem_desc(sa + ia * 4096, 128, 256), bd, id, 1u);
+        }
+      tc::mma_commit(&mbar[buf]);
+    }
+    const int last = iters - 1;
+    tc::mbar_wait(&mbar[last & 1], (last >> 1) & 1);
+    cyc[blockIdx.x] = clock64() - c0;
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (w == 0) tc::tmem_dealloc(taddr_s, 512);
+}
+}  // namespace
+}  // namespace bem
+
+extern "C" bem_status bem_debug_i8_rate(int32_t N, int32_t mode, int32_t iters, int32_t device, double* macs_per_s,
+                                        double* cycles_per_mma) {
+  using namespace bem;
+  BEM_REQ(macs_per_s && cycles_per_mma, "bem_debug_i8_rate: NULL output");
+  BEM_REQ(N == 32 || N == 64 || N == 128 || N == 256, "bem_debug_i8_rate: N in {32, 64, 128, 256}");
+  DeviceGuard dg(device);
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  DBuf<long long> cyc;
+  BEM_CK(cyc.alloc(nsm));
+  const size_t smem = 6 * 256 * 32 + 128 * 32 * 6;
+  BEM_CK(cudaFuncSetAttribute(i8_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  i8_rate_kernel<<<nsm, 128, smem>>>(10, N, mode, cyc.p);
+  cudaEvent_t e0, e1;
+  BEM_CK(cudaEventCreate(&e0));
+  BEM_CK(cudaEventCreate(&e1));
+  BEM_CK(cudaEventRecord(e0));
+  i8_rate_kernel<<<nsm, 128, smem>>>(iters, N, mode, cyc.p);
+  BEM_CK(cudaEventRecord(e1));
+  BEM_CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  BEM_CK(cudaEventElapsedTime(&ms, e0, e1));
+  std::vector<long long> h(nsm);
+  BEM_CK(cudaMemcpy(h.data(), cyc.p, sizeof(long long) * nsm, cudaMemcpyDeviceToHost));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double mmas = 21.0 * iters;
+  *macs_per_s = (double)nsm * mmas * 128.0 * N * 32.0 / (ms * 1e-3);
+  *cycles_per_mma = (double)h[0] / mmas;
+  return BEM_OK;
+}

@@ -229,7 +229,7 @@ struct Op {
   DBuf<double> d_xmax;  // far10: [C][nl] max_nu |xhat|
   // kernel selection (env BEM_FAR_KERNEL / BEM_FAR8_KC / BEM_FAR_GENERIC, read at assembly: tests)
   bool force_generic = false;
-  int far_kernel = 0;                 // 0: auto (far8 for p > 32, far7 otherwise); 8, 7, 10 (INT8 tensor cores)
+  int far_kernel = 0;                 // 0: auto (far10 where it applies, else far8 for p > 32 / far7); 10, 8, 7
   size_t far4_smem_cap = 113 * 1024;  // 2 CTAs per SM
   int far8_kc = 0;                    // far8 nu-chunk width (0: automatic)
   bool far8_m3 = true;                // far8: 3M complex products at 16-row mu chunks (env BEM_FAR8_M3=0: 4M, 32 rows)

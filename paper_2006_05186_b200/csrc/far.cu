@@ -1044,7 +1044,9 @@ static FarGeom far_geom(const Op& op) {
   const Tree& t = *op.tree;
   const int p = t.p, nl = op.n_local;
   FarGeom g;
-  g.fk = op.far_kernel != 0 ? op.far_kernel : (p > 32 ? 8 : 7);  // r01: far8 wins at p = 64, far7 at p = 27
+  // default: far10 (INT8 tensor cores) wherever it applies; far8 / far7 (FP64 tensor cores)
+  // otherwise -- r01: far8 wins at p = 64, far7 at p = 27
+  g.fk = op.far_kernel != 0 ? op.far_kernel : 10;
   if (op.force_generic || op.n_segs == 0) { g.fk = 0; return g; }
   if (g.fk == 10) {
     // far10 (farq.cu): 128-column frequency tiles, <= 2 leftover columns on the FP64 pipe;

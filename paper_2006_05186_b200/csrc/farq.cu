@@ -11,7 +11,7 @@
 // far below the 1e-10 parity bar).
 //
 // Scaling (exact powers of two, so the integer sums are exact):
-//   B (kernel slice S_j, regenerated from the kernel as in far8): S_j / sigma_j with
+//   B (kernel slice S_j, regenerated from the kernel -- far8's table exp / sincos): S_j / sigma_j with
 //     sigma_j = max |S_j| over this CTA's rows = max(f(r_min), f(r_max)), f(r) =
 //     |e^{-s r}| / (4 pi r) (f has no interior maximum for any Re s);
 //   A (Z_b[j, t] sigma_j xhat_c[nu, t]): per frequency column t the power of two above
@@ -112,10 +112,11 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
   const int p = a.p, m = a.m;
   uint8_t* sB = smq;                                          // 2 x [6][64][32] int8
   double2* xsb = (double2*)(smq + 2 * kQBStage);              // 2 x [16][kQXP]
-  double2* dtab = xsb + 2 * kQKC * kQXP;                      // [32][p] (r, 1/(4 pi r))
-  double2* svs = dtab + (size_t)kQRW * p;                     // [rcap] pivot frequencies s_{k_j}
+  double2* svs = xsb + 2 * kQKC * kQXP;                       // [rcap] pivot frequencies s_{k_j}
   double* sig = (double*)(svs + a.rcap);                      // [rcap] sigma_j
   double* isig = sig + a.rcap;                                // [rcap] 2^46 / sigma_j
+  double* accs = isig + a.rcap;                               // [64][128] FP64 accumulators (column-major in t)
+  double2* lzs = (double2*)(accs + (size_t)kQN * kQT);        // [rcap][2] Z_b[j, leftover columns]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int4 sg = a.segs[blockIdx.x / a.nch];
   const int r = sg.x;
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
   tc::fence_after();
   const uint32_t tD = taddr_s, tA0 = taddr_s + kQAcol;
   const int bend = cta_on ? sg.z : sg.y;
+  const uint32_t full_a = tc::smem_u32(&full[0]), empty_a = tc::smem_u32(&empty[0]), drained_a = tc::smem_u32(&drained);
 
   if (warp == kQProd / 32) {
     // ================= MMA-issue warp: every lane runs the loop (operands stay warp-uniform),
@@ -160,12 +162,12 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
     for (int bi = sg.y; bi < bend; ++bi) {
       const int rk = a.rank[a.far_sorted[bi]];
       if (rk == 0) continue;
-      if (blk > 0) tc::mbar_wait(&drained, (blk - 1) & 1);  // previous block read out
+      if (blk > 0) tc::mbar_wait_a(drained_a, (blk - 1) & 1);  // previous block read out
       tc::fence_after();
       const int ns = rk * nkc;
       for (int s = 0; s < ns; ++s, ++stage) {
         const int buf = stage & 1;
-        tc::mbar_wait(&full[buf], (stage >> 1) & 1);
+        tc::mbar_wait_a(full_a + 8 * buf, (stage >> 1) & 1);
         tc::fence_after();
         const uint32_t ta = tA0 + (uint32_t)buf * 48;
         const uint32_t sbb = tc::smem_u32(sB + buf * kQBStage);
@@ -175,23 +177,23 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
           for (int ib = 0; ib < kQSl - ia; ++ib)
             tc::mma_i8_ts_warp(tD + (uint32_t)(ia + ib) * kQN, ta + ia * 8,
                                tc::smem_desc(sbb + ib * kQBSlice, 128, 256), kQIdesc, (s == 0 && ia == 0) ? 0u : 1u);
-        tc::mma_commit_warp(&empty[buf]);
+        tc::mma_commit_warp_a(empty_a + 8 * buf);
       }
       ++blk;
     }
   } else {
     // ================= producer warps
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    double acc[16];
+    double* acc = accs + (16 * q4) * kQT + t_l;  // this thread's 16 columns, stride kQT
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+    for (int i = 0; i < 16; ++i) acc[i * kQT] = 0.0;
     double2 lacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
     uint32_t stage = 0;
     int pending = 0;        // a block whose accumulators still have to be read out
     double et_prev = 1.0;   // its readout scale for column t_l
     auto readout = [&]() {
       const uint32_t last = stage - 1;
-      tc::mbar_wait(&empty[last & 1], (last >> 1) & 1);
+      tc::mbar_wait_a(empty_a + 8 * (last & 1), (last >> 1) & 1);
       tc::fence_after();
       const double hs = et_prev * 0x1p-28, ls = et_prev * 0x1p-52;
 #pragma unroll
@@ -209,11 +211,11 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
         for (int cc = 0; cc < 8; ++cc) {
           const long long H = ((long long)(int)d0[cc] << 16) + ((long long)(int)d1[cc] << 8) + (long long)(int)d2[cc];
           const long long Lo = ((long long)(int)d3[cc] << 16) + ((long long)(int)d4[cc] << 8) + (long long)(int)d5[cc];
-          acc[8 * g + cc] = fma((double)H, hs, fma((double)Lo, ls, acc[8 * g + cc]));
+          acc[(8 * g + cc) * kQT] = fma((double)H, hs, fma((double)Lo, ls, acc[(8 * g + cc) * kQT]));
         }
       }
       tc::fence_before();
-      tc::mbar_arrive(&drained);
+      tc::mbar_arrive_a(drained_a);
     };
     auto stage_x = [&](const double2* xh, int k0, double2* xs) {  // x^ chunk [16][kQXP] (cp.async, zero-filled)
       for (int idx = tid; idx < kQXP * kQKC; idx += kQProd) {
@@ -236,22 +238,19 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
       const double2 *zD, *zL;
       int zst;
       zrows(a.z, b, a.nl, a.tb, tc0, zD, zL, zst);
-      prod_sync();  // every producer done with the previous block's smem (dtab, sig, svs, x^)
+      prod_sync();  // every producer done with the previous block's smem (sig, svs, x^)
       stage_x(xh, 0, xsb);  // chunk 0 in flight during the prologue
-      // (1) the block's (r, 1/(4 pi r)) table over this CTA's rows, r_min and r_max
+      // (1) r_min and r_max over this CTA's rows and the block's columns (the (r, 1/(4 pi r))
+      // pair of a thread's own slice entry is recomputed per nu chunk, in a register)
       double rmn = 1e300, rmx = 0.0;
-      for (int e = tid; e < kQRW * p; e += kQProd) {
+      for (int e = tid; e < nrow * p; e += kQProd) {
         const int i = e / p, nu = e - i * p;
-        double2 v = make_double2(1.0, 0.0);
-        if (i < nrow) {
-          double cn[3];
-          node(a.xi + (int64_t)c * 3 * m, m, nu, cn);
-          const double dx = cn[0] - xr[3 * i], dy = cn[1] - xr[3 * i + 1], dz = cn[2] - xr[3 * i + 2];
-          v = dist_pair(dx * dx + dy * dy + dz * dz);
-          rmn = fmin(rmn, v.x);
-          rmx = fmax(rmx, v.x);
-        }
-        dtab[e] = v;
+        double cn[3];
+        node(a.xi + (int64_t)c * 3 * m, m, nu, cn);
+        const double dx = cn[0] - xr[3 * i], dy = cn[1] - xr[3 * i + 1], dz = cn[2] - xr[3 * i + 2];
+        const double2 v = dist_pair(dx * dx + dy * dy + dz * dz);
+        rmn = fmin(rmn, v.x);
+        rmx = fmax(rmx, v.x);
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -269,6 +268,8 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
         const double2 sv = a.s[a.pivk[(int64_t)b * a.rcap + j]];
         const double sgm = fmax(kmag(rmn, sv.x, etab), kmag(rmx, sv.x, etab)) * (1.0 + 0x1p-30);
         svs[j] = sv;
+        if (ntb > 0) lzs[2 * j] = zL[(int64_t)j * zst];
+        if (ntb > 1) lzs[2 * j + 1] = zL[(int64_t)j * zst + 1];
         sig[j] = sgm;
         isig[j] = sgm > 0.0 ? 0x1p46 / sgm : 0.0;
       }
@@ -302,22 +303,36 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
       pending = 1;
       // (5) stages: nu chunks (x^ chunk double-buffered), then the ACA terms
       double2 znext = tv ? zD[tg] : make_double2(0.0, 0.0);
+      double2 svn = svs[0];
+      double sgn = sig[0], isn = isig[0];
       for (int kc = 0; kc < nkc; ++kc) {
         const int k0 = kc * kQKC;
         double2* xs = xsb + (kc & 1) * kQKC * kQXP;
         cp_async_wait_all();
         prod_sync();  // chunk kc landed everywhere; chunk kc - 1's buffer is free
         if (kc + 1 < nkc) stage_x(xh, k0 + kQKC, xsb + ((kc + 1) & 1) * kQKC * kQXP);
+        const bool bon = bmu < nrow && k0 + bnu < p;  // this thread's slice entry exists
+        double2 rw = make_double2(1.0, 0.0);
+        if (bon) {
+          double cn[3];
+          node(a.xi + (int64_t)c * 3 * m, m, k0 + bnu, cn);
+          const double dx = cn[0] - xr[3 * bmu], dy = cn[1] - xr[3 * bmu + 1], dz = cn[2] - xr[3 * bmu + 2];
+          rw = dist_pair(dx * dx + dy * dy + dz * dz);
+        }
         for (int j = 0; j < rk; ++j, ++stage) {
           const int buf = stage & 1;
           const double2 zc = znext;
           const int jn = j + 1 < rk ? j + 1 : 0;
           znext = tv ? zD[(int64_t)jn * zst + tg] : make_double2(0.0, 0.0);
-          if (stage >= 2) tc::mbar_wait(&empty[buf], ((stage >> 1) - 1) & 1);
+          const double2 sv = svn;
+          const double sgj = sgn, isj = isn;
+          svn = svs[jn];
+          sgn = sig[jn];
+          isn = isig[jn];
+          if (stage >= 2) tc::mbar_wait_a(empty_a + 8 * buf, ((stage >> 1) - 1) & 1);
           tc::fence_after();
-          const double2 sv = svs[j];
           {  // ---- A: column t_l, nu 4 q4 .. 4 q4 + 3 -> TMEM lane t_l, columns 2 q4, 2 q4 + 1 per slice
-            const double f = sig[j] * as_t;
+            const double f = sgj * as_t;
             const double zx = zc.x * f, zy = zc.y * f;
             double w[8];  // (re, im) of the 4 nu, as digit carriers
 #pragma unroll
@@ -341,19 +356,21 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
             tc::tmem_st2(ta + 5 * 8, lo0[0], lo1[0]);
           }
           {  // ---- B: slice entry (bmu, bnu), regenerated from the kernel (far8's DT path)
-            const int nu = k0 + bnu;
             double e = 0.0, sn = 0.0, cs = 0.0;
-            if (bmu < nrow && nu < p) kern_parts(dtab[bmu * p + nu], sv, etab, sctab, e, sn, cs);
+            if (bon) kern_parts(rw, sv, etab, sctab, e, sn, cs);
             if (ntb > 0) {  // leftover columns on the FP64 pipe (lead CTA)
               const double sx = e * cs, sy = -e * sn;
-              for (int tl = 0; tl < ntb; ++tl) {
-                const double2 zz = zL[(int64_t)j * zst + tl], xv = xs[bnu * kQXP + kQT + tl];
-                const double ax = zz.x * xv.x - zz.y * xv.y, ay = zz.x * xv.y + zz.y * xv.x;
-                lacc[tl].x = fma(sx, ax, fma(-sy, ay, lacc[tl].x));
-                lacc[tl].y = fma(sx, ay, fma(sy, ax, lacc[tl].y));
+#pragma unroll
+              for (int tl = 0; tl < 2; ++tl) {
+                if (tl < ntb) {
+                  const double2 zz = lzs[2 * j + tl], xv = xs[bnu * kQXP + kQT + tl];
+                  const double ax = zz.x * xv.x - zz.y * xv.y, ay = zz.x * xv.y + zz.y * xv.x;
+                  lacc[tl].x = fma(sx, ax, fma(-sy, ay, lacc[tl].x));
+                  lacc[tl].y = fma(sx, ay, fma(sy, ax, lacc[tl].y));
+                }
               }
             }
-            const double es = e * isig[j];
+            const double es = e * isj;
             const double wr = fma(es, cs, kQMagic), wi = fma(-es, sn, kQMagic), wn = fma(es, sn, kQMagic);
             // row 2 bmu: (Re S, -Im S) at k = 2 bnu, 2 bnu + 1; row 2 bmu + 1: (Im S, Re S)
             const uint32_t rl = __double2loint(wr), il = __double2loint(wi), nlw = __double2loint(wn);
@@ -373,7 +390,7 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
           tc::wait_st();
           tc::fence_proxy_async();
           tc::fence_before();
-          tc::mbar_arrive(&full[buf]);
+          tc::mbar_arrive_a(full_a + 8 * buf);
         }
       }
     }
@@ -386,11 +403,13 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
         const int mu = 8 * q4 + i;
         if (mu < nrow) {
           BEM_DASSERT((out - a.part) + (int64_t)tg * p + mu0 + mu < a.part_n);
-          out[(int64_t)tg * p + mu0 + mu] = tv ? make_double2(acc[2 * i], acc[2 * i + 1]) : make_double2(0.0, 0.0);
+          out[(int64_t)tg * p + mu0 + mu] = tv ? make_double2(acc[2 * i * kQT], acc[(2 * i + 1) * kQT]) : make_double2(0.0, 0.0);
         }
       }
     }
-    for (int tl = 0; tl < ntb; ++tl) {
+#pragma unroll
+    for (int tl = 0; tl < 2; ++tl) {
+      if (tl >= ntb) break;
       double2 v = lacc[tl];
 #pragma unroll
       for (int o = 1; o < 16; o <<= 1) {
@@ -424,8 +443,8 @@ __global__ void __launch_bounds__(256) xmax_kernel(const double2* __restrict__ x
 }  // namespace
 
 cudaError_t launch_far10(const Far10Args& a, int nseg, int ntile, cudaStream_t st) {
-  const size_t need = 2 * (size_t)kQBStage + sizeof(double2) * (2 * (size_t)kQKC * kQXP + (size_t)kQRW * a.p) +
-                      sizeof(double) * 4 * (size_t)a.rcap + 64;
+  const size_t need = 2 * (size_t)kQBStage + sizeof(double2) * (2 * (size_t)kQKC * kQXP) +
+                      sizeof(double) * (8 * (size_t)a.rcap + (size_t)kQN * kQT) + 64;
   const size_t smem = need > kQMinSmem ? need : kQMinSmem;
   cudaError_t e = cudaFuncSetAttribute(far10_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -529,7 +529,10 @@ def test_full_size_properties(pb, torch, cfg):
     y1, y2 = op.apply(x1), op.apply(x2)
     y12 = op.apply(0.75 * x1 - 1.5j * x2)
     lin = torch.linalg.vector_norm(y12 - (0.75 * y1 - 1.5j * y2)) / torch.linalg.vector_norm(y12)
-    assert float(lin) <= 1e-13
+    # FP64 kernels: rounding only (1e-13); far10 rounds every coupling operand to a 48-bit
+    # fixed-point number per block and drops slice levels >= 6 (~4e-13 per block product,
+    # DESIGN.md §7 far10): 1e-11
+    assert float(lin) <= (1e-11 if op.info()["far_kernel"] == 10 else 1e-13)
     assert torch.equal(op.apply(x1), y1)
     op2 = pb.Operator(tree, s, c["eps"], mode=pb.BEM_MODE_H2ONLY)
     yo = op2.apply(x1)

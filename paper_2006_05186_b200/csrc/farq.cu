@@ -28,6 +28,8 @@
 // shared-memory read bandwidth spent on it), B in shared memory (canonical K-major
 // layout).  Two stages in flight: the threads build stage s + 1 while the tensor
 // cores run stage s (completion through an mbarrier per stage buffer).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "far_common.cuh"
 #include "fastmath.cuh"
@@ -46,7 +48,8 @@ constexpr int kQThreads = kQProd + 32;    // + the MMA-issue warp
 constexpr int kQSl = 6;               // byte slices per operand
 constexpr int kQBSlice = kQN * 32;    // bytes of one B slice tile [64][32]
 constexpr int kQBStage = kQSl * kQBSlice;
-constexpr uint32_t kQCols = 512;      // TMEM: six level accumulators [0, 384), two A stages [384, 480)
+constexpr uint32_t kQCols = 512;      // TMEM: six level accumulators [0, 384), A of stages 0, 1 [384, 480)
+constexpr int kQASlice = kQT * 32;    // bytes of one A slice tile [128][32] (shared-memory stage)
 constexpr uint32_t kQAcol = 384;
 constexpr uint32_t kQIdesc = tc::idesc_i8(kQT, kQN);
 constexpr size_t kQMinSmem = 116 * 1024;  // one CTA per SM (it owns all 512 TMEM columns)
@@ -99,10 +102,12 @@ __device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool ok)
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// NB: pipeline stages (2: both A stages in TMEM; 3: the third stage's A in shared memory)
+template <int kQNB>
 __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) {
   extern __shared__ __align__(1024) uint8_t smq[];
   __shared__ uint32_t taddr_s;
-  __shared__ __align__(8) uint64_t full[2], empty[2], drained;
+  __shared__ __align__(8) uint64_t full[kQNB], empty[kQNB], drained;
   __shared__ double etab[64];
   __shared__ double2 sctab[64];
   __shared__ double xr[3 * kQRW];
@@ -110,8 +115,9 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
   __shared__ double zred[kQProd / kQT][kQT];
   __shared__ double redmin[kQProd / 32], redmax[kQProd / 32];
   const int p = a.p, m = a.m;
-  uint8_t* sB = smq;                                          // 2 x [6][64][32] int8
-  double2* xsb = (double2*)(smq + 2 * kQBStage);              // 2 x [16][kQXP]
+  uint8_t* sB = smq;                                          // 3 x [6][64][32] int8
+  uint8_t* sA2 = smq + kQNB * kQBStage;                       // [6][128][32] int8: A of stage buffer 2 (NB = 3)
+  double2* xsb = (double2*)(sA2 + (kQNB == 3 ? kQSl * kQASlice : 0));  // 2 x [16][kQXP]
   double2* svs = xsb + 2 * kQKC * kQXP;                       // [rcap] pivot frequencies s_{k_j}
   double* sig = (double*)(svs + a.rcap);                      // [rcap] sigma_j
   double* isig = sig + a.rcap;                                // [rcap] 2^46 / sigma_j
@@ -135,11 +141,11 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
   for (int i = tid; i < nrow; i += kQThreads) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
   if (warp == 0) tc::tmem_alloc(&taddr_s, kQCols);
   if (tid == 0) {
-    tc::mbar_init(&full[0], kQProd);
-    tc::mbar_init(&full[1], kQProd);
-    tc::mbar_init(&empty[0], 1);
-    tc::mbar_init(&empty[1], 1);
-    tc::mbar_init(&drained, kQProd);
+    for (int i = 0; i < kQNB; ++i) {
+      tc::mbar_init(&full[i], kQProd / 32);  // one arrival per producer warp
+      tc::mbar_init(&empty[i], 1);
+    }
+    tc::mbar_init(&drained, kQProd / 32);
   }
   // producer roles: A / readout (frequency column t_l, quarter q4: nu 4 q4 .. 4 q4 + 3 of a
   // stage, accumulator columns 16 q4 .. 16 q4 + 15 = rows mu 8 q4 .. 8 q4 + 7); B (slice entry
@@ -165,19 +171,30 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
       if (blk > 0) tc::mbar_wait_a(drained_a, (blk - 1) & 1);  // previous block read out
       tc::fence_after();
       const int ns = rk * nkc;
+      uint32_t buf = stage % kQNB, use = stage / kQNB;
       for (int s = 0; s < ns; ++s, ++stage) {
-        const int buf = stage & 1;
-        tc::mbar_wait_a(full_a + 8 * buf, (stage >> 1) & 1);
+        tc::mbar_wait_a(full_a + 8 * buf, use & 1);
         tc::fence_after();
-        const uint32_t ta = tA0 + (uint32_t)buf * 48;
         const uint32_t sbb = tc::smem_u32(sB + buf * kQBStage);
+        if (buf < 2) {
+          const uint32_t ta = tA0 + buf * 48;
 #pragma unroll
-        for (int ia = 0; ia < kQSl; ++ia)
+          for (int ia = 0; ia < kQSl; ++ia)
 #pragma unroll
-          for (int ib = 0; ib < kQSl - ia; ++ib)
-            tc::mma_i8_ts_warp(tD + (uint32_t)(ia + ib) * kQN, ta + ia * 8,
-                               tc::smem_desc(sbb + ib * kQBSlice, 128, 256), kQIdesc, (s == 0 && ia == 0) ? 0u : 1u);
+            for (int ib = 0; ib < kQSl - ia; ++ib)
+              tc::mma_i8_ts_warp(tD + (uint32_t)(ia + ib) * kQN, ta + ia * 8,
+                                 tc::smem_desc(sbb + ib * kQBSlice, 128, 256), kQIdesc, (s == 0 && ia == 0) ? 0u : 1u);
+        } else {
+          const uint32_t saa = tc::smem_u32(sA2);
+#pragma unroll
+          for (int ia = 0; ia < kQSl; ++ia)
+#pragma unroll
+            for (int ib = 0; ib < kQSl - ia; ++ib)
+              tc::mma_i8_ss_warp(tD + (uint32_t)(ia + ib) * kQN, tc::smem_desc(saa + ia * kQASlice, 128, 256),
+                                 tc::smem_desc(sbb + ib * kQBSlice, 128, 256), kQIdesc, (s == 0 && ia == 0) ? 0u : 1u);
+        }
         tc::mma_commit_warp_a(empty_a + 8 * buf);
+        if (++buf == kQNB) { buf = 0; ++use; }
       }
       ++blk;
     }
@@ -193,7 +210,7 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
     double et_prev = 1.0;   // its readout scale for column t_l
     auto readout = [&]() {
       const uint32_t last = stage - 1;
-      tc::mbar_wait_a(empty_a + 8 * (last & 1), (last >> 1) & 1);
+      tc::mbar_wait_a(empty_a + 8 * (last % kQNB), (last / kQNB) & 1);
       tc::fence_after();
       const double hs = et_prev * 0x1p-28, ls = et_prev * 0x1p-52;
 #pragma unroll
@@ -215,7 +232,8 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
         }
       }
       tc::fence_before();
-      tc::mbar_arrive_a(drained_a);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_a(drained_a);
     };
     auto stage_x = [&](const double2* xh, int k0, double2* xs) {  // x^ chunk [16][kQXP] (cp.async, zero-filled)
       for (int idx = tid; idx < kQXP * kQKC; idx += kQProd) {
@@ -312,7 +330,7 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
         prod_sync();  // chunk kc landed everywhere; chunk kc - 1's buffer is free
         if (kc + 1 < nkc) stage_x(xh, k0 + kQKC, xsb + ((kc + 1) & 1) * kQKC * kQXP);
         const bool bon = bmu < nrow && k0 + bnu < p;  // this thread's slice entry exists
-        double2 rw = make_double2(1.0, 0.0);
+        double2 rw = make_double2(1.0, 0.0);           // off the slice: 1 / (4 pi r) := 0
         if (bon) {
           double cn[3];
           node(a.xi + (int64_t)c * 3 * m, m, k0 + bnu, cn);
@@ -320,7 +338,7 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
           rw = dist_pair(dx * dx + dy * dy + dz * dz);
         }
         for (int j = 0; j < rk; ++j, ++stage) {
-          const int buf = stage & 1;
+          const uint32_t buf = stage % kQNB;
           const double2 zc = znext;
           const int jn = j + 1 < rk ? j + 1 : 0;
           znext = tv ? zD[(int64_t)jn * zst + tg] : make_double2(0.0, 0.0);
@@ -329,68 +347,85 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
           svn = svs[jn];
           sgn = sig[jn];
           isn = isig[jn];
-          if (stage >= 2) tc::mbar_wait_a(empty_a + 8 * buf, ((stage >> 1) - 1) & 1);
-          tc::fence_after();
-          {  // ---- A: column t_l, nu 4 q4 .. 4 q4 + 3 -> TMEM lane t_l, columns 2 q4, 2 q4 + 1 per slice
-            const double f = sgj * as_t;
-            const double zx = zc.x * f, zy = zc.y * f;
-            double w[8];  // (re, im) of the 4 nu, as digit carriers
+          // ---- compute (one basic block, no buffer access): A = Z x^ for column t_l and
+          // nu 4 q4 .. 4 q4 + 3; B = slice entry (bmu, bnu) regenerated from the kernel (far8's
+          // table exp / sincos; rw = (1, 0) off the slice gives 0)
+          const double f = sgj * as_t;
+          const double zx = zc.x * f, zy = zc.y * f;
+          double w[8];  // (re, im) of the 4 nu, as digit carriers
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const double2 x = xs[(4 * q4 + u) * kQXP + t_l];
-              w[2 * u] = fma(zx, x.x, fma(-zy, x.y, kQMagic));
-              w[2 * u + 1] = fma(zx, x.y, fma(zy, x.x, kQMagic));
-            }
-            uint32_t lo0[4], lo1[4], hi0[2], hi1[2];
-            tr_lo(__double2loint(w[0]), __double2loint(w[1]), __double2loint(w[2]), __double2loint(w[3]), lo0);
-            tr_lo(__double2loint(w[4]), __double2loint(w[5]), __double2loint(w[6]), __double2loint(w[7]), lo1);
-            tr_hi(__double2hiint(w[0]), __double2hiint(w[1]), __double2hiint(w[2]), __double2hiint(w[3]), hi0);
-            tr_hi(__double2hiint(w[4]), __double2hiint(w[5]), __double2hiint(w[6]), __double2hiint(w[7]), hi1);
-            const uint32_t ta = tA0 + (uint32_t)buf * 48 + lane_base + 2 * q4;
-            // slice si = 5 - byte: bytes 5, 4 from the hi words, 3 .. 0 from the lo words
+          for (int u = 0; u < 4; ++u) {
+            const double2 x = xs[(4 * q4 + u) * kQXP + t_l];
+            w[2 * u] = fma(zx, x.x, fma(-zy, x.y, kQMagic));
+            w[2 * u + 1] = fma(zx, x.y, fma(zy, x.x, kQMagic));
+          }
+          double e, sn, cs;
+          kern_parts(rw, sv, etab, sctab, e, sn, cs);
+          const double es = e * isj;
+          const double wr = fma(es, cs, kQMagic), wi = fma(-es, sn, kQMagic), wn = fma(es, sn, kQMagic);
+          uint32_t lo0[4], lo1[4], hi0[2], hi1[2];
+          tr_lo(__double2loint(w[0]), __double2loint(w[1]), __double2loint(w[2]), __double2loint(w[3]), lo0);
+          tr_lo(__double2loint(w[4]), __double2loint(w[5]), __double2loint(w[6]), __double2loint(w[7]), lo1);
+          tr_hi(__double2hiint(w[0]), __double2hiint(w[1]), __double2hiint(w[2]), __double2hiint(w[3]), hi0);
+          tr_hi(__double2hiint(w[4]), __double2hiint(w[5]), __double2hiint(w[6]), __double2hiint(w[7]), hi1);
+          // B rows 2 bmu: (Re S, -Im S) at k = 2 bnu, 2 bnu + 1; 2 bmu + 1: (Im S, Re S)
+          const uint32_t rl = __double2loint(wr), il = __double2loint(wi), nlw = __double2loint(wn);
+          const uint32_t rh = __double2hiint(wr), ih = __double2hiint(wi), nh = __double2hiint(wn);
+          uint32_t bw0[6], bw1[6];
+#define FAR10_B(SI, X, Y, Z_, SEL)                                                                        \
+  bw0[SI] = __byte_perm(X, Y, SEL) ^ 0x8080u;                                                            \
+  bw1[SI] = __byte_perm(Z_, X, SEL) ^ 0x8080u;
+          FAR10_B(0, rh, nh, ih, 0x51) FAR10_B(1, rh, nh, ih, 0x40)
+          FAR10_B(2, rl, nlw, il, 0x73) FAR10_B(3, rl, nlw, il, 0x62)
+          FAR10_B(4, rl, nlw, il, 0x51) FAR10_B(5, rl, nlw, il, 0x40)
+#undef FAR10_B
+          // ---- the buffer is free once the MMAs of its previous use completed
+          if (stage >= kQNB) tc::mbar_wait_a(empty_a + 8 * buf, ((stage / kQNB) - 1) & 1);
+          tc::fence_after();
+          // slice si = 5 - byte: bytes 5, 4 from the hi words, 3 .. 0 from the lo words
+          if (buf < 2) {
+            const uint32_t ta = tA0 + buf * 48 + lane_base + 2 * q4;
             tc::tmem_st2(ta + 0 * 8, hi0[1], hi1[1]);
             tc::tmem_st2(ta + 1 * 8, hi0[0], hi1[0]);
             tc::tmem_st2(ta + 2 * 8, lo0[3], lo1[3]);
             tc::tmem_st2(ta + 3 * 8, lo0[2], lo1[2]);
             tc::tmem_st2(ta + 4 * 8, lo0[1], lo1[1]);
             tc::tmem_st2(ta + 5 * 8, lo0[0], lo1[0]);
+          } else {  // canonical K-major [128][32] tiles: row t_l, bytes 8 q4 .. 8 q4 + 7
+            uint8_t* pa = sA2 + (t_l >> 3) * 256 + (q4 >> 1) * 128 + (t_l & 7) * 16 + (q4 & 1) * 8;
+            *(uint2*)(pa + 0 * kQASlice) = make_uint2(hi0[1], hi1[1]);
+            *(uint2*)(pa + 1 * kQASlice) = make_uint2(hi0[0], hi1[0]);
+            *(uint2*)(pa + 2 * kQASlice) = make_uint2(lo0[3], lo1[3]);
+            *(uint2*)(pa + 3 * kQASlice) = make_uint2(lo0[2], lo1[2]);
+            *(uint2*)(pa + 4 * kQASlice) = make_uint2(lo0[1], lo1[1]);
+            *(uint2*)(pa + 5 * kQASlice) = make_uint2(lo0[0], lo1[0]);
           }
-          {  // ---- B: slice entry (bmu, bnu), regenerated from the kernel (far8's DT path)
-            double e = 0.0, sn = 0.0, cs = 0.0;
-            if (bon) kern_parts(rw, sv, etab, sctab, e, sn, cs);
-            if (ntb > 0) {  // leftover columns on the FP64 pipe (lead CTA)
-              const double sx = e * cs, sy = -e * sn;
-#pragma unroll
-              for (int tl = 0; tl < 2; ++tl) {
-                if (tl < ntb) {
-                  const double2 zz = lzs[2 * j + tl], xv = xs[bnu * kQXP + kQT + tl];
-                  const double ax = zz.x * xv.x - zz.y * xv.y, ay = zz.x * xv.y + zz.y * xv.x;
-                  lacc[tl].x = fma(sx, ax, fma(-sy, ay, lacc[tl].x));
-                  lacc[tl].y = fma(sx, ay, fma(sy, ax, lacc[tl].y));
-                }
-              }
-            }
-            const double es = e * isj;
-            const double wr = fma(es, cs, kQMagic), wi = fma(-es, sn, kQMagic), wn = fma(es, sn, kQMagic);
-            // row 2 bmu: (Re S, -Im S) at k = 2 bnu, 2 bnu + 1; row 2 bmu + 1: (Im S, Re S)
-            const uint32_t rl = __double2loint(wr), il = __double2loint(wi), nlw = __double2loint(wn);
-            const uint32_t rh = __double2hiint(wr), ih = __double2hiint(wi), nh = __double2hiint(wn);
+          {
             uint8_t* sb = sB + buf * kQBStage;
             const uint32_t o0 = boff(2 * bmu, 2 * bnu), o1 = boff(2 * bmu + 1, 2 * bnu);
-#define FAR10_B(SI, X, Y, Z_, SEL)                                                                        \
-  {                                                                                                      \
-    *(uint16_t*)(sb + SI * kQBSlice + o0) = (uint16_t)(__byte_perm(X, Y, SEL) ^ 0x8080u);                 \
-    *(uint16_t*)(sb + SI * kQBSlice + o1) = (uint16_t)(__byte_perm(Z_, X, SEL) ^ 0x8080u);                \
-  }
-            FAR10_B(0, rh, nh, ih, 0x51) FAR10_B(1, rh, nh, ih, 0x40)
-            FAR10_B(2, rl, nlw, il, 0x73) FAR10_B(3, rl, nlw, il, 0x62)
-            FAR10_B(4, rl, nlw, il, 0x51) FAR10_B(5, rl, nlw, il, 0x40)
-#undef FAR10_B
+#pragma unroll
+            for (int si = 0; si < kQSl; ++si) {
+              *(uint16_t*)(sb + si * kQBSlice + o0) = (uint16_t)bw0[si];
+              *(uint16_t*)(sb + si * kQBSlice + o1) = (uint16_t)bw1[si];
+            }
           }
           tc::wait_st();
           tc::fence_proxy_async();
           tc::fence_before();
-          tc::mbar_arrive_a(full_a + 8 * buf);
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_a(full_a + 8 * buf);
+          if (ntb > 0) {  // leftover columns on the FP64 pipe (lead CTA; no buffer access)
+            const double sx = e * cs, sy = -e * sn;
+#pragma unroll
+            for (int tl = 0; tl < 2; ++tl) {
+              if (tl < ntb) {
+                const double2 zz = lzs[2 * j + tl], xv = xs[bnu * kQXP + kQT + tl];
+                const double ax = zz.x * xv.x - zz.y * xv.y, ay = zz.x * xv.y + zz.y * xv.x;
+                lacc[tl].x = fma(sx, ax, fma(-sy, ay, lacc[tl].x));
+                lacc[tl].y = fma(sx, ay, fma(sy, ax, lacc[tl].y));
+              }
+            }
+          }
         }
       }
     }
@@ -443,12 +478,15 @@ __global__ void __launch_bounds__(256) xmax_kernel(const double2* __restrict__ x
 }  // namespace
 
 cudaError_t launch_far10(const Far10Args& a, int nseg, int ntile, cudaStream_t st) {
-  const size_t need = 2 * (size_t)kQBStage + sizeof(double2) * (2 * (size_t)kQKC * kQXP) +
+  static const int nb = [] { const char* e = getenv("BEM_FAR10_NB"); return e ? atoi(e) : 2; }();
+  const size_t need = (nb == 3 ? 3 * (size_t)kQBStage + kQSl * (size_t)kQASlice : 2 * (size_t)kQBStage) +
+                      sizeof(double2) * (2 * (size_t)kQKC * kQXP) +
                       sizeof(double) * (8 * (size_t)a.rcap + (size_t)kQN * kQT) + 64;
   const size_t smem = need > kQMinSmem ? need : kQMinSmem;
-  cudaError_t e = cudaFuncSetAttribute(far10_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto k = nb == 3 ? far10_kernel<3> : far10_kernel<2>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  far10_kernel<<<dim3((unsigned)(nseg * a.nch), (unsigned)ntile, 1u), kQThreads, smem, st>>>(a);
+  k<<<dim3((unsigned)(nseg * a.nch), (unsigned)ntile, 1u), kQThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

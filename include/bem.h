@@ -327,6 +327,12 @@ bem_status bem_debug_sharded_step(int32_t G, bem_op* ops, const bem_c128* const*
  * layouts of the INT8 coupling kernel (far10) against plain integer arithmetic. */
 bem_status bem_debug_i8_gemm(const int8_t* A, const int8_t* B, int32_t* D, int32_t K, int32_t N, int32_t mode,
                              int32_t device);
+/* The CTA-pair form (cta_group::2, M = 256) on a cluster of two CTAs: A host [256][K],
+ * B host [N][K], D host [256][N]; K a multiple of 32 in [32, 512], N a multiple of 32 in
+ * [32, 128].  Pins the operand split the paired far10 relies on (CTA r: A rows 128 r..,
+ * B rows r N/2..). */
+bem_status bem_debug_i8_gemm_pair(const int8_t* A, const int8_t* B, int32_t* D, int32_t K, int32_t N,
+                                  int32_t device);
 /* tcgen05 kind::i8 issue-rate microbenchmark (far10's MMA pattern: groups of 21 MMAs, M = 128,
  * K = 32, N in {32, 64, 128, 256}; mode 0: A in tensor memory, 1: A in shared memory): int8 MACs/s over
  * all SMs and tensor-core cycles per MMA on SM 0. */

@@ -50,7 +50,7 @@ EXPORTS = [
     "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count", "bem_debug_fp64_peak_ex",
     "bem_op_get_info", "bem_comm_unique_id", "bem_comm_init", "bem_comm_destroy", "bem_shard_frequencies",
     "bem_time_step_sharded", "bem_debug_aca_blocks", "bem_debug_sharded_step", "bem_debug_i8_gemm",
-    "bem_debug_i8_rate",
+    "bem_debug_i8_rate", "bem_debug_i8_gemm_pair",
 ]
 
 
@@ -108,6 +108,7 @@ def lib():
         "bem_debug_sharded_step": [i32, vp, vp, vp, d, vp],
         "bem_debug_i8_gemm": [vp, vp, vp, i32, i32, i32, i32],
         "bem_debug_i8_rate": [i32, i32, i32, i32, vp, vp],
+        "bem_debug_i8_gemm_pair": [vp, vp, vp, i32, i32, i32],
     }
     for name, args in sig.items():
         f = getattr(L, name)

@@ -204,3 +204,88 @@ extern "C" bem_status bem_debug_i8_rate(int32_t N, int32_t mode, int32_t iters, 
   *cycles_per_mma = (double)h[0] / mmas;
   return BEM_OK;
 }
+
+// ---- CTA-pair (cta_group::2) layout test: D = A B^T with M = 256 over a cluster of two
+// CTAs.  CTA r holds A rows [128 r, 128 r + 128) in its TMEM and B rows [r N/2, (r + 1) N/2)
+// in its shared memory; each CTA reads its 128 D rows x N columns back from its TMEM.
+namespace bem {
+namespace {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    i8_pair_test_kernel(const int8_t* __restrict__ A, const int8_t* __restrict__ B, int32_t* __restrict__ D, int K,
+                        int N) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t taddr_s;
+  __shared__ __align__(8) uint64_t ready, done;
+  const int t = threadIdx.x, w = t >> 5;
+  const uint32_t rank = tc::cluster_rank();
+  const int nh = N / 2;
+  for (int i = t; i < nh * K / 16; i += 128) {
+    const int n = i / (K / 16), kc = i % (K / 16);
+    *(uint4*)(sm + canon_off(n, kc * 16, K)) = *(const uint4*)(B + (size_t)(rank * nh + n) * K + kc * 16);
+  }
+  if (w == 0) tc::tmem_alloc2(&taddr_s, 256);
+  if (t == 0) {
+    tc::mbar_init(&ready, 2);
+    tc::mbar_init(&done, 1);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  tc::fence_before();
+  tc::cluster_sync();
+  tc::fence_after();
+  const uint32_t tD = taddr_s, tA = taddr_s + 128;
+  const uint32_t lane_base = (uint32_t)(w * 32) << 16;
+  for (int c = 0; c < K / 4; c += 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = *(const uint32_t*)(A + (size_t)(rank * 128 + t) * K + (c + j) * 4);
+    tc::tmem_st8(tA + lane_base + c, v);
+  }
+  tc::wait_st();
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  if (t == 0) tc::mbar_arrive_remote(tc::smem_u32(&ready), 0);
+  if (rank == 0 && w == 0) {
+    tc::mbar_wait_a(tc::smem_u32(&ready), 0);
+    tc::fence_after();
+    const uint32_t id = tc::idesc_i8(256, N);
+    for (int kk = 0; kk < K / 32; ++kk)
+      tc::mma2_i8_ts_warp(tD, tA + kk * 8, tc::smem_desc(tc::smem_u32(sm) + kk * 256, 128, K * 8), id, kk > 0);
+    tc::mma2_commit_mc_warp(tc::smem_u32(&done), 3);
+  }
+  tc::mbar_wait_a(tc::smem_u32(&done), 0);
+  tc::fence_after();
+  for (int c = 0; c < N; c += 16) {
+    uint32_t v[16];
+    tc::tmem_ld16(tD + lane_base + c, v);
+    tc::wait_ld();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) D[(size_t)(rank * 128 + t) * N + c + j] = (int32_t)v[j];
+  }
+  tc::fence_before();
+  tc::cluster_sync();
+  if (w == 0) tc::tmem_dealloc2(taddr_s, 256);
+}
+}  // namespace
+}  // namespace bem
+
+extern "C" bem_status bem_debug_i8_gemm_pair(const int8_t* A, const int8_t* B, int32_t* D, int32_t K, int32_t N,
+                                             int32_t device) {
+  using namespace bem;
+  BEM_REQ(A && B && D, "bem_debug_i8_gemm_pair: NULL argument");
+  BEM_REQ(K >= 32 && K <= 512 && K % 32 == 0, "bem_debug_i8_gemm_pair: K must be a multiple of 32 in [32, 512]");
+  BEM_REQ(N >= 32 && N <= 128 && N % 32 == 0, "bem_debug_i8_gemm_pair: N must be a multiple of 32 in [32, 128]");
+  DeviceGuard dg(device);
+  DBuf<int8_t> dA, dB;
+  DBuf<int32_t> dD;
+  BEM_CK(dA.alloc((size_t)256 * K)); BEM_CK(dB.alloc((size_t)N * K)); BEM_CK(dD.alloc((size_t)256 * N));
+  BEM_CK(cudaMemcpy(dA.p, A, (size_t)256 * K, cudaMemcpyHostToDevice));
+  BEM_CK(cudaMemcpy(dB.p, B, (size_t)N * K, cudaMemcpyHostToDevice));
+  const size_t smem = (size_t)(N / 2) * K;
+  BEM_CK(cudaFuncSetAttribute(i8_pair_test_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  i8_pair_test_kernel<<<2, 128, smem>>>(dA.p, dB.p, dD.p, K, N);
+  BEM_CK(cudaGetLastError());
+  BEM_CK(cudaDeviceSynchronize());
+  BEM_CK(cudaMemcpy(D, dD.p, sizeof(int32_t) * 256 * N, cudaMemcpyDeviceToHost));
+  return BEM_OK;
+}

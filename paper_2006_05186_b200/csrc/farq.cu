@@ -28,8 +28,6 @@
 // shared-memory read bandwidth spent on it), B in shared memory (canonical K-major
 // layout).  Two stages in flight: the threads build stage s + 1 while the tensor
 // cores run stage s (completion through an mbarrier per stage buffer).
-#include <cstdlib>
-
 #include "common.cuh"
 #include "far_common.cuh"
 #include "fastmath.cuh"
@@ -49,9 +47,10 @@ constexpr int kQSl = 6;               // byte slices per operand
 constexpr int kQBSlice = kQN * 32;    // bytes of one B slice tile [64][32]
 constexpr int kQBStage = kQSl * kQBSlice;
 constexpr uint32_t kQCols = 512;      // TMEM: six level accumulators [0, 384), A of stages 0, 1 [384, 480)
-constexpr int kQASlice = kQT * 32;    // bytes of one A slice tile [128][32] (shared-memory stage)
 constexpr uint32_t kQAcol = 384;
 constexpr uint32_t kQIdesc = tc::idesc_i8(kQT, kQN);
+constexpr int kQNB = 2;               // pipeline stages, both A stages in TMEM (a third stage with A in shared
+                                      // memory measured slower: 982 vs 930 ms at config 4)
 constexpr size_t kQMinSmem = 116 * 1024;  // one CTA per SM (it owns all 512 TMEM columns)
 
 // canonical K-major no-swizzle offset of (n, k) in a [64][32] int8 tile: 8-row x 16-byte
@@ -102,8 +101,6 @@ __device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool ok)
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// NB: pipeline stages (2: both A stages in TMEM; 3: the third stage's A in shared memory)
-template <int kQNB>
 __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) {
   extern __shared__ __align__(1024) uint8_t smq[];
   __shared__ uint32_t taddr_s;
@@ -115,9 +112,8 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
   __shared__ double zred[kQProd / kQT][kQT];
   __shared__ double redmin[kQProd / 32], redmax[kQProd / 32];
   const int p = a.p, m = a.m;
-  uint8_t* sB = smq;                                          // 3 x [6][64][32] int8
-  uint8_t* sA2 = smq + kQNB * kQBStage;                       // [6][128][32] int8: A of stage buffer 2 (NB = 3)
-  double2* xsb = (double2*)(sA2 + (kQNB == 3 ? kQSl * kQASlice : 0));  // 2 x [16][kQXP]
+  uint8_t* sB = smq;                                          // 2 x [6][64][32] int8
+  double2* xsb = (double2*)(smq + kQNB * kQBStage);           // 2 x [16][kQXP]
   double2* svs = xsb + 2 * kQKC * kQXP;                       // [rcap] pivot frequencies s_{k_j}
   double* sig = (double*)(svs + a.rcap);                      // [rcap] sigma_j
   double* isig = sig + a.rcap;                                // [rcap] 2^46 / sigma_j
@@ -176,23 +172,13 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
         tc::mbar_wait_a(full_a + 8 * buf, use & 1);
         tc::fence_after();
         const uint32_t sbb = tc::smem_u32(sB + buf * kQBStage);
-        if (buf < 2) {
-          const uint32_t ta = tA0 + buf * 48;
+        const uint32_t ta = tA0 + buf * 48;
 #pragma unroll
-          for (int ia = 0; ia < kQSl; ++ia)
+        for (int ia = 0; ia < kQSl; ++ia)
 #pragma unroll
-            for (int ib = 0; ib < kQSl - ia; ++ib)
-              tc::mma_i8_ts_warp(tD + (uint32_t)(ia + ib) * kQN, ta + ia * 8,
-                                 tc::smem_desc(sbb + ib * kQBSlice, 128, 256), kQIdesc, (s == 0 && ia == 0) ? 0u : 1u);
-        } else {
-          const uint32_t saa = tc::smem_u32(sA2);
-#pragma unroll
-          for (int ia = 0; ia < kQSl; ++ia)
-#pragma unroll
-            for (int ib = 0; ib < kQSl - ia; ++ib)
-              tc::mma_i8_ss_warp(tD + (uint32_t)(ia + ib) * kQN, tc::smem_desc(saa + ia * kQASlice, 128, 256),
-                                 tc::smem_desc(sbb + ib * kQBSlice, 128, 256), kQIdesc, (s == 0 && ia == 0) ? 0u : 1u);
-        }
+          for (int ib = 0; ib < kQSl - ia; ++ib)
+            tc::mma_i8_ts_warp(tD + (uint32_t)(ia + ib) * kQN, ta + ia * 8,
+                               tc::smem_desc(sbb + ib * kQBSlice, 128, 256), kQIdesc, (s == 0 && ia == 0) ? 0u : 1u);
         tc::mma_commit_warp_a(empty_a + 8 * buf);
         if (++buf == kQNB) { buf = 0; ++use; }
       }
@@ -383,7 +369,7 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
           if (stage >= kQNB) tc::mbar_wait_a(empty_a + 8 * buf, ((stage / kQNB) - 1) & 1);
           tc::fence_after();
           // slice si = 5 - byte: bytes 5, 4 from the hi words, 3 .. 0 from the lo words
-          if (buf < 2) {
+          {
             const uint32_t ta = tA0 + buf * 48 + lane_base + 2 * q4;
             tc::tmem_st2(ta + 0 * 8, hi0[1], hi1[1]);
             tc::tmem_st2(ta + 1 * 8, hi0[0], hi1[0]);
@@ -391,14 +377,6 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
             tc::tmem_st2(ta + 3 * 8, lo0[2], lo1[2]);
             tc::tmem_st2(ta + 4 * 8, lo0[1], lo1[1]);
             tc::tmem_st2(ta + 5 * 8, lo0[0], lo1[0]);
-          } else {  // canonical K-major [128][32] tiles: row t_l, bytes 8 q4 .. 8 q4 + 7
-            uint8_t* pa = sA2 + (t_l >> 3) * 256 + (q4 >> 1) * 128 + (t_l & 7) * 16 + (q4 & 1) * 8;
-            *(uint2*)(pa + 0 * kQASlice) = make_uint2(hi0[1], hi1[1]);
-            *(uint2*)(pa + 1 * kQASlice) = make_uint2(hi0[0], hi1[0]);
-            *(uint2*)(pa + 2 * kQASlice) = make_uint2(lo0[3], lo1[3]);
-            *(uint2*)(pa + 3 * kQASlice) = make_uint2(lo0[2], lo1[2]);
-            *(uint2*)(pa + 4 * kQASlice) = make_uint2(lo0[1], lo1[1]);
-            *(uint2*)(pa + 5 * kQASlice) = make_uint2(lo0[0], lo1[0]);
           }
           {
             uint8_t* sb = sB + buf * kQBStage;
@@ -478,15 +456,12 @@ __global__ void __launch_bounds__(256) xmax_kernel(const double2* __restrict__ x
 }  // namespace
 
 cudaError_t launch_far10(const Far10Args& a, int nseg, int ntile, cudaStream_t st) {
-  static const int nb = [] { const char* e = getenv("BEM_FAR10_NB"); return e ? atoi(e) : 2; }();
-  const size_t need = (nb == 3 ? 3 * (size_t)kQBStage + kQSl * (size_t)kQASlice : 2 * (size_t)kQBStage) +
-                      sizeof(double2) * (2 * (size_t)kQKC * kQXP) +
+  const size_t need = kQNB * (size_t)kQBStage + sizeof(double2) * (2 * (size_t)kQKC * kQXP) +
                       sizeof(double) * (8 * (size_t)a.rcap + (size_t)kQN * kQT) + 64;
   const size_t smem = need > kQMinSmem ? need : kQMinSmem;
-  auto k = nb == 3 ? far10_kernel<3> : far10_kernel<2>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(far10_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<dim3((unsigned)(nseg * a.nch), (unsigned)ntile, 1u), kQThreads, smem, st>>>(a);
+  far10_kernel<<<dim3((unsigned)(nseg * a.nch), (unsigned)ntile, 1u), kQThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

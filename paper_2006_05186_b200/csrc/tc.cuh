@@ -168,8 +168,18 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t addr, uint32_t cta) 
   asm volatile(
       "{\n\t.reg .b32 ra;\n\t"
       "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
-      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(addr),
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(addr),
       "r"(cta)
+      : "memory");
+}
+// wait with cluster-scope acquire (arrivals released by the peer CTA)
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
       : "memory");
 }
 __device__ __forceinline__ uint32_t cluster_rank() {

@@ -28,6 +28,8 @@
 // shared-memory read bandwidth spent on it), B in shared memory (canonical K-major
 // layout).  Two stages in flight: the threads build stage s + 1 while the tensor
 // cores run stage s (completion through an mbarrier per stage buffer).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "far_common.cuh"
 #include "fastmath.cuh"
@@ -41,8 +43,6 @@ constexpr int kQRW = 32;              // mu rows per CTA
 constexpr int kQN = 2 * kQRW;         // MMA N: (mu, Re/Im output part)
 constexpr int kQKC = 16;              // nu per stage (MMA K = 32 bytes)
 constexpr int kQXP = kQT + 2;         // x^ chunk row: tile columns, then <= 2 leftover columns
-constexpr int kQProd = 512;               // producer threads (16 warps)
-constexpr int kQThreads = kQProd + 32;    // + the MMA-issue warp
 constexpr int kQSl = 6;               // byte slices per operand
 constexpr int kQBSlice = kQN * 32;    // bytes of one B slice tile [64][32]
 constexpr int kQBStage = kQSl * kQBSlice;
@@ -92,8 +92,9 @@ __device__ __forceinline__ double kmag(double r, double sre, const double* etab)
   return (sre >= 0.0 ? fast::exp_neg_tab(-sre * r, etab) : exp(-sre * r)) * (0.079577471545947667884 / r);
 }
 
+template <int NP>
 __device__ __forceinline__ void prod_sync() {  // the producer warps only (named barrier 1)
-  asm volatile("bar.sync 1, %0;" ::"n"(kQProd) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(NP) : "memory");
 }
 __device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool ok) {  // zero-fill when !ok
   const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
@@ -101,7 +102,18 @@ __device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool ok)
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-__global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) {
+// PW producer warps (16: one B slice entry and 4 nu of A per thread per stage, 96 registers;
+// 8: two B entries and 8 nu, 168 registers -- fewer warps, more independent work per thread)
+template <int PW>
+__global__ void __launch_bounds__(PW * 32 + 32, 1) far10_kernel(const Far10Args a) {
+  constexpr int kQProd = PW * 32;        // producer threads
+  constexpr int kQThreads = kQProd + 32;  // + the MMA-issue warp
+  constexpr int NQ = kQProd / kQT;        // nu groups per frequency column (4 / 2)
+  constexpr int NUP = kQKC / NQ;          // nu of A per producer thread per stage (4 / 8)
+  constexpr int NG = NUP / 2;             // A words per slice per thread (2 / 4)
+  constexpr int NCOL = kQN / NQ;          // accumulator columns per thread (16 / 32)
+  constexpr int EB = kQRW * kQKC / kQProd;  // B slice entries per thread per stage (1 / 2)
+  static_assert(EB == 1 || EB == 2, "far10: 8 or 16 producer warps");
   extern __shared__ __align__(1024) uint8_t smq[];
   __shared__ uint32_t taddr_s;
   __shared__ __align__(8) uint64_t full[kQNB], empty[kQNB], drained;
@@ -146,10 +158,12 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
   // producer roles: A / readout (frequency column t_l, quarter q4: nu 4 q4 .. 4 q4 + 3 of a
   // stage, accumulator columns 16 q4 .. 16 q4 + 15 = rows mu 8 q4 .. 8 q4 + 7); B (slice entry
   // (bmu, bnu) of a stage)
-  const int t_l = tid & (kQT - 1), q4 = (tid >> 7) & 3;
+  const int t_l = tid & (kQT - 1), q4 = (tid >> 7) & (NQ - 1);
   const int tg = tc0 + t_l;
   const bool tv = tid < kQProd && t_l < ncol && tg < a.nl && (a.mask == nullptr || a.mask[tg]);
-  const int bmu = (tid >> 4) & 31, bnu = tid & 15;
+  // B: EB = 1: entry (bmu, bnu); EB = 2: entries (bmu, bnu), (bmu, bnu + 1), bnu even
+  const int bmu = EB == 1 ? (tid >> 4) & 31 : (tid >> 3) & 31;
+  const int bnu = EB == 1 ? tid & 15 : 2 * (tid & 7);
   const bool cta_on = __syncthreads_or(tv || (lead && tid < a.tb && (a.mask == nullptr || a.mask[tid]))) != 0;
   tc::fence_after();
   const uint32_t tD = taddr_s, tA0 = taddr_s + kQAcol;
@@ -187,9 +201,9 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
   } else {
     // ================= producer warps
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    double* acc = accs + (16 * q4) * kQT + t_l;  // this thread's 16 columns, stride kQT
+    double* acc = accs + (NCOL * q4) * kQT + t_l;  // this thread's NCOL columns, stride kQT
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i * kQT] = 0.0;
+    for (int i = 0; i < NCOL; ++i) acc[i * kQT] = 0.0;
     double2 lacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
     uint32_t stage = 0;
     int pending = 0;        // a block whose accumulators still have to be read out
@@ -200,9 +214,9 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
       tc::fence_after();
       const double hs = et_prev * 0x1p-28, ls = et_prev * 0x1p-52;
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
+      for (int g = 0; g < NCOL / 8; ++g) {
         uint32_t d0[8], d1[8], d2[8], d3[8], d4[8], d5[8];
-        const uint32_t col = tD + lane_base + 16 * q4 + 8 * g;
+        const uint32_t col = tD + lane_base + NCOL * q4 + 8 * g;
         tc::tmem_ld8(col + 0 * kQN, d0);
         tc::tmem_ld8(col + 1 * kQN, d1);
         tc::tmem_ld8(col + 2 * kQN, d2);
@@ -242,7 +256,7 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
       const double2 *zD, *zL;
       int zst;
       zrows(a.z, b, a.nl, a.tb, tc0, zD, zL, zst);
-      prod_sync();  // every producer done with the previous block's smem (sig, svs, x^)
+      prod_sync<kQProd>();  // every producer done with the previous block's smem (sig, svs, x^)
       stage_x(xh, 0, xsb);  // chunk 0 in flight during the prologue
       // (1) r_min and r_max over this CTA's rows and the block's columns (the (r, 1/(4 pi r))
       // pair of a thread's own slice entry is recomputed per nu chunk, in a register)
@@ -262,7 +276,7 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
         rmx = fmax(rmx, __shfl_xor_sync(0xffffffffu, rmx, o));
       }
       if (lane == 0) { redmin[warp] = rmn; redmax[warp] = rmx; }
-      prod_sync();
+      prod_sync<kQProd>();
       rmn = redmin[0]; rmx = redmax[0];
 #pragma unroll
       for (int w = 1; w < kQProd / 32; ++w) { rmn = fmin(rmn, redmin[w]); rmx = fmax(rmx, redmax[w]); }
@@ -277,7 +291,7 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
         sig[j] = sgm;
         isig[j] = sgm > 0.0 ? 0x1p46 / sgm : 0.0;
       }
-      prod_sync();
+      prod_sync<kQProd>();
       // (3) per column t: A scale 2^(46 - e_t), readout scale 2^e_t (terms split over the quarters)
       {
         double zm = 0.0;
@@ -288,7 +302,7 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
           }
         zred[q4][t_l] = zm;
       }
-      prod_sync();
+      prod_sync<kQProd>();
       if (tid < kQT) {
         double zm = zred[0][tid];
 #pragma unroll
@@ -301,7 +315,7 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
       }
       // (4) the previous block's accumulators (its MMAs ran during this prologue)
       if (pending) readout();
-      prod_sync();  // ascl / oscl written
+      prod_sync<kQProd>();  // ascl / oscl written
       const double as_t = ascl[t_l];
       et_prev = oscl[t_l];
       pending = 1;
@@ -313,15 +327,18 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
         const int k0 = kc * kQKC;
         double2* xs = xsb + (kc & 1) * kQKC * kQXP;
         cp_async_wait_all();
-        prod_sync();  // chunk kc landed everywhere; chunk kc - 1's buffer is free
+        prod_sync<kQProd>();  // chunk kc landed everywhere; chunk kc - 1's buffer is free
         if (kc + 1 < nkc) stage_x(xh, k0 + kQKC, xsb + ((kc + 1) & 1) * kQKC * kQXP);
-        const bool bon = bmu < nrow && k0 + bnu < p;  // this thread's slice entry exists
-        double2 rw = make_double2(1.0, 0.0);           // off the slice: 1 / (4 pi r) := 0
-        if (bon) {
-          double cn[3];
-          node(a.xi + (int64_t)c * 3 * m, m, k0 + bnu, cn);
-          const double dx = cn[0] - xr[3 * bmu], dy = cn[1] - xr[3 * bmu + 1], dz = cn[2] - xr[3 * bmu + 2];
-          rw = dist_pair(dx * dx + dy * dy + dz * dz);
+        double2 rw[EB];  // (r, 1/(4 pi r)) of this thread's slice entries; off the slice (1, 0): S = 0
+#pragma unroll
+        for (int eb = 0; eb < EB; ++eb) {
+          rw[eb] = make_double2(1.0, 0.0);
+          if (bmu < nrow && k0 + bnu + eb < p) {
+            double cn[3];
+            node(a.xi + (int64_t)c * 3 * m, m, k0 + bnu + eb, cn);
+            const double dx = cn[0] - xr[3 * bmu], dy = cn[1] - xr[3 * bmu + 1], dz = cn[2] - xr[3 * bmu + 2];
+            rw[eb] = dist_pair(dx * dx + dy * dy + dz * dz);
+          }
         }
         for (int j = 0; j < rk; ++j, ++stage) {
           const uint32_t buf = stage % kQNB;
@@ -334,57 +351,80 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
           sgn = sig[jn];
           isn = isig[jn];
           // ---- compute (one basic block, no buffer access): A = Z x^ for column t_l and
-          // nu 4 q4 .. 4 q4 + 3; B = slice entry (bmu, bnu) regenerated from the kernel (far8's
-          // table exp / sincos; rw = (1, 0) off the slice gives 0)
+          // nu NUP q4 ..; B = slice entries regenerated from the kernel (far8's table exp / sincos)
           const double f = sgj * as_t;
           const double zx = zc.x * f, zy = zc.y * f;
-          double w[8];  // (re, im) of the 4 nu, as digit carriers
+          double w[2 * NUP];  // (re, im) of the NUP nu, as digit carriers
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const double2 x = xs[(4 * q4 + u) * kQXP + t_l];
+          for (int u = 0; u < NUP; ++u) {
+            const double2 x = xs[(NUP * q4 + u) * kQXP + t_l];
             w[2 * u] = fma(zx, x.x, fma(-zy, x.y, kQMagic));
             w[2 * u + 1] = fma(zx, x.y, fma(zy, x.x, kQMagic));
           }
-          double e, sn, cs;
-          kern_parts(rw, sv, etab, sctab, e, sn, cs);
-          const double es = e * isj;
-          const double wr = fma(es, cs, kQMagic), wi = fma(-es, sn, kQMagic), wn = fma(es, sn, kQMagic);
-          uint32_t lo0[4], lo1[4], hi0[2], hi1[2];
-          tr_lo(__double2loint(w[0]), __double2loint(w[1]), __double2loint(w[2]), __double2loint(w[3]), lo0);
-          tr_lo(__double2loint(w[4]), __double2loint(w[5]), __double2loint(w[6]), __double2loint(w[7]), lo1);
-          tr_hi(__double2hiint(w[0]), __double2hiint(w[1]), __double2hiint(w[2]), __double2hiint(w[3]), hi0);
-          tr_hi(__double2hiint(w[4]), __double2hiint(w[5]), __double2hiint(w[6]), __double2hiint(w[7]), hi1);
-          // B rows 2 bmu: (Re S, -Im S) at k = 2 bnu, 2 bnu + 1; 2 bmu + 1: (Im S, Re S)
-          const uint32_t rl = __double2loint(wr), il = __double2loint(wi), nlw = __double2loint(wn);
-          const uint32_t rh = __double2hiint(wr), ih = __double2hiint(wi), nh = __double2hiint(wn);
+          double e[EB], sn[EB], cs[EB], wr[EB], wi[EB], wn[EB];
+#pragma unroll
+          for (int eb = 0; eb < EB; ++eb) {
+            kern_parts(rw[eb], sv, etab, sctab, e[eb], sn[eb], cs[eb]);
+            const double es = e[eb] * isj;
+            wr[eb] = fma(es, cs[eb], kQMagic);
+            wi[eb] = fma(-es, sn[eb], kQMagic);
+            wn[eb] = fma(es, sn[eb], kQMagic);
+          }
+          uint32_t lo[NG][4], hi[NG][2];
+#pragma unroll
+          for (int g = 0; g < NG; ++g) {
+            tr_lo(__double2loint(w[4 * g]), __double2loint(w[4 * g + 1]), __double2loint(w[4 * g + 2]),
+                  __double2loint(w[4 * g + 3]), lo[g]);
+            tr_hi(__double2hiint(w[4 * g]), __double2hiint(w[4 * g + 1]), __double2hiint(w[4 * g + 2]),
+                  __double2hiint(w[4 * g + 3]), hi[g]);
+          }
+          // B rows 2 bmu: (Re S, -Im S) at k = 2 nu, 2 nu + 1; 2 bmu + 1: (Im S, Re S)
           uint32_t bw0[6], bw1[6];
+          if constexpr (EB == 1) {
+            const uint32_t rl = __double2loint(wr[0]), il = __double2loint(wi[0]), nlw = __double2loint(wn[0]);
+            const uint32_t rh = __double2hiint(wr[0]), ih = __double2hiint(wi[0]), nh = __double2hiint(wn[0]);
 #define FAR10_B(SI, X, Y, Z_, SEL)                                                                        \
   bw0[SI] = __byte_perm(X, Y, SEL) ^ 0x8080u;                                                            \
   bw1[SI] = __byte_perm(Z_, X, SEL) ^ 0x8080u;
-          FAR10_B(0, rh, nh, ih, 0x51) FAR10_B(1, rh, nh, ih, 0x40)
-          FAR10_B(2, rl, nlw, il, 0x73) FAR10_B(3, rl, nlw, il, 0x62)
-          FAR10_B(4, rl, nlw, il, 0x51) FAR10_B(5, rl, nlw, il, 0x40)
+            FAR10_B(0, rh, nh, ih, 0x51) FAR10_B(1, rh, nh, ih, 0x40)
+            FAR10_B(2, rl, nlw, il, 0x73) FAR10_B(3, rl, nlw, il, 0x62)
+            FAR10_B(4, rl, nlw, il, 0x51) FAR10_B(5, rl, nlw, il, 0x40)
 #undef FAR10_B
+          } else {  // two entries: whole 32-bit words (k = 2 bnu .. 2 bnu + 3) per row and slice
+            uint32_t l0[4], h0[2], l1[4], h1[2];
+            tr_lo(__double2loint(wr[0]), __double2loint(wn[0]), __double2loint(wr[1]), __double2loint(wn[1]), l0);
+            tr_hi(__double2hiint(wr[0]), __double2hiint(wn[0]), __double2hiint(wr[1]), __double2hiint(wn[1]), h0);
+            tr_lo(__double2loint(wi[0]), __double2loint(wr[0]), __double2loint(wi[1]), __double2loint(wr[1]), l1);
+            tr_hi(__double2hiint(wi[0]), __double2hiint(wr[0]), __double2hiint(wi[1]), __double2hiint(wr[1]), h1);
+            bw0[0] = h0[1]; bw0[1] = h0[0]; bw0[2] = l0[3]; bw0[3] = l0[2]; bw0[4] = l0[1]; bw0[5] = l0[0];
+            bw1[0] = h1[1]; bw1[1] = h1[0]; bw1[2] = l1[3]; bw1[3] = l1[2]; bw1[4] = l1[1]; bw1[5] = l1[0];
+          }
           // ---- the buffer is free once the MMAs of its previous use completed
           if (stage >= kQNB) tc::mbar_wait_a(empty_a + 8 * buf, ((stage / kQNB) - 1) & 1);
           tc::fence_after();
-          // slice si = 5 - byte: bytes 5, 4 from the hi words, 3 .. 0 from the lo words
-          {
-            const uint32_t ta = tA0 + buf * 48 + lane_base + 2 * q4;
-            tc::tmem_st2(ta + 0 * 8, hi0[1], hi1[1]);
-            tc::tmem_st2(ta + 1 * 8, hi0[0], hi1[0]);
-            tc::tmem_st2(ta + 2 * 8, lo0[3], lo1[3]);
-            tc::tmem_st2(ta + 3 * 8, lo0[2], lo1[2]);
-            tc::tmem_st2(ta + 4 * 8, lo0[1], lo1[1]);
-            tc::tmem_st2(ta + 5 * 8, lo0[0], lo1[0]);
+          {  // A: slice si = 5 - byte (bytes 5, 4 from the hi words, 3 .. 0 from the lo words)
+            const uint32_t ta = tA0 + buf * 48 + lane_base + NG * q4;
+#pragma unroll
+            for (int si = 0; si < kQSl; ++si) {
+              uint32_t v[NG];
+#pragma unroll
+              for (int g = 0; g < NG; ++g) v[g] = si < 2 ? hi[g][1 - si] : lo[g][5 - si];
+              if constexpr (NG == 2) tc::tmem_st2(ta + si * 8, v[0], v[1]);
+              else tc::tmem_st4(ta + si * 8, *reinterpret_cast<uint32_t(*)[4]>(v));
+            }
           }
           {
             uint8_t* sb = sB + buf * kQBStage;
             const uint32_t o0 = boff(2 * bmu, 2 * bnu), o1 = boff(2 * bmu + 1, 2 * bnu);
 #pragma unroll
             for (int si = 0; si < kQSl; ++si) {
-              *(uint16_t*)(sb + si * kQBSlice + o0) = (uint16_t)bw0[si];
-              *(uint16_t*)(sb + si * kQBSlice + o1) = (uint16_t)bw1[si];
+              if constexpr (EB == 1) {
+                *(uint16_t*)(sb + si * kQBSlice + o0) = (uint16_t)bw0[si];
+                *(uint16_t*)(sb + si * kQBSlice + o1) = (uint16_t)bw1[si];
+              } else {
+                *(uint32_t*)(sb + si * kQBSlice + o0) = bw0[si];
+                *(uint32_t*)(sb + si * kQBSlice + o1) = bw1[si];
+              }
             }
           }
           tc::wait_st();
@@ -393,14 +433,17 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
           __syncwarp();
           if (lane == 0) tc::mbar_arrive_a(full_a + 8 * buf);
           if (ntb > 0) {  // leftover columns on the FP64 pipe (lead CTA; no buffer access)
-            const double sx = e * cs, sy = -e * sn;
 #pragma unroll
-            for (int tl = 0; tl < 2; ++tl) {
-              if (tl < ntb) {
-                const double2 zz = lzs[2 * j + tl], xv = xs[bnu * kQXP + kQT + tl];
-                const double ax = zz.x * xv.x - zz.y * xv.y, ay = zz.x * xv.y + zz.y * xv.x;
-                lacc[tl].x = fma(sx, ax, fma(-sy, ay, lacc[tl].x));
-                lacc[tl].y = fma(sx, ay, fma(sy, ax, lacc[tl].y));
+            for (int eb = 0; eb < EB; ++eb) {
+              const double sx = e[eb] * cs[eb], sy = -e[eb] * sn[eb];
+#pragma unroll
+              for (int tl = 0; tl < 2; ++tl) {
+                if (tl < ntb) {
+                  const double2 zz = lzs[2 * j + tl], xv = xs[(bnu + eb) * kQXP + kQT + tl];
+                  const double ax = zz.x * xv.x - zz.y * xv.y, ay = zz.x * xv.y + zz.y * xv.x;
+                  lacc[tl].x = fma(sx, ax, fma(-sy, ay, lacc[tl].x));
+                  lacc[tl].y = fma(sx, ay, fma(sy, ax, lacc[tl].y));
+                }
               }
             }
           }
@@ -412,8 +455,8 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
     double2* out = a.part + (int64_t)sg.w * a.nl * p;
     if (t_l < ncol && tg < a.nl) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int mu = 8 * q4 + i;
+      for (int i = 0; i < NCOL / 2; ++i) {
+        const int mu = (NCOL / 2) * q4 + i;
         if (mu < nrow) {
           BEM_DASSERT((out - a.part) + (int64_t)tg * p + mu0 + mu < a.part_n);
           out[(int64_t)tg * p + mu0 + mu] = tv ? make_double2(acc[2 * i * kQT], acc[(2 * i + 1) * kQT]) : make_double2(0.0, 0.0);
@@ -425,7 +468,7 @@ __global__ void __launch_bounds__(kQThreads, 1) far10_kernel(const Far10Args a) 
       if (tl >= ntb) break;
       double2 v = lacc[tl];
 #pragma unroll
-      for (int o = 1; o < 16; o <<= 1) {
+      for (int o = 1; o < (EB == 1 ? 16 : 8); o <<= 1) {  // the lanes holding the row's nu
         v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
         v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
       }
@@ -456,12 +499,14 @@ __global__ void __launch_bounds__(256) xmax_kernel(const double2* __restrict__ x
 }  // namespace
 
 cudaError_t launch_far10(const Far10Args& a, int nseg, int ntile, cudaStream_t st) {
+  static const int pw = [] { const char* e = getenv("BEM_FAR10_PW"); return e ? atoi(e) : 8; }();  // r3d: 8 warps 912 ms, 16 warps 934 ms (config 4)
   const size_t need = kQNB * (size_t)kQBStage + sizeof(double2) * (2 * (size_t)kQKC * kQXP) +
                       sizeof(double) * (8 * (size_t)a.rcap + (size_t)kQN * kQT) + 64;
   const size_t smem = need > kQMinSmem ? need : kQMinSmem;
-  cudaError_t e = cudaFuncSetAttribute(far10_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto k = pw == 8 ? far10_kernel<8> : far10_kernel<16>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  far10_kernel<<<dim3((unsigned)(nseg * a.nch), (unsigned)ntile, 1u), kQThreads, smem, st>>>(a);
+  k<<<dim3((unsigned)(nseg * a.nch), (unsigned)ntile, 1u), (pw == 8 ? 8 : 16) * 32 + 32, smem, st>>>(a);
   return cudaGetLastError();
 }
 

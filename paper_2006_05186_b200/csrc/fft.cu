@@ -533,6 +533,155 @@ __device__ __forceinline__ void stockham_pipe_body(const K4Args& a, const double
   cp_async_wait1();  // nothing outstanding at exit (the trailing group is empty)
 }
 
+// ---- L = 513 = 27 * 19 (config 4): the whole transform of a column in registers, two
+// passes through shared memory instead of one per radix stage (the generic Stockham kernel
+// above is shared-memory bound: ~40 wavefronts per element at L = 513).  Cooley-Tukey with
+// n = 19 n1 + n2, k = k1 + 27 k2:
+//   X[k1 + 27 k2] = sum_{n2} W19^{n2 k2} W513^{n2 k1} sum_{n1} x[19 n1 + n2] W27^{n1 k1};
+// pass 1: thread (n2, column) reads its 27 inputs from global memory (R^n folded in), does
+// the 27-point DFT (3 x 3 x 3) in registers and the W513 twiddle, writes T[k1][n2] to shared
+// memory; pass 2: thread (k1, column) reads 19 values, does the 19-point DFT (output pairs
+// (k, 19 - k) share inputs and roots), writes its 19 output rows (R^{-n}/L folded in).
+// Roots of 27 and 19 come from the constant bank (compile-time indices after unrolling).
+__constant__ double2 kT27[2][27];  // e^{sign 2 pi i x / 27}: [0] forward (sign -1), [1] inverse
+__constant__ double2 kT19[2][19];
+constexpr int k513NC = 8;          // DOF columns per CTA (128-byte row segments)
+
+template <int INV>
+__device__ __forceinline__ void dft3(double2& a0, double2& a1, double2& a2) {
+  constexpr double s = INV ? 0.86602540378443864676 : -0.86602540378443864676;  // sign * sqrt(3) / 2
+  const double t1x = a1.x + a2.x, t1y = a1.y + a2.y, t2x = a1.x - a2.x, t2y = a1.y - a2.y;
+  const double mx = fma(-0.5, t1x, a0.x), my = fma(-0.5, t1y, a0.y);
+  a0 = make_double2(a0.x + t1x, a0.y + t1y);
+  a1 = make_double2(fma(-s, t2y, mx), fma(s, t2x, my));
+  a2 = make_double2(fma(s, t2y, mx), fma(-s, t2x, my));
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 w) {
+  return make_double2(fma(a.x, w.x, -a.y * w.y), fma(a.x, w.y, a.y * w.x));
+}
+// in-place 9-point DFT (n = 3 n1 + n2, k = k1 + 3 k2); twiddles W9^x = W27^{3x}
+template <int INV>
+__device__ __forceinline__ void dft9(double2 (&v)[9]) {
+  double2 u[3][3];  // u[k1][n2]
+#pragma unroll
+  for (int n2 = 0; n2 < 3; ++n2) {
+    double2 a0 = v[n2], a1 = v[3 + n2], a2 = v[6 + n2];
+    dft3<INV>(a0, a1, a2);
+    u[0][n2] = a0;
+    u[1][n2] = n2 == 0 ? a1 : cmulc(a1, kT27[INV][(3 * n2) % 27]);
+    u[2][n2] = n2 == 0 ? a2 : cmulc(a2, kT27[INV][(6 * n2) % 27]);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < 3; ++k1) {
+    dft3<INV>(u[k1][0], u[k1][1], u[k1][2]);
+#pragma unroll
+    for (int k2 = 0; k2 < 3; ++k2) v[k1 + 3 * k2] = u[k1][k2];
+  }
+}
+// in-place 27-point DFT (n = 9 n1 + n2, k = k1 + 3 k2)
+template <int INV>
+__device__ __forceinline__ void dft27(double2 (&v)[27]) {
+  double2 u[3][9];  // u[k1][n2]
+#pragma unroll
+  for (int n2 = 0; n2 < 9; ++n2) {
+    double2 a0 = v[n2], a1 = v[9 + n2], a2 = v[18 + n2];
+    dft3<INV>(a0, a1, a2);
+    u[0][n2] = a0;
+    u[1][n2] = n2 == 0 ? a1 : cmulc(a1, kT27[INV][n2 % 27]);
+    u[2][n2] = n2 == 0 ? a2 : cmulc(a2, kT27[INV][(2 * n2) % 27]);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < 3; ++k1) {
+    dft9<INV>(u[k1]);
+#pragma unroll
+    for (int k2 = 0; k2 < 9; ++k2) v[k1 + 3 * k2] = u[k1][k2];
+  }
+}
+
+template <int INV>
+__global__ void __launch_bounds__(256, 2) k513_kernel(const double2* __restrict__ in, double2* __restrict__ out,
+                                                      int64_t M, const double2* __restrict__ roots,
+                                                      const double* __restrict__ scale) {
+  constexpr int L = 513, NC = k513NC;
+  extern __shared__ double2 sm513[];
+  double2* T = sm513;          // [k1][n2][c]
+  double2* W = T + L * NC;     // roots
+  const int tid = threadIdx.x;
+  const int64_t c0 = (int64_t)blockIdx.x * NC;
+  for (int i = tid; i < L; i += blockDim.x) W[i] = roots[i];
+  __syncthreads();
+  if (tid < 19 * NC) {  // pass 1
+    const int c = tid % NC, n2 = tid / NC;
+    const bool ok = c0 + c < M;
+    double2 v[27];
+#pragma unroll
+    for (int n1 = 0; n1 < 27; ++n1) {
+      const int n = 19 * n1 + n2;
+      double2 x = ok ? in[(int64_t)n * M + c0 + c] : make_double2(0.0, 0.0);
+      if (!INV) { const double sc = scale[n]; x.x *= sc; x.y *= sc; }
+      v[n1] = x;
+    }
+    dft27<INV>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < 27; ++k1) T[(k1 * 19 + n2) * NC + c] = k1 == 0 ? v[0] : cmulc(v[k1], W[(n2 * k1) % L]);
+  }
+  __syncthreads();
+  if (tid < 27 * NC) {  // pass 2
+    const int c = tid % NC, k1 = tid / NC;
+    double2 v[19];
+#pragma unroll
+    for (int n2 = 0; n2 < 19; ++n2) v[n2] = T[(k1 * 19 + n2) * NC + c];
+    if (c0 + c < M) {
+      double2* o = out + c0 + c;
+      double sx = v[0].x, sy = v[0].y;
+#pragma unroll
+      for (int r = 1; r < 19; ++r) { sx += v[r].x; sy += v[r].y; }
+      {
+        double2 y = make_double2(sx, sy);
+        if (INV) { const double sc = scale[k1]; y.x *= sc; y.y *= sc; }
+        o[(int64_t)k1 * M] = y;
+      }
+#pragma unroll
+      for (int k = 1; k <= 9; ++k) {
+        double sac = v[0].x, sbd = 0.0, sad = 0.0, sbc = v[0].y;
+#pragma unroll
+        for (int r = 1; r < 19; ++r) {
+          const double2 w = kT19[INV][(r * k) % 19];
+          sac = fma(v[r].x, w.x, sac);
+          sbd = fma(v[r].y, w.y, sbd);
+          sad = fma(v[r].x, w.y, sad);
+          sbc = fma(v[r].y, w.x, sbc);
+        }
+        const int ka = k1 + 27 * k, kb = k1 + 27 * (19 - k);
+        double2 ya = make_double2(sac - sbd, sad + sbc), yb = make_double2(sac + sbd, sbc - sad);
+        if (INV) {
+          const double sa = scale[ka], sb = scale[kb];
+          ya.x *= sa; ya.y *= sa; yb.x *= sb; yb.y *= sb;
+        }
+        o[(int64_t)ka * M] = ya;
+        o[(int64_t)kb * M] = yb;
+      }
+    }
+  }
+}
+
+bool k513_tables_ready = false;
+std::mutex k513_mu;
+cudaError_t k513_tables() {  // per device process: constant tables (idempotent)
+  std::lock_guard<std::mutex> lk(k513_mu);
+  if (k513_tables_ready) return cudaSuccess;
+  double2 t27[2][27], t19[2][19];
+  for (int d = 0; d < 2; ++d) {
+    const double sg = d ? 1.0 : -1.0;
+    for (int x = 0; x < 27; ++x) t27[d][x] = make_double2(std::cos(2.0 * M_PI * x / 27.0), sg * std::sin(2.0 * M_PI * x / 27.0));
+    for (int x = 0; x < 19; ++x) t19[d][x] = make_double2(std::cos(2.0 * M_PI * x / 19.0), sg * std::sin(2.0 * M_PI * x / 19.0));
+  }
+  cudaError_t e = cudaMemcpyToSymbol(kT27, t27, sizeof(t27));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(kT19, t19, sizeof(t19));
+  if (e == cudaSuccess) k513_tables_ready = true;
+  return e;
+}
+
 constexpr int kMaxRows = 2048;
 struct RowTab {
   const double2* p[kMaxRows];
@@ -609,6 +758,17 @@ bem_status fft_transform_rows(const double* in, double* out, int64_t M, int N, d
     smem = sizeof(double2) * (size_t)a.NC * pl->P;
   }
   unsigned grid = (unsigned)((M + a.NC - 1) / a.NC);
+  static const int k513_env = [] { const char* e = getenv("BEM_FFT_513"); return e ? atoi(e) : 1; }();
+  if (pl->stock && pl->L == 513 && mode == 0 && k513_env) {
+    BEM_CK(k513_tables());
+    const unsigned g = (unsigned)((M + k513NC - 1) / k513NC);
+    const int sm = (int)sizeof(double2) * 513 * (k513NC + 1);
+    auto kk = inverse ? k513_kernel<1> : k513_kernel<0>;
+    BEM_CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    kk<<<g, 256, sm, st>>>(a.in, a.out, M, a.roots, a.scale);
+    BEM_CK(cudaGetLastError());
+    return BEM_OK;
+  }
   if (pipe) {
     auto k = rt ? (void*)stockham_pipe_rows_kernel : (void*)stockham_pipe_kernel;
     BEM_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

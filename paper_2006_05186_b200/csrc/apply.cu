@@ -553,8 +553,9 @@ __global__ void __launch_bounds__(kPassThreads) down_leaf_p_kernel(const int32_t
 
 // frequencies per CTA of the pipelined leaf kernels: about eight 16-frequency sub-tiles
 inline int leaf_chunk(int nl) {
+  static const int per = [] { const char* e = getenv("BEM_LEAF_SUB"); return e ? std::max(1, atoi(e)) : 8; }();
   const int nsub = (nl + kLeafT - 1) / kLeafT;
-  const int nch = (nsub + 7) / 8;
+  const int nch = (nsub + per - 1) / per;  // CTAs per leaf, each pipelining <= per 16-column sub-tiles
   return kLeafT * ((nsub + nch - 1) / nch);
 }
 inline bool leaf_pipe() {
@@ -781,7 +782,9 @@ bem_status run_up(Tree& t, const double* W, const double2* xc, double2* xhat, in
   }
   BEM_CK(cudaGetLastError());
   // Kronecker transfers: TF frequencies per CTA with four [TF][p] tiles in shared memory
-  const int TF = std::max(1, std::min(16, (int)(kTransferSmem / (sizeof(double2) * 4 * p))));
+  static const int tf_env = [] { const char* e = getenv("BEM_K2_TF"); return e ? atoi(e) : 0; }();
+  // r3g sweep (config 4, up / down ms): TF 13 (56 KB budget) 2.62 / 3.05, TF 4 2.28 / 2.77, TF 8 2.27 / 2.88
+  const int TF = tf_env > 0 ? tf_env : std::min(4, std::max(1, (int)(kTransferSmem / (sizeof(double2) * 4 * p))));
   const size_t sm_k = sizeof(double2) * 4 * (size_t)TF * p + sizeof(double) * 6 * t.m * t.m;
   const unsigned ttk = (unsigned)((nl + TF - 1) / TF);
   if (t.d_E1.p) {
@@ -815,7 +818,8 @@ bem_status run_down(Tree& t, double2* yhat, const double2* yc, double2* y, int n
                     cudaStream_t st, cudaEvent_t wait_before_leaf = nullptr) {
   const int p = t.p;
   const unsigned tt = (unsigned)((nl + kPassT - 1) / kPassT);
-  const int TF = std::max(1, std::min(16, (int)(kTransferSmem / (sizeof(double2) * 5 * p))));
+  static const int tf_env = [] { const char* e = getenv("BEM_K2_TF"); return e ? atoi(e) : 0; }();
+  const int TF = tf_env > 0 ? tf_env : std::min(4, std::max(1, (int)(kTransferSmem / (sizeof(double2) * 5 * p))));
   const size_t sm_k = sizeof(double2) * 5 * (size_t)TF * p + sizeof(double) * 6 * t.m * t.m;
   const unsigned ttk = (unsigned)((nl + TF - 1) / TF);
   const size_t sm_tr = sizeof(double2) * kPassT * p + sizeof(double) * 2 * (size_t)p * p;

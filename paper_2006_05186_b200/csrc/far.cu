@@ -1049,11 +1049,11 @@ static FarGeom far_geom(const Op& op) {
   g.fk = op.far_kernel != 0 ? op.far_kernel : 10;
   if (op.force_generic || op.n_segs == 0) { g.fk = 0; return g; }
   if (g.fk == 10) {
-    // far10 (farq.cu): 128-column frequency tiles, <= 2 leftover columns on the FP64 pipe;
-    // int32 level sums stay exact for ranks <= 160
+    // far10 (farq.cu): 128-column frequency tiles, <= 2 leftover columns on the FP64 pipe
+    // (the per-term tables in shared memory bound the rank capacity)
     int tb = nl % kFar10Tile;
     if (tb > 2 || tb == nl) tb = 0;
-    if (p <= 128 && op.rmax <= 160 && nl > tb) {
+    if (p <= 128 && op.rcap <= 512 && nl > tb) {
       g.tb = tb; g.nd = nl - tb; g.TT = kFar10Tile; g.ntiles = (g.nd + kFar10Tile - 1) / kFar10Tile;
       g.ZW = g.tb + g.TT;
       return g;
@@ -1163,6 +1163,11 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
         Far10Args a;
         a.nl = nl; a.m = t.m; a.p = p; a.rcap = op.rcap; a.tb = g.tb; a.nd = g.nd; a.tile0 = fac ? tile : 0;
         a.nch = (p + 31) / 32;
+        // level l sums <= 5 u8 x s8 + 1 s8 x s8 slice products per k byte: <= 179584 per k,
+        // K = 32 bytes per nu chunk and term
+        a.gmax = std::max(1, (int)(2147483647LL / (179584LL * 32 * ((p + 15) / 16))));
+        if (const char* ge = getenv("BEM_FAR10_GMAX"))  // tests: force term groups
+          if (atoi(ge) > 0) a.gmax = std::min(a.gmax, atoi(ge));
         a.segs = (const int4*)op.d_segs.p; a.far_sorted = t.d_far_sorted.p; a.far_c = t.d_far_c.p;
         a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
         a.z = z; a.xhat = xhat; a.xmax = op.d_xmax.p; a.part = (double2*)op.d_part.p; a.mask = op.d_mask;

@@ -23,6 +23,7 @@ struct Far10Args {
   int nl, m, p, rcap, tb, nd;
   int tile0 = 0;  // first frequency tile of this launch (grid y offset)
   int nch = 1;    // mu chunks of 32 rows (grid x = segment * nch + chunk)
+  int gmax = 1;   // ACA terms per readout group (int32 level sums stay below 2^31)
   int64_t part_n = 0;
   const int4* segs;
   const int32_t* far_sorted;

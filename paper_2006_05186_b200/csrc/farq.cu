@@ -4,8 +4,8 @@
 // as complex FP64 products emulated exactly on tcgen05.mma kind::i8 (DESIGN.md §7,
 // "far10").  B200's FP64 path (DMMA / DFMA) peaks at 37 TFLOP/s while its INT8 tensor
 // cores run 8192 MACs per clock per SM; every FP64 operand is written as a 48-bit
-// fixed-point number of six signed bytes (balanced digits: d_i = byte_i(v + 0x80..80) - 128),
-// and the 21 byte-slice products with i + j <= 5 (weights 2^{8(10-i-j)}) are
+// fixed-point number of six bytes (A: two's complement bytes, the top one signed; B: balanced
+// signed digits), and the 21 byte-slice products with i + j <= 5 (weights 2^{8(10-i-j)}) are
 // accumulated exactly in int32 tensor-memory accumulators, one per level i + j
 // (dropped levels and the roundings to 48 bits: ~4e-13 relative per block product,
 // far below the 1e-10 parity bar).
@@ -16,9 +16,9 @@
 //     |e^{-s r}| / (4 pi r) (f has no interior maximum for any Re s);
 //   A (Z_b[j, t] sigma_j xhat_c[nu, t]): per frequency column t the power of two above
 //     max_j |Z_b[j, t]| sigma_j * max_nu |xhat_c[nu, t]|.
-// Per block the six level accumulators are read out, recombined in int64 and
-// added to FP64 register accumulators (readout after every block keeps every int32
-// sum below 2^31 for ranks <= 160).
+// After every block (and every group of gmax ACA terms of a long block: level sums are
+// bounded by 179584 per contracted byte, so gmax = floor((2^31 - 1) / (179584 K_term))) the
+// six level accumulators are read out, recombined in int64 and added to FP64 accumulators.
 //
 // GEMM per stage (one ACA term j, 16 nu): D[t][n] (M = 128 frequency columns,
 // N = 64 = 32 mu rows x (Re, Im)) += A[t][k] B[n][k], K = 32 bytes = 16 nu x (Re, Im):
@@ -48,7 +48,10 @@ constexpr int kQBSlice = kQN * 32;    // bytes of one B slice tile [64][32]
 constexpr int kQBStage = kQSl * kQBSlice;
 constexpr uint32_t kQCols = 512;      // TMEM: six level accumulators [0, 384), A of stages 0, 1 [384, 480)
 constexpr uint32_t kQAcol = 384;
-constexpr uint32_t kQIdesc = tc::idesc_i8(kQT, kQN);
+// slice products: A's top slice (index 0) signed, its other slices unsigned; B balanced (signed)
+__device__ __forceinline__ constexpr uint32_t qidesc(int ia, int ib) {
+  return tc::idesc_i8s(kQT, kQN, ia == 0 ? 1 : 0, 1);
+}
 constexpr int kQNB = 2;               // pipeline stages, both A stages in TMEM (a third stage with A in shared
                                       // memory measured slower: 982 vs 930 ms at config 4)
 constexpr size_t kQMinSmem = 116 * 1024;  // one CTA per SM (it owns all 512 TMEM columns)
@@ -59,26 +62,31 @@ __device__ __forceinline__ uint32_t boff(int n, int k) {
   return (uint32_t)((n >> 3) * 256 + (k >> 4) * 128 + (n & 7) * 16 + (k & 15));
 }
 
-// Fixed-point conversion on the FP64 pipe: for |v| < 2^47, v + kQMagic (= 1.5 2^52 + C,
-// C = 0x808080808080) rounds v to the nearest integer and leaves C + v in the low 48 bits
-// of the double (exponent fixed), so bytes 0..5 of the bit pattern are the biased digits
-// (digit_i = byte_i - 128, i.e. byte_i ^ 0x80 read as a signed byte).
-constexpr double kQMagic = 6896688841130112.0;  // 1.5 * 2^52 + 0x808080808080
+// Fixed-point conversion on the FP64 pipe: for |v| < 2^47, v + 1.5 2^52 rounds v to the
+// nearest integer and leaves v mod 2^48 (two's complement) in the low 48 bits of the double
+// (exponent fixed).  A operand (kQMagicA): v = d5 2^40 + sum_{i<5} d_i 2^{8i} with d5 = byte 5
+// read as a signed byte, d_0..d_4 = bytes 0..4 read as unsigned bytes (no fix-up at all).
+// B operand (kQMagicB = 1.5 2^52 + 0x808080808080): balanced digits byte_i(v + C) - 128 =
+// byte_i ^ 0x80 read as signed bytes.  One zero-mean operand keeps the dropped slice levels
+// (i + j >= 6) unbiased: with unsigned lower digits on both sides the truncation error adds
+// up linearly (measured: config 4 rel. error 3.2e-10 instead of ~1e-12).
+constexpr double kQMagicA = 6755399441055744.0;  // 1.5 * 2^52
+constexpr double kQMagicB = 6896688841130112.0;  // 1.5 * 2^52 + 0x808080808080
 
 // 4 x 4 byte transpose of the low words of four digit carriers: out[b] = byte b of (a, b, c, d)
-// packed little-endian, as balanced signed digits (slice 5 - b); hi words give slices 1, 0
+// packed little-endian (slice 5 - b); hi words give slices 1, 0
 __device__ __forceinline__ void tr_lo(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t (&o)[4]) {
   const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(c, d, 0x5140);
   const uint32_t t2 = __byte_perm(a, b, 0x7362), t3 = __byte_perm(c, d, 0x7362);
-  o[0] = __byte_perm(t0, t1, 0x5410) ^ 0x80808080u;
-  o[1] = __byte_perm(t0, t1, 0x7632) ^ 0x80808080u;
-  o[2] = __byte_perm(t2, t3, 0x5410) ^ 0x80808080u;
-  o[3] = __byte_perm(t2, t3, 0x7632) ^ 0x80808080u;
+  o[0] = __byte_perm(t0, t1, 0x5410);
+  o[1] = __byte_perm(t0, t1, 0x7632);
+  o[2] = __byte_perm(t2, t3, 0x5410);
+  o[3] = __byte_perm(t2, t3, 0x7632);
 }
 __device__ __forceinline__ void tr_hi(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t (&o)[2]) {
   const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(c, d, 0x5140);
-  o[0] = __byte_perm(t0, t1, 0x5410) ^ 0x80808080u;
-  o[1] = __byte_perm(t0, t1, 0x7632) ^ 0x80808080u;
+  o[0] = __byte_perm(t0, t1, 0x5410);
+  o[1] = __byte_perm(t0, t1, 0x7632);
 }
 
 // the slice entry's modulus and phase factors (kern_tab's intermediates): S = e (cs, -sn)
@@ -177,10 +185,10 @@ __global__ void __launch_bounds__(PW * 32 + 32, 1) far10_kernel(const Far10Args 
     uint32_t stage = 0, blk = 0;
     for (int bi = sg.y; bi < bend; ++bi) {
       const int rk = a.rank[a.far_sorted[bi]];
-      if (rk == 0) continue;
-      if (blk > 0) tc::mbar_wait_a(drained_a, (blk - 1) & 1);  // previous block read out
+      for (int g0 = 0; g0 < rk; g0 += a.gmax, ++blk) {  // term groups (int32 sums stay exact)
+      if (blk > 0) tc::mbar_wait_a(drained_a, (blk - 1) & 1);  // previous group read out
       tc::fence_after();
-      const int ns = rk * nkc;
+      const int ns = (min(rk, g0 + a.gmax) - g0) * nkc;
       uint32_t buf = stage % kQNB, use = stage / kQNB;
       for (int s = 0; s < ns; ++s, ++stage) {
         tc::mbar_wait_a(full_a + 8 * buf, use & 1);
@@ -192,11 +200,11 @@ __global__ void __launch_bounds__(PW * 32 + 32, 1) far10_kernel(const Far10Args 
 #pragma unroll
           for (int ib = 0; ib < kQSl - ia; ++ib)
             tc::mma_i8_ts_warp(tD + (uint32_t)(ia + ib) * kQN, ta + ia * 8,
-                               tc::smem_desc(sbb + ib * kQBSlice, 128, 256), kQIdesc, (s == 0 && ia == 0) ? 0u : 1u);
+                               tc::smem_desc(sbb + ib * kQBSlice, 128, 256), qidesc(ia, ib), (s == 0 && ia == 0) ? 0u : 1u);
         tc::mma_commit_warp_a(empty_a + 8 * buf);
         if (++buf == kQNB) { buf = 0; ++use; }
       }
-      ++blk;
+      }
     }
   } else {
     // ================= producer warps
@@ -319,10 +327,18 @@ __global__ void __launch_bounds__(PW * 32 + 32, 1) far10_kernel(const Far10Args 
       const double as_t = ascl[t_l];
       et_prev = oscl[t_l];
       pending = 1;
-      // (5) stages: nu chunks (x^ chunk double-buffered), then the ACA terms
-      double2 znext = tv ? zD[tg] : make_double2(0.0, 0.0);
-      double2 svn = svs[0];
-      double sgn = sig[0], isn = isig[0];
+      // (5) term groups of <= gmax terms (readout between groups: every int32 level sum stays
+      // below 2^31), per group the nu chunks (x^ chunk double-buffered), then its terms
+      for (int g0 = 0; g0 < rk; g0 += a.gmax) {
+      const int g1 = min(rk, g0 + a.gmax);
+      if (g0 > 0) {
+        readout();
+        prod_sync<kQProd>();  // every producer past the previous group's x^ chunks
+        stage_x(xh, 0, xsb);
+      }
+      double2 znext = tv ? zD[(int64_t)g0 * zst + tg] : make_double2(0.0, 0.0);
+      double2 svn = svs[g0];
+      double sgn = sig[g0], isn = isig[g0];
       for (int kc = 0; kc < nkc; ++kc) {
         const int k0 = kc * kQKC;
         double2* xs = xsb + (kc & 1) * kQKC * kQXP;
@@ -340,10 +356,10 @@ __global__ void __launch_bounds__(PW * 32 + 32, 1) far10_kernel(const Far10Args 
             rw[eb] = dist_pair(dx * dx + dy * dy + dz * dz);
           }
         }
-        for (int j = 0; j < rk; ++j, ++stage) {
+        for (int j = g0; j < g1; ++j, ++stage) {
           const uint32_t buf = stage % kQNB;
           const double2 zc = znext;
-          const int jn = j + 1 < rk ? j + 1 : 0;
+          const int jn = j + 1 < g1 ? j + 1 : g0;
           znext = tv ? zD[(int64_t)jn * zst + tg] : make_double2(0.0, 0.0);
           const double2 sv = svn;
           const double sgj = sgn, isj = isn;
@@ -358,17 +374,17 @@ __global__ void __launch_bounds__(PW * 32 + 32, 1) far10_kernel(const Far10Args 
 #pragma unroll
           for (int u = 0; u < NUP; ++u) {
             const double2 x = xs[(NUP * q4 + u) * kQXP + t_l];
-            w[2 * u] = fma(zx, x.x, fma(-zy, x.y, kQMagic));
-            w[2 * u + 1] = fma(zx, x.y, fma(zy, x.x, kQMagic));
+            w[2 * u] = fma(zx, x.x, fma(-zy, x.y, kQMagicA));
+            w[2 * u + 1] = fma(zx, x.y, fma(zy, x.x, kQMagicA));
           }
           double e[EB], sn[EB], cs[EB], wr[EB], wi[EB], wn[EB];
 #pragma unroll
           for (int eb = 0; eb < EB; ++eb) {
             kern_parts(rw[eb], sv, etab, sctab, e[eb], sn[eb], cs[eb]);
             const double es = e[eb] * isj;
-            wr[eb] = fma(es, cs[eb], kQMagic);
-            wi[eb] = fma(-es, sn[eb], kQMagic);
-            wn[eb] = fma(es, sn[eb], kQMagic);
+            wr[eb] = fma(es, cs[eb], kQMagicB);
+            wi[eb] = fma(-es, sn[eb], kQMagicB);
+            wn[eb] = fma(es, sn[eb], kQMagicB);
           }
           uint32_t lo[NG][4], hi[NG][2];
 #pragma unroll
@@ -398,6 +414,8 @@ __global__ void __launch_bounds__(PW * 32 + 32, 1) far10_kernel(const Far10Args 
             tr_hi(__double2hiint(wi[0]), __double2hiint(wr[0]), __double2hiint(wi[1]), __double2hiint(wr[1]), h1);
             bw0[0] = h0[1]; bw0[1] = h0[0]; bw0[2] = l0[3]; bw0[3] = l0[2]; bw0[4] = l0[1]; bw0[5] = l0[0];
             bw1[0] = h1[1]; bw1[1] = h1[0]; bw1[2] = l1[3]; bw1[3] = l1[2]; bw1[4] = l1[1]; bw1[5] = l1[0];
+#pragma unroll
+            for (int si = 0; si < kQSl; ++si) { bw0[si] ^= 0x80808080u; bw1[si] ^= 0x80808080u; }  // balanced
           }
           // ---- the buffer is free once the MMAs of its previous use completed
           if (stage >= kQNB) tc::mbar_wait_a(empty_a + 8 * buf, ((stage / kQNB) - 1) & 1);
@@ -448,6 +466,7 @@ __global__ void __launch_bounds__(PW * 32 + 32, 1) far10_kernel(const Far10Args 
             }
           }
         }
+      }
       }
     }
     if (pending) readout();

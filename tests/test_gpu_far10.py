@@ -99,3 +99,23 @@ def test_far10_frequency_shard(pb, torch, nloc, monkeypatch):
     y = _apply(torch, op, x)
     yo = oh.apply(O.MODE_H2ACA, s, x, local)
     assert _rel(y, yo) <= 1e-10
+
+
+def test_far10_term_groups(pb, torch, monkeypatch):
+    """Blocks longer than gmax ACA terms are read out in groups (the int32 level sums stay
+    exact); forcing groups of 3 terms changes only the FP64 summation order."""
+    V, T = synth.icosphere(3)
+    N = 256
+    M, L = len(T), N + 1
+    s = pb.cqm_frequencies(N, 2.0)
+    tree = pb.Tree(V, T, 48, 1.0, 4)
+    x = synth.random_density(13, L, M)
+    monkeypatch.setenv("BEM_FAR_KERNEL", "10")
+    y = _apply(torch, pb.Operator(tree, s, 1e-6, mode=pb.BEM_MODE_H2ACA), x)
+    monkeypatch.setenv("BEM_FAR10_GMAX", "3")
+    yg = _apply(torch, pb.Operator(tree, s, 1e-6, mode=pb.BEM_MODE_H2ACA), x)
+    assert _rel(yg, y) <= 1e-13
+    lsel = np.array([0, 1, 128, 256])
+    oh = O.H2(V, T, 48, 1.0, 4)
+    oh.aca(s, 1e-6, keep=lsel)
+    assert _rel(yg[lsel], oh.apply(O.MODE_H2ACA, s, x[lsel], lsel)) <= 1e-10

@@ -665,11 +665,15 @@ __global__ void __launch_bounds__(256, 2) k513_kernel(const double2* __restrict_
   }
 }
 
-bool k513_tables_ready = false;
+bool k513_tables_ready[64] = {};
 std::mutex k513_mu;
-cudaError_t k513_tables() {  // per device process: constant tables (idempotent)
+cudaError_t k513_tables() {  // constant tables of the current device (idempotent per device)
+  int dev = 0;
+  cudaError_t e0 = cudaGetDevice(&dev);
+  if (e0 != cudaSuccess) return e0;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
   std::lock_guard<std::mutex> lk(k513_mu);
-  if (k513_tables_ready) return cudaSuccess;
+  if (k513_tables_ready[dev]) return cudaSuccess;
   double2 t27[2][27], t19[2][19];
   for (int d = 0; d < 2; ++d) {
     const double sg = d ? 1.0 : -1.0;
@@ -678,7 +682,7 @@ cudaError_t k513_tables() {  // per device process: constant tables (idempotent)
   }
   cudaError_t e = cudaMemcpyToSymbol(kT27, t27, sizeof(t27));
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(kT19, t19, sizeof(t19));
-  if (e == cudaSuccess) k513_tables_ready = true;
+  if (e == cudaSuccess) k513_tables_ready[dev] = true;
   return e;
 }
 

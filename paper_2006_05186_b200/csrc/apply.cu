@@ -13,6 +13,7 @@
 #include <cmath>
 
 #include "common.cuh"
+#include "near_common.cuh"
 
 namespace bem {
 namespace {
@@ -900,7 +901,15 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
   // K1 (near field) and the far branch (K2 up, K3, K2 down transfers) are independent until
   // the leaf-level scatter: unless per-kernel timers are on, K1 runs on a side stream forked
   // from st (event fork/join, graph-capturable) so both kernels share the SMs' FP64 pipes
-  const bool overlap = op.overlap && has_far && !prof;
+  // K1 fused into the far10 launch (near-field warps beside the coupling work, then a tail
+  // kernel for the items they left) where far10 runs; per-kernel timers keep the kernels apart
+  const bool fuse = !dl && has_far && !prof && far_fuses_near(op);
+  const bool overlap = op.overlap && has_far && !prof && !fuse;
+  NearArgs fna;
+  if (fuse) {
+    int F = 4;
+    near_args(op, xc, yc, fna, F);
+  }
   cudaStream_t sk1 = st;
   if (overlap) {
     if (!op.side) {
@@ -914,7 +923,7 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
     BEM_CK(cudaStreamWaitEvent(op.side, op.ev_fork, 0));
     sk1 = op.side;
   }
-  {
+  if (!fuse) {
     Nvtx nv("a3 K1 near field");
     bem_status rs = launch_near(op, xc, yc, sk1, dl);
     if (rs != BEM_OK) return rs;
@@ -930,8 +939,8 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
     if (prof) BEM_CK(cudaEventRecord(op.ev[2], st));
     bem_status rs;
     {
-      Nvtx nv("a5 K3 coupling");
-      rs = launch_far(op, xhat, yhat, st);
+      Nvtx nv(fuse ? "a5 K3 coupling + a3 K1 near field (fused)" : "a5 K3 coupling");
+      rs = launch_far(op, xhat, yhat, st, fuse ? &fna : nullptr);
     }
     if (rs != BEM_OK) return rs;
     if (prof) BEM_CK(cudaEventRecord(op.ev[3], st));

@@ -243,6 +243,11 @@ struct Op {
   StepGraph step;  // bem_time_step
   // K1 || far-branch overlap (apply.cu): side stream and fork/join events, created lazily
   bool overlap = true;
+  bool k1_fuse = true;           // K1 fused into far10 where it runs (BEM_K1_FUSE=0: separate kernel)
+  DBuf<unsigned> d_nctr;         // its item counter
+  int k1_warps = 3;              // near-field warps per far10 CTA (1..3; 9 + 3 warps x 168 registers fill an SM)
+  bool far10_persist = true;     // far10 as persistent CTAs (one per SM) taking items from d_f10ctr
+  DBuf<int32_t> d_f10ctr;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // profiling
@@ -254,7 +259,11 @@ struct Op {
 // launchers (apply.cu, near.cu, far.cu)
 bem_status apply_launch(Op& op, const double* x, double* y, cudaStream_t st, bool dl = false, double alpha = 0.0);
 bem_status launch_near(Op& op, const double2* xc, double2* yc, cudaStream_t st, bool dl = false);
-bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st);
+struct NearArgs;
+// fna != nullptr (only when far_fuses_near(op)): K1 runs inside the far10 launch (near-field warps)
+// and in a tail kernel after it, both taking items from op.d_nctr
+bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st, const NearArgs* fna = nullptr);
+bool far_fuses_near(const Op& op);
 bem_status far_prepare(Op& op);  // K3 scratch of the factors-only skeleton (far.cu)
 int far_kernel_selected(const Op& op);  // the K3 kernel an apply launches (10, 8, 7; 0: generic)
 bem_status launch_near_maca(Op& op, const double2* xc, double2* yc, cudaStream_t st);  // nearm.cu

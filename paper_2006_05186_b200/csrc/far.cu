@@ -32,6 +32,8 @@
 // 6-warp CTAs, 3M complex products, split remainder rows) were removed; they
 // are in git history and profiles/r01_sweeps.md.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -1073,6 +1075,13 @@ static FarGeom far_geom(const Op& op) {
 
 int far_kernel_selected(const Op& op) { return far_geom(op).fk; }
 
+bool far_fuses_near(const Op& op) {
+  if (!op.k1_fuse || op.mode != BEM_MODE_H2ACA || op.d_nctr.p == nullptr) return false;
+  const int c = op.n_class;  // near_args's class tile must be 4 (the fused warps' F)
+  const double w4 = double((c + 3) / 4 * 4 - c) / c, w5 = double((c + 4) / 5 * 5 - c) / c;
+  return !(w4 > 0.03 && w5 < w4) && far_geom(op).fk == 10;
+}
+
 constexpr int kZgenSmem = 64 * 1024;  // zgen_tile_kernel batch buffer (4096 complex)
 
 // Factors-only skeleton: the tile buffer (sum_b r_b x ZW complex) and its per-block
@@ -1081,7 +1090,11 @@ bem_status far_prepare(Op& op) {
   if (op.ranks.empty()) return BEM_OK;
   op.rmax = *std::max_element(op.ranks.begin(), op.ranks.end());
   const FarGeom g = far_geom(op);
-  if (g.fk == 10) BEM_CK(op.d_xmax.alloc((size_t)op.tree->C * op.n_local));
+  if (g.fk == 10) {
+    BEM_CK(op.d_xmax.alloc((size_t)op.tree->C * op.n_local));
+    BEM_CK(op.d_nctr.alloc(1));
+    BEM_CK(op.d_f10ctr.alloc(1));
+  }
   if (op.z_stored) return BEM_OK;
   if (g.fk == 0) {
     set_error("bem_assemble_h2_aca: factors-only skeleton needs the tiled coupling kernels (p <= 128)");
@@ -1097,7 +1110,7 @@ bem_status far_prepare(Op& op) {
   return BEM_OK;
 }
 
-bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st) {
+bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st, const NearArgs* fna) {
   Tree& t = *op.tree;
   const int nl = op.n_local, p = t.p;
   const bool aca = op.mode == BEM_MODE_H2ACA || op.mode == BEM_MODE_COMBINED;  // far blocks via the MACA skeleton
@@ -1172,7 +1185,14 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
         a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
         a.z = z; a.xhat = xhat; a.xmax = op.d_xmax.p; a.part = (double2*)op.d_part.p; a.mask = op.d_mask;
         a.part_n = (int64_t)op.d_part.n / 2;
-        BEM_CK(launch_far10(a, op.n_segs, ntile, st));
+        if (fna != nullptr) {
+          if (tile == 0) BEM_CK(cudaMemsetAsync(op.d_nctr.p, 0, sizeof(unsigned), st));
+          a.na = *fna;
+          a.nctr = op.d_nctr.p;
+          a.n_items = (unsigned)(fna->M * (int64_t)((fna->n_class + 3) / 4));
+        }
+        a.ctr = op.far10_persist ? op.d_f10ctr.p : nullptr;
+        BEM_CK(launch_far10(a, op.n_segs, ntile, st, fna != nullptr ? op.k1_warps : 0));
       } else if (g.fk == 8) {
         const Far8Cfg& f8 = g.f8;
         Far8Args a;
@@ -1198,6 +1218,14 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
     seg_reduce_kernel<<<op.n_seg_rows, 256, 0, st>>>(op.d_seg_rows.p, op.d_seg_ptr.p, (const double2*)op.d_part.p,
                                                      yhat, (int64_t)nl * p);
     BEM_CK(cudaGetLastError());
+    if (fna != nullptr) {
+      if (g.fk != 10) {
+        set_error("launch_far: K1 fusion needs far10");
+        return BEM_ESTATE;
+      }
+      bem_status rs = launch_near_tail(*fna, 4, op.d_nctr.p, st);  // the K1 items the fused warps left
+      if (rs != BEM_OK) return rs;
+    }
     return BEM_OK;
   }
   if (fac) {

@@ -4,6 +4,7 @@
 // Z_b[j, t] live (stored pool or the factors-only tile buffer).
 #pragma once
 #include "common.cuh"
+#include "near_common.cuh"
 #include "fastmath.cuh"
 
 namespace bem {
@@ -24,6 +25,8 @@ struct Far10Args {
   int tile0 = 0;  // first frequency tile of this launch (grid y offset)
   int nch = 1;    // mu chunks of 32 rows (grid x = segment * nch + chunk)
   int gmax = 1;   // ACA terms per readout group (int32 level sums stay below 2^31)
+  int gx = 0, nitems = 0;  // set by launch_far10: grid x (segments x mu chunks), work items (x tiles)
+  int* ctr = nullptr;      // non-null: persistent CTAs taking work items from this counter
   int64_t part_n = 0;
   const int4* segs;
   const int32_t* far_sorted;
@@ -37,9 +40,14 @@ struct Far10Args {
   const double* xmax;  // [C][nl]: max_nu |xhat_c(nu, t)|
   double2* part;
   const int32_t* mask;
+  // K1 fused into the launch (nctr != nullptr): near-field warps take (target, class tile)
+  // items from *nctr (F = 4 classes per item) while the CTA's coupling work runs
+  NearArgs na;
+  unsigned* nctr = nullptr;
+  unsigned n_items = 0;
 };
 constexpr int kFar10Tile = 128;  // frequency columns per CTA (the MMA's M)
-cudaError_t launch_far10(const Far10Args& a, int nseg, int ntile, cudaStream_t st);
+cudaError_t launch_far10(const Far10Args& a, int nseg, int ntile, cudaStream_t st, int nearw = 0);
 cudaError_t launch_xmax(const double2* xhat, int64_t rows, int p, double* out, cudaStream_t st);
 
 namespace {

@@ -28,6 +28,14 @@
 // shared-memory read bandwidth spent on it), B in shared memory (canonical K-major
 // layout).  Two stages in flight: the threads build stage s + 1 while the tensor
 // cores run stage s (completion through an mbarrier per stage buffer).
+//
+// Persistent CTAs (default): one CTA per SM takes (segment x mu chunk, frequency tile) work
+// items from a counter; the coupling warps synchronise with named barriers only, so that
+// NEARW extra warps can run K1 (near field, a3) items from a second counter for as long as
+// the CTA's coupling work lasts (near_common.cuh; the items they leave run in a tail kernel
+// after the launch). K1 as a separate kernel never shares an SM with a far10 CTA (DESIGN.md
+// §7); 9 + 3 warps x 168 registers fill the register file.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -100,6 +108,17 @@ __device__ __forceinline__ double kmag(double r, double sre, const double* etab)
   return (sre >= 0.0 ? fast::exp_neg_tab(-sre * r, etab) : exp(-sre * r)) * (0.079577471545947667884 / r);
 }
 
+template <int ID, int N>
+__device__ __forceinline__ void named_sync() {
+  asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory");
+}
+template <int ID, int N>
+__device__ __forceinline__ bool named_or(bool v) {  // barrier over N threads, OR of v
+  uint32_t r;
+  asm volatile("{\n .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n barrier.red.or.pred q, %2, %3, p;\n selp.u32 %0, 1, 0, q;\n}"
+               : "=r"(r) : "r"((uint32_t)v), "n"(ID), "n"(N) : "memory");
+  return r != 0;
+}
 template <int NP>
 __device__ __forceinline__ void prod_sync() {  // the producer warps only (named barrier 1)
   asm volatile("bar.sync 1, %0;" ::"n"(NP) : "memory");
@@ -112,8 +131,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // PW producer warps (16: one B slice entry and 4 nu of A per thread per stage, 96 registers;
 // 8: two B entries and 8 nu, 168 registers -- fewer warps, more independent work per thread)
-template <int PW>
-__global__ void __launch_bounds__(PW * 32 + 32, 1) far10_kernel(const Far10Args a) {
+// NEARW > 0: that many extra warps run K1 (near field) items from a.nctr while the coupling work
+// of the CTA lasts (the SMs' FP64 pipes are ~20 % busy in far10; K1 cannot co-reside as a
+// separate kernel)
+template <int PW, int NEARW>
+__global__ void __launch_bounds__(PW * 32 + 32 + NEARW * 32, 1) far10_kernel(const Far10Args a) {
   constexpr int kQProd = PW * 32;        // producer threads
   constexpr int kQThreads = kQProd + 32;  // + the MMA-issue warp
   constexpr int NQ = kQProd / kQT;        // nu groups per frequency column (4 / 2)
@@ -124,6 +146,7 @@ __global__ void __launch_bounds__(PW * 32 + 32, 1) far10_kernel(const Far10Args 
   static_assert(EB == 1 || EB == 2, "far10: 8 or 16 producer warps");
   extern __shared__ __align__(1024) uint8_t smq[];
   __shared__ uint32_t taddr_s;
+  __shared__ int k3done, item_s;
   __shared__ __align__(8) uint64_t full[kQNB], empty[kQNB], drained;
   __shared__ double etab[64];
   __shared__ double2 sctab[64];
@@ -140,21 +163,11 @@ __global__ void __launch_bounds__(PW * 32 + 32, 1) far10_kernel(const Far10Args 
   double* accs = isig + a.rcap;                               // [64][128] FP64 accumulators (column-major in t)
   double2* lzs = (double2*)(accs + (size_t)kQN * kQT);        // [rcap][2] Z_b[j, leftover columns]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int4 sg = a.segs[blockIdx.x / a.nch];
-  const int r = sg.x;
-  const int tile = blockIdx.y + a.tile0;
-  const int tc0 = a.tb + tile * kQT;
-  const int ncol = min(kQT, a.tb + a.nd - tc0);
-  const bool lead = tile == 0;
-  const int ntb = lead ? a.tb : 0;  // leftover columns (FP64 path) handled by this CTA
-  const int mu0 = (blockIdx.x % a.nch) * kQRW;
-  const int nrow = min(kQRW, p - mu0);
   const int nkc = (p + kQKC - 1) / kQKC;  // nu chunks per term
-  for (int i = tid; i < 64; i += kQThreads) {
+  for (int i = tid; i < 64; i += blockDim.x) {
     etab[i] = fast::kExp2Tab[i];
     sctab[i] = fast::kSinCosTab[i];
   }
-  for (int i = tid; i < nrow; i += kQThreads) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
   if (warp == 0) tc::tmem_alloc(&taddr_s, kQCols);
   if (tid == 0) {
     for (int i = 0; i < kQNB; ++i) {
@@ -162,27 +175,70 @@ __global__ void __launch_bounds__(PW * 32 + 32, 1) far10_kernel(const Far10Args 
       tc::mbar_init(&empty[i], 1);
     }
     tc::mbar_init(&drained, kQProd / 32);
+    k3done = 0;
   }
   // producer roles: A / readout (frequency column t_l, quarter q4: nu 4 q4 .. 4 q4 + 3 of a
   // stage, accumulator columns 16 q4 .. 16 q4 + 15 = rows mu 8 q4 .. 8 q4 + 7); B (slice entry
   // (bmu, bnu) of a stage)
   const int t_l = tid & (kQT - 1), q4 = (tid >> 7) & (NQ - 1);
-  const int tg = tc0 + t_l;
-  const bool tv = tid < kQProd && t_l < ncol && tg < a.nl && (a.mask == nullptr || a.mask[tg]);
   // B: EB = 1: entry (bmu, bnu); EB = 2: entries (bmu, bnu), (bmu, bnu + 1), bnu even
   const int bmu = EB == 1 ? (tid >> 4) & 31 : (tid >> 3) & 31;
   const int bnu = EB == 1 ? tid & 15 : 2 * (tid & 7);
-  const bool cta_on = __syncthreads_or(tv || (lead && tid < a.tb && (a.mask == nullptr || a.mask[tid]))) != 0;
+  const uint32_t full_a = tc::smem_u32(&full[0]), empty_a = tc::smem_u32(&empty[0]), drained_a = tc::smem_u32(&drained);
+  __syncthreads();  // tables, barriers, TMEM address
   tc::fence_after();
   const uint32_t tD = taddr_s, tA0 = taddr_s + kQAcol;
-  const int bend = cta_on ? sg.z : sg.y;
-  const uint32_t full_a = tc::smem_u32(&full[0]), empty_a = tc::smem_u32(&empty[0]), drained_a = tc::smem_u32(&drained);
 
+  if (warp > kQProd / 32) {
+    // ================= fused K1 warps: (target, 4-class tile) items until the coupling work is done
+    if constexpr (NEARW > 0) {
+      if (a.nctr != nullptr) {
+        for (;;) {
+          if (*(volatile int*)&k3done) break;
+          unsigned i = 0;
+          if (lane == 0) i = atomicAdd(a.nctr, 1u);
+          i = __shfl_sync(0xffffffffu, i, 0);
+          if (i >= a.n_items) break;
+          near_item<4, false>(a.na, (int64_t)(i % (unsigned)a.na.M), (int)(i / (unsigned)a.na.M) * 4, etab, sctab);
+        }
+      }
+    }
+  } else {
+  // pipeline counters (mbarrier phases) run on across the work items of a persistent CTA
+  uint32_t mstage = 0, mblk = 0, pstage = 0;
+  // work items (segment x mu chunk, frequency tile): one per CTA (grid = all items), or
+  // persistent CTAs (one per SM) taking items from a.ctr (named barriers: the coupling warps only)
+  for (int it = 0;; ++it) {
+  int w;
+  if (a.ctr != nullptr) {
+    if (tid == 0) item_s = atomicAdd(a.ctr, 1);
+    named_sync<2, kQThreads>();  // also: every coupling warp is done with the previous item
+    w = item_s;
+  } else {
+    if (it > 0) break;
+    w = blockIdx.x + blockIdx.y * gridDim.x;
+  }
+  if (w >= a.nitems) break;
+  const int bx = w % a.gx;
+  const int4 sg = a.segs[bx / a.nch];
+  const int r = sg.x;
+  const int tile = w / a.gx + a.tile0;
+  const int tc0 = a.tb + tile * kQT;
+  const int ncol = min(kQT, a.tb + a.nd - tc0);
+  const bool lead = tile == 0;
+  const int ntb = lead ? a.tb : 0;  // leftover columns (FP64 path) handled by this CTA
+  const int mu0 = (bx % a.nch) * kQRW;
+  const int nrow = min(kQRW, p - mu0);
+  for (int i = tid; i < nrow; i += kQThreads) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
+  const int tg = tc0 + t_l;
+  const bool tv = tid < kQProd && t_l < ncol && tg < a.nl && (a.mask == nullptr || a.mask[tg]);
+  const bool cta_on = named_or<3, kQThreads>(tv || (lead && tid < a.tb && (a.mask == nullptr || a.mask[tid])));
+  const int bend = cta_on ? sg.z : sg.y;
   if (warp == kQProd / 32) {
     // ================= MMA-issue warp: every lane runs the loop (operands stay warp-uniform),
     // one elected lane issues -- a divergent single-thread issue loop measured ~4x slower
     // per MMA (tools/i8_rate.py: 117-156 vs 35 cycles at N = 64)
-    uint32_t stage = 0, blk = 0;
+    uint32_t &stage = mstage, &blk = mblk;
     for (int bi = sg.y; bi < bend; ++bi) {
       const int rk = a.rank[a.far_sorted[bi]];
       for (int g0 = 0; g0 < rk; g0 += a.gmax, ++blk) {  // term groups (int32 sums stay exact)
@@ -213,7 +269,7 @@ __global__ void __launch_bounds__(PW * 32 + 32, 1) far10_kernel(const Far10Args 
 #pragma unroll
     for (int i = 0; i < NCOL; ++i) acc[i * kQT] = 0.0;
     double2 lacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-    uint32_t stage = 0;
+    uint32_t& stage = pstage;
     int pending = 0;        // a block whose accumulators still have to be read out
     double et_prev = 1.0;   // its readout scale for column t_l
     auto readout = [&]() {
@@ -494,6 +550,9 @@ __global__ void __launch_bounds__(PW * 32 + 32, 1) far10_kernel(const Far10Args 
       if (bnu == 0 && bmu < nrow) out[(int64_t)tl * p + mu0 + bmu] = v;
     }
   }
+  }  // work items
+  if (tid == 0) *(volatile int*)&k3done = 1;
+  }
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(taddr_s, kQCols);
@@ -517,15 +576,30 @@ __global__ void __launch_bounds__(256) xmax_kernel(const double2* __restrict__ x
 
 }  // namespace
 
-cudaError_t launch_far10(const Far10Args& a, int nseg, int ntile, cudaStream_t st) {
+cudaError_t launch_far10(const Far10Args& a, int nseg, int ntile, cudaStream_t st, int nearw) {
   static const int pw = [] { const char* e = getenv("BEM_FAR10_PW"); return e ? atoi(e) : 8; }();  // r3d: 8 warps 912 ms, 16 warps 934 ms (config 4)
   const size_t need = kQNB * (size_t)kQBStage + sizeof(double2) * (2 * (size_t)kQKC * kQXP) +
                       sizeof(double) * (8 * (size_t)a.rcap + (size_t)kQN * kQT) + 64;
   const size_t smem = need > kQMinSmem ? need : kQMinSmem;
-  auto k = pw == 8 ? far10_kernel<8> : far10_kernel<16>;
+  const bool fused = a.nctr != nullptr && nearw > 0 && pw == 8;
+  auto k = pw != 8 ? far10_kernel<16, 0>
+           : !fused ? far10_kernel<8, 0>
+           : nearw == 1 ? far10_kernel<8, 1> : nearw == 2 ? far10_kernel<8, 2> : far10_kernel<8, 3>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<dim3((unsigned)(nseg * a.nch), (unsigned)ntile, 1u), (pw == 8 ? 8 : 16) * 32 + 32, smem, st>>>(a);
+  const unsigned nthr = (pw == 8 ? 8 : 16) * 32 + 32 + (fused ? std::min(nearw, 3) * 32 : 0);
+  Far10Args b = a;
+  b.gx = nseg * a.nch;
+  b.nitems = b.gx * ntile;
+  if (b.ctr != nullptr) {  // persistent: one CTA per SM, items from the counter (zeroed here, in stream order)
+    int dev = 0, nsm = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(b.ctr, 0, sizeof(int), st)) != cudaSuccess) return e;
+    k<<<(unsigned)std::max(1, std::min(b.nitems, nsm)), nthr, smem, st>>>(b);
+  } else {
+    k<<<dim3((unsigned)b.gx, (unsigned)ntile, 1u), nthr, smem, st>>>(b);
+  }
   return cudaGetLastError();
 }
 

@@ -119,3 +119,33 @@ def test_far10_term_groups(pb, torch, monkeypatch):
     oh = O.H2(V, T, 48, 1.0, 4)
     oh.aca(s, 1e-6, keep=lsel)
     assert _rel(yg[lsel], oh.apply(O.MODE_H2ACA, s, x[lsel], lsel)) <= 1e-10
+
+
+def test_far10_fused_near_field(pb, torch, monkeypatch):
+    """K1 fused into the far10 launch (near-field warps beside the coupling work + a tail
+    kernel for the items they leave; the default where far10 runs with 4-class tiles) gives
+    the same near field as the standalone K1 kernel -- the same per-item code, so bitwise --
+    and the same operator as the oracle. Also through the graph-replayed time step."""
+    V, T = synth.icosphere(3)
+    N = 256  # 129 classes -> 4-class tiles
+    M, L = len(T), N + 1
+    s = pb.cqm_frequencies(N, 2.0)
+    tree = pb.Tree(V, T, 48, 1.0, 4)
+    x = synth.random_density(17, L, M)
+    monkeypatch.setenv("BEM_FAR_KERNEL", "10")
+    opf = pb.Operator(tree, s, 1e-6, mode=pb.BEM_MODE_H2ACA)
+    yf = _apply(torch, opf, x)
+    monkeypatch.setenv("BEM_K1_FUSE", "0")
+    ops = pb.Operator(tree, s, 1e-6, mode=pb.BEM_MODE_H2ACA)
+    ys = _apply(torch, ops, x)
+    assert np.array_equal(yf, ys)
+    lsel = np.array([0, 1, 128, 256])
+    oh = O.H2(V, T, 48, 1.0, 4)
+    oh.aca(s, 1e-6, keep=lsel)
+    assert _rel(yf[lsel], oh.apply(O.MODE_H2ACA, s, x[lsel], lsel)) <= 1e-10
+    R = 10.0 ** (-5.0 / N)
+    xt = torch.from_numpy(synth.random_time_data(5, N, M).astype(np.complex128)).cuda()
+    yt_f = opf.time_step(xt, R)
+    yt_s = ops.time_step(xt, R)
+    torch.cuda.synchronize()
+    assert torch.equal(yt_f, yt_s)

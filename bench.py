@@ -405,7 +405,14 @@ def main():
         ms_eager = timed(lambda: step_prof(x), True)
     else:
         ms_eager = timed(lambda: step(x), True)
+    # work actually run under the underflow cutoffs (bem_op_get_work): the rooflines below count
+    # executed work only (K1 evaluations counted on the device in the last profiled apply; K3
+    # (rank x frequency column) products under the (block, tile) mask)
+    wk = op.work()
     op.set_profiling(False)
+    frac_near = (wk["near_evals_run"] / wk["near_evals_total"]
+                 if wk["near_evals_run"] >= 0 and wk["near_evals_total"] > 0 else 1.0)
+    frac_far = (wk["far_rank_cols_run"] / wk["far_rank_cols_total"] if wk["far_rank_cols_total"] > 0 else 1.0)
     # (2) headline: the same step captured once in a CUDA graph and replayed (removes the
     # host launch gaps of the ~25 small launches per step); 1 GPU only
     graph, graph_error = None, None
@@ -482,10 +489,10 @@ def main():
     if aca_far:
         # 8 flops per complex MAC of a pivot slice; 4 for the real slice S_b(s_0) (complex x real)
         kpiv = op.aca_export()["pivots"][:, 0]
-        flops_far = float(np.where(np.imag(s[kpiv]) == 0.0, 4.0, 8.0).sum()) * stats["p"] ** 2 * nl
+        flops_far = float(np.where(np.imag(s[kpiv]) == 0.0, 4.0, 8.0).sum()) * stats["p"] ** 2 * nl * frac_far
     else:  # plain H^2: one kernel evaluation per (block entry, frequency class) + the complex MACs
         flops_far = 75.0 * stats["far_blocks"] * stats["p"] ** 2 * n_class + 8.0 * stats["far_blocks"] * stats["p"] ** 2 * nl
-    evals_near = 7.0 * stats["nnz_near"] * n_class
+    evals_near = 7.0 * stats["nnz_near"] * n_class * (frac_near if base_mode != pb.BEM_MODE_COMBINED else 1.0)
     flops_near = 75.0 * evals_near  # SURVEY §8(d) model: ~75 FP64 flops per complex exponential + MACs
     near_rank = None
     if base_mode == pb.BEM_MODE_COMBINED:  # K1m: 8 flops per (slice entry, term, frequency) on DMMA
@@ -505,7 +512,7 @@ def main():
     far_kernel = op.info().get("far_kernel", 0) if aca_far else 0
     i8 = None
     if far_kernel == 10:  # far10: 4 real products per complex MAC (re/im embedding) x 21 byte-slice products
-        cmacs = float(op.aca_export()["ranks"].astype(np.float64).sum()) * stats["p"] ** 2 * nl
+        cmacs = float(op.aca_export()["ranks"].astype(np.float64).sum()) * stats["p"] ** 2 * nl * frac_far
         i8_peak, i8_src = int8_peak_tops()
         i8 = {"ops": 2.0 * 84.0 * cmacs, "peak": i8_peak,
               "src": (f"{i8_src}: 2 x bf16_tflops_sustained (MEASURED_PEAKS.json; nominal int8/bf16 dense ratio "
@@ -605,6 +612,10 @@ def main():
            "transpose": transpose,
            "mean_aca_rank": float(op.aca_export()["ranks"].mean()) if aca_far else None,
            "op": op.info(), "skeleton": op.skeleton(),
+           "work": {"k1_evals_run_frac": frac_near, "k3_rank_cols_run_frac": frac_far, "near_tau": wk["near_tau"],
+                    "far_delta": wk["far_delta"],
+                    "note": "underflow cutoffs (include/bem.h bem_op_get_work): work left out is below the rounding "
+                            "of the result; every roofline above counts executed work only"},
            "mean_near_aca_rank": near_rank}
     if vshard:
         out["config"]["parallelism"] = (f"virtual shard {args.shard_rank} of {args.shard_of}: frequency-domain apply of "

@@ -346,6 +346,24 @@ bem_status bem_debug_fp64_peak_ex(int32_t device, void* cuda_stream, int32_t mod
  * profiling enabled (bem_op_set_profiling): ms for K1, K2up, K3, K2down, other. */
 bem_status bem_op_set_profiling(bem_op op, int32_t enable);
 bem_status bem_op_get_timings(bem_op op, double* ms5);
+/* Work an apply of this op runs under the two underflow cutoffs (both are
+ * exact to the rounding of the result: |e^{-s r}| = e^{-Re s r}, eq:fundsol P:479-482, so at
+ * the strongly damped CQM frequencies the kernel underflows beyond a few mesh widths):
+ *   K1 (a3): over a warp step of 32 source panels, a frequency class with Re s r_min > near_tau
+ *     (default 42, env BEM_NEAR_TAU, 0 = off) is not evaluated;
+ *   K3 (a5, far10): a (far block, 128-frequency tile) whose compressed fibres sum_j S(s_kj) Z[j,t]
+ *     (eq:maca P:1314-1320) are bounded entrywise by far_delta / max(|s_t|, 1) for every column t
+ *     (default far_delta = 2^-70, env BEM_FAR_SKIP_LOG2 = 70, 0 = off) is not computed.
+ * far_rank_cols_*: sum over far blocks of r_b x (frequency columns), in total and under the
+ * mask (equal when no mask applies); near_evals_total = 7 nnz_near n_class, near_evals_run =
+ * the kernel evaluations K1 ran in the last apply issued with profiling enabled (-1: none).
+ * Synchronises the device. */
+typedef struct {
+  int64_t far_rank_cols_total, far_rank_cols_run;
+  int64_t near_evals_total, near_evals_run;
+  double near_tau, far_delta;
+} bem_op_work;
+bem_status bem_op_get_work(bem_op op, bem_op_work* out);
 /* Number of kernels one bem_apply_multifreq on this op launches. */
 bem_status bem_op_launch_count(bem_op op, int32_t* n);
 

@@ -37,6 +37,12 @@ class OpInfo(C.Structure):
                 ("device_bytes", C.c_int64), ("far_kernel", C.c_int32), ("reserved_", C.c_int32)]
 
 
+class OpWork(C.Structure):
+    _fields_ = [("far_rank_cols_total", C.c_int64), ("far_rank_cols_run", C.c_int64),
+                ("near_evals_total", C.c_int64), ("near_evals_run", C.c_int64),
+                ("near_tau", C.c_double), ("far_delta", C.c_double)]
+
+
 class SolveStats(C.Structure):
     _fields_ = [("iters_max", C.c_int32), ("iters_sum", C.c_int32), ("n_unconverged", C.c_int32),
                 ("pad_", C.c_int32), ("resid_max", C.c_double), ("imag_rel_max", C.c_double)]
@@ -50,7 +56,7 @@ EXPORTS = [
     "bem_op_set_profiling", "bem_op_get_timings", "bem_op_launch_count", "bem_debug_fp64_peak_ex",
     "bem_op_get_info", "bem_comm_unique_id", "bem_comm_init", "bem_comm_destroy", "bem_shard_frequencies",
     "bem_time_step_sharded", "bem_debug_aca_blocks", "bem_debug_sharded_step", "bem_debug_i8_gemm",
-    "bem_debug_i8_rate", "bem_debug_i8_gemm_pair",
+    "bem_debug_i8_rate", "bem_debug_i8_gemm_pair", "bem_op_get_work",
 ]
 
 
@@ -99,6 +105,7 @@ def lib():
         "bem_op_launch_count": [vp, vp],
         "bem_debug_fp64_peak_ex": [i32, vp, i32, vp],
         "bem_op_get_info": [vp, vp],
+        "bem_op_get_work": [vp, vp],
         "bem_comm_unique_id": [vp],
         "bem_comm_init": [vp, i32, i32, i32, vp],
         "bem_comm_destroy": [vp],
@@ -289,6 +296,12 @@ class Operator:
         assert y.dtype == torch.complex128 and y.is_contiguous() and y.shape == x.shape and y.device == x.device
         _check(lib().bem_apply_double_layer(self.h, _p(x), _p(y), float(alpha), _stream(stream)))
         return y
+
+    def work(self) -> dict:
+        """Work an apply runs under the underflow cutoffs (bem_op_get_work)."""
+        w = OpWork()
+        _check(lib().bem_op_get_work(self.h, C.byref(w)))
+        return {k: getattr(w, k) for k, _ in OpWork._fields_}
 
     def launch_count(self) -> int:
         n = C.c_int32()

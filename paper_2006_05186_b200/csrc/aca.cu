@@ -623,6 +623,8 @@ extern "C" bem_status bem_assemble_h2_aca(bem_tree th, const bem_c128* s, int32_
   if (const char* e = getenv("BEM_K1_FUSE")) op.k1_fuse = atoi(e) != 0;
   if (const char* e = getenv("BEM_K1_WARPS")) op.k1_warps = std::min(3, std::max(1, atoi(e)));
   if (const char* e = getenv("BEM_FAR10_PERSIST")) op.far10_persist = atoi(e) != 0;
+  if (const char* e = getenv("BEM_NEAR_TAU")) op.near_tau = atof(e);  // 0: no K1 underflow cutoff
+  if (const char* e = getenv("BEM_FAR_SKIP_LOG2")) op.far_delta = atoi(e) != 0 ? ldexp(1.0, -abs(atoi(e))) : 0.0;  // 0: no mask
   auto fail = [&](bem_status stt) { delete h; return stt; };
   std::vector<double> sh(2 * (size_t)L);
   for (int l = 0; l < L; ++l) { sh[2 * l] = s[l].re; sh[2 * l + 1] = s[l].im; }

@@ -888,6 +888,7 @@ bem_status apply_launch(Op& op, const double* xin, double* yout, cudaStream_t st
     for (auto& e : op.ev)
       if (!e) BEM_CK(cudaEventCreate(&e));
     BEM_CK(cudaEventRecord(op.ev[0], st));
+    if (op.d_near_evals.p) BEM_CK(cudaMemsetAsync(op.d_near_evals.p, 0, sizeof(unsigned long long), st));
   }
   Nvtx nv_apply(dl ? "apply_double_layer" : "apply_multifreq");
   const int64_t tot = M * nl;
@@ -1040,7 +1041,34 @@ extern "C" bem_status bem_op_launch_count(bem_op oh, int32_t* n) {
 
 extern "C" bem_status bem_op_set_profiling(bem_op oh, int32_t enable) {
   BEM_REQ(oh, "bem_op_set_profiling: NULL op");
-  oh->o.profile = enable != 0;
+  Op& op = oh->o;
+  op.profile = enable != 0;
+  if (op.profile && op.d_near_evals.p == nullptr) {
+    DeviceGuard dg(op.tree->device);
+    BEM_CK(op.d_near_evals.alloc(1));
+    BEM_CK(cudaMemset(op.d_near_evals.p, 0, sizeof(unsigned long long)));
+  }
+  return BEM_OK;
+}
+
+extern "C" bem_status bem_op_get_work(bem_op oh, bem_op_work* out) {
+  BEM_REQ(oh && out, "bem_op_get_work: NULL argument");
+  Op& op = oh->o;
+  DeviceGuard dg(op.tree->device);
+  BEM_CK(cudaDeviceSynchronize());
+  const bool aca = op.mode == BEM_MODE_H2ACA || op.mode == BEM_MODE_COMBINED;
+  out->far_rank_cols_run = out->far_rank_cols_total = 0;
+  if (aca) far10_work(op, &out->far_rank_cols_run, &out->far_rank_cols_total);
+  const int64_t nnz = op.mode == BEM_MODE_DENSE ? op.tree->M * op.tree->M : op.tree->nnz_near;
+  out->near_evals_total = 7 * nnz * op.n_class;
+  out->near_evals_run = -1;
+  if (op.d_near_evals.p != nullptr) {
+    unsigned long long v = 0;
+    BEM_CK(cudaMemcpy(&v, op.d_near_evals.p, sizeof(v), cudaMemcpyDeviceToHost));
+    out->near_evals_run = (int64_t)v;
+  }
+  out->near_tau = op.near_tau;
+  out->far_delta = op.d_skip.p != nullptr ? op.far_delta : 0.0;
   return BEM_OK;
 }
 

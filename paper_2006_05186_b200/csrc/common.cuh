@@ -133,6 +133,7 @@ struct Tree {
   std::vector<int32_t> leaves;                   // leaf cluster ids in DFS order
   std::vector<std::vector<int32_t>> level_nonleaf;  // non-leaf clusters per level
   int64_t nnz_near = 0;
+  double hmax = 0.0;  // largest quadrature-node-to-centroid distance (K1's underflow cutoff)
   // device, cluster order
   DBuf<int32_t> d_perm, d_begin, d_end, d_son0, d_son1, d_parent, d_leaf_of;
   DBuf<double> d_cen;    // M*3
@@ -248,6 +249,15 @@ struct Op {
   int k1_warps = 3;              // near-field warps per far10 CTA (1..3; 9 + 3 warps x 168 registers fill an SM)
   bool far10_persist = true;     // far10 as persistent CTAs (one per SM) taking items from d_f10ctr
   DBuf<int32_t> d_f10ctr;
+  // underflow cutoffs: K1 skips a class over a warp step of sources when
+  // Re s r_min > near_tau (env BEM_NEAR_TAU, 0: off); far10 skips a (block, frequency tile) whose
+  // compressed fibres are bounded by far_delta / max(|s_t|, 1) (env BEM_FAR_SKIP_LOG2, 0: off)
+  double near_tau = 42.0;
+  double far_delta = 0x1p-70;
+  DBuf<unsigned> d_skip;                 // far10: bit `tile` of d_skip[b]
+  DBuf<int32_t> d_colmap;                // far10: [tiles][128] local frequency of a tile column (-1: padding)
+  std::vector<int32_t> colmap;
+  DBuf<unsigned long long> d_near_evals;  // profiling: kernel evaluations K1 ran in the last apply
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // profiling
@@ -265,6 +275,7 @@ struct NearArgs;
 bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t st, const NearArgs* fna = nullptr);
 bool far_fuses_near(const Op& op);
 bem_status far_prepare(Op& op);  // K3 scratch of the factors-only skeleton (far.cu)
+void far10_work(Op& op, int64_t* run, int64_t* total);  // (rank x column) products run / in total (far.cu)
 int far_kernel_selected(const Op& op);  // the K3 kernel an apply launches (10, 8, 7; 0: generic)
 bem_status launch_near_maca(Op& op, const double2* xc, double2* yc, cudaStream_t st);  // nearm.cu
 bem_status h2_gather(Op& op, const double2* x, double2* xc, int ncols, cudaStream_t st);

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(256) zgen_tile_kernel(zgen::Src g, int nfar, c
                                                         const int32_t* __restrict__ local_l,
                                                         const int32_t* __restrict__ mask, int nl, int tb, int tc0,
                                                         int ncol, int lead, int ZW, int cap, double2* __restrict__ Zt,
-                                                        int64_t zt_n) {
+                                                        int64_t zt_n, const int32_t* __restrict__ cmap) {
   extern __shared__ double2 work[];
   const int ncp = tb + ncol;
   for (int b = blockIdx.x; b < nfar; b += gridDim.x) {
@@ -94,8 +94,9 @@ __global__ void __launch_bounds__(256) zgen_tile_kernel(zgen::Src g, int nfar, c
     zgen::block_columns(
         g, b, rank[b], lead ? 0 : tb, ncp,
         [&](int c) {
-          const int t = c < tb ? c : tc0 + (c - tb);
-          return (t < nl && (mask == nullptr || mask[t])) ? local_l[t] : -1;
+          // cmap (far10): the tile's columns in its damping order; else the natural order
+          const int t = c < tb ? c : cmap != nullptr ? cmap[c - tb] : tc0 + (c - tb);
+          return (t >= 0 && t < nl && (mask == nullptr || mask[t])) ? local_l[t] : -1;
         },
         work, cap, [&](int j, int c, double2 v) { out[(int64_t)j * ZW + c] = v; });
   }
@@ -1082,6 +1083,39 @@ bool far_fuses_near(const Op& op) {
   return !(w4 > 0.03 && w5 < w4) && far_geom(op).fk == 10;
 }
 
+static Far10SkipArgs far10_skip_args(Op& op, int tb, int nd, int tile_lo, int tile_hi, const ZSrc& z) {
+  Tree& t = *op.tree;
+  Far10SkipArgs a;
+  a.nfar = (int)t.far_r.size(); a.nl = op.n_local; a.m = t.m; a.rcap = op.rcap; a.tb = tb; a.nd = nd;
+  a.tile_lo = tile_lo; a.tile_hi = tile_hi; a.delta = op.far_delta;
+  a.far_r = t.d_far_r.p; a.far_c = t.d_far_c.p; a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p;
+  a.local_l = op.d_local_l.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p; a.z = z; a.skip = op.d_skip.p;
+  a.colmap = op.d_colmap.p;
+  return a;
+}
+
+// executed / total (rank x frequency column) products of the far10 coupling step under the
+// underflow mask (bench accounting); without a mask both are the total
+void far10_work(Op& op, int64_t* run, int64_t* total) {
+  const FarGeom g = far_geom(op);
+  int64_t tot = 0, r = 0;
+  std::vector<unsigned> h;
+  if (g.fk == 10 && op.d_skip.p != nullptr) {
+    h.resize(op.d_skip.n);
+    if (cudaMemcpy(h.data(), op.d_skip.p, sizeof(unsigned) * h.size(), cudaMemcpyDeviceToHost) != cudaSuccess) h.clear();
+  }
+  for (size_t b = 0; b < op.ranks.size(); ++b) {
+    tot += (int64_t)op.ranks[b] * op.n_local;
+    if (h.empty()) { r += (int64_t)op.ranks[b] * op.n_local; continue; }
+    for (int tile = 0; tile < g.ntiles; ++tile) {
+      if ((h[b] >> tile) & 1u) continue;
+      const int tc0 = g.tb + tile * g.TT;
+      r += (int64_t)op.ranks[b] * (std::min(g.TT, g.tb + g.nd - tc0) + (tile == 0 ? g.tb : 0));  // nd columns over the tiles
+    }
+  }
+  *run = r; *total = tot;
+}
+
 constexpr int kZgenSmem = 64 * 1024;  // zgen_tile_kernel batch buffer (4096 complex)
 
 // Factors-only skeleton: the tile buffer (sum_b r_b x ZW complex) and its per-block
@@ -1094,6 +1128,36 @@ bem_status far_prepare(Op& op) {
     BEM_CK(op.d_xmax.alloc((size_t)op.tree->C * op.n_local));
     BEM_CK(op.d_nctr.alloc(1));
     BEM_CK(op.d_f10ctr.alloc(1));
+    op.d_skip.release();
+    const bool masked = op.far_delta > 0.0 && g.ntiles <= 32 && op.mode == BEM_MODE_H2ACA;
+    {
+      // tile columns: the local frequencies [tb, nl) by damping (Re s ascending, stable), so that
+      // the strongly damped ones share tiles (tile 0, which carries the leftover columns, holds
+      // the least damped); the natural order without the mask
+      std::vector<int32_t> ord((size_t)g.nd);
+      for (int i = 0; i < g.nd; ++i) ord[i] = g.tb + i;
+      if (masked) {
+        std::vector<double> sh(2 * (size_t)op.L);
+        BEM_CK(cudaMemcpy(sh.data(), op.d_s.p, sizeof(double) * sh.size(), cudaMemcpyDeviceToHost));
+        std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+          return sh[2 * (size_t)op.local_l[x]] < sh[2 * (size_t)op.local_l[y]];
+        });
+      }
+      op.colmap.assign((size_t)g.ntiles * kFar10Tile, -1);
+      for (int i = 0; i < g.nd; ++i) op.colmap[i] = ord[i];
+      BEM_CK(op.d_colmap.upload(op.colmap));
+    }
+    if (masked) {
+      BEM_CK(op.d_skip.alloc(op.ranks.size()));
+      BEM_CK(cudaMemset(op.d_skip.p, 0, sizeof(unsigned) * op.ranks.size()));
+      if (op.z_stored) {  // the mask depends on the skeleton only: one pass over every tile
+        BEM_CK(cudaDeviceSynchronize());
+        ZSrc z{};
+        z.zoff = op.d_zoff.p; z.Z = (const double2*)op.d_Z.p; z.tiled = 0; z.ZW = g.ZW; z.zn = (int64_t)op.d_Z.n / 2;
+        BEM_CK(launch_far10_skip(far10_skip_args(op, g.tb, g.nd, 0, g.ntiles, z), nullptr));
+        BEM_CK(cudaDeviceSynchronize());
+      }
+    }
   }
   if (op.z_stored) return BEM_OK;
   if (g.fk == 0) {
@@ -1168,8 +1232,10 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
         const int ncol = std::min(g.TT, g.tb + nd - tc0);
         zgen_tile_kernel<<<std::min(nfar, 148 * 8), 256, kZgenSmem, st>>>(
             zsrc, nfar, op.d_rank.p, op.d_ztoff.p, op.d_local_l.p, op.d_mask, nl, g.tb, tc0, ncol, tile == 0 ? 1 : 0,
-            g.ZW, kZgenSmem / (int)sizeof(double2), (double2*)op.d_zs.p, (int64_t)op.d_zs.n / 2);
+            g.ZW, kZgenSmem / (int)sizeof(double2), (double2*)op.d_zs.p, (int64_t)op.d_zs.n / 2,
+            g.fk == 10 ? op.d_colmap.p + (size_t)tile * kFar10Tile : nullptr);
         BEM_CK(cudaGetLastError());
+        if (g.fk == 10 && op.d_skip.p != nullptr) BEM_CK(launch_far10_skip(far10_skip_args(op, g.tb, g.nd, tile, tile + 1, z), st));
       }
       if (g.fk == 10) {
         if (tile == 0) BEM_CK(launch_xmax(xhat, (int64_t)t.C * nl, p, op.d_xmax.p, st));
@@ -1185,6 +1251,8 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
         a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p;
         a.z = z; a.xhat = xhat; a.xmax = op.d_xmax.p; a.part = (double2*)op.d_part.p; a.mask = op.d_mask;
         a.part_n = (int64_t)op.d_part.n / 2;
+        a.skip = op.d_skip.p;
+        a.colmap = op.d_colmap.p;
         if (fna != nullptr) {
           if (tile == 0) BEM_CK(cudaMemsetAsync(op.d_nctr.p, 0, sizeof(unsigned), st));
           a.na = *fna;

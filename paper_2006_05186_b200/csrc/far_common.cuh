@@ -40,6 +40,10 @@ struct Far10Args {
   const double* xmax;  // [C][nl]: max_nu |xhat_c(nu, t)|
   double2* part;
   const int32_t* mask;
+  // (block, tile) underflow mask (bit `tile` of skip[b] set: the block's compressed fibres of that
+  // frequency tile are below the rounding of the result and are not computed); nullable
+  const uint32_t* skip = nullptr;
+  const int32_t* colmap = nullptr;  // [tiles][128]: local frequency of every tile column (-1: padding)
   // K1 fused into the launch (nctr != nullptr): near-field warps take (target, class tile)
   // items from *nctr (F = 4 classes per item) while the CTA's coupling work runs
   NearArgs na;
@@ -47,6 +51,23 @@ struct Far10Args {
   unsigned n_items = 0;
 };
 constexpr int kFar10Tile = 128;  // frequency columns per CTA (the MMA's M)
+// far10's (block, frequency tile) underflow mask, see far10_skip_kernel (farq.cu)
+struct Far10SkipArgs {
+  int nfar, nl, m, rcap, tb, nd;
+  int tile_lo, tile_hi;  // tiles whose bits are (re)computed
+  double delta;
+  const int32_t* far_r;
+  const int32_t* far_c;
+  const double* xi;
+  const double2* s;
+  const int32_t* local_l;
+  const int32_t* rank;
+  const int32_t* pivk;
+  ZSrc z;
+  const int32_t* colmap;
+  uint32_t* skip;
+};
+cudaError_t launch_far10_skip(const Far10SkipArgs& a, cudaStream_t st);
 cudaError_t launch_far10(const Far10Args& a, int nseg, int ntile, cudaStream_t st, int nearw = 0);
 cudaError_t launch_xmax(const double2* xhat, int64_t rows, int p, double* out, cudaStream_t st);
 

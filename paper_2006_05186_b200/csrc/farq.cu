@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(PW * 32 + 32 + NEARW * 32, 1) far10_kernel(con
   __shared__ double ascl[kQT], oscl[kQT];
   __shared__ double zred[kQProd / kQT][kQT];
   __shared__ double redmin[kQProd / 32], redmax[kQProd / 32];
+  __shared__ int cmap[kQT];  // local frequency of the tile's column t_l (-1: padding)
   const int p = a.p, m = a.m;
   uint8_t* sB = smq;                                          // 2 x [6][64][32] int8
   double2* xsb = (double2*)(smq + kQNB * kQBStage);           // 2 x [16][kQXP]
@@ -230,8 +231,12 @@ __global__ void __launch_bounds__(PW * 32 + 32 + NEARW * 32, 1) far10_kernel(con
   const int mu0 = (bx % a.nch) * kQRW;
   const int nrow = min(kQRW, p - mu0);
   for (int i = tid; i < nrow; i += kQThreads) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
-  const int tg = tc0 + t_l;
-  const bool tv = tid < kQProd && t_l < ncol && tg < a.nl && (a.mask == nullptr || a.mask[tg]);
+  // the tile's columns: a.colmap orders the local frequencies by damping (Re s ascending), so
+  // that whole tiles fall under the underflow mask; identity when the mask is off
+  const int tg = t_l < ncol ? a.colmap[tile * kQT + t_l] : -1;
+  if (tid < kQT) cmap[tid] = tg;  // read after the named_or barrier below
+  const int zt = a.z.tiled ? tc0 + t_l : tg;  // Z column: tile buffers hold the tile's columns in tile order
+  const bool tv = tid < kQProd && tg >= 0 && (a.mask == nullptr || a.mask[tg]);
   const bool cta_on = named_or<3, kQThreads>(tv || (lead && tid < a.tb && (a.mask == nullptr || a.mask[tid])));
   const int bend = cta_on ? sg.z : sg.y;
   if (warp == kQProd / 32) {
@@ -240,7 +245,9 @@ __global__ void __launch_bounds__(PW * 32 + 32 + NEARW * 32, 1) far10_kernel(con
     // per MMA (tools/i8_rate.py: 117-156 vs 35 cycles at N = 64)
     uint32_t &stage = mstage, &blk = mblk;
     for (int bi = sg.y; bi < bend; ++bi) {
-      const int rk = a.rank[a.far_sorted[bi]];
+      const int b = a.far_sorted[bi];
+      if (a.skip != nullptr && ((a.skip[b] >> tile) & 1u)) continue;  // underflow mask (same test in the producers)
+      const int rk = a.rank[b];
       for (int g0 = 0; g0 < rk; g0 += a.gmax, ++blk) {  // term groups (int32 sums stay exact)
       if (blk > 0) tc::mbar_wait_a(drained_a, (blk - 1) & 1);  // previous group read out
       tc::fence_after();
@@ -304,7 +311,7 @@ __global__ void __launch_bounds__(PW * 32 + 32 + NEARW * 32, 1) far10_kernel(con
         const int tl = idx / kQKC, nu = idx - tl * kQKC;
         int tcol;
         bool ok;
-        if (tl < kQT) { tcol = tc0 + tl; ok = tl < ncol && tcol < a.nl; }
+        if (tl < kQT) { tcol = cmap[tl]; ok = tcol >= 0; }
         else { tcol = tl - kQT; ok = tcol < ntb; }
         ok = ok && k0 + nu < p;
         cp_async16z(xs + nu * kQXP + tl, ok ? (const void*)(xh + (int64_t)tcol * p + k0 + nu) : (const void*)xh, ok);
@@ -315,6 +322,7 @@ __global__ void __launch_bounds__(PW * 32 + 32 + NEARW * 32, 1) far10_kernel(con
       const int b = a.far_sorted[bi];
       const int rk = a.rank[b];
       if (rk == 0) continue;
+      if (a.skip != nullptr && ((a.skip[b] >> tile) & 1u)) continue;
       const int c = a.far_c[b];
       const double2* xh = a.xhat + (int64_t)c * a.nl * p;
       const double2 *zD, *zL;
@@ -361,7 +369,7 @@ __global__ void __launch_bounds__(PW * 32 + 32 + NEARW * 32, 1) far10_kernel(con
         double zm = 0.0;
         if (tv)
           for (int j = q4; j < rk; j += kQProd / kQT) {
-            const double2 z = zD[(int64_t)j * zst + tg];
+            const double2 z = zD[(int64_t)j * zst + zt];
             zm = fmax(zm, sqrt(fma(z.x, z.x, z.y * z.y)) * sig[j]);
           }
         zred[q4][t_l] = zm;
@@ -392,7 +400,7 @@ __global__ void __launch_bounds__(PW * 32 + 32 + NEARW * 32, 1) far10_kernel(con
         prod_sync<kQProd>();  // every producer past the previous group's x^ chunks
         stage_x(xh, 0, xsb);
       }
-      double2 znext = tv ? zD[(int64_t)g0 * zst + tg] : make_double2(0.0, 0.0);
+      double2 znext = tv ? zD[(int64_t)g0 * zst + zt] : make_double2(0.0, 0.0);
       double2 svn = svs[g0];
       double sgn = sig[g0], isn = isig[g0];
       for (int kc = 0; kc < nkc; ++kc) {
@@ -416,7 +424,7 @@ __global__ void __launch_bounds__(PW * 32 + 32 + NEARW * 32, 1) far10_kernel(con
           const uint32_t buf = stage % kQNB;
           const double2 zc = znext;
           const int jn = j + 1 < g1 ? j + 1 : g0;
-          znext = tv ? zD[(int64_t)jn * zst + tg] : make_double2(0.0, 0.0);
+          znext = tv ? zD[(int64_t)jn * zst + zt] : make_double2(0.0, 0.0);
           const double2 sv = svn;
           const double sgj = sgn, isj = isn;
           svn = svs[jn];
@@ -528,7 +536,7 @@ __global__ void __launch_bounds__(PW * 32 + 32 + NEARW * 32, 1) far10_kernel(con
     if (pending) readout();
     // (6) this segment's partial: columns 16 q4 .. 16 q4 + 15 = rows mu 8 q4 .. 8 q4 + 7 (Re, Im)
     double2* out = a.part + (int64_t)sg.w * a.nl * p;
-    if (t_l < ncol && tg < a.nl) {
+    if (tg >= 0) {
 #pragma unroll
       for (int i = 0; i < NCOL / 2; ++i) {
         const int mu = (NCOL / 2) * q4 + i;
@@ -556,6 +564,68 @@ __global__ void __launch_bounds__(PW * 32 + 32 + NEARW * 32, 1) far10_kernel(con
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(taddr_s, kQCols);
+}
+
+// (block, frequency tile) underflow mask of the coupling step ("K3 underflow mask").
+// The compressed block of frequency t is sum_j S_b(s_{k_j}) Z_b[j, t] (eq:maca P:1314-1320); with
+// r_lb = the distance of the two clusters' node boxes, |S_b(s)[mu, nu]| = e^{-Re s r} / (4 pi r)
+// <= g_j := e^{-Re s_{k_j} r_lb} / (4 pi r_lb) (Re s >= 0), so every entry of the fibre is bounded
+// by beta_t = sum_j g_j |Z_b[j, t]|.  At the strongly damped CQM frequencies (Re s_t r >> 1) the
+// far field underflows against the O(1 / |s_t|) diagonal of V(s_t): a tile whose columns all have
+// beta_t max(|s_t|, 1) < delta (2^-70) is not computed.  The mask depends on the skeleton only
+// (not on x): one pass at assembly (stored Z) or per regenerated tile (factors-only; the Z
+// columns are bitwise the same, hence the same mask).
+__global__ void __launch_bounds__(kQT) far10_skip_kernel(const Far10SkipArgs a) {
+  __shared__ double gs[512];
+  __shared__ double gap[3];
+  const int tid = threadIdx.x;
+  for (int b = blockIdx.x; b < a.nfar; b += gridDim.x) {
+    const int rk = a.rank[b];
+    __syncthreads();  // gs / gap of the previous block
+    if (tid < 3) {
+      const double* xr = a.xi + (int64_t)a.far_r[b] * 3 * a.m + tid * a.m;
+      const double* xc = a.xi + (int64_t)a.far_c[b] * 3 * a.m + tid * a.m;
+      double lr = xr[0], hr = xr[0], lc = xc[0], hc = xc[0];
+      for (int i = 1; i < a.m; ++i) {
+        lr = fmin(lr, xr[i]); hr = fmax(hr, xr[i]);
+        lc = fmin(lc, xc[i]); hc = fmax(hc, xc[i]);
+      }
+      gap[tid] = fmax(0.0, fmax(lr - hc, lc - hr));
+    }
+    __syncthreads();
+    const double rlb = sqrt(gap[0] * gap[0] + gap[1] * gap[1] + gap[2] * gap[2]) * (1.0 - 0x1p-40);
+    for (int j = tid; j < rk; j += kQT) {
+      const double sre = a.s[a.pivk[(int64_t)b * a.rcap + j]].x;
+      gs[j] = (rlb > 0.0 && sre >= 0.0) ? exp(-sre * rlb) * (0.079577471545947667884 / rlb) * (1.0 + 0x1p-30)
+                                         : __longlong_as_double(0x7ff0000000000000LL);
+    }
+    __syncthreads();
+    uint32_t bits = a.skip[b];
+    for (int tile = a.tile_lo; tile < a.tile_hi; ++tile) {
+      const int tc0 = a.tb + tile * kQT;
+      const int ncol = min(kQT, a.tb + a.nd - tc0);
+      const double2 *zD, *zL;
+      int zst;
+      zrows(a.z, b, a.nl, a.tb, tc0, zD, zL, zst);
+      bool keep = false;
+      auto column = [&](const double2* zc, int t) {  // zc: the column's Z entries (stride zst), t: local frequency
+        double beta = 0.0;
+        for (int j = 0; j < rk; ++j) {
+          const double2 z = zc[(int64_t)j * zst];
+          beta = fma(sqrt(fma(z.x, z.x, z.y * z.y)), gs[j], beta);
+        }
+        const double2 st = a.s[a.local_l[t]];
+        const double v = beta * (1.0 + 0x1p-20) * fmax(sqrt(fma(st.x, st.x, st.y * st.y)), 1.0);
+        if (!(v < a.delta)) keep = true;  // NaN / inf keep the tile
+      };
+      const int t = tid < ncol ? a.colmap[tile * kQT + tid] : -1;
+      if (t >= 0) column(zD + (a.z.tiled ? tc0 + tid : t), t);
+      if (tile == 0 && tid < a.tb) column(zL + tid, tid);  // leftover columns ride with tile 0
+      keep = __syncthreads_or(keep) || rk > 512;
+      bits = keep ? bits & ~(1u << tile) : bits | (1u << tile);
+    }
+    if (tid == 0) a.skip[b] = bits;
+  }
 }
 
 // max_nu |xhat_c(nu, t)| for every (cluster, frequency) row: one warp per row
@@ -600,6 +670,12 @@ cudaError_t launch_far10(const Far10Args& a, int nseg, int ntile, cudaStream_t s
   } else {
     k<<<dim3((unsigned)b.gx, (unsigned)ntile, 1u), nthr, smem, st>>>(b);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_far10_skip(const Far10SkipArgs& a, cudaStream_t st) {
+  if (a.nfar <= 0 || a.tile_hi <= a.tile_lo) return cudaSuccess;
+  far10_skip_kernel<<<(unsigned)std::min(a.nfar, 148 * 16), kQT, 0, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -459,6 +459,14 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
   } while (0)
   UP(d_perm, t.perm); UP(d_begin, t.begin); UP(d_end, t.end); UP(d_son0, t.son0); UP(d_son1, t.son1);
   UP(d_parent, t.parent); UP(d_leaf_of, leaf_of);
+  t.hmax = 0.0;  // K1's underflow cutoff: r >= |c_i - c_j| - hmax for every quadrature node of panel j
+  for (int64_t k = 0; k < t.M; ++k)
+    for (int q = 0; q < 7; ++q) {
+      const double dx = qn[21 * k + 3 * q] - cen[3 * k], dy = qn[21 * k + 3 * q + 1] - cen[3 * k + 1],
+                   dz = qn[21 * k + 3 * q + 2] - cen[3 * k + 2];
+      t.hmax = std::max(t.hmax, std::sqrt(dx * dx + dy * dy + dz * dz));
+    }
+  t.hmax *= 1.0 + 0x1p-40;
   UP(d_cen, cen); UP(d_qn, qn); UP(d_qw, qw); UP(d_selfJ, sj); UP(d_area, area); UP(d_nrm, nrm); UP(d_WK, WK);
   // transposed copies for the downward pass (K2): lanes run over lambda / panel k, so
   // E^T[c][mu][lambda] and U^T[mu][k] make its loads coalesced

@@ -21,7 +21,7 @@ namespace {
 
 constexpr int kNearWarps = 4;
 
-template <int F, bool DL = false>
+template <int F, bool DL, bool CUT>
 __device__ __forceinline__ void near_body(const NearArgs& a) {
   __shared__ double etab[64];
   __shared__ double2 sctab[64];
@@ -30,7 +30,7 @@ __device__ __forceinline__ void near_body(const NearArgs& a) {
     sctab[i] = fast::kSinCosTab[i];
   }
   __syncthreads();
-  near_item<F, DL>(a, (int64_t)blockIdx.x * kNearWarps + (threadIdx.x >> 5), blockIdx.y * F, etab, sctab);
+  near_item<F, DL, CUT>(a, (int64_t)blockIdx.x * kNearWarps + (threadIdx.x >> 5), blockIdx.y * F, etab, sctab);
 }
 
 // the items K3's fused near-field warps left: (target k, class tile) = (i mod M, i div M), one
@@ -54,17 +54,18 @@ __global__ void __launch_bounds__(kNearWarps * 32) near_tail_kernel(NearArgs a, 
   }
 }
 
-template <int F>
+template <int F, bool CUT>
 __global__ void __launch_bounds__(kNearWarps * 32) near_kernel(NearArgs a) {
-  near_body<F, false>(a);
+  near_body<F, false, CUT>(a);
 }
 // double-layer near field (NEXT-1)
-__global__ void __launch_bounds__(kNearWarps * 32) near_kernel_dl(NearArgs a) { near_body<4, true>(a); }
+__global__ void __launch_bounds__(kNearWarps * 32) near_kernel_dl(NearArgs a) { near_body<4, true, false>(a); }
 
 template <int F>
 cudaError_t launch(const NearArgs& na, cudaStream_t st) {
   dim3 g((unsigned)((na.M + kNearWarps - 1) / kNearWarps), (unsigned)((na.n_class + F - 1) / F));
-  near_kernel<F><<<g, kNearWarps * 32, 0, st>>>(na);
+  if (na.tau > 0.0) near_kernel<F, true><<<g, kNearWarps * 32, 0, st>>>(na);
+  else near_kernel<F, false><<<g, kNearWarps * 32, 0, st>>>(na);
   return cudaGetLastError();
 }
 
@@ -80,6 +81,9 @@ void near_args(Op& op, const double2* xc, double2* yc, NearArgs& na, int& F) {
   na.cen = t.d_cen.p; na.qn = t.d_qn.p; na.qw = t.d_qw.p; na.nrm = t.d_nrm.p; na.selfJ = t.d_selfJ.p;
   na.s = (const double2*)op.d_s.p; na.local_l = op.d_local_l.p;
   na.class_t1 = op.d_class_t1.p; na.class_t2 = op.d_class_t2.p; na.mask = op.d_mask; na.xc = xc; na.yc = yc;
+  na.tau = op.near_tau;
+  na.hmax = t.hmax;
+  na.evals = op.profile ? op.d_near_evals.p : nullptr;
   // F = 4 classes per warp unless that pads the last class tile by more than 3 % and F = 5
   // pads less (config 2: 65 classes -> F = 5, 5.71 -> 5.64 ms; configs 3/4 keep F = 4)
   const int c = op.n_class;

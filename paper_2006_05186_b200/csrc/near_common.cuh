@@ -25,6 +25,9 @@ struct NearArgs {
   const int32_t* mask;  // nullable: per local frequency, 0 = skip (output 0)
   const double2* xc;
   double2* yc;
+  double tau = 0.0;  // underflow cutoff on Re s * r (0: off)
+  double hmax = 0.0;  // largest quadrature-node-to-centroid distance of the mesh (the cutoff's slack)
+  unsigned long long* evals = nullptr;  // profiling: += kernel evaluations run (nullable)
 };
 
 __device__ __forceinline__ void cmac(double2& acc, double2 a, double2 b) {
@@ -64,7 +67,8 @@ __device__ __forceinline__ double2 self_node(const double* qn, const double* qw,
 // x is loaded after the node loop (r01: 128 instead of 164 registers, 4 CTAs per SM).
 // one warp: target k, frequency classes c0 .. c0 + F - 1 (etab / sctab: the exp / sincos tables
 // in shared memory)
-template <int F, bool DL = false>
+// CUT: the underflow cutoff below is compiled in (a.tau <= 0 then means no cutoff)
+template <int F, bool DL = false, bool CUT = !DL>
 __device__ __forceinline__ void near_item(const NearArgs& a, int64_t k, int c0, const double* etab,
                                           const double2* sctab) {
   const int lane = threadIdx.x & 31;
@@ -103,52 +107,87 @@ __device__ __forceinline__ void near_item(const NearArgs& a, int64_t k, int c0, 
   const double cx = a.cen[3 * k], cy = a.cen[3 * k + 1], cz = a.cen[3 * k + 2];
   const int li = a.leaf_of[k];
   const int jb = a.near_jb[li], je = a.near_je[li];
+  // Underflow cutoff ("K1 underflow cutoff"): |e^{-s r}| = e^{-Re s r}, so a class
+  // whose Re s r_min exceeds a.tau over the 32 sources of a warp step adds less than e^{-tau}
+  // (tau = 42: 6e-19) of the kernel's 1/(4 pi r) scale -- below the rounding of the row sum.
+  // r_min >= min_j |c_k - c_j| - hmax (source centroids, hmax = the largest node-to-centroid
+  // distance of the mesh); the centroids are loaded one step ahead like the indices, so a
+  // skipped step costs three loads, eight flops and one warp reduction.  The decision is
+  // warp-uniform and all-or-nothing for the F classes of the tile (they are neighbours in Re s:
+  // a per-class decision would leave out 0.5 % more at config 4 and costs the kernel its
+  // instruction-level parallelism), so nothing diverges.
+  const double tau = CUT ? (a.tau > 0.0 ? a.tau : 1e300) : 0.0;
+  double smin = 1e300;  // smallest Re s of the tile's active classes
+  unsigned nact = 0;
+#pragma unroll
+  for (int f = 0; f < F; ++f)
+    if (o1[f] >= 0) { smin = fmin(smin, sre[f]); ++nact; }
+  unsigned nev = 0;  // kernel evaluations of this lane (profiling)
   int jn = jb + lane < je ? a.near_j[jb + lane] : 0;
-  for (int jj = jb + lane; jj < je; jj += 32) {
-    {
-      const int j = jn;  // index loaded one iteration ahead (one dependent global load fewer per source)
+  int jn2 = 0;
+  double ncx = 0.0, ncy = 0.0, ncz = 0.0;  // centroid of source jn
+  if (CUT) {
+    jn2 = jb + 32 + lane < je ? a.near_j[jb + 32 + lane] : 0;
+    ncx = a.cen[3 * (int64_t)jn]; ncy = a.cen[3 * (int64_t)jn + 1]; ncz = a.cen[3 * (int64_t)jn + 2];
+  }
+  for (int j0 = jb; j0 < je; j0 += 32) {
+    const int jj = j0 + lane;
+    const int j = jn;  // index loaded ahead (one dependent global load fewer per source)
+    const bool use = jj < je && j != k;  // self panel below
+    if (CUT) {
+      const double ddx = cx - ncx, ddy = cy - ncy, ddz = cz - ncz;
+      const double d2c = use ? ddx * ddx + ddy * ddy + ddz * ddz : 1e30;
+      jn = jn2;  // two steps of indices and one step of centroids in flight
+      if (jj + 64 < je) jn2 = a.near_j[jj + 64];
+      ncx = a.cen[3 * (int64_t)jn]; ncy = a.cen[3 * (int64_t)jn + 1]; ncz = a.cen[3 * (int64_t)jn + 2];
+      // warp minimum through the (monotone) bit pattern of the value rounded down to float
+      const unsigned bits = __reduce_min_sync(0xffffffffu, __float_as_uint(__double2float_rd(d2c)));
+      const double rmin = fmax((double)(sqrtf(__uint_as_float(bits)) * 0.999999f) - a.hmax, 0.0);
+      if (smin * rmin > tau) continue;
+    } else {
       if (jj + 32 < je) jn = a.near_j[jj + 32];
-      if (j == k) continue;  // self panel below
-      double2 x1[F], x2[F];
-      double2 v[F];
+    }
+    const double* qn = a.qn + 21 * (int64_t)j;
+    const double* qw = a.qw + 7 * (int64_t)j;
+    if (!use) continue;
+    nev += 7u * nact;
+    double2 x1[F], x2[F];
+    double2 v[F];
 #pragma unroll
-      for (int f = 0; f < F; ++f) v[f] = make_double2(0.0, 0.0);
-      const double* qn = a.qn + 21 * (int64_t)j;
-      const double* qw = a.qw + 7 * (int64_t)j;
-      double nx = 0.0, ny = 0.0, nz = 0.0;
-      if (DL) { nx = a.nrm[3 * (int64_t)j]; ny = a.nrm[3 * (int64_t)j + 1]; nz = a.nrm[3 * (int64_t)j + 2]; }
+    for (int f = 0; f < F; ++f) v[f] = make_double2(0.0, 0.0);
+    double nx = 0.0, ny = 0.0, nz = 0.0;
+    if (DL) { nx = a.nrm[3 * (int64_t)j]; ny = a.nrm[3 * (int64_t)j + 1]; nz = a.nrm[3 * (int64_t)j + 2]; }
 #pragma unroll 7
-      for (int q = 0; q < 7; ++q) {
-        const double dx = cx - qn[3 * q], dy = cy - qn[3 * q + 1], dz = cz - qn[3 * q + 2];
-        const double d2 = dx * dx + dy * dy + dz * dz;
-        const double ir = rsqrt(d2);
-        const double r = d2 * ir;
-        const double w = DL ? qw[q] * ((dx * nx + dy * ny) + dz * nz) * (ir * ir * ir) : qw[q] * ir;
+    for (int q = 0; q < 7; ++q) {
+      const double dx = cx - qn[3 * q], dy = cy - qn[3 * q + 1], dz = cz - qn[3 * q + 2];
+      const double d2 = dx * dx + dy * dy + dz * dz;
+      const double ir = rsqrt(d2);
+      const double r = d2 * ir;
+      const double w = DL ? qw[q] * ((dx * nx + dy * ny) + dz * nz) * (ir * ir * ir) : qw[q] * ir;
 #pragma unroll
-        for (int f = 0; f < F; ++f) {
-          const double e = fast::exp_neg_tab(-sre[f] * r, etab) * w;
-          double sn, cs;
-          fast::sincos_tab(sim[f] * r, sctab, &sn, &cs);
-          if (DL) {  // (1 + s r) e^{-s r}: (alpha + i beta)(cos - i sin) E
-            const double ea = e * fma(sre[f], r, 1.0), eb = e * (sim[f] * r);
-            v[f].x = fma(ea, cs, fma(eb, sn, v[f].x));
-            v[f].y = fma(eb, cs, fma(-ea, sn, v[f].y));
-          } else {
-            v[f].x = fma(e, cs, v[f].x);
-            v[f].y = fma(-e, sn, v[f].y);
-          }
+      for (int f = 0; f < F; ++f) {
+        const double e = fast::exp_neg_tab(-sre[f] * r, etab) * w;
+        double sn, cs;
+        fast::sincos_tab(sim[f] * r, sctab, &sn, &cs);
+        if (DL) {  // (1 + s r) e^{-s r}: (alpha + i beta)(cos - i sin) E
+          const double ea = e * fma(sre[f], r, 1.0), eb = e * (sim[f] * r);
+          v[f].x = fma(ea, cs, fma(eb, sn, v[f].x));
+          v[f].y = fma(eb, cs, fma(-ea, sn, v[f].y));
+        } else {
+          v[f].x = fma(e, cs, v[f].x);
+          v[f].y = fma(-e, sn, v[f].y);
         }
       }
+    }
 #pragma unroll
-      for (int f = 0; f < F; ++f) {
-        x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
-        x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
-      }
+    for (int f = 0; f < F; ++f) {
+      x1[f] = o1[f] >= 0 ? a.xc[o1[f] + j] : make_double2(0.0, 0.0);
+      x2[f] = o2[f] >= 0 ? a.xc[o2[f] + j] : make_double2(0.0, 0.0);
+    }
 #pragma unroll
-      for (int f = 0; f < F; ++f) {
-        cmac(acc1[f], v[f], x1[f]);
-        cmac_conj(acc2[f], v[f], x2[f]);
-      }
+    for (int f = 0; f < F; ++f) {
+      cmac(acc1[f], v[f], x1[f]);
+      cmac_conj(acc2[f], v[f], x2[f]);
     }
   }
   if (!DL) {
@@ -180,6 +219,14 @@ __device__ __forceinline__ void near_item(const NearArgs& a, int64_t k, int c0, 
       acc2[f].x += __shfl_xor_sync(0xffffffffu, acc2[f].x, off);
       acc2[f].y += __shfl_xor_sync(0xffffffffu, acc2[f].y, off);
     }
+  }
+  if (a.evals != nullptr) {
+    if (!DL && lane == 0) {  // the self panel's rule
+#pragma unroll
+      for (int f = 0; f < F; ++f) nev += o1[f] >= 0 ? 7u : 0u;
+    }
+    nev = __reduce_add_sync(0xffffffffu, nev);
+    if (lane == 0) atomicAdd(a.evals, (unsigned long long)nev);
   }
 #pragma unroll
   for (int f = 0; f < F; ++f) {

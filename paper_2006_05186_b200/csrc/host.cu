@@ -410,16 +410,54 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
   // concatenated column-leaf ranges in partition order
   std::vector<int32_t> leaf_pos(C, -1);
   for (int li = 0; li < t.n_leaves; ++li) leaf_pos[t.leaves[li]] = li;
+  // The source leaves of a target leaf are listed by increasing box distance from it (a warp
+  // step of 32 consecutive sources is then compact), and every step carries gsuf = the smallest
+  // distance of the target leaf's box to the centroid of any source from that step on: K1's
+  // underflow cutoff leaves the loop once Re s (gsuf - hmax) > tau (near_common.cuh; every later
+  // source is then out of reach too).
   std::vector<std::vector<int32_t>> per_leaf(t.n_leaves);
-  for (size_t b = 0; b < t.near_r.size(); ++b) {
-    auto& v = per_leaf[leaf_pos[t.near_r[b]]];
-    for (int j = t.begin[t.near_c[b]]; j < t.end[t.near_c[b]]; ++j) v.push_back(j);
+  {
+    auto box_dist = [&](int a, int b) {
+      double d2 = 0.0;
+      for (int k = 0; k < 3; ++k) {
+        const double gp = std::max(0.0, std::max(t.box[6 * a + k] - t.box[6 * b + 3 + k], t.box[6 * b + k] - t.box[6 * a + 3 + k]));
+        d2 += gp * gp;
+      }
+      return d2;
+    };
+    std::vector<std::vector<std::pair<double, int32_t>>> cols(t.n_leaves);
+    for (size_t b = 0; b < t.near_r.size(); ++b)
+      cols[leaf_pos[t.near_r[b]]].push_back({box_dist(t.near_r[b], t.near_c[b]), t.near_c[b]});
+    for (int li = 0; li < t.n_leaves; ++li) {
+      std::stable_sort(cols[li].begin(), cols[li].end(),
+                       [](const std::pair<double, int32_t>& x, const std::pair<double, int32_t>& y) { return x.first < y.first; });
+      for (auto& e : cols[li])
+        for (int j = t.begin[e.second]; j < t.end[e.second]; ++j) per_leaf[li].push_back(j);
+    }
   }
-  std::vector<int32_t> njb(t.n_leaves), nje(t.n_leaves), nj;
+  std::vector<int32_t> njb(t.n_leaves), nje(t.n_leaves), nj, ngb(t.n_leaves);
+  std::vector<double> gsuf;
   for (int li = 0; li < t.n_leaves; ++li) {
     njb[li] = (int32_t)nj.size();
     nj.insert(nj.end(), per_leaf[li].begin(), per_leaf[li].end());
     nje[li] = (int32_t)nj.size();
+    ngb[li] = (int32_t)gsuf.size();
+    const int n = (int)per_leaf[li].size(), ng = (n + 31) / 32;
+    const double* bx = &t.box[6 * (size_t)t.leaves[li]];
+    gsuf.resize(gsuf.size() + ng);
+    double run = 1e300;
+    for (int g = ng - 1; g >= 0; --g) {
+      for (int i = 32 * g; i < std::min(n, 32 * g + 32); ++i) {
+        const int64_t j = per_leaf[li][i];
+        double d2 = 0.0;
+        for (int k = 0; k < 3; ++k) {
+          const double gp = std::max(0.0, std::max(bx[k] - cen[3 * j + k], cen[3 * j + k] - bx[3 + k]));
+          d2 += gp * gp;
+        }
+        run = std::min(run, std::sqrt(d2) * (1.0 - 0x1p-40));
+      }
+      gsuf[ngb[li] + g] = run;
+    }
   }
   // near blocks grouped by row leaf (partition order within a row): the combined
   // mode's near-field MACA apply walks a row leaf's blocks
@@ -495,7 +533,7 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
   }
   UP(d_E1, E1);
   UP(d_U, U); UP(d_W, W); UP(d_E, E); UP(d_ET, ET); UP(d_UT, UT); UP(d_xi, t.xi); UP(d_leaves, t.leaves);
-  UP(d_near_jb, njb); UP(d_near_je, nje); UP(d_near_j, nj);
+  UP(d_near_jb, njb); UP(d_near_je, nje); UP(d_near_j, nj); UP(d_near_gb, ngb); UP(d_near_gsuf, gsuf);
   UP(d_J, rawJ); UP(d_near_r, t.near_r); UP(d_near_c, t.near_c); UP(d_nb_ptr, nb_ptr); UP(d_nb_sorted, nb_sorted);
   UP(d_far_ptr, t.far_ptr); UP(d_far_sorted, t.far_sorted); UP(d_far_r, t.far_r); UP(d_far_c, t.far_c);
   t.d_level_nonleaf.resize(t.depth + 1);

@@ -82,6 +82,8 @@ void near_args(Op& op, const double2* xc, double2* yc, NearArgs& na, int& F) {
   na.s = (const double2*)op.d_s.p; na.local_l = op.d_local_l.p;
   na.class_t1 = op.d_class_t1.p; na.class_t2 = op.d_class_t2.p; na.mask = op.d_mask; na.xc = xc; na.yc = yc;
   na.tau = op.near_tau;
+  na.near_gb = dense ? nullptr : t.d_near_gb.p;
+  na.gsuf = dense ? nullptr : t.d_near_gsuf.p;
   na.hmax = t.hmax;
   na.evals = op.profile ? op.d_near_evals.p : nullptr;
   // F = 4 classes per warp unless that pads the last class tile by more than 3 % and F = 5

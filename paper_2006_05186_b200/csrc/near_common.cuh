@@ -13,6 +13,8 @@ struct NearArgs {
   const int32_t* near_jb;
   const int32_t* near_je;
   const int32_t* near_j;
+  const int32_t* near_gb = nullptr;  // with gsuf: the cutoff's early exit (nullable)
+  const double* gsuf = nullptr;
   const double* cen;
   const double* qn;
   const double* qw;
@@ -126,6 +128,8 @@ __device__ __forceinline__ void near_item(const NearArgs& a, int64_t k, int c0, 
   int jn = jb + lane < je ? a.near_j[jb + lane] : 0;
   int jn2 = 0;
   double ncx = 0.0, ncy = 0.0, ncz = 0.0;  // centroid of source jn
+  const double* gs = CUT && a.gsuf != nullptr ? a.gsuf + a.near_gb[li] : nullptr;
+  double gnext = gs != nullptr && jb < je ? gs[0] : 0.0;  // this step's suffix distance, loaded a step ahead
   if (CUT) {
     jn2 = jb + 32 + lane < je ? a.near_j[jb + 32 + lane] : 0;
     ncx = a.cen[3 * (int64_t)jn]; ncy = a.cen[3 * (int64_t)jn + 1]; ncz = a.cen[3 * (int64_t)jn + 2];
@@ -135,6 +139,9 @@ __device__ __forceinline__ void near_item(const NearArgs& a, int64_t k, int c0, 
     const int j = jn;  // index loaded ahead (one dependent global load fewer per source)
     const bool use = jj < je && j != k;  // self panel below
     if (CUT) {
+      // every source from this step on is further than gsuf from the target leaf's box
+      if (smin * fmax(gnext - a.hmax, 0.0) > tau) break;
+      if (gs != nullptr && j0 + 32 < je) gnext = gs[(j0 - jb) / 32 + 1];
       const double ddx = cx - ncx, ddy = cy - ncy, ddz = cz - ncz;
       const double d2c = use ? ddx * ddx + ddy * ddy + ddz * ddz : 1e30;
       jn = jn2;  // two steps of indices and one step of centroids in flight

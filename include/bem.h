@@ -237,8 +237,9 @@ bem_status cqm_solve(bem_op op, const double* g_time, double* phi_time, int64_t 
 
 /* ---- multi-GPU frequency sharding over NCCL (Remark P:1607-1614) ----
  * Rank g of G owns the DOFs [M g/G, M (g+1)/G) of time-domain data and the frequency
- * classes {0}, {j, L-j} of bem_shard_frequencies (balanced contiguous class ranges,
- * conjugate pairs kept together).  NCCL is loaded at run time (libnccl.so.2).
+ * classes {0}, {j, L-j} of bem_shard_frequencies (class i -> rank i mod G: conjugate pairs
+ * kept together, every rank an even sample of the frequency circle, so the underflow cutoffs
+ * of bem_op_get_work take the same share from every rank).  NCCL is loaded at run time (libnccl.so.2).
  *   bem_comm_unique_id: 128-byte ncclUniqueId, created on one rank and broadcast by
  *     the caller (e.g. torch.distributed); ENCCL when NCCL cannot be loaded.
  *   bem_comm_init: collective over the nranks processes (ncclCommInitRank); device =

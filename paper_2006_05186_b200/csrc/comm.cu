@@ -3,8 +3,8 @@
 //
 // Layout of a G-rank run (rank g):
 //   * frequency classes {0} and {j, L-j} (j = 1..) stay whole on one rank -- K1
-//     shares one exp/sincos per conjugate pair -- in balanced contiguous class
-//     ranges (shard_frequencies below == paper_2006_05186_b200/dist.py, tested);
+//     shares one exp/sincos per conjugate pair --, class i on rank i mod G
+//     (shard_frequencies below == paper_2006_05186_b200/dist.py, tested);
 //     the op of rank g holds exactly that local frequency list, in that order;
 //   * time-domain data are DOF-sharded: rank g owns panels [M g/G, M (g+1)/G).
 // The time <-> frequency transpose is ONE all-to-all per direction, grouped
@@ -80,9 +80,8 @@ Nccl& nccl() {
 }  // namespace
 
 // Frequency shard of every rank: owner[l] = rank holding l, slot[l] = its row in that
-// rank's local list.  Classes {0}, {j, L-j} in balanced contiguous ranges: the class
-// boundary of rank g is the class whose preceding frequency count is closest to L g/G
-// (first on ties), kept strictly increasing with at least one class per rank.
+// rank's local list.  Classes {0}, {j, L-j} dealt round-robin (class i on rank i mod G, a
+// rank's classes in increasing i), at least one class per rank.
 bool shard_frequencies(int L, int G, std::vector<int>& owner, std::vector<int>& slot,
                        std::vector<std::vector<int>>* lists) {
   std::vector<std::vector<int>> cls;
@@ -93,28 +92,15 @@ bool shard_frequencies(int L, int G, std::vector<int>& owner, std::vector<int>& 
   }
   const int nc = (int)cls.size();
   if (G < 1 || G > nc) return false;
-  std::vector<long long> before(nc);
-  long long acc = 0;
-  for (int i = 0; i < nc; ++i) { before[i] = acc; acc += (long long)cls[i].size(); }
-  std::vector<int> bounds{0};
-  for (int g = 1; g < G; ++g) {
-    const double target = (double)(acc * g) / (double)G;
-    int b = 0;
-    double best = std::fabs((double)before[0] - target);
-    for (int i = 1; i < nc; ++i) {
-      const double d = std::fabs((double)before[i] - target);
-      if (d < best) { best = d; b = i; }
-    }
-    b = std::min(std::max(b, bounds.back() + 1), nc - (G - g));
-    bounds.push_back(b);
-  }
-  bounds.push_back(nc);
   owner.assign(L, -1);
   slot.assign(L, -1);
   if (lists) lists->assign(G, {});
+  // class i -> rank i mod G: every rank holds an even sample of the frequency circle, so the
+  // underflow cutoffs (K1 / K3 leave out most work of the strongly damped frequencies) take
+  // the same share from every rank
   for (int g = 0; g < G; ++g) {
     int k = 0;
-    for (int i = bounds[g]; i < bounds[g + 1]; ++i)
+    for (int i = g; i < nc; i += G)
       for (int l : cls[i]) {
         owner[l] = g;
         slot[l] = k++;

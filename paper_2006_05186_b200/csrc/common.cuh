@@ -152,7 +152,7 @@ struct Tree {
   // near field per leaf index: [jb, je) into the flat list of near source panels
   DBuf<int32_t> d_near_jb, d_near_je, d_near_j;
   DBuf<int32_t> d_near_gb;   // per leaf: first entry of its warp steps in d_near_gsuf
-  DBuf<double> d_near_gsuf;  // per warp step of 32 sources: min distance of the leaf box to any later source centroid
+  DBuf<unsigned> d_near_gsuf;  // per warp step of 32 sources: float bits of the min squared distance of the leaf box to any later source centroid (rounded down)
   // near blocks (combined mode, NEXT-4): block list, per-row-leaf CSR, raw J(T) (cluster order)
   DBuf<int32_t> d_near_r, d_near_c, d_nb_ptr, d_nb_sorted;
   DBuf<double> d_J;

@@ -412,9 +412,9 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
   for (int li = 0; li < t.n_leaves; ++li) leaf_pos[t.leaves[li]] = li;
   // The source leaves of a target leaf are listed by increasing box distance from it (a warp
   // step of 32 consecutive sources is then compact), and every step carries gsuf = the smallest
-  // distance of the target leaf's box to the centroid of any source from that step on: K1's
-  // underflow cutoff leaves the loop once Re s (gsuf - hmax) > tau (near_common.cuh; every later
-  // source is then out of reach too).
+  // squared distance of the target leaf's box to the centroid of any source from that step on:
+  // K1's underflow cutoff leaves the loop once gsuf > (tau / Re s + hmax)^2 (near_common.cuh;
+  // every later source is then out of reach too).
   std::vector<std::vector<int32_t>> per_leaf(t.n_leaves);
   {
     auto box_dist = [&](int a, int b) {
@@ -436,7 +436,7 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
     }
   }
   std::vector<int32_t> njb(t.n_leaves), nje(t.n_leaves), nj, ngb(t.n_leaves);
-  std::vector<double> gsuf;
+  std::vector<unsigned> gsuf;  // float bits of the squared distances, rounded down
   for (int li = 0; li < t.n_leaves; ++li) {
     njb[li] = (int32_t)nj.size();
     nj.insert(nj.end(), per_leaf[li].begin(), per_leaf[li].end());
@@ -454,9 +454,13 @@ extern "C" bem_status bem_build_tree(const double* V, int64_t nv, const int32_t*
           const double gp = std::max(0.0, std::max(bx[k] - cen[3 * j + k], cen[3 * j + k] - bx[3 + k]));
           d2 += gp * gp;
         }
-        run = std::min(run, std::sqrt(d2) * (1.0 - 0x1p-40));
+        run = std::min(run, d2);
       }
-      gsuf[ngb[li] + g] = run;
+      float fr = (float)std::min(run, 1e30);
+      if ((double)fr > run) fr = std::nextafterf(fr, 0.0f);
+      unsigned ub;
+      std::memcpy(&ub, &fr, sizeof ub);
+      gsuf[ngb[li] + g] = ub;
     }
   }
   // near blocks grouped by row leaf (partition order within a row): the combined

@@ -14,6 +14,8 @@
 // over the source panels (coalesced loads of panel geometry and x); the node
 // loop is kept rolled so the code body stays small (I-cache), F classes are
 // unrolled for ILP; warp butterfly reduction, no atomics.
+#include <cstdlib>
+
 #include "near_common.cuh"
 
 namespace bem {

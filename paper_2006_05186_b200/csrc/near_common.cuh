@@ -14,7 +14,7 @@ struct NearArgs {
   const int32_t* near_je;
   const int32_t* near_j;
   const int32_t* near_gb = nullptr;  // with gsuf: the cutoff's early exit (nullable)
-  const double* gsuf = nullptr;
+  const unsigned* gsuf = nullptr;    // float bits of the squared suffix distances (rounded down)
   const double* cen;
   const double* qn;
   const double* qw;
@@ -113,46 +113,44 @@ __device__ __forceinline__ void near_item(const NearArgs& a, int64_t k, int c0, 
   // whose Re s r_min exceeds a.tau over the 32 sources of a warp step adds less than e^{-tau}
   // (tau = 42: 6e-19) of the kernel's 1/(4 pi r) scale -- below the rounding of the row sum.
   // r_min >= min_j |c_k - c_j| - hmax (source centroids, hmax = the largest node-to-centroid
-  // distance of the mesh); the centroids are loaded one step ahead like the indices, so a
-  // skipped step costs three loads, eight flops and one warp reduction.  The decision is
-  // warp-uniform and all-or-nothing for the F classes of the tile (they are neighbours in Re s:
-  // a per-class decision would leave out 0.5 % more at config 4 and costs the kernel its
-  // instruction-level parallelism), so nothing diverges.
-  const double tau = CUT ? (a.tau > 0.0 ? a.tau : 1e300) : 0.0;
-  double smin = 1e300;  // smallest Re s of the tile's active classes
+  // distance of the mesh): the step is left out when min_j |c_k - c_j|^2 > rc^2, rc = tau /
+  // min_f Re s_f + hmax, compared as float bit patterns (distances rounded down, rc^2 up; no
+  // square root, one register of state: the loop sits at its 128-register budget and a test
+  // with its operands in double cost 10 % per evaluated step, this one 4 %).  a.gsuf carries per
+  // step the smallest squared distance of the target leaf's box to any later source centroid:
+  // past rc^2 the loop ends.  The decision is warp-uniform and all-or-nothing for the F classes
+  // of the tile (neighbours in Re s: a per-class decision would leave out 0.5 % more at config 4
+  // and costs the kernel its instruction-level parallelism), so nothing diverges.
+  unsigned rc2bits = 0x7f800000u;  // +inf: run every step
   unsigned nact = 0;
+  {
+    double smin = 1e300;  // smallest Re s of the tile's active classes
 #pragma unroll
-  for (int f = 0; f < F; ++f)
-    if (o1[f] >= 0) { smin = fmin(smin, sre[f]); ++nact; }
+    for (int f = 0; f < F; ++f)
+      if (o1[f] >= 0) { smin = fmin(smin, sre[f]); ++nact; }
+    if (CUT && a.tau > 0.0 && smin > 0.0) {
+      const double rc = a.tau / smin + a.hmax;
+      const double rc2 = rc * rc * (1.0 + 1e-6);
+      if (rc2 < 1e30) rc2bits = __float_as_uint(__double2float_ru(rc2));
+    }
+  }
   unsigned nev = 0;  // kernel evaluations of this lane (profiling)
   int jn = jb + lane < je ? a.near_j[jb + lane] : 0;
-  int jn2 = 0;
-  double ncx = 0.0, ncy = 0.0, ncz = 0.0;  // centroid of source jn
-  const double* gs = CUT && a.gsuf != nullptr ? a.gsuf + a.near_gb[li] : nullptr;
-  double gnext = gs != nullptr && jb < je ? gs[0] : 0.0;  // this step's suffix distance, loaded a step ahead
-  if (CUT) {
-    jn2 = jb + 32 + lane < je ? a.near_j[jb + 32 + lane] : 0;
-    ncx = a.cen[3 * (int64_t)jn]; ncy = a.cen[3 * (int64_t)jn + 1]; ncz = a.cen[3 * (int64_t)jn + 2];
-  }
+  int gi = CUT && a.gsuf != nullptr ? a.near_gb[li] : -1;  // this step's entry of a.gsuf
   for (int j0 = jb; j0 < je; j0 += 32) {
     const int jj = j0 + lane;
-    const int j = jn;  // index loaded ahead (one dependent global load fewer per source)
+    const int j = jn;  // index loaded one step ahead (one dependent global load fewer per source)
+    if (jj + 32 < je) jn = a.near_j[jj + 32];
     const bool use = jj < je && j != k;  // self panel below
     if (CUT) {
-      // every source from this step on is further than gsuf from the target leaf's box
-      if (smin * fmax(gnext - a.hmax, 0.0) > tau) break;
-      if (gs != nullptr && j0 + 32 < je) gnext = gs[(j0 - jb) / 32 + 1];
-      const double ddx = cx - ncx, ddy = cy - ncy, ddz = cz - ncz;
-      const double d2c = use ? ddx * ddx + ddy * ddy + ddz * ddz : 1e30;
-      jn = jn2;  // two steps of indices and one step of centroids in flight
-      if (jj + 64 < je) jn2 = a.near_j[jj + 64];
-      ncx = a.cen[3 * (int64_t)jn]; ncy = a.cen[3 * (int64_t)jn + 1]; ncz = a.cen[3 * (int64_t)jn + 2];
-      // warp minimum through the (monotone) bit pattern of the value rounded down to float
-      const unsigned bits = __reduce_min_sync(0xffffffffu, __float_as_uint(__double2float_rd(d2c)));
-      const double rmin = fmax((double)(sqrtf(__uint_as_float(bits)) * 0.999999f) - a.hmax, 0.0);
-      if (smin * rmin > tau) continue;
-    } else {
-      if (jj + 32 < je) jn = a.near_j[jj + 32];
+      if (gi >= 0 && a.gsuf[gi++] > rc2bits) break;  // every later source is out of reach too
+      float d2 = 1e30f;
+      if (use) {
+        const double ddx = cx - a.cen[3 * (int64_t)j], ddy = cy - a.cen[3 * (int64_t)j + 1], ddz = cz - a.cen[3 * (int64_t)j + 2];
+        d2 = __double2float_rd(ddx * ddx + ddy * ddy + ddz * ddz);
+      }
+      // warp minimum through the (monotone) bit pattern of the non-negative float
+      if (__reduce_min_sync(0xffffffffu, __float_as_uint(d2)) > rc2bits) continue;
     }
     const double* qn = a.qn + 21 * (int64_t)j;
     const double* qw = a.qw + 7 * (int64_t)j;

@@ -26,19 +26,12 @@ def freq_classes(L: int):
 
 
 def shard_frequencies(L: int, G: int):
-    """local frequency lists per rank (balanced contiguous ranges of classes)."""
+    """local frequency lists per rank: class i -> rank i mod G (every rank holds an even sample of
+    the frequency circle, so the underflow cutoffs of K1 / K3 take the same share from every rank)."""
     cls = freq_classes(L)
     if G > len(cls):
         raise ValueError(f"{G} ranks but only {len(cls)} frequency classes")
-    sizes = np.array([len(c) for c in cls])
-    before = np.cumsum(sizes) - sizes  # frequencies preceding each class
-    bounds = [0]
-    for g in range(1, G):
-        b = int(np.argmin(np.abs(before - sizes.sum() * g / G)))
-        b = min(max(b, bounds[-1] + 1), len(cls) - (G - g))
-        bounds.append(b)
-    bounds.append(len(cls))
-    return [np.array([l for c in cls[bounds[g]:bounds[g + 1]] for l in c], dtype=np.int32) for g in range(G)]
+    return [np.array([l for c in cls[g::G] for l in c], dtype=np.int32) for g in range(G)]
 
 
 def dof_ranges(M: int, G: int):

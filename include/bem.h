@@ -353,7 +353,8 @@ bem_status bem_op_get_timings(bem_op op, double* ms5);
  *   K1 (a3): over a warp step of 32 source panels, a frequency class with Re s r_min > near_tau
  *     (default 42, env BEM_NEAR_TAU, 0 = off) is not evaluated;
  *   K3 (a5, far10): a (far block, 128-frequency tile) whose compressed fibres sum_j S(s_kj) Z[j,t]
- *     (eq:maca P:1314-1320) are bounded entrywise by far_delta / max(|s_t|, 1) for every column t
+ *     (eq:maca P:1314-1320) are bounded entrywise by far_delta / max(|s_t|, 1, 1/(4 h)) for every column t
+ *     (h = the mesh's largest quadrature-node-to-centroid distance)
  *     (default far_delta = 2^-70, env BEM_FAR_SKIP_LOG2 = 70, 0 = off) is not computed.
  * far_rank_cols_*: sum over far blocks of r_b x (frequency columns), in total and under the
  * mask (equal when no mask applies); near_evals_total = 7 nnz_near n_class, near_evals_run =

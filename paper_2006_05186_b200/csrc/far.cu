@@ -1088,6 +1088,7 @@ static Far10SkipArgs far10_skip_args(Op& op, int tb, int nd, int tile_lo, int ti
   Far10SkipArgs a;
   a.nfar = (int)t.far_r.size(); a.nl = op.n_local; a.m = t.m; a.rcap = op.rcap; a.tb = tb; a.nd = nd;
   a.tile_lo = tile_lo; a.tile_hi = tile_hi; a.delta = op.far_delta;
+  a.sref = std::max(1.0, t.hmax > 0.0 ? 0.25 / t.hmax : 1.0);
   a.far_r = t.d_far_r.p; a.far_c = t.d_far_c.p; a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p;
   a.local_l = op.d_local_l.p; a.rank = op.d_rank.p; a.pivk = op.d_pivk.p; a.z = z; a.skip = op.d_skip.p;
   a.colmap = op.d_colmap.p;
@@ -1253,6 +1254,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
         a.part_n = (int64_t)op.d_part.n / 2;
         a.skip = op.d_skip.p;
         a.colmap = op.d_colmap.p;
+        a.nfar = (int)op.d_skip.n; a.ncm = (int)op.d_colmap.n;
         if (fna != nullptr) {
           if (tile == 0) BEM_CK(cudaMemsetAsync(op.d_nctr.p, 0, sizeof(unsigned), st));
           a.na = *fna;

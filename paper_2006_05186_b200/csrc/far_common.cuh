@@ -44,6 +44,7 @@ struct Far10Args {
   // frequency tile are below the rounding of the result and are not computed); nullable
   const uint32_t* skip = nullptr;
   const int32_t* colmap = nullptr;  // [tiles][128]: local frequency of every tile column (-1: padding)
+  int nfar = 0, ncm = 0;            // entries of skip / colmap (bounds checks)
   // K1 fused into the launch (nctr != nullptr): near-field warps take (target, class tile)
   // items from *nctr (F = 4 classes per item) while the CTA's coupling work runs
   NearArgs na;
@@ -56,6 +57,7 @@ struct Far10SkipArgs {
   int nfar, nl, m, rcap, tb, nd;
   int tile_lo, tile_hi;  // tiles whose bits are (re)computed
   double delta;
+  double sref;  // lower bound of the 1 / diagonal scale: max(1, 1 / (4 hmax))
   const int32_t* far_r;
   const int32_t* far_c;
   const double* xi;

@@ -233,7 +233,9 @@ __global__ void __launch_bounds__(PW * 32 + 32 + NEARW * 32, 1) far10_kernel(con
   for (int i = tid; i < nrow; i += kQThreads) node(a.xi + (int64_t)r * 3 * m, m, mu0 + i, xr + 3 * i);
   // the tile's columns: a.colmap orders the local frequencies by damping (Re s ascending), so
   // that whole tiles fall under the underflow mask; identity when the mask is off
+  BEM_DASSERT(tile >= 0 && tile * kQT + t_l < a.ncm);
   const int tg = t_l < ncol ? a.colmap[tile * kQT + t_l] : -1;
+  BEM_DASSERT(tg < a.nl);
   if (tid < kQT) cmap[tid] = tg;  // read after the named_or barrier below
   const int zt = a.z.tiled ? tc0 + t_l : tg;  // Z column: tile buffers hold the tile's columns in tile order
   const bool tv = tid < kQProd && tg >= 0 && (a.mask == nullptr || a.mask[tg]);
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(PW * 32 + 32 + NEARW * 32, 1) far10_kernel(con
     uint32_t &stage = mstage, &blk = mblk;
     for (int bi = sg.y; bi < bend; ++bi) {
       const int b = a.far_sorted[bi];
+      BEM_DASSERT(b >= 0 && (a.skip == nullptr || b < a.nfar));
       if (a.skip != nullptr && ((a.skip[b] >> tile) & 1u)) continue;  // underflow mask (same test in the producers)
       const int rk = a.rank[b];
       for (int g0 = 0; g0 < rk; g0 += a.gmax, ++blk) {  // term groups (int32 sums stay exact)
@@ -572,7 +575,8 @@ __global__ void __launch_bounds__(PW * 32 + 32 + NEARW * 32, 1) far10_kernel(con
 // <= g_j := e^{-Re s_{k_j} r_lb} / (4 pi r_lb) (Re s >= 0), so every entry of the fibre is bounded
 // by beta_t = sum_j g_j |Z_b[j, t]|.  At the strongly damped CQM frequencies (Re s_t r >> 1) the
 // far field underflows against the O(1 / |s_t|) diagonal of V(s_t): a tile whose columns all have
-// beta_t max(|s_t|, 1) < delta (2^-70) is not computed.  The mask depends on the skeleton only
+// beta_t max(|s_t|, 1, 1 / (4 hmax)) < delta (2^-70; hmax = the mesh's largest node-to-centroid
+// distance: the diagonal is O(1 / |s|) only while |s| h >> 1, O(h) below) is not computed.  The mask depends on the skeleton only
 // (not on x): one pass at assembly (stored Z) or per regenerated tile (factors-only; the Z
 // columns are bitwise the same, hence the same mask).
 __global__ void __launch_bounds__(kQT) far10_skip_kernel(const Far10SkipArgs a) {
@@ -615,7 +619,7 @@ __global__ void __launch_bounds__(kQT) far10_skip_kernel(const Far10SkipArgs a) 
           beta = fma(sqrt(fma(z.x, z.x, z.y * z.y)), gs[j], beta);
         }
         const double2 st = a.s[a.local_l[t]];
-        const double v = beta * (1.0 + 0x1p-20) * fmax(sqrt(fma(st.x, st.x, st.y * st.y)), 1.0);
+        const double v = beta * (1.0 + 0x1p-20) * fmax(sqrt(fma(st.x, st.x, st.y * st.y)), a.sref);
         if (!(v < a.delta)) keep = true;  // NaN / inf keep the tile
       };
       const int t = tid < ncol ? a.colmap[tile * kQT + tid] : -1;

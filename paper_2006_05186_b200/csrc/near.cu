@@ -86,6 +86,7 @@ void near_args(Op& op, const double2* xc, double2* yc, NearArgs& na, int& F) {
   na.tau = op.near_tau;
   na.near_gb = dense ? nullptr : t.d_near_gb.p;
   na.gsuf = dense ? nullptr : t.d_near_gsuf.p;
+  na.gsuf_n = (int64_t)t.d_near_gsuf.n;
   na.hmax = t.hmax;
   na.evals = op.profile ? op.d_near_evals.p : nullptr;
   // F = 4 classes per warp unless that pads the last class tile by more than 3 % and F = 5

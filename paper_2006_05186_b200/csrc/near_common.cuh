@@ -15,6 +15,7 @@ struct NearArgs {
   const int32_t* near_j;
   const int32_t* near_gb = nullptr;  // with gsuf: the cutoff's early exit (nullable)
   const unsigned* gsuf = nullptr;    // float bits of the squared suffix distances (rounded down)
+  int64_t gsuf_n = 0;                // its entries (bounds checks)
   const double* cen;
   const double* qn;
   const double* qw;
@@ -143,6 +144,7 @@ __device__ __forceinline__ void near_item(const NearArgs& a, int64_t k, int c0, 
     if (jj + 32 < je) jn = a.near_j[jj + 32];
     const bool use = jj < je && j != k;  // self panel below
     if (CUT) {
+      BEM_DASSERT(gi < a.gsuf_n);
       if (gi >= 0 && a.gsuf[gi++] > rc2bits) break;  // every later source is out of reach too
       float d2 = 1e30f;
       if (use) {

@@ -10,7 +10,11 @@ K2 down, scatter) -> [all-to-all] -> cqm_inverse (K4).  Metric: unknowns x
 frequencies per second, value = M * L / (device time per step), max over
 ranks.  Inputs are device-resident; L2 is flushed (256 MB write) before every
 timed step.  `e2e` repeats the step through the same public API from pinned
-HOST buffers with the copies inside the timed region.
+HOST buffers with the copies inside the timed region.  K1 and K3 leave out work that is below
+the rounding of the result at the strongly damped frequencies (underflow
+cutoffs; the metric's M * L still counts every unknown and frequency, the result matches the
+oracle's full evaluation within the parity bar); `work` reports the executed fractions and
+every roofline counts executed work only.
 """
 from __future__ import annotations
 

@@ -116,4 +116,5 @@ def test_null_handles_rejected_without_gpu():
     assert lib.cqm_mot_solve(None, None, None, 1e-8, 10, 10, None, None) == -1
     assert lib.bem_time_step(None, None, None, 0.5, None) == -1
     assert lib.bem_op_get_info(None, None) == -1
+    assert lib.bem_op_get_work(None, None) == -1
     assert b"NULL" in lib.bem_last_error()

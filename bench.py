@@ -528,7 +528,9 @@ def main():
     elif dom == "coupling" and not aca_far:
         fl = flops_far
         peak = FP64_PEAK_DERIVED / 1e12
-        bound, src = "alu", "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §7); 75 flops/evaluation model"
+        bound, src = "alu", ("derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §7); 75 flops/evaluation model"
+                             + ("; flops count every (block, class), the K3' underflow cutoff is not counted: upper bound"
+                                if wk["near_tau"] > 0 else ""))
     elif dom == "coupling" and i8 is not None:
         fl = i8["ops"]
         peak = i8["peak"]
@@ -581,6 +583,9 @@ def main():
         "down": {"flops": f_up, "bytes": b_down, "ms": kt["down"], "peak_tflops": FP64_PEAK_DERIVED / 1e12,
                  "peak_gbs": hbm},
     }
+    if not aca_far and wk["near_tau"] > 0:
+        # plain H^2 (K3'): its underflow cutoff has no work counter, so these flops count every block and class
+        kern["coupling"]["note"] = "flops count every (block, class); the K3' underflow cutoff is not counted: frac is an upper bound"
     if k4_ms:  # K4 forward + inverse: 32 M L bytes each (read + write of complex128 [L][M]), HBM-bound
         torch.cuda.synchronize()
         t_k4 = statistics.mean(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in k4_ms)

@@ -784,6 +784,9 @@ struct H2oArgs {
   const double2* xhat;
   double2* part;
   const int32_t* mask;
+  // underflow cutoff: a block whose node boxes are r_lb apart is left out for a
+  // class tile with min Re s * r_lb > tau (every entry is below e^{-tau} / (4 pi r_lb)); 0: off
+  double tau = 0.0;
 };
 
 constexpr int kH2oWarps = 4;
@@ -831,10 +834,36 @@ __global__ void __launch_bounds__(kH2oWarps * 32, 3) h2o_kernel(H2oArgs a) {
   bool any = false;
 #pragma unroll
   for (int f = 0; f < FC; ++f) any |= t1[f] >= 0;
+  // underflow cutoff: the row cluster's node box (shared memory) and the smallest Re s of the
+  // tile's classes
+  __shared__ double rbox[6];
+  double smin = 1e300;
+#pragma unroll
+  for (int f = 0; f < FC; ++f)
+    if (t1[f] >= 0) smin = fmin(smin, sre[f]);
+  if (tid < 3) {
+    const double* x = a.xi + (int64_t)r * 3 * m + tid * m;
+    double lo = x[0], hi = x[0];
+    for (int i = 1; i < m; ++i) { lo = fmin(lo, x[i]); hi = fmax(hi, x[i]); }
+    rbox[tid] = lo;
+    rbox[3 + tid] = hi;
+  }
   __syncthreads();
   for (int bi = sg.y + warp; bi < (any ? sg.z : sg.y); bi += kH2oWarps) {
     const int b = a.far_sorted[bi];
     const int c = a.far_c[b];
+    if (a.tau > 0.0 && smin > 0.0) {  // warp-uniform: every lane computes the same distance
+      double g2 = 0.0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double* x = a.xi + (int64_t)c * 3 * m + d * m;
+        double lo = x[0], hi = x[0];
+        for (int i = 1; i < m; ++i) { lo = fmin(lo, x[i]); hi = fmax(hi, x[i]); }
+        const double gp = fmax(0.0, fmax(rbox[d] - hi, lo - rbox[3 + d]));
+        g2 = fma(gp, gp, g2);
+      }
+      if (smin * (sqrt(g2) * (1.0 - 0x1p-40)) > a.tau) continue;
+    }
     const double2* xh = a.xhat + (int64_t)c * a.nl * p;
     __syncwarp();
     for (int i = lane; i < p; i += 32) node(a.xi + (int64_t)c * 3 * m, m, i, cw + 3 * i);
@@ -1187,6 +1216,7 @@ bem_status launch_far(Op& op, const double2* xhat, double2* yhat, cudaStream_t s
     a.xi = t.d_xi.p; a.s = (const double2*)op.d_s.p; a.local_l = op.d_local_l.p;
     a.class_t1 = op.d_class_t1.p; a.class_t2 = op.d_class_t2.p; a.xhat = xhat; a.part = (double2*)op.d_part.p;
     a.mask = op.d_mask;
+    a.tau = op.near_tau > 0.0 ? op.near_tau + 8.0 : 0.0;  // far blocks: e^{-50} of 1 / (4 pi r_lb)
     const int U = (p + 31) / 32;
     int FC = p <= 32 ? 6 : 2;  // r01 sweep: p = 27 FC 2/4/6 = 2.45/2.48/2.39 ms; p = 64 FC 2/3/4 = 356/369/383 ms
     if (op.h2o_fc > 0) FC = op.h2o_fc;

@@ -101,3 +101,29 @@ def test_cutoff_dense_mode(pb, torch, monkeypatch):
     for l in (0, 1, L // 2, L - 1):
         yo = O.dense_matrix(V, T, s[l]) @ x[l]
         assert _rel(y[l], yo) <= 1e-10, l
+
+
+def test_cutoff_h2only(pb, torch, monkeypatch):
+    """Plain-H^2 couplings (NEXT-3, K3'): a far block is left out for a class tile with
+    min Re s * r_lb > tau + 8 (r_lb = distance of the node boxes); on vs off and the oracle's
+    plain-H^2 apply."""
+    V, T = synth.icosphere(4)
+    N, m, leaf = 512, 3, 32
+    M, L = len(T), N + 1
+    s = pb.cqm_frequencies(N, 2.0)
+    x = synth.random_density(14, L, M)
+    tree = pb.Tree(V, T, leaf, 1.0, m)
+    op = pb.Operator(tree, s, 1e-6, mode=pb.BEM_MODE_H2ONLY)
+    y = _apply(torch, op, x)
+    monkeypatch.setenv("BEM_NEAR_TAU", "0")
+    op0 = pb.Operator(tree, s, 1e-6, mode=pb.BEM_MODE_H2ONLY)
+    y0 = _apply(torch, op0, x)
+    assert _rel(y, y0) <= 1e-14
+    for l in range(L):
+        assert _rel(y[l], y0[l]) <= 1e-13, l
+    lsel = np.unique(np.r_[0, 1, L // 4, L // 2, L // 2 + 1, L - 1])
+    oh = O.H2(V, T, leaf, 1.0, m)
+    yo = oh.apply(O.MODE_H2ONLY, s, x[lsel], lsel)
+    assert _rel(y[lsel], yo) <= 1e-10
+    for i in range(len(lsel)):
+        assert _rel(y[lsel[i]], yo[i]) <= 1e-10, lsel[i]
